@@ -1,0 +1,223 @@
+/*
+ * leo_b200.h — C ABI of the B200-native LEO analysis hot path.
+ *
+ * Drop-in boundary for the `stalltrace` analyzer (reference: arXiv 2604.20032
+ * reproduction, /root/reference/pkg/src/stalltrace).  The reference has no FFI;
+ * its contract is the Python API re-exported in `stalltrace/__init__.py:9-64`.
+ * Each entry point below replaces one of those Python functions; the host mirror
+ * in `paper_2604_20032_b200/api.py` keeps the reference names and types and
+ * marshals them into the structure-of-arrays (SoA) layout declared here.
+ *
+ *   leo_bin_samples   <- new stage 0 (reference reads pre-binned counts,
+ *                        profile.py:186-239; breakdown_at profile.py:307-313)
+ *   leo_build_graph   <- depgraph.build_graph            depgraph.py:507-528
+ *                        (reaching_definitions :135-177, per_use_link :188-223,
+ *                         liveness_filter :274-293, trace_waitcnt :402-416,
+ *                         trace_barriers :446-463, trace_swsb :466-482)
+ *   leo_prune         <- analysis.run_pruning            analysis.py:302-314
+ *                        (prune_opcode :143, prune_barrier :165,
+ *                         prune_latency :256, prune_execution :289)
+ *   leo_blame         <- analysis.attribute_blame        analysis.py:431-484
+ *                        (self_blame :414-428) + per-source-line rollup
+ *   leo_slice         <- multi-source backward slice over DependencyGraph.incoming
+ *                        (depgraph.py:102-108; semantics frozen in DESIGN.md)
+ *   leo_analyze       <- fused build -> prune -> slice -> blame -> lines
+ *                        (report.py:132-142 call sequence)
+ *
+ * Conventions
+ *  - Every pointer inside a struct is a DEVICE pointer owned by the caller.
+ *  - Calls are stream-ordered and asynchronous; `stream` is a cudaStream_t
+ *    passed as void*.  Scratch memory is taken from the stream-ordered
+ *    allocator and released on the same stream.  No global mutable state.
+ *  - Variable-size outputs use "capacity + device counter": the kernel writes
+ *    the true count to the device counter even when it exceeds capacity; the
+ *    host reads the counter after synchronising, and re-runs with larger
+ *    buffers when count > capacity (status LEO_ERR_CAPACITY in the status word).
+ *  - Return value: 0 = launched; < 0 = argument error detected on the host
+ *    (mapped to InputError by the Python layer, errors.py:12-39).
+ *  - Non-fatal findings are typed diagnostic records (LeoDiag) which the host
+ *    renders with the reference's exact format strings.
+ */
+#ifndef LEO_B200_H
+#define LEO_B200_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define LEO_ABI_VERSION 1
+
+/* ---- enumerations (indices follow the reference enum definition order) --- */
+/* Dialect  isa.py:19-22 */
+enum { LEO_NVIDIA = 0, LEO_AMD = 1, LEO_INTEL = 2 };
+/* RegClass isa.py:32-39 */
+enum { LEO_RC_VECTOR = 0, LEO_RC_SCALAR = 1, LEO_RC_PREDICATE = 2, LEO_RC_BARRIER = 3,
+       LEO_RC_UNIFORM = 4, LEO_RC_SBID = 5, LEO_RC_SPECIAL = 6, LEO_N_RC = 7 };
+/* OpcodeClass isa.py:42-58 */
+enum { LEO_OC_GLOBAL_LOAD = 0, LEO_OC_GLOBAL_STORE, LEO_OC_LOCAL_LOAD, LEO_OC_LOCAL_STORE,
+       LEO_OC_SCALAR_LOAD, LEO_OC_CONSTANT_LOAD, LEO_OC_ATOMIC, LEO_OC_FP_ARITH,
+       LEO_OC_INT_ARITH, LEO_OC_CONVERSION, LEO_OC_CONTROL_FLOW, LEO_OC_SYNC_WAIT,
+       LEO_OC_BARRIER_ALL, LEO_OC_SEND, LEO_OC_NOP, LEO_OC_OTHER, LEO_N_OC };
+/* CommonStall profile.py:29-43 (order = dominant-class tie-break) */
+enum { LEO_CS_MEMORY_DEP = 0, LEO_CS_EXECUTION_DEP, LEO_CS_SYNCHRONIZATION,
+       LEO_CS_INSTRUCTION_FETCH, LEO_CS_PIPELINE_BUSY, LEO_CS_NOT_SELECTED,
+       LEO_CS_IDLE, LEO_CS_OTHER, LEO_N_CS };
+/* EdgeKind depgraph.py:46-51 */
+enum { LEO_EK_RAW = 0, LEO_EK_GUARD = 1, LEO_EK_MEM_WAITCNT = 2, LEO_EK_MEM_BARRIER = 3,
+       LEO_EK_MEM_SWSB = 4 };
+/* DepClass depgraph.py:57-60 */
+enum { LEO_DC_MEMORY = 0, LEO_DC_EXECUTION = 1, LEO_DC_SYNCHRONIZATION = 2 };
+/* SelfBlame analysis.py:320-326 */
+enum { LEO_SB_MEMORY_LATENCY = 0, LEO_SB_COMPUTE_SATURATION, LEO_SB_SYNCHRONIZATION_OVERHEAD,
+       LEO_SB_PIPELINE_CONTENTION, LEO_SB_INSTRUCTION_FETCH, LEO_SB_INDIRECT_ADDRESSING };
+/* per-instruction sync variant (isa.py:153-206) */
+enum { LEO_SYNC_NONE = 0, LEO_SYNC_WAITCNT = 1, LEO_SYNC_BARRIER = 2, LEO_SYNC_SWSB = 3 };
+#define LEO_NONE_U32 0xFFFFFFFFu
+
+/* ---- operand record: one RegisterRef (isa.py:92-117) with its role ------- */
+/* bits 0-15 index, 16-23 span, 24-26 RegClass, 27-28 role                  */
+enum { LEO_ROLE_SRC = 0, LEO_ROLE_GUARD = 1, LEO_ROLE_DST = 2 };
+#define LEO_OPND(role, cls, index, span) \
+  ((uint32_t)(index) | ((uint32_t)(span) << 16) | ((uint32_t)(cls) << 24) | ((uint32_t)(role) << 27))
+
+/* ---- edge meta word --------------------------------------------------------
+ * bits 0-26 register ref (index|span<<16|class<<24; zero for sync edges),
+ * 27-29 EdgeKind, 30-31 DepClass                                            */
+#define LEO_META(kind, dc, ref27) ((uint32_t)(ref27) | ((uint32_t)(kind) << 27) | ((uint32_t)(dc) << 30))
+
+/* ---- one kernel: instruction stream + CFG (disasm.py:477-499) ------------ */
+typedef struct LeoKernel {
+  int32_t n_instr;            /* N */
+  int32_t n_blocks;           /* B */
+  int32_t n_units;            /* U: dense register-unit ids (depgraph.py:41) */
+  int32_t dialect;            /* LEO_NVIDIA / LEO_AMD / LEO_INTEL */
+  int32_t n_opnd;             /* operand records */
+  int32_t unit_base[8];       /* RegClass -> first unit id */
+  const uint8_t*  opclass;    /* [N] OpcodeClass */
+  const int32_t*  block_of;   /* [N] */
+  const int32_t*  opnd_ptr;   /* [N+1] CSR; per instruction: srcs, guard, dests */
+  const uint32_t* opnd;       /* [n_opnd] LEO_OPND records */
+  const uint8_t*  sync_kind;  /* [N] LEO_SYNC_* */
+  const uint32_t* sync_a;     /* [N] waitcnt: vmcnt | barrier: w|r<<8|wait<<16 | swsb: set token */
+  const uint32_t* sync_b;     /* [N] waitcnt: lgkmcnt | barrier: stall cycles | swsb: wait mask */
+  const int32_t*  blk_first;  /* [B] */
+  const int32_t*  blk_last;   /* [B] */
+  const int32_t*  succ_ptr;   /* [B+1] successor order [target, fallthrough] disasm.py:572 */
+  const int32_t*  succ;
+  const int32_t*  pred_ptr;   /* [B+1] predecessors sorted disasm.py:596 */
+  const int32_t*  pred;
+} LeoKernel;
+
+/* ---- per-instruction profile (profile.py:114-170, 284-329) --------------- */
+typedef struct LeoProfile {
+  int64_t period;             /* sampling_period_cycles */
+  const int32_t* lat;         /* [N] latency_samples */
+  const int32_t* cls_cnt;     /* [N*8] latency samples per CommonStall */
+  const int64_t* exec_cnt;    /* [N] exec_count, -1 = None */
+  const int32_t* total;       /* [N] total_samples, -1 = None (effective total = lat) */
+  const double*  eff;         /* [N] efficiency */
+  const uint8_t* sampled;     /* [N] a profile record attached (profile.py:296) */
+} LeoProfile;
+
+/* ---- raw PC-sample stream (new stage 0) ---------------------------------- */
+typedef struct LeoSamples {
+  int64_t n_samples;          /* S */
+  const int32_t* pc;          /* [S] instruction index */
+  const uint8_t* cat;         /* [S] vendor stall category id */
+  const uint8_t* cat_to_cs;   /* [256] vendor category id -> CommonStall (map_stall) */
+} LeoSamples;
+
+/* ---- analysis configuration (analysis.py:115-124) ------------------------ */
+typedef struct LeoConfig {
+  uint32_t stage_mask;        /* bit s-1 set when stage s is enabled */
+  int32_t  prune_exec;
+  int32_t  max_paths;         /* DEFAULT_MAX_PATHS 64 */
+  int32_t  max_depth;         /* DEFAULT_MAX_DEPTH 512 */
+  double   threshold[16];     /* LatencyTable.get per OpcodeClass (fallback = max) */
+} LeoConfig;
+
+/* ---- edge list (DepEdge depgraph.py:77-91) -------------------------------- */
+typedef struct LeoEdges {
+  int32_t   capacity;
+  int32_t*  prod;             /* [cap] */
+  int32_t*  cons;             /* [cap] */
+  uint32_t* meta;             /* [cap] LEO_META */
+  int32_t*  count;            /* device scalar: total edges */
+  int32_t*  n_regular;        /* device scalar: raw/guard edges (they precede sync edges) */
+} LeoEdges;
+
+/* ---- valid_paths of pruned edges (PathRecord depgraph.py:71-74) ---------- */
+typedef struct LeoPaths {
+  int32_t  capacity;          /* path-record capacity */
+  int32_t* first;             /* [edge cap] first record of edge, -1 = none */
+  int32_t* npaths;            /* [edge cap] */
+  double*  dist;              /* [edge cap] _edge_distance analysis.py:371-376 */
+  int32_t* len;               /* [cap] length_instructions */
+  double*  accum;             /* [cap] accumulated_issue_cycles */
+  int32_t* count;             /* device scalar */
+} LeoPaths;
+
+/* ---- diagnostics ----------------------------------------------------------- */
+enum {
+  LEO_DIAG_UNRESOLVED = 1,    /* depgraph.py:219-222  a0 = operand record            */
+  LEO_DIAG_WAITCNT = 2,       /* depgraph.py:395-399  a0 = counter(0 vm,1 lgkm), a1 = level, a2 = best_m */
+  LEO_DIAG_NO_SETTER = 3,     /* depgraph.py:461-462 / 480-481  a0 = barrier or token */
+  LEO_DIAG_PATH_CAPPED = 4    /* analysis.py:277-284  instr = producer, a0 = consumer, a1 = 1 kept-with-partial / 0 conservative */
+};
+typedef struct LeoDiag { int32_t code, instr, a0, a1, a2, seq; } LeoDiag;
+typedef struct LeoDiags {
+  int32_t  capacity;
+  LeoDiag* rec;               /* [cap] unordered; host sorts by (code group, instr, seq) */
+  int32_t* count;             /* device scalar */
+} LeoDiags;
+
+/* ---- blame entries (BlameEntry analysis.py:360-368) ---------------------- */
+typedef struct LeoBlame {
+  int32_t  capacity;
+  int32_t* stalled;           /* [cap] */
+  int32_t* edge;              /* [cap] index into pruned edges, -1 = self-blame */
+  uint8_t* sub;               /* [cap] SelfBlame for self entries, 255 otherwise */
+  double*  blame;             /* [cap] blame_cycles */
+  double*  factors;           /* [cap*4] dist, eff, isu, match */
+  int32_t* count;             /* device scalar */
+} LeoBlame;
+
+/* ---- status word (device) ------------------------------------------------ */
+enum { LEO_ST_EDGE_OVERFLOW = 1, LEO_ST_PATH_OVERFLOW = 2, LEO_ST_DIAG_OVERFLOW = 4,
+       LEO_ST_BLAME_OVERFLOW = 8, LEO_ST_SCRATCH_OVERFLOW = 16, LEO_ST_BAD_INPUT = 32 };
+
+/* ---- entry points ---------------------------------------------------------- */
+int leo_abi_version(void);
+
+/* stage 0: raw (pc, category) stream -> lat[N], cls_cnt[N*8] (zeroed here). */
+int leo_bin_samples(const LeoSamples* s, int32_t n_instr, int32_t* lat, int32_t* cls_cnt,
+                    void* stream);
+
+/* build_graph: raw/guard edges sorted (consumer, producer, kind, class, index, span)
+ * followed by the dialect's sync edges sorted (producer, consumer). */
+int leo_build_graph(const LeoKernel* k, LeoEdges* out, LeoDiags* diags, uint32_t* status,
+                    void* stream);
+
+/* run_pruning: stages 1->2->3->4 honouring cfg; `out` keeps input order. */
+int leo_prune(const LeoKernel* k, const LeoProfile* p, const LeoConfig* cfg,
+              const LeoEdges* in, LeoEdges* out, LeoPaths* paths, LeoDiags* diags,
+              uint32_t* status, void* stream);
+
+/* backward slice from every instruction with S_j > 0 over `pruned` incoming
+ * adjacency: bitmap[(N+31)/32], level[N] (-1 outside the slice). */
+int leo_slice(const LeoKernel* k, const LeoProfile* p, const LeoEdges* pruned,
+              uint32_t* bitmap, int32_t* level, void* stream);
+
+/* attribute_blame(pruned, base_graph=base) + per-line rollup.
+ * line_id[N] (may be NULL), line_blame[n_lines], line_stall[n_lines] zeroed here. */
+int leo_blame(const LeoKernel* k, const LeoProfile* p, const LeoEdges* pruned,
+              const LeoPaths* paths, const LeoEdges* base, const int32_t* line_id,
+              int32_t n_lines, LeoBlame* out, double* line_blame, double* line_stall,
+              uint32_t* status, void* stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* LEO_B200_H */

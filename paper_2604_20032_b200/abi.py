@@ -1,0 +1,122 @@
+"""ctypes mirror of include/leo_b200.h (structs only; no library loading).
+
+Shared by the device wrapper (`_lib.py`, device pointers) and the oracle
+wrapper in oracle/ (host pointers)."""
+
+from __future__ import annotations
+
+import ctypes as C
+
+from . import enums as E
+
+P = C.c_void_p
+
+
+class LeoKernel(C.Structure):
+    _fields_ = [
+        ("n_instr", C.c_int32), ("n_blocks", C.c_int32), ("n_units", C.c_int32),
+        ("dialect", C.c_int32), ("n_opnd", C.c_int32), ("unit_base", C.c_int32 * 8),
+        ("opclass", P), ("block_of", P), ("opnd_ptr", P), ("opnd", P),
+        ("sync_kind", P), ("sync_a", P), ("sync_b", P),
+        ("blk_first", P), ("blk_last", P), ("succ_ptr", P), ("succ", P),
+        ("pred_ptr", P), ("pred", P),
+    ]
+
+
+class LeoProfile(C.Structure):
+    _fields_ = [
+        ("period", C.c_int64), ("lat", P), ("cls_cnt", P), ("exec_cnt", P),
+        ("total", P), ("eff", P), ("sampled", P),
+    ]
+
+
+class LeoSamples(C.Structure):
+    _fields_ = [("n_samples", C.c_int64), ("pc", P), ("cat", P), ("cat_to_cs", P)]
+
+
+class LeoConfig(C.Structure):
+    _fields_ = [
+        ("stage_mask", C.c_uint32), ("prune_exec", C.c_int32), ("max_paths", C.c_int32),
+        ("max_depth", C.c_int32), ("threshold", C.c_double * 16),
+    ]
+
+
+class LeoEdges(C.Structure):
+    _fields_ = [("capacity", C.c_int32), ("prod", P), ("cons", P), ("meta", P),
+                ("count", P), ("n_regular", P)]
+
+
+class LeoPaths(C.Structure):
+    _fields_ = [("capacity", C.c_int32), ("first", P), ("npaths", P), ("dist", P),
+                ("len", P), ("accum", P), ("count", P)]
+
+
+class LeoDiag(C.Structure):
+    _fields_ = [("code", C.c_int32), ("instr", C.c_int32), ("a0", C.c_int32),
+                ("a1", C.c_int32), ("a2", C.c_int32), ("seq", C.c_int32)]
+
+
+class LeoDiags(C.Structure):
+    _fields_ = [("capacity", C.c_int32), ("rec", P), ("count", P)]
+
+
+class LeoBlame(C.Structure):
+    _fields_ = [("capacity", C.c_int32), ("stalled", P), ("edge", P), ("sub", P),
+                ("blame", P), ("factors", P), ("count", P)]
+
+
+DIAG_UNRESOLVED, DIAG_WAITCNT, DIAG_NO_SETTER, DIAG_PATH_CAPPED = 1, 2, 3, 4
+ST_EDGE_OVERFLOW, ST_PATH_OVERFLOW, ST_DIAG_OVERFLOW = 1, 2, 4
+ST_BLAME_OVERFLOW, ST_SCRATCH_OVERFLOW, ST_BAD_INPUT = 8, 16, 32
+
+
+def make_config(stage_mask=(1, 2, 3, 4), prune_exec=False, max_paths=64, max_depth=512,
+                thresholds=None, dialect="nvidia") -> LeoConfig:
+    cfg = LeoConfig()
+    m = 0
+    for s in stage_mask:
+        if 1 <= int(s) <= 4:
+            m |= 1 << (int(s) - 1)
+    cfg.stage_mask = m
+    cfg.prune_exec = 1 if prune_exec else 0
+    cfg.max_paths = int(max_paths)
+    cfg.max_depth = int(max_depth)
+    th = thresholds if thresholds is not None else E.default_thresholds(dialect)
+    for i, v in enumerate(th):
+        cfg.threshold[i] = float(v)
+    return cfg
+
+
+def config_from_reference(config, dialect: str) -> LeoConfig:
+    """Translate a reference `AnalysisConfig` (analysis.py:115-124), duck-typed."""
+    table = config.latency
+    if table is None:
+        th = E.default_thresholds(dialect)
+    else:
+        th = E.dense_thresholds((c.value, v) for c, v in table.thresholds)
+    return make_config(config.stage_mask, config.prune_exec, config.max_paths,
+                       config.max_depth, th, dialect)
+
+
+def kernel_struct(ks, ptr) -> LeoKernel:
+    """Fill a LeoKernel whose array fields come from `ptr(name) -> address`."""
+    k = LeoKernel()
+    k.n_instr = ks.n_instr
+    k.n_blocks = ks.n_blocks
+    k.n_units = ks.n_units
+    k.dialect = ks.dialect_idx
+    k.n_opnd = int(ks.opnd.shape[0])
+    for c in range(8):
+        k.unit_base[c] = int(ks.unit_base[c])
+    for name in ("opclass", "block_of", "opnd_ptr", "opnd", "sync_kind", "sync_a", "sync_b",
+                 "blk_first", "blk_last", "succ_ptr", "succ", "pred_ptr", "pred"):
+        setattr(k, name, ptr(name))
+    return k
+
+
+def profile_struct(prof, ptr) -> LeoProfile:
+    p = LeoProfile()
+    p.period = int(prof.period)
+    for name in ("lat", "cls_cnt", "exec_cnt", "total", "eff", "sampled"):
+        setattr(p, name, ptr(name))
+    return p
