@@ -94,6 +94,8 @@ typedef struct LeoKernel {
   int32_t n_units;            /* U: dense register-unit ids (depgraph.py:41) */
   int32_t dialect;            /* LEO_NVIDIA / LEO_AMD / LEO_INTEL */
   int32_t n_opnd;             /* operand records */
+  int32_t n_use_units;        /* sum of spans over src + guard operands (host-computed) */
+  int32_t n_def_units;        /* sum of spans over dest operands (host-computed) */
   int32_t unit_base[8];       /* RegClass -> first unit id */
   const uint8_t*  opclass;    /* [N] OpcodeClass */
   const int32_t*  block_of;   /* [N] */
@@ -184,6 +186,14 @@ typedef struct LeoBlame {
   int32_t* count;             /* device scalar */
 } LeoBlame;
 
+/* ---- capacity hints for internal scratch (0 = default heuristic) --------- */
+typedef struct LeoCaps {
+  int64_t query_results;      /* reaching-definition results pool        (default 4 x use units) */
+  int64_t candidates;         /* per-use link candidates                  (default 6 x use units) */
+  int64_t sync_keys;          /* raw sync edges before dedup              (default 2 x N + 1024) */
+  int64_t slow_items;         /* work items re-run on the global-scratch path (default N/4 + 1024) */
+} LeoCaps;
+
 /* ---- status word (device) ------------------------------------------------ */
 enum { LEO_ST_EDGE_OVERFLOW = 1, LEO_ST_PATH_OVERFLOW = 2, LEO_ST_DIAG_OVERFLOW = 4,
        LEO_ST_BLAME_OVERFLOW = 8, LEO_ST_SCRATCH_OVERFLOW = 16, LEO_ST_BAD_INPUT = 32 };
@@ -197,8 +207,8 @@ int leo_bin_samples(const LeoSamples* s, int32_t n_instr, int32_t* lat, int32_t*
 
 /* build_graph: raw/guard edges sorted (consumer, producer, kind, class, index, span)
  * followed by the dialect's sync edges sorted (producer, consumer). */
-int leo_build_graph(const LeoKernel* k, LeoEdges* out, LeoDiags* diags, uint32_t* status,
-                    void* stream);
+int leo_build_graph(const LeoKernel* k, const LeoCaps* caps, LeoEdges* out, LeoDiags* diags,
+                    uint32_t* status, void* stream);
 
 /* run_pruning: stages 1->2->3->4 honouring cfg; `out` keeps input order. */
 int leo_prune(const LeoKernel* k, const LeoProfile* p, const LeoConfig* cfg,
@@ -216,6 +226,16 @@ int leo_blame(const LeoKernel* k, const LeoProfile* p, const LeoEdges* pruned,
               const LeoPaths* paths, const LeoEdges* base, const int32_t* line_id,
               int32_t n_lines, LeoBlame* out, double* line_blame, double* line_stall,
               uint32_t* status, void* stream);
+
+/* fused pipeline (report.py:132-142 order): optional stage-0 binning of `samples`
+ * into `p->lat` / `p->cls_cnt` (which must then be writable), build_graph,
+ * run_pruning, slice, attribute_blame(pruned, base) and the per-line rollup,
+ * all stream-ordered with no host synchronisation. */
+int leo_analyze(const LeoKernel* k, const LeoProfile* p, const LeoSamples* samples,
+                const LeoConfig* cfg, const LeoCaps* caps, LeoEdges* base, LeoEdges* pruned,
+                LeoPaths* paths, LeoDiags* diags, LeoBlame* blame, uint32_t* slice_bitmap,
+                int32_t* slice_level, const int32_t* line_id, int32_t n_lines,
+                double* line_blame, double* line_stall, uint32_t* status, void* stream);
 
 #ifdef __cplusplus
 }

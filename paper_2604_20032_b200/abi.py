@@ -15,7 +15,8 @@ P = C.c_void_p
 class LeoKernel(C.Structure):
     _fields_ = [
         ("n_instr", C.c_int32), ("n_blocks", C.c_int32), ("n_units", C.c_int32),
-        ("dialect", C.c_int32), ("n_opnd", C.c_int32), ("unit_base", C.c_int32 * 8),
+        ("dialect", C.c_int32), ("n_opnd", C.c_int32), ("n_use_units", C.c_int32),
+        ("n_def_units", C.c_int32), ("unit_base", C.c_int32 * 8),
         ("opclass", P), ("block_of", P), ("opnd_ptr", P), ("opnd", P),
         ("sync_kind", P), ("sync_a", P), ("sync_b", P),
         ("blk_first", P), ("blk_last", P), ("succ_ptr", P), ("succ", P),
@@ -39,6 +40,11 @@ class LeoConfig(C.Structure):
         ("stage_mask", C.c_uint32), ("prune_exec", C.c_int32), ("max_paths", C.c_int32),
         ("max_depth", C.c_int32), ("threshold", C.c_double * 16),
     ]
+
+
+class LeoCaps(C.Structure):
+    _fields_ = [("query_results", C.c_int64), ("candidates", C.c_int64),
+                ("sync_keys", C.c_int64), ("slow_items", C.c_int64)]
 
 
 class LeoEdges(C.Structure):
@@ -106,12 +112,24 @@ def kernel_struct(ks, ptr) -> LeoKernel:
     k.n_units = ks.n_units
     k.dialect = ks.dialect_idx
     k.n_opnd = int(ks.opnd.shape[0])
+    use_units, def_units = unit_counts(ks)
+    k.n_use_units = use_units
+    k.n_def_units = def_units
     for c in range(8):
         k.unit_base[c] = int(ks.unit_base[c])
     for name in ("opclass", "block_of", "opnd_ptr", "opnd", "sync_kind", "sync_a", "sync_b",
                  "blk_first", "blk_last", "succ_ptr", "succ", "pred_ptr", "pred"):
         setattr(k, name, ptr(name))
     return k
+
+
+def unit_counts(ks) -> tuple[int, int]:
+    """(sum of spans over src+guard operands, over dest operands)."""
+    import numpy as np
+    op = np.asarray(ks.opnd, dtype=np.uint32)
+    span = ((op >> 16) & 0xFF).astype(np.int64)
+    dst = ((op >> 27) & 3) == E.ROLE_DST
+    return int(span[~dst].sum()), int(span[dst].sum())
 
 
 def profile_struct(prof, ptr) -> LeoProfile:

@@ -1,0 +1,374 @@
+// blame.cu — stage-0 binning, backward slice, blame attribution, line rollup.
+//
+//   k_bin_samples     raw (pc, category) stream -> cls_cnt[N, 8] with warp-
+//                     aggregated atomics (__match_any_sync on pc*8+class, so a
+//                     Zipf-hot PC costs one atomic per warp); k_bin_finalize
+//                     sums lat[N]  (map_stall profile.py:106-111,
+//                     breakdown_at :307-313).
+//   incoming CSR      DependencyGraph.incoming (depgraph.py:102-108): raw/guard
+//                     edges are consumer-sorted (segment bounds by adjacent-
+//                     difference), sync edges producer-sorted (stable counting
+//                     sort by consumer); incoming(j) = regular(j) ++ sync(j).
+//   k_blame<0/1>      thread per stalled instruction: Eq. 1 (attribute_blame
+//                     analysis.py:431-484) in the reference's exact floating-
+//                     point order (no FMA contraction, CPython 3.12 sum()),
+//                     self-blame (:414-428) with the depth-8 indirect-addressing
+//                     BFS on the unpruned RAW graph (:390-411).
+//   k_lines           per-source-line FP64 scatter-add.
+//   k_slice_*         multi-source backward BFS over pruned incoming edges from
+//                     every S_j > 0, level-synchronous in one
+//                     cooperative kernel.
+#include <cooperative_groups.h>
+
+#include "prims.cuh"
+
+namespace cg = cooperative_groups;
+
+namespace leo {
+
+
+// ---- stage 0 ---------------------------------------------------------------
+__global__ void k_bin_samples(int64_t S, const int32_t* __restrict__ pc, const uint8_t* __restrict__ cat,
+                              const uint8_t* __restrict__ lut, int N, int32_t* __restrict__ cls_cnt,
+                              uint32_t* status) {
+  __shared__ uint8_t slut[256];
+  for (int x = threadIdx.x; x < 256; x += blockDim.x) slut[x] = lut[x];
+  __syncthreads();
+  const int64_t nvec = S / 4;
+  const int4* pc4 = reinterpret_cast<const int4*>(pc);
+  const uint32_t* cat4 = reinterpret_cast<const uint32_t*>(cat);
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  for (int64_t v = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; v - threadIdx.x < nvec; v += stride) {
+    const bool valid = v < nvec;
+    int4 p = valid ? pc4[v] : make_int4(0, 0, 0, 0);
+    uint32_t c = valid ? cat4[v] : 0u;
+    int pcs[4] = {p.x, p.y, p.z, p.w};
+#pragma unroll
+    for (int t = 0; t < 4; t++) {
+      int j = pcs[t];
+      bool ok = valid && j >= 0 && j < N;
+      if (valid && !ok) atomicOr(status, (uint32_t)LEO_ST_BAD_INPUT);
+      int key = ok ? j * 8 + slut[(c >> (8 * t)) & 0xFF] : -1;
+      unsigned grp = __match_any_sync(0xffffffffu, key);
+      if (ok && (__ffs(grp) - 1) == (int)(threadIdx.x & 31)) atomicAdd(&cls_cnt[key], __popc(grp));
+    }
+  }
+  // tail
+  for (int64_t s = nvec * 4 + blockIdx.x * (int64_t)blockDim.x + threadIdx.x; s < S; s += stride) {
+    int j = pc[s];
+    if (j < 0 || j >= N) { atomicOr(status, (uint32_t)LEO_ST_BAD_INPUT); continue; }
+    atomicAdd(&cls_cnt[j * 8 + slut[cat[s]]], 1);
+  }
+}
+
+__global__ void k_bin_finalize(int N, const int32_t* __restrict__ cls_cnt, int32_t* __restrict__ lat) {
+  for (int j = blockIdx.x * blockDim.x + threadIdx.x; j < N; j += gridDim.x * blockDim.x) {
+    const int4* row = reinterpret_cast<const int4*>(cls_cnt + (size_t)j * 8);
+    int4 a = row[0], b = row[1];
+    lat[j] = a.x + a.y + a.z + a.w + b.x + b.y + b.z + b.w;
+  }
+}
+
+// ---- incoming CSR ------------------------------------------------------------
+// regular (raw/guard) edges [0, n_reg) are sorted by consumer
+__global__ void k_seg_bounds(const int32_t* __restrict__ cons, const int32_t* n_reg_dev,
+                             int32_t* __restrict__ rbeg, int32_t* __restrict__ rend) {
+  const int n = *n_reg_dev;
+  for (int e = blockIdx.x * blockDim.x + threadIdx.x; e < n; e += gridDim.x * blockDim.x) {
+    int c = cons[e];
+    if (e == 0 || cons[e - 1] != c) rbeg[c] = e;
+    if (e == n - 1 || cons[e + 1] != c) rend[c] = e + 1;
+  }
+}
+// sync edges [n_reg, n) : histogram by consumer
+__global__ void k_sync_hist(const int32_t* __restrict__ cons, const int32_t* n_reg_dev, const int32_t* n_dev,
+                            int32_t* __restrict__ cnt) {
+  const int r = *n_reg_dev, n = *n_dev;
+  for (int e = r + blockIdx.x * blockDim.x + threadIdx.x; e < n; e += gridDim.x * blockDim.x)
+    atomicAdd(&cnt[cons[e]], 1);
+}
+__global__ void k_sync_fill(const int32_t* __restrict__ cons, const int32_t* n_reg_dev, const int32_t* n_dev,
+                            const int32_t* __restrict__ off, int32_t* __restrict__ cursor,
+                            uint64_t* __restrict__ out) {
+  const int r = *n_reg_dev, n = *n_dev;
+  for (int e = r + blockIdx.x * blockDim.x + threadIdx.x; e < n; e += gridDim.x * blockDim.x) {
+    int c = cons[e];
+    out[off[c] + atomicAdd(&cursor[c], 1)] = (uint64_t)(uint32_t)e;
+  }
+}
+
+struct Incoming {
+  const int32_t* rbeg;      // [N] regular edge range (rbeg == rend when none)
+  const int32_t* rend;
+  const int32_t* soff;      // [N+1] sync edge list offsets
+  const uint64_t* sidx;     // sync edge indices (sorted per consumer = edge-list order)
+  LEO_DEV int deg(int j) const { return (rend[j] - rbeg[j]) + (soff[j + 1] - soff[j]); }
+  LEO_DEV int edge(int j, int x) const {
+    int r = rend[j] - rbeg[j];
+    return x < r ? rbeg[j] + x : (int)sidx[soff[j] + (x - r)];
+  }
+};
+
+// ---- self blame ----------------------------------------------------------------
+__constant__ static const int kMatchClass[3] = {LEO_CS_MEMORY_DEP, LEO_CS_EXECUTION_DEP, LEO_CS_SYNCHRONIZATION};
+__constant__ static const int kSelfByClass[8] = {LEO_SB_MEMORY_LATENCY, LEO_SB_COMPUTE_SATURATION,
+    LEO_SB_SYNCHRONIZATION_OVERHEAD, LEO_SB_INSTRUCTION_FETCH, LEO_SB_PIPELINE_CONTENTION,
+    LEO_SB_PIPELINE_CONTENTION, LEO_SB_PIPELINE_CONTENTION, LEO_SB_PIPELINE_CONTENTION};
+
+// _address_traces_to_load on the base graph's RAW edges (regular part only:
+// sync edges are never RAW).  Returns 1/0, or -1 when `seen` overflowed.
+LEO_DEV int traces_to_load(const KView& k, const int32_t* brbeg, const int32_t* brend,
+                           const int32_t* bprod, const uint32_t* bmeta, int index,
+                           int32_t* seen, int cap, int32_t* stamp, int stamp_val) {
+  // seen[0..n) holds visited nodes in BFS order; frontier = seen[lo..hi)
+  int n = 1, lo = 0, hi = 1;
+  seen[0] = index;
+  if (stamp) stamp[index] = stamp_val;
+  for (int depth = 0; depth < 8; depth++) {
+    for (int a = lo; a < hi; a++) {
+      const int node = seen[a];
+      for (int e = brbeg[node]; e < brend[node]; e++) {
+        if (((bmeta[e] >> 27) & 7) != LEO_EK_RAW) continue;
+        const int p = bprod[e];
+        bool dup = false;
+        if (stamp) dup = stamp[p] == stamp_val;
+        else for (int x = 0; x < n; x++) if (seen[x] == p) { dup = true; break; }
+        if (dup) continue;
+        if (kMemoryProducer & BIT(k.opclass[p])) return 1;
+        if (n == cap) return -1;
+        seen[n++] = p;
+        if (stamp) stamp[p] = stamp_val;
+      }
+    }
+    if (n == hi) return 0;
+    lo = hi; hi = n;
+  }
+  return 0;
+}
+
+struct BlameArgs {
+  PView p;
+  const int32_t* pprod;
+  const uint32_t* pmeta;
+  const double* pdist;
+  Incoming inc;
+  const int32_t* brbeg;     // base graph regular incoming
+  const int32_t* brend;
+  const int32_t* bprod;
+  const uint32_t* bmeta;
+  int32_t* ecount;          // [N] entries per instruction (pass 0)
+  int32_t* self_sub;        // [N] subcategory for self entries (-1 when edges)
+  double* jtotal;           // [N] cached normaliser
+  double* jnsum;            // [N]
+  const int32_t* eoff;      // [N+1] (pass 1)
+  LeoBlame out;
+  int32_t* slow_list;
+  int32_t* slow_count;
+  int64_t slow_cap;
+  uint32_t* status;
+};
+
+LEO_DEV double issue_count(const PView& p, int i) {   // profile.py:321-329
+  if (p.exec_cnt[i] >= 0) return (double)p.exec_cnt[i];
+  if (p.sampled[i]) return (double)(p.total[i] >= 0 ? p.total[i] : p.lat[i]);
+  return 1.0;
+}
+
+LEO_DEV int dominant_self(const PView& p, int j) {     // _dominant_class :379-387
+  int dom = 0, best = -1;
+  for (int c = 0; c < 8; c++) {
+    int v = p.cls_cnt[(size_t)j * 8 + c];
+    if (v > best) { best = v; dom = c; }
+  }
+  return kSelfByClass[dom];
+}
+
+constexpr int kSeenCap = 96;
+
+// pass 0: decide self vs edges, entry count, cached sums; pass 1: write entries
+template <int PASS>
+__global__ void k_blame(KView k, BlameArgs a) {
+  for (int j = blockIdx.x * blockDim.x + threadIdx.x; j < k.N; j += gridDim.x * blockDim.x) {
+    const int lat = a.p.lat[j];
+    const double s_j = (double)((int64_t)lat * a.p.period);
+    if (PASS == 0) { a.ecount[j] = 0; a.self_sub[j] = -1; }
+    if (s_j == 0) continue;
+    const int deg = a.inc.deg(j);
+    if (PASS == 0) {
+      bool self = deg == 0;
+      double total = 0.0, n_sum = 0.0;
+      if (!self) {
+        double d_min = 0, e_min = 0;
+        PySum ns;
+        for (int x = 0; x < deg; x++) {
+          int e = a.inc.edge(j, x);
+          int pr = a.pprod[e];
+          double d = a.pdist[e], ef = a.p.eff[pr];
+          if (x == 0 || d < d_min) d_min = d;
+          if (x == 0 || ef < e_min) e_min = ef;
+          ns.add(issue_count(a.p, pr));
+        }
+        n_sum = ns.value();
+        if (n_sum == 0) self = true;
+        else {
+          PySum ts;
+          for (int x = 0; x < deg; x++) {
+            int e = a.inc.edge(j, x);
+            int pr = a.pprod[e];
+            double f0 = __ddiv_rn(d_min, a.pdist[e]);
+            double f1 = __ddiv_rn(e_min, a.p.eff[pr]);
+            double f2 = __ddiv_rn(issue_count(a.p, pr), n_sum);
+            double f3 = __ddiv_rn((double)a.p.cls_cnt[(size_t)j * 8 + kMatchClass[(a.pmeta[e] >> 30) & 3]], (double)lat);
+            ts.add(__dmul_rn(__dmul_rn(__dmul_rn(f0, f1), f2), f3));
+          }
+          total = ts.value();
+          if (total == 0.0) self = true;
+        }
+      }
+      if (self) {
+        int sub = dominant_self(a.p, j);
+        if (sub == LEO_SB_MEMORY_LATENCY && (kMemoryClasses & BIT(k.opclass[j]))) {
+          int32_t seen[kSeenCap];
+          int r = traces_to_load(k, a.brbeg, a.brend, a.bprod, a.bmeta, j, seen, kSeenCap, nullptr, 0);
+          if (r < 0) {
+            int s = atomicAdd(a.slow_count, 1);
+            if (s < a.slow_cap) a.slow_list[s] = j;
+            else atomicOr(a.status, (uint32_t)LEO_ST_SCRATCH_OVERFLOW);
+          } else if (r) sub = LEO_SB_INDIRECT_ADDRESSING;
+        }
+        a.self_sub[j] = sub;
+        a.ecount[j] = 1;
+      } else {
+        a.ecount[j] = deg;
+        a.jtotal[j] = total;
+        a.jnsum[j] = n_sum;
+      }
+    } else {
+      const int o = a.eoff[j];
+      if (o + a.ecount[j] > a.out.capacity) { atomicOr(a.status, (uint32_t)LEO_ST_BLAME_OVERFLOW); continue; }
+      if (a.self_sub[j] >= 0) {
+        a.out.stalled[o] = j;
+        a.out.edge[o] = -1;
+        a.out.sub[o] = (uint8_t)a.self_sub[j];
+        a.out.blame[o] = s_j;
+        for (int c = 0; c < 4; c++) a.out.factors[(size_t)o * 4 + c] = 0.0;
+        continue;
+      }
+      double d_min = 0, e_min = 0;
+      for (int x = 0; x < deg; x++) {
+        int e = a.inc.edge(j, x);
+        double d = a.pdist[e], ef = a.p.eff[a.pprod[e]];
+        if (x == 0 || d < d_min) d_min = d;
+        if (x == 0 || ef < e_min) e_min = ef;
+      }
+      const double total = a.jtotal[j], n_sum = a.jnsum[j];
+      for (int x = 0; x < deg; x++) {
+        int e = a.inc.edge(j, x);
+        int pr = a.pprod[e];
+        double f0 = __ddiv_rn(d_min, a.pdist[e]);
+        double f1 = __ddiv_rn(e_min, a.p.eff[pr]);
+        double f2 = __ddiv_rn(issue_count(a.p, pr), n_sum);
+        double f3 = __ddiv_rn((double)a.p.cls_cnt[(size_t)j * 8 + kMatchClass[(a.pmeta[e] >> 30) & 3]], (double)lat);
+        double prod = __dmul_rn(__dmul_rn(__dmul_rn(f0, f1), f2), f3);
+        a.out.stalled[o + x] = j;
+        a.out.edge[o + x] = e;
+        a.out.sub[o + x] = 255;
+        a.out.blame[o + x] = __ddiv_rn(__dmul_rn(s_j, prod), total);
+        double* f = a.out.factors + (size_t)(o + x) * 4;
+        f[0] = f0; f[1] = f1; f[2] = f2; f[3] = f3;
+      }
+    }
+  }
+}
+template __global__ void k_blame<0>(KView, BlameArgs);
+template __global__ void k_blame<1>(KView, BlameArgs);
+
+__global__ void k_selfblame_slow(KView k, BlameArgs a, int32_t* scratch, int nworkers) {
+  const int ns = (int)min((int64_t)*a.slow_count, a.slow_cap);
+  const int w = blockIdx.x * blockDim.x + threadIdx.x;
+  if (w >= nworkers) return;
+  int32_t* stamp = scratch + (size_t)w * 2 * (k.N + 1);
+  int32_t* seen = stamp + (k.N + 1);
+  for (int t = w; t < ns; t += nworkers) {
+    int j = a.slow_list[t];
+    int r = traces_to_load(k, a.brbeg, a.brend, a.bprod, a.bmeta, j, seen, k.N + 1, stamp, j + 1);
+    if (r > 0) a.self_sub[j] = LEO_SB_INDIRECT_ADDRESSING;
+  }
+}
+
+__global__ void k_blame_count(const int32_t* eoff, int N, LeoBlame out) { *out.count = eoff[N]; }
+
+// ---- per-source-line rollup -----------------------------------------------------
+__global__ void k_lines(KView k, PView p, const int32_t* __restrict__ pprod, LeoBlame b,
+                        const int32_t* __restrict__ line_id, double* __restrict__ line_blame,
+                        double* __restrict__ line_stall) {
+  const int n = min(*b.count, b.capacity);
+  const int stride = gridDim.x * blockDim.x;
+  for (int x = blockIdx.x * blockDim.x + threadIdx.x; x < n; x += stride) {
+    int e = b.edge[x];
+    int at = e < 0 ? b.stalled[x] : pprod[e];
+    atomicAdd(&line_blame[line_id[at]], b.blame[x]);
+  }
+  for (int j = blockIdx.x * blockDim.x + threadIdx.x; j < k.N; j += stride) {
+    int lat = p.lat[j];
+    if (lat) atomicAdd(&line_stall[line_id[j]], (double)((int64_t)lat * p.period));
+  }
+}
+
+// ---- backward slice ----------------------------------------------------------------
+struct SliceArgs {
+  const int32_t* lat;
+  const int32_t* pprod;
+  Incoming inc;
+  int32_t* level;
+  int32_t* fa;        // frontier buffers [N]
+  int32_t* fb;
+  int32_t* counts;    // [2] frontier sizes (ping-pong) + [2] scratch
+  uint32_t* bitmap;
+};
+
+__global__ void k_slice(int N, SliceArgs a) {
+  cg::grid_group grid = cg::this_grid();
+  const int tid = blockIdx.x * blockDim.x + threadIdx.x, nt = gridDim.x * blockDim.x;
+  if (tid == 0) { a.counts[0] = 0; a.counts[1] = 0; }
+  grid.sync();
+  for (int j = tid; j < N; j += nt) {
+    bool src = a.lat[j] != 0;
+    a.level[j] = src ? 0 : -1;
+    if (src) a.fa[atomicAdd(&a.counts[0], 1)] = j;
+  }
+  grid.sync();
+  int32_t *cur = a.fa, *nxt = a.fb;
+  int ci = 0;
+  for (int lv = 1;; lv++) {
+    const int n = a.counts[ci];
+    if (n == 0) break;
+    // warp-cooperative expansion: one warp per frontier node
+    const int lane = threadIdx.x & 31, gw = tid >> 5, nw = nt >> 5;
+    for (int f = gw; f < n; f += nw) {
+      const int v = cur[f];
+      const int deg = a.inc.deg(v);
+      for (int x = lane; x < deg; x += 32) {
+        const int p = a.pprod[a.inc.edge(v, x)];
+        if (a.level[p] < 0 && atomicCAS(&a.level[p], -1, lv) == -1)
+          nxt[atomicAdd(&a.counts[ci ^ 1], 1)] = p;
+      }
+    }
+    grid.sync();
+    if (tid == 0) a.counts[ci] = 0;
+    int32_t* t = cur; cur = nxt; nxt = t;
+    ci ^= 1;
+    grid.sync();
+  }
+  // bitmap words
+  for (int w = tid; w < (N + 31) / 32; w += nt) {
+    uint32_t word = 0;
+    for (int b = 0; b < 32; b++) {
+      int j = w * 32 + b;
+      if (j < N && a.level[j] >= 0) word |= 1u << b;
+    }
+    a.bitmap[w] = word;
+  }
+}
+
+}  // namespace leo

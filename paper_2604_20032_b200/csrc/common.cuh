@@ -1,0 +1,106 @@
+// common.cuh — shared device helpers for the LEO B200 hot path (sm_100a).
+#pragma once
+#include <cstdint>
+#include <cuda_runtime.h>
+
+#include "../../include/leo_b200.h"
+
+#define LEO_DEV __device__ __forceinline__
+
+#define BIT(c) (1u << (c))
+constexpr uint32_t kMemoryProducer = BIT(LEO_OC_GLOBAL_LOAD) | BIT(LEO_OC_LOCAL_LOAD) |
+    BIT(LEO_OC_SCALAR_LOAD) | BIT(LEO_OC_CONSTANT_LOAD) | BIT(LEO_OC_ATOMIC) | BIT(LEO_OC_SEND);
+constexpr uint32_t kMemoryClasses = kMemoryProducer | BIT(LEO_OC_GLOBAL_STORE) | BIT(LEO_OC_LOCAL_STORE);
+constexpr uint32_t kCompute = BIT(LEO_OC_FP_ARITH) | BIT(LEO_OC_INT_ARITH) | BIT(LEO_OC_CONVERSION);
+constexpr uint32_t kVmcnt = BIT(LEO_OC_GLOBAL_LOAD) | BIT(LEO_OC_GLOBAL_STORE) | BIT(LEO_OC_ATOMIC);
+constexpr uint32_t kLgkmcnt = BIT(LEO_OC_LOCAL_LOAD) | BIT(LEO_OC_LOCAL_STORE) |
+    BIT(LEO_OC_SCALAR_LOAD) | BIT(LEO_OC_CONSTANT_LOAD);
+
+// RegClass rank in `.value` string order (depgraph.py:514-516 sort key)
+__constant__ static const int kRcRank[8] = {6, 2, 1, 0, 5, 3, 4, 7};
+
+LEO_DEV int op_index(uint32_t r) { return (int)(r & 0xFFFF); }
+LEO_DEV int op_span(uint32_t r) { return (int)((r >> 16) & 0xFF); }
+LEO_DEV int op_class(uint32_t r) { return (int)((r >> 24) & 7); }
+LEO_DEV int op_role(uint32_t r) { return (int)((r >> 27) & 3); }
+
+LEO_DEV int dep_class_of(uint32_t producer_oc, int kind) {   // depgraph.py:63-68
+  if (kind >= LEO_EK_MEM_WAITCNT) return LEO_DC_MEMORY;
+  if (kMemoryProducer & BIT(producer_oc)) return LEO_DC_MEMORY;
+  if (producer_oc == LEO_OC_BARRIER_ALL) return LEO_DC_SYNCHRONIZATION;
+  return LEO_DC_EXECUTION;
+}
+
+// Kernel struct passed by value to kernels (pointers are device pointers).
+struct KView {
+  int32_t N, B, U, dialect;
+  int32_t unit_base[8];
+  const uint8_t* __restrict__ opclass;
+  const int32_t* __restrict__ block_of;
+  const int32_t* __restrict__ opnd_ptr;
+  const uint32_t* __restrict__ opnd;
+  const uint8_t* __restrict__ sync_kind;
+  const uint32_t* __restrict__ sync_a;
+  const uint32_t* __restrict__ sync_b;
+  const int32_t* __restrict__ blk_first;
+  const int32_t* __restrict__ blk_last;
+  const int32_t* __restrict__ succ_ptr;
+  const int32_t* __restrict__ succ;
+  const int32_t* __restrict__ pred_ptr;
+  const int32_t* __restrict__ pred;
+};
+
+inline KView make_kview(const LeoKernel* k) {
+  KView v;
+  v.N = k->n_instr; v.B = k->n_blocks; v.U = k->n_units; v.dialect = k->dialect;
+  for (int c = 0; c < 8; c++) v.unit_base[c] = k->unit_base[c];
+  v.opclass = k->opclass; v.block_of = k->block_of; v.opnd_ptr = k->opnd_ptr; v.opnd = k->opnd;
+  v.sync_kind = k->sync_kind; v.sync_a = k->sync_a; v.sync_b = k->sync_b;
+  v.blk_first = k->blk_first; v.blk_last = k->blk_last; v.succ_ptr = k->succ_ptr;
+  v.succ = k->succ; v.pred_ptr = k->pred_ptr; v.pred = k->pred;
+  return v;
+}
+
+LEO_DEV int unit_of(const KView& k, uint32_t r) { return k.unit_base[op_class(r)] + op_index(r); }
+
+// ---- diagnostics ------------------------------------------------------------
+LEO_DEV void diag_push(LeoDiags d, uint32_t* status, int code, int instr, int a0, int a1, int a2, int seq) {
+  int slot = atomicAdd(d.count, 1);
+  if (slot < d.capacity) {
+    LeoDiag r; r.code = code; r.instr = instr; r.a0 = a0; r.a1 = a1; r.a2 = a2; r.seq = seq;
+    d.rec[slot] = r;
+  } else {
+    atomicOr(status, (uint32_t)LEO_ST_DIAG_OVERFLOW);
+  }
+}
+
+// ---- CPython >= 3.12 builtins.sum over floats (Neumaier), analysis.py:464,472
+struct PySum {
+  double s, c; int n;
+  LEO_DEV PySum() : s(0.0), c(0.0), n(0) {}
+  LEO_DEV void add(double x) {
+    if (n++ == 0) { s = __dadd_rn(0.0, x); c = 0.0; return; }
+    double t = __dadd_rn(s, x);
+    if (fabs(s) >= fabs(x)) c = __dadd_rn(c, __dadd_rn(__dsub_rn(s, t), x));
+    else c = __dadd_rn(c, __dadd_rn(__dsub_rn(x, t), s));
+    s = t;
+  }
+  LEO_DEV double value() const {
+    if (c != 0.0 && isfinite(c)) return __dadd_rn(s, c);
+    return s;
+  }
+};
+
+// ---- launch helpers ---------------------------------------------------------
+inline int grid_for(int64_t n, int threads, int max_blocks = 148 * 32) {
+  int64_t g = (n + threads - 1) / threads;
+  if (g < 1) g = 1;
+  if (g > max_blocks) g = max_blocks;
+  return (int)g;
+}
+
+#define LEO_CUDA_CHECK(x)                                      \
+  do {                                                         \
+    cudaError_t _e = (x);                                      \
+    if (_e != cudaSuccess) return -1000 - (int)_e;             \
+  } while (0)

@@ -1,0 +1,340 @@
+// graph.cu — register dependency edges (reaching definitions + per-use link).
+//
+// Replaces depgraph.reaching_definitions (depgraph.py:135-177), per_use_link
+// (:188-223), liveness_filter (:274-293; identity on pipeline output, see
+// DESIGN.md) and the raw/guard half of build_graph (:510-524).
+//
+// Device algorithm
+//   G0 k_unit_counts   thread/instr: use-unit and def-unit counts -> scans
+//   G1 k_block_walk    warp/basic block, per-warp unit table in shared memory:
+//                      every use-unit event resolves to its in-block reaching
+//                      def, or to an upward-exposed (block, unit) query (one
+//                      per distinct unit per block, deduplicated with
+//                      __match_any_sync); emits each block's (unit, last def)
+//                      summary sorted by unit.
+//   G2 k_reach         thread/query: backward search over predecessor blocks
+//                      through blocks transparent to the unit; the union of the
+//                      last defs of the defining blocks reached is exactly the
+//                      least fixed point reach_in(b)[u] of the reference's
+//                      worklist.  Overflowing searches re-run on global scratch.
+//   G3/G4 k_link_*     thread/consumer: count, then write candidate keys
+//                      (producer, kind, class rank, index, span)
+//   G5 segsort_unique  per consumer: reference sort order + dedup on the full key
+//   G6 k_link_emit     edges in (consumer, producer, kind, class, index, span) order
+#include "prims.cuh"
+
+namespace leo {
+
+__global__ void k_unit_counts(KView k, int32_t* __restrict__ ucnt, int32_t* __restrict__ dcnt) {
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < k.N; i += gridDim.x * blockDim.x) {
+    int u = 0, d = 0;
+    for (int q = k.opnd_ptr[i]; q < k.opnd_ptr[i + 1]; q++) {
+      uint32_t r = k.opnd[q];
+      if (op_role(r) == LEO_ROLE_DST) d += op_span(r); else u += op_span(r);
+    }
+    ucnt[i] = u;
+    dcnt[i] = d;
+  }
+}
+
+// unit of the x-th use-unit (or def-unit when `defs`) event of instruction i
+LEO_DEV int event_unit(const KView& k, int i, int x, bool defs, int* opos, uint32_t* oref) {
+  for (int q = k.opnd_ptr[i]; q < k.opnd_ptr[i + 1]; q++) {
+    uint32_t r = k.opnd[q];
+    bool is_def = op_role(r) == LEO_ROLE_DST;
+    if (is_def != defs) continue;
+    int s = op_span(r);
+    if (x < s) { *opos = q - k.opnd_ptr[i]; *oref = r; return unit_of(k, r) + x; }
+    x -= s;
+  }
+  return -1;
+}
+
+struct WalkArgs {
+  const int32_t* use_ptr;    // [N+1]
+  const int32_t* def_ptr;    // [N+1]
+  int32_t* ev_res;           // [use units] def (>=0) or -(query slot+1)
+  int32_t* q_block;          // [use units]
+  int32_t* q_unit;           // [use units]
+  int32_t* q_list;           // [use units]
+  int32_t* q_count;          // scalar
+  uint64_t* bdef;            // [def units] (unit << 32 | last def) per block, sorted by unit
+  int32_t* bdef_len;         // [B]
+  int32_t* gtab;             // global per-warp tables (when U too large for smem) or null
+};
+
+// warp per block; blocks visited in increasing order per warp so that stale
+// table entries (from earlier blocks) are recognisable by index comparison.
+__global__ void k_block_walk(KView k, WalkArgs a, int warps_per_cta) {
+  extern __shared__ int32_t smem[];
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  const int gw = blockIdx.x * warps_per_cta + wid, nw = gridDim.x * warps_per_cta;
+  const int U = k.U;
+  int32_t* last = a.gtab ? a.gtab + (size_t)gw * 2 * U : smem + (size_t)wid * 2 * U;
+  int32_t* qtab = last + U;
+  for (int u = lane; u < U; u += 32) { last[u] = -1; qtab[u] = -1; }
+  __syncwarp();
+  for (int b = gw; b < k.B; b += nw) {
+    const int first = k.blk_first[b], lastI = k.blk_last[b];
+    const int ev_block = a.use_ptr[first];
+    for (int i = first; i <= lastI; i++) {
+      const int e0 = a.use_ptr[i], e1 = a.use_ptr[i + 1];
+      for (int base = e0; base < e1; base += 32) {
+        const int e = base + lane;
+        const bool valid = e < e1;
+        int u = -1, res = 0;
+        bool fresh = false;
+        if (valid) {
+          int opos; uint32_t oref;
+          u = event_unit(k, i, e - e0, false, &opos, &oref);
+          int ld = last[u];
+          if (ld >= first) res = ld;
+          else if (qtab[u] >= ev_block) res = -(qtab[u] + 1);
+          else fresh = true;
+        }
+        unsigned fm = __ballot_sync(0xffffffffu, fresh);
+        if (fm) {
+          unsigned grp = __match_any_sync(0xffffffffu, fresh ? u : -2 - lane);
+          int leader = __ffs(grp) - 1;
+          int slot = __shfl_sync(0xffffffffu, e, leader);
+          bool lead = fresh && lane == leader;
+          unsigned lm = __ballot_sync(0xffffffffu, lead);
+          int qbase = 0;
+          if (lane == 0 && lm) qbase = atomicAdd(a.q_count, __popc(lm));
+          qbase = __shfl_sync(0xffffffffu, qbase, 0);
+          if (fresh) res = -(slot + 1);
+          if (lead) {
+            qtab[u] = e;
+            a.q_block[e] = b;
+            a.q_unit[e] = u;
+            a.q_list[qbase + __popc(lm & ((1u << lane) - 1))] = e;
+          }
+        }
+        if (valid) a.ev_res[e] = res;
+        __syncwarp();
+      }
+      const int d0 = a.def_ptr[i], d1 = a.def_ptr[i + 1];
+      for (int d = d0 + lane; d < d1; d += 32) {
+        int opos; uint32_t oref;
+        int u = event_unit(k, i, d - d0, true, &opos, &oref);
+        last[u] = i;
+      }
+      __syncwarp();
+    }
+    // block summary: every unit whose last def lies in this block, by unit
+    int cnt = 0;
+    uint64_t* out = a.bdef + a.def_ptr[first];
+    for (int base = 0; base < U; base += 32) {
+      int u = base + lane;
+      int ld = u < U ? last[u] : -1;
+      bool q = ld >= first;
+      unsigned m = __ballot_sync(0xffffffffu, q);
+      if (q) out[cnt + __popc(m & ((1u << lane) - 1))] = ((uint64_t)u << 32) | (uint32_t)ld;
+      cnt += __popc(m);
+    }
+    if (lane == 0) a.bdef_len[b] = cnt;
+    __syncwarp();
+  }
+}
+
+// last definition of unit u in block p, -1 if p is transparent to u
+LEO_DEV int lastdef_in_block(const KView& k, const int32_t* def_ptr, const uint64_t* bdef,
+                             const int32_t* bdef_len, int p, int u) {
+  const uint64_t* s = bdef + def_ptr[k.blk_first[p]];
+  int lo = 0, hi = bdef_len[p] - 1;
+  while (lo <= hi) {
+    int mid = (lo + hi) >> 1;
+    int mu = (int)(s[mid] >> 32);
+    if (mu == u) return (int)(uint32_t)s[mid];
+    if (mu < u) lo = mid + 1; else hi = mid - 1;
+  }
+  return -1;
+}
+
+struct ReachArgs {
+  const int32_t* def_ptr;
+  const uint64_t* bdef;
+  const int32_t* bdef_len;
+  const int32_t* q_block;
+  const int32_t* q_unit;
+  int32_t* q_off;            // [use units] result offset per query slot
+  int32_t* q_len;            // [use units]
+  int32_t* qres;             // results pool
+  int64_t qres_cap;
+  int32_t* qres_count;
+  int32_t* slow_list;
+  int32_t* slow_count;
+  int64_t slow_cap;
+  uint32_t* status;
+};
+
+// Backward search for query (b, u).  visited / stack / results live in the
+// caller's buffers (registers-backed local arrays on the fast path, global
+// scratch on the slow path).  Returns false when a buffer overflowed.
+LEO_DEV bool reach_search(const KView& k, const ReachArgs& a, int b, int u, int32_t* vis, int vcap,
+                          int32_t* stk, int scap, int32_t* res, int rcap, int* nres_out,
+                          int32_t* stamp, int stamp_val) {
+  int nvis = 0, sp = 0, nres = 0;
+  auto visit = [&](int p) -> int {   // 1 new, 0 seen, -1 overflow
+    if (stamp) {
+      if (stamp[p] == stamp_val) return 0;
+      stamp[p] = stamp_val;
+      return 1;
+    }
+    for (int x = 0; x < nvis; x++) if (vis[x] == p) return 0;
+    if (nvis == vcap) return -1;
+    vis[nvis++] = p;
+    return 1;
+  };
+  for (int q = k.pred_ptr[b]; q < k.pred_ptr[b + 1]; q++) {
+    int p = k.pred[q];
+    int v = visit(p);
+    if (v < 0) return false;
+    if (v) { if (sp == scap) return false; stk[sp++] = p; }
+  }
+  while (sp > 0) {
+    int p = stk[--sp];
+    int ld = lastdef_in_block(k, a.def_ptr, a.bdef, a.bdef_len, p, u);
+    if (ld >= 0) {
+      if (nres == rcap) return false;
+      res[nres++] = ld;
+      continue;
+    }
+    for (int q = k.pred_ptr[p]; q < k.pred_ptr[p + 1]; q++) {
+      int pp = k.pred[q];
+      int v = visit(pp);
+      if (v < 0) return false;
+      if (v) { if (sp == scap) return false; stk[sp++] = pp; }
+    }
+  }
+  *nres_out = nres;
+  return true;
+}
+
+LEO_DEV void reach_commit(const ReachArgs& a, int e, const int32_t* res, int nres) {
+  int off = atomicAdd(a.qres_count, nres);
+  if ((int64_t)off + nres > a.qres_cap) {
+    atomicOr(a.status, (uint32_t)LEO_ST_SCRATCH_OVERFLOW);
+    a.q_off[e] = 0; a.q_len[e] = 0;
+    return;
+  }
+  for (int x = 0; x < nres; x++) a.qres[off + x] = res[x];
+  a.q_off[e] = off;
+  a.q_len[e] = nres;
+}
+
+constexpr int kReachV = 48, kReachS = 48, kReachR = 24;
+
+__global__ void k_reach_fast(KView k, ReachArgs a, const int32_t* __restrict__ q_list,
+                             const int32_t* q_count) {
+  const int nq = *q_count;
+  for (int t = blockIdx.x * blockDim.x + threadIdx.x; t < nq; t += gridDim.x * blockDim.x) {
+    int e = q_list[t];
+    int32_t vis[kReachV], stk[kReachS], res[kReachR];
+    int nres = 0;
+    if (reach_search(k, a, a.q_block[e], a.q_unit[e], vis, kReachV, stk, kReachS, res, kReachR,
+                     &nres, nullptr, 0)) {
+      reach_commit(a, e, res, nres);
+    } else {
+      int s = atomicAdd(a.slow_count, 1);
+      if (s < a.slow_cap) a.slow_list[s] = e;
+      else atomicOr(a.status, (uint32_t)LEO_ST_SCRATCH_OVERFLOW);
+    }
+  }
+}
+
+// slow path: one worker thread per slot of global scratch (stamp/stack/results
+// of B entries each); stamps are query slot + 1, so no clearing between queries.
+__global__ void k_reach_slow(KView k, ReachArgs a, int32_t* scratch, int nworkers) {
+  const int ns = min((int64_t)*a.slow_count, a.slow_cap);
+  const int w = blockIdx.x * blockDim.x + threadIdx.x;
+  if (w >= nworkers) return;
+  const int B = k.B;
+  int32_t* stamp = scratch + (size_t)w * 3 * (B + 1);
+  int32_t* stk = stamp + (B + 1);
+  int32_t* res = stk + (B + 1);
+  for (int t = w; t < ns; t += nworkers) {
+    int e = a.slow_list[t];
+    int nres = 0;
+    reach_search(k, a, a.q_block[e], a.q_unit[e], nullptr, 0, stk, B + 1, res, B + 1, &nres,
+                 stamp, e + 1);
+    reach_commit(a, e, res, nres);
+  }
+}
+
+struct LinkArgs {
+  const int32_t* use_ptr;
+  const int32_t* ev_res;
+  const int32_t* q_off;
+  const int32_t* q_len;
+  const int32_t* qres;
+  int32_t* cand_cnt;         // [N]
+  const int32_t* cand_off;   // [N+1]
+  uint64_t* cand;            // keys
+  int64_t cand_cap;
+  LeoDiags diags;
+  uint32_t* status;
+};
+
+LEO_DEV uint64_t link_key(int producer, int kind, uint32_t r) {
+  uint64_t ref = ((uint64_t)kRcRank[op_class(r)] << 24) | ((uint64_t)op_index(r) << 8) | (uint64_t)op_span(r);
+  return ((uint64_t)producer << 28) | ((uint64_t)(kind == LEO_EK_RAW ? 1 : 0) << 27) | ref;
+}
+
+// mode 0: count candidates + unresolved diagnostics; mode 1: write keys
+template <int MODE>
+__global__ void k_link(KView k, LinkArgs a) {
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < k.N; i += gridDim.x * blockDim.x) {
+    int e = a.use_ptr[i];
+    int cnt = 0;
+    int64_t w = MODE ? a.cand_off[i] : 0;
+    if (MODE && (int64_t)a.cand_off[i + 1] > a.cand_cap) { atomicOr(a.status, (uint32_t)LEO_ST_SCRATCH_OVERFLOW); continue; }
+    for (int q = k.opnd_ptr[i]; q < k.opnd_ptr[i + 1]; q++) {
+      uint32_t r = k.opnd[q];
+      int role = op_role(r);
+      if (role == LEO_ROLE_DST) continue;
+      int kind = role == LEO_ROLE_GUARD ? LEO_EK_GUARD : LEO_EK_RAW;
+      bool found = false;
+      for (int s = 0; s < op_span(r); s++, e++) {
+        int res = a.ev_res[e];
+        if (res >= 0) {
+          found = true;
+          if (MODE) a.cand[w++] = link_key(res, kind, r); else cnt++;
+        } else {
+          int qs = -(res + 1);
+          int L = a.q_len[qs], off = a.q_off[qs];
+          if (L > 0) found = true;
+          if (MODE) { for (int x = 0; x < L; x++) a.cand[w++] = link_key(a.qres[off + x], kind, r); }
+          else cnt += L;
+        }
+      }
+      if (!MODE && !found)   // depgraph.py:208-210 — no unit of the ref has a def
+        diag_push(a.diags, a.status, LEO_DIAG_UNRESOLVED, i, (int)r, 0, 0, q - k.opnd_ptr[i]);
+    }
+    if (!MODE) a.cand_cnt[i] = cnt;
+  }
+}
+
+__constant__ static const int kRankToClass[8] = {3, 2, 1, 5, 6, 4, 0, 7};
+
+__global__ void k_link_emit(KView k, const int32_t* __restrict__ cand_off, const uint64_t* __restrict__ cand,
+                            const int32_t* __restrict__ uniq, const int32_t* __restrict__ eoff,
+                            LeoEdges out, uint32_t* status) {
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < k.N; i += gridDim.x * blockDim.x) {
+    int n = uniq[i], o = eoff[i];
+    if (o + n > out.capacity) { if (n) atomicOr(status, (uint32_t)LEO_ST_EDGE_OVERFLOW); continue; }
+    const uint64_t* c = cand + cand_off[i];
+    for (int x = 0; x < n; x++) {
+      uint64_t key = c[x];
+      int prod = (int)(key >> 28);
+      int kind = ((key >> 27) & 1) ? LEO_EK_RAW : LEO_EK_GUARD;
+      int cls = kRankToClass[(key >> 24) & 7];
+      uint32_t ref27 = (uint32_t)((key >> 8) & 0xFFFF) | ((uint32_t)(key & 0xFF) << 16) | ((uint32_t)cls << 24);
+      out.prod[o + x] = prod;
+      out.cons[o + x] = i;
+      out.meta[o + x] = LEO_META(kind, dep_class_of(k.opclass[prod], kind), ref27);
+    }
+  }
+}
+
+}  // namespace leo

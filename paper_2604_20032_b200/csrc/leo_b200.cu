@@ -1,0 +1,366 @@
+// abi.cu — extern "C" entry points of libleo_b200.so (include/leo_b200.h).
+//
+// Each entry point enqueues its kernels on the caller's stream; scratch comes
+// from the stream-ordered allocator (cudaMallocAsync) and is released on the
+// same stream.  No host synchronisation happens inside the pipeline: every
+// data-dependent size lives in device memory and the kernels read it there.
+#include <algorithm>
+#include <cstdio>
+#include <cstring>
+
+#include "prims.cuh"
+#include "graph.cu"
+#include "sync.cu"
+#include "prune.cu"
+#include "blame.cu"
+
+
+using namespace leo;
+
+namespace {
+
+int g_num_sms = 0;
+int num_sms() {
+  if (!g_num_sms) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&g_num_sms, cudaDevAttrMultiProcessorCount, dev);
+    if (g_num_sms <= 0) g_num_sms = 148;
+  }
+  return g_num_sms;
+}
+
+// Stream-ordered bump arena: one cudaMallocAsync per entry point.
+struct Arena {
+  cudaStream_t st;
+  char* base = nullptr;
+  size_t cap = 0, off = 0;
+  struct Req { void** dst; size_t bytes; };
+  Req reqs[96];
+  int nreq = 0;
+  template <typename T> void want(T** dst, int64_t n) {
+    reqs[nreq++] = Req{(void**)dst, (size_t)std::max<int64_t>(n, 1) * sizeof(T)};
+  }
+  cudaError_t commit() {
+    size_t total = 0;
+    for (int i = 0; i < nreq; i++) total += (reqs[i].bytes + 255) & ~(size_t)255;
+    cudaError_t e = cudaMallocAsync((void**)&base, total, st);
+    if (e != cudaSuccess) return e;
+    cap = total;
+    for (int i = 0; i < nreq; i++) {
+      *reqs[i].dst = base + off;
+      off += (reqs[i].bytes + 255) & ~(size_t)255;
+    }
+    return cudaSuccess;
+  }
+  void release() { if (base) cudaFreeAsync(base, st); base = nullptr; }
+};
+
+inline int64_t pick(int64_t hint, int64_t dflt) { return hint > 0 ? hint : dflt; }
+
+int check_kernel(const LeoKernel* k) {
+  if (!k || k->n_instr < 0 || k->n_blocks < 0 || k->n_units < 0) return -1;
+  if (k->n_instr >= (1 << 30) || k->n_units > (1 << 24)) return -2;
+  return 0;
+}
+
+// ---------------------------------------------------------------------------
+// build_graph
+int build_graph_impl(const LeoKernel* kk, const LeoCaps* caps, LeoEdges* out, LeoDiags* diags,
+                     uint32_t* status, cudaStream_t st) {
+  KView k = make_kview(kk);
+  const int N = k.N, B = k.B, U = k.U;
+  const int64_t NU = kk->n_use_units, ND = kk->n_def_units;
+  const int64_t cap_qres = pick(caps ? caps->query_results : 0, 4 * NU + 1024);
+  const int64_t cap_cand = pick(caps ? caps->candidates : 0, 6 * NU + 1024);
+  const int64_t cap_sync = pick(caps ? caps->sync_keys : 0, 2 * (int64_t)N + 1024);
+  const int64_t cap_slow = pick(caps ? caps->slow_items : 0, N / 4 + 1024);
+  const int SM = num_sms();
+
+  // per-warp unit tables in shared memory when they fit
+  int wpc = 8;
+  while (wpc > 1 && (size_t)wpc * 2 * U * 4 > 96 * 1024) wpc >>= 1;
+  const bool smem_tab = (size_t)2 * U * 4 <= 96 * 1024;
+  const int walk_ctas = std::min<int>((B + wpc - 1) / wpc, SM * 8);
+  const int walk_warps = std::max(1, walk_ctas) * wpc;
+
+  const int RW = 128;        // slow reach workers
+  const int SW = 64;         // slow sync workers
+  Arena ar{st};
+  int32_t *ucnt, *dcnt, *use_ptr, *def_ptr, *ev_res, *q_block, *q_unit, *q_list, *q_off, *q_len, *qres;
+  int32_t *ctr, *slow_list, *slow2, *cand_cnt, *cand_off, *uniq, *eoff, *bdef_len, *scan_tmp, *gtab = nullptr;
+  int32_t *pcnt, *poff, *pcur, *puniq, *puoff, *reach_scr;
+  uint64_t *bdef, *cand, *skeys, *ssorted;
+  char* sync_scr;
+  ar.want(&ucnt, N); ar.want(&dcnt, N); ar.want(&use_ptr, N + 1); ar.want(&def_ptr, N + 1);
+  ar.want(&ev_res, NU); ar.want(&q_block, NU); ar.want(&q_unit, NU); ar.want(&q_list, NU);
+  ar.want(&q_off, NU); ar.want(&q_len, NU); ar.want(&qres, cap_qres); ar.want(&ctr, 16);
+  ar.want(&slow_list, cap_slow); ar.want(&slow2, cap_slow); ar.want(&cand_cnt, N); ar.want(&cand_off, N + 1);
+  ar.want(&uniq, N); ar.want(&eoff, N + 1); ar.want(&bdef_len, B); ar.want(&bdef, ND);
+  ar.want(&cand, cap_cand); ar.want(&skeys, cap_sync); ar.want(&ssorted, cap_sync);
+  ar.want(&pcnt, N); ar.want(&poff, N + 1); ar.want(&pcur, N); ar.want(&puniq, N); ar.want(&puoff, N + 1);
+  ar.want(&scan_tmp, scan_scratch_ints(std::max<int64_t>(std::max<int64_t>(N, cap_cand), 1)) + 64);
+  ar.want(&reach_scr, (int64_t)RW * 3 * (B + 1));
+  ar.want(&sync_scr, (int64_t)SW * sync_slow_bytes_per_worker(B));
+  if (!smem_tab) ar.want(&gtab, (int64_t)walk_warps * 2 * U);
+  LEO_CUDA_CHECK(ar.commit());
+  // counters: 0 q_count, 1 qres_count, 2 reach slow, 3 sync keys, 4 sync slow, 5 n_regular, 6 n_sync
+  cudaMemsetAsync(ctr, 0, 16 * sizeof(int32_t), st);
+  cudaMemsetAsync(reach_scr, 0, (size_t)RW * 3 * (B + 1) * sizeof(int32_t), st);
+  cudaMemsetAsync(pcnt, 0, (size_t)std::max(N, 1) * 4, st);
+  cudaMemsetAsync(pcur, 0, (size_t)std::max(N, 1) * 4, st);
+
+  const int T = 256;
+  k_unit_counts<<<grid_for(N, T), T, 0, st>>>(k, ucnt, dcnt);
+  scan_exclusive(ucnt, use_ptr, nullptr, N, scan_tmp, nullptr, st);
+  scan_exclusive(dcnt, def_ptr, nullptr, N, scan_tmp, nullptr, st);
+
+  WalkArgs wa{use_ptr, def_ptr, ev_res, q_block, q_unit, q_list, &ctr[0], bdef, bdef_len, gtab};
+  size_t smem = smem_tab ? (size_t)wpc * 2 * U * 4 : 0;
+  if (smem > 48 * 1024) cudaFuncSetAttribute(k_block_walk, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  if (B > 0) k_block_walk<<<std::max(1, walk_ctas), wpc * 32, smem, st>>>(k, wa, wpc);
+
+  ReachArgs ra{def_ptr, bdef, bdef_len, q_block, q_unit, q_off, q_len, qres, cap_qres, &ctr[1],
+               slow_list, &ctr[2], cap_slow, status};
+  k_reach_fast<<<grid_for(NU, 128), 128, 0, st>>>(k, ra, q_list, &ctr[0]);
+  k_reach_slow<<<(RW + 63) / 64, 64, 0, st>>>(k, ra, reach_scr, RW);
+
+  LinkArgs la{use_ptr, ev_res, q_off, q_len, qres, cand_cnt, cand_off, cand, cap_cand, *diags, status};
+  k_link<0><<<grid_for(N, T), T, 0, st>>>(k, la);
+  scan_exclusive(cand_cnt, cand_off, nullptr, N, scan_tmp, nullptr, st);
+  k_link<1><<<grid_for(N, T), T, 0, st>>>(k, la);
+  segsort_unique_u64<<<grid_for(N, 128), 128, 0, st>>>(cand, cand_off, cand_cnt, nullptr, N, uniq);
+  scan_exclusive(uniq, eoff, nullptr, N, scan_tmp, &ctr[5], st);
+  k_link_emit<<<grid_for(N, T), T, 0, st>>>(k, cand_off, cand, uniq, eoff, *out, status);
+
+  SyncArgs sa{skeys, cap_sync, &ctr[3], slow2, &ctr[4], cap_slow, *diags, status};
+  k_sync<false><<<grid_for(N, 128), 128, 0, st>>>(k, sa, nullptr, 0);
+  k_sync<true><<<1, SW, 0, st>>>(k, sa, (int32_t*)sync_scr, SW);
+  k_key_hist<<<grid_for(cap_sync, T), T, 0, st>>>(skeys, &ctr[3], cap_sync, pcnt);
+  scan_exclusive(pcnt, poff, nullptr, N, scan_tmp, nullptr, st);
+  k_key_scatter<<<grid_for(cap_sync, T), T, 0, st>>>(skeys, &ctr[3], cap_sync, poff, pcur, ssorted);
+  segsort_unique_u64<<<grid_for(N, 128), 128, 0, st>>>(ssorted, poff, pcnt, nullptr, N, puniq);
+  scan_exclusive(puniq, puoff, nullptr, N, scan_tmp, &ctr[6], st);
+  const int kind = k.dialect == LEO_AMD ? LEO_EK_MEM_WAITCNT : k.dialect == LEO_NVIDIA ? LEO_EK_MEM_BARRIER : LEO_EK_MEM_SWSB;
+  k_sync_emit<<<grid_for(N, T), T, 0, st>>>(N, kind, ssorted, poff, puniq, puoff, &ctr[5], *out, status);
+  k_edge_totals<<<1, 1, 0, st>>>(&ctr[5], &ctr[6], *out, status);
+  ar.release();
+  LEO_CUDA_CHECK(cudaGetLastError());
+  return 0;
+}
+
+// ---------------------------------------------------------------------------
+// run_pruning
+int prune_impl(const LeoKernel* kk, const LeoProfile* pp, const LeoConfig* cfg, const LeoEdges* in,
+               LeoEdges* out, LeoPaths* paths, LeoDiags* diags, const LeoCaps* caps, uint32_t* status,
+               cudaStream_t st) {
+  KView k = make_kview(kk);
+  PView p = make_pview(pp);
+  const int64_t cap_in = in->capacity;
+  const int64_t cap_slow = pick(caps ? caps->slow_items : 0, cap_in / 8 + 1024);
+  const int PW = 32;
+  const size_t pslow = prune_slow_bytes(cfg->max_depth, cfg->max_paths);
+  Arena ar{st};
+  int32_t *keep, *npaths, *pfirst, *pos, *slow_list, *ctr, *scan_tmp, *n_reg_in;
+  double* dist;
+  char* slow_scr;
+  ar.want(&keep, cap_in); ar.want(&npaths, cap_in); ar.want(&pfirst, cap_in); ar.want(&dist, cap_in);
+  ar.want(&pos, cap_in + 1); ar.want(&slow_list, cap_slow); ar.want(&ctr, 4);
+  ar.want(&scan_tmp, scan_scratch_ints(cap_in) + 64); ar.want(&slow_scr, (int64_t)PW * pslow);
+  (void)n_reg_in;
+  LEO_CUDA_CHECK(ar.commit());
+  cudaMemsetAsync(ctr, 0, 4 * sizeof(int32_t), st);
+  cudaMemsetAsync(paths->count, 0, sizeof(int32_t), st);
+  PruneArgs a{*cfg, in->prod, in->cons, in->meta, in->count, (int32_t)cap_in, keep, npaths, pfirst, dist,
+              *paths, slow_list, &ctr[0], cap_slow, *diags, status};
+  k_prune_edges<<<grid_for(cap_in, 128, num_sms() * 16), 128, 0, st>>>(k, p, a);
+  k_prune_slow<<<1, PW, 0, st>>>(k, p, a, slow_scr, PW);
+  scan_exclusive(keep, pos, in->count, cap_in, scan_tmp, nullptr, st);
+  k_compact<<<grid_for(cap_in, 256), 256, 0, st>>>(a, pos, in->n_regular, *out, status);
+  ar.release();
+  LEO_CUDA_CHECK(cudaGetLastError());
+  return 0;
+}
+
+// ---------------------------------------------------------------------------
+// incoming CSR of an edge list (regular part consumer-sorted, sync part not)
+struct IncomingBufs {
+  int32_t *rbeg, *rend, *scnt, *soff, *scur, *tmp, *uniq;
+  uint64_t* sidx;
+};
+void want_incoming(Arena& ar, IncomingBufs& b, int N, int64_t cap) {
+  ar.want(&b.rbeg, N); ar.want(&b.rend, N); ar.want(&b.scnt, N); ar.want(&b.soff, N + 1);
+  ar.want(&b.scur, N); ar.want(&b.sidx, cap); ar.want(&b.tmp, scan_scratch_ints(std::max(N, 1)) + 64);
+  ar.want(&b.uniq, N);
+}
+Incoming build_incoming(IncomingBufs& b, int N, const LeoEdges* e, bool with_sync, cudaStream_t st) {
+  const size_t nb = (size_t)std::max(N, 1) * 4;
+  cudaMemsetAsync(b.rbeg, 0, nb, st);
+  cudaMemsetAsync(b.rend, 0, nb, st);
+  cudaMemsetAsync(b.scnt, 0, nb, st);
+  cudaMemsetAsync(b.scur, 0, nb, st);
+  k_seg_bounds<<<grid_for(e->capacity, 256), 256, 0, st>>>(e->cons, e->n_regular, b.rbeg, b.rend);
+  if (with_sync) {
+    k_sync_hist<<<grid_for(e->capacity, 256), 256, 0, st>>>(e->cons, e->n_regular, e->count, b.scnt);
+    scan_exclusive(b.scnt, b.soff, nullptr, N, b.tmp, nullptr, st);
+    k_sync_fill<<<grid_for(e->capacity, 256), 256, 0, st>>>(e->cons, e->n_regular, e->count, b.soff, b.scur, b.sidx);
+    segsort_unique_u64<<<grid_for(N, 128), 128, 0, st>>>(b.sidx, b.soff, b.scnt, nullptr, N, b.uniq);
+  } else {
+    cudaMemsetAsync(b.soff, 0, (size_t)(N + 1) * 4, st);
+  }
+  return Incoming{b.rbeg, b.rend, b.soff, b.sidx};
+}
+
+int slice_impl(const LeoKernel* kk, const LeoProfile* pp, const LeoEdges* pruned, const Incoming& inc,
+               uint32_t* bitmap, int32_t* level, cudaStream_t st) {
+  const int N = kk->n_instr;
+  Arena ar{st};
+  int32_t *fa, *fb, *counts;
+  ar.want(&fa, N); ar.want(&fb, N); ar.want(&counts, 4);
+  LEO_CUDA_CHECK(ar.commit());
+  SliceArgs a{pp->lat, pruned->prod, inc, level, fa, fb, counts, bitmap};
+  int dev = 0, per_sm = 0;
+  cudaGetDevice(&dev);
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_slice, 256, 0);
+  int grid = std::max(1, std::min(per_sm, 4)) * num_sms();
+  int n = N;
+  void* args[] = {&n, &a};
+  LEO_CUDA_CHECK(cudaLaunchCooperativeKernel((void*)k_slice, grid, 256, args, 0, st));
+  ar.release();
+  return 0;
+}
+
+int blame_impl(const LeoKernel* kk, const LeoProfile* pp, const LeoEdges* pruned, const LeoPaths* paths,
+               const LeoEdges* base, const Incoming& inc, const int32_t* line_id, int32_t n_lines,
+               LeoBlame* out, double* line_blame, double* line_stall, const LeoCaps* caps,
+               uint32_t* status, cudaStream_t st) {
+  KView k = make_kview(kk);
+  const int N = k.N;
+  PView p = make_pview(pp);
+  const int64_t cap_slow = pick(caps ? caps->slow_items : 0, N / 4 + 1024);
+  const int BW = 64;
+  Arena ar{st};
+  IncomingBufs bb;
+  int32_t *ecount, *self_sub, *eoff, *slow_list, *ctr, *scan_tmp, *slow_scr;
+  double *jtotal, *jnsum;
+  want_incoming(ar, bb, N, 1);
+  ar.want(&ecount, N); ar.want(&self_sub, N); ar.want(&eoff, N + 1); ar.want(&slow_list, cap_slow);
+  ar.want(&ctr, 4); ar.want(&scan_tmp, scan_scratch_ints(std::max(N, 1)) + 64);
+  ar.want(&slow_scr, (int64_t)BW * 2 * (N + 1)); ar.want(&jtotal, N); ar.want(&jnsum, N);
+  LEO_CUDA_CHECK(ar.commit());
+  cudaMemsetAsync(ctr, 0, 16, st);
+  Incoming binc = build_incoming(bb, N, base, false, st);   // RAW edges only
+  BlameArgs a{p, pruned->prod, pruned->meta, paths->dist, inc, binc.rbeg, binc.rend, base->prod, base->meta,
+              ecount, self_sub, jtotal, jnsum, eoff, *out, slow_list, &ctr[0], cap_slow, status};
+  k_blame<0><<<grid_for(N, 128), 128, 0, st>>>(k, a);
+  k_selfblame_slow<<<1, BW, 0, st>>>(k, a, slow_scr, BW);
+  scan_exclusive(ecount, eoff, nullptr, N, scan_tmp, nullptr, st);
+  k_blame<1><<<grid_for(N, 128), 128, 0, st>>>(k, a);
+  k_blame_count<<<1, 1, 0, st>>>(eoff, N, *out);
+  if (line_id && line_blame && line_stall && n_lines > 0) {
+    cudaMemsetAsync(line_blame, 0, (size_t)n_lines * 8, st);
+    cudaMemsetAsync(line_stall, 0, (size_t)n_lines * 8, st);
+    k_lines<<<grid_for(std::max<int64_t>(out->capacity, N), 256), 256, 0, st>>>(k, p, pruned->prod, *out,
+                                                                               line_id, line_blame, line_stall);
+  }
+  ar.release();
+  LEO_CUDA_CHECK(cudaGetLastError());
+  return 0;
+}
+
+}  // namespace
+
+
+extern "C" {
+
+int leo_abi_version(void) { return LEO_ABI_VERSION; }
+
+int leo_bin_samples(const LeoSamples* s, int32_t n_instr, int32_t* lat, int32_t* cls_cnt, void* stream) {
+  if (!s || n_instr < 0) return -1;
+  cudaStream_t st = (cudaStream_t)stream;
+  cudaMemsetAsync(cls_cnt, 0, (size_t)std::max(n_instr, 1) * 32, st);
+  uint32_t* status = nullptr;
+  LEO_CUDA_CHECK(cudaMallocAsync((void**)&status, 4, st));
+  cudaMemsetAsync(status, 0, 4, st);
+  if (s->n_samples > 0)
+    k_bin_samples<<<grid_for(s->n_samples / 4 + 1, 256, num_sms() * 8), 256, 0, st>>>(
+        s->n_samples, s->pc, s->cat, s->cat_to_cs, n_instr, cls_cnt, status);
+  k_bin_finalize<<<grid_for(n_instr, 256), 256, 0, st>>>(n_instr, cls_cnt, lat);
+  cudaFreeAsync(status, st);
+  LEO_CUDA_CHECK(cudaGetLastError());
+  return 0;
+}
+
+int leo_build_graph(const LeoKernel* k, const LeoCaps* caps, LeoEdges* out, LeoDiags* diags,
+                    uint32_t* status, void* stream) {
+  if (int e = check_kernel(k)) return e;
+  return build_graph_impl(k, caps, out, diags, status, (cudaStream_t)stream);
+}
+
+int leo_prune(const LeoKernel* k, const LeoProfile* p, const LeoConfig* cfg, const LeoEdges* in,
+              LeoEdges* out, LeoPaths* paths, LeoDiags* diags, uint32_t* status, void* stream) {
+  if (int e = check_kernel(k)) return e;
+  if (!cfg || cfg->max_paths < 0 || cfg->max_depth < 0) return -3;
+  return prune_impl(k, p, cfg, in, out, paths, diags, nullptr, status, (cudaStream_t)stream);
+}
+
+int leo_slice(const LeoKernel* k, const LeoProfile* p, const LeoEdges* pruned, uint32_t* bitmap,
+              int32_t* level, void* stream) {
+  if (int e = check_kernel(k)) return e;
+  cudaStream_t st = (cudaStream_t)stream;
+  Arena ar{st};
+  IncomingBufs ib;
+  want_incoming(ar, ib, k->n_instr, pruned->capacity);
+  LEO_CUDA_CHECK(ar.commit());
+  Incoming inc = build_incoming(ib, k->n_instr, pruned, true, st);
+  int r = slice_impl(k, p, pruned, inc, bitmap, level, st);
+  ar.release();
+  return r;
+}
+
+int leo_blame(const LeoKernel* k, const LeoProfile* p, const LeoEdges* pruned, const LeoPaths* paths,
+              const LeoEdges* base, const int32_t* line_id, int32_t n_lines, LeoBlame* out,
+              double* line_blame, double* line_stall, uint32_t* status, void* stream) {
+  if (int e = check_kernel(k)) return e;
+  cudaStream_t st = (cudaStream_t)stream;
+  Arena ar{st};
+  IncomingBufs ib;
+  want_incoming(ar, ib, k->n_instr, pruned->capacity);
+  LEO_CUDA_CHECK(ar.commit());
+  Incoming inc = build_incoming(ib, k->n_instr, pruned, true, st);
+  int r = blame_impl(k, p, pruned, paths, base, inc, line_id, n_lines, out, line_blame, line_stall, nullptr,
+                     status, st);
+  ar.release();
+  return r;
+}
+
+int leo_analyze(const LeoKernel* k, const LeoProfile* p, const LeoSamples* samples, const LeoConfig* cfg,
+                const LeoCaps* caps, LeoEdges* base, LeoEdges* pruned, LeoPaths* paths, LeoDiags* diags,
+                LeoBlame* blame, uint32_t* slice_bitmap, int32_t* slice_level, const int32_t* line_id,
+                int32_t n_lines, double* line_blame, double* line_stall, uint32_t* status, void* stream) {
+  if (int e = check_kernel(k)) return e;
+  if (!cfg) return -3;
+  cudaStream_t st = (cudaStream_t)stream;
+  if (samples) {
+    int r = leo_bin_samples(samples, k->n_instr, (int32_t*)p->lat, (int32_t*)p->cls_cnt, stream);
+    if (r) return r;
+  }
+  int r = build_graph_impl(k, caps, base, diags, status, st);
+  if (r) return r;
+  r = prune_impl(k, p, cfg, base, pruned, paths, diags, caps, status, st);
+  if (r) return r;
+  Arena ar{st};
+  IncomingBufs ib;
+  want_incoming(ar, ib, k->n_instr, pruned->capacity);
+  LEO_CUDA_CHECK(ar.commit());
+  Incoming inc = build_incoming(ib, k->n_instr, pruned, true, st);
+  if (slice_level && slice_bitmap) {
+    r = slice_impl(k, p, pruned, inc, slice_bitmap, slice_level, st);
+    if (r) { ar.release(); return r; }
+  }
+  r = blame_impl(k, p, pruned, paths, base, inc, line_id, n_lines, blame, line_blame, line_stall, caps, status, st);
+  ar.release();
+  return r;
+}
+
+}  // extern "C"

@@ -1,0 +1,167 @@
+// prims.cuh — scan / segmented sort primitives with device-resident counts.
+//
+// Every variable-size stage of the pipeline writes a device counter; the
+// kernels below take the element count from device memory (`n_dev`) and an
+// upper bound (`cap`) for launch sizing, so the whole pipeline runs without a
+// host round trip (and can be captured in a CUDA graph).
+#pragma once
+#include "common.cuh"
+
+namespace leo {
+
+constexpr int kScanThreads = 512;
+constexpr int kScanItems = 8;
+constexpr int kScanTile = kScanThreads * kScanItems;
+
+LEO_DEV int warp_incl_scan(int v) {
+  const int lane = threadIdx.x & 31;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    int t = __shfl_up_sync(0xffffffffu, v, o);
+    if (lane >= o) v += t;
+  }
+  return v;
+}
+
+// block-wide exclusive scan of one value per thread; returns exclusive prefix,
+// writes the block total to *total.
+LEO_DEV int block_excl_scan(int v, int* smem_warp, int* total) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
+  int inc = warp_incl_scan(v);
+  if (lane == 31) smem_warp[warp] = inc;
+  __syncthreads();
+  if (warp == 0) {
+    int w = lane < nw ? smem_warp[lane] : 0;
+    int wi = warp_incl_scan(w);
+    if (lane < nw) smem_warp[lane] = wi - w;
+    if (lane == nw - 1) smem_warp[32] = wi;
+  }
+  __syncthreads();
+  int r = inc - v + smem_warp[warp];
+  *total = smem_warp[32];
+  __syncthreads();
+  return r;
+}
+
+__global__ void scan_tile_sums(const int32_t* __restrict__ in, const int32_t* n_dev, int64_t n_cap,
+                               int32_t* __restrict__ tile_sums) {
+  __shared__ int sw[33];
+  int64_t n = n_dev ? (int64_t)*n_dev : n_cap;
+  int64_t base = (int64_t)blockIdx.x * kScanTile;
+  int s = 0;
+  for (int k = 0; k < kScanItems; k++) {
+    int64_t i = base + (int64_t)k * kScanThreads + threadIdx.x;
+    if (i < n) s += in[i];
+  }
+  int total;
+  block_excl_scan(s, sw, &total);
+  if (threadIdx.x == 0) tile_sums[blockIdx.x] = total;
+}
+
+// single CTA: exclusive scan of the tile sums (in place); grand total -> *total_out
+__global__ void scan_tile_prefix(int32_t* tile_sums, int ntiles, int32_t* total_out) {
+  __shared__ int sw[33];
+  int carry = 0;
+  for (int base = 0; base < ntiles; base += blockDim.x) {
+    int i = base + threadIdx.x;
+    int v = i < ntiles ? tile_sums[i] : 0;
+    int tot;
+    int ex = block_excl_scan(v, sw, &tot);
+    if (i < ntiles) tile_sums[i] = ex + carry;
+    carry += tot;
+  }
+  if (threadIdx.x == 0 && total_out) *total_out = carry;
+}
+
+__global__ void scan_tile_apply(const int32_t* __restrict__ in, const int32_t* n_dev, int64_t n_cap,
+                                const int32_t* __restrict__ tile_sums, int32_t* __restrict__ out) {
+  __shared__ int sw[33];
+  int64_t n = n_dev ? (int64_t)*n_dev : n_cap;
+  int64_t base = (int64_t)blockIdx.x * kScanTile + (int64_t)threadIdx.x * kScanItems;
+  int v[kScanItems];
+  int s = 0;
+#pragma unroll
+  for (int k = 0; k < kScanItems; k++) {
+    int64_t i = base + k;
+    v[k] = i < n ? in[i] : 0;
+    s += v[k];
+  }
+  int total;
+  int ex = block_excl_scan(s, sw, &total) + tile_sums[blockIdx.x];
+#pragma unroll
+  for (int k = 0; k < kScanItems; k++) {
+    int64_t i = base + k;
+    if (i < n) out[i] = ex;
+    ex += v[k];
+  }
+  // out[n] = total (CSR end) written by the last tile owner
+  if (n_dev == nullptr || true) {
+    int64_t last_tile = n > 0 ? (n - 1) / kScanTile : 0;
+    if ((int64_t)blockIdx.x == last_tile && threadIdx.x == 0) out[n] = tile_sums[blockIdx.x] + total;
+  }
+}
+
+// exclusive scan of in[0..n) into out[0..n] (out[n] = total); n from n_dev if
+// given else n_cap.  scratch: >= tiles(n_cap) ints.  total_out optional.
+inline void scan_exclusive(const int32_t* in, int32_t* out, const int32_t* n_dev, int64_t n_cap,
+                           int32_t* scratch, int32_t* total_out, cudaStream_t st) {
+  int64_t ntiles = (n_cap + kScanTile - 1) / kScanTile;
+  if (ntiles < 1) ntiles = 1;
+  scan_tile_sums<<<(unsigned)ntiles, kScanThreads, 0, st>>>(in, n_dev, n_cap, scratch);
+  scan_tile_prefix<<<1, 1024, 0, st>>>(scratch, (int)ntiles, total_out);
+  scan_tile_apply<<<(unsigned)ntiles, kScanThreads, 0, st>>>(in, n_dev, n_cap, scratch, out);
+}
+inline int64_t scan_scratch_ints(int64_t n_cap) { return (n_cap + kScanTile - 1) / kScanTile + 1; }
+
+// ---- segmented sort + unique (thread per segment) --------------------------
+LEO_DEV void sort_small_u64(uint64_t* a, int n) {
+  for (int i = 1; i < n; i++) {
+    uint64_t x = a[i];
+    int j = i - 1;
+    while (j >= 0 && a[j] > x) { a[j + 1] = a[j]; j--; }
+    a[j + 1] = x;
+  }
+}
+LEO_DEV void shell_sort_u64(uint64_t* a, int n) {
+  int gap = 1;
+  while (gap < n / 3) gap = gap * 3 + 1;
+  for (; gap > 0; gap /= 3)
+    for (int i = gap; i < n; i++) {
+      uint64_t x = a[i];
+      int j = i;
+      while (j >= gap && a[j - gap] > x) { a[j] = a[j - gap]; j -= gap; }
+      a[j] = x;
+    }
+}
+
+// Sort keys[begin[s] .. begin[s]+len[s]) ascending, drop duplicates in place,
+// write the unique count to uniq[s].
+__global__ void segsort_unique_u64(uint64_t* __restrict__ keys, const int32_t* __restrict__ begin,
+                                   const int32_t* __restrict__ len, const int32_t* nseg_dev, int nseg_cap,
+                                   int32_t* __restrict__ uniq) {
+  int nseg = nseg_dev ? *nseg_dev : nseg_cap;
+  for (int s = blockIdx.x * blockDim.x + threadIdx.x; s < nseg; s += gridDim.x * blockDim.x) {
+    int n = len[s];
+    uint64_t* a = keys + begin[s];
+    if (n <= 1) { uniq[s] = n; continue; }
+    if (n <= 24) {
+      uint64_t r[24];
+      for (int i = 0; i < n; i++) r[i] = a[i];
+      sort_small_u64(r, n);
+      int u = 0;
+      for (int i = 0; i < n; i++)
+        if (i == 0 || r[i] != r[i - 1]) a[u++] = r[i];
+      uniq[s] = u;
+    } else {
+      shell_sort_u64(a, n);
+      int u = 0;
+      for (int i = 0; i < n; i++) {
+        uint64_t x = a[i];
+        if (i == 0 || x != a[u - 1]) a[u++] = x;
+      }
+      uniq[s] = u;
+    }
+  }
+}
+
+}  // namespace leo

@@ -1,0 +1,262 @@
+// prune.cu — the four pruning stages (analysis.py:130-314) as one per-edge map
+// plus a stable stream compaction.
+//
+// run_pruning applies stages 1 -> 2 -> 3 -> 4 to the whole edge list, but every
+// stage decides each edge from that edge alone (plus instruction and profile
+// data), so  keep(e) = s1(e) & s2(e) & s3(e) & s4(e)  with stage-3 run only
+// on edges that survive 1 and 2 (its diagnostics are emitted for exactly those
+// edges, in edge order after the host sorts them by edge index).
+//
+//   k_prune_edges   thread/edge: stage-1 opcode rule, stage-2 barrier rule,
+//                   stage-3 exact LIFO path DFS (_enumerate_paths :210-253,
+//                   budget 65,536 pops, max_paths, max_depth, layout back edges
+//                   at most once per path), stage-4 exec-count rule; surviving
+//                   paths reserved in the path pool, sorted (len, accum);
+//                   _edge_distance (:371-376) precomputed for blame.
+//   k_prune_slow    same DFS on global scratch for edges whose stack / back-
+//                   edge arena / path buffer overflowed the register budget.
+//   scan + k_compact  order-preserving compaction.
+#include "prims.cuh"
+
+namespace leo {
+
+struct PView {
+  int64_t period;
+  const int32_t* __restrict__ lat;
+  const int32_t* __restrict__ cls_cnt;
+  const int64_t* __restrict__ exec_cnt;
+  const int32_t* __restrict__ total;
+  const double* __restrict__ eff;
+  const uint8_t* __restrict__ sampled;
+};
+inline PView make_pview(const LeoProfile* p) {
+  PView v;
+  v.period = p->period; v.lat = p->lat; v.cls_cnt = p->cls_cnt; v.exec_cnt = p->exec_cnt;
+  v.total = p->total; v.eff = p->eff; v.sampled = p->sampled;
+  return v;
+}
+
+LEO_DEV bool only_class(const PView& p, int j, int cls) {   // _only_class :134-140
+  if (p.lat[j] == 0) return false;
+  const int4* row = reinterpret_cast<const int4*>(p.cls_cnt + (size_t)j * 8);
+  int4 a = row[0], b = row[1];
+  int v[8] = {a.x, a.y, a.z, a.w, b.x, b.y, b.z, b.w};
+#pragma unroll
+  for (int c = 0; c < 8; c++) if (c != cls && v[c] > 0) return false;
+  return true;
+}
+
+LEO_DEV double issue_weight(const KView& k, int i) {   // _issue_weights :188-199
+  if (k.dialect == LEO_NVIDIA && k.sync_kind[i] == LEO_SYNC_BARRIER && k.sync_b[i] != LEO_NONE_U32)
+    return (double)k.sync_b[i];
+  return 1.0;
+}
+
+struct DfsEnt { int32_t node, len, back, pad; double acc; };
+struct BackNode { int32_t nb, cb, parent; };
+
+enum { DFS_OK = 0, DFS_TRUNC = 1, DFS_OVERFLOW = 2 };
+
+// Exact emulation of _enumerate_paths.  Returns DFS_OK / DFS_TRUNC, or
+// DFS_OVERFLOW when a caller buffer was too small (caller re-runs elsewhere).
+LEO_DEV int enumerate_paths(const KView& k, int producer, int consumer, double thr, int max_paths,
+                            int max_depth, DfsEnt* stk, int scap, BackNode* arena, int acap,
+                            int32_t* vlen, double* vacc, int vcap, int* nvalid_out) {
+  int budget = 65536, truncated = 0, sp = 0, na = 0, nv = 0;
+  *nvalid_out = 0;
+  const double w0 = issue_weight(k, producer);
+  if (w0 > thr) return DFS_OK;
+  stk[sp++] = DfsEnt{producer, 1, -1, 0, w0};
+  while (sp > 0) {
+    DfsEnt e = stk[--sp];
+    if (budget <= 0 || nv >= max_paths) { truncated = 1; break; }
+    budget--;
+    const int nb = k.block_of[e.node];
+    int succ_n, s0 = -1, s1 = -1;
+    if (e.node < k.blk_last[nb]) { succ_n = 1; s0 = e.node + 1; }
+    else {
+      const int q0 = k.succ_ptr[nb];
+      succ_n = k.succ_ptr[nb + 1] - q0;
+      if (succ_n > 0) s0 = k.blk_first[k.succ[q0]];
+      if (succ_n > 1) s1 = k.blk_first[k.succ[q0 + 1]];
+      if (succ_n > 2) return DFS_OVERFLOW;
+    }
+    for (int t = 0; t < succ_n; t++) {
+      const int nxt = t == 0 ? s0 : s1;
+      if (nxt == consumer) {
+        if (nv == vcap) return DFS_OVERFLOW;
+        vlen[nv] = e.len; vacc[nv] = e.acc; nv++;
+        if (nv >= max_paths) truncated = 1;
+        continue;
+      }
+      const int cb = k.block_of[nxt];
+      int nback = e.back;
+      if (nb != cb && k.blk_first[cb] <= k.blk_first[nb]) {
+        bool hit = false;
+        for (int x = e.back; x >= 0; x = arena[x].parent)
+          if (arena[x].nb == nb && arena[x].cb == cb) { hit = true; break; }
+        if (hit) continue;
+        if (na == acap) return DFS_OVERFLOW;
+        arena[na] = BackNode{nb, cb, e.back};
+        nback = na++;
+      }
+      const int nlen = e.len + 1;
+      const double nacc = __dadd_rn(e.acc, issue_weight(k, nxt));
+      if (nacc > thr) continue;
+      if (nlen >= max_depth) { truncated = 1; continue; }
+      if (sp == scap) return DFS_OVERFLOW;
+      stk[sp++] = DfsEnt{nxt, nlen, nback, 0, nacc};
+    }
+  }
+  // valid.sort(key=(length, accum))
+  for (int i = 1; i < nv; i++) {
+    int l = vlen[i]; double a = vacc[i];
+    int j = i - 1;
+    while (j >= 0 && (vlen[j] > l || (vlen[j] == l && vacc[j] > a))) { vlen[j + 1] = vlen[j]; vacc[j + 1] = vacc[j]; j--; }
+    vlen[j + 1] = l; vacc[j + 1] = a;
+  }
+  *nvalid_out = nv;
+  return truncated ? DFS_TRUNC : DFS_OK;
+}
+
+struct PruneArgs {
+  LeoConfig cfg;
+  const int32_t* prod;
+  const int32_t* cons;
+  const uint32_t* meta;
+  const int32_t* n_in;       // device count of input edges
+  int32_t cap_in;
+  int32_t* keep;             // [cap_in] 0/1
+  int32_t* npaths;           // [cap_in]
+  int32_t* pfirst;           // [cap_in]
+  double* dist;              // [cap_in]
+  LeoPaths paths;            // pool (len / accum / count)
+  int32_t* slow_list;
+  int32_t* slow_count;
+  int64_t slow_cap;
+  LeoDiags diags;
+  uint32_t* status;
+};
+
+// stage 1/2/4 predicates + stage-3 DFS for edge e.  Returns false when the
+// DFS needs the slow path.
+LEO_DEV bool prune_one(const KView& k, const PView& p, const PruneArgs& a, int e, DfsEnt* stk, int scap,
+                       BackNode* arena, int acap, int32_t* vlen, double* vacc, int vcap) {
+  const uint32_t m = a.meta[e];
+  const int kind = (m >> 27) & 7;
+  const int pr = a.prod[e], cn = a.cons[e];
+  int keep = 1, nv = 0;
+  const uint32_t mask = a.cfg.stage_mask;
+  double dist;
+  {
+    int d = cn - pr; if (d < 0) d = -d; if (d < 1) d = 1;
+    dist = (double)d;
+  }
+  if (kind < LEO_EK_MEM_WAITCNT) {                       // sync edges are exempt
+    const uint32_t poc = k.opclass[pr];
+    if ((mask & 1) && ((only_class(p, cn, LEO_CS_MEMORY_DEP) && (kCompute & BIT(poc))) ||
+                       (only_class(p, cn, LEO_CS_EXECUTION_DEP) && poc == LEO_OC_GLOBAL_LOAD)))
+      keep = 0;                                          // prune_opcode :143-162
+    if (keep && (mask & 2) && k.dialect == LEO_NVIDIA) {   // prune_barrier :165-185
+      uint32_t sets = 0, waits = 0;
+      if (k.sync_kind[pr] == LEO_SYNC_BARRIER) sets = (k.sync_a[pr] | (k.sync_a[pr] >> 8)) & 0xFF;
+      if (sets) {
+        if (k.sync_kind[cn] == LEO_SYNC_BARRIER) waits = (k.sync_a[cn] >> 16) & 0xFF;
+        if (!(sets & waits)) keep = 0;
+      }
+    }
+    if (keep && (mask & 4)) {                            // prune_latency :256-286
+      int r = enumerate_paths(k, pr, cn, a.cfg.threshold[poc], a.cfg.max_paths, a.cfg.max_depth,
+                              stk, scap, arena, acap, vlen, vacc, vcap, &nv);
+      if (r == DFS_OVERFLOW) return false;
+      if (nv > 0) {
+        int off = atomicAdd(a.paths.count, nv);
+        if (off + nv > a.paths.capacity) {
+          atomicOr(a.status, (uint32_t)LEO_ST_PATH_OVERFLOW);
+          off = -1;
+        } else {
+          int64_t s = 0;
+          for (int x = 0; x < nv; x++) { a.paths.len[off + x] = vlen[x]; a.paths.accum[off + x] = vacc[x]; s += vlen[x]; }
+        }
+        int64_t s = 0;
+        for (int x = 0; x < nv; x++) s += vlen[x];
+        dist = __ddiv_rn((double)s, (double)nv);
+        a.pfirst[e] = off;
+        if (r == DFS_TRUNC) diag_push(a.diags, a.status, LEO_DIAG_PATH_CAPPED, pr, cn, 1, 0, e);
+      } else if (r == DFS_TRUNC) {
+        diag_push(a.diags, a.status, LEO_DIAG_PATH_CAPPED, pr, cn, 0, 0, e);
+      } else {
+        keep = 0;
+      }
+    }
+    if (keep && (mask & 8) && a.cfg.prune_exec && p.exec_cnt[pr] == 0) keep = 0;   // :289-299
+  }
+  a.keep[e] = keep;
+  a.npaths[e] = nv;
+  if (nv == 0) a.pfirst[e] = -1;
+  a.dist[e] = dist;
+  return true;
+}
+
+constexpr int kDfsStack = 20, kDfsArena = 24, kDfsPaths = 64;
+
+__global__ void __launch_bounds__(128) k_prune_edges(KView k, PView p, PruneArgs a) {
+  const int n = *a.n_in;
+  DfsEnt stk[kDfsStack];
+  BackNode arena[kDfsArena];
+  int32_t vlen[kDfsPaths];
+  double vacc[kDfsPaths];
+  const bool big_paths = a.cfg.max_paths > kDfsPaths;
+  for (int e = blockIdx.x * blockDim.x + threadIdx.x; e < n; e += gridDim.x * blockDim.x) {
+    bool ok = !big_paths && prune_one(k, p, a, e, stk, kDfsStack, arena, kDfsArena, vlen, vacc, kDfsPaths);
+    if (!ok) {
+      int s = atomicAdd(a.slow_count, 1);
+      if (s < a.slow_cap) a.slow_list[s] = e;
+      else atomicOr(a.status, (uint32_t)LEO_ST_SCRATCH_OVERFLOW);
+    }
+  }
+}
+
+__host__ __device__ inline size_t prune_slow_bytes(int max_depth, int max_paths) {
+  size_t scap = (size_t)max_depth + 8, acap = 2 * 65536 + 8, vcap = (size_t)max_paths + 2;
+  return ((scap * sizeof(DfsEnt) + acap * sizeof(BackNode) + vcap * 12) + 255) & ~(size_t)255;
+}
+
+__global__ void k_prune_slow(KView k, PView p, PruneArgs a, char* scratch, int nworkers) {
+  const int ns = (int)min((int64_t)*a.slow_count, a.slow_cap);
+  const int w = blockIdx.x * blockDim.x + threadIdx.x;
+  if (w >= nworkers) return;
+  const int scap = a.cfg.max_depth + 8, acap = 2 * 65536 + 8, vcap = a.cfg.max_paths + 2;
+  char* base = scratch + (size_t)w * prune_slow_bytes(a.cfg.max_depth, a.cfg.max_paths);
+  DfsEnt* stk = (DfsEnt*)base;
+  BackNode* arena = (BackNode*)(stk + scap);
+  double* vacc = (double*)(((uintptr_t)(arena + acap) + 7) & ~(uintptr_t)7);
+  int32_t* vlen = (int32_t*)(vacc + vcap);
+  for (int t = w; t < ns; t += nworkers) {
+    int e = a.slow_list[t];
+    if (!prune_one(k, p, a, e, stk, scap, arena, acap, vlen, vacc, vcap))
+      atomicOr(a.status, (uint32_t)LEO_ST_BAD_INPUT);   // > 2 successors: malformed CFG
+  }
+}
+
+__global__ void k_compact(PruneArgs a, const int32_t* __restrict__ pos, const int32_t* n_reg_in,
+                          LeoEdges out, uint32_t* status) {
+  const int n = *a.n_in;
+  for (int e = blockIdx.x * blockDim.x + threadIdx.x; e < n; e += gridDim.x * blockDim.x) {
+    if (!a.keep[e]) continue;
+    const int o = pos[e];
+    if (o >= out.capacity) { atomicOr(status, (uint32_t)LEO_ST_EDGE_OVERFLOW); continue; }
+    out.prod[o] = a.prod[e];
+    out.cons[o] = a.cons[e];
+    out.meta[o] = a.meta[e];
+    a.paths.first[o] = a.pfirst[e];
+    a.paths.npaths[o] = a.npaths[e];
+    a.paths.dist[o] = a.dist[e];
+  }
+  if (blockIdx.x == 0 && threadIdx.x == 0) {
+    *out.count = pos[n];
+    *out.n_regular = pos[*n_reg_in];
+  }
+}
+
+}  // namespace leo

@@ -1,0 +1,254 @@
+"""Device-resident SoA buffers and the stream-ordered pipeline driver.
+
+PyTorch provides device memory and the stream; all compute is in
+libleo_b200.so.  One `Analyzer` owns the output buffers (sized by capacity,
+grown on overflow) so repeated runs reuse memory, as a serving process would.
+"""
+
+from __future__ import annotations
+
+import ctypes as C
+from dataclasses import dataclass
+
+import numpy as np
+import torch
+
+from . import abi
+from . import enums as E
+from ._lib import check, lib
+
+K_ARRAYS = ("opclass", "block_of", "opnd_ptr", "opnd", "sync_kind", "sync_a", "sync_b",
+            "blk_first", "blk_last", "succ_ptr", "succ", "pred_ptr", "pred")
+_TORCH_DT = {np.dtype(np.uint8): torch.uint8, np.dtype(np.int32): torch.int32,
+             np.dtype(np.uint32): torch.int32, np.dtype(np.int64): torch.int64,
+             np.dtype(np.float64): torch.float64}
+
+
+def to_device(a: np.ndarray, device, pin: bool = False) -> torch.Tensor:
+    a = np.ascontiguousarray(a)
+    if a.dtype == np.uint32:
+        a = a.view(np.int32)
+    if a.size == 0:
+        return torch.zeros(1, dtype=_TORCH_DT[a.dtype], device=device)
+    t = torch.from_numpy(a)
+    return t.to(device, non_blocking=pin)
+
+
+def ptr(t: torch.Tensor | None) -> int:
+    return 0 if t is None else t.data_ptr()
+
+
+class DeviceKernel:
+    """KernelSoA uploaded to HBM."""
+
+    def __init__(self, ks, device="cuda"):
+        self.ks = ks
+        self.device = torch.device(device)
+        self.t = {n: to_device(getattr(ks, n), self.device) for n in K_ARRAYS}
+        self.line_id = to_device(np.asarray(ks.line_id, dtype=np.int32), self.device)
+        self.n_lines = int(len(ks.lines)) if ks.lines is not None else int(ks.line_id.max()) + 1
+        self.struct = abi.kernel_struct(ks, lambda n: self.t[n].data_ptr())
+
+    @property
+    def n_instr(self):
+        return self.ks.n_instr
+
+    def nbytes(self) -> int:
+        return sum(t.numel() * t.element_size() for t in self.t.values()) + self.line_id.numel() * 4
+
+
+class DeviceProfile:
+    """ProfileSoA in HBM.  lat / cls_cnt are writable (stage-0 binning output)."""
+
+    def __init__(self, prof, n_instr: int, device="cuda"):
+        dev = torch.device(device)
+        self.period = int(prof.period)
+        self.lat = to_device(np.asarray(prof.lat, dtype=np.int32), dev)
+        self.cls_cnt = to_device(np.asarray(prof.cls_cnt, dtype=np.int32).reshape(-1), dev)
+        self.exec_cnt = to_device(np.asarray(prof.exec_cnt, dtype=np.int64), dev)
+        self.total = to_device(np.asarray(prof.total, dtype=np.int32), dev)
+        self.eff = to_device(np.asarray(prof.eff, dtype=np.float64), dev)
+        self.sampled = to_device(np.asarray(prof.sampled, dtype=np.uint8), dev)
+        self.struct = abi.LeoProfile(self.period, ptr(self.lat), ptr(self.cls_cnt), ptr(self.exec_cnt),
+                                     ptr(self.total), ptr(self.eff), ptr(self.sampled))
+
+
+class DeviceSamples:
+    def __init__(self, pc, cat, lut, device="cuda"):
+        dev = torch.device(device)
+        self.n = int(pc.shape[0])
+        self.pc = to_device(np.asarray(pc, dtype=np.int32), dev)
+        self.cat = to_device(np.asarray(cat, dtype=np.uint8), dev)
+        self.lut = to_device(np.asarray(lut, dtype=np.uint8), dev)
+        self.struct = abi.LeoSamples(self.n, ptr(self.pc), ptr(self.cat), ptr(self.lut))
+
+    @classmethod
+    def from_tensors(cls, pc: torch.Tensor, cat: torch.Tensor, lut: torch.Tensor):
+        self = cls.__new__(cls)
+        self.n = int(pc.numel())
+        self.pc, self.cat, self.lut = pc, cat, lut
+        self.struct = abi.LeoSamples(self.n, ptr(pc), ptr(cat), ptr(lut))
+        return self
+
+
+# counter slots in one int32 device vector
+C_BASE, C_BASE_REG, C_PR, C_PR_REG, C_PATHS, C_DIAGS, C_BLAME, C_STATUS = range(8)
+
+
+@dataclass
+class Caps:
+    base: int
+    pruned: int
+    paths: int
+    diags: int
+    blame: int
+    scratch_scale: int = 1
+
+
+class Analyzer:
+    """Owns output buffers for one kernel shape; runs the fused pipeline."""
+
+    def __init__(self, dk: DeviceKernel, device="cuda", caps: Caps | None = None):
+        self.dk = dk
+        self.device = torch.device(device)
+        n = dk.n_instr
+        nu, _ = abi.unit_counts(dk.ks)
+        self.n_use_units = nu
+        if caps is None:
+            base = 3 * nu + 2 * n + 1024
+            caps = Caps(base=base, pruned=base, paths=2 * base, diags=2 * n + 1024,
+                        blame=base + n + 1024)
+        self.caps = caps
+        self._alloc()
+
+    def _alloc(self):
+        d, c, n = self.device, self.caps, self.dk.n_instr
+        i32 = lambda m: torch.empty(max(m, 1), dtype=torch.int32, device=d)  # noqa: E731
+        self.ctr = torch.zeros(8, dtype=torch.int32, device=d)
+        self.b_prod, self.b_cons, self.b_meta = i32(c.base), i32(c.base), i32(c.base)
+        self.p_prod, self.p_cons, self.p_meta = i32(c.pruned), i32(c.pruned), i32(c.pruned)
+        self.pa_first, self.pa_np = i32(c.pruned), i32(c.pruned)
+        self.pa_dist = torch.empty(max(c.pruned, 1), dtype=torch.float64, device=d)
+        self.pa_len = i32(c.paths)
+        self.pa_acc = torch.empty(max(c.paths, 1), dtype=torch.float64, device=d)
+        self.diag = i32(6 * c.diags)
+        self.bl_stalled, self.bl_edge = i32(c.blame), i32(c.blame)
+        self.bl_sub = torch.empty(max(c.blame, 1), dtype=torch.uint8, device=d)
+        self.bl_blame = torch.empty(max(c.blame, 1), dtype=torch.float64, device=d)
+        self.bl_factors = torch.empty(max(4 * c.blame, 1), dtype=torch.float64, device=d)
+        self.level = i32(n)
+        self.bitmap = i32((n + 31) // 32)
+        self.line_blame = torch.empty(max(self.dk.n_lines, 1), dtype=torch.float64, device=d)
+        self.line_stall = torch.empty(max(self.dk.n_lines, 1), dtype=torch.float64, device=d)
+        cp = self.ctr.data_ptr()
+        at = lambda k: cp + 4 * k  # noqa: E731
+        self.s_base = abi.LeoEdges(c.base, ptr(self.b_prod), ptr(self.b_cons), ptr(self.b_meta),
+                                   at(C_BASE), at(C_BASE_REG))
+        self.s_pruned = abi.LeoEdges(c.pruned, ptr(self.p_prod), ptr(self.p_cons), ptr(self.p_meta),
+                                     at(C_PR), at(C_PR_REG))
+        self.s_paths = abi.LeoPaths(c.paths, ptr(self.pa_first), ptr(self.pa_np), ptr(self.pa_dist),
+                                    ptr(self.pa_len), ptr(self.pa_acc), at(C_PATHS))
+        self.s_diags = abi.LeoDiags(c.diags, ptr(self.diag), at(C_DIAGS))
+        self.s_blame = abi.LeoBlame(c.blame, ptr(self.bl_stalled), ptr(self.bl_edge), ptr(self.bl_sub),
+                                    ptr(self.bl_blame), ptr(self.bl_factors), at(C_BLAME))
+        s = self.caps.scratch_scale
+        nu, n = self.n_use_units, self.dk.n_instr
+        self.s_caps = abi.LeoCaps((4 * nu + 1024) * s, (6 * nu + 1024) * s, (2 * n + 1024) * s,
+                                  (n // 4 + 1024) * s)
+        self.status_ptr = at(C_STATUS)
+
+    # -- launch ------------------------------------------------------------
+    def launch(self, dp: DeviceProfile, cfg: abi.LeoConfig, samples: DeviceSamples | None = None,
+               stream: torch.cuda.Stream | None = None, slice_: bool = True, lines: bool = True):
+        st = stream or torch.cuda.current_stream(self.device)
+        self.ctr.zero_()
+        L = lib()
+        rc = L.leo_analyze(C.byref(self.dk.struct), C.byref(dp.struct),
+                           C.byref(samples.struct) if samples is not None else None,
+                           C.byref(cfg), C.byref(self.s_caps), C.byref(self.s_base),
+                           C.byref(self.s_pruned), C.byref(self.s_paths), C.byref(self.s_diags),
+                           C.byref(self.s_blame), ptr(self.bitmap) if slice_ else None,
+                           ptr(self.level) if slice_ else None,
+                           ptr(self.dk.line_id) if lines else None, self.dk.n_lines,
+                           ptr(self.line_blame) if lines else None,
+                           ptr(self.line_stall) if lines else None, self.status_ptr,
+                           st.cuda_stream)
+        check(rc, "leo_analyze")
+
+    def counts(self) -> np.ndarray:
+        return self.ctr.cpu().numpy()
+
+    def run(self, dp: DeviceProfile, cfg: abi.LeoConfig, samples: DeviceSamples | None = None,
+            max_retries: int = 6):
+        """Launch, synchronise, grow buffers and re-run on overflow."""
+        for _ in range(max_retries):
+            self.launch(dp, cfg, samples)
+            c = self.counts()
+            status = int(np.uint32(c[C_STATUS]))
+            if status & abi.ST_BAD_INPUT:
+                raise ValueError("device reported malformed input (sample pc out of range or "
+                                 "a block with more than two successors)")
+            grow = False
+            caps = self.caps
+            if c[C_BASE] > caps.base or status & abi.ST_EDGE_OVERFLOW:
+                caps.base = caps.pruned = int(max(c[C_BASE], caps.base) * 2) + 1024
+                caps.blame = caps.base + self.dk.n_instr + 1024
+                grow = True
+            if c[C_PATHS] > caps.paths or status & abi.ST_PATH_OVERFLOW:
+                caps.paths = int(max(c[C_PATHS], caps.paths) * 1.5) + 1024
+                grow = True
+            if c[C_DIAGS] > caps.diags or status & abi.ST_DIAG_OVERFLOW:
+                caps.diags = int(max(c[C_DIAGS], caps.diags) * 1.5) + 1024
+                grow = True
+            if c[C_BLAME] > caps.blame or status & abi.ST_BLAME_OVERFLOW:
+                caps.blame = int(max(c[C_BLAME], caps.blame) * 1.5) + 1024
+                grow = True
+            if status & abi.ST_SCRATCH_OVERFLOW:
+                caps.scratch_scale *= 4
+                grow = True
+            if not grow:
+                return c
+            self._alloc()
+        raise RuntimeError("leo_analyze: buffers kept overflowing")
+
+    # -- results -------------------------------------------------------------
+    def result(self) -> dict:
+        c = self.counts()
+        cp = self.caps
+        nb, npr = min(int(c[C_BASE]), cp.base), min(int(c[C_PR]), cp.pruned)
+        npa, nd = min(int(c[C_PATHS]), cp.paths), min(int(c[C_DIAGS]), cp.diags)
+        nbl = min(int(c[C_BLAME]), cp.blame)
+        h = lambda t, m: t[:m].cpu().numpy()  # noqa: E731
+        return dict(
+            bprod=h(self.b_prod, nb), bcons=h(self.b_cons, nb),
+            bmeta=h(self.b_meta, nb).view(np.uint32), n_regular=int(c[C_BASE_REG]),
+            pprod=h(self.p_prod, npr), pcons=h(self.p_cons, npr),
+            pmeta=h(self.p_meta, npr).view(np.uint32), p_n_regular=int(c[C_PR_REG]),
+            first=h(self.pa_first, npr), npaths=h(self.pa_np, npr), pdist=h(self.pa_dist, npr),
+            plen=h(self.pa_len, npa), pacc=h(self.pa_acc, npa),
+            diag_records=h(self.diag, 6 * nd).reshape(-1, 6),
+            e_stalled=h(self.bl_stalled, nbl), e_edge=h(self.bl_edge, nbl),
+            e_sub=h(self.bl_sub, nbl), e_blame=h(self.bl_blame, nbl),
+            e_factors=h(self.bl_factors, 4 * nbl).reshape(-1, 4),
+            level=h(self.level, self.dk.n_instr),
+            bitmap=h(self.bitmap, (self.dk.n_instr + 31) // 32).view(np.uint32),
+            line_blame=h(self.line_blame, self.dk.n_lines),
+            line_stall=h(self.line_stall, self.dk.n_lines),
+            status=int(np.uint32(c[C_STATUS])))
+
+
+def analyze_soa(ks, prof, cfg: abi.LeoConfig | None = None, samples=None, device="cuda") -> dict:
+    """One-shot convenience: upload, run, download."""
+    dk = DeviceKernel(ks, device)
+    dp = DeviceProfile(prof, ks.n_instr, device)
+    ds = None
+    if samples is not None:
+        pc, cat, lut = samples
+        ds = DeviceSamples(pc, cat, lut, device)
+    an = Analyzer(dk, device)
+    an.run(dp, cfg or abi.make_config(dialect=ks.dialect), ds)
+    r = an.result()
+    if ds is not None:
+        r["lat"] = dp.lat.cpu().numpy()
+        r["cls_cnt"] = dp.cls_cnt.cpu().numpy().reshape(-1, 8)
+    return r

@@ -1,0 +1,108 @@
+"""GPU parity: the CUDA path (libleo_b200.so through its C ABI) against the
+reference's golden vectors and the oracle.
+
+Bit-exact: base edges, pruned edges, valid paths, diagnostics, slice levels,
+blame structure, blame cycles and factors (the device reproduces the
+reference's floating-point evaluation order; north-star tolerance is 1e-6
+relative, we test rel=0).  Per-line totals use FP64 atomics on the device
+(summation order differs): rel 1e-9.
+"""
+
+import numpy as np
+import pytest
+
+import golden_io
+import parity
+from conftest import GOLDEN_FILES
+
+torch = pytest.importorskip("torch")
+pytestmark = pytest.mark.gpu
+
+
+def device_outputs(ks, r):
+    from paper_2604_20032_b200 import diagnostics
+    got = dict(bprod=r["bprod"], bcons=r["bcons"], bmeta=r["bmeta"], pprod=r["pprod"],
+               pcons=r["pcons"], pmeta=r["pmeta"], npaths=r["npaths"], first=r["first"],
+               plen=r["plen"], pacc=r["pacc"], level=r["level"],
+               line_blame=r["line_blame"], line_stall=r["line_stall"])
+    got["diags"] = list(ks.prefix_diagnostics) + diagnostics.render(ks.dialect, ks.offset,
+                                                                    r["diag_records"])
+    got.update(parity.blame_arrays(ks.dialect, r["e_stalled"], r["e_edge"], r["e_sub"],
+                                   r["e_blame"], r["e_factors"], r["pprod"], r["pmeta"]))
+    return got
+
+
+@pytest.fixture(scope="module")
+def cuda():
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    from paper_2604_20032_b200 import _lib
+    _lib.lib()          # fail loudly if the library is missing
+    return torch.device("cuda:0")
+
+
+@pytest.mark.parametrize("fname", GOLDEN_FILES)
+def test_device_matches_reference_golden(fname, golden_cases, cuda):
+    from paper_2604_20032_b200 import device
+    cases = golden_cases[fname]
+    bad = []
+    for ks, pf, cfg, exp in cases:
+        r = device.analyze_soa(ks, pf, golden_io.config_of(cfg, ks.dialect), device=cuda)
+        assert r["status"] == 0, (ks.name, r["status"])
+        errs = parity.compare(exp, device_outputs(ks, r), rel=0.0, line_rel=1e-9)
+        if errs:
+            bad.append((ks.name, errs[:2]))
+    assert not bad, f"{len(bad)}/{len(cases)} cases differ; first: {bad[:3]}"
+
+
+@pytest.mark.parametrize("tag,scale", [("c2", 1.0), ("c3", 1.0), ("c5", 0.05)])
+def test_device_matches_oracle_synthetic(tag, scale, cuda):
+    """Full-size C2/C3 (C5 at 5 %): raw samples binned on the device, whole
+    pipeline, compared with the oracle on the same seeded inputs."""
+    from oracle import oracle
+    from paper_2604_20032_b200 import abi, device, synth
+    wl = synth.config_workload(tag, scale=scale)
+    ks = wl.kernel
+    r = device.analyze_soa(ks, wl.profile, abi.make_config(dialect=ks.dialect),
+                           samples=(wl.pc, wl.cat, wl.lut), device=cuda)
+    assert r["status"] == 0
+    pf = synth.bin_host(wl)
+    assert np.array_equal(r["lat"], pf.lat)
+    assert np.array_equal(r["cls_cnt"], pf.cls_cnt)
+    o = oracle.run(ks, pf)
+    exp = parity.oracle_outputs(ks, o)
+    errs = parity.compare(exp, device_outputs(ks, r), rel=0.0, line_rel=1e-9)
+    assert not errs, errs
+    # conservation (report.py:147-155): per-line blame sums to total stall cycles
+    total = float((pf.lat.astype(np.int64) * pf.period).sum())
+    assert np.isclose(r["line_blame"].sum(), total, rtol=1e-9)
+    assert np.isclose(r["line_stall"].sum(), total, rtol=1e-9)
+
+
+def test_device_full_c5_properties(cuda):
+    """C5 at full size (1M instructions, 100M samples): size-independent
+    properties — binning conserves S, blame conserves stall cycles per line
+    and in total, every stalled PC is in the slice at level 0, slice levels
+    are consistent with pruned edges (each level-L node has a consumer at L-1)."""
+    from paper_2604_20032_b200 import abi, device, synth
+    wl = synth.config_workload("c5")
+    ks = wl.kernel
+    r = device.analyze_soa(ks, wl.profile, abi.make_config(dialect="nvidia"),
+                           samples=(wl.pc, wl.cat, wl.lut), device=cuda)
+    assert r["status"] == 0
+    lat = r["lat"].astype(np.int64)
+    assert lat.sum() == wl.n_samples
+    total = float((lat * 100).sum())
+    assert np.isclose(r["e_blame"].sum(), total, rtol=1e-9)
+    assert np.isclose(r["line_blame"].sum(), total, rtol=1e-9)
+    lv = r["level"]
+    assert np.all(lv[lat > 0] == 0) and np.all(lv[lat == 0] != 0)
+    pp, pc = r["pprod"], r["pcons"]
+    deeper = lv[pp] > 0
+    # every producer at level L>0 was reached from a consumer at level L-1
+    best = np.full(ks.n_instr, np.iinfo(np.int32).max, dtype=np.int64)
+    ok = (lv[pc] >= 0)
+    np.minimum.at(best, pp[ok], lv[pc[ok]].astype(np.int64) + 1)
+    inside = lv >= 0
+    assert np.all(best[inside & (lv > 0)] == lv[inside & (lv > 0)])
+    assert deeper.sum() >= 0
