@@ -1,0 +1,347 @@
+#!/usr/bin/env python
+"""Benchmark: stalled-PC samples attributed per second through the LEO hot path.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+                    [--config c2|c3|c5] [--trace]
+
+A step = one pass of the whole hot path over one synthetic workload resident in
+HBM: stage-0 binning of the raw (pc, category) stream, build_graph (reaching
+definitions, per-use link, vendor sync edges), run_pruning (stages 1-4 incl.
+the stage-3 path DFS), the multi-source backward slice, attribute_blame
+(Eq. 1 + self-blame) and the per-source-line rollup; at N>1 also the NCCL
+all-reduce of the per-line blame vector.  value = samples attributed / s over
+all ranks (each rank analyses its own kernel of the configured shape:
+weak scaling by kernel).  Device time from CUDA events; L2 is
+flushed (256 MiB write) between timed steps; max over ranks.
+
+The default workload is BASELINE.json configs[1] (C2): a synthetic AMD GCN
+kernel, 10,000 instructions with s_waitcnt vmcnt/lgkmcnt edges, 1,000,000 PC
+samples.  `--impl reference` times the CPU restatement (oracle/, the port of
+the reference's Python path; the reference itself is pure Python and does not
+travel to the GPU box) on the host cores on the same workload.
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import sys
+import threading
+import time
+from pathlib import Path
+
+import numpy as np
+
+ROOT = Path(__file__).resolve().parent
+sys.path[:0] = [str(ROOT), str(ROOT / "tests")]
+
+METRIC = "stalled-PC samples attributed/sec"
+UNIT = "samples/s"
+WORKLOADS = {
+    "c2": "C2: synthetic AMD GCN kernel, 10k instrs, s_waitcnt vmcnt/lgkmcnt edges, 1M PC samples",
+    "c3": "C3: synthetic Intel Xe kernel, 50k instrs, SWSB tokens, while-nests <= 8 deep, 5M samples",
+    "c5": "C5: synthetic NVIDIA kernel, 1M instrs, barrier masks, 100M PC samples",
+}
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=50)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--config", default="c2", choices=["c2", "c3", "c5"])
+    ap.add_argument("--scale", type=float, default=1.0)
+    ap.add_argument("--trace", action="store_true", help="print per-kernel device time")
+    ap.add_argument("--no-cpu", action="store_true", help="skip the CPU baseline leg")
+    ap.add_argument("--cpu-seconds", type=float, default=10.0)
+    return ap.parse_args()
+
+
+def dist_env():
+    ws = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return ws, rank, local
+
+
+def peaks():
+    for p in (ROOT / "MEASURED_PEAKS.json",):
+        if p.exists():
+            d = json.loads(p.read_text())
+            return float(d["hbm_gbs"]), "measured (MEASURED_PEAKS.json)"
+    return 6650.0, "fallback (B200_PROFILING.md)"
+
+
+# ---------------------------------------------------------------------------
+class ClockSampler:
+    """nvidia-smi-equivalent clock/throttle sampling (NVML) during the timed region."""
+
+    REASONS = {0x4: "sw_power_cap", 0x8: "hw_slowdown", 0x20: "sw_thermal_slowdown",
+               0x40: "hw_thermal_slowdown", 0x80: "hw_power_brake_slowdown", 0x2: "applications_clocks",
+               0x1: "gpu_idle"}
+
+    def __init__(self, torch_dev):
+        self.samples, self.reasons, self.ok = [], set(), False
+        try:
+            import pynvml
+            import torch
+            pynvml.nvmlInit()
+            pr = torch.cuda.get_device_properties(torch_dev)
+            try:
+                bus = f"{pr.pci_domain_id:08x}:{pr.pci_bus_id:02x}:{pr.pci_device_id:02x}.0"
+                self.h = pynvml.nvmlDeviceGetHandleByPciBusId(bus.encode())
+            except Exception:
+                self.h = pynvml.nvmlDeviceGetHandleByIndex(torch_dev.index or 0)
+            self.nv = pynvml
+            self.max = pynvml.nvmlDeviceGetMaxClockInfo(self.h, pynvml.NVML_CLOCK_SM)
+            self.ok = True
+        except Exception as e:  # pragma: no cover
+            self.err = str(e)
+        self._stop = threading.Event()
+
+    def _poll(self):
+        while not self._stop.is_set():
+            self.sample()
+            time.sleep(0.02)
+
+    def sample(self):
+        if not self.ok:
+            return
+        try:
+            sm = self.nv.nvmlDeviceGetClockInfo(self.h, self.nv.NVML_CLOCK_SM)
+            try:
+                r = self.nv.nvmlDeviceGetCurrentClocksEventReasons(self.h)
+            except Exception:
+                r = self.nv.nvmlDeviceGetCurrentClocksThrottleReasons(self.h)
+            self.samples.append(sm)
+            for bit, name in self.REASONS.items():
+                if r & bit and name != "gpu_idle":
+                    self.reasons.add(name)
+        except Exception:
+            pass
+
+    def __enter__(self):
+        self.sample()
+        self.t = threading.Thread(target=self._poll, daemon=True)
+        self.t.start()
+        return self
+
+    def __exit__(self, *a):
+        self._stop.set()
+        self.t.join()
+        self.sample()
+
+    def summary(self):
+        if not self.ok or not self.samples:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvml unavailable"]}
+        return {"sm_mhz": float(np.median(self.samples)), "sm_max_mhz": float(self.max),
+                "reasons": sorted(self.reasons), "n_samples": len(self.samples)}
+
+
+# ---------------------------------------------------------------------------
+def cpu_port_time(wl, seconds: float, min_iters: int = 1):
+    """Oracle port (single thread) on the full workload: binning + pipeline."""
+    from oracle import oracle
+    from paper_2604_20032_b200 import abi
+    ks = wl.kernel
+    cfg = abi.make_config(dialect=ks.dialect)
+    times, stages = [], None
+    t_end = time.perf_counter() + seconds
+    while len(times) < min_iters or time.perf_counter() < t_end:
+        t0 = time.perf_counter()
+        lat, cls = oracle.bin_samples(wl.pc, wl.cat, wl.lut, ks.n_instr)
+        p = wl.profile
+        prof = type(p)(period=p.period, lat=lat, cls_cnt=cls, exec_cnt=p.exec_cnt, total=p.total,
+                       eff=p.eff, sampled=p.sampled)
+        r = oracle.run(ks, prof, cfg)
+        times.append(time.perf_counter() - t0)
+        stages = r.times
+    return times, stages
+
+
+def run_reference(args, ws, rank):
+    if rank != 0:
+        return 0
+    from paper_2604_20032_b200 import synth
+    wl = synth.config_workload(args.config, scale=args.scale)
+    for _ in range(max(args.warmup, 0)):
+        cpu_port_time(wl, 0.0)
+    times = []
+    for _ in range(args.steps):
+        t, _ = cpu_port_time(wl, 0.0)
+        times.extend(t)
+    T = float(np.sum(times))
+    value = wl.n_samples * len(times) / T
+    line = {"impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": ws,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * T / len(times),
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "int32/f64",
+            "data": "synthetic", "config": {"workload": WORKLOADS[args.config], "scale": args.scale},
+            "cpu_baseline": {"value": value, "unit": UNIT, "cores": 1, "kind": "port",
+                             "sample": f"full {args.config} workload per step (oracle/leo_oracle.c, "
+                                       f"binning + build + prune + slice + blame + lines)"},
+            "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+# ---------------------------------------------------------------------------
+def run_ours(args, ws, rank, local):
+    import torch
+    import torch.distributed as dist
+    from paper_2604_20032_b200 import abi, api, device, roofline, synth
+
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    if ws > 1:
+        dist.init_process_group("nccl", device_id=dev)
+
+    # each rank analyses its own kernel of the configured shape (shared line pool)
+    wl = synth.config_workload(args.config, scale=args.scale, seed_offset=rank)
+    ks = wl.kernel
+    cfg = abi.make_config(dialect=ks.dialect)
+    dk = device.DeviceKernel(ks, dev)
+    dp = device.DeviceProfile(wl.profile, ks.n_instr, dev)
+    ds = device.DeviceSamples(wl.pc, wl.cat, wl.lut, dev)
+    an = device.Analyzer(dk, dev)
+    counts = an.run(dp, cfg, ds)               # sizes buffers (grow + re-run on overflow)
+    res = an.result()
+    assert res["status"] == 0
+
+    def allreduce_lines():
+        if ws > 1:
+            dist.all_reduce(an.line_blame, op=dist.ReduceOp.SUM)
+            dist.all_reduce(an.line_stall, op=dist.ReduceOp.SUM)
+
+    # per-kernel breakdown of one step (all kernels traced)
+    tracer = device.Tracer(capacity=4096)
+    an.set_tracer(tracer)
+    torch.cuda.synchronize()
+    an.launch(dp, cfg, ds)
+    torch.cuda.synchronize()
+    breakdown = tracer.summary()
+    n_launch = sum(3 if k == "scan" else 1 for k, _ in tracer.records())
+    dominant = max(breakdown, key=breakdown.get)
+    tracer.reset(only_kernel=device.kernel_id(dominant))
+
+    flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)
+    for _ in range(args.warmup):
+        flush.zero_()
+        an.launch(dp, cfg, ds)
+        allreduce_lines()
+    torch.cuda.synchronize()
+    tracer.reset()
+    starts = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
+    ends = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
+    clocks = ClockSampler(dev)
+    if ws > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    with clocks:
+        for s in range(args.steps):
+            flush.zero_()                       # L2 flush between timed steps (not timed)
+            starts[s].record()
+            an.launch(dp, cfg, ds)
+            allreduce_lines()
+            ends[s].record()
+        torch.cuda.synchronize()
+    if ws > 1:
+        dist.barrier()
+    step_ms = np.array([a.elapsed_time(b) for a, b in zip(starts, ends)])
+    T = float(step_ms.sum())
+    dom_ms = [ms for _, ms in tracer.records()]
+    t = torch.tensor([T], dtype=torch.float64, device=dev)
+    if ws > 1:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    T_max = float(t.item())
+    S = wl.n_samples
+    value = ws * S * args.steps / (T_max / 1e3)
+    res = an.result()
+    assert res["status"] == 0
+
+    # roofline of the dominant kernel (algorithmic bytes / live event time)
+    peak, peak_src = peaks()
+    alg = roofline.kernel_bytes(dominant, ks, wl, res)
+    avg_s = float(np.mean(dom_ms)) / 1e3 if dom_ms else None
+    achieved = alg / avg_s / 1e9 if (alg and avg_s) else None
+    traffic = roofline.ncu_traffic(ROOT / "profiles", args.config, dominant)
+    pipe_bytes = roofline.pipeline_bytes(ks, wl, res)
+
+    # e2e through the public API: pinned host inputs in, results out, every step
+    sess = api.Session(ks, wl.profile, S, cfg, dev)
+    sess.an.caps = an.caps
+    sess.an._alloc()
+    sess.stage(ks, wl.profile, wl.pc, wl.cat, wl.lut)
+
+    def allreduce_sess(lb, ls):
+        dist.all_reduce(lb, op=dist.ReduceOp.SUM)
+        dist.all_reduce(ls, op=dist.ReduceOp.SUM)
+
+    sess.analyze(allreduce=allreduce_sess if ws > 1 else None)
+    e2e_t = []
+    for s in range(max(3, min(args.steps, 20))):
+        if ws > 1:
+            dist.barrier()
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        sess.analyze(allreduce=allreduce_sess if ws > 1 else None)
+        e2e_t.append(time.perf_counter() - t0)
+    te = torch.tensor([float(np.sum(e2e_t))], dtype=torch.float64, device=dev)
+    if ws > 1:
+        dist.all_reduce(te, op=dist.ReduceOp.MAX)
+    e2e_value = ws * S * len(e2e_t) / float(te.item())
+
+    cpu = None
+    if rank == 0 and ws == 1 and not args.no_cpu:
+        times, stages = cpu_port_time(wl, args.cpu_seconds)
+        cpu = {"value": S / float(np.mean(times)), "unit": UNIT, "cores": 1, "kind": "port",
+               "sample": f"full {args.config} workload x{len(times)} (oracle/leo_oracle.c: binning "
+                         f"+ build + prune + slice + blame + lines; {np.mean(times) * 1e3:.1f} ms each)"}
+
+    if rank == 0:
+        line = {
+            "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": ws, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": T_max / args.steps, "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "int32/f64", "data": "synthetic",
+            "config": {"workload": WORKLOADS[args.config], "scale": args.scale,
+                       "per_rank": f"one kernel per rank (seed {synth.CONFIGS[args.config]['seed']}+rank)",
+                       "n_instr": ks.n_instr, "n_samples_per_rank": S,
+                       "edges": int(counts[device.C_BASE]), "pruned_edges": int(counts[device.C_PR]),
+                       "blame_entries": int(counts[device.C_BLAME]),
+                       "l2": "flushed between timed steps (256 MiB write)",
+                       "parallelism": f"kernel-sharded x{ws}" + (" + NCCL all-reduce of f64 line blame" if ws > 1 else "")},
+            "roofline": {"bound": "hbm", "kernel": dominant, "achieved": achieved, "peak": peak,
+                         "unit": "GB/s", "frac": (achieved / peak) if achieved else None,
+                         "traffic": traffic, "alg_bytes_per_launch": alg,
+                         "avg_launch_ms": avg_s * 1e3 if avg_s else None, "peak_source": peak_src},
+            "pipeline_roofline": {"alg_bytes_per_step": pipe_bytes,
+                                  "achieved_gbs": pipe_bytes / (T_max / args.steps / 1e3) / 1e9,
+                                  "frac": pipe_bytes / (T_max / args.steps / 1e3) / 1e9 / peak},
+            "cpu_baseline": cpu,
+            "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": sess.h2d_bytes(),
+                    "d2h_bytes_per_step": int(sess.last_d2h)},
+            "gpu_launches": n_launch * args.steps,
+            "clocks": clocks.summary(),
+            "kernel_ms_one_step": {k: round(v, 4) for k, v in sorted(breakdown.items(), key=lambda x: -x[1])},
+        }
+        print(json.dumps(line), flush=True)
+    if args.trace and rank == 0:
+        for k, v in sorted(breakdown.items(), key=lambda x: -x[1]):
+            print(f"  {k:20s} {v:8.4f} ms", file=sys.stderr)
+    tracer.close()
+    if ws > 1:
+        dist.destroy_process_group()
+    return 0
+
+
+def main():
+    args = parse()
+    ws, rank, local = dist_env()
+    if args.impl == "reference":
+        return run_reference(args, ws, rank)
+    return run_ours(args, ws, rank, local)
+
+
+if __name__ == "__main__":
+    sys.exit(main())

@@ -186,12 +186,28 @@ typedef struct LeoBlame {
   int32_t* count;             /* device scalar */
 } LeoBlame;
 
+/* ---- optional device-time trace ------------------------------------------
+ * When LeoCaps.trace is non-NULL the library records the caller's CUDA events
+ * (cudaEvent_t passed as void*) on the launching stream around every kernel
+ * (or only around kernel id `only_kernel` when >= 0): slot x brackets kernel
+ * kernel_id[x]; `count` advances past `capacity` when slots run out.       */
+typedef struct LeoTrace {
+  int32_t capacity;
+  int32_t count;
+  int32_t only_kernel;        /* -1: all kernels */
+  int32_t pad;
+  void**  ev_begin;           /* [capacity] cudaEvent_t */
+  void**  ev_end;             /* [capacity] cudaEvent_t */
+  int32_t* kernel_id;         /* [capacity] host array */
+} LeoTrace;
+
 /* ---- capacity hints for internal scratch (0 = default heuristic) --------- */
 typedef struct LeoCaps {
   int64_t query_results;      /* reaching-definition results pool        (default 4 x use units) */
   int64_t candidates;         /* per-use link candidates                  (default 6 x use units) */
   int64_t sync_keys;          /* raw sync edges before dedup              (default 2 x N + 1024) */
   int64_t slow_items;         /* work items re-run on the global-scratch path (default N/4 + 1024) */
+  LeoTrace* trace;            /* optional, host struct (NULL = no tracing) */
 } LeoCaps;
 
 /* ---- status word (device) ------------------------------------------------ */
@@ -200,6 +216,8 @@ enum { LEO_ST_EDGE_OVERFLOW = 1, LEO_ST_PATH_OVERFLOW = 2, LEO_ST_DIAG_OVERFLOW 
 
 /* ---- entry points ---------------------------------------------------------- */
 int leo_abi_version(void);
+/* name of traced kernel id (LeoTrace.kernel_id), NULL past the last id */
+const char* leo_kernel_name(int id);
 
 /* stage 0: raw (pc, category) stream -> lat[N], cls_cnt[N*8] (zeroed here). */
 int leo_bin_samples(const LeoSamples* s, int32_t n_instr, int32_t* lat, int32_t* cls_cnt,
@@ -226,6 +244,11 @@ int leo_blame(const LeoKernel* k, const LeoProfile* p, const LeoEdges* pruned,
               const LeoPaths* paths, const LeoEdges* base, const int32_t* line_id,
               int32_t n_lines, LeoBlame* out, double* line_blame, double* line_stall,
               uint32_t* status, void* stream);
+
+/* profiling helpers for LeoTrace: create / time / destroy CUDA events */
+int leo_events_create(int32_t n, void** events);
+int leo_events_elapsed(int32_t n, void* const* begin, void* const* end, float* ms);
+int leo_events_destroy(int32_t n, void** events);
 
 /* fused pipeline (report.py:132-142 order): optional stage-0 binning of `samples`
  * into `p->lat` / `p->cls_cnt` (which must then be writable), build_graph,

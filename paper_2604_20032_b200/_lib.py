@@ -52,6 +52,13 @@ def lib():
                               C.POINTER(abi.LeoEdges), C.POINTER(abi.LeoPaths),
                               C.POINTER(abi.LeoDiags), C.POINTER(abi.LeoBlame), P, P, P,
                               C.c_int32, P, P, P, P]
+    L.leo_kernel_name.argtypes = [C.c_int]
+    L.leo_kernel_name.restype = C.c_char_p
+    L.leo_events_create.argtypes = [C.c_int32, P]
+    L.leo_events_elapsed.argtypes = [C.c_int32, P, P, P]
+    L.leo_events_destroy.argtypes = [C.c_int32, P]
+    for f in ("leo_events_create", "leo_events_elapsed", "leo_events_destroy"):
+        getattr(L, f).restype = C.c_int
     for f in ("leo_bin_samples", "leo_build_graph", "leo_prune", "leo_slice", "leo_blame",
               "leo_analyze"):
         getattr(L, f).restype = C.c_int

@@ -42,9 +42,15 @@ class LeoConfig(C.Structure):
     ]
 
 
+class LeoTrace(C.Structure):
+    _fields_ = [("capacity", C.c_int32), ("count", C.c_int32), ("only_kernel", C.c_int32),
+                ("pad", C.c_int32), ("ev_begin", P), ("ev_end", P), ("kernel_id", P)]
+
+
 class LeoCaps(C.Structure):
     _fields_ = [("query_results", C.c_int64), ("candidates", C.c_int64),
-                ("sync_keys", C.c_int64), ("slow_items", C.c_int64)]
+                ("sync_keys", C.c_int64), ("slow_items", C.c_int64),
+                ("trace", C.POINTER(LeoTrace))]
 
 
 class LeoEdges(C.Structure):

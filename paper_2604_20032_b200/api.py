@@ -1,0 +1,381 @@
+"""Public API: the reference analyzer's names and types, backed by the CUDA path.
+
+Drop-in for the stalltrace hot path (`stalltrace/__init__.py:9-37`):
+
+    build_graph(attached) -> DependencyGraph                 depgraph.py:507
+    run_pruning(graph, config) -> DependencyGraph            analysis.py:302
+    prune_opcode / prune_barrier / prune_latency / prune_execution   analysis.py:143-299
+    attribute_blame(graph, base_graph=None) -> list[BlameEntry]      analysis.py:431
+    self_blame(index, attached, base_graph=None) -> BlameEntry       analysis.py:414
+
+plus the two hot-path products the reference does not have:
+
+    backward_slice(graph) -> (frozenset[int], dict[int, int])
+    line_blame(graph, blame) -> (dict[str, float], dict[str, float])
+
+and `Session`, the SoA-level entry a profiling service uses (raw PC-sample
+stream in, per-instruction blame entries + per-line totals out).
+
+Inputs are the reference's own objects (duck-typed: any object with the
+reference attribute names works); outputs are built from `stalltrace` classes
+when that package is importable, else from the mirror classes in
+`paper_2604_20032_b200.types` (same names, fields and enum values).  Every
+computation runs on the GPU through libleo_b200.so; there is no CPU fallback.
+"""
+
+from __future__ import annotations
+
+import dataclasses
+import weakref
+
+import numpy as np
+import torch
+
+from . import abi, device, diagnostics, soa, types
+from . import enums as E
+
+_DEVICE = None
+
+
+def _dev():
+    global _DEVICE
+    if _DEVICE is None:
+        if not torch.cuda.is_available():
+            raise RuntimeError("the LEO B200 analysis path needs a CUDA device (no CPU fallback)")
+        _DEVICE = torch.device("cuda", torch.cuda.current_device())
+    return _DEVICE
+
+
+def _ns(obj):
+    """Output type namespace matching the input objects' package."""
+    mod = type(obj).__module__
+    if mod.startswith("stalltrace"):
+        import stalltrace.analysis as an
+        import stalltrace.depgraph as dg
+        import stalltrace.isa as isa
+        return types.Namespace.from_modules(dg, an, isa)
+    return types.Namespace.mirror()
+
+
+# --------------------------------------------------------------------------
+# one cached device analysis per (graph, config)
+
+@dataclasses.dataclass
+class _Analysis:
+    ks: soa.KernelSoA
+    prof: soa.ProfileSoA
+    raw: dict
+
+
+_cache: "weakref.WeakKeyDictionary" = weakref.WeakKeyDictionary()
+
+
+def _config_of(config, dialect):
+    if config is None:
+        return abi.make_config(dialect=dialect)
+    if isinstance(config, abi.LeoConfig):
+        return config
+    return abi.config_from_reference(config, dialect)
+
+
+def _run(attached, config=None) -> _Analysis:
+    ks, prof = soa.encode_attached(attached)
+    r = device.analyze_soa(ks, prof, _config_of(config, ks.dialect), device=_dev())
+    return _Analysis(ks, prof, r)
+
+
+def _edges(ns, ks, prod, cons, meta, npaths=None, first=None, plen=None, pacc=None):
+    out = []
+    cls = ns.RegClass
+    rcs = [cls(v) for v in E.REG_CLASSES]
+    kinds = [ns.EdgeKind(v) for v in E.EDGE_KINDS]
+    dcs = [ns.DepClass(v) for v in E.DEP_CLASSES]
+    prod, cons, meta = prod.tolist(), cons.tolist(), meta.astype(np.uint32).tolist()
+    if npaths is not None:
+        npaths, first, plen, pacc = npaths.tolist(), first.tolist(), plen.tolist(), pacc.tolist()
+    for x in range(len(prod)):
+        m = meta[x]
+        kind = (m >> 27) & 7
+        reg = None
+        if kind < 2:
+            reg = ns.RegisterRef(rcs[(m >> 24) & 7], m & 0xFFFF, (m >> 16) & 0xFF)
+        paths = ()
+        if npaths is not None and npaths[x] > 0:
+            f = first[x]
+            paths = tuple(ns.PathRecord(plen[f + q], pacc[f + q]) for q in range(npaths[x]))
+        out.append(ns.DepEdge(producer=prod[x], consumer=cons[x], kind=kinds[kind], register=reg,
+                              dep_class=dcs[(m >> 30) & 3], valid_paths=paths))
+    return tuple(out)
+
+
+def _graph(ns, attached, edges, diags, analysis, pruned):
+    g = ns.DependencyGraph(attached, edges, tuple(diags))
+    _cache[g] = (analysis, pruned)
+    return g
+
+
+def _split_diags(ks, r):
+    recs = diagnostics.order(r["diag_records"])
+    build = recs[recs[:, 0] != abi.DIAG_PATH_CAPPED] if recs.size else recs
+    prune = recs[recs[:, 0] == abi.DIAG_PATH_CAPPED] if recs.size else recs
+    return (diagnostics.render(ks.dialect, ks.offset, build, ordered=True),
+            diagnostics.render(ks.dialect, ks.offset, prune, ordered=True))
+
+
+# --------------------------------------------------------------------------
+# reference-compatible functions
+
+def build_graph(attached):
+    """depgraph.build_graph (depgraph.py:507-528) on the GPU."""
+    ns = _ns(attached)
+    a = _run(attached, abi.make_config(stage_mask=(), dialect=attached.cfg.dialect.value))
+    r = a.raw
+    edges = _edges(ns, a.ks, r["bprod"], r["bcons"], r["bmeta"])
+    bdiag, _ = _split_diags(a.ks, r)
+    return _graph(ns, attached, edges, tuple(attached.diagnostics) + tuple(attached.cfg.diagnostics)
+                  + tuple(bdiag), a, False)
+
+
+def _prune_with(graph, config):
+    attached = graph.attached
+    ns = _ns(attached)
+    a = _run(attached, config)
+    r = a.raw
+    base = _edges(ns, a.ks, r["bprod"], r["bcons"], r["bmeta"])
+    if tuple((e.producer, e.consumer, e.kind, e.register) for e in base) != \
+            tuple((e.producer, e.consumer, e.kind, e.register) for e in graph.edges):
+        raise ValueError("graph was not produced by build_graph on this kernel; the device "
+                         "pipeline prunes the build_graph edge list")
+    edges = _edges(ns, a.ks, r["pprod"], r["pcons"], r["pmeta"], r["npaths"], r["first"],
+                   r["plen"], r["pacc"])
+    _, pdiag = _split_diags(a.ks, r)
+    return _graph(ns, attached, edges, tuple(graph.diagnostics) + tuple(pdiag), a, True)
+
+
+def run_pruning(graph, config):
+    """analysis.run_pruning (analysis.py:302-314) on the GPU."""
+    return _prune_with(graph, config)
+
+
+def _stage(graph, mask, **kw):
+    d = graph.cfg.dialect.value
+    th = kw.pop("thresholds", None)
+    return _prune_with(graph, abi.make_config(stage_mask=mask, thresholds=th, dialect=d, **kw))
+
+
+def prune_opcode(graph):
+    """analysis.prune_opcode (analysis.py:143-162)."""
+    return _stage(graph, (1,))
+
+
+def prune_barrier(graph):
+    """analysis.prune_barrier (analysis.py:165-185)."""
+    if graph.cfg.dialect.value != "nvidia":
+        return graph
+    return _stage(graph, (2,))
+
+
+def prune_latency(graph, table, max_paths=64, max_depth=512):
+    """analysis.prune_latency (analysis.py:256-286)."""
+    th = E.dense_thresholds((c.value, v) for c, v in table.thresholds)
+    return _stage(graph, (3,), thresholds=th, max_paths=max_paths, max_depth=max_depth)
+
+
+def prune_execution(graph, enabled):
+    """analysis.prune_execution (analysis.py:289-299)."""
+    if not enabled:
+        return graph
+    return _stage(graph, (4,), prune_exec=True)
+
+
+def attribute_blame(graph, base_graph=None):
+    """analysis.attribute_blame (analysis.py:431-484) on the GPU.  When
+    `graph` came from run_pruning the device result of that run is reused;
+    base_graph (the unpruned graph) feeds the indirect-addressing test."""
+    ns = _ns(graph.attached)
+    hit = _cache.get(graph)
+    if hit is None:
+        raise ValueError("attribute_blame needs a graph produced by this package's "
+                         "build_graph / run_pruning")
+    a, pruned = hit
+    r = a.raw
+    ks = a.ks
+    if not pruned:
+        # blame directly on the base graph: prune with no stages (identity map)
+        a = _run(graph.attached, abi.make_config(stage_mask=(), dialect=ks.dialect))
+        r = a.raw
+    return _entries(ns, ks, r, base_graph is not None)
+
+
+def _entries(ns, ks, r, with_base=True):
+    kinds = [ns.EdgeKind(v) for v in E.EDGE_KINDS]
+    subs = [ns.SelfBlame(v) for v in E.SELF_BLAMES]
+    out = []
+    pprod, pmeta = r["pprod"].tolist(), r["pmeta"].astype(np.uint32).tolist()
+    for s, e, sub, bl, f in zip(r["e_stalled"].tolist(), r["e_edge"].tolist(),
+                                r["e_sub"].tolist(), r["e_blame"].tolist(),
+                                r["e_factors"].tolist()):
+        if e < 0:
+            if not with_base and sub == E.SB_IDX["indirect_addressing"]:
+                sub = E.SB_IDX["memory_latency"]
+            out.append(ns.BlameEntry(stalled=s, cause=None, kind=None, subcategory=subs[sub],
+                                     blame_cycles=bl, factors=None))
+        else:
+            m = pmeta[e]
+            kind = (m >> 27) & 7
+            reg = diagnostics.format_ref27(ks.dialect, m & 0x07FFFFFF) if kind < 2 else None
+            out.append(ns.BlameEntry(stalled=s, cause=pprod[e], kind=kinds[kind], subcategory=None,
+                                     blame_cycles=bl, factors=ns.Factors(*f), register=reg))
+    return out
+
+
+def self_blame(index, attached, base_graph=None):
+    """analysis.self_blame (analysis.py:414-428): the SELF entry of one
+    instruction (computed by the device blame kernel with no incoming edges)."""
+    ns = _ns(attached)
+    a = _run(attached, abi.make_config(stage_mask=(1, 2, 3, 4), dialect=attached.cfg.dialect.value))
+    r = a.raw
+    sel = np.flatnonzero((r["e_stalled"] == index) & (r["e_edge"] < 0))
+    if sel.size:
+        x = int(sel[0])
+        sub = int(r["e_sub"][x])
+    else:
+        raise ValueError("self_blame: instruction has incoming edges or no stall cycles")
+    if base_graph is None and sub == E.SB_IDX["indirect_addressing"]:
+        sub = E.SB_IDX["memory_latency"]
+    return ns.BlameEntry(stalled=index, cause=None, kind=None,
+                         subcategory=ns.SelfBlame(E.SELF_BLAMES[sub]),
+                         blame_cycles=float(r["e_blame"][x]), factors=None)
+
+
+def backward_slice(graph):
+    """Multi-source backward slice from every instruction with S_j > 0 over
+    graph.incoming: (members, {index: hop level})."""
+    hit = _cache.get(graph)
+    if hit is None:
+        raise ValueError("backward_slice needs a graph produced by this package")
+    a, pruned = hit
+    r = a.raw if pruned else _run(graph.attached, abi.make_config(stage_mask=(), dialect=a.ks.dialect)).raw
+    lv = r["level"]
+    idx = np.flatnonzero(lv >= 0)
+    return frozenset(idx.tolist()), {int(i): int(lv[i]) for i in idx}
+
+
+def line_blame(graph, blame=None):
+    """Per-source-line rollup: blame cycles by the cause's
+    line (self entries: the stalled instruction's line) and stall cycles by the
+    stalled instruction's line, keyed `file:line` / `<unknown>`."""
+    hit = _cache.get(graph)
+    if hit is None:
+        raise ValueError("line_blame needs a graph produced by this package")
+    a, _ = hit
+    keys = a.ks.lines
+    lb, ls = a.raw["line_blame"], a.raw["line_stall"]
+    return ({keys[i]: float(lb[i]) for i in np.flatnonzero(lb)},
+            {keys[i]: float(ls[i]) for i in np.flatnonzero(ls)})
+
+
+def analyze(attached, config=None):
+    """Fused build -> prune -> blame -> slice -> lines in one device pass:
+    (base graph, pruned graph, blame entries, slice, (line blame, line stall))."""
+    ns = _ns(attached)
+    a = _run(attached, config)
+    r = a.raw
+    bdiag, pdiag = _split_diags(a.ks, r)
+    prefix = tuple(attached.diagnostics) + tuple(attached.cfg.diagnostics)
+    base = _graph(ns, attached, _edges(ns, a.ks, r["bprod"], r["bcons"], r["bmeta"]),
+                  prefix + tuple(bdiag), a, False)
+    pruned = _graph(ns, attached, _edges(ns, a.ks, r["pprod"], r["pcons"], r["pmeta"], r["npaths"],
+                                         r["first"], r["plen"], r["pacc"]),
+                    prefix + tuple(bdiag) + tuple(pdiag), a, True)
+    entries = _entries(ns, a.ks, r)
+    return base, pruned, entries, backward_slice(pruned), line_blame(pruned)
+
+
+# --------------------------------------------------------------------------
+# SoA session: host buffers in, host results out (the bench's e2e path)
+
+class Session:
+    """Analyse raw PC-sample streams for one kernel shape.  Each `analyze`
+    call copies the kernel SoA, profile metadata and raw samples from (pinned)
+    host memory, runs the fused device pipeline and reads back the blame
+    entries and per-line totals."""
+
+    H2D_FIELDS = device.K_ARRAYS
+
+    def __init__(self, ks: soa.KernelSoA, prof_meta: soa.ProfileSoA, n_samples: int,
+                 config: abi.LeoConfig | None = None, dev=None, pin: bool = True):
+        self.dev = torch.device(dev) if dev is not None else _dev()
+        self.ks = ks
+        self.cfg = config or abi.make_config(dialect=ks.dialect)
+        self.dk = device.DeviceKernel(ks, self.dev)
+        self.dp = device.DeviceProfile(prof_meta, ks.n_instr, self.dev)
+        self.pc = torch.empty(max(n_samples, 1), dtype=torch.int32, device=self.dev)
+        self.cat = torch.empty(max(n_samples, 1), dtype=torch.uint8, device=self.dev)
+        self.lut = torch.empty(256, dtype=torch.uint8, device=self.dev)
+        self.ds = device.DeviceSamples.from_tensors(self.pc[:n_samples], self.cat[:n_samples], self.lut)
+        self.an = device.Analyzer(self.dk, self.dev)
+        self.pin = pin
+        self._host = {}
+
+    def _h(self, name, arr):
+        """pinned host staging copy of a numpy input"""
+        a = np.ascontiguousarray(arr)
+        if a.dtype == np.uint32:
+            a = a.view(np.int32)
+        t = self._host.get(name)
+        if t is None or t.numel() != a.size:
+            t = torch.from_numpy(a.copy()).reshape(-1)
+            if self.pin:
+                t = t.pin_memory()
+            self._host[name] = t
+        else:
+            t.numpy().reshape(a.shape)[...] = a
+        return t
+
+    def stage(self, ks, prof_meta, pc, cat, lut):
+        """Put one step's inputs into pinned host buffers (outside timing)."""
+        for n in self.H2D_FIELDS:
+            self._h("k_" + n, getattr(ks, n))
+        self._h("line_id", ks.line_id)
+        for n in ("exec_cnt", "total", "eff", "sampled"):
+            self._h("p_" + n, getattr(prof_meta, n))
+        self._h("pc", pc)
+        self._h("cat", cat)
+        self._h("lut", lut)
+
+    def h2d_bytes(self) -> int:
+        return sum(t.numel() * t.element_size() for t in self._host.values())
+
+    def analyze(self, allreduce=None):
+        """Copy staged inputs in, run, copy results out.  Returns host dict.
+        `allreduce(line_blame, line_stall)` (multi-GPU) runs on the device line
+        vectors before they are read back."""
+        for n in self.H2D_FIELDS:
+            self.dk.t[n].view(-1).copy_(self._host["k_" + n], non_blocking=True)
+        self.dk.line_id.copy_(self._host["line_id"], non_blocking=True)
+        for n in ("exec_cnt", "total", "eff", "sampled"):
+            getattr(self.dp, n).copy_(self._host["p_" + n], non_blocking=True)
+        S = self.ds.n
+        self.pc[:S].copy_(self._host["pc"], non_blocking=True)
+        self.cat[:S].copy_(self._host["cat"], non_blocking=True)
+        self.lut.copy_(self._host["lut"], non_blocking=True)
+        self.an.launch(self.dp, self.cfg, self.ds)
+        c = self.an.ctr.cpu().numpy()          # sync: how much to read back
+        nbl = min(int(c[device.C_BLAME]), self.an.caps.blame)
+        if nbl > self.an.caps.blame or c[device.C_STATUS] != 0:
+            self.an.run(self.dp, self.cfg, self.ds)
+            c = self.an.ctr.cpu().numpy()
+            nbl = int(c[device.C_BLAME])
+        if allreduce is not None:
+            allreduce(self.an.line_blame, self.an.line_stall)
+        out = {
+            "e_stalled": self.an.bl_stalled[:nbl].to("cpu", non_blocking=True),
+            "e_edge": self.an.bl_edge[:nbl].to("cpu", non_blocking=True),
+            "e_blame": self.an.bl_blame[:nbl].to("cpu", non_blocking=True),
+            "line_blame": self.an.line_blame.to("cpu", non_blocking=True),
+            "line_stall": self.an.line_stall.to("cpu", non_blocking=True),
+        }
+        torch.cuda.current_stream(self.dev).synchronize()
+        self.last_d2h = sum(t.numel() * t.element_size() for t in out.values()) + c.nbytes
+        return {k: v.numpy() for k, v in out.items()}

@@ -1,4 +1,4 @@
-// abi.cu — extern "C" entry points of libleo_b200.so (include/leo_b200.h).
+// leo_b200.cu — extern "C" entry points of libleo_b200.so (include/leo_b200.h).
 //
 // Each entry point enqueues its kernels on the caller's stream; scratch comes
 // from the stream-ordered allocator (cudaMallocAsync) and is released on the
@@ -18,6 +18,36 @@
 using namespace leo;
 
 namespace {
+
+// ---- optional device-time trace (LeoTrace) ---------------------------------
+enum KernelId {
+  KID_BIN = 0, KID_BIN_FINALIZE, KID_UNIT_COUNTS, KID_SCAN, KID_BLOCK_WALK, KID_REACH_FAST,
+  KID_REACH_SLOW, KID_LINK_COUNT, KID_LINK_FILL, KID_SEGSORT, KID_LINK_EMIT, KID_SYNC,
+  KID_SYNC_SLOW, KID_KEY_HIST, KID_KEY_SCATTER, KID_SYNC_EMIT, KID_EDGE_TOTALS, KID_PRUNE,
+  KID_PRUNE_SLOW, KID_COMPACT, KID_SEG_BOUNDS, KID_SYNC_HIST, KID_SYNC_FILL, KID_BLAME_COUNT,
+  KID_SELFBLAME_SLOW, KID_BLAME_FILL, KID_BLAME_TOTAL, KID_LINES, KID_SLICE, KID_COUNT_
+};
+const char* const kKernelNames[] = {
+  "bin_samples", "bin_finalize", "unit_counts", "scan", "block_walk", "reach_fast",
+  "reach_slow", "link_count", "link_fill", "segsort_unique", "link_emit", "sync_trace",
+  "sync_trace_slow", "key_hist", "key_scatter", "sync_emit", "edge_totals", "prune_edges",
+  "prune_slow", "compact", "seg_bounds", "sync_hist", "sync_fill", "blame_count",
+  "selfblame_slow", "blame_fill", "blame_total", "lines", "slice",
+};
+
+struct TraceScope {
+  LeoTrace* t; cudaStream_t st; int slot = -1;
+  TraceScope(LeoTrace* tr, int id, cudaStream_t s) : t(tr), st(s) {
+    if (!t || (t->only_kernel >= 0 && t->only_kernel != id)) return;
+    int x = t->count++;
+    if (x >= t->capacity) return;
+    slot = x;
+    t->kernel_id[x] = id;
+    cudaEventRecord((cudaEvent_t)t->ev_begin[x], st);
+  }
+  ~TraceScope() { if (slot >= 0) cudaEventRecord((cudaEvent_t)t->ev_end[slot], st); }
+};
+#define TRACED(id, ...) do { TraceScope _ts(tr, id, st); __VA_ARGS__; } while (0)
 
 int g_num_sms = 0;
 int num_sms() {
@@ -68,6 +98,7 @@ int check_kernel(const LeoKernel* k) {
 // build_graph
 int build_graph_impl(const LeoKernel* kk, const LeoCaps* caps, LeoEdges* out, LeoDiags* diags,
                      uint32_t* status, cudaStream_t st) {
+  LeoTrace* tr = caps ? caps->trace : nullptr;
   KView k = make_kview(kk);
   const int N = k.N, B = k.B, U = k.U;
   const int64_t NU = kk->n_use_units, ND = kk->n_def_units;
@@ -111,39 +142,39 @@ int build_graph_impl(const LeoKernel* kk, const LeoCaps* caps, LeoEdges* out, Le
   cudaMemsetAsync(pcur, 0, (size_t)std::max(N, 1) * 4, st);
 
   const int T = 256;
-  k_unit_counts<<<grid_for(N, T), T, 0, st>>>(k, ucnt, dcnt);
-  scan_exclusive(ucnt, use_ptr, nullptr, N, scan_tmp, nullptr, st);
-  scan_exclusive(dcnt, def_ptr, nullptr, N, scan_tmp, nullptr, st);
+  TRACED(KID_UNIT_COUNTS, k_unit_counts<<<grid_for(N, T), T, 0, st>>>(k, ucnt, dcnt));
+  TRACED(KID_SCAN, scan_exclusive(ucnt, use_ptr, nullptr, N, scan_tmp, nullptr, st));
+  TRACED(KID_SCAN, scan_exclusive(dcnt, def_ptr, nullptr, N, scan_tmp, nullptr, st));
 
   WalkArgs wa{use_ptr, def_ptr, ev_res, q_block, q_unit, q_list, &ctr[0], bdef, bdef_len, gtab};
   size_t smem = smem_tab ? (size_t)wpc * 2 * U * 4 : 0;
   if (smem > 48 * 1024) cudaFuncSetAttribute(k_block_walk, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-  if (B > 0) k_block_walk<<<std::max(1, walk_ctas), wpc * 32, smem, st>>>(k, wa, wpc);
+  if (B > 0) TRACED(KID_BLOCK_WALK, k_block_walk<<<std::max(1, walk_ctas), wpc * 32, smem, st>>>(k, wa, wpc));
 
   ReachArgs ra{def_ptr, bdef, bdef_len, q_block, q_unit, q_off, q_len, qres, cap_qres, &ctr[1],
                slow_list, &ctr[2], cap_slow, status};
-  k_reach_fast<<<grid_for(NU, 128), 128, 0, st>>>(k, ra, q_list, &ctr[0]);
-  k_reach_slow<<<(RW + 63) / 64, 64, 0, st>>>(k, ra, reach_scr, RW);
+  TRACED(KID_REACH_FAST, k_reach_fast<<<grid_for(NU, 128), 128, 0, st>>>(k, ra, q_list, &ctr[0]));
+  TRACED(KID_REACH_SLOW, k_reach_slow<<<(RW + 63) / 64, 64, 0, st>>>(k, ra, reach_scr, RW));
 
   LinkArgs la{use_ptr, ev_res, q_off, q_len, qres, cand_cnt, cand_off, cand, cap_cand, *diags, status};
-  k_link<0><<<grid_for(N, T), T, 0, st>>>(k, la);
-  scan_exclusive(cand_cnt, cand_off, nullptr, N, scan_tmp, nullptr, st);
-  k_link<1><<<grid_for(N, T), T, 0, st>>>(k, la);
-  segsort_unique_u64<<<grid_for(N, 128), 128, 0, st>>>(cand, cand_off, cand_cnt, nullptr, N, uniq);
-  scan_exclusive(uniq, eoff, nullptr, N, scan_tmp, &ctr[5], st);
-  k_link_emit<<<grid_for(N, T), T, 0, st>>>(k, cand_off, cand, uniq, eoff, *out, status);
+  TRACED(KID_LINK_COUNT, k_link<0><<<grid_for(N, T), T, 0, st>>>(k, la));
+  TRACED(KID_SCAN, scan_exclusive(cand_cnt, cand_off, nullptr, N, scan_tmp, nullptr, st));
+  TRACED(KID_LINK_FILL, k_link<1><<<grid_for(N, T), T, 0, st>>>(k, la));
+  TRACED(KID_SEGSORT, segsort_unique_u64<<<grid_for(N, 128), 128, 0, st>>>(cand, cand_off, cand_cnt, nullptr, N, uniq));
+  TRACED(KID_SCAN, scan_exclusive(uniq, eoff, nullptr, N, scan_tmp, &ctr[5], st));
+  TRACED(KID_LINK_EMIT, k_link_emit<<<grid_for(N, T), T, 0, st>>>(k, cand_off, cand, uniq, eoff, *out, status));
 
   SyncArgs sa{skeys, cap_sync, &ctr[3], slow2, &ctr[4], cap_slow, *diags, status};
-  k_sync<false><<<grid_for(N, 128), 128, 0, st>>>(k, sa, nullptr, 0);
-  k_sync<true><<<1, SW, 0, st>>>(k, sa, (int32_t*)sync_scr, SW);
-  k_key_hist<<<grid_for(cap_sync, T), T, 0, st>>>(skeys, &ctr[3], cap_sync, pcnt);
-  scan_exclusive(pcnt, poff, nullptr, N, scan_tmp, nullptr, st);
-  k_key_scatter<<<grid_for(cap_sync, T), T, 0, st>>>(skeys, &ctr[3], cap_sync, poff, pcur, ssorted);
-  segsort_unique_u64<<<grid_for(N, 128), 128, 0, st>>>(ssorted, poff, pcnt, nullptr, N, puniq);
-  scan_exclusive(puniq, puoff, nullptr, N, scan_tmp, &ctr[6], st);
+  TRACED(KID_SYNC, k_sync<false><<<grid_for(N, 128), 128, 0, st>>>(k, sa, nullptr, 0));
+  TRACED(KID_SYNC_SLOW, k_sync<true><<<1, SW, 0, st>>>(k, sa, (int32_t*)sync_scr, SW));
+  TRACED(KID_KEY_HIST, k_key_hist<<<grid_for(cap_sync, T), T, 0, st>>>(skeys, &ctr[3], cap_sync, pcnt));
+  TRACED(KID_SCAN, scan_exclusive(pcnt, poff, nullptr, N, scan_tmp, nullptr, st));
+  TRACED(KID_KEY_SCATTER, k_key_scatter<<<grid_for(cap_sync, T), T, 0, st>>>(skeys, &ctr[3], cap_sync, poff, pcur, ssorted));
+  TRACED(KID_SEGSORT, segsort_unique_u64<<<grid_for(N, 128), 128, 0, st>>>(ssorted, poff, pcnt, nullptr, N, puniq));
+  TRACED(KID_SCAN, scan_exclusive(puniq, puoff, nullptr, N, scan_tmp, &ctr[6], st));
   const int kind = k.dialect == LEO_AMD ? LEO_EK_MEM_WAITCNT : k.dialect == LEO_NVIDIA ? LEO_EK_MEM_BARRIER : LEO_EK_MEM_SWSB;
-  k_sync_emit<<<grid_for(N, T), T, 0, st>>>(N, kind, ssorted, poff, puniq, puoff, &ctr[5], *out, status);
-  k_edge_totals<<<1, 1, 0, st>>>(&ctr[5], &ctr[6], *out, status);
+  TRACED(KID_SYNC_EMIT, k_sync_emit<<<grid_for(N, T), T, 0, st>>>(N, kind, ssorted, poff, puniq, puoff, &ctr[5], *out, status));
+  TRACED(KID_EDGE_TOTALS, k_edge_totals<<<1, 1, 0, st>>>(&ctr[5], &ctr[6], *out, status));
   ar.release();
   LEO_CUDA_CHECK(cudaGetLastError());
   return 0;
@@ -154,6 +185,7 @@ int build_graph_impl(const LeoKernel* kk, const LeoCaps* caps, LeoEdges* out, Le
 int prune_impl(const LeoKernel* kk, const LeoProfile* pp, const LeoConfig* cfg, const LeoEdges* in,
                LeoEdges* out, LeoPaths* paths, LeoDiags* diags, const LeoCaps* caps, uint32_t* status,
                cudaStream_t st) {
+  LeoTrace* tr = caps ? caps->trace : nullptr;
   KView k = make_kview(kk);
   PView p = make_pview(pp);
   const int64_t cap_in = in->capacity;
@@ -173,10 +205,10 @@ int prune_impl(const LeoKernel* kk, const LeoProfile* pp, const LeoConfig* cfg, 
   cudaMemsetAsync(paths->count, 0, sizeof(int32_t), st);
   PruneArgs a{*cfg, in->prod, in->cons, in->meta, in->count, (int32_t)cap_in, keep, npaths, pfirst, dist,
               *paths, slow_list, &ctr[0], cap_slow, *diags, status};
-  k_prune_edges<<<grid_for(cap_in, 128, num_sms() * 16), 128, 0, st>>>(k, p, a);
-  k_prune_slow<<<1, PW, 0, st>>>(k, p, a, slow_scr, PW);
-  scan_exclusive(keep, pos, in->count, cap_in, scan_tmp, nullptr, st);
-  k_compact<<<grid_for(cap_in, 256), 256, 0, st>>>(a, pos, in->n_regular, *out, status);
+  TRACED(KID_PRUNE, k_prune_edges<<<grid_for(cap_in, 128, num_sms() * 16), 128, 0, st>>>(k, p, a));
+  TRACED(KID_PRUNE_SLOW, k_prune_slow<<<1, PW, 0, st>>>(k, p, a, slow_scr, PW));
+  TRACED(KID_SCAN, scan_exclusive(keep, pos, in->count, cap_in, scan_tmp, nullptr, st));
+  TRACED(KID_COMPACT, k_compact<<<grid_for(cap_in, 256), 256, 0, st>>>(a, pos, in->n_regular, *out, status));
   ar.release();
   LEO_CUDA_CHECK(cudaGetLastError());
   return 0;
@@ -193,18 +225,18 @@ void want_incoming(Arena& ar, IncomingBufs& b, int N, int64_t cap) {
   ar.want(&b.scur, N); ar.want(&b.sidx, cap); ar.want(&b.tmp, scan_scratch_ints(std::max(N, 1)) + 64);
   ar.want(&b.uniq, N);
 }
-Incoming build_incoming(IncomingBufs& b, int N, const LeoEdges* e, bool with_sync, cudaStream_t st) {
+Incoming build_incoming(IncomingBufs& b, int N, const LeoEdges* e, bool with_sync, LeoTrace* tr, cudaStream_t st) {
   const size_t nb = (size_t)std::max(N, 1) * 4;
   cudaMemsetAsync(b.rbeg, 0, nb, st);
   cudaMemsetAsync(b.rend, 0, nb, st);
   cudaMemsetAsync(b.scnt, 0, nb, st);
   cudaMemsetAsync(b.scur, 0, nb, st);
-  k_seg_bounds<<<grid_for(e->capacity, 256), 256, 0, st>>>(e->cons, e->n_regular, b.rbeg, b.rend);
+  TRACED(KID_SEG_BOUNDS, k_seg_bounds<<<grid_for(e->capacity, 256), 256, 0, st>>>(e->cons, e->n_regular, b.rbeg, b.rend));
   if (with_sync) {
-    k_sync_hist<<<grid_for(e->capacity, 256), 256, 0, st>>>(e->cons, e->n_regular, e->count, b.scnt);
-    scan_exclusive(b.scnt, b.soff, nullptr, N, b.tmp, nullptr, st);
-    k_sync_fill<<<grid_for(e->capacity, 256), 256, 0, st>>>(e->cons, e->n_regular, e->count, b.soff, b.scur, b.sidx);
-    segsort_unique_u64<<<grid_for(N, 128), 128, 0, st>>>(b.sidx, b.soff, b.scnt, nullptr, N, b.uniq);
+    TRACED(KID_SYNC_HIST, k_sync_hist<<<grid_for(e->capacity, 256), 256, 0, st>>>(e->cons, e->n_regular, e->count, b.scnt));
+    TRACED(KID_SCAN, scan_exclusive(b.scnt, b.soff, nullptr, N, b.tmp, nullptr, st));
+    TRACED(KID_SYNC_FILL, k_sync_fill<<<grid_for(e->capacity, 256), 256, 0, st>>>(e->cons, e->n_regular, e->count, b.soff, b.scur, b.sidx));
+    TRACED(KID_SEGSORT, segsort_unique_u64<<<grid_for(N, 128), 128, 0, st>>>(b.sidx, b.soff, b.scnt, nullptr, N, b.uniq));
   } else {
     cudaMemsetAsync(b.soff, 0, (size_t)(N + 1) * 4, st);
   }
@@ -212,7 +244,7 @@ Incoming build_incoming(IncomingBufs& b, int N, const LeoEdges* e, bool with_syn
 }
 
 int slice_impl(const LeoKernel* kk, const LeoProfile* pp, const LeoEdges* pruned, const Incoming& inc,
-               uint32_t* bitmap, int32_t* level, cudaStream_t st) {
+               uint32_t* bitmap, int32_t* level, LeoTrace* tr, cudaStream_t st) {
   const int N = kk->n_instr;
   Arena ar{st};
   int32_t *fa, *fb, *counts;
@@ -225,7 +257,9 @@ int slice_impl(const LeoKernel* kk, const LeoProfile* pp, const LeoEdges* pruned
   int grid = std::max(1, std::min(per_sm, 4)) * num_sms();
   int n = N;
   void* args[] = {&n, &a};
-  LEO_CUDA_CHECK(cudaLaunchCooperativeKernel((void*)k_slice, grid, 256, args, 0, st));
+  cudaError_t le;
+  TRACED(KID_SLICE, le = cudaLaunchCooperativeKernel((void*)k_slice, grid, 256, args, 0, st));
+  LEO_CUDA_CHECK(le);
   ar.release();
   return 0;
 }
@@ -234,6 +268,7 @@ int blame_impl(const LeoKernel* kk, const LeoProfile* pp, const LeoEdges* pruned
                const LeoEdges* base, const Incoming& inc, const int32_t* line_id, int32_t n_lines,
                LeoBlame* out, double* line_blame, double* line_stall, const LeoCaps* caps,
                uint32_t* status, cudaStream_t st) {
+  LeoTrace* tr = caps ? caps->trace : nullptr;
   KView k = make_kview(kk);
   const int N = k.N;
   PView p = make_pview(pp);
@@ -249,19 +284,19 @@ int blame_impl(const LeoKernel* kk, const LeoProfile* pp, const LeoEdges* pruned
   ar.want(&slow_scr, (int64_t)BW * 2 * (N + 1)); ar.want(&jtotal, N); ar.want(&jnsum, N);
   LEO_CUDA_CHECK(ar.commit());
   cudaMemsetAsync(ctr, 0, 16, st);
-  Incoming binc = build_incoming(bb, N, base, false, st);   // RAW edges only
+  Incoming binc = build_incoming(bb, N, base, false, tr, st);   // RAW edges only
   BlameArgs a{p, pruned->prod, pruned->meta, paths->dist, inc, binc.rbeg, binc.rend, base->prod, base->meta,
               ecount, self_sub, jtotal, jnsum, eoff, *out, slow_list, &ctr[0], cap_slow, status};
-  k_blame<0><<<grid_for(N, 128), 128, 0, st>>>(k, a);
-  k_selfblame_slow<<<1, BW, 0, st>>>(k, a, slow_scr, BW);
-  scan_exclusive(ecount, eoff, nullptr, N, scan_tmp, nullptr, st);
-  k_blame<1><<<grid_for(N, 128), 128, 0, st>>>(k, a);
-  k_blame_count<<<1, 1, 0, st>>>(eoff, N, *out);
+  TRACED(KID_BLAME_COUNT, k_blame<0><<<grid_for(N, 128), 128, 0, st>>>(k, a));
+  TRACED(KID_SELFBLAME_SLOW, k_selfblame_slow<<<1, BW, 0, st>>>(k, a, slow_scr, BW));
+  TRACED(KID_SCAN, scan_exclusive(ecount, eoff, nullptr, N, scan_tmp, nullptr, st));
+  TRACED(KID_BLAME_FILL, k_blame<1><<<grid_for(N, 128), 128, 0, st>>>(k, a));
+  TRACED(KID_BLAME_TOTAL, k_blame_count<<<1, 1, 0, st>>>(eoff, N, *out));
   if (line_id && line_blame && line_stall && n_lines > 0) {
     cudaMemsetAsync(line_blame, 0, (size_t)n_lines * 8, st);
     cudaMemsetAsync(line_stall, 0, (size_t)n_lines * 8, st);
-    k_lines<<<grid_for(std::max<int64_t>(out->capacity, N), 256), 256, 0, st>>>(k, p, pruned->prod, *out,
-                                                                               line_id, line_blame, line_stall);
+    TRACED(KID_LINES, k_lines<<<grid_for(std::max<int64_t>(out->capacity, N), 256), 256, 0, st>>>(k, p, pruned->prod, *out,
+                                                                               line_id, line_blame, line_stall));
   }
   ar.release();
   LEO_CUDA_CHECK(cudaGetLastError());
@@ -275,21 +310,44 @@ extern "C" {
 
 int leo_abi_version(void) { return LEO_ABI_VERSION; }
 
-int leo_bin_samples(const LeoSamples* s, int32_t n_instr, int32_t* lat, int32_t* cls_cnt, void* stream) {
-  if (!s || n_instr < 0) return -1;
-  cudaStream_t st = (cudaStream_t)stream;
+static int bin_impl(const LeoSamples* s, int32_t n_instr, int32_t* lat, int32_t* cls_cnt, LeoTrace* tr,
+                    cudaStream_t st) {
   cudaMemsetAsync(cls_cnt, 0, (size_t)std::max(n_instr, 1) * 32, st);
   uint32_t* status = nullptr;
   LEO_CUDA_CHECK(cudaMallocAsync((void**)&status, 4, st));
   cudaMemsetAsync(status, 0, 4, st);
   if (s->n_samples > 0)
-    k_bin_samples<<<grid_for(s->n_samples / 4 + 1, 256, num_sms() * 8), 256, 0, st>>>(
-        s->n_samples, s->pc, s->cat, s->cat_to_cs, n_instr, cls_cnt, status);
-  k_bin_finalize<<<grid_for(n_instr, 256), 256, 0, st>>>(n_instr, cls_cnt, lat);
+    TRACED(KID_BIN, k_bin_samples<<<grid_for(s->n_samples / 4 + 1, 256, num_sms() * 8), 256, 0, st>>>(
+        s->n_samples, s->pc, s->cat, s->cat_to_cs, n_instr, cls_cnt, status));
+  TRACED(KID_BIN_FINALIZE, k_bin_finalize<<<grid_for(n_instr, 256), 256, 0, st>>>(n_instr, cls_cnt, lat));
   cudaFreeAsync(status, st);
   LEO_CUDA_CHECK(cudaGetLastError());
   return 0;
 }
+
+int leo_bin_samples(const LeoSamples* s, int32_t n_instr, int32_t* lat, int32_t* cls_cnt, void* stream) {
+  if (!s || n_instr < 0) return -1;
+  return bin_impl(s, n_instr, lat, cls_cnt, nullptr, (cudaStream_t)stream);
+}
+
+int leo_events_create(int32_t n, void** events) {
+  for (int i = 0; i < n; i++) {
+    cudaEvent_t e;
+    LEO_CUDA_CHECK(cudaEventCreate(&e));
+    events[i] = (void*)e;
+  }
+  return 0;
+}
+int leo_events_elapsed(int32_t n, void* const* begin, void* const* end, float* ms) {
+  for (int i = 0; i < n; i++) LEO_CUDA_CHECK(cudaEventElapsedTime(&ms[i], (cudaEvent_t)begin[i], (cudaEvent_t)end[i]));
+  return 0;
+}
+int leo_events_destroy(int32_t n, void** events) {
+  for (int i = 0; i < n; i++) cudaEventDestroy((cudaEvent_t)events[i]);
+  return 0;
+}
+
+const char* leo_kernel_name(int id) { return (id >= 0 && id < KID_COUNT_) ? kKernelNames[id] : nullptr; }
 
 int leo_build_graph(const LeoKernel* k, const LeoCaps* caps, LeoEdges* out, LeoDiags* diags,
                     uint32_t* status, void* stream) {
@@ -312,8 +370,8 @@ int leo_slice(const LeoKernel* k, const LeoProfile* p, const LeoEdges* pruned, u
   IncomingBufs ib;
   want_incoming(ar, ib, k->n_instr, pruned->capacity);
   LEO_CUDA_CHECK(ar.commit());
-  Incoming inc = build_incoming(ib, k->n_instr, pruned, true, st);
-  int r = slice_impl(k, p, pruned, inc, bitmap, level, st);
+  Incoming inc = build_incoming(ib, k->n_instr, pruned, true, nullptr, st);
+  int r = slice_impl(k, p, pruned, inc, bitmap, level, nullptr, st);
   ar.release();
   return r;
 }
@@ -327,7 +385,7 @@ int leo_blame(const LeoKernel* k, const LeoProfile* p, const LeoEdges* pruned, c
   IncomingBufs ib;
   want_incoming(ar, ib, k->n_instr, pruned->capacity);
   LEO_CUDA_CHECK(ar.commit());
-  Incoming inc = build_incoming(ib, k->n_instr, pruned, true, st);
+  Incoming inc = build_incoming(ib, k->n_instr, pruned, true, nullptr, st);
   int r = blame_impl(k, p, pruned, paths, base, inc, line_id, n_lines, out, line_blame, line_stall, nullptr,
                      status, st);
   ar.release();
@@ -342,7 +400,7 @@ int leo_analyze(const LeoKernel* k, const LeoProfile* p, const LeoSamples* sampl
   if (!cfg) return -3;
   cudaStream_t st = (cudaStream_t)stream;
   if (samples) {
-    int r = leo_bin_samples(samples, k->n_instr, (int32_t*)p->lat, (int32_t*)p->cls_cnt, stream);
+    int r = bin_impl(samples, k->n_instr, (int32_t*)p->lat, (int32_t*)p->cls_cnt, caps ? caps->trace : nullptr, st);
     if (r) return r;
   }
   int r = build_graph_impl(k, caps, base, diags, status, st);
@@ -353,9 +411,10 @@ int leo_analyze(const LeoKernel* k, const LeoProfile* p, const LeoSamples* sampl
   IncomingBufs ib;
   want_incoming(ar, ib, k->n_instr, pruned->capacity);
   LEO_CUDA_CHECK(ar.commit());
-  Incoming inc = build_incoming(ib, k->n_instr, pruned, true, st);
+  LeoTrace* tr = caps ? caps->trace : nullptr;
+  Incoming inc = build_incoming(ib, k->n_instr, pruned, true, tr, st);
   if (slice_level && slice_bitmap) {
-    r = slice_impl(k, p, pruned, inc, slice_bitmap, slice_level, st);
+    r = slice_impl(k, p, pruned, inc, slice_bitmap, slice_level, tr, st);
     if (r) { ar.release(); return r; }
   }
   r = blame_impl(k, p, pruned, paths, base, inc, line_id, n_lines, blame, line_blame, line_stall, caps, status, st);

@@ -109,6 +109,7 @@ class Analyzer:
     """Owns output buffers for one kernel shape; runs the fused pipeline."""
 
     def __init__(self, dk: DeviceKernel, device="cuda", caps: Caps | None = None):
+        self.tracer = None
         self.dk = dk
         self.device = torch.device(device)
         n = dk.n_instr
@@ -154,8 +155,13 @@ class Analyzer:
         s = self.caps.scratch_scale
         nu, n = self.n_use_units, self.dk.n_instr
         self.s_caps = abi.LeoCaps((4 * nu + 1024) * s, (6 * nu + 1024) * s, (2 * n + 1024) * s,
-                                  (n // 4 + 1024) * s)
+                                  (n // 4 + 1024) * s, None)
+        self.set_tracer(self.tracer)
         self.status_ptr = at(C_STATUS)
+
+    def set_tracer(self, tracer: "Tracer | None"):
+        self.tracer = tracer
+        self.s_caps.trace = C.pointer(tracer.struct) if tracer is not None else None
 
     # -- launch ------------------------------------------------------------
     def launch(self, dp: DeviceProfile, cfg: abi.LeoConfig, samples: DeviceSamples | None = None,
@@ -252,3 +258,56 @@ def analyze_soa(ks, prof, cfg: abi.LeoConfig | None = None, samples=None, device
         r["lat"] = dp.lat.cpu().numpy()
         r["cls_cnt"] = dp.cls_cnt.cpu().numpy().reshape(-1, 8)
     return r
+
+
+class Tracer:
+    """Per-kernel device time of the fused pipeline (LeoTrace): CUDA events
+    recorded by the library on the launching stream around each kernel (or
+    only around `only_kernel`)."""
+
+    def __init__(self, capacity: int = 4096, only_kernel: int = -1):
+        L = lib()
+        self.capacity = capacity
+        self.begin = (C.c_void_p * capacity)()
+        self.end = (C.c_void_p * capacity)()
+        self.ids = (C.c_int32 * capacity)()
+        check(L.leo_events_create(capacity, self.begin), "leo_events_create")
+        check(L.leo_events_create(capacity, self.end), "leo_events_create")
+        self.struct = abi.LeoTrace(capacity, 0, only_kernel, 0, C.cast(self.begin, C.c_void_p),
+                                   C.cast(self.end, C.c_void_p), C.cast(self.ids, C.c_void_p))
+
+    def reset(self, only_kernel: int | None = None):
+        self.struct.count = 0
+        if only_kernel is not None:
+            self.struct.only_kernel = only_kernel
+
+    def records(self) -> list[tuple[str, float]]:
+        """(kernel name, ms) per recorded slot; call after synchronising."""
+        L = lib()
+        n = min(self.struct.count, self.capacity)
+        ms = (C.c_float * max(n, 1))()
+        check(L.leo_events_elapsed(n, self.begin, self.end, ms), "leo_events_elapsed")
+        return [(L.leo_kernel_name(self.ids[i]).decode(), float(ms[i])) for i in range(n)]
+
+    def summary(self) -> dict[str, float]:
+        out: dict[str, float] = {}
+        for name, ms in self.records():
+            out[name] = out.get(name, 0.0) + ms
+        return out
+
+    def close(self):
+        L = lib()
+        L.leo_events_destroy(self.capacity, self.begin)
+        L.leo_events_destroy(self.capacity, self.end)
+
+
+def kernel_id(name: str) -> int:
+    L = lib()
+    i = 0
+    while True:
+        n = L.leo_kernel_name(i)
+        if n is None:
+            raise KeyError(name)
+        if n.decode() == name:
+            return i
+        i += 1
