@@ -61,6 +61,124 @@ __global__ void k_bin_samples(int64_t S, const int32_t* __restrict__ pc, const u
   }
 }
 
+// ---- stage 0, bucketed: samples are partitioned by pc / R into NB buckets
+// (R instructions x 8 classes of u32 counters fit in shared memory), packed to
+// u16 keys ((pc mod R) * 8 + class), then each (bucket, slice) is counted in
+// shared memory with warp-aggregated atomics and merged into cls_cnt.  Hot
+// buckets (Zipf-heavy PCs) are split over many CTAs, so no counter sees more
+// than one global atomic per CTA.
+constexpr int kBinR = 2048;          // instructions per bucket (64 KiB of counters)
+constexpr int kBinMaxBuckets = 4096;
+constexpr int kBinSlice = 1 << 16;   // samples per counting CTA
+
+__global__ void k_bin_hist(int64_t S, const int32_t* __restrict__ pc, int N, int nb,
+                           int32_t* __restrict__ bucket_cnt, uint32_t* status) {
+  __shared__ int32_t h[kBinMaxBuckets];
+  for (int x = threadIdx.x; x < nb; x += blockDim.x) h[x] = 0;
+  __syncthreads();
+  const int64_t nvec = S / 4;
+  const int4* pc4 = reinterpret_cast<const int4*>(pc);
+  for (int64_t v = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; v < nvec; v += (int64_t)gridDim.x * blockDim.x) {
+    int4 p = pc4[v];
+    int ps[4] = {p.x, p.y, p.z, p.w};
+#pragma unroll
+    for (int t = 0; t < 4; t++) {
+      int j = ps[t];
+      if (j < 0 || j >= N) { atomicOr(status, (uint32_t)LEO_ST_BAD_INPUT); continue; }
+      atomicAdd(&h[j / kBinR], 1);
+    }
+  }
+  for (int64_t s = nvec * 4 + blockIdx.x * (int64_t)blockDim.x + threadIdx.x; s < S; s += (int64_t)gridDim.x * blockDim.x) {
+    int j = pc[s];
+    if (j < 0 || j >= N) { atomicOr(status, (uint32_t)LEO_ST_BAD_INPUT); continue; }
+    atomicAdd(&h[j / kBinR], 1);
+  }
+  __syncthreads();
+  for (int x = threadIdx.x; x < nb; x += blockDim.x)
+    if (h[x]) atomicAdd(&bucket_cnt[x], h[x]);
+}
+
+// single CTA: bucket offsets, per-bucket cursors and slice offsets
+__global__ void k_bin_plan(int nb, const int32_t* __restrict__ bucket_cnt, int32_t* __restrict__ bucket_off,
+                           int32_t* __restrict__ cursor, int32_t* __restrict__ slice_off) {
+  __shared__ int sw[33];
+  int carry = 0, scarry = 0;
+  for (int base = 0; base < nb; base += blockDim.x) {
+    int i = base + threadIdx.x;
+    int c = i < nb ? bucket_cnt[i] : 0;
+    int ns = (c + kBinSlice - 1) / kBinSlice;
+    int tot, stot;
+    int ex = block_excl_scan(c, sw, &tot);
+    int sex = block_excl_scan(ns, sw, &stot);
+    if (i < nb) { bucket_off[i] = carry + ex; cursor[i] = carry + ex; slice_off[i] = scarry + sex; }
+    carry += tot; scarry += stot;
+  }
+  if (threadIdx.x == 0) { bucket_off[nb] = carry; slice_off[nb] = scarry; }
+}
+
+__global__ void k_bin_scatter(int64_t S, const int32_t* __restrict__ pc, const uint8_t* __restrict__ cat,
+                              const uint8_t* __restrict__ lut, int N, int nb, int32_t* __restrict__ cursor,
+                              uint16_t* __restrict__ keys) {
+  __shared__ int32_t h[kBinMaxBuckets];
+  __shared__ uint8_t slut[256];
+  for (int x = threadIdx.x; x < nb; x += blockDim.x) h[x] = 0;
+  for (int x = threadIdx.x; x < 256; x += blockDim.x) slut[x] = lut[x];
+  __syncthreads();
+  // this CTA's contiguous chunk
+  const int64_t per = (S + gridDim.x - 1) / gridDim.x;
+  const int64_t s0 = (int64_t)blockIdx.x * per, s1 = min(S, s0 + per);
+  for (int64_t s = s0 + threadIdx.x; s < s1; s += blockDim.x) {
+    int j = pc[s];
+    if (j >= 0 && j < N) atomicAdd(&h[j / kBinR], 1);
+  }
+  __syncthreads();
+  for (int x = threadIdx.x; x < nb; x += blockDim.x) {
+    int c = h[x];
+    h[x] = c ? atomicAdd(&cursor[x], c) : 0;        // this CTA's base in bucket x
+  }
+  __syncthreads();
+  for (int64_t s = s0 + threadIdx.x; s < s1; s += blockDim.x) {
+    int j = pc[s];
+    if (j < 0 || j >= N) continue;
+    int b = j / kBinR;
+    int pos = atomicAdd(&h[b], 1);
+    keys[pos] = (uint16_t)(((j - b * kBinR) << 3) | slut[cat[s]]);
+  }
+}
+
+__global__ void __launch_bounds__(512) k_bin_count(int N, int nb, const int32_t* __restrict__ bucket_off,
+                                                   const int32_t* __restrict__ slice_off,
+                                                   const uint16_t* __restrict__ keys,
+                                                   int32_t* __restrict__ cls_cnt) {
+  extern __shared__ int32_t cnt[];              // kBinR * 8
+  const int total_slices = slice_off[nb];
+  for (int sl = blockIdx.x; sl < total_slices; sl += gridDim.x) {
+    // bucket of this slice: largest b with slice_off[b] <= sl
+    int lo = 0, hi = nb - 1;
+    while (lo < hi) {
+      int mid = (lo + hi + 1) >> 1;
+      if (slice_off[mid] <= sl) lo = mid; else hi = mid - 1;
+    }
+    const int b = lo;
+    const int k = sl - slice_off[b];
+    const int64_t e0 = (int64_t)bucket_off[b] + (int64_t)k * kBinSlice;
+    const int64_t e1 = min((int64_t)bucket_off[b + 1], e0 + kBinSlice);
+    for (int x = threadIdx.x; x < kBinR * 8; x += blockDim.x) cnt[x] = 0;
+    __syncthreads();
+    for (int64_t e = e0 + threadIdx.x; e - threadIdx.x < e1; e += blockDim.x) {
+      int key = e < e1 ? (int)keys[e] : -1;
+      unsigned grp = __match_any_sync(0xffffffffu, key);
+      if (key >= 0 && (__ffs(grp) - 1) == (int)(threadIdx.x & 31)) atomicAdd(&cnt[key], __popc(grp));
+    }
+    __syncthreads();
+    const int base = b * kBinR * 8;
+    const int lim = min(kBinR * 8, (N - b * kBinR) * 8);
+    for (int x = threadIdx.x; x < lim; x += blockDim.x)
+      if (cnt[x]) atomicAdd(&cls_cnt[base + x], cnt[x]);
+    __syncthreads();
+  }
+}
+
 __global__ void k_bin_finalize(int N, const int32_t* __restrict__ cls_cnt, int32_t* __restrict__ lat) {
   for (int j = blockIdx.x * blockDim.x + threadIdx.x; j < N; j += gridDim.x * blockDim.x) {
     const int4* row = reinterpret_cast<const int4*>(cls_cnt + (size_t)j * 8);

@@ -58,8 +58,7 @@ struct WalkArgs {
   int32_t* q_unit;           // [use units]
   int32_t* q_list;           // [use units]
   int32_t* q_count;          // scalar
-  uint64_t* bdef;            // [def units] (unit << 32 | last def) per block, sorted by unit
-  int32_t* bdef_len;         // [B]
+  int32_t* ldtab;            // [B * U] last def of unit u in block b, -1 if none
   int32_t* gtab;             // global per-warp tables (when U too large for smem) or null
 };
 
@@ -121,40 +120,32 @@ __global__ void k_block_walk(KView k, WalkArgs a, int warps_per_cta) {
       }
       __syncwarp();
     }
-    // block summary: every unit whose last def lies in this block, by unit
-    int cnt = 0;
-    uint64_t* out = a.bdef + a.def_ptr[first];
-    for (int base = 0; base < U; base += 32) {
-      int u = base + lane;
-      int ld = u < U ? last[u] : -1;
-      bool q = ld >= first;
-      unsigned m = __ballot_sync(0xffffffffu, q);
-      if (q) out[cnt + __popc(m & ((1u << lane) - 1))] = ((uint64_t)u << 32) | (uint32_t)ld;
-      cnt += __popc(m);
+    // dense row of the block's last definitions (block_defs depgraph.py:143-149)
+    int32_t* row = a.ldtab + (size_t)b * U;
+    for (int u = lane; u < U; u += 32) {
+      int ld = last[u];
+      row[u] = ld >= first ? ld : -1;
     }
-    if (lane == 0) a.bdef_len[b] = cnt;
     __syncwarp();
   }
 }
 
-// last definition of unit u in block p, -1 if p is transparent to u
-LEO_DEV int lastdef_in_block(const KView& k, const int32_t* def_ptr, const uint64_t* bdef,
-                             const int32_t* bdef_len, int p, int u) {
-  const uint64_t* s = bdef + def_ptr[k.blk_first[p]];
-  int lo = 0, hi = bdef_len[p] - 1;
-  while (lo <= hi) {
-    int mid = (lo + hi) >> 1;
-    int mu = (int)(s[mid] >> 32);
-    if (mu == u) return (int)(uint32_t)s[mid];
-    if (mu < u) lo = mid + 1; else hi = mid - 1;
+// Fallthrough-run heads: runhead[b] = first block of the maximal run ending at
+// b in which every block but the first has exactly one predecessor, the
+// previous block.  A backward search entering the run at y can only leave it
+// through preds(runhead[y]), so the run is resolved with independent loads.
+__global__ void k_run_heads(KView k, int32_t* __restrict__ head) {
+  for (int b = blockIdx.x * blockDim.x + threadIdx.x; b < k.B; b += gridDim.x * blockDim.x) {
+    int x = b;
+    while (x > 0 && k.pred_ptr[x + 1] - k.pred_ptr[x] == 1 && k.pred[k.pred_ptr[x]] == x - 1) x--;
+    head[b] = x;
   }
-  return -1;
 }
 
 struct ReachArgs {
-  const int32_t* def_ptr;
-  const uint64_t* bdef;
-  const int32_t* bdef_len;
+  const int32_t* ldtab;      // [B * U]
+  const int32_t* runhead;    // [B]
+  int32_t U;
   const int32_t* q_block;
   const int32_t* q_unit;
   int32_t* q_off;            // [use units] result offset per query slot
@@ -167,6 +158,25 @@ struct ReachArgs {
   int64_t slow_cap;
   uint32_t* status;
 };
+
+// Entering block y backward: the nearest definition of u in y, y-1, ...,
+// runhead[y] (loads issued four at a time), or -1 with *head = runhead[y].
+LEO_DEV int run_lookup(const ReachArgs& a, int y, int u, int* head) {
+  const int h = a.runhead[y];
+  *head = h;
+  const size_t U = (size_t)a.U;
+  for (int x = y; x >= h; x -= 4) {
+    int v0 = a.ldtab[(size_t)x * U + u];
+    int v1 = x - 1 >= h ? a.ldtab[(size_t)(x - 1) * U + u] : -1;
+    int v2 = x - 2 >= h ? a.ldtab[(size_t)(x - 2) * U + u] : -1;
+    int v3 = x - 3 >= h ? a.ldtab[(size_t)(x - 3) * U + u] : -1;
+    if (v0 >= 0) return v0;
+    if (v1 >= 0) return v1;
+    if (v2 >= 0) return v2;
+    if (v3 >= 0) return v3;
+  }
+  return -1;
+}
 
 // Backward search for query (b, u).  visited / stack / results live in the
 // caller's buffers (registers-backed local arrays on the fast path, global
@@ -193,8 +203,8 @@ LEO_DEV bool reach_search(const KView& k, const ReachArgs& a, int b, int u, int3
     if (v) { if (sp == scap) return false; stk[sp++] = p; }
   }
   while (sp > 0) {
-    int p = stk[--sp];
-    int ld = lastdef_in_block(k, a.def_ptr, a.bdef, a.bdef_len, p, u);
+    int y = stk[--sp], p;
+    int ld = run_lookup(a, y, u, &p);
     if (ld >= 0) {
       if (nres == rcap) return false;
       res[nres++] = ld;
@@ -223,7 +233,7 @@ LEO_DEV void reach_commit(const ReachArgs& a, int e, const int32_t* res, int nre
   a.q_len[e] = nres;
 }
 
-constexpr int kReachV = 48, kReachS = 48, kReachR = 24;
+constexpr int kReachV = 16, kReachS = 16, kReachR = 8;
 
 __global__ void k_reach_fast(KView k, ReachArgs a, const int32_t* __restrict__ q_list,
                              const int32_t* q_count) {
@@ -243,10 +253,103 @@ __global__ void k_reach_fast(KView k, ReachArgs a, const int32_t* __restrict__ q
   }
 }
 
+// Tier 2: one warp per query, BFS level by level; visited set = open-addressing
+// hash in shared memory, frontiers + results in shared memory.
+constexpr int kWHash = 1024, kWFront = 512, kWRes = 128;
+constexpr int kWarpSmemInts = kWHash + 2 * kWFront + kWRes + 8;
+
+LEO_DEV bool hash_insert(int32_t* h, int key, int* count) {
+  uint32_t x = ((uint32_t)key * 2654435761u) >> 22;   // 10 bits
+  for (int probe = 0; probe < kWHash; probe++) {
+    int32_t prev = atomicCAS(&h[x], -1, key);
+    if (prev == -1) { atomicAdd(count, 1); return true; }
+    if (prev == key) return false;
+    x = (x + 1) & (kWHash - 1);
+  }
+  return false;
+}
+
+__global__ void k_reach_warp(KView k, ReachArgs a, const int32_t* __restrict__ list,
+                             const int32_t* count, int64_t list_cap, int32_t* slow_list,
+                             int32_t* slow_count) {
+  extern __shared__ int32_t smem[];
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  const int wpc = blockDim.x >> 5;
+  int32_t* base = smem + (size_t)wid * kWarpSmemInts;
+  int32_t* hash = base;
+  int32_t* fa = hash + kWHash;
+  int32_t* fb = fa + kWFront;
+  int32_t* res = fb + kWFront;
+  int32_t* c = res + kWRes;   // 0 nres, 1 ncur, 2 nnext, 3 ovf, 4 nhash
+  const int n = (int)min((int64_t)*count, list_cap);
+  for (int t = blockIdx.x * wpc + wid; t < n; t += gridDim.x * wpc) {
+    const int e = list[t];
+    const int b = a.q_block[e], u = a.q_unit[e];
+    for (int x = lane; x < kWHash; x += 32) hash[x] = -1;
+    if (lane < 8) c[lane] = 0;
+    __syncwarp();
+    for (int q = k.pred_ptr[b] + lane; q < k.pred_ptr[b + 1]; q += 32) {
+      int p = k.pred[q];
+      if (hash_insert(hash, p, &c[4])) {
+        int pos = atomicAdd(&c[1], 1);
+        if (pos < kWFront) fa[pos] = p; else c[3] = 1;
+      }
+    }
+    __syncwarp();
+    int32_t *cur = fa, *nxt = fb;
+    while (true) {
+      const int ncur = c[1];
+      if (ncur == 0 || c[3]) break;
+      for (int x = lane; x < ncur; x += 32) {
+        int p;
+        const int ld = run_lookup(a, cur[x], u, &p);
+        if (ld >= 0) {
+          int r = atomicAdd(&c[0], 1);
+          if (r < kWRes) res[r] = ld; else c[3] = 1;
+          continue;
+        }
+        for (int q = k.pred_ptr[p]; q < k.pred_ptr[p + 1]; q++) {
+          const int pp = k.pred[q];
+          if (hash_insert(hash, pp, &c[4])) {
+            int pos = atomicAdd(&c[2], 1);
+            if (pos < kWFront) nxt[pos] = pp; else c[3] = 1;
+          }
+        }
+      }
+      __syncwarp();
+      if (c[4] > kWHash / 2) c[3] = 1;          // keep probing short
+      if (lane == 0) { c[1] = c[2]; c[2] = 0; }
+      __syncwarp();
+      int32_t* tmp = cur; cur = nxt; nxt = tmp;
+    }
+    __syncwarp();
+    if (c[3]) {
+      if (lane == 0) {
+        int s = atomicAdd(slow_count, 1);
+        if (s < a.slow_cap) slow_list[s] = e;
+        else atomicOr(a.status, (uint32_t)LEO_ST_SCRATCH_OVERFLOW);
+      }
+    } else {
+      const int nres = c[0];
+      int off = 0;
+      if (lane == 0) off = atomicAdd(a.qres_count, nres);
+      off = __shfl_sync(0xffffffffu, off, 0);
+      if ((int64_t)off + nres > a.qres_cap) {
+        if (lane == 0) { atomicOr(a.status, (uint32_t)LEO_ST_SCRATCH_OVERFLOW); a.q_off[e] = 0; a.q_len[e] = 0; }
+      } else {
+        for (int x = lane; x < nres; x += 32) a.qres[off + x] = res[x];
+        if (lane == 0) { a.q_off[e] = off; a.q_len[e] = nres; }
+      }
+    }
+    __syncwarp();
+  }
+}
+
 // slow path: one worker thread per slot of global scratch (stamp/stack/results
 // of B entries each); stamps are query slot + 1, so no clearing between queries.
-__global__ void k_reach_slow(KView k, ReachArgs a, int32_t* scratch, int nworkers) {
-  const int ns = min((int64_t)*a.slow_count, a.slow_cap);
+__global__ void k_reach_slow(KView k, ReachArgs a, const int32_t* list, const int32_t* count,
+                             int32_t* scratch, int nworkers) {
+  const int ns = (int)min((int64_t)*count, a.slow_cap);
   const int w = blockIdx.x * blockDim.x + threadIdx.x;
   if (w >= nworkers) return;
   const int B = k.B;
@@ -254,7 +357,7 @@ __global__ void k_reach_slow(KView k, ReachArgs a, int32_t* scratch, int nworker
   int32_t* stk = stamp + (B + 1);
   int32_t* res = stk + (B + 1);
   for (int t = w; t < ns; t += nworkers) {
-    int e = a.slow_list[t];
+    int e = list[t];
     int nres = 0;
     reach_search(k, a, a.q_block[e], a.q_unit[e], nullptr, 0, stk, B + 1, res, B + 1, &nres,
                  stamp, e + 1);

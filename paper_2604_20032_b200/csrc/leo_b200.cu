@@ -25,14 +25,14 @@ enum KernelId {
   KID_REACH_SLOW, KID_LINK_COUNT, KID_LINK_FILL, KID_SEGSORT, KID_LINK_EMIT, KID_SYNC,
   KID_SYNC_SLOW, KID_KEY_HIST, KID_KEY_SCATTER, KID_SYNC_EMIT, KID_EDGE_TOTALS, KID_PRUNE,
   KID_PRUNE_SLOW, KID_COMPACT, KID_SEG_BOUNDS, KID_SYNC_HIST, KID_SYNC_FILL, KID_BLAME_COUNT,
-  KID_SELFBLAME_SLOW, KID_BLAME_FILL, KID_BLAME_TOTAL, KID_LINES, KID_SLICE, KID_COUNT_
+  KID_SELFBLAME_SLOW, KID_BLAME_FILL, KID_BLAME_TOTAL, KID_LINES, KID_SLICE, KID_REACH_WARP, KID_RUN_HEADS, KID_BIN_HIST, KID_BIN_PLAN, KID_BIN_SCATTER, KID_COUNT_
 };
 const char* const kKernelNames[] = {
   "bin_samples", "bin_finalize", "unit_counts", "scan", "block_walk", "reach_fast",
   "reach_slow", "link_count", "link_fill", "segsort_unique", "link_emit", "sync_trace",
   "sync_trace_slow", "key_hist", "key_scatter", "sync_emit", "edge_totals", "prune_edges",
   "prune_slow", "compact", "seg_bounds", "sync_hist", "sync_fill", "blame_count",
-  "selfblame_slow", "blame_fill", "blame_total", "lines", "slice",
+  "selfblame_slow", "blame_fill", "blame_total", "lines", "slice", "reach_warp", "run_heads", "bin_hist", "bin_plan", "bin_scatter",
 };
 
 struct TraceScope {
@@ -91,6 +91,7 @@ inline int64_t pick(int64_t hint, int64_t dflt) { return hint > 0 ? hint : dflt;
 int check_kernel(const LeoKernel* k) {
   if (!k || k->n_instr < 0 || k->n_blocks < 0 || k->n_units < 0) return -1;
   if (k->n_instr >= (1 << 30) || k->n_units > (1 << 24)) return -2;
+  if ((int64_t)k->n_blocks * k->n_units > ((int64_t)1 << 30)) return -4;   // dense last-def table
   return 0;
 }
 
@@ -119,15 +120,15 @@ int build_graph_impl(const LeoKernel* kk, const LeoCaps* caps, LeoEdges* out, Le
   const int SW = 64;         // slow sync workers
   Arena ar{st};
   int32_t *ucnt, *dcnt, *use_ptr, *def_ptr, *ev_res, *q_block, *q_unit, *q_list, *q_off, *q_len, *qres;
-  int32_t *ctr, *slow_list, *slow2, *cand_cnt, *cand_off, *uniq, *eoff, *bdef_len, *scan_tmp, *gtab = nullptr;
+  int32_t *ctr, *slow_list, *slow2, *slow3, *cand_cnt, *cand_off, *uniq, *eoff, *ldtab, *runhead, *scan_tmp, *gtab = nullptr;
   int32_t *pcnt, *poff, *pcur, *puniq, *puoff, *reach_scr;
-  uint64_t *bdef, *cand, *skeys, *ssorted;
+  uint64_t *cand, *skeys, *ssorted;
   char* sync_scr;
   ar.want(&ucnt, N); ar.want(&dcnt, N); ar.want(&use_ptr, N + 1); ar.want(&def_ptr, N + 1);
   ar.want(&ev_res, NU); ar.want(&q_block, NU); ar.want(&q_unit, NU); ar.want(&q_list, NU);
   ar.want(&q_off, NU); ar.want(&q_len, NU); ar.want(&qres, cap_qres); ar.want(&ctr, 16);
-  ar.want(&slow_list, cap_slow); ar.want(&slow2, cap_slow); ar.want(&cand_cnt, N); ar.want(&cand_off, N + 1);
-  ar.want(&uniq, N); ar.want(&eoff, N + 1); ar.want(&bdef_len, B); ar.want(&bdef, ND);
+  ar.want(&slow_list, NU + 1024); ar.want(&slow2, cap_slow); ar.want(&slow3, NU + 1024); ar.want(&cand_cnt, N); ar.want(&cand_off, N + 1);
+  ar.want(&uniq, N); ar.want(&eoff, N + 1); ar.want(&ldtab, (int64_t)B * U); ar.want(&runhead, B);
   ar.want(&cand, cap_cand); ar.want(&skeys, cap_sync); ar.want(&ssorted, cap_sync);
   ar.want(&pcnt, N); ar.want(&poff, N + 1); ar.want(&pcur, N); ar.want(&puniq, N); ar.want(&puoff, N + 1);
   ar.want(&scan_tmp, scan_scratch_ints(std::max<int64_t>(std::max<int64_t>(N, cap_cand), 1)) + 64);
@@ -146,15 +147,22 @@ int build_graph_impl(const LeoKernel* kk, const LeoCaps* caps, LeoEdges* out, Le
   TRACED(KID_SCAN, scan_exclusive(ucnt, use_ptr, nullptr, N, scan_tmp, nullptr, st));
   TRACED(KID_SCAN, scan_exclusive(dcnt, def_ptr, nullptr, N, scan_tmp, nullptr, st));
 
-  WalkArgs wa{use_ptr, def_ptr, ev_res, q_block, q_unit, q_list, &ctr[0], bdef, bdef_len, gtab};
+  WalkArgs wa{use_ptr, def_ptr, ev_res, q_block, q_unit, q_list, &ctr[0], ldtab, gtab};
   size_t smem = smem_tab ? (size_t)wpc * 2 * U * 4 : 0;
   if (smem > 48 * 1024) cudaFuncSetAttribute(k_block_walk, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (B > 0) TRACED(KID_BLOCK_WALK, k_block_walk<<<std::max(1, walk_ctas), wpc * 32, smem, st>>>(k, wa, wpc));
 
-  ReachArgs ra{def_ptr, bdef, bdef_len, q_block, q_unit, q_off, q_len, qres, cap_qres, &ctr[1],
-               slow_list, &ctr[2], cap_slow, status};
+  if (B > 0) TRACED(KID_RUN_HEADS, k_run_heads<<<grid_for(B, T), T, 0, st>>>(k, runhead));
+  ReachArgs ra{ldtab, runhead, U, q_block, q_unit, q_off, q_len, qres, cap_qres, &ctr[1],
+               slow_list, &ctr[2], NU + 1024, status};
   TRACED(KID_REACH_FAST, k_reach_fast<<<grid_for(NU, 128), 128, 0, st>>>(k, ra, q_list, &ctr[0]));
-  TRACED(KID_REACH_SLOW, k_reach_slow<<<(RW + 63) / 64, 64, 0, st>>>(k, ra, reach_scr, RW));
+  {
+    const int wpc_r = 4;
+    const size_t sm_r = (size_t)wpc_r * kWarpSmemInts * 4;
+    TRACED(KID_REACH_WARP, k_reach_warp<<<std::max(1, std::min<int>(SM * 4, (int)((NU + 1024 + wpc_r - 1) / wpc_r))),
+                                          wpc_r * 32, sm_r, st>>>(k, ra, slow_list, &ctr[2], NU + 1024, slow3, &ctr[7]));
+  }
+  TRACED(KID_REACH_SLOW, k_reach_slow<<<(RW + 63) / 64, 64, 0, st>>>(k, ra, slow3, &ctr[7], reach_scr, RW));
 
   LinkArgs la{use_ptr, ev_res, q_off, q_len, qres, cand_cnt, cand_off, cand, cap_cand, *diags, status};
   TRACED(KID_LINK_COUNT, k_link<0><<<grid_for(N, T), T, 0, st>>>(k, la));
@@ -313,14 +321,34 @@ int leo_abi_version(void) { return LEO_ABI_VERSION; }
 static int bin_impl(const LeoSamples* s, int32_t n_instr, int32_t* lat, int32_t* cls_cnt, LeoTrace* tr,
                     cudaStream_t st) {
   cudaMemsetAsync(cls_cnt, 0, (size_t)std::max(n_instr, 1) * 32, st);
-  uint32_t* status = nullptr;
-  LEO_CUDA_CHECK(cudaMallocAsync((void**)&status, 4, st));
+  const int64_t S = s->n_samples;
+  const int nb = (n_instr + kBinR - 1) / kBinR;
+  Arena ar{st};
+  uint32_t* status;
+  int32_t *bcnt, *boff, *bcur, *soff;
+  uint16_t* keys;
+  const bool bucketed = nb <= kBinMaxBuckets && S > 0;
+  ar.want(&status, 1);
+  ar.want(&bcnt, nb + 1); ar.want(&boff, nb + 1); ar.want(&bcur, nb + 1); ar.want(&soff, nb + 1);
+  ar.want(&keys, bucketed ? S : 1);
+  LEO_CUDA_CHECK(ar.commit());
   cudaMemsetAsync(status, 0, 4, st);
-  if (s->n_samples > 0)
-    TRACED(KID_BIN, k_bin_samples<<<grid_for(s->n_samples / 4 + 1, 256, num_sms() * 8), 256, 0, st>>>(
-        s->n_samples, s->pc, s->cat, s->cat_to_cs, n_instr, cls_cnt, status));
+  if (bucketed) {
+    static bool attr = false;
+    const int smem = kBinR * 8 * 4;
+    if (!attr) { cudaFuncSetAttribute(k_bin_count, cudaFuncAttributeMaxDynamicSharedMemorySize, smem); attr = true; }
+    cudaMemsetAsync(bcnt, 0, (size_t)(nb + 1) * 4, st);
+    const int G = num_sms() * 4;
+    TRACED(KID_BIN_HIST, k_bin_hist<<<grid_for(S / 4 + 1, 256, G), 256, 0, st>>>(S, s->pc, n_instr, nb, bcnt, status));
+    TRACED(KID_BIN_PLAN, k_bin_plan<<<1, 1024, 0, st>>>(nb, bcnt, boff, bcur, soff));
+    TRACED(KID_BIN_SCATTER, k_bin_scatter<<<grid_for(S, 1024, G), 1024, 0, st>>>(S, s->pc, s->cat, s->cat_to_cs, n_instr, nb, bcur, keys));
+    TRACED(KID_BIN, k_bin_count<<<num_sms() * 3, 512, smem, st>>>(n_instr, nb, boff, soff, keys, cls_cnt));
+  } else if (S > 0) {
+    TRACED(KID_BIN, k_bin_samples<<<grid_for(S / 4 + 1, 256, num_sms() * 8), 256, 0, st>>>(
+        S, s->pc, s->cat, s->cat_to_cs, n_instr, cls_cnt, status));
+  }
   TRACED(KID_BIN_FINALIZE, k_bin_finalize<<<grid_for(n_instr, 256), 256, 0, st>>>(n_instr, cls_cnt, lat));
-  cudaFreeAsync(status, st);
+  ar.release();
   LEO_CUDA_CHECK(cudaGetLastError());
   return 0;
 }

@@ -181,6 +181,31 @@ class Analyzer:
                            st.cuda_stream)
         check(rc, "leo_analyze")
 
+    # -- CUDA graph ----------------------------------------------------------
+    def capture(self, dp: DeviceProfile, cfg: abi.LeoConfig, samples: DeviceSamples | None = None):
+        """Capture the whole stream-ordered pipeline (no host syncs inside) into
+        one CUDA graph; `replay()` then re-runs it on the current buffers.
+        Buffers must already be sized (call run() first)."""
+        tracer = self.tracer
+        self.set_tracer(None)
+        self._graph_args = (dp, cfg, samples)
+        g = torch.cuda.CUDAGraph()
+        side = torch.cuda.Stream(self.device)
+        side.wait_stream(torch.cuda.current_stream(self.device))
+        with torch.cuda.stream(side):
+            self.launch(dp, cfg, samples)
+        torch.cuda.current_stream(self.device).wait_stream(side)
+        torch.cuda.synchronize(self.device)
+        with torch.cuda.graph(g, capture_error_mode="thread_local"):
+            self.launch(dp, cfg, samples)
+        torch.cuda.synchronize(self.device)
+        self.graph = g
+        self.set_tracer(tracer)
+        return g
+
+    def replay(self):
+        self.graph.replay()
+
     def counts(self) -> np.ndarray:
         return self.ctr.cpu().numpy()
 
