@@ -208,7 +208,11 @@ typedef struct LeoCaps {
   int64_t sync_keys;          /* raw sync edges before dedup              (default 2 x N + 1024) */
   int64_t slow_items;         /* work items re-run on the global-scratch path (default N/4 + 1024) */
   LeoTrace* trace;            /* optional, host struct (NULL = no tracing) */
+  int32_t debug_flags;        /* testing: route every item to a larger tier (LEO_DBG_*) */
+  int32_t pad;
 } LeoCaps;
+enum { LEO_DBG_REACH_T2 = 1, LEO_DBG_REACH_T3 = 2, LEO_DBG_SYNC_SLOW = 4, LEO_DBG_PRUNE_SLOW = 8,
+       LEO_DBG_SELF_SLOW = 16 };
 
 /* ---- status word (device) ------------------------------------------------ */
 enum { LEO_ST_EDGE_OVERFLOW = 1, LEO_ST_PATH_OVERFLOW = 2, LEO_ST_DIAG_OVERFLOW = 4,

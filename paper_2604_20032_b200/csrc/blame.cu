@@ -69,7 +69,6 @@ __global__ void k_bin_samples(int64_t S, const int32_t* __restrict__ pc, const u
 // than one global atomic per CTA.
 constexpr int kBinR = 2048;          // instructions per bucket (64 KiB of counters)
 constexpr int kBinMaxBuckets = 4096;
-constexpr int kBinSlice = 1 << 16;   // samples per counting CTA
 
 __global__ void k_bin_hist(int64_t S, const int32_t* __restrict__ pc, int N, int nb,
                            int32_t* __restrict__ bucket_cnt, uint32_t* status) {
@@ -99,14 +98,14 @@ __global__ void k_bin_hist(int64_t S, const int32_t* __restrict__ pc, int N, int
 }
 
 // single CTA: bucket offsets, per-bucket cursors and slice offsets
-__global__ void k_bin_plan(int nb, const int32_t* __restrict__ bucket_cnt, int32_t* __restrict__ bucket_off,
+__global__ void k_bin_plan(int nb, int slice, const int32_t* __restrict__ bucket_cnt, int32_t* __restrict__ bucket_off,
                            int32_t* __restrict__ cursor, int32_t* __restrict__ slice_off) {
   __shared__ int sw[33];
   int carry = 0, scarry = 0;
   for (int base = 0; base < nb; base += blockDim.x) {
     int i = base + threadIdx.x;
     int c = i < nb ? bucket_cnt[i] : 0;
-    int ns = (c + kBinSlice - 1) / kBinSlice;
+    int ns = (c + slice - 1) / slice;
     int tot, stot;
     int ex = block_excl_scan(c, sw, &tot);
     int sex = block_excl_scan(ns, sw, &stot);
@@ -146,7 +145,7 @@ __global__ void k_bin_scatter(int64_t S, const int32_t* __restrict__ pc, const u
   }
 }
 
-__global__ void __launch_bounds__(512) k_bin_count(int N, int nb, const int32_t* __restrict__ bucket_off,
+__global__ void __launch_bounds__(512) k_bin_count(int N, int nb, int slice, const int32_t* __restrict__ bucket_off,
                                                    const int32_t* __restrict__ slice_off,
                                                    const uint16_t* __restrict__ keys,
                                                    int32_t* __restrict__ cls_cnt) {
@@ -161,8 +160,8 @@ __global__ void __launch_bounds__(512) k_bin_count(int N, int nb, const int32_t*
     }
     const int b = lo;
     const int k = sl - slice_off[b];
-    const int64_t e0 = (int64_t)bucket_off[b] + (int64_t)k * kBinSlice;
-    const int64_t e1 = min((int64_t)bucket_off[b + 1], e0 + kBinSlice);
+    const int64_t e0 = (int64_t)bucket_off[b] + (int64_t)k * slice;
+    const int64_t e1 = min((int64_t)bucket_off[b + 1], e0 + slice);
     for (int x = threadIdx.x; x < kBinR * 8; x += blockDim.x) cnt[x] = 0;
     __syncthreads();
     for (int64_t e = e0 + threadIdx.x; e - threadIdx.x < e1; e += blockDim.x) {
@@ -265,6 +264,7 @@ LEO_DEV int traces_to_load(const KView& k, const int32_t* brbeg, const int32_t* 
 }
 
 struct BlameArgs {
+  int32_t dbg;
   PView p;
   const int32_t* pprod;
   const uint32_t* pmeta;
@@ -347,7 +347,8 @@ __global__ void k_blame(KView k, BlameArgs a) {
         int sub = dominant_self(a.p, j);
         if (sub == LEO_SB_MEMORY_LATENCY && (kMemoryClasses & BIT(k.opclass[j]))) {
           int32_t seen[kSeenCap];
-          int r = traces_to_load(k, a.brbeg, a.brend, a.bprod, a.bmeta, j, seen, kSeenCap, nullptr, 0);
+          int r = (a.dbg & LEO_DBG_SELF_SLOW) ? -1
+                  : traces_to_load(k, a.brbeg, a.brend, a.bprod, a.bmeta, j, seen, kSeenCap, nullptr, 0);
           if (r < 0) {
             int s = atomicAdd(a.slow_count, 1);
             if (s < a.slow_cap) a.slow_list[s] = j;

@@ -130,21 +130,32 @@ __global__ void k_block_walk(KView k, WalkArgs a, int warps_per_cta) {
   }
 }
 
-// Fallthrough-run heads: runhead[b] = first block of the maximal run ending at
-// b in which every block but the first has exactly one predecessor, the
-// previous block.  A backward search entering the run at y can only leave it
-// through preds(runhead[y]), so the run is resolved with independent loads.
-__global__ void k_run_heads(KView k, int32_t* __restrict__ head) {
+// Fallthrough runs: runhead(b) = first block of the maximal run ending at b in
+// which every block but the first has exactly one predecessor, the previous
+// block.  A backward search entering the run at y can only leave it through
+// preds(runhead(y)), so a run is resolved with independent loads of the dense
+// last-def table instead of one search level per block.
+//
+// Block record (one 16-byte load per search step):
+//   rec[y] = {h = runhead(y), np = |preds(h)|, p0, p1}
+//   np <= 2: p0/p1 are the predecessors of h; np > 2: p0 = pred_ptr[h].
+__global__ void k_block_records(KView k, int4* __restrict__ rec) {
   for (int b = blockIdx.x * blockDim.x + threadIdx.x; b < k.B; b += gridDim.x * blockDim.x) {
     int x = b;
     while (x > 0 && k.pred_ptr[x + 1] - k.pred_ptr[x] == 1 && k.pred[k.pred_ptr[x]] == x - 1) x--;
-    head[b] = x;
+    const int q0 = k.pred_ptr[x], np = k.pred_ptr[x + 1] - q0;
+    int4 r;
+    r.x = x; r.y = np;
+    if (np <= 2) { r.z = np > 0 ? k.pred[q0] : -1; r.w = np > 1 ? k.pred[q0 + 1] : -1; }
+    else { r.z = q0; r.w = -1; }
+    rec[b] = r;
   }
 }
 
 struct ReachArgs {
+  int32_t dbg;               // LEO_DBG_* routing (testing)
   const int32_t* ldtab;      // [B * U]
-  const int32_t* runhead;    // [B]
+  const int4* rec;           // [B]
   int32_t U;
   const int32_t* q_block;
   const int32_t* q_unit;
@@ -160,10 +171,8 @@ struct ReachArgs {
 };
 
 // Entering block y backward: the nearest definition of u in y, y-1, ...,
-// runhead[y] (loads issued four at a time), or -1 with *head = runhead[y].
-LEO_DEV int run_lookup(const ReachArgs& a, int y, int u, int* head) {
-  const int h = a.runhead[y];
-  *head = h;
+// runhead(y) (loads issued four at a time), or -1.
+LEO_DEV int run_lookup(const ReachArgs& a, int y, int h, int u) {
   const size_t U = (size_t)a.U;
   for (int x = y; x >= h; x -= 4) {
     int v0 = a.ldtab[(size_t)x * U + u];
@@ -178,41 +187,56 @@ LEO_DEV int run_lookup(const ReachArgs& a, int y, int u, int* head) {
   return -1;
 }
 
-// Backward search for query (b, u).  visited / stack / results live in the
-// caller's buffers (registers-backed local arrays on the fast path, global
-// scratch on the slow path).  Returns false when a buffer overflowed.
-LEO_DEV bool reach_search(const KView& k, const ReachArgs& a, int b, int u, int32_t* vis, int vcap,
-                          int32_t* stk, int scap, int32_t* res, int rcap, int* nres_out,
-                          int32_t* stamp, int stamp_val) {
-  int nvis = 0, sp = 0, nres = 0;
-  auto visit = [&](int p) -> int {   // 1 new, 0 seen, -1 overflow
-    if (stamp) {
-      if (stamp[p] == stamp_val) return 0;
-      stamp[p] = stamp_val;
-      return 1;
+// Visited-set policies for the search: a private open-addressing hash
+// (shared memory, strided per thread) or a stamp array in global scratch.
+struct SmemHash {
+  int32_t* h; int stride, cap, n, limit;
+  LEO_DEV void clear() { for (int s = 0; s < cap; s++) h[s * stride] = -1; n = 0; }
+  LEO_DEV int insert(int key) {            // 1 new, 0 seen, -1 overflow
+    int s = (int)(((uint32_t)key * 2654435761u) >> 26) & (cap - 1);
+    for (int probe = 0; probe < cap; probe++) {
+      int v = h[s * stride];
+      if (v == key) return 0;
+      if (v == -1) {
+        if (n == limit) return -1;
+        h[s * stride] = key; n++;
+        return 1;
+      }
+      s = (s + 1) & (cap - 1);
     }
-    for (int x = 0; x < nvis; x++) if (vis[x] == p) return 0;
-    if (nvis == vcap) return -1;
-    vis[nvis++] = p;
-    return 1;
-  };
+    return -1;
+  }
+};
+struct StampSet {
+  int32_t* stamp; int val;
+  LEO_DEV int insert(int key) { if (stamp[key] == val) return 0; stamp[key] = val; return 1; }
+};
+
+// Backward search for query (b, u) over run-contracted blocks.  Returns false
+// when a buffer overflowed (the caller re-runs the query on a larger tier).
+template <class Visited>
+LEO_DEV bool reach_search(const KView& k, const ReachArgs& a, int b, int u, Visited& vis,
+                          int32_t* stk, int scap, int32_t* res, int rcap, int* nres_out) {
+  int sp = 0, nres = 0;
   for (int q = k.pred_ptr[b]; q < k.pred_ptr[b + 1]; q++) {
     int p = k.pred[q];
-    int v = visit(p);
+    int v = vis.insert(p);
     if (v < 0) return false;
     if (v) { if (sp == scap) return false; stk[sp++] = p; }
   }
   while (sp > 0) {
-    int y = stk[--sp], p;
-    int ld = run_lookup(a, y, u, &p);
+    const int y = stk[--sp];
+    const int4 r = a.rec[y];
+    const int ld = run_lookup(a, y, r.x, u);
     if (ld >= 0) {
       if (nres == rcap) return false;
       res[nres++] = ld;
       continue;
     }
-    for (int q = k.pred_ptr[p]; q < k.pred_ptr[p + 1]; q++) {
-      int pp = k.pred[q];
-      int v = visit(pp);
+    const int np = r.y;
+    for (int t = 0; t < np; t++) {
+      const int pp = np <= 2 ? (t == 0 ? r.z : r.w) : k.pred[r.z + t];
+      int v = vis.insert(pp);
       if (v < 0) return false;
       if (v) { if (sp == scap) return false; stk[sp++] = pp; }
     }
@@ -233,17 +257,24 @@ LEO_DEV void reach_commit(const ReachArgs& a, int e, const int32_t* res, int nre
   a.q_len[e] = nres;
 }
 
-constexpr int kReachV = 16, kReachS = 16, kReachR = 8;
+// Tier 1: one thread per query; the visited hash lives in shared memory
+// (64 slots per thread, strided for bank spread), so every query of a kernel
+// is in flight at once and latency is hidden by thread-level parallelism.
+constexpr int kT1Hash = 64, kT1Limit = 40, kT1Stack = 40, kT1Res = 16, kT1Threads = 256;
 
-__global__ void k_reach_fast(KView k, ReachArgs a, const int32_t* __restrict__ q_list,
-                             const int32_t* q_count) {
+__global__ void __launch_bounds__(kT1Threads) k_reach_fast(KView k, ReachArgs a,
+                                                           const int32_t* __restrict__ q_list,
+                                                           const int32_t* q_count) {
+  extern __shared__ int32_t hsm[];
   const int nq = *q_count;
+  SmemHash vis{hsm + threadIdx.x, (int)blockDim.x, kT1Hash, 0, kT1Limit};
+  int32_t stk[kT1Stack], res[kT1Res];
   for (int t = blockIdx.x * blockDim.x + threadIdx.x; t < nq; t += gridDim.x * blockDim.x) {
-    int e = q_list[t];
-    int32_t vis[kReachV], stk[kReachS], res[kReachR];
+    const int e = q_list[t];
+    vis.clear();
     int nres = 0;
-    if (reach_search(k, a, a.q_block[e], a.q_unit[e], vis, kReachV, stk, kReachS, res, kReachR,
-                     &nres, nullptr, 0)) {
+    if (!(a.dbg & (LEO_DBG_REACH_T2 | LEO_DBG_REACH_T3)) &&
+        reach_search(k, a, a.q_block[e], a.q_unit[e], vis, stk, kT1Stack, res, kT1Res, &nres)) {
       reach_commit(a, e, res, nres);
     } else {
       int s = atomicAdd(a.slow_count, 1);
@@ -295,21 +326,23 @@ __global__ void k_reach_warp(KView k, ReachArgs a, const int32_t* __restrict__ l
         if (pos < kWFront) fa[pos] = p; else c[3] = 1;
       }
     }
+    if ((a.dbg & LEO_DBG_REACH_T3) && lane == 0) c[3] = 1;
     __syncwarp();
     int32_t *cur = fa, *nxt = fb;
     while (true) {
       const int ncur = c[1];
       if (ncur == 0 || c[3]) break;
       for (int x = lane; x < ncur; x += 32) {
-        int p;
-        const int ld = run_lookup(a, cur[x], u, &p);
+        const int y = cur[x];
+        const int4 r = a.rec[y];
+        const int ld = run_lookup(a, y, r.x, u);
         if (ld >= 0) {
-          int r = atomicAdd(&c[0], 1);
-          if (r < kWRes) res[r] = ld; else c[3] = 1;
+          int rr = atomicAdd(&c[0], 1);
+          if (rr < kWRes) res[rr] = ld; else c[3] = 1;
           continue;
         }
-        for (int q = k.pred_ptr[p]; q < k.pred_ptr[p + 1]; q++) {
-          const int pp = k.pred[q];
+        for (int t2 = 0; t2 < r.y; t2++) {
+          const int pp = r.y <= 2 ? (t2 == 0 ? r.z : r.w) : k.pred[r.z + t2];
           if (hash_insert(hash, pp, &c[4])) {
             int pos = atomicAdd(&c[2], 1);
             if (pos < kWFront) nxt[pos] = pp; else c[3] = 1;
@@ -345,7 +378,7 @@ __global__ void k_reach_warp(KView k, ReachArgs a, const int32_t* __restrict__ l
   }
 }
 
-// slow path: one worker thread per slot of global scratch (stamp/stack/results
+// Tier 3: one worker thread per slot of global scratch (stamp / stack / results
 // of B entries each); stamps are query slot + 1, so no clearing between queries.
 __global__ void k_reach_slow(KView k, ReachArgs a, const int32_t* list, const int32_t* count,
                              int32_t* scratch, int nworkers) {
@@ -359,8 +392,8 @@ __global__ void k_reach_slow(KView k, ReachArgs a, const int32_t* list, const in
   for (int t = w; t < ns; t += nworkers) {
     int e = list[t];
     int nres = 0;
-    reach_search(k, a, a.q_block[e], a.q_unit[e], nullptr, 0, stk, B + 1, res, B + 1, &nres,
-                 stamp, e + 1);
+    StampSet vis{stamp, e + 1};
+    reach_search(k, a, a.q_block[e], a.q_unit[e], vis, stk, B + 1, res, B + 1, &nres);
     reach_commit(a, e, res, nres);
   }
 }

@@ -25,14 +25,14 @@ enum KernelId {
   KID_REACH_SLOW, KID_LINK_COUNT, KID_LINK_FILL, KID_SEGSORT, KID_LINK_EMIT, KID_SYNC,
   KID_SYNC_SLOW, KID_KEY_HIST, KID_KEY_SCATTER, KID_SYNC_EMIT, KID_EDGE_TOTALS, KID_PRUNE,
   KID_PRUNE_SLOW, KID_COMPACT, KID_SEG_BOUNDS, KID_SYNC_HIST, KID_SYNC_FILL, KID_BLAME_COUNT,
-  KID_SELFBLAME_SLOW, KID_BLAME_FILL, KID_BLAME_TOTAL, KID_LINES, KID_SLICE, KID_REACH_WARP, KID_RUN_HEADS, KID_BIN_HIST, KID_BIN_PLAN, KID_BIN_SCATTER, KID_COUNT_
+  KID_SELFBLAME_SLOW, KID_BLAME_FILL, KID_BLAME_TOTAL, KID_LINES, KID_SLICE, KID_REACH_WARP, KID_RUN_HEADS, KID_BIN_HIST, KID_BIN_PLAN, KID_BIN_SCATTER, KID_SYNC_PACK, KID_COUNT_
 };
 const char* const kKernelNames[] = {
   "bin_samples", "bin_finalize", "unit_counts", "scan", "block_walk", "reach_fast",
   "reach_slow", "link_count", "link_fill", "segsort_unique", "link_emit", "sync_trace",
   "sync_trace_slow", "key_hist", "key_scatter", "sync_emit", "edge_totals", "prune_edges",
   "prune_slow", "compact", "seg_bounds", "sync_hist", "sync_fill", "blame_count",
-  "selfblame_slow", "blame_fill", "blame_total", "lines", "slice", "reach_warp", "run_heads", "bin_hist", "bin_plan", "bin_scatter",
+  "selfblame_slow", "blame_fill", "blame_total", "lines", "slice", "reach_warp", "run_heads", "bin_hist", "bin_plan", "bin_scatter", "sync_pack",
 };
 
 struct TraceScope {
@@ -88,7 +88,18 @@ struct Arena {
 
 inline int64_t pick(int64_t hint, int64_t dflt) { return hint > 0 ? hint : dflt; }
 
+// kernels that take more than 48 KiB of dynamic shared memory (set once)
+void set_smem_attributes() {
+  static bool done = false;
+  if (done) return;
+  cudaFuncSetAttribute(k_reach_fast, cudaFuncAttributeMaxDynamicSharedMemorySize, kT1Threads * kT1Hash * 4);
+  cudaFuncSetAttribute(k_bin_count, cudaFuncAttributeMaxDynamicSharedMemorySize, kBinR * 8 * 4);
+  cudaFuncSetAttribute(k_block_walk, cudaFuncAttributeMaxDynamicSharedMemorySize, 96 * 1024);
+  done = true;
+}
+
 int check_kernel(const LeoKernel* k) {
+  set_smem_attributes();
   if (!k || k->n_instr < 0 || k->n_blocks < 0 || k->n_units < 0) return -1;
   if (k->n_instr >= (1 << 30) || k->n_units > (1 << 24)) return -2;
   if ((int64_t)k->n_blocks * k->n_units > ((int64_t)1 << 30)) return -4;   // dense last-def table
@@ -117,23 +128,29 @@ int build_graph_impl(const LeoKernel* kk, const LeoCaps* caps, LeoEdges* out, Le
   const int walk_warps = std::max(1, walk_ctas) * wpc;
 
   const int RW = 128;        // slow reach workers
-  const int SW = 64;         // slow sync workers
+  const int SW = 16;         // slow sync workers
   Arena ar{st};
   int32_t *ucnt, *dcnt, *use_ptr, *def_ptr, *ev_res, *q_block, *q_unit, *q_list, *q_off, *q_len, *qres;
-  int32_t *ctr, *slow_list, *slow2, *slow3, *cand_cnt, *cand_off, *uniq, *eoff, *ldtab, *runhead, *scan_tmp, *gtab = nullptr;
+  int32_t *ctr, *slow_list, *slow2, *slow3, *cand_cnt, *cand_off, *uniq, *eoff, *ldtab, *scan_tmp, *gtab = nullptr;
+  int4* brec;
   int32_t *pcnt, *poff, *pcur, *puniq, *puoff, *reach_scr;
   uint64_t *cand, *skeys, *ssorted;
+  uint32_t* wcword;
+  uint8_t* setword;
+  int32_t* lastset;
   char* sync_scr;
   ar.want(&ucnt, N); ar.want(&dcnt, N); ar.want(&use_ptr, N + 1); ar.want(&def_ptr, N + 1);
   ar.want(&ev_res, NU); ar.want(&q_block, NU); ar.want(&q_unit, NU); ar.want(&q_list, NU);
   ar.want(&q_off, NU); ar.want(&q_len, NU); ar.want(&qres, cap_qres); ar.want(&ctr, 16);
   ar.want(&slow_list, NU + 1024); ar.want(&slow2, cap_slow); ar.want(&slow3, NU + 1024); ar.want(&cand_cnt, N); ar.want(&cand_off, N + 1);
-  ar.want(&uniq, N); ar.want(&eoff, N + 1); ar.want(&ldtab, (int64_t)B * U); ar.want(&runhead, B);
+  ar.want(&uniq, N); ar.want(&eoff, N + 1); ar.want(&ldtab, (int64_t)B * U); ar.want(&brec, B);
   ar.want(&cand, cap_cand); ar.want(&skeys, cap_sync); ar.want(&ssorted, cap_sync);
   ar.want(&pcnt, N); ar.want(&poff, N + 1); ar.want(&pcur, N); ar.want(&puniq, N); ar.want(&puoff, N + 1);
   ar.want(&scan_tmp, scan_scratch_ints(std::max<int64_t>(std::max<int64_t>(N, cap_cand), 1)) + 64);
   ar.want(&reach_scr, (int64_t)RW * 3 * (B + 1));
   ar.want(&sync_scr, (int64_t)SW * sync_slow_bytes_per_worker(B));
+  const int n_ids = k.dialect == LEO_INTEL ? 32 : 8;
+  ar.want(&wcword, N); ar.want(&setword, N); ar.want(&lastset, (int64_t)B * n_ids);
   if (!smem_tab) ar.want(&gtab, (int64_t)walk_warps * 2 * U);
   LEO_CUDA_CHECK(ar.commit());
   // counters: 0 q_count, 1 qres_count, 2 reach slow, 3 sync keys, 4 sync slow, 5 n_regular, 6 n_sync
@@ -149,13 +166,12 @@ int build_graph_impl(const LeoKernel* kk, const LeoCaps* caps, LeoEdges* out, Le
 
   WalkArgs wa{use_ptr, def_ptr, ev_res, q_block, q_unit, q_list, &ctr[0], ldtab, gtab};
   size_t smem = smem_tab ? (size_t)wpc * 2 * U * 4 : 0;
-  if (smem > 48 * 1024) cudaFuncSetAttribute(k_block_walk, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (B > 0) TRACED(KID_BLOCK_WALK, k_block_walk<<<std::max(1, walk_ctas), wpc * 32, smem, st>>>(k, wa, wpc));
 
-  if (B > 0) TRACED(KID_RUN_HEADS, k_run_heads<<<grid_for(B, T), T, 0, st>>>(k, runhead));
-  ReachArgs ra{ldtab, runhead, U, q_block, q_unit, q_off, q_len, qres, cap_qres, &ctr[1],
+  if (B > 0) TRACED(KID_RUN_HEADS, k_block_records<<<grid_for(B, T), T, 0, st>>>(k, brec));
+  ReachArgs ra{caps ? caps->debug_flags : 0, ldtab, brec, U, q_block, q_unit, q_off, q_len, qres, cap_qres, &ctr[1],
                slow_list, &ctr[2], NU + 1024, status};
-  TRACED(KID_REACH_FAST, k_reach_fast<<<grid_for(NU, 128), 128, 0, st>>>(k, ra, q_list, &ctr[0]));
+  TRACED(KID_REACH_FAST, k_reach_fast<<<grid_for(NU, kT1Threads), kT1Threads, kT1Threads * kT1Hash * 4, st>>>(k, ra, q_list, &ctr[0]));
   {
     const int wpc_r = 4;
     const size_t sm_r = (size_t)wpc_r * kWarpSmemInts * 4;
@@ -172,9 +188,13 @@ int build_graph_impl(const LeoKernel* kk, const LeoCaps* caps, LeoEdges* out, Le
   TRACED(KID_SCAN, scan_exclusive(uniq, eoff, nullptr, N, scan_tmp, &ctr[5], st));
   TRACED(KID_LINK_EMIT, k_link_emit<<<grid_for(N, T), T, 0, st>>>(k, cand_off, cand, uniq, eoff, *out, status));
 
-  SyncArgs sa{skeys, cap_sync, &ctr[3], slow2, &ctr[4], cap_slow, *diags, status};
+  cudaMemsetAsync(sync_scr, 0, (size_t)SW * sync_slow_bytes_per_worker(B), st);
+  TRACED(KID_SYNC_PACK, k_sync_pack<<<grid_for(N, T), T, 0, st>>>(k, wcword, setword));
+  if (k.dialect != LEO_AMD && B > 0)
+    TRACED(KID_SYNC_PACK, k_block_setters<<<grid_for(B, T), T, 0, st>>>(k, setword, n_ids, lastset));
+  SyncArgs sa{caps ? caps->debug_flags : 0, skeys, cap_sync, &ctr[3], slow2, &ctr[4], cap_slow, *diags, status, wcword, setword, lastset, n_ids};
   TRACED(KID_SYNC, k_sync<false><<<grid_for(N, 128), 128, 0, st>>>(k, sa, nullptr, 0));
-  TRACED(KID_SYNC_SLOW, k_sync<true><<<1, SW, 0, st>>>(k, sa, (int32_t*)sync_scr, SW));
+  TRACED(KID_SYNC_SLOW, k_sync<true><<<1, SW, 0, st>>>(k, sa, sync_scr, SW));
   TRACED(KID_KEY_HIST, k_key_hist<<<grid_for(cap_sync, T), T, 0, st>>>(skeys, &ctr[3], cap_sync, pcnt));
   TRACED(KID_SCAN, scan_exclusive(pcnt, poff, nullptr, N, scan_tmp, nullptr, st));
   TRACED(KID_KEY_SCATTER, k_key_scatter<<<grid_for(cap_sync, T), T, 0, st>>>(skeys, &ctr[3], cap_sync, poff, pcur, ssorted));
@@ -211,7 +231,7 @@ int prune_impl(const LeoKernel* kk, const LeoProfile* pp, const LeoConfig* cfg, 
   LEO_CUDA_CHECK(ar.commit());
   cudaMemsetAsync(ctr, 0, 4 * sizeof(int32_t), st);
   cudaMemsetAsync(paths->count, 0, sizeof(int32_t), st);
-  PruneArgs a{*cfg, in->prod, in->cons, in->meta, in->count, (int32_t)cap_in, keep, npaths, pfirst, dist,
+  PruneArgs a{caps ? caps->debug_flags : 0, *cfg, in->prod, in->cons, in->meta, in->count, (int32_t)cap_in, keep, npaths, pfirst, dist,
               *paths, slow_list, &ctr[0], cap_slow, *diags, status};
   TRACED(KID_PRUNE, k_prune_edges<<<grid_for(cap_in, 128, num_sms() * 16), 128, 0, st>>>(k, p, a));
   TRACED(KID_PRUNE_SLOW, k_prune_slow<<<1, PW, 0, st>>>(k, p, a, slow_scr, PW));
@@ -293,7 +313,7 @@ int blame_impl(const LeoKernel* kk, const LeoProfile* pp, const LeoEdges* pruned
   LEO_CUDA_CHECK(ar.commit());
   cudaMemsetAsync(ctr, 0, 16, st);
   Incoming binc = build_incoming(bb, N, base, false, tr, st);   // RAW edges only
-  BlameArgs a{p, pruned->prod, pruned->meta, paths->dist, inc, binc.rbeg, binc.rend, base->prod, base->meta,
+  BlameArgs a{caps ? caps->debug_flags : 0, p, pruned->prod, pruned->meta, paths->dist, inc, binc.rbeg, binc.rend, base->prod, base->meta,
               ecount, self_sub, jtotal, jnsum, eoff, *out, slow_list, &ctr[0], cap_slow, status};
   TRACED(KID_BLAME_COUNT, k_blame<0><<<grid_for(N, 128), 128, 0, st>>>(k, a));
   TRACED(KID_SELFBLAME_SLOW, k_selfblame_slow<<<1, BW, 0, st>>>(k, a, slow_scr, BW));
@@ -320,6 +340,7 @@ int leo_abi_version(void) { return LEO_ABI_VERSION; }
 
 static int bin_impl(const LeoSamples* s, int32_t n_instr, int32_t* lat, int32_t* cls_cnt, LeoTrace* tr,
                     cudaStream_t st) {
+  set_smem_attributes();
   cudaMemsetAsync(cls_cnt, 0, (size_t)std::max(n_instr, 1) * 32, st);
   const int64_t S = s->n_samples;
   const int nb = (n_instr + kBinR - 1) / kBinR;
@@ -334,15 +355,15 @@ static int bin_impl(const LeoSamples* s, int32_t n_instr, int32_t* lat, int32_t*
   LEO_CUDA_CHECK(ar.commit());
   cudaMemsetAsync(status, 0, 4, st);
   if (bucketed) {
-    static bool attr = false;
     const int smem = kBinR * 8 * 4;
-    if (!attr) { cudaFuncSetAttribute(k_bin_count, cudaFuncAttributeMaxDynamicSharedMemorySize, smem); attr = true; }
     cudaMemsetAsync(bcnt, 0, (size_t)(nb + 1) * 4, st);
     const int G = num_sms() * 4;
     TRACED(KID_BIN_HIST, k_bin_hist<<<grid_for(S / 4 + 1, 256, G), 256, 0, st>>>(S, s->pc, n_instr, nb, bcnt, status));
-    TRACED(KID_BIN_PLAN, k_bin_plan<<<1, 1024, 0, st>>>(nb, bcnt, boff, bcur, soff));
+    // slices: enough counting CTAs to fill the chip, >= 4K samples each
+    const int slice = (int)std::min<int64_t>(65536, std::max<int64_t>(4096, S / (num_sms() * 3)));
+    TRACED(KID_BIN_PLAN, k_bin_plan<<<1, 1024, 0, st>>>(nb, slice, bcnt, boff, bcur, soff));
     TRACED(KID_BIN_SCATTER, k_bin_scatter<<<grid_for(S, 1024, G), 1024, 0, st>>>(S, s->pc, s->cat, s->cat_to_cs, n_instr, nb, bcur, keys));
-    TRACED(KID_BIN, k_bin_count<<<num_sms() * 3, 512, smem, st>>>(n_instr, nb, boff, soff, keys, cls_cnt));
+    TRACED(KID_BIN, k_bin_count<<<num_sms() * 3, 512, smem, st>>>(n_instr, nb, slice, boff, soff, keys, cls_cnt));
   } else if (S > 0) {
     TRACED(KID_BIN, k_bin_samples<<<grid_for(S / 4 + 1, 256, num_sms() * 8), 256, 0, st>>>(
         S, s->pc, s->cat, s->cat_to_cs, n_instr, cls_cnt, status));

@@ -95,16 +95,40 @@ __global__ void scan_tile_apply(const int32_t* __restrict__ in, const int32_t* n
     ex += v[k];
   }
   // out[n] = total (CSR end) written by the last tile owner
-  if (n_dev == nullptr || true) {
-    int64_t last_tile = n > 0 ? (n - 1) / kScanTile : 0;
-    if ((int64_t)blockIdx.x == last_tile && threadIdx.x == 0) out[n] = tile_sums[blockIdx.x] + total;
+  const int64_t last_tile = n > 0 ? (n - 1) / kScanTile : 0;
+  if ((int64_t)blockIdx.x == last_tile && threadIdx.x == 0) out[n] = tile_sums[blockIdx.x] + total;
+}
+
+// one CTA scans the whole array tile by tile (small arrays: one launch)
+__global__ void __launch_bounds__(1024) scan_single_cta(const int32_t* __restrict__ in, const int32_t* n_dev,
+                                                        int64_t n_cap, int32_t* __restrict__ out,
+                                                        int32_t* total_out) {
+  __shared__ int sw[33];
+  const int64_t n = n_dev ? (int64_t)*n_dev : n_cap;
+  int carry = 0;
+  for (int64_t base = 0; base < n; base += (int64_t)blockDim.x * kScanItems) {
+    const int64_t i0 = base + (int64_t)threadIdx.x * kScanItems;
+    int v[kScanItems];
+    int s = 0;
+#pragma unroll
+    for (int k = 0; k < kScanItems; k++) { v[k] = i0 + k < n ? in[i0 + k] : 0; s += v[k]; }
+    int tot;
+    int ex = block_excl_scan(s, sw, &tot) + carry;
+#pragma unroll
+    for (int k = 0; k < kScanItems; k++) { if (i0 + k < n) out[i0 + k] = ex; ex += v[k]; }
+    carry += tot;
   }
+  if (threadIdx.x == 0) { out[n] = carry; if (total_out) *total_out = carry; }
 }
 
 // exclusive scan of in[0..n) into out[0..n] (out[n] = total); n from n_dev if
 // given else n_cap.  scratch: >= tiles(n_cap) ints.  total_out optional.
 inline void scan_exclusive(const int32_t* in, int32_t* out, const int32_t* n_dev, int64_t n_cap,
                            int32_t* scratch, int32_t* total_out, cudaStream_t st) {
+  if (n_cap <= 65536) {
+    scan_single_cta<<<1, 1024, 0, st>>>(in, n_dev, n_cap, out, total_out);
+    return;
+  }
   int64_t ntiles = (n_cap + kScanTile - 1) / kScanTile;
   if (ntiles < 1) ntiles = 1;
   scan_tile_sums<<<(unsigned)ntiles, kScanThreads, 0, st>>>(in, n_dev, n_cap, scratch);

@@ -120,6 +120,7 @@ LEO_DEV int enumerate_paths(const KView& k, int producer, int consumer, double t
 }
 
 struct PruneArgs {
+  int32_t dbg;
   LeoConfig cfg;
   const int32_t* prod;
   const int32_t* cons;
@@ -206,7 +207,7 @@ __global__ void __launch_bounds__(128) k_prune_edges(KView k, PView p, PruneArgs
   BackNode arena[kDfsArena];
   int32_t vlen[kDfsPaths];
   double vacc[kDfsPaths];
-  const bool big_paths = a.cfg.max_paths > kDfsPaths;
+  const bool big_paths = a.cfg.max_paths > kDfsPaths || (a.dbg & LEO_DBG_PRUNE_SLOW);
   for (int e = blockIdx.x * blockDim.x + threadIdx.x; e < n; e += gridDim.x * blockDim.x) {
     bool ok = !big_paths && prune_one(k, p, a, e, stk, kDfsStack, arena, kDfsArena, vlen, vacc, kDfsPaths);
     if (!ok) {

@@ -1,27 +1,36 @@
 // sync.cu — vendor synchronization edges (depgraph.py:296-501).
 //
 //   amd    s_waitcnt:  exact chain enumeration (_scan_backward :312-348 with the
-//          _WaitcntState visitor :365-399): one thread per waiting instruction
+//          _WaitcntState visitor :365-399): one thread per (wait, counter)
 //          walks every simple backward block path (b0 pre-visited, forks inherit
 //          the remaining 4096-instruction budget); member operations appended at
 //          pending index >= level become edges; best_m drives the diagnostic.
+//          Instructions are scanned through a packed 32-bit word per instruction
+//          (waitcnt flag, counter values, membership bits), eight per batch of
+//          independent loads.
 //   nvidia barrier / intel SWSB setter search (_trace_setter :431-443): closed
 //          form — nearest setter before the wait in its own block, otherwise a
 //          node-weighted Dijkstra over setter-free predecessor blocks (b0
 //          excluded): a setter block p yields its last setter iff the cheapest
-//          path reaches it within the budget.  (Shortest paths are simple, so
-//          this equals the union over the reference's per-chain simple paths.)
+//          path reaches it within the budget.  Shortest paths are simple, so
+//          this equals the union over the reference's per-chain simple paths.
+//          Per-block "last setter of id" summaries make every Dijkstra node O(1).
 //
-// Raw (producer, wait) keys are appended to a buffer; k_sync_* then group them
-// by producer, sort + dedup per producer and append them after the raw/guard
-// edges in (producer, consumer) order (_materialize_sync :485-492).
+// Raw (producer, wait) keys are appended to a buffer; they are then grouped by
+// producer, sorted + deduplicated per producer and appended after the
+// raw/guard edges in (producer, consumer) order (_materialize_sync :485-492).
 #include "prims.cuh"
 
 namespace leo {
 
 constexpr int kSyncBudget = 4096;   // SYNC_SCAN_BUDGET depgraph.py:43
 
+// packed amd scan word
+constexpr uint32_t kWcNone = 0x3FF;
+constexpr uint32_t kWcIsWait = 1u << 20, kWcVm = 1u << 21, kWcLgkm = 1u << 22, kWcBig = 1u << 23;
+
 struct SyncArgs {
+  int32_t dbg;
   uint64_t* keys;            // raw (producer << 32 | consumer)
   int64_t key_cap;
   int32_t* key_count;
@@ -30,7 +39,52 @@ struct SyncArgs {
   int64_t slow_cap;
   LeoDiags diags;
   uint32_t* status;
+  const uint32_t* wcword;    // [N] amd packed scan words
+  const uint8_t* setword;    // [N] nvidia set mask (w|r) / intel set token (255 none)
+  const int32_t* lastset;    // [B * ids] last setter of id in block, -1 none
+  int32_t n_ids;             // 8 (nvidia, ids 1..6) or 32 (intel)
 };
+
+__global__ void k_sync_pack(KView k, uint32_t* __restrict__ wcword, uint8_t* __restrict__ setword) {
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < k.N; i += gridDim.x * blockDim.x) {
+    const uint8_t sk = k.sync_kind[i];
+    const uint32_t a = k.sync_a[i], b = k.sync_b[i];
+    if (k.dialect == LEO_AMD) {
+      uint32_t w = 0;
+      if (sk == LEO_SYNC_WAITCNT) {
+        w |= kWcIsWait;
+        uint32_t vm = a == LEO_NONE_U32 ? kWcNone : a, lg = b == LEO_NONE_U32 ? kWcNone : b;
+        if ((a != LEO_NONE_U32 && a >= kWcNone) || (b != LEO_NONE_U32 && b >= kWcNone)) w |= kWcBig;
+        w |= (min(vm, kWcNone)) | (min(lg, kWcNone) << 10);
+      } else {
+        w |= kWcNone | (kWcNone << 10);
+        if (kVmcnt & BIT(k.opclass[i])) w |= kWcVm;
+        if (kLgkmcnt & BIT(k.opclass[i])) w |= kWcLgkm;
+      }
+      wcword[i] = w;
+    } else if (k.dialect == LEO_NVIDIA) {
+      setword[i] = sk == LEO_SYNC_BARRIER ? (uint8_t)((a | (a >> 8)) & 0x7E) : 0;
+    } else {
+      setword[i] = (sk == LEO_SYNC_SWSB && a < 32) ? (uint8_t)a : 0xFF;
+    }
+  }
+}
+
+__global__ void k_block_setters(KView k, const uint8_t* __restrict__ setword, int n_ids,
+                                int32_t* __restrict__ lastset) {
+  for (int b = blockIdx.x * blockDim.x + threadIdx.x; b < k.B; b += gridDim.x * blockDim.x) {
+    int32_t* row = lastset + (size_t)b * n_ids;
+    for (int t = 0; t < n_ids; t++) row[t] = -1;
+    for (int x = k.blk_first[b]; x <= k.blk_last[b]; x++) {
+      const uint8_t s = setword[x];
+      if (k.dialect == LEO_NVIDIA) {
+        for (int id = 1; id <= 6; id++) if ((s >> id) & 1) row[id] = x;
+      } else if (s != 0xFF) {
+        row[s] = x;
+      }
+    }
+  }
+}
 
 LEO_DEV void sync_emit(const SyncArgs& a, int producer, int wait) {
   int s = atomicAdd(a.key_count, 1);
@@ -40,30 +94,57 @@ LEO_DEV void sync_emit(const SyncArgs& a, int producer, int wait) {
 
 struct Frame { int blk, q, m, a, budget; };
 
-// waitcnt visitor (depgraph.py:368-384); returns false to stop the chain
-LEO_DEV bool wc_visit(const KView& k, int x, int counter, uint32_t members, int level, int wait,
-                      int& m, int& a, const SyncArgs& sa, int32_t* seen, int& nseen, int seen_cap) {
-  if (k.sync_kind[x] == LEO_SYNC_WAITCNT) {
-    uint32_t v = counter == 0 ? k.sync_a[x] : k.sync_b[x];
-    if (v != LEO_NONE_U32) {
+struct WcState {
+  int counter, level, wait;
+  uint32_t member_bit;
+  int32_t seen[16];
+  int nseen;
+};
+
+// waitcnt visitor (depgraph.py:368-384) on a packed word; returns 0 to stop,
+// 1 to continue, -1 when the word needs the exact (unpacked) path.
+LEO_DEV int wc_visit(uint32_t w, int x, WcState& s, int& m, int& a, const SyncArgs& sa) {
+  if (w & kWcIsWait) {
+    if (w & kWcBig) return -1;
+    uint32_t v = s.counter == 0 ? (w & 0x3FF) : ((w >> 10) & 0x3FF);
+    if (v != kWcNone) {
       a = (a < 0) ? (int)v : min(a, (int)v);
-      if (a == 0) return false;
+      if (a == 0) return 0;
     }
-  } else if (members & BIT(k.opclass[x])) {
+  } else if (w & s.member_bit) {
     if (a != 0) {
-      if (m >= level) {   // pending[level:] -> edge (emitted once per wait when possible)
+      if (m >= s.level) {   // pending[level:] -> edge (emitted once per wait when possible)
         bool dup = false;
-        for (int t = 0; t < nseen; t++) if (seen[t] == x) { dup = true; break; }
+        for (int t = 0; t < s.nseen; t++) if (s.seen[t] == x) { dup = true; break; }
         if (!dup) {
-          if (nseen < seen_cap) seen[nseen++] = x;
-          sync_emit(sa, x, wait);
+          if (s.nseen < 16) s.seen[s.nseen++] = x;
+          sync_emit(sa, x, s.wait);
         }
       }
       m++;
-      if (a > 0) { a--; if (a == 0) return false; }
+      if (a > 0) { a--; if (a == 0) return 0; }
     }
   }
-  return true;
+  return 1;
+}
+
+// Scan instructions hi..lo backward (budget per chain).  Returns 0 stopped,
+// 1 ran off the block, -1 needs the exact path.
+LEO_DEV int wc_scan(const SyncArgs& sa, int hi, int lo, int& budget, WcState& s, int& m, int& a) {
+  for (int x = hi; x >= lo; x -= 8) {
+    uint32_t w[8];
+#pragma unroll
+    for (int t = 0; t < 8; t++) w[t] = (x - t >= lo) ? sa.wcword[x - t] : 0u;
+#pragma unroll
+    for (int t = 0; t < 8; t++) {
+      if (x - t < lo) return 1;
+      if (budget == 0) return 0;
+      budget--;
+      int r = wc_visit(w[t], x - t, s, m, a, sa);
+      if (r <= 0) return r;
+    }
+  }
+  return 1;
 }
 
 LEO_DEV bool on_path(const Frame* fr, int top, int blk) {
@@ -71,21 +152,20 @@ LEO_DEV bool on_path(const Frame* fr, int top, int blk) {
   return false;
 }
 
-// Enumerate all chains of one (wait, counter).  Returns false on frame overflow.
-LEO_DEV bool trace_waitcnt_one(const KView& k, int wait, int counter, int level, uint32_t members,
-                               const SyncArgs& sa, Frame* fr, int fcap, int& best_m) {
-  int32_t seen[16];
-  int nseen = 0;
+// Enumerate all chains of one (wait, counter).  Returns false on frame
+// overflow (re-run with a bigger frame stack) or an unpackable counter value.
+LEO_DEV bool trace_waitcnt_one(const KView& k, int wait, int counter, int level, const SyncArgs& sa,
+                               Frame* fr, int fcap, int& best_m) {
+  WcState s;
+  s.counter = counter; s.level = level; s.wait = wait;
+  s.member_bit = counter == 0 ? kWcVm : kWcLgkm;
+  s.nseen = 0;
   const int b0 = k.block_of[wait];
   int m = 0, a = -1, budget = kSyncBudget;
-  bool stopped = false;
-  for (int x = wait - 1; x >= k.blk_first[b0]; x--) {
-    if (budget == 0) { stopped = true; break; }
-    budget--;
-    if (!wc_visit(k, x, counter, members, level, wait, m, a, sa, seen, nseen, 16)) { stopped = true; break; }
-  }
+  int r = wc_scan(sa, wait - 1, k.blk_first[b0], budget, s, m, a);
+  if (r < 0) return false;
   best_m = 0;
-  if (stopped) { best_m = m; return true; }
+  if (r == 0) { best_m = m; return true; }
   int top = 0;
   fr[top++] = Frame{b0, k.pred_ptr[b0], m, a, budget};
   {
@@ -101,11 +181,70 @@ LEO_DEV bool trace_waitcnt_one(const KView& k, int wait, int counter, int level,
       if (!on_path(fr, top, c)) { p = c; break; }
     }
     if (p < 0) { top--; continue; }
+    m = f.m; a = f.a; budget = f.budget;
+    r = wc_scan(sa, k.blk_last[p], k.blk_first[p], budget, s, m, a);
+    if (r < 0) return false;
+    if (r == 0) { best_m = max(best_m, m); continue; }
+    if (top == fcap) return false;
+    fr[top++] = Frame{p, k.pred_ptr[p], m, a, budget};
+    bool any = false;
+    for (int q = k.pred_ptr[p]; q < k.pred_ptr[p + 1] && !any; q++)
+      if (!on_path(fr, top, k.pred[q])) any = true;
+    if (!any) { best_m = max(best_m, m); top--; }
+  }
+  return true;
+}
+
+// ---- exact (unpacked) waitcnt walker for the slow path ----------------------
+LEO_DEV int wc_visit_exact(const KView& k, int x, WcState& s, int& m, int& a, const SyncArgs& sa) {
+  if (k.sync_kind[x] == LEO_SYNC_WAITCNT) {
+    uint32_t v = s.counter == 0 ? k.sync_a[x] : k.sync_b[x];
+    if (v != LEO_NONE_U32) {
+      long long nv = (a < 0) ? (long long)v : min((long long)a, (long long)v);
+      a = (int)min(nv, (long long)0x7FFFFFFF);
+      if (a == 0) return 0;
+    }
+  } else if ((s.counter == 0 ? kVmcnt : kLgkmcnt) & BIT(k.opclass[x])) {
+    if (a != 0) {
+      if (m >= s.level) sync_emit(sa, x, s.wait);
+      m++;
+      if (a > 0) { a--; if (a == 0) return 0; }
+    }
+  }
+  return 1;
+}
+LEO_DEV bool trace_waitcnt_exact(const KView& k, int wait, int counter, int level, const SyncArgs& sa,
+                                 Frame* fr, int fcap, int& best_m) {
+  WcState s;
+  s.counter = counter; s.level = level; s.wait = wait; s.nseen = 0;
+  const int b0 = k.block_of[wait];
+  int m = 0, a = -1, budget = kSyncBudget;
+  bool stopped = false;
+  for (int x = wait - 1; x >= k.blk_first[b0]; x--) {
+    if (budget == 0) { stopped = true; break; }
+    budget--;
+    if (!wc_visit_exact(k, x, s, m, a, sa)) { stopped = true; break; }
+  }
+  best_m = 0;
+  if (stopped) { best_m = m; return true; }
+  int top = 0;
+  fr[top++] = Frame{b0, k.pred_ptr[b0], m, a, budget};
+  bool any0 = false;
+  for (int q = k.pred_ptr[b0]; q < k.pred_ptr[b0 + 1]; q++) if (k.pred[q] != b0) any0 = true;
+  if (!any0) { best_m = m; return true; }
+  while (top > 0) {
+    Frame& f = fr[top - 1];
+    int p = -1;
+    while (f.q < k.pred_ptr[f.blk + 1]) {
+      int c = k.pred[f.q++];
+      if (!on_path(fr, top, c)) { p = c; break; }
+    }
+    if (p < 0) { top--; continue; }
     m = f.m; a = f.a; budget = f.budget; stopped = false;
     for (int x = k.blk_last[p]; x >= k.blk_first[p]; x--) {
       if (budget == 0) { stopped = true; break; }
       budget--;
-      if (!wc_visit(k, x, counter, members, level, wait, m, a, sa, seen, nseen, 16)) { stopped = true; break; }
+      if (!wc_visit_exact(k, x, s, m, a, sa)) { stopped = true; break; }
     }
     if (stopped) { best_m = max(best_m, m); continue; }
     if (top == fcap) return false;
@@ -118,53 +257,98 @@ LEO_DEV bool trace_waitcnt_one(const KView& k, int wait, int counter, int level,
   return true;
 }
 
-LEO_DEV bool is_setter(const KView& k, int x, int kind, int id) {
-  if (kind == LEO_EK_MEM_BARRIER)
-    return k.sync_kind[x] == LEO_SYNC_BARRIER && (((k.sync_a[x] | (k.sync_a[x] >> 8)) >> id) & 1);
-  return k.sync_kind[x] == LEO_SYNC_SWSB && k.sync_a[x] == (uint32_t)id;
+LEO_DEV bool set_hit(int dialect, uint8_t s, int id) {
+  return dialect == LEO_NVIDIA ? ((s >> id) & 1) : (s == (uint8_t)id);
 }
 
-// Setter search for one (wait, id).  Dijkstra state in (node, dist, done)
-// arrays of capacity ncap.  Returns -1 on overflow, else found (0/1).
-LEO_DEV int setter_search(const KView& k, int wait, int kind, int id, const SyncArgs& sa,
-                          int32_t* node, int32_t* dist, uint8_t* done, int ncap) {
-  const int b0 = k.block_of[wait];
-  const int first0 = k.blk_first[b0];
-  int lim = min(wait - first0, kSyncBudget);
-  for (int x = wait - 1; x >= wait - lim; x--)
-    if (is_setter(k, x, kind, id)) { sync_emit(sa, x, wait); return 1; }
-  const int cost0 = wait - first0;
-  if (cost0 >= kSyncBudget) return 0;
-  int n = 0, found = 0;
-  auto relax = [&](int blk, int d) -> bool {
-    if (blk == b0) return true;
+// Dijkstra state: a small list (fast path) or block-indexed stamp arrays +
+// binary heap (slow path).
+struct DijSmall {
+  int32_t* node; int32_t* dist; uint8_t* done; int cap, n;
+  LEO_DEV bool relax(int blk, int d) {
     for (int t = 0; t < n; t++)
       if (node[t] == blk) { if (!done[t] && d < dist[t]) dist[t] = d; return true; }
-    if (n == ncap) return false;
+    if (n == cap) return false;
     node[n] = blk; dist[n] = d; done[n] = 0; n++;
     return true;
-  };
-  for (int q = k.pred_ptr[b0]; q < k.pred_ptr[b0 + 1]; q++)
-    if (!relax(k.pred[q], cost0)) return -1;
-  while (true) {
+  }
+  LEO_DEV bool pop(int& blk, int& d) {
     int best = -1;
     for (int t = 0; t < n; t++)
       if (!done[t] && (best < 0 || dist[t] < dist[best])) best = t;
-    if (best < 0) break;
-    done[best] = 1;
-    const int p = node[best], d = dist[best];
-    if (d >= kSyncBudget) break;                       // entering with no budget left
-    int s = -1;
-    for (int x = k.blk_last[p]; x >= k.blk_first[p]; x--)
-      if (is_setter(k, x, kind, id)) { s = x; break; }
+    if (best < 0) return false;
+    done[best] = 1; blk = node[best]; d = dist[best];
+    return true;
+  }
+};
+struct DijHeap {
+  int32_t* stamp; int32_t* dist; uint64_t* heap; int stamp_val, n, cap;
+  LEO_DEV bool relax(int blk, int d) {
+    if (stamp[blk] == -stamp_val) return true;              // finalised
+    if (stamp[blk] == stamp_val && dist[blk] <= d) return true;
+    stamp[blk] = stamp_val; dist[blk] = d;
+    if (n == cap) return false;
+    int i = n++;
+    uint64_t key = ((uint64_t)(uint32_t)d << 32) | (uint32_t)blk;
+    while (i > 0) { int p = (i - 1) >> 1; if (heap[p] <= key) break; heap[i] = heap[p]; i = p; }
+    heap[i] = key;
+    return true;
+  }
+  LEO_DEV bool pop(int& blk, int& d) {
+    while (n > 0) {
+      uint64_t top = heap[0];
+      uint64_t last = heap[--n];
+      int i = 0;
+      while (true) {
+        int c = 2 * i + 1;
+        if (c >= n) break;
+        if (c + 1 < n && heap[c + 1] < heap[c]) c++;
+        if (heap[c] >= last) break;
+        heap[i] = heap[c]; i = c;
+      }
+      if (n > 0) heap[i] = last;
+      blk = (int)(uint32_t)top; d = (int)(top >> 32);
+      if (stamp[blk] == stamp_val && dist[blk] == d) { stamp[blk] = -stamp_val; return true; }
+    }
+    return false;
+  }
+};
+
+// Setter search for one (wait, id).  Returns -1 on overflow, else found (0/1).
+template <class Dij>
+LEO_DEV int setter_search(const KView& k, int wait, int id, const SyncArgs& sa, Dij& dj) {
+  const int b0 = k.block_of[wait];
+  const int first0 = k.blk_first[b0];
+  const int lo = wait - min(wait - first0, kSyncBudget);
+  for (int x = wait - 1; x >= lo; x -= 8) {                 // nearest setter in b0
+    uint8_t w[8];
+#pragma unroll
+    for (int t = 0; t < 8; t++) w[t] = (x - t >= lo) ? sa.setword[x - t] : 0;
+#pragma unroll
+    for (int t = 0; t < 8; t++)
+      if (x - t >= lo && set_hit(k.dialect, w[t], id)) { sync_emit(sa, x - t, wait); return 1; }
+  }
+  const int cost0 = wait - first0;
+  if (cost0 >= kSyncBudget) return 0;
+  int found = 0;
+  for (int q = k.pred_ptr[b0]; q < k.pred_ptr[b0 + 1]; q++) {
+    const int p = k.pred[q];
+    if (p != b0 && !dj.relax(p, cost0)) return -1;
+  }
+  int p, d;
+  while (dj.pop(p, d)) {
+    if (d >= kSyncBudget) break;                             // entering with no budget left
+    const int s = sa.lastset[(size_t)p * sa.n_ids + id];
     if (s >= 0) {
       if (d + (k.blk_last[p] - s + 1) <= kSyncBudget) { sync_emit(sa, s, wait); found = 1; }
       continue;
     }
     const int nd = d + (k.blk_last[p] - k.blk_first[p] + 1);
     if (nd >= kSyncBudget) continue;
-    for (int q = k.pred_ptr[p]; q < k.pred_ptr[p + 1]; q++)
-      if (!relax(k.pred[q], nd)) return -1;
+    for (int q = k.pred_ptr[p]; q < k.pred_ptr[p + 1]; q++) {
+      const int pp = k.pred[q];
+      if (pp != b0 && !dj.relax(pp, nd)) return -1;
+    }
   }
   return found;
 }
@@ -172,17 +356,18 @@ LEO_DEV int setter_search(const KView& k, int wait, int kind, int id, const Sync
 constexpr int kFrames = 24, kDij = 64;
 
 __host__ __device__ inline size_t sync_slow_bytes_per_worker(int B) {
-  return (((size_t)(B + 2) * (sizeof(Frame) + 9)) + 15) & ~(size_t)15;
+  // frames (B+2) + stamp/dist (B+2 each) + heap (4B+8 u64)
+  return ((size_t)(B + 2) * (sizeof(Frame) + 8) + (size_t)(4 * B + 16) * 8 + 255) & ~(size_t)255;
 }
 
 // One thread per instruction; sub-items: amd counters 0/1, nvidia barriers
 // 1..6, intel tokens 0..31.  Overflowing items go to the slow list.
 template <bool SLOW>
-__global__ void k_sync(KView k, SyncArgs a, int32_t* scratch, int nworkers) {
+__global__ void k_sync(KView k, SyncArgs a, char* scratch, int nworkers) {
   const int dialect = k.dialect;
   int n_items, stride, start;
   if (SLOW) {
-    n_items = min((int64_t)*a.slow_count, a.slow_cap);
+    n_items = (int)min((int64_t)*a.slow_count, a.slow_cap);
     start = blockIdx.x * blockDim.x + threadIdx.x;
     stride = nworkers;
     if (start >= nworkers) return;
@@ -195,17 +380,16 @@ __global__ void k_sync(KView k, SyncArgs a, int32_t* scratch, int nworkers) {
   int32_t lnode[SLOW ? 1 : kDij], ldist[SLOW ? 1 : kDij];
   uint8_t ldone[SLOW ? 1 : kDij];
   Frame* fr = lfr;
-  int32_t *node = lnode, *dist = ldist;
-  uint8_t* done = ldone;
-  int fcap = kFrames, ncap = kDij;
+  int fcap = kFrames;
+  int32_t *stamp = nullptr, *gdist = nullptr;
+  uint64_t* heap = nullptr;
   if (SLOW) {
-    const size_t per = sync_slow_bytes_per_worker(k.B);
-    char* base = (char*)scratch + (size_t)start * per;
+    char* base = scratch + (size_t)start * sync_slow_bytes_per_worker(k.B);
     fr = (Frame*)base;
-    node = (int32_t*)(base + (size_t)(k.B + 2) * sizeof(Frame));
-    dist = node + (k.B + 2);
-    done = (uint8_t*)(dist + (k.B + 2));
-    fcap = k.B + 2; ncap = k.B + 2;
+    stamp = (int32_t*)(base + (size_t)(k.B + 2) * sizeof(Frame));
+    gdist = stamp + (k.B + 2);
+    heap = (uint64_t*)(((uintptr_t)(gdist + (k.B + 2)) + 7) & ~(uintptr_t)7);
+    fcap = k.B + 2;
   }
   for (int t = start; t < n_items; t += stride) {
     int i, only = -1;
@@ -218,31 +402,41 @@ __global__ void k_sync(KView k, SyncArgs a, int32_t* scratch, int nworkers) {
         uint32_t lv = counter == 0 ? k.sync_a[i] : k.sync_b[i];
         if (lv == LEO_NONE_U32) continue;
         int best_m = 0;
-        if (!trace_waitcnt_one(k, i, counter, (int)lv, counter == 0 ? kVmcnt : kLgkmcnt, a, fr, fcap, best_m)) {
+        bool ok = SLOW ? trace_waitcnt_exact(k, i, counter, (int)min(lv, 0x7FFFFFFFu), a, fr, fcap, best_m)
+                       : (!(a.dbg & LEO_DBG_SYNC_SLOW) && lv < kWcNone &&
+                          trace_waitcnt_one(k, i, counter, (int)lv, a, fr, fcap, best_m));
+        if (!ok) {
           int s = atomicAdd(a.slow_count, 1);
           if (s < a.slow_cap) a.slow_list[s] = (i << 6) | counter;
           else atomicOr(a.status, (uint32_t)LEO_ST_SCRATCH_OVERFLOW);
           continue;
         }
-        if (best_m < (int)lv) diag_push(a.diags, a.status, LEO_DIAG_WAITCNT, i, counter, (int)lv, best_m, counter);
+        if ((long long)best_m < (long long)lv)
+          diag_push(a.diags, a.status, LEO_DIAG_WAITCNT, i, counter, (int)min(lv, 0x7FFFFFFFu), best_m, counter);
       }
     } else {
       uint32_t mask;
-      int kind;
       if (dialect == LEO_NVIDIA) {
         if (k.sync_kind[i] != LEO_SYNC_BARRIER) continue;
         mask = (k.sync_a[i] >> 16) & 0x7E;
-        kind = LEO_EK_MEM_BARRIER;
       } else {
         if (k.sync_kind[i] != LEO_SYNC_SWSB) continue;
         mask = k.sync_b[i];
-        kind = LEO_EK_MEM_SWSB;
       }
       while (mask) {
         int id = __ffs(mask) - 1;
         mask &= mask - 1;
         if (only >= 0 && only != id) continue;
-        int f = setter_search(k, i, kind, id, a, node, dist, done, ncap);
+        int f;
+        if (SLOW) {
+          DijHeap dj{stamp, gdist, heap, t + 1, 0, 4 * k.B + 8};
+          f = setter_search(k, i, id, a, dj);
+        } else if (a.dbg & LEO_DBG_SYNC_SLOW) {
+          f = -1;
+        } else {
+          DijSmall dj{lnode, ldist, ldone, kDij, 0};
+          f = setter_search(k, i, id, a, dj);
+        }
         if (f < 0) {
           int s = atomicAdd(a.slow_count, 1);
           if (s < a.slow_cap) a.slow_list[s] = (i << 6) | id;
@@ -255,8 +449,8 @@ __global__ void k_sync(KView k, SyncArgs a, int32_t* scratch, int nworkers) {
   }
 }
 
-template __global__ void k_sync<false>(KView, SyncArgs, int32_t*, int);
-template __global__ void k_sync<true>(KView, SyncArgs, int32_t*, int);
+template __global__ void k_sync<false>(KView, SyncArgs, char*, int);
+template __global__ void k_sync<true>(KView, SyncArgs, char*, int);
 
 // ---- group raw keys by producer, dedup, append after the raw/guard edges ----
 __global__ void k_key_hist(const uint64_t* __restrict__ keys, const int32_t* n_dev, int64_t cap,

@@ -108,8 +108,10 @@ class Caps:
 class Analyzer:
     """Owns output buffers for one kernel shape; runs the fused pipeline."""
 
-    def __init__(self, dk: DeviceKernel, device="cuda", caps: Caps | None = None):
+    def __init__(self, dk: DeviceKernel, device="cuda", caps: Caps | None = None,
+                 debug_flags: int = 0):
         self.tracer = None
+        self.debug_flags = debug_flags
         self.dk = dk
         self.device = torch.device(device)
         n = dk.n_instr
@@ -155,7 +157,7 @@ class Analyzer:
         s = self.caps.scratch_scale
         nu, n = self.n_use_units, self.dk.n_instr
         self.s_caps = abi.LeoCaps((4 * nu + 1024) * s, (6 * nu + 1024) * s, (2 * n + 1024) * s,
-                                  (n // 4 + 1024) * s, None)
+                                  (n // 4 + 1024) * s, None, self.debug_flags, 0)
         self.set_tracer(self.tracer)
         self.status_ptr = at(C_STATUS)
 
@@ -268,7 +270,8 @@ class Analyzer:
             status=int(np.uint32(c[C_STATUS])))
 
 
-def analyze_soa(ks, prof, cfg: abi.LeoConfig | None = None, samples=None, device="cuda") -> dict:
+def analyze_soa(ks, prof, cfg: abi.LeoConfig | None = None, samples=None, device="cuda",
+                debug_flags: int = 0) -> dict:
     """One-shot convenience: upload, run, download."""
     dk = DeviceKernel(ks, device)
     dp = DeviceProfile(prof, ks.n_instr, device)
@@ -276,7 +279,7 @@ def analyze_soa(ks, prof, cfg: abi.LeoConfig | None = None, samples=None, device
     if samples is not None:
         pc, cat, lut = samples
         ds = DeviceSamples(pc, cat, lut, device)
-    an = Analyzer(dk, device)
+    an = Analyzer(dk, device, debug_flags=debug_flags)
     an.run(dp, cfg or abi.make_config(dialect=ks.dialect), ds)
     r = an.result()
     if ds is not None:

@@ -106,3 +106,20 @@ def test_device_full_c5_properties(cuda):
     inside = lv >= 0
     assert np.all(best[inside & (lv > 0)] == lv[inside & (lv > 0)])
     assert deeper.sum() >= 0
+
+
+@pytest.mark.parametrize("flags", [1, 2 | 4 | 8 | 16])
+@pytest.mark.parametrize("fname", ["corpus_c1.npz", "random.npz", "synth.npz"])
+def test_device_fallback_tiers_match_golden(fname, flags, golden_cases, cuda):
+    """Every work item forced onto the larger tiers (warp / global-scratch
+    reach search, exact sync walker, global-scratch DFS, global self-blame BFS)
+    must give the same bits as the fast tiers."""
+    from paper_2604_20032_b200 import device
+    bad = []
+    for ks, pf, cfg, exp in golden_cases[fname]:
+        r = device.analyze_soa(ks, pf, golden_io.config_of(cfg, ks.dialect), device=cuda,
+                               debug_flags=flags)
+        errs = parity.compare(exp, device_outputs(ks, r), rel=0.0, line_rel=1e-9)
+        if errs:
+            bad.append((ks.name, errs[:2]))
+    assert not bad, f"{len(bad)} cases differ with debug flags {flags}; first: {bad[:3]}"
