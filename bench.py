@@ -209,6 +209,7 @@ def run_ours(args, ws, rank, local):
     counts = an.run(dp, cfg, ds)               # sizes buffers (grow + re-run on overflow)
     res = an.result()
     assert res["status"] == 0
+    eager_res = res
 
     def allreduce_lines():
         if ws > 1:
@@ -274,6 +275,8 @@ def run_ours(args, ws, rank, local):
     value = ws * S * args.steps / (T_max / 1e3)
     res = an.result()
     assert res["status"] == 0
+    for key in ("bprod", "bcons", "bmeta", "pprod", "pmeta", "e_stalled", "e_edge", "e_blame", "level"):
+        assert np.array_equal(res[key], eager_res[key]), f"graph replay changed {key}"
 
     # roofline of the dominant kernel (algorithmic bytes / live event time)
     peak, peak_src = peaks()

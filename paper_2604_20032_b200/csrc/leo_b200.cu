@@ -88,6 +88,31 @@ struct Arena {
 
 inline int64_t pick(int64_t hint, int64_t dflt) { return hint > 0 ? hint : dflt; }
 
+// Side streams + events for fork/join concurrency inside one pipeline call
+// (independent stages run as parallel branches; under stream capture they
+// become parallel branches of the CUDA graph).  Created once per host thread.
+struct SidePool {
+  cudaStream_t s[3] = {nullptr, nullptr, nullptr};
+  cudaEvent_t e[8] = {};
+  bool ok = false;
+  void init() {
+    if (ok) return;
+    for (auto& x : s) cudaStreamCreateWithFlags(&x, cudaStreamNonBlocking);
+    for (auto& x : e) cudaEventCreateWithFlags(&x, cudaEventDisableTiming);
+    ok = true;
+  }
+};
+SidePool& side_pool() {
+  static thread_local SidePool p;
+  p.init();
+  return p;
+}
+// `to` waits for all work enqueued so far on `from`
+inline void link_streams(cudaStream_t from, cudaStream_t to, cudaEvent_t ev) {
+  cudaEventRecord(ev, from);
+  cudaStreamWaitEvent(to, ev, 0);
+}
+
 // kernels that take more than 48 KiB of dynamic shared memory (set once)
 void set_smem_attributes() {
   static bool done = false;
@@ -133,7 +158,7 @@ int build_graph_impl(const LeoKernel* kk, const LeoCaps* caps, LeoEdges* out, Le
   int32_t *ucnt, *dcnt, *use_ptr, *def_ptr, *ev_res, *q_block, *q_unit, *q_list, *q_off, *q_len, *qres;
   int32_t *ctr, *slow_list, *slow2, *slow3, *cand_cnt, *cand_off, *uniq, *eoff, *ldtab, *scan_tmp, *gtab = nullptr;
   int4* brec;
-  int32_t *pcnt, *poff, *pcur, *puniq, *puoff, *reach_scr;
+  int32_t *pcnt, *poff, *pcur, *puniq, *puoff, *reach_scr, *scan_tmp2, *wlist;
   uint64_t *cand, *skeys, *ssorted;
   uint32_t* wcword;
   uint8_t* setword;
@@ -148,6 +173,8 @@ int build_graph_impl(const LeoKernel* kk, const LeoCaps* caps, LeoEdges* out, Le
   ar.want(&pcnt, N); ar.want(&poff, N + 1); ar.want(&pcur, N); ar.want(&puniq, N); ar.want(&puoff, N + 1);
   ar.want(&scan_tmp, scan_scratch_ints(std::max<int64_t>(std::max<int64_t>(N, cap_cand), 1)) + 64);
   ar.want(&reach_scr, (int64_t)RW * 3 * (B + 1));
+  ar.want(&scan_tmp2, scan_scratch_ints(std::max<int64_t>(N, 1)) + 64);
+  ar.want(&wlist, N);
   ar.want(&sync_scr, (int64_t)SW * sync_slow_bytes_per_worker(B));
   const int n_ids = k.dialect == LEO_INTEL ? 32 : 8;
   ar.want(&wcword, N); ar.want(&setword, N); ar.want(&lastset, (int64_t)B * n_ids);
@@ -156,10 +183,32 @@ int build_graph_impl(const LeoKernel* kk, const LeoCaps* caps, LeoEdges* out, Le
   // counters: 0 q_count, 1 qres_count, 2 reach slow, 3 sync keys, 4 sync slow, 5 n_regular, 6 n_sync
   cudaMemsetAsync(ctr, 0, 16 * sizeof(int32_t), st);
   cudaMemsetAsync(reach_scr, 0, (size_t)RW * 3 * (B + 1) * sizeof(int32_t), st);
-  cudaMemsetAsync(pcnt, 0, (size_t)std::max(N, 1) * 4, st);
-  cudaMemsetAsync(pcur, 0, (size_t)std::max(N, 1) * 4, st);
-
   const int T = 256;
+  // fork: vendor sync tracing runs on a side stream, concurrently with the
+  // register dataflow chain below
+  SidePool& sp = side_pool();
+  cudaStream_t s_sync = sp.s[0];
+  link_streams(st, s_sync, sp.e[0]);
+  const int kind = k.dialect == LEO_AMD ? LEO_EK_MEM_WAITCNT : k.dialect == LEO_NVIDIA ? LEO_EK_MEM_BARRIER : LEO_EK_MEM_SWSB;
+  {
+    cudaStream_t st = s_sync;   // shadows the caller's stream for the TRACED scopes
+    cudaMemsetAsync(pcnt, 0, (size_t)std::max(N, 1) * 4, st);
+    cudaMemsetAsync(pcur, 0, (size_t)std::max(N, 1) * 4, st);
+    cudaMemsetAsync(sync_scr, 0, (size_t)SW * sync_slow_bytes_per_worker(B), st);
+    TRACED(KID_SYNC_PACK, k_sync_pack<<<grid_for(N, T), T, 0, st>>>(k, wcword, setword));
+    if (k.dialect != LEO_AMD && B > 0)
+      TRACED(KID_SYNC_PACK, k_block_setters<<<grid_for(B, T), T, 0, st>>>(k, setword, n_ids, lastset));
+    TRACED(KID_SYNC_PACK, k_wait_list<<<grid_for(N, T), T, 0, st>>>(k, wlist, &ctr[8]));
+    SyncArgs sa{caps ? caps->debug_flags : 0, skeys, cap_sync, &ctr[3], slow2, &ctr[4], cap_slow, *diags, status,
+                wcword, setword, lastset, n_ids, wlist, &ctr[8]};
+    TRACED(KID_SYNC, k_sync<false><<<grid_for(N, 64), 64, 0, st>>>(k, sa, nullptr, 0));
+    TRACED(KID_SYNC_SLOW, k_sync<true><<<1, SW, 0, st>>>(k, sa, sync_scr, SW));
+    TRACED(KID_KEY_HIST, k_key_hist<<<grid_for(cap_sync, T), T, 0, st>>>(skeys, &ctr[3], cap_sync, pcnt));
+    TRACED(KID_SCAN, scan_exclusive(pcnt, poff, nullptr, N, scan_tmp2, nullptr, st));
+    TRACED(KID_KEY_SCATTER, k_key_scatter<<<grid_for(cap_sync, T), T, 0, st>>>(skeys, &ctr[3], cap_sync, poff, pcur, ssorted));
+    TRACED(KID_SEGSORT, segsort_unique_u64<<<grid_for(N, 128), 128, 0, st>>>(ssorted, poff, pcnt, nullptr, N, puniq));
+    TRACED(KID_SCAN, scan_exclusive(puniq, puoff, nullptr, N, scan_tmp2, &ctr[6], st));
+  }
   TRACED(KID_UNIT_COUNTS, k_unit_counts<<<grid_for(N, T), T, 0, st>>>(k, ucnt, dcnt));
   TRACED(KID_SCAN, scan_exclusive(ucnt, use_ptr, nullptr, N, scan_tmp, nullptr, st));
   TRACED(KID_SCAN, scan_exclusive(dcnt, def_ptr, nullptr, N, scan_tmp, nullptr, st));
@@ -188,19 +237,7 @@ int build_graph_impl(const LeoKernel* kk, const LeoCaps* caps, LeoEdges* out, Le
   TRACED(KID_SCAN, scan_exclusive(uniq, eoff, nullptr, N, scan_tmp, &ctr[5], st));
   TRACED(KID_LINK_EMIT, k_link_emit<<<grid_for(N, T), T, 0, st>>>(k, cand_off, cand, uniq, eoff, *out, status));
 
-  cudaMemsetAsync(sync_scr, 0, (size_t)SW * sync_slow_bytes_per_worker(B), st);
-  TRACED(KID_SYNC_PACK, k_sync_pack<<<grid_for(N, T), T, 0, st>>>(k, wcword, setword));
-  if (k.dialect != LEO_AMD && B > 0)
-    TRACED(KID_SYNC_PACK, k_block_setters<<<grid_for(B, T), T, 0, st>>>(k, setword, n_ids, lastset));
-  SyncArgs sa{caps ? caps->debug_flags : 0, skeys, cap_sync, &ctr[3], slow2, &ctr[4], cap_slow, *diags, status, wcword, setword, lastset, n_ids};
-  TRACED(KID_SYNC, k_sync<false><<<grid_for(N, 128), 128, 0, st>>>(k, sa, nullptr, 0));
-  TRACED(KID_SYNC_SLOW, k_sync<true><<<1, SW, 0, st>>>(k, sa, sync_scr, SW));
-  TRACED(KID_KEY_HIST, k_key_hist<<<grid_for(cap_sync, T), T, 0, st>>>(skeys, &ctr[3], cap_sync, pcnt));
-  TRACED(KID_SCAN, scan_exclusive(pcnt, poff, nullptr, N, scan_tmp, nullptr, st));
-  TRACED(KID_KEY_SCATTER, k_key_scatter<<<grid_for(cap_sync, T), T, 0, st>>>(skeys, &ctr[3], cap_sync, poff, pcur, ssorted));
-  TRACED(KID_SEGSORT, segsort_unique_u64<<<grid_for(N, 128), 128, 0, st>>>(ssorted, poff, pcnt, nullptr, N, puniq));
-  TRACED(KID_SCAN, scan_exclusive(puniq, puoff, nullptr, N, scan_tmp, &ctr[6], st));
-  const int kind = k.dialect == LEO_AMD ? LEO_EK_MEM_WAITCNT : k.dialect == LEO_NVIDIA ? LEO_EK_MEM_BARRIER : LEO_EK_MEM_SWSB;
+  link_streams(s_sync, st, sp.e[1]);   // join
   TRACED(KID_SYNC_EMIT, k_sync_emit<<<grid_for(N, T), T, 0, st>>>(N, kind, ssorted, poff, puniq, puoff, &ctr[5], *out, status));
   TRACED(KID_EDGE_TOTALS, k_edge_totals<<<1, 1, 0, st>>>(&ctr[5], &ctr[6], *out, status));
   ar.release();
@@ -448,25 +485,35 @@ int leo_analyze(const LeoKernel* k, const LeoProfile* p, const LeoSamples* sampl
   if (int e = check_kernel(k)) return e;
   if (!cfg) return -3;
   cudaStream_t st = (cudaStream_t)stream;
+  SidePool& sp = side_pool();
+  LeoTrace* tr = caps ? caps->trace : nullptr;
+  // stage-0 binning only feeds pruning and blame: run it beside build_graph
   if (samples) {
-    int r = bin_impl(samples, k->n_instr, (int32_t*)p->lat, (int32_t*)p->cls_cnt, caps ? caps->trace : nullptr, st);
+    cudaStream_t s_bin = sp.s[1];
+    link_streams(st, s_bin, sp.e[2]);
+    int r = bin_impl(samples, k->n_instr, (int32_t*)p->lat, (int32_t*)p->cls_cnt, tr, s_bin);
     if (r) return r;
   }
   int r = build_graph_impl(k, caps, base, diags, status, st);
   if (r) return r;
+  if (samples) link_streams(sp.s[1], st, sp.e[3]);
   r = prune_impl(k, p, cfg, base, pruned, paths, diags, caps, status, st);
   if (r) return r;
   Arena ar{st};
   IncomingBufs ib;
   want_incoming(ar, ib, k->n_instr, pruned->capacity);
   LEO_CUDA_CHECK(ar.commit());
-  LeoTrace* tr = caps ? caps->trace : nullptr;
   Incoming inc = build_incoming(ib, k->n_instr, pruned, true, tr, st);
-  if (slice_level && slice_bitmap) {
-    r = slice_impl(k, p, pruned, inc, slice_bitmap, slice_level, tr, st);
+  // the slice and blame attribution both read the pruned incoming CSR: run
+  // them as parallel branches
+  const bool do_slice = slice_level && slice_bitmap;
+  if (do_slice) {
+    link_streams(st, sp.s[2], sp.e[4]);
+    r = slice_impl(k, p, pruned, inc, slice_bitmap, slice_level, tr, sp.s[2]);
     if (r) { ar.release(); return r; }
   }
   r = blame_impl(k, p, pruned, paths, base, inc, line_id, n_lines, blame, line_blame, line_stall, caps, status, st);
+  if (do_slice) link_streams(sp.s[2], st, sp.e[5]);
   ar.release();
   return r;
 }

@@ -43,6 +43,8 @@ struct SyncArgs {
   const uint8_t* setword;    // [N] nvidia set mask (w|r) / intel set token (255 none)
   const int32_t* lastset;    // [B * ids] last setter of id in block, -1 none
   int32_t n_ids;             // 8 (nvidia, ids 1..6) or 32 (intel)
+  const int32_t* wait_list;  // compact waiting instructions
+  const int32_t* wait_count;
 };
 
 __global__ void k_sync_pack(KView k, uint32_t* __restrict__ wcword, uint8_t* __restrict__ setword) {
@@ -360,8 +362,27 @@ __host__ __device__ inline size_t sync_slow_bytes_per_worker(int B) {
   return ((size_t)(B + 2) * (sizeof(Frame) + 8) + (size_t)(4 * B + 16) * 8 + 255) & ~(size_t)255;
 }
 
-// One thread per instruction; sub-items: amd counters 0/1, nvidia barriers
-// 1..6, intel tokens 0..31.  Overflowing items go to the slow list.
+// compact list of waiting instructions (so no lane idles on non-waits)
+__global__ void k_wait_list(KView k, int32_t* __restrict__ list, int32_t* count) {
+  for (int i0 = blockIdx.x * blockDim.x; i0 < k.N; i0 += gridDim.x * blockDim.x) {
+    const int i = i0 + threadIdx.x;
+    bool w = false;
+    if (i < k.N) {
+      const uint8_t sk = k.sync_kind[i];
+      if (k.dialect == LEO_AMD) w = sk == LEO_SYNC_WAITCNT;
+      else if (k.dialect == LEO_NVIDIA) w = sk == LEO_SYNC_BARRIER && ((k.sync_a[i] >> 16) & 0x7E);
+      else w = sk == LEO_SYNC_SWSB && k.sync_b[i] != 0;
+    }
+    const unsigned m = __ballot_sync(0xffffffffu, w);
+    int base = 0;
+    if ((threadIdx.x & 31) == 0 && m) base = atomicAdd(count, __popc(m));
+    base = __shfl_sync(0xffffffffu, base, 0);
+    if (w) list[base + __popc(m & ((1u << (threadIdx.x & 31)) - 1))] = i;
+  }
+}
+
+// One thread per waiting instruction; sub-items: amd counters 0/1, nvidia
+// barriers 1..6, intel tokens 0..31.  Overflowing items go to the slow list.
 template <bool SLOW>
 __global__ void k_sync(KView k, SyncArgs a, char* scratch, int nworkers) {
   const int dialect = k.dialect;
@@ -372,7 +393,7 @@ __global__ void k_sync(KView k, SyncArgs a, char* scratch, int nworkers) {
     stride = nworkers;
     if (start >= nworkers) return;
   } else {
-    n_items = k.N;
+    n_items = *a.wait_count;
     start = blockIdx.x * blockDim.x + threadIdx.x;
     stride = gridDim.x * blockDim.x;
   }
@@ -394,7 +415,7 @@ __global__ void k_sync(KView k, SyncArgs a, char* scratch, int nworkers) {
   for (int t = start; t < n_items; t += stride) {
     int i, only = -1;
     if (SLOW) { int it = a.slow_list[t]; i = it >> 6; only = it & 63; }
-    else i = t;
+    else i = a.wait_list[t];
     if (dialect == LEO_AMD) {
       if (k.sync_kind[i] != LEO_SYNC_WAITCNT) continue;
       for (int counter = 0; counter < 2; counter++) {   // vmcnt before lgkmcnt (:410-415)
