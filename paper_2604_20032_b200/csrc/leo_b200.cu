@@ -349,6 +349,7 @@ int blame_impl(const LeoKernel* kk, const LeoProfile* pp, const LeoEdges* pruned
   ar.want(&slow_scr, (int64_t)BW * 2 * (N + 1)); ar.want(&jtotal, N); ar.want(&jnsum, N);
   LEO_CUDA_CHECK(ar.commit());
   cudaMemsetAsync(ctr, 0, 16, st);
+  cudaMemsetAsync(slow_scr, 0, (size_t)BW * 2 * (N + 1) * sizeof(int32_t), st);   // stamps
   Incoming binc = build_incoming(bb, N, base, false, tr, st);   // RAW edges only
   BlameArgs a{caps ? caps->debug_flags : 0, p, pruned->prod, pruned->meta, paths->dist, inc, binc.rbeg, binc.rend, base->prod, base->meta,
               ecount, self_sub, jtotal, jnsum, eoff, *out, slow_list, &ctr[0], cap_slow, status};
