@@ -138,6 +138,8 @@ typedef struct LeoConfig {
   int32_t  max_paths;         /* DEFAULT_MAX_PATHS 64 */
   int32_t  max_depth;         /* DEFAULT_MAX_DEPTH 512 */
   double   threshold[16];     /* LatencyTable.get per OpcodeClass (fallback = max) */
+  int32_t  consumer_lo;       /* stalled-PC sharding: this call owns consumers          */
+  int32_t  consumer_hi;       /*   [lo, hi); hi <= 0 means all (single-GPU / replica)   */
 } LeoConfig;
 
 /* ---- edge list (DepEdge depgraph.py:77-91) -------------------------------- */

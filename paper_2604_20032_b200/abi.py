@@ -39,6 +39,7 @@ class LeoConfig(C.Structure):
     _fields_ = [
         ("stage_mask", C.c_uint32), ("prune_exec", C.c_int32), ("max_paths", C.c_int32),
         ("max_depth", C.c_int32), ("threshold", C.c_double * 16),
+        ("consumer_lo", C.c_int32), ("consumer_hi", C.c_int32),
     ]
 
 
@@ -86,8 +87,10 @@ ST_BLAME_OVERFLOW, ST_SCRATCH_OVERFLOW, ST_BAD_INPUT = 8, 16, 32
 
 
 def make_config(stage_mask=(1, 2, 3, 4), prune_exec=False, max_paths=64, max_depth=512,
-                thresholds=None, dialect="nvidia") -> LeoConfig:
+                thresholds=None, dialect="nvidia", consumer_range=None) -> LeoConfig:
     cfg = LeoConfig()
+    if consumer_range is not None:
+        cfg.consumer_lo, cfg.consumer_hi = int(consumer_range[0]), int(consumer_range[1])
     m = 0
     for s in stage_mask:
         if 1 <= int(s) <= 4:

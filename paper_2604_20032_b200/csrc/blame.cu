@@ -265,6 +265,7 @@ LEO_DEV int traces_to_load(const KView& k, const int32_t* brbeg, const int32_t* 
 
 struct BlameArgs {
   int32_t dbg;
+  Range own;
   PView p;
   const int32_t* pprod;
   const uint32_t* pmeta;
@@ -310,7 +311,7 @@ __global__ void k_blame(KView k, BlameArgs a) {
     const int lat = a.p.lat[j];
     const double s_j = (double)((int64_t)lat * a.p.period);
     if (PASS == 0) { a.ecount[j] = 0; a.self_sub[j] = -1; }
-    if (s_j == 0) continue;
+    if (s_j == 0 || !a.own.has(j)) continue;
     const int deg = a.inc.deg(j);
     if (PASS == 0) {
       bool self = deg == 0;
@@ -418,7 +419,7 @@ __global__ void k_selfblame_slow(KView k, BlameArgs a, int32_t* scratch, int nwo
 __global__ void k_blame_count(const int32_t* eoff, int N, LeoBlame out) { *out.count = eoff[N]; }
 
 // ---- per-source-line rollup -----------------------------------------------------
-__global__ void k_lines(KView k, PView p, const int32_t* __restrict__ pprod, LeoBlame b,
+__global__ void k_lines(KView k, PView p, Range own, const int32_t* __restrict__ pprod, LeoBlame b,
                         const int32_t* __restrict__ line_id, double* __restrict__ line_blame,
                         double* __restrict__ line_stall) {
   const int n = min(*b.count, b.capacity);
@@ -430,7 +431,7 @@ __global__ void k_lines(KView k, PView p, const int32_t* __restrict__ pprod, Leo
   }
   for (int j = blockIdx.x * blockDim.x + threadIdx.x; j < k.N; j += stride) {
     int lat = p.lat[j];
-    if (lat) atomicAdd(&line_stall[line_id[j]], (double)((int64_t)lat * p.period));
+    if (lat && own.has(j)) atomicAdd(&line_stall[line_id[j]], (double)((int64_t)lat * p.period));
   }
 }
 

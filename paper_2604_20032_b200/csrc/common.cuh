@@ -61,6 +61,12 @@ inline KView make_kview(const LeoKernel* k) {
   return v;
 }
 
+// consumer ownership under stalled-PC sharding (LeoConfig.consumer_lo/hi)
+struct Range {
+  int lo, hi;
+  LEO_DEV bool has(int j) const { return hi <= 0 || (j >= lo && j < hi); }
+};
+
 LEO_DEV int unit_of(const KView& k, uint32_t r) { return k.unit_base[op_class(r)] + op_index(r); }
 
 // ---- diagnostics ------------------------------------------------------------

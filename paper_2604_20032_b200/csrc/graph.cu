@@ -410,6 +410,7 @@ struct LinkArgs {
   int64_t cand_cap;
   LeoDiags diags;
   uint32_t* status;
+  Range own;
 };
 
 LEO_DEV uint64_t link_key(int producer, int kind, uint32_t r) {
@@ -444,7 +445,7 @@ __global__ void k_link(KView k, LinkArgs a) {
           else cnt += L;
         }
       }
-      if (!MODE && !found)   // depgraph.py:208-210 — no unit of the ref has a def
+      if (!MODE && !found && a.own.has(i))   // depgraph.py:208-210 — no unit of the ref has a def
         diag_push(a.diags, a.status, LEO_DIAG_UNRESOLVED, i, (int)r, 0, 0, q - k.opnd_ptr[i]);
     }
     if (!MODE) a.cand_cnt[i] = cnt;

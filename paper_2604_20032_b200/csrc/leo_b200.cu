@@ -134,7 +134,7 @@ int check_kernel(const LeoKernel* k) {
 // ---------------------------------------------------------------------------
 // build_graph
 int build_graph_impl(const LeoKernel* kk, const LeoCaps* caps, LeoEdges* out, LeoDiags* diags,
-                     uint32_t* status, cudaStream_t st) {
+                     uint32_t* status, cudaStream_t st, Range own = Range{0, 0}) {
   LeoTrace* tr = caps ? caps->trace : nullptr;
   KView k = make_kview(kk);
   const int N = k.N, B = k.B, U = k.U;
@@ -198,7 +198,7 @@ int build_graph_impl(const LeoKernel* kk, const LeoCaps* caps, LeoEdges* out, Le
     TRACED(KID_SYNC_PACK, k_sync_pack<<<grid_for(N, T), T, 0, st>>>(k, wcword, setword));
     if (k.dialect != LEO_AMD && B > 0)
       TRACED(KID_SYNC_PACK, k_block_setters<<<grid_for(B, T), T, 0, st>>>(k, setword, n_ids, lastset));
-    TRACED(KID_SYNC_PACK, k_wait_list<<<grid_for(N, T), T, 0, st>>>(k, wlist, &ctr[8]));
+    TRACED(KID_SYNC_PACK, k_wait_list<<<grid_for(N, T), T, 0, st>>>(k, own, wlist, &ctr[8]));
     SyncArgs sa{caps ? caps->debug_flags : 0, skeys, cap_sync, &ctr[3], slow2, &ctr[4], cap_slow, *diags, status,
                 wcword, setword, lastset, n_ids, wlist, &ctr[8]};
     TRACED(KID_SYNC, k_sync<false><<<grid_for(N, 64), 64, 0, st>>>(k, sa, nullptr, 0));
@@ -229,7 +229,7 @@ int build_graph_impl(const LeoKernel* kk, const LeoCaps* caps, LeoEdges* out, Le
   }
   TRACED(KID_REACH_SLOW, k_reach_slow<<<(RW + 63) / 64, 64, 0, st>>>(k, ra, slow3, &ctr[7], reach_scr, RW));
 
-  LinkArgs la{use_ptr, ev_res, q_off, q_len, qres, cand_cnt, cand_off, cand, cap_cand, *diags, status};
+  LinkArgs la{use_ptr, ev_res, q_off, q_len, qres, cand_cnt, cand_off, cand, cap_cand, *diags, status, own};
   TRACED(KID_LINK_COUNT, k_link<0><<<grid_for(N, T), T, 0, st>>>(k, la));
   TRACED(KID_SCAN, scan_exclusive(cand_cnt, cand_off, nullptr, N, scan_tmp, nullptr, st));
   TRACED(KID_LINK_FILL, k_link<1><<<grid_for(N, T), T, 0, st>>>(k, la));
@@ -332,7 +332,7 @@ int slice_impl(const LeoKernel* kk, const LeoProfile* pp, const LeoEdges* pruned
 int blame_impl(const LeoKernel* kk, const LeoProfile* pp, const LeoEdges* pruned, const LeoPaths* paths,
                const LeoEdges* base, const Incoming& inc, const int32_t* line_id, int32_t n_lines,
                LeoBlame* out, double* line_blame, double* line_stall, const LeoCaps* caps,
-               uint32_t* status, cudaStream_t st) {
+               uint32_t* status, cudaStream_t st, Range own = Range{0, 0}) {
   LeoTrace* tr = caps ? caps->trace : nullptr;
   KView k = make_kview(kk);
   const int N = k.N;
@@ -351,7 +351,7 @@ int blame_impl(const LeoKernel* kk, const LeoProfile* pp, const LeoEdges* pruned
   cudaMemsetAsync(ctr, 0, 16, st);
   cudaMemsetAsync(slow_scr, 0, (size_t)BW * 2 * (N + 1) * sizeof(int32_t), st);   // stamps
   Incoming binc = build_incoming(bb, N, base, false, tr, st);   // RAW edges only
-  BlameArgs a{caps ? caps->debug_flags : 0, p, pruned->prod, pruned->meta, paths->dist, inc, binc.rbeg, binc.rend, base->prod, base->meta,
+  BlameArgs a{caps ? caps->debug_flags : 0, own, p, pruned->prod, pruned->meta, paths->dist, inc, binc.rbeg, binc.rend, base->prod, base->meta,
               ecount, self_sub, jtotal, jnsum, eoff, *out, slow_list, &ctr[0], cap_slow, status};
   TRACED(KID_BLAME_COUNT, k_blame<0><<<grid_for(N, 128), 128, 0, st>>>(k, a));
   TRACED(KID_SELFBLAME_SLOW, k_selfblame_slow<<<1, BW, 0, st>>>(k, a, slow_scr, BW));
@@ -361,7 +361,7 @@ int blame_impl(const LeoKernel* kk, const LeoProfile* pp, const LeoEdges* pruned
   if (line_id && line_blame && line_stall && n_lines > 0) {
     cudaMemsetAsync(line_blame, 0, (size_t)n_lines * 8, st);
     cudaMemsetAsync(line_stall, 0, (size_t)n_lines * 8, st);
-    TRACED(KID_LINES, k_lines<<<grid_for(std::max<int64_t>(out->capacity, N), 256), 256, 0, st>>>(k, p, pruned->prod, *out,
+    TRACED(KID_LINES, k_lines<<<grid_for(std::max<int64_t>(out->capacity, N), 256), 256, 0, st>>>(k, p, own, pruned->prod, *out,
                                                                                line_id, line_blame, line_stall));
   }
   ar.release();
@@ -495,7 +495,8 @@ int leo_analyze(const LeoKernel* k, const LeoProfile* p, const LeoSamples* sampl
     int r = bin_impl(samples, k->n_instr, (int32_t*)p->lat, (int32_t*)p->cls_cnt, tr, s_bin);
     if (r) return r;
   }
-  int r = build_graph_impl(k, caps, base, diags, status, st);
+  const Range own{cfg->consumer_lo, cfg->consumer_hi};
+  int r = build_graph_impl(k, caps, base, diags, status, st, own);
   if (r) return r;
   if (samples) link_streams(sp.s[1], st, sp.e[3]);
   r = prune_impl(k, p, cfg, base, pruned, paths, diags, caps, status, st);
@@ -513,7 +514,7 @@ int leo_analyze(const LeoKernel* k, const LeoProfile* p, const LeoSamples* sampl
     r = slice_impl(k, p, pruned, inc, slice_bitmap, slice_level, tr, sp.s[2]);
     if (r) { ar.release(); return r; }
   }
-  r = blame_impl(k, p, pruned, paths, base, inc, line_id, n_lines, blame, line_blame, line_stall, caps, status, st);
+  r = blame_impl(k, p, pruned, paths, base, inc, line_id, n_lines, blame, line_blame, line_stall, caps, status, st, own);
   if (do_slice) link_streams(sp.s[2], st, sp.e[5]);
   ar.release();
   return r;

@@ -147,6 +147,10 @@ LEO_DEV bool prune_one(const KView& k, const PView& p, const PruneArgs& a, int e
   const int kind = (m >> 27) & 7;
   const int pr = a.prod[e], cn = a.cons[e];
   int keep = 1, nv = 0;
+  if (a.cfg.consumer_hi > 0 && (cn < a.cfg.consumer_lo || cn >= a.cfg.consumer_hi)) {
+    a.keep[e] = 0; a.npaths[e] = 0; a.pfirst[e] = -1; a.dist[e] = 1.0;   // not owned (sharding)
+    return true;
+  }
   const uint32_t mask = a.cfg.stage_mask;
   double dist;
   {

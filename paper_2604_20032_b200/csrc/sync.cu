@@ -363,11 +363,11 @@ __host__ __device__ inline size_t sync_slow_bytes_per_worker(int B) {
 }
 
 // compact list of waiting instructions (so no lane idles on non-waits)
-__global__ void k_wait_list(KView k, int32_t* __restrict__ list, int32_t* count) {
+__global__ void k_wait_list(KView k, Range own, int32_t* __restrict__ list, int32_t* count) {
   for (int i0 = blockIdx.x * blockDim.x; i0 < k.N; i0 += gridDim.x * blockDim.x) {
     const int i = i0 + threadIdx.x;
     bool w = false;
-    if (i < k.N) {
+    if (i < k.N && own.has(i)) {
       const uint8_t sk = k.sync_kind[i];
       if (k.dialect == LEO_AMD) w = sk == LEO_SYNC_WAITCNT;
       else if (k.dialect == LEO_NVIDIA) w = sk == LEO_SYNC_BARRIER && ((k.sync_a[i] >> 16) & 0x7E);

@@ -123,3 +123,39 @@ def test_device_fallback_tiers_match_golden(fname, flags, golden_cases, cuda):
         if errs:
             bad.append((ks.name, errs[:2]))
     assert not bad, f"{len(bad)} cases differ with debug flags {flags}; first: {bad[:3]}"
+
+
+@pytest.mark.parametrize("tag,scale,world", [("c5", 0.05, 3), ("c2", 1.0, 2)])
+def test_device_consumer_shards_recombine(tag, scale, world, cuda):
+    """Stalled-PC sharding on the device (LeoConfig.consumer_lo/hi + samples
+    partitioned by owner of pc): per-rank blame entries concatenated in rank
+    order equal the unsharded entries bit-exactly; summed per-line vectors
+    equal the unsharded totals; per-rank pruned edges are exactly the
+    unsharded pruned edges whose consumer the rank owns."""
+    from paper_2604_20032_b200 import abi, device, synth
+    from paper_2604_20032_b200 import dist as D
+    wl = synth.config_workload(tag, scale=scale)
+    ks = wl.kernel
+    full = device.analyze_soa(ks, wl.profile, abi.make_config(dialect=ks.dialect),
+                              samples=(wl.pc, wl.cat, wl.lut), device=cuda)
+    ranges = D.consumer_ranges(ks, world)
+    parts = D.partition_samples(wl.pc, ranges)
+    st, bl, lb, ls = [], [], 0.0, 0.0
+    for (lo, hi), idx in zip(ranges, parts):
+        r = device.analyze_soa(ks, wl.profile,
+                               abi.make_config(dialect=ks.dialect, consumer_range=(lo, hi)),
+                               samples=(wl.pc[idx], wl.cat[idx], wl.lut), device=cuda)
+        assert r["status"] == 0
+        st.append(r["e_stalled"])
+        bl.append(r["e_blame"])
+        lb = lb + r["line_blame"]
+        ls = ls + r["line_stall"]
+        own = (full["pcons"] >= lo) & (full["pcons"] < hi)
+        got = set(zip(r["pprod"].tolist(), r["pcons"].tolist(), r["pmeta"].tolist()))
+        exp = set(zip(full["pprod"][own].tolist(), full["pcons"][own].tolist(),
+                      full["pmeta"][own].tolist()))
+        assert got == exp
+    assert np.array_equal(np.concatenate(st), full["e_stalled"])
+    assert np.array_equal(np.concatenate(bl), full["e_blame"])
+    assert np.allclose(lb, full["line_blame"], rtol=1e-9, atol=1e-6)
+    assert np.allclose(ls, full["line_stall"], rtol=1e-9, atol=1e-6)
