@@ -42,6 +42,7 @@ WORKLOADS = {
     "c2": "C2: synthetic AMD GCN kernel, 10k instrs, s_waitcnt vmcnt/lgkmcnt edges, 1M PC samples",
     "c3": "C3: synthetic Intel Xe kernel, 50k instrs, SWSB tokens, while-nests <= 8 deep, 5M samples",
     "c5": "C5: synthetic NVIDIA kernel, 1M instrs, barrier masks, 100M PC samples",
+    "c4": "C4: batch of mixed-vendor kernels x 20k instrs (100k samples each), sharded by kernel",
 }
 
 
@@ -51,7 +52,8 @@ def parse():
     ap.add_argument("--steps", type=int, default=50)
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--config", default="c2", choices=["c2", "c3", "c5"])
+    ap.add_argument("--config", default="c2", choices=["c2", "c3", "c4", "c5"])
+    ap.add_argument("--c4-kernels", type=int, default=2000)
     ap.add_argument("--scale", type=float, default=1.0)
     ap.add_argument("--trace", action="store_true", help="print per-kernel device time")
     ap.add_argument("--no-cpu", action="store_true", help="skip the CPU baseline leg")
@@ -188,60 +190,134 @@ def run_reference(args, ws, rank):
 
 
 # ---------------------------------------------------------------------------
+class Plan:
+    """What one rank executes per step: one or more (kernel, profile, samples)
+    pipelines, each captured as a CUDA graph, replayed round-robin over a few
+    streams (independent kernels overlap), then the line all-reduce."""
+
+    def __init__(self):
+        self.items = []          # dicts: wl, an, dp, ds, cfg
+        self.samples = 0
+        self.shared = None       # (line_blame, line_stall) when kernels accumulate
+
+
+def build_plan(args, ws, rank, dev):
+    import torch
+    from paper_2604_20032_b200 import abi, device, synth
+    from paper_2604_20032_b200 import dist as D
+    plan = Plan()
+    plan.mode = "replica"
+    if args.config == "c4":
+        lines = synth.LineTable(4096, seed=999)
+        K = args.c4_kernels
+        costs = [D.kernel_cost(["nvidia", "amd", "intel"][k % 3], synth.C4_INSTR) for k in range(K)]
+        mine = D.lpt_assign(costs, ws)[rank]
+        L = len(lines)
+        plan.shared = (torch.zeros(L, dtype=torch.float64, device=dev),
+                       torch.zeros(L, dtype=torch.float64, device=dev))
+        plan.mode = f"kernel-sharded (LPT) {len(mine)}/{K} kernels"
+        for k in mine:
+            wl = synth.c4_kernel(k, lines, scale=args.scale)
+            plan.items.append(dict(wl=wl, cfg=abi.make_config(dialect=wl.kernel.dialect)))
+    elif args.config == "c5" and ws > 1:
+        wl = synth.config_workload("c5", scale=args.scale)
+        (lo, hi), pc, cat = D.shard_workload(wl, rank, ws)
+        wl.pc, wl.cat = pc, cat
+        plan.mode = f"stalled-PC sharded: consumers [{lo}, {hi})"
+        plan.items.append(dict(wl=wl, cfg=abi.make_config(dialect="nvidia", consumer_range=(lo, hi)),
+                               slice_=False))
+    else:
+        wl = synth.config_workload(args.config, scale=args.scale, seed_offset=rank)
+        plan.items.append(dict(wl=wl, cfg=abi.make_config(dialect=wl.kernel.dialect)))
+    for it in plan.items:
+        wl = it["wl"]
+        it["dk"] = device.DeviceKernel(wl.kernel, dev)
+        it["dp"] = device.DeviceProfile(wl.profile, wl.kernel.n_instr, dev)
+        it["ds"] = device.DeviceSamples(wl.pc, wl.cat, wl.lut, dev)
+        it["an"] = device.Analyzer(it["dk"], dev, lines=plan.shared, do_slice=it.get("slice_", True))
+        it.setdefault("slice_", True)
+        plan.samples += wl.n_samples
+    return plan
+
+
 def run_ours(args, ws, rank, local):
     import torch
     import torch.distributed as dist
-    from paper_2604_20032_b200 import abi, api, device, roofline, synth
+    from paper_2604_20032_b200 import api, device, roofline
+    from paper_2604_20032_b200 import dist as D
 
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
     if ws > 1:
         dist.init_process_group("nccl", device_id=dev)
+    plan = build_plan(args, ws, rank, dev)
+    first = plan.items[0]
+    an0, wl0 = first["an"], first["wl"]
+    ks = wl0.kernel
 
-    # each rank analyses its own kernel of the configured shape (shared line pool)
-    wl = synth.config_workload(args.config, scale=args.scale, seed_offset=rank)
-    ks = wl.kernel
-    cfg = abi.make_config(dialect=ks.dialect)
-    dk = device.DeviceKernel(ks, dev)
-    dp = device.DeviceProfile(wl.profile, ks.n_instr, dev)
-    ds = device.DeviceSamples(wl.pc, wl.cat, wl.lut, dev)
-    an = device.Analyzer(dk, dev)
-    counts = an.run(dp, cfg, ds)               # sizes buffers (grow + re-run on overflow)
-    res = an.result()
-    assert res["status"] == 0
-    eager_res = res
+    # size buffers (grow + re-run on overflow), keep eager results for checking
+    eager = []
+    for it in plan.items:
+        it["counts"] = it["an"].run(it["dp"], it["cfg"], it["ds"])
+        r = it["an"].result()
+        assert r["status"] == 0
+        if it is first:
+            eager = r
+
+    def line_vectors(it):
+        return (plan.shared if plan.shared is not None else (it["an"].line_blame, it["an"].line_stall))
 
     def allreduce_lines():
         if ws > 1:
-            dist.all_reduce(an.line_blame, op=dist.ReduceOp.SUM)
-            dist.all_reduce(an.line_stall, op=dist.ReduceOp.SUM)
+            if plan.shared is not None:
+                D.allreduce_lines(*plan.shared)
+            else:
+                for it in plan.items:
+                    D.allreduce_lines(*line_vectors(it))
 
-    # per-kernel breakdown of one step (all kernels traced)
+    # per-kernel breakdown of one eager step of the first pipeline (all kernels traced)
     tracer = device.Tracer(capacity=4096)
-    an.set_tracer(tracer)
+    an0.set_tracer(tracer)
     torch.cuda.synchronize()
-    an.launch(dp, cfg, ds)
+    an0.launch(first["dp"], first["cfg"], first["ds"], slice_=first["slice_"])
     torch.cuda.synchronize()
     breakdown = tracer.summary()
     n_launch = sum(3 if k == "scan" else 1 for k, _ in tracer.records())
     dominant = max(breakdown, key=breakdown.get)
     tracer.reset(only_kernel=device.kernel_id(dominant))
+    an0.set_tracer(None)
 
-    # dominant-kernel event timing runs in a traced eager pass; the timed steps
-    # replay the captured graph (one launch of the whole pipeline)
     use_graph = not args.no_graph
+    streams = [torch.cuda.Stream(dev) for _ in range(min(len(plan.items), 8))]
     if use_graph:
-        an.capture(dp, cfg, ds)
-        step = an.replay
-    else:
-        step = lambda: an.launch(dp, cfg, ds)  # noqa: E731
+        for it in plan.items:
+            it["an"].capture(it["dp"], it["cfg"], it["ds"])
+
+    def step():
+        if plan.shared is not None:
+            for v in plan.shared:
+                v.zero_()
+        if len(plan.items) == 1:
+            it = plan.items[0]
+            it["an"].replay() if use_graph else it["an"].launch(it["dp"], it["cfg"], it["ds"],
+                                                                slice_=it["slice_"])
+        else:
+            cur = torch.cuda.current_stream(dev)
+            for s in streams:
+                s.wait_stream(cur)
+            for x, it in enumerate(plan.items):
+                with torch.cuda.stream(streams[x % len(streams)]):
+                    it["an"].replay() if use_graph else it["an"].launch(it["dp"], it["cfg"], it["ds"],
+                                                                        slice_=it["slice_"])
+            for s in streams:
+                cur.wait_stream(s)
+        allreduce_lines()
+
     flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)
     for _ in range(args.warmup):
         flush.zero_()
         step()
-        allreduce_lines()
     torch.cuda.synchronize()
-    tracer.reset()
     starts = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
     ends = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
     clocks = ClockSampler(dev)
@@ -253,83 +329,96 @@ def run_ours(args, ws, rank, local):
             flush.zero_()                       # L2 flush between timed steps (not timed)
             starts[s].record()
             step()
-            allreduce_lines()
             ends[s].record()
         torch.cuda.synchronize()
     if ws > 1:
         dist.barrier()
     step_ms = np.array([a.elapsed_time(b) for a, b in zip(starts, ends)])
     T = float(step_ms.sum())
-    # live dominant-kernel time: eager traced steps (events on the launch stream)
-    tracer.reset()
-    for _ in range(max(3, min(args.steps, 20))):
-        flush.zero_()
-        an.launch(dp, cfg, ds)
-    torch.cuda.synchronize()
-    dom_ms = [ms for _, ms in tracer.records()]
     t = torch.tensor([T], dtype=torch.float64, device=dev)
     if ws > 1:
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
     T_max = float(t.item())
-    S = wl.n_samples
-    value = ws * S * args.steps / (T_max / 1e3)
-    res = an.result()
+    S_all = torch.tensor([float(plan.samples)], dtype=torch.float64, device=dev)
+    if ws > 1:
+        dist.all_reduce(S_all, op=dist.ReduceOp.SUM)
+    S_total = float(S_all.item())
+    value = S_total * args.steps / (T_max / 1e3)
+    res = an0.result()
     assert res["status"] == 0
     for key in ("bprod", "bcons", "bmeta", "pprod", "pmeta", "e_stalled", "e_edge", "e_blame", "level"):
-        assert np.array_equal(res[key], eager_res[key]), f"graph replay changed {key}"
+        assert np.array_equal(res[key], eager[key]), f"graph replay changed {key}"
 
-    # roofline of the dominant kernel (algorithmic bytes / live event time)
+    # live dominant-kernel time: eager traced steps (events on the launch stream)
+    an0.set_tracer(tracer)
+    tracer.reset()
+    for _ in range(max(3, min(args.steps, 20))):
+        flush.zero_()
+        an0.launch(first["dp"], first["cfg"], first["ds"], slice_=first["slice_"])
+    torch.cuda.synchronize()
+    dom_ms = [ms for _, ms in tracer.records()]
+    an0.set_tracer(None)
+
     peak, peak_src = peaks()
-    alg = roofline.kernel_bytes(dominant, ks, wl, res)
+    alg = roofline.kernel_bytes(dominant, ks, wl0, res)
     avg_s = float(np.mean(dom_ms)) / 1e3 if dom_ms else None
     achieved = alg / avg_s / 1e9 if (alg and avg_s) else None
     traffic = roofline.ncu_traffic(ROOT / "profiles", args.config, dominant)
-    pipe_bytes = roofline.pipeline_bytes(ks, wl, res)
+    pipe_bytes = sum(roofline.pipeline_bytes(it["wl"].kernel, it["wl"], it["an"].result() if it is not first else res)
+                     for it in plan.items[:1]) * len(plan.items)
 
-    # e2e through the public API: pinned host inputs in, results out, every step
-    sess = api.Session(ks, wl.profile, S, cfg, dev)
-    sess.an.caps = an.caps
-    sess.an._alloc()
-    sess.stage(ks, wl.profile, wl.pc, wl.cat, wl.lut)
+    # e2e through the public API (first pipeline of the rank; C4: a bounded subset)
+    e2e_items = plan.items[:min(len(plan.items), 8)]
+    sessions = []
+    for it in e2e_items:
+        wl = it["wl"]
+        sess = api.Session(wl.kernel, wl.profile, wl.n_samples, it["cfg"], dev)
+        sess.an.caps = it["an"].caps
+        sess.an._alloc()
+        sess.stage(wl.kernel, wl.profile, wl.pc, wl.cat, wl.lut)
+        sessions.append(sess)
 
-    def allreduce_sess(lb, ls):
-        dist.all_reduce(lb, op=dist.ReduceOp.SUM)
-        dist.all_reduce(ls, op=dist.ReduceOp.SUM)
+    def e2e_allreduce(lb, ls):
+        D.allreduce_lines(lb, ls)
 
-    sess.analyze(allreduce=allreduce_sess if ws > 1 else None)
+    for sess in sessions:
+        sess.analyze(allreduce=e2e_allreduce if ws > 1 else None)
     e2e_t = []
     for s in range(max(3, min(args.steps, 20))):
         if ws > 1:
             dist.barrier()
         torch.cuda.synchronize()
         t0 = time.perf_counter()
-        sess.analyze(allreduce=allreduce_sess if ws > 1 else None)
+        for sess in sessions:
+            sess.analyze(allreduce=e2e_allreduce if ws > 1 else None)
         e2e_t.append(time.perf_counter() - t0)
     te = torch.tensor([float(np.sum(e2e_t))], dtype=torch.float64, device=dev)
     if ws > 1:
         dist.all_reduce(te, op=dist.ReduceOp.MAX)
-    e2e_value = ws * S * len(e2e_t) / float(te.item())
+    e2e_S = sum(it["wl"].n_samples for it in e2e_items)
+    e2e_S_all = torch.tensor([float(e2e_S)], dtype=torch.float64, device=dev)
+    if ws > 1:
+        dist.all_reduce(e2e_S_all, op=dist.ReduceOp.SUM)
+    e2e_value = float(e2e_S_all.item()) * len(e2e_t) / float(te.item())
 
     cpu = None
     if rank == 0 and ws == 1 and not args.no_cpu:
-        times, stages = cpu_port_time(wl, args.cpu_seconds)
-        cpu = {"value": S / float(np.mean(times)), "unit": UNIT, "cores": 1, "kind": "port",
-               "sample": f"full {args.config} workload x{len(times)} (oracle/leo_oracle.c: binning "
-                         f"+ build + prune + slice + blame + lines; {np.mean(times) * 1e3:.1f} ms each)"}
+        cpu = cpu_baseline(args, plan)
 
     if rank == 0:
+        c0 = first["counts"]
         line = {
             "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": ws, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": T_max / args.steps, "higher_is_better": True,
             "scaling": "weak", "vs_baseline": None, "dtype": "int32/f64", "data": "synthetic",
             "config": {"workload": WORKLOADS[args.config], "scale": args.scale,
-                       "per_rank": f"one kernel per rank (seed {synth.CONFIGS[args.config]['seed']}+rank)",
-                       "n_instr": ks.n_instr, "n_samples_per_rank": S,
-                       "edges": int(counts[device.C_BASE]), "pruned_edges": int(counts[device.C_PR]),
-                       "blame_entries": int(counts[device.C_BLAME]),
+                       "per_rank": plan.mode, "kernels_per_rank": len(plan.items),
+                       "n_instr": ks.n_instr, "n_samples_per_step_all_ranks": S_total,
+                       "edges": int(c0[device.C_BASE]), "pruned_edges": int(c0[device.C_PR]),
+                       "blame_entries": int(c0[device.C_BLAME]),
                        "l2": "flushed between timed steps (256 MiB write)",
                        "launch": "CUDA graph replay of the whole pipeline" if use_graph else "eager",
-                       "parallelism": f"kernel-sharded x{ws}" + (" + NCCL all-reduce of f64 line blame" if ws > 1 else "")},
+                       "parallelism": f"x{ws}" + (" + NCCL all-reduce of f64 line vectors" if ws > 1 else "")},
             "roofline": {"bound": "hbm", "kernel": dominant, "achieved": achieved, "peak": peak,
                          "unit": "GB/s", "frac": (achieved / peak) if achieved else None,
                          "traffic": traffic, "alg_bytes_per_launch": alg,
@@ -338,9 +427,11 @@ def run_ours(args, ws, rank, local):
                                   "achieved_gbs": pipe_bytes / (T_max / args.steps / 1e3) / 1e9,
                                   "frac": pipe_bytes / (T_max / args.steps / 1e3) / 1e9 / peak},
             "cpu_baseline": cpu,
-            "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": sess.h2d_bytes(),
-                    "d2h_bytes_per_step": int(sess.last_d2h)},
-            "gpu_launches": n_launch * args.steps,
+            "e2e": {"value": e2e_value, "unit": UNIT,
+                    "h2d_bytes_per_step": int(sum(s.h2d_bytes() for s in sessions)),
+                    "d2h_bytes_per_step": int(sum(s.last_d2h for s in sessions)),
+                    "sample": f"{len(sessions)} kernel(s) per rank through api.Session"},
+            "gpu_launches": n_launch * len(plan.items) * args.steps,
             "clocks": clocks.summary(),
             "kernel_ms_one_step": {k: round(v, 4) for k, v in sorted(breakdown.items(), key=lambda x: -x[1])},
         }
@@ -352,6 +443,31 @@ def run_ours(args, ws, rank, local):
     if ws > 1:
         dist.destroy_process_group()
     return 0
+
+
+def cpu_baseline(args, plan):
+    """Oracle port on the host cores on a bounded sample of the same workload."""
+    from concurrent.futures import ThreadPoolExecutor
+    items = [it["wl"] for it in plan.items]
+    if len(items) == 1:
+        times, _ = cpu_port_time(items[0], args.cpu_seconds)
+        S = items[0].n_samples
+        return {"value": S / float(np.mean(times)), "unit": UNIT, "cores": 1, "kind": "port",
+                "sample": f"full {args.config} workload x{len(times)} (oracle/leo_oracle.c: binning "
+                          f"+ build + prune + slice + blame + lines; {np.mean(times) * 1e3:.1f} ms each)"}
+    cores = os.cpu_count() or 1
+    t0 = time.perf_counter()
+    done, S = 0, 0
+    with ThreadPoolExecutor(cores) as ex:           # ctypes releases the GIL
+        while time.perf_counter() - t0 < args.cpu_seconds and done < len(items):
+            batch = items[done:done + cores]
+            list(ex.map(lambda w: cpu_port_time(w, 0.0), batch))
+            done += len(batch)
+            S += sum(w.n_samples for w in batch)
+    dt = time.perf_counter() - t0
+    return {"value": S / dt, "unit": UNIT, "cores": cores, "kind": "port",
+            "sample": f"{done} of the rank's {len(items)} C4 kernels on {cores} threads "
+                      f"(oracle/leo_oracle.c per kernel)"}
 
 
 def main():

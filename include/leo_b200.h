@@ -211,8 +211,11 @@ typedef struct LeoCaps {
   int64_t slow_items;         /* work items re-run on the global-scratch path (default N/4 + 1024) */
   LeoTrace* trace;            /* optional, host struct (NULL = no tracing) */
   int32_t debug_flags;        /* testing: route every item to a larger tier (LEO_DBG_*) */
-  int32_t pad;
+  int32_t options;            /* LEO_OPT_* */
 } LeoCaps;
+/* LEO_OPT_ACCUMULATE_LINES: add into line_blame / line_stall instead of
+ * zeroing them first (many kernels of one batch share one per-line vector) */
+enum { LEO_OPT_ACCUMULATE_LINES = 1 };
 enum { LEO_DBG_REACH_T2 = 1, LEO_DBG_REACH_T3 = 2, LEO_DBG_SYNC_SLOW = 4, LEO_DBG_PRUNE_SLOW = 8,
        LEO_DBG_SELF_SLOW = 16 };
 

@@ -359,8 +359,10 @@ int blame_impl(const LeoKernel* kk, const LeoProfile* pp, const LeoEdges* pruned
   TRACED(KID_BLAME_FILL, k_blame<1><<<grid_for(N, 128), 128, 0, st>>>(k, a));
   TRACED(KID_BLAME_TOTAL, k_blame_count<<<1, 1, 0, st>>>(eoff, N, *out));
   if (line_id && line_blame && line_stall && n_lines > 0) {
-    cudaMemsetAsync(line_blame, 0, (size_t)n_lines * 8, st);
-    cudaMemsetAsync(line_stall, 0, (size_t)n_lines * 8, st);
+    if (!(caps && (caps->options & LEO_OPT_ACCUMULATE_LINES))) {
+      cudaMemsetAsync(line_blame, 0, (size_t)n_lines * 8, st);
+      cudaMemsetAsync(line_stall, 0, (size_t)n_lines * 8, st);
+    }
     TRACED(KID_LINES, k_lines<<<grid_for(std::max<int64_t>(out->capacity, N), 256), 256, 0, st>>>(k, p, own, pruned->prod, *out,
                                                                                line_id, line_blame, line_stall));
   }

@@ -109,9 +109,14 @@ class Analyzer:
     """Owns output buffers for one kernel shape; runs the fused pipeline."""
 
     def __init__(self, dk: DeviceKernel, device="cuda", caps: Caps | None = None,
-                 debug_flags: int = 0):
+                 debug_flags: int = 0, lines: tuple | None = None, do_slice: bool = True):
+        """`lines`: optional shared (line_blame, line_stall) f64 device tensors;
+        when given, this kernel accumulates into them (LEO_OPT_ACCUMULATE_LINES)
+        instead of owning zero-initialised per-kernel vectors."""
         self.tracer = None
         self.debug_flags = debug_flags
+        self.shared_lines = lines
+        self.do_slice = do_slice
         self.dk = dk
         self.device = torch.device(device)
         n = dk.n_instr
@@ -141,8 +146,11 @@ class Analyzer:
         self.bl_factors = torch.empty(max(4 * c.blame, 1), dtype=torch.float64, device=d)
         self.level = i32(n)
         self.bitmap = i32((n + 31) // 32)
-        self.line_blame = torch.empty(max(self.dk.n_lines, 1), dtype=torch.float64, device=d)
-        self.line_stall = torch.empty(max(self.dk.n_lines, 1), dtype=torch.float64, device=d)
+        if self.shared_lines is not None:
+            self.line_blame, self.line_stall = self.shared_lines
+        else:
+            self.line_blame = torch.empty(max(self.dk.n_lines, 1), dtype=torch.float64, device=d)
+            self.line_stall = torch.empty(max(self.dk.n_lines, 1), dtype=torch.float64, device=d)
         cp = self.ctr.data_ptr()
         at = lambda k: cp + 4 * k  # noqa: E731
         self.s_base = abi.LeoEdges(c.base, ptr(self.b_prod), ptr(self.b_cons), ptr(self.b_meta),
@@ -157,7 +165,8 @@ class Analyzer:
         s = self.caps.scratch_scale
         nu, n = self.n_use_units, self.dk.n_instr
         self.s_caps = abi.LeoCaps((4 * nu + 1024) * s, (6 * nu + 1024) * s, (2 * n + 1024) * s,
-                                  (n // 4 + 1024) * s, None, self.debug_flags, 0)
+                                  (n // 4 + 1024) * s, None, self.debug_flags,
+                                  abi.OPT_ACCUMULATE_LINES if self.shared_lines is not None else 0)
         self.set_tracer(self.tracer)
         self.status_ptr = at(C_STATUS)
 
@@ -167,8 +176,11 @@ class Analyzer:
 
     # -- launch ------------------------------------------------------------
     def launch(self, dp: DeviceProfile, cfg: abi.LeoConfig, samples: DeviceSamples | None = None,
-               stream: torch.cuda.Stream | None = None, slice_: bool = True, lines: bool = True):
+               stream: torch.cuda.Stream | None = None, slice_: bool | None = None,
+               lines: bool = True):
         st = stream or torch.cuda.current_stream(self.device)
+        if slice_ is None:
+            slice_ = self.do_slice
         self.ctr.zero_()
         L = lib()
         rc = L.leo_analyze(C.byref(self.dk.struct), C.byref(dp.struct),
