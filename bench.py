@@ -208,6 +208,7 @@ def build_plan(args, ws, rank, dev):
     plan = Plan()
     plan.mode = "replica"
     if args.config == "c4":
+        from paper_2604_20032_b200 import batch as BT
         lines = synth.LineTable(4096, seed=999)
         K = args.c4_kernels
         costs = [D.kernel_cost(["nvidia", "amd", "intel"][k % 3], synth.C4_INSTR) for k in range(K)]
@@ -215,10 +216,15 @@ def build_plan(args, ws, rank, dev):
         L = len(lines)
         plan.shared = (torch.zeros(L, dtype=torch.float64, device=dev),
                        torch.zeros(L, dtype=torch.float64, device=dev))
-        plan.mode = f"kernel-sharded (LPT) {len(mine)}/{K} kernels"
+        groups = {}
         for k in mine:
             wl = synth.c4_kernel(k, lines, scale=args.scale)
-            plan.items.append(dict(wl=wl, cfg=abi.make_config(dialect=wl.kernel.dialect)))
+            groups.setdefault(BT.group_key(wl), []).append(wl)
+        plan.mode = (f"kernel-sharded (LPT) {len(mine)}/{K} kernels, concatenated per "
+                     f"(dialect, period) into {len(groups)} batch pipelines")
+        for key in sorted(groups):
+            b = BT.concat(groups[key])
+            plan.items.append(dict(wl=b, cfg=abi.make_config(dialect=key[0])))
     elif args.config == "c5" and ws > 1:
         wl = synth.config_workload("c5", scale=args.scale)
         (lo, hi), pc, cat = D.shard_workload(wl, rank, ws)

@@ -67,10 +67,11 @@ __global__ void k_bin_samples(int64_t S, const int32_t* __restrict__ pc, const u
 // shared memory with warp-aggregated atomics and merged into cls_cnt.  Hot
 // buckets (Zipf-heavy PCs) are split over many CTAs, so no counter sees more
 // than one global atomic per CTA.
-constexpr int kBinR = 2048;          // instructions per bucket (64 KiB of counters)
+constexpr int kBinR = 2048;          // default instructions per bucket (64 KiB of counters)
+constexpr int kBinRMax = 4096;       // 128 KiB of counters: up to 16.7M instructions
 constexpr int kBinMaxBuckets = 4096;
 
-__global__ void k_bin_hist(int64_t S, const int32_t* __restrict__ pc, int N, int nb,
+__global__ void k_bin_hist(int64_t S, const int32_t* __restrict__ pc, int N, int nb, int R,
                            int32_t* __restrict__ bucket_cnt, uint32_t* status) {
   __shared__ int32_t h[kBinMaxBuckets];
   for (int x = threadIdx.x; x < nb; x += blockDim.x) h[x] = 0;
@@ -84,13 +85,13 @@ __global__ void k_bin_hist(int64_t S, const int32_t* __restrict__ pc, int N, int
     for (int t = 0; t < 4; t++) {
       int j = ps[t];
       if (j < 0 || j >= N) { atomicOr(status, (uint32_t)LEO_ST_BAD_INPUT); continue; }
-      atomicAdd(&h[j / kBinR], 1);
+      atomicAdd(&h[j / R], 1);
     }
   }
   for (int64_t s = nvec * 4 + blockIdx.x * (int64_t)blockDim.x + threadIdx.x; s < S; s += (int64_t)gridDim.x * blockDim.x) {
     int j = pc[s];
     if (j < 0 || j >= N) { atomicOr(status, (uint32_t)LEO_ST_BAD_INPUT); continue; }
-    atomicAdd(&h[j / kBinR], 1);
+    atomicAdd(&h[j / R], 1);
   }
   __syncthreads();
   for (int x = threadIdx.x; x < nb; x += blockDim.x)
@@ -116,7 +117,7 @@ __global__ void k_bin_plan(int nb, int slice, const int32_t* __restrict__ bucket
 }
 
 __global__ void k_bin_scatter(int64_t S, const int32_t* __restrict__ pc, const uint8_t* __restrict__ cat,
-                              const uint8_t* __restrict__ lut, int N, int nb, int32_t* __restrict__ cursor,
+                              const uint8_t* __restrict__ lut, int N, int nb, int R, int32_t* __restrict__ cursor,
                               uint16_t* __restrict__ keys) {
   __shared__ int32_t h[kBinMaxBuckets];
   __shared__ uint8_t slut[256];
@@ -128,7 +129,7 @@ __global__ void k_bin_scatter(int64_t S, const int32_t* __restrict__ pc, const u
   const int64_t s0 = (int64_t)blockIdx.x * per, s1 = min(S, s0 + per);
   for (int64_t s = s0 + threadIdx.x; s < s1; s += blockDim.x) {
     int j = pc[s];
-    if (j >= 0 && j < N) atomicAdd(&h[j / kBinR], 1);
+    if (j >= 0 && j < N) atomicAdd(&h[j / R], 1);
   }
   __syncthreads();
   for (int x = threadIdx.x; x < nb; x += blockDim.x) {
@@ -139,17 +140,17 @@ __global__ void k_bin_scatter(int64_t S, const int32_t* __restrict__ pc, const u
   for (int64_t s = s0 + threadIdx.x; s < s1; s += blockDim.x) {
     int j = pc[s];
     if (j < 0 || j >= N) continue;
-    int b = j / kBinR;
+    int b = j / R;
     int pos = atomicAdd(&h[b], 1);
-    keys[pos] = (uint16_t)(((j - b * kBinR) << 3) | slut[cat[s]]);
+    keys[pos] = (uint16_t)(((j - b * R) << 3) | slut[cat[s]]);
   }
 }
 
-__global__ void __launch_bounds__(512) k_bin_count(int N, int nb, int slice, const int32_t* __restrict__ bucket_off,
+__global__ void __launch_bounds__(512) k_bin_count(int N, int nb, int R, int slice, const int32_t* __restrict__ bucket_off,
                                                    const int32_t* __restrict__ slice_off,
                                                    const uint16_t* __restrict__ keys,
                                                    int32_t* __restrict__ cls_cnt) {
-  extern __shared__ int32_t cnt[];              // kBinR * 8
+  extern __shared__ int32_t cnt[];              // R * 8
   const int total_slices = slice_off[nb];
   for (int sl = blockIdx.x; sl < total_slices; sl += gridDim.x) {
     // bucket of this slice: largest b with slice_off[b] <= sl
@@ -162,7 +163,7 @@ __global__ void __launch_bounds__(512) k_bin_count(int N, int nb, int slice, con
     const int k = sl - slice_off[b];
     const int64_t e0 = (int64_t)bucket_off[b] + (int64_t)k * slice;
     const int64_t e1 = min((int64_t)bucket_off[b + 1], e0 + slice);
-    for (int x = threadIdx.x; x < kBinR * 8; x += blockDim.x) cnt[x] = 0;
+    for (int x = threadIdx.x; x < R * 8; x += blockDim.x) cnt[x] = 0;
     __syncthreads();
     for (int64_t e = e0 + threadIdx.x; e - threadIdx.x < e1; e += blockDim.x) {
       int key = e < e1 ? (int)keys[e] : -1;
@@ -170,8 +171,8 @@ __global__ void __launch_bounds__(512) k_bin_count(int N, int nb, int slice, con
       if (key >= 0 && (__ffs(grp) - 1) == (int)(threadIdx.x & 31)) atomicAdd(&cnt[key], __popc(grp));
     }
     __syncthreads();
-    const int base = b * kBinR * 8;
-    const int lim = min(kBinR * 8, (N - b * kBinR) * 8);
+    const int64_t base = (int64_t)b * R * 8;
+    const int lim = (int)min((int64_t)R * 8, ((int64_t)N - (int64_t)b * R) * 8);
     for (int x = threadIdx.x; x < lim; x += blockDim.x)
       if (cnt[x]) atomicAdd(&cls_cnt[base + x], cnt[x]);
     __syncthreads();

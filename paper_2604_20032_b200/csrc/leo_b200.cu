@@ -118,7 +118,7 @@ void set_smem_attributes() {
   static bool done = false;
   if (done) return;
   cudaFuncSetAttribute(k_reach_fast, cudaFuncAttributeMaxDynamicSharedMemorySize, kT1Threads * kT1Hash * 4);
-  cudaFuncSetAttribute(k_bin_count, cudaFuncAttributeMaxDynamicSharedMemorySize, kBinR * 8 * 4);
+  cudaFuncSetAttribute(k_bin_count, cudaFuncAttributeMaxDynamicSharedMemorySize, kBinRMax * 8 * 4);
   cudaFuncSetAttribute(k_block_walk, cudaFuncAttributeMaxDynamicSharedMemorySize, 96 * 1024);
   done = true;
 }
@@ -383,7 +383,8 @@ static int bin_impl(const LeoSamples* s, int32_t n_instr, int32_t* lat, int32_t*
   set_smem_attributes();
   cudaMemsetAsync(cls_cnt, 0, (size_t)std::max(n_instr, 1) * 32, st);
   const int64_t S = s->n_samples;
-  const int nb = (n_instr + kBinR - 1) / kBinR;
+  const int R = (n_instr + kBinR - 1) / kBinR <= kBinMaxBuckets ? kBinR : kBinRMax;
+  const int nb = (n_instr + R - 1) / R;
   Arena ar{st};
   uint32_t* status;
   int32_t *bcnt, *boff, *bcur, *soff;
@@ -395,15 +396,15 @@ static int bin_impl(const LeoSamples* s, int32_t n_instr, int32_t* lat, int32_t*
   LEO_CUDA_CHECK(ar.commit());
   cudaMemsetAsync(status, 0, 4, st);
   if (bucketed) {
-    const int smem = kBinR * 8 * 4;
+    const int smem = R * 8 * 4;
     cudaMemsetAsync(bcnt, 0, (size_t)(nb + 1) * 4, st);
     const int G = num_sms() * 4;
-    TRACED(KID_BIN_HIST, k_bin_hist<<<grid_for(S / 4 + 1, 256, G), 256, 0, st>>>(S, s->pc, n_instr, nb, bcnt, status));
+    TRACED(KID_BIN_HIST, k_bin_hist<<<grid_for(S / 4 + 1, 256, G), 256, 0, st>>>(S, s->pc, n_instr, nb, R, bcnt, status));
     // slices: enough counting CTAs to fill the chip, >= 4K samples each
     const int slice = (int)std::min<int64_t>(65536, std::max<int64_t>(4096, S / (num_sms() * 3)));
     TRACED(KID_BIN_PLAN, k_bin_plan<<<1, 1024, 0, st>>>(nb, slice, bcnt, boff, bcur, soff));
-    TRACED(KID_BIN_SCATTER, k_bin_scatter<<<grid_for(S, 1024, G), 1024, 0, st>>>(S, s->pc, s->cat, s->cat_to_cs, n_instr, nb, bcur, keys));
-    TRACED(KID_BIN, k_bin_count<<<num_sms() * 3, 512, smem, st>>>(n_instr, nb, slice, boff, soff, keys, cls_cnt));
+    TRACED(KID_BIN_SCATTER, k_bin_scatter<<<grid_for(S, 1024, G), 1024, 0, st>>>(S, s->pc, s->cat, s->cat_to_cs, n_instr, nb, R, bcur, keys));
+    TRACED(KID_BIN, k_bin_count<<<num_sms() * 3, 512, smem, st>>>(n_instr, nb, R, slice, boff, soff, keys, cls_cnt));
   } else if (S > 0) {
     TRACED(KID_BIN, k_bin_samples<<<grid_for(S / 4 + 1, 256, num_sms() * 8), 256, 0, st>>>(
         S, s->pc, s->cat, s->cat_to_cs, n_instr, cls_cnt, status));

@@ -159,3 +159,26 @@ def test_device_consumer_shards_recombine(tag, scale, world, cuda):
     assert np.array_equal(np.concatenate(bl), full["e_blame"])
     assert np.allclose(lb, full["line_blame"], rtol=1e-9, atol=1e-6)
     assert np.allclose(ls, full["line_stall"], rtol=1e-9, atol=1e-6)
+
+
+def test_device_batch_matches_per_kernel_oracle(cuda):
+    """C4-style batch (kernels concatenated per dialect, one pipeline pass on
+    the device): every kernel's slice of the batch result equals the oracle
+    on that kernel alone."""
+    from oracle import oracle
+    from paper_2604_20032_b200 import abi, device, synth
+    from paper_2604_20032_b200 import batch as BT
+    lines = synth.LineTable(256, seed=999)
+    for dialect in ("nvidia", "amd", "intel"):
+        wls = [synth.make_workload(dialect, 2000, 10_000, 7000 + s, lines=lines, name=f"k{s}")
+               for s in range(12)]
+        b = BT.concat(wls)
+        r = device.analyze_soa(b.kernel, b.profile, abi.make_config(dialect=dialect),
+                               samples=(b.pc, b.cat, b.lut), device=cuda)
+        assert r["status"] == 0
+        for wl, got in zip(wls, BT.split_result(b, r)):
+            o = oracle.run(wl.kernel, synth.bin_host(wl))
+            for f, e in (("bprod", o.prod), ("bmeta", o.meta), ("pprod", o.p_prod),
+                         ("pmeta", o.p_meta), ("e_stalled", o.e_stalled), ("e_blame", o.e_blame),
+                         ("level", o.level)):
+                assert np.array_equal(got[f], e), (dialect, wl.kernel.name, f)
