@@ -199,6 +199,7 @@ class Plan:
         self.items = []          # dicts: wl, an, dp, ds, cfg
         self.samples = 0
         self.shared = None       # (line_blame, line_stall) when kernels accumulate
+        self.members = None      # individual kernels of batched pipelines (CPU baseline)
 
 
 def build_plan(args, ws, rank, dev):
@@ -222,6 +223,7 @@ def build_plan(args, ws, rank, dev):
             groups.setdefault(BT.group_key(wl), []).append(wl)
         plan.mode = (f"kernel-sharded (LPT) {len(mine)}/{K} kernels, concatenated per "
                      f"(dialect, period) into {len(groups)} batch pipelines")
+        plan.members = [w for key in sorted(groups) for w in groups[key]]
         for key in sorted(groups):
             b = BT.concat(groups[key])
             plan.items.append(dict(wl=b, cfg=abi.make_config(dialect=key[0])))
@@ -454,7 +456,7 @@ def run_ours(args, ws, rank, local):
 def cpu_baseline(args, plan):
     """Oracle port on the host cores on a bounded sample of the same workload."""
     from concurrent.futures import ThreadPoolExecutor
-    items = [it["wl"] for it in plan.items]
+    items = getattr(plan, "members", None) or [it["wl"] for it in plan.items]
     if len(items) == 1:
         times, _ = cpu_port_time(items[0], args.cpu_seconds)
         S = items[0].n_samples

@@ -187,8 +187,11 @@ int build_graph_impl(const LeoKernel* kk, const LeoCaps* caps, LeoEdges* out, Le
   // fork: vendor sync tracing runs on a side stream, concurrently with the
   // register dataflow chain below
   SidePool& sp = side_pool();
-  cudaStream_t s_sync = sp.s[0];
-  link_streams(st, s_sync, sp.e[0]);
+  // traced runs stay on one stream so per-kernel event times are not
+  // inflated by queueing behind concurrent branches
+  const bool fork = tr == nullptr;
+  cudaStream_t s_sync = fork ? sp.s[0] : st;
+  if (fork) link_streams(st, s_sync, sp.e[0]);
   const int kind = k.dialect == LEO_AMD ? LEO_EK_MEM_WAITCNT : k.dialect == LEO_NVIDIA ? LEO_EK_MEM_BARRIER : LEO_EK_MEM_SWSB;
   {
     cudaStream_t st = s_sync;   // shadows the caller's stream for the TRACED scopes
@@ -237,7 +240,7 @@ int build_graph_impl(const LeoKernel* kk, const LeoCaps* caps, LeoEdges* out, Le
   TRACED(KID_SCAN, scan_exclusive(uniq, eoff, nullptr, N, scan_tmp, &ctr[5], st));
   TRACED(KID_LINK_EMIT, k_link_emit<<<grid_for(N, T), T, 0, st>>>(k, cand_off, cand, uniq, eoff, *out, status));
 
-  link_streams(s_sync, st, sp.e[1]);   // join
+  if (fork) link_streams(s_sync, st, sp.e[1]);   // join
   TRACED(KID_SYNC_EMIT, k_sync_emit<<<grid_for(N, T), T, 0, st>>>(N, kind, ssorted, poff, puniq, puoff, &ctr[5], *out, status));
   TRACED(KID_EDGE_TOTALS, k_edge_totals<<<1, 1, 0, st>>>(&ctr[5], &ctr[6], *out, status));
   ar.release();
@@ -492,16 +495,17 @@ int leo_analyze(const LeoKernel* k, const LeoProfile* p, const LeoSamples* sampl
   SidePool& sp = side_pool();
   LeoTrace* tr = caps ? caps->trace : nullptr;
   // stage-0 binning only feeds pruning and blame: run it beside build_graph
+  const bool fork = tr == nullptr;
   if (samples) {
-    cudaStream_t s_bin = sp.s[1];
-    link_streams(st, s_bin, sp.e[2]);
+    cudaStream_t s_bin = fork ? sp.s[1] : st;
+    if (fork) link_streams(st, s_bin, sp.e[2]);
     int r = bin_impl(samples, k->n_instr, (int32_t*)p->lat, (int32_t*)p->cls_cnt, tr, s_bin);
     if (r) return r;
   }
   const Range own{cfg->consumer_lo, cfg->consumer_hi};
   int r = build_graph_impl(k, caps, base, diags, status, st, own);
   if (r) return r;
-  if (samples) link_streams(sp.s[1], st, sp.e[3]);
+  if (samples && fork) link_streams(sp.s[1], st, sp.e[3]);
   r = prune_impl(k, p, cfg, base, pruned, paths, diags, caps, status, st);
   if (r) return r;
   Arena ar{st};
@@ -513,12 +517,12 @@ int leo_analyze(const LeoKernel* k, const LeoProfile* p, const LeoSamples* sampl
   // them as parallel branches
   const bool do_slice = slice_level && slice_bitmap;
   if (do_slice) {
-    link_streams(st, sp.s[2], sp.e[4]);
-    r = slice_impl(k, p, pruned, inc, slice_bitmap, slice_level, tr, sp.s[2]);
+    if (fork) link_streams(st, sp.s[2], sp.e[4]);
+    r = slice_impl(k, p, pruned, inc, slice_bitmap, slice_level, tr, fork ? sp.s[2] : st);
     if (r) { ar.release(); return r; }
   }
   r = blame_impl(k, p, pruned, paths, base, inc, line_id, n_lines, blame, line_blame, line_stall, caps, status, st, own);
-  if (do_slice) link_streams(sp.s[2], st, sp.e[5]);
+  if (do_slice && fork) link_streams(sp.s[2], st, sp.e[5]);
   ar.release();
   return r;
 }
