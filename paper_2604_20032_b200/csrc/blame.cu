@@ -71,36 +71,52 @@ constexpr int kBinR = 2048;          // default instructions per bucket (64 KiB 
 constexpr int kBinRMax = 4096;       // 128 KiB of counters: up to 16.7M instructions
 constexpr int kBinMaxBuckets = 4096;
 
-__global__ void k_bin_hist(int64_t S, const int32_t* __restrict__ pc, int N, int nb, int R,
-                           int32_t* __restrict__ bucket_cnt, uint32_t* status) {
-  __shared__ int32_t h[kBinMaxBuckets];
+// chunk c of the sample stream = [c*per, min(S, (c+1)*per)), per a multiple of 4
+LEO_DEV int64_t bin_chunk_per(int64_t S, int G) { return (((S + G - 1) / G) + 3) & ~(int64_t)3; }
+
+// pass 1: chunk-local bucket histogram -> M[c * nb + b]
+__global__ void __launch_bounds__(512) k_bin_hist(int64_t S, const int32_t* __restrict__ pc, int N, int nb, int R,
+                                                  int32_t* __restrict__ M, uint32_t* status) {
+  extern __shared__ int32_t h[];                 // nb
   for (int x = threadIdx.x; x < nb; x += blockDim.x) h[x] = 0;
   __syncthreads();
-  const int64_t nvec = S / 4;
-  const int4* pc4 = reinterpret_cast<const int4*>(pc);
-  for (int64_t v = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; v < nvec; v += (int64_t)gridDim.x * blockDim.x) {
-    int4 p = pc4[v];
-    int ps[4] = {p.x, p.y, p.z, p.w};
+  const int64_t per = bin_chunk_per(S, gridDim.x);
+  const int64_t s0 = (int64_t)blockIdx.x * per, s1 = min(S, s0 + per);
+  if (s0 < s1) {
+    const int64_t v0 = s0 / 4, v1 = s1 / 4;     // s0 is a multiple of 4
+    const int4* pc4 = reinterpret_cast<const int4*>(pc);
+    for (int64_t v = v0 + threadIdx.x; v < v1; v += blockDim.x) {
+      const int4 p = pc4[v];
+      const int ps[4] = {p.x, p.y, p.z, p.w};
 #pragma unroll
-    for (int t = 0; t < 4; t++) {
-      int j = ps[t];
+      for (int t = 0; t < 4; t++) {
+        const int j = ps[t];
+        if (j < 0 || j >= N) { atomicOr(status, (uint32_t)LEO_ST_BAD_INPUT); continue; }
+        atomicAdd(&h[j / R], 1);
+      }
+    }
+    for (int64_t x = v1 * 4 + threadIdx.x; x < s1; x += blockDim.x) {
+      const int j = pc[x];
       if (j < 0 || j >= N) { atomicOr(status, (uint32_t)LEO_ST_BAD_INPUT); continue; }
       atomicAdd(&h[j / R], 1);
     }
   }
-  for (int64_t s = nvec * 4 + blockIdx.x * (int64_t)blockDim.x + threadIdx.x; s < S; s += (int64_t)gridDim.x * blockDim.x) {
-    int j = pc[s];
-    if (j < 0 || j >= N) { atomicOr(status, (uint32_t)LEO_ST_BAD_INPUT); continue; }
-    atomicAdd(&h[j / R], 1);
-  }
   __syncthreads();
-  for (int x = threadIdx.x; x < nb; x += blockDim.x)
-    if (h[x]) atomicAdd(&bucket_cnt[x], h[x]);
+  for (int x = threadIdx.x; x < nb; x += blockDim.x) M[(size_t)blockIdx.x * nb + x] = h[x];
 }
 
-// single CTA: bucket offsets, per-bucket cursors and slice offsets
+// pass 2a: bucket totals (thread per bucket, column sums over chunks)
+__global__ void k_bin_totals(int nb, int G, const int32_t* __restrict__ M, int32_t* __restrict__ tot) {
+  for (int b = blockIdx.x * blockDim.x + threadIdx.x; b < nb; b += gridDim.x * blockDim.x) {
+    int t = 0;
+    for (int c = 0; c < G; c++) t += M[(size_t)c * nb + b];
+    tot[b] = t;
+  }
+}
+
+// pass 2b (single CTA): bucket offsets + slice offsets
 __global__ void k_bin_plan(int nb, int slice, const int32_t* __restrict__ bucket_cnt, int32_t* __restrict__ bucket_off,
-                           int32_t* __restrict__ cursor, int32_t* __restrict__ slice_off) {
+                           int32_t* __restrict__ slice_off) {
   __shared__ int sw[33];
   int carry = 0, scarry = 0;
   for (int base = 0; base < nb; base += blockDim.x) {
@@ -110,42 +126,62 @@ __global__ void k_bin_plan(int nb, int slice, const int32_t* __restrict__ bucket
     int tot, stot;
     int ex = block_excl_scan(c, sw, &tot);
     int sex = block_excl_scan(ns, sw, &stot);
-    if (i < nb) { bucket_off[i] = carry + ex; cursor[i] = carry + ex; slice_off[i] = scarry + sex; }
+    if (i < nb) { bucket_off[i] = carry + ex; slice_off[i] = scarry + sex; }
     carry += tot; scarry += stot;
   }
   if (threadIdx.x == 0) { bucket_off[nb] = carry; slice_off[nb] = scarry; }
 }
 
-__global__ void k_bin_scatter(int64_t S, const int32_t* __restrict__ pc, const uint8_t* __restrict__ cat,
-                              const uint8_t* __restrict__ lut, int N, int nb, int R, int32_t* __restrict__ cursor,
-                              uint16_t* __restrict__ keys) {
-  __shared__ int32_t h[kBinMaxBuckets];
-  __shared__ uint8_t slut[256];
-  for (int x = threadIdx.x; x < nb; x += blockDim.x) h[x] = 0;
-  for (int x = threadIdx.x; x < 256; x += blockDim.x) slut[x] = lut[x];
-  __syncthreads();
-  // this CTA's contiguous chunk
-  const int64_t per = (S + gridDim.x - 1) / gridDim.x;
-  const int64_t s0 = (int64_t)blockIdx.x * per, s1 = min(S, s0 + per);
-  for (int64_t s = s0 + threadIdx.x; s < s1; s += blockDim.x) {
-    int j = pc[s];
-    if (j >= 0 && j < N) atomicAdd(&h[j / R], 1);
-  }
-  __syncthreads();
-  for (int x = threadIdx.x; x < nb; x += blockDim.x) {
-    int c = h[x];
-    h[x] = c ? atomicAdd(&cursor[x], c) : 0;        // this CTA's base in bucket x
-  }
-  __syncthreads();
-  for (int64_t s = s0 + threadIdx.x; s < s1; s += blockDim.x) {
-    int j = pc[s];
-    if (j < 0 || j >= N) continue;
-    int b = j / R;
-    int pos = atomicAdd(&h[b], 1);
-    keys[pos] = (uint16_t)(((j - b * R) << 3) | slut[cat[s]]);
+// pass 2c: per (chunk, bucket) write base = bucket_off[b] + sum of earlier chunks
+__global__ void k_bin_bases(int nb, int G, const int32_t* __restrict__ bucket_off, int32_t* __restrict__ M) {
+  for (int b = blockIdx.x * blockDim.x + threadIdx.x; b < nb; b += gridDim.x * blockDim.x) {
+    int run = bucket_off[b];
+    for (int c = 0; c < G; c++) {
+      const int v = M[(size_t)c * nb + b];
+      M[(size_t)c * nb + b] = run;
+      run += v;
+    }
   }
 }
 
+// pass 3: scatter u16 keys ((pc mod R) * 8 + class) into bucket ranges
+__global__ void __launch_bounds__(512) k_bin_scatter(int64_t S, const int32_t* __restrict__ pc, const uint8_t* __restrict__ cat,
+                                                     const uint8_t* __restrict__ lut, int N, int nb, int R,
+                                                     const int32_t* __restrict__ M, uint16_t* __restrict__ keys) {
+  extern __shared__ int32_t cur[];               // nb cursors
+  __shared__ uint8_t slut[256];
+  for (int x = threadIdx.x; x < nb; x += blockDim.x) cur[x] = M[(size_t)blockIdx.x * nb + x];
+  for (int x = threadIdx.x; x < 256; x += blockDim.x) slut[x] = lut[x];
+  __syncthreads();
+  const int64_t per = bin_chunk_per(S, gridDim.x);
+  const int64_t s0 = (int64_t)blockIdx.x * per, s1 = min(S, s0 + per);
+  if (s0 >= s1) return;
+  const int64_t v0 = s0 / 4, v1 = s1 / 4;
+  const int4* pc4 = reinterpret_cast<const int4*>(pc);
+  const uint32_t* cat4 = reinterpret_cast<const uint32_t*>(cat);
+  for (int64_t v = v0 + threadIdx.x; v < v1; v += blockDim.x) {
+    const int4 p = pc4[v];
+    const uint32_t c = cat4[v];
+    const int ps[4] = {p.x, p.y, p.z, p.w};
+#pragma unroll
+    for (int t = 0; t < 4; t++) {
+      const int j = ps[t];
+      if (j < 0 || j >= N) continue;
+      const int b = j / R;
+      const int pos = atomicAdd(&cur[b], 1);
+      keys[pos] = (uint16_t)(((j - b * R) << 3) | slut[(c >> (8 * t)) & 0xFF]);
+    }
+  }
+  for (int64_t x = v1 * 4 + threadIdx.x; x < s1; x += blockDim.x) {
+    const int j = pc[x];
+    if (j < 0 || j >= N) continue;
+    const int b = j / R;
+    const int pos = atomicAdd(&cur[b], 1);
+    keys[pos] = (uint16_t)(((j - b * R) << 3) | slut[cat[x]]);
+  }
+}
+
+// pass 4: count each (bucket, slice) in shared memory, merge into cls_cnt
 __global__ void __launch_bounds__(512) k_bin_count(int N, int nb, int R, int slice, const int32_t* __restrict__ bucket_off,
                                                    const int32_t* __restrict__ slice_off,
                                                    const uint16_t* __restrict__ keys,
@@ -153,8 +189,7 @@ __global__ void __launch_bounds__(512) k_bin_count(int N, int nb, int R, int sli
   extern __shared__ int32_t cnt[];              // R * 8
   const int total_slices = slice_off[nb];
   for (int sl = blockIdx.x; sl < total_slices; sl += gridDim.x) {
-    // bucket of this slice: largest b with slice_off[b] <= sl
-    int lo = 0, hi = nb - 1;
+    int lo = 0, hi = nb - 1;                      // bucket: largest b with slice_off[b] <= sl
     while (lo < hi) {
       int mid = (lo + hi + 1) >> 1;
       if (slice_off[mid] <= sl) lo = mid; else hi = mid - 1;
@@ -165,11 +200,20 @@ __global__ void __launch_bounds__(512) k_bin_count(int N, int nb, int R, int sli
     const int64_t e1 = min((int64_t)bucket_off[b + 1], e0 + slice);
     for (int x = threadIdx.x; x < R * 8; x += blockDim.x) cnt[x] = 0;
     __syncthreads();
-    for (int64_t e = e0 + threadIdx.x; e - threadIdx.x < e1; e += blockDim.x) {
-      int key = e < e1 ? (int)keys[e] : -1;
-      unsigned grp = __match_any_sync(0xffffffffu, key);
-      if (key >= 0 && (__ffs(grp) - 1) == (int)(threadIdx.x & 31)) atomicAdd(&cnt[key], __popc(grp));
+    // aligned body: 8 keys per uint4
+    const int64_t a0 = min(e1, (e0 + 7) & ~(int64_t)7), a1 = max(a0, e1 & ~(int64_t)7);
+    for (int64_t e = e0 + threadIdx.x; e < a0; e += blockDim.x) atomicAdd(&cnt[keys[e]], 1);
+    const uint4* k4 = reinterpret_cast<const uint4*>(keys);
+    for (int64_t v = a0 / 8 + threadIdx.x; v < a1 / 8; v += blockDim.x) {
+      const uint4 q = k4[v];
+      const uint32_t w[4] = {q.x, q.y, q.z, q.w};
+#pragma unroll
+      for (int t = 0; t < 4; t++) {
+        atomicAdd(&cnt[w[t] & 0xFFFF], 1);
+        atomicAdd(&cnt[w[t] >> 16], 1);
+      }
     }
+    for (int64_t e = a1 + threadIdx.x; e < e1; e += blockDim.x) atomicAdd(&cnt[keys[e]], 1);
     __syncthreads();
     const int64_t base = (int64_t)b * R * 8;
     const int lim = (int)min((int64_t)R * 8, ((int64_t)N - (int64_t)b * R) * 8);

@@ -91,19 +91,21 @@ __global__ void k_block_walk(KView k, WalkArgs a, int warps_per_cta) {
           else if (qtab[u] >= ev_block) res = -(qtab[u] + 1);
           else fresh = true;
         }
-        unsigned fm = __ballot_sync(0xffffffffu, fresh);
-        if (fm) {
-          unsigned grp = __match_any_sync(0xffffffffu, fresh ? u : -2 - lane);
-          int leader = __ffs(grp) - 1;
-          int slot = __shfl_sync(0xffffffffu, e, leader);
-          bool lead = fresh && lane == leader;
-          unsigned lm = __ballot_sync(0xffffffffu, lead);
+        // first claimant of (block, unit) creates the query: qtab[u] still
+        // holds a stale slot (< ev_block) until one lane's CAS replaces it
+        bool lead = false;
+        if (fresh) {
+          const int seen = qtab[u];
+          const int prev = atomicCAS(&qtab[u], seen, e);
+          if (prev == seen) { lead = true; res = -(e + 1); }
+          else res = -(prev + 1);          // another lane of this chunk claimed it
+        }
+        const unsigned lm = __ballot_sync(0xffffffffu, lead);
+        if (lm) {
           int qbase = 0;
-          if (lane == 0 && lm) qbase = atomicAdd(a.q_count, __popc(lm));
+          if (lane == 0) qbase = atomicAdd(a.q_count, __popc(lm));
           qbase = __shfl_sync(0xffffffffu, qbase, 0);
-          if (fresh) res = -(slot + 1);
           if (lead) {
-            qtab[u] = e;
             a.q_block[e] = b;
             a.q_unit[e] = u;
             a.q_list[qbase + __popc(lm & ((1u << lane) - 1))] = e;
@@ -257,29 +259,103 @@ LEO_DEV void reach_commit(const ReachArgs& a, int e, const int32_t* res, int nre
   a.q_len[e] = nres;
 }
 
-// Tier 1: one thread per query; the visited hash lives in shared memory
-// (64 slots per thread, strided for bank spread), so every query of a kernel
-// is in flight at once and latency is hidden by thread-level parallelism.
+// Tier 1: lockstep per-lane state machine.  Every lane owns one query at a
+// time and advances it by one search step per loop iteration; a lane whose
+// query finished fetches the next from a shared queue (warp-aggregated
+// atomic), so lanes never idle behind the warp's longest query.  The visited
+// set is a private open-addressing hash in shared memory (strided per thread),
+// cleared through the list of slots it used.
 constexpr int kT1Hash = 64, kT1Limit = 40, kT1Stack = 40, kT1Res = 16, kT1Threads = 256;
 
 __global__ void __launch_bounds__(kT1Threads) k_reach_fast(KView k, ReachArgs a,
                                                            const int32_t* __restrict__ q_list,
-                                                           const int32_t* q_count) {
+                                                           const int32_t* q_count, int32_t* q_head) {
   extern __shared__ int32_t hsm[];
   const int nq = *q_count;
-  SmemHash vis{hsm + threadIdx.x, (int)blockDim.x, kT1Hash, 0, kT1Limit};
+  const int lane = threadIdx.x & 31;
+  int32_t* H = hsm + threadIdx.x;                  // slot s at H[s * blockDim.x]
+  const int stride = blockDim.x;
+  for (int s2 = 0; s2 < kT1Hash; s2++) H[s2 * stride] = -1;
   int32_t stk[kT1Stack], res[kT1Res];
-  for (int t = blockIdx.x * blockDim.x + threadIdx.x; t < nq; t += gridDim.x * blockDim.x) {
-    const int e = q_list[t];
-    vis.clear();
-    int nres = 0;
-    if (!(a.dbg & (LEO_DBG_REACH_T2 | LEO_DBG_REACH_T3)) &&
-        reach_search(k, a, a.q_block[e], a.q_unit[e], vis, stk, kT1Stack, res, kT1Res, &nres)) {
-      reach_commit(a, e, res, nres);
-    } else {
-      int s = atomicAdd(a.slow_count, 1);
-      if (s < a.slow_cap) a.slow_list[s] = e;
-      else atomicOr(a.status, (uint32_t)LEO_ST_SCRATCH_OVERFLOW);
+  uint8_t used[kT1Limit];
+  int e = -1, u = 0, sp = 0, nres = 0, nused = 0;
+  bool drained = false, ovf = false;
+
+  auto insert = [&](int key) -> int {              // 1 new, 0 seen, -1 overflow
+    int x = (int)(((uint32_t)key * 2654435761u) >> 26);
+    for (int probe = 0; probe < kT1Hash; probe++) {
+      const int v = H[x * stride];
+      if (v == key) return 0;
+      if (v == -1) {
+        if (nused == kT1Limit) return -1;
+        H[x * stride] = key;
+        used[nused++] = (uint8_t)x;
+        return 1;
+      }
+      x = (x + 1) & (kT1Hash - 1);
+    }
+    return -1;
+  };
+  auto release = [&]() {
+    for (int t = 0; t < nused; t++) H[used[t] * stride] = -1;
+    nused = 0; sp = 0; nres = 0; ovf = false; e = -1;
+  };
+
+  while (true) {
+    // lanes without a query fetch one (one atomic per warp)
+    const bool need = e < 0 && !drained;
+    const unsigned m = __ballot_sync(0xffffffffu, need);
+    if (m) {
+      int base = 0;
+      if (lane == __ffs(m) - 1) base = atomicAdd(q_head, __popc(m));
+      base = __shfl_sync(0xffffffffu, base, __ffs(m) - 1);
+      if (need) {
+        const int t = base + __popc(m & ((1u << lane) - 1));
+        if (t >= nq) {
+          drained = true;
+        } else {
+          e = q_list[t];
+          u = a.q_unit[e];
+          const int b = a.q_block[e];
+          if (a.dbg & (LEO_DBG_REACH_T2 | LEO_DBG_REACH_T3)) ovf = true;
+          for (int q = k.pred_ptr[b]; q < k.pred_ptr[b + 1] && !ovf; q++) {
+            const int p = k.pred[q];
+            const int v = insert(p);
+            if (v < 0 || (v && sp == kT1Stack)) ovf = true;
+            else if (v) stk[sp++] = p;
+          }
+        }
+      }
+    }
+    if (!__any_sync(0xffffffffu, e >= 0)) {
+      if (__all_sync(0xffffffffu, drained)) break;
+      continue;
+    }
+    if (e >= 0) {
+      if (!ovf && sp > 0) {                        // one search step
+        const int y = stk[--sp];
+        const int4 r = a.rec[y];
+        const int ld = run_lookup(a, y, r.x, u);
+        if (ld >= 0) {
+          if (nres == kT1Res) ovf = true; else res[nres++] = ld;
+        } else {
+          for (int t = 0; t < r.y && !ovf; t++) {
+            const int pp = r.y <= 2 ? (t == 0 ? r.z : r.w) : k.pred[r.z + t];
+            const int v = insert(pp);
+            if (v < 0 || (v && sp == kT1Stack)) ovf = true;
+            else if (v) stk[sp++] = pp;
+          }
+        }
+      }
+      if (ovf) {                                   // hand the query to tier 2
+        const int s2 = atomicAdd(a.slow_count, 1);
+        if (s2 < a.slow_cap) a.slow_list[s2] = e;
+        else atomicOr(a.status, (uint32_t)LEO_ST_SCRATCH_OVERFLOW);
+        release();
+      } else if (sp == 0) {                        // done: commit the results
+        reach_commit(a, e, res, nres);
+        release();
+      }
     }
   }
 }

@@ -223,7 +223,9 @@ int build_graph_impl(const LeoKernel* kk, const LeoCaps* caps, LeoEdges* out, Le
   if (B > 0) TRACED(KID_RUN_HEADS, k_block_records<<<grid_for(B, T), T, 0, st>>>(k, brec));
   ReachArgs ra{caps ? caps->debug_flags : 0, ldtab, brec, U, q_block, q_unit, q_off, q_len, qres, cap_qres, &ctr[1],
                slow_list, &ctr[2], NU + 1024, status};
-  TRACED(KID_REACH_FAST, k_reach_fast<<<grid_for(NU, kT1Threads), kT1Threads, kT1Threads * kT1Hash * 4, st>>>(k, ra, q_list, &ctr[0]));
+  // tier 1 is persistent: enough CTAs to fill the chip, queries fetched dynamically
+  TRACED(KID_REACH_FAST, k_reach_fast<<<std::max(1, std::min<int>(grid_for(NU, kT1Threads), SM * 3)), kT1Threads,
+                                        kT1Threads * kT1Hash * 4, st>>>(k, ra, q_list, &ctr[0], &ctr[9]));
   {
     const int wpc_r = 4;
     const size_t sm_r = (size_t)wpc_r * kWarpSmemInts * 4;
@@ -387,26 +389,28 @@ static int bin_impl(const LeoSamples* s, int32_t n_instr, int32_t* lat, int32_t*
   cudaMemsetAsync(cls_cnt, 0, (size_t)std::max(n_instr, 1) * 32, st);
   const int64_t S = s->n_samples;
   const int R = (n_instr + kBinR - 1) / kBinR <= kBinMaxBuckets ? kBinR : kBinRMax;
-  const int nb = (n_instr + R - 1) / R;
+  const int nb = std::max(1, (n_instr + R - 1) / R);
+  const bool bucketed = nb <= kBinMaxBuckets && S > 0;
+  // chunks: enough CTAs to stream the samples, bounded so the [G x nb] matrix stays small
+  const int G = (int)std::max<int64_t>(1, std::min<int64_t>(num_sms() * 4, (S + 8191) / 8192));
   Arena ar{st};
   uint32_t* status;
-  int32_t *bcnt, *boff, *bcur, *soff;
+  int32_t *M, *btot, *boff, *soff;
   uint16_t* keys;
-  const bool bucketed = nb <= kBinMaxBuckets && S > 0;
   ar.want(&status, 1);
-  ar.want(&bcnt, nb + 1); ar.want(&boff, nb + 1); ar.want(&bcur, nb + 1); ar.want(&soff, nb + 1);
-  ar.want(&keys, bucketed ? S : 1);
+  ar.want(&M, bucketed ? (int64_t)G * nb : 1);
+  ar.want(&btot, nb + 1); ar.want(&boff, nb + 1); ar.want(&soff, nb + 1);
+  ar.want(&keys, bucketed ? S + 8 : 1);
   LEO_CUDA_CHECK(ar.commit());
   cudaMemsetAsync(status, 0, 4, st);
   if (bucketed) {
     const int smem = R * 8 * 4;
-    cudaMemsetAsync(bcnt, 0, (size_t)(nb + 1) * 4, st);
-    const int G = num_sms() * 4;
-    TRACED(KID_BIN_HIST, k_bin_hist<<<grid_for(S / 4 + 1, 256, G), 256, 0, st>>>(S, s->pc, n_instr, nb, R, bcnt, status));
-    // slices: enough counting CTAs to fill the chip, >= 4K samples each
     const int slice = (int)std::min<int64_t>(65536, std::max<int64_t>(4096, S / (num_sms() * 3)));
-    TRACED(KID_BIN_PLAN, k_bin_plan<<<1, 1024, 0, st>>>(nb, slice, bcnt, boff, bcur, soff));
-    TRACED(KID_BIN_SCATTER, k_bin_scatter<<<grid_for(S, 1024, G), 1024, 0, st>>>(S, s->pc, s->cat, s->cat_to_cs, n_instr, nb, R, bcur, keys));
+    TRACED(KID_BIN_HIST, k_bin_hist<<<G, 512, nb * 4, st>>>(S, s->pc, n_instr, nb, R, M, status));
+    TRACED(KID_BIN_PLAN, k_bin_totals<<<grid_for(nb, 128), 128, 0, st>>>(nb, G, M, btot));
+    TRACED(KID_BIN_PLAN, k_bin_plan<<<1, 1024, 0, st>>>(nb, slice, btot, boff, soff));
+    TRACED(KID_BIN_PLAN, k_bin_bases<<<grid_for(nb, 128), 128, 0, st>>>(nb, G, boff, M));
+    TRACED(KID_BIN_SCATTER, k_bin_scatter<<<G, 512, nb * 4, st>>>(S, s->pc, s->cat, s->cat_to_cs, n_instr, nb, R, M, keys));
     TRACED(KID_BIN, k_bin_count<<<num_sms() * 3, 512, smem, st>>>(n_instr, nb, R, slice, boff, soff, keys, cls_cnt));
   } else if (S > 0) {
     TRACED(KID_BIN, k_bin_samples<<<grid_for(S / 4 + 1, 256, num_sms() * 8), 256, 0, st>>>(
