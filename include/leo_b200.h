@@ -212,6 +212,10 @@ typedef struct LeoCaps {
   LeoTrace* trace;            /* optional, host struct (NULL = no tracing) */
   int32_t debug_flags;        /* testing: route every item to a larger tier (LEO_DBG_*) */
   int32_t options;            /* LEO_OPT_* */
+  void*    workspace;         /* optional caller-owned device scratch (bump-allocated per call) */
+  int64_t  workspace_bytes;
+  int64_t* workspace_needed;  /* optional HOST out: bytes this call wanted; when it exceeds
+                                 workspace_bytes the library used the stream-ordered allocator */
 } LeoCaps;
 /* LEO_OPT_ACCUMULATE_LINES: add into line_blame / line_stall instead of
  * zeroing them first (many kernels of one batch share one per-line vector) */

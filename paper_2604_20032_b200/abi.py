@@ -51,7 +51,9 @@ class LeoTrace(C.Structure):
 class LeoCaps(C.Structure):
     _fields_ = [("query_results", C.c_int64), ("candidates", C.c_int64),
                 ("sync_keys", C.c_int64), ("slow_items", C.c_int64),
-                ("trace", C.POINTER(LeoTrace)), ("debug_flags", C.c_int32), ("options", C.c_int32)]
+                ("trace", C.POINTER(LeoTrace)), ("debug_flags", C.c_int32), ("options", C.c_int32),
+                ("workspace", C.c_void_p), ("workspace_bytes", C.c_int64),
+                ("workspace_needed", C.POINTER(C.c_int64))]
 
 
 DBG_REACH_T2, DBG_REACH_T3, DBG_SYNC_SLOW, DBG_PRUNE_SLOW, DBG_SELF_SLOW = 1, 2, 4, 8, 16

@@ -60,7 +60,30 @@ int num_sms() {
   return g_num_sms;
 }
 
-// Stream-ordered bump arena: one cudaMallocAsync per entry point.
+// Caller-owned workspace (LeoCaps.workspace): every arena of one entry-point
+// call is bump-allocated from it (no reuse inside a call, so concurrent
+// branches never alias); the bytes wanted are reported back so the caller can
+// size it.  Without a big enough workspace the stream-ordered allocator is used.
+struct WsCursor { char* base = nullptr; size_t cap = 0, off = 0, needed = 0; };
+thread_local WsCursor* t_ws = nullptr;
+struct WsScope {
+  WsCursor c;
+  WsCursor* prev;
+  const LeoCaps* caps;
+  explicit WsScope(const LeoCaps* cp) : prev(t_ws), caps(cp) {
+    if (cp && cp->workspace && cp->workspace_bytes > 0) {
+      c.base = (char*)cp->workspace;
+      c.cap = (size_t)cp->workspace_bytes;
+    }
+    t_ws = &c;
+  }
+  ~WsScope() {
+    if (caps && caps->workspace_needed) *caps->workspace_needed = (int64_t)c.needed;
+    t_ws = prev;
+  }
+};
+
+// Stream-ordered bump arena: one allocation per stage.
 struct Arena {
   cudaStream_t st;
   char* base = nullptr;
@@ -71,11 +94,19 @@ struct Arena {
   template <typename T> void want(T** dst, int64_t n) {
     reqs[nreq++] = Req{(void**)dst, (size_t)std::max<int64_t>(n, 1) * sizeof(T)};
   }
+  bool from_ws = false;
   cudaError_t commit() {
     size_t total = 0;
     for (int i = 0; i < nreq; i++) total += (reqs[i].bytes + 255) & ~(size_t)255;
-    cudaError_t e = cudaMallocAsync((void**)&base, total, st);
-    if (e != cudaSuccess) return e;
+    if (t_ws) t_ws->needed += total;
+    if (t_ws && t_ws->base && t_ws->off + total <= t_ws->cap) {
+      base = t_ws->base + t_ws->off;
+      t_ws->off += total;
+      from_ws = true;
+    } else {
+      cudaError_t e = cudaMallocAsync((void**)&base, total, st);
+      if (e != cudaSuccess) return e;
+    }
     cap = total;
     for (int i = 0; i < nreq; i++) {
       *reqs[i].dst = base + off;
@@ -83,7 +114,7 @@ struct Arena {
     }
     return cudaSuccess;
   }
-  void release() { if (base) cudaFreeAsync(base, st); base = nullptr; }
+  void release() { if (base && !from_ws) cudaFreeAsync(base, st); base = nullptr; }
 };
 
 inline int64_t pick(int64_t hint, int64_t dflt) { return hint > 0 ? hint : dflt; }
@@ -448,12 +479,14 @@ const char* leo_kernel_name(int id) { return (id >= 0 && id < KID_COUNT_) ? kKer
 
 int leo_build_graph(const LeoKernel* k, const LeoCaps* caps, LeoEdges* out, LeoDiags* diags,
                     uint32_t* status, void* stream) {
+  WsScope ws_scope(caps);
   if (int e = check_kernel(k)) return e;
   return build_graph_impl(k, caps, out, diags, status, (cudaStream_t)stream);
 }
 
 int leo_prune(const LeoKernel* k, const LeoProfile* p, const LeoConfig* cfg, const LeoEdges* in,
               LeoEdges* out, LeoPaths* paths, LeoDiags* diags, uint32_t* status, void* stream) {
+  WsScope ws_scope(nullptr);
   if (int e = check_kernel(k)) return e;
   if (!cfg || cfg->max_paths < 0 || cfg->max_depth < 0) return -3;
   return prune_impl(k, p, cfg, in, out, paths, diags, nullptr, status, (cudaStream_t)stream);
@@ -461,6 +494,7 @@ int leo_prune(const LeoKernel* k, const LeoProfile* p, const LeoConfig* cfg, con
 
 int leo_slice(const LeoKernel* k, const LeoProfile* p, const LeoEdges* pruned, uint32_t* bitmap,
               int32_t* level, void* stream) {
+  WsScope ws_scope(nullptr);
   if (int e = check_kernel(k)) return e;
   cudaStream_t st = (cudaStream_t)stream;
   Arena ar{st};
@@ -476,6 +510,7 @@ int leo_slice(const LeoKernel* k, const LeoProfile* p, const LeoEdges* pruned, u
 int leo_blame(const LeoKernel* k, const LeoProfile* p, const LeoEdges* pruned, const LeoPaths* paths,
               const LeoEdges* base, const int32_t* line_id, int32_t n_lines, LeoBlame* out,
               double* line_blame, double* line_stall, uint32_t* status, void* stream) {
+  WsScope ws_scope(nullptr);
   if (int e = check_kernel(k)) return e;
   cudaStream_t st = (cudaStream_t)stream;
   Arena ar{st};
@@ -493,6 +528,7 @@ int leo_analyze(const LeoKernel* k, const LeoProfile* p, const LeoSamples* sampl
                 const LeoCaps* caps, LeoEdges* base, LeoEdges* pruned, LeoPaths* paths, LeoDiags* diags,
                 LeoBlame* blame, uint32_t* slice_bitmap, int32_t* slice_level, const int32_t* line_id,
                 int32_t n_lines, double* line_blame, double* line_stall, uint32_t* status, void* stream) {
+  WsScope ws_scope(caps);
   if (int e = check_kernel(k)) return e;
   if (!cfg) return -3;
   cudaStream_t st = (cudaStream_t)stream;

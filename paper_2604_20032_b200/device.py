@@ -117,6 +117,8 @@ class Analyzer:
         self.debug_flags = debug_flags
         self.shared_lines = lines
         self.do_slice = do_slice
+        self.ws = None                       # persistent device workspace (LeoCaps.workspace)
+        self.ws_needed = C.c_int64(0)
         self.dk = dk
         self.device = torch.device(device)
         n = dk.n_instr
@@ -166,8 +168,25 @@ class Analyzer:
         nu, n = self.n_use_units, self.dk.n_instr
         self.s_caps = abi.LeoCaps((4 * nu + 1024) * s, (6 * nu + 1024) * s, (2 * n + 1024) * s,
                                   (n // 4 + 1024) * s, None, self.debug_flags,
-                                  abi.OPT_ACCUMULATE_LINES if self.shared_lines is not None else 0)
+                                  abi.OPT_ACCUMULATE_LINES if self.shared_lines is not None else 0,
+                                  None, 0, C.pointer(self.ws_needed))
+        self._bind_workspace()
         self.set_tracer(self.tracer)
+
+    def _bind_workspace(self):
+        if self.ws is not None:
+            self.s_caps.workspace = self.ws.data_ptr()
+            self.s_caps.workspace_bytes = self.ws.numel()
+
+    def ensure_workspace(self) -> bool:
+        """Grow the persistent workspace to what the last call wanted; True if grown."""
+        need = int(self.ws_needed.value)
+        have = 0 if self.ws is None else self.ws.numel()
+        if need <= have:
+            return False
+        self.ws = torch.empty(int(need * 1.25) + (1 << 20), dtype=torch.uint8, device=self.device)
+        self._bind_workspace()
+        return True
         self.status_ptr = at(C_STATUS)
 
     def set_tracer(self, tracer: "Tracer | None"):
@@ -251,9 +270,12 @@ class Analyzer:
             if status & abi.ST_SCRATCH_OVERFLOW:
                 caps.scratch_scale *= 4
                 grow = True
+            if grow:
+                self._alloc()
+            if self.ensure_workspace():
+                grow = True
             if not grow:
                 return c
-            self._alloc()
         raise RuntimeError("leo_analyze: buffers kept overflowing")
 
     # -- results -------------------------------------------------------------

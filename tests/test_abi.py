@@ -41,7 +41,7 @@ def test_ctypes_struct_sizes_match_header():
     # pointer-heavy structs: fields laid out as in the header
     assert C.sizeof(abi.LeoDiag) == 24
     assert C.sizeof(abi.LeoConfig) == 16 + 16 * 8 + 8
-    assert C.sizeof(abi.LeoCaps) == 48
+    assert C.sizeof(abi.LeoCaps) == 72
     assert abi.LeoKernel.opclass.offset == 4 * 15 + 4  # 15 int32 + padding to 8
 
 
