@@ -170,6 +170,7 @@ class Analyzer:
                                   (n // 4 + 1024) * s, None, self.debug_flags,
                                   abi.OPT_ACCUMULATE_LINES if self.shared_lines is not None else 0,
                                   None, 0, C.pointer(self.ws_needed))
+        self.status_ptr = at(C_STATUS)
         self._bind_workspace()
         self.set_tracer(self.tracer)
 
@@ -187,7 +188,6 @@ class Analyzer:
         self.ws = torch.empty(int(need * 1.25) + (1 << 20), dtype=torch.uint8, device=self.device)
         self._bind_workspace()
         return True
-        self.status_ptr = at(C_STATUS)
 
     def set_tracer(self, tracer: "Tracer | None"):
         self.tracer = tracer
