@@ -362,6 +362,7 @@ class Session:
         self.lut.copy_(self._host["lut"], non_blocking=True)
         self.an.launch(self.dp, self.cfg, self.ds)
         c = self.an.ctr.cpu().numpy()          # sync: how much to read back
+        self.an.ensure_workspace()             # persistent scratch for the next call
         nbl = min(int(c[device.C_BLAME]), self.an.caps.blame)
         if nbl > self.an.caps.blame or c[device.C_STATUS] != 0:
             self.an.run(self.dp, self.cfg, self.ds)

@@ -350,7 +350,7 @@ __global__ void __launch_bounds__(kT1Threads) k_reach_fast(KView k, ReachArgs a,
       if (ovf) {                                   // hand the query to tier 2
         const int s2 = atomicAdd(a.slow_count, 1);
         if (s2 < a.slow_cap) a.slow_list[s2] = e;
-        else atomicOr(a.status, (uint32_t)LEO_ST_SCRATCH_OVERFLOW);
+        else { a.q_off[e] = 0; a.q_len[e] = 0; atomicOr(a.status, (uint32_t)LEO_ST_SCRATCH_OVERFLOW); }
         release();
       } else if (sp == 0) {                        // done: commit the results
         reach_commit(a, e, res, nres);
@@ -436,7 +436,7 @@ __global__ void k_reach_warp(KView k, ReachArgs a, const int32_t* __restrict__ l
       if (lane == 0) {
         int s = atomicAdd(slow_count, 1);
         if (s < a.slow_cap) slow_list[s] = e;
-        else atomicOr(a.status, (uint32_t)LEO_ST_SCRATCH_OVERFLOW);
+        else { a.q_off[e] = 0; a.q_len[e] = 0; atomicOr(a.status, (uint32_t)LEO_ST_SCRATCH_OVERFLOW); }
       }
     } else {
       const int nres = c[0];

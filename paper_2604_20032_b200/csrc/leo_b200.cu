@@ -290,7 +290,7 @@ int prune_impl(const LeoKernel* kk, const LeoProfile* pp, const LeoConfig* cfg, 
   KView k = make_kview(kk);
   PView p = make_pview(pp);
   const int64_t cap_in = in->capacity;
-  const int64_t cap_slow = pick(caps ? caps->slow_items : 0, cap_in / 8 + 1024);
+  const int64_t cap_slow = std::max<int64_t>(caps ? caps->slow_items : 0, cap_in / 8 + 1024);
   const int PW = 32;
   const size_t pslow = prune_slow_bytes(cfg->max_depth, cfg->max_paths);
   Arena ar{st};

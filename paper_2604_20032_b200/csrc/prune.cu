@@ -179,6 +179,7 @@ LEO_DEV bool prune_one(const KView& k, const PView& p, const PruneArgs& a, int e
         if (off + nv > a.paths.capacity) {
           atomicOr(a.status, (uint32_t)LEO_ST_PATH_OVERFLOW);
           off = -1;
+          nv = 0;                                        // keep readers in bounds
         } else {
           int64_t s = 0;
           for (int x = 0; x < nv; x++) { a.paths.len[off + x] = vlen[x]; a.paths.accum[off + x] = vacc[x]; s += vlen[x]; }
@@ -216,8 +217,14 @@ __global__ void __launch_bounds__(128) k_prune_edges(KView k, PView p, PruneArgs
     bool ok = !big_paths && prune_one(k, p, a, e, stk, kDfsStack, arena, kDfsArena, vlen, vacc, kDfsPaths);
     if (!ok) {
       int s = atomicAdd(a.slow_count, 1);
-      if (s < a.slow_cap) a.slow_list[s] = e;
-      else atomicOr(a.status, (uint32_t)LEO_ST_SCRATCH_OVERFLOW);
+      if (s < a.slow_cap) {
+        a.slow_list[s] = e;
+      } else {
+        // no room: leave safe outputs (dropped edge, no paths); the host sees
+        // the status bit and re-runs with a larger slow list
+        a.keep[e] = 0; a.npaths[e] = 0; a.pfirst[e] = -1; a.dist[e] = 1.0;
+        atomicOr(a.status, (uint32_t)LEO_ST_SCRATCH_OVERFLOW);
+      }
     }
   }
 }
