@@ -265,7 +265,7 @@ LEO_DEV void reach_commit(const ReachArgs& a, int e, const int32_t* res, int nre
 // atomic), so lanes never idle behind the warp's longest query.  The visited
 // set is a private open-addressing hash in shared memory (strided per thread),
 // cleared through the list of slots it used.
-constexpr int kT1Hash = 64, kT1Limit = 40, kT1Stack = 40, kT1Res = 16, kT1Threads = 256;
+constexpr int kT1Hash = 128, kT1Limit = 96, kT1Stack = 96, kT1Res = 32, kT1Threads = 128;
 
 __global__ void __launch_bounds__(kT1Threads) k_reach_fast(KView k, ReachArgs a,
                                                            const int32_t* __restrict__ q_list,
@@ -282,7 +282,7 @@ __global__ void __launch_bounds__(kT1Threads) k_reach_fast(KView k, ReachArgs a,
   bool drained = false, ovf = false;
 
   auto insert = [&](int key) -> int {              // 1 new, 0 seen, -1 overflow
-    int x = (int)(((uint32_t)key * 2654435761u) >> 26);
+    int x = (int)(((uint32_t)key * 2654435761u) >> 25);   // 7 bits
     for (int probe = 0; probe < kT1Hash; probe++) {
       const int v = H[x * stride];
       if (v == key) return 0;
@@ -334,8 +334,9 @@ __global__ void __launch_bounds__(kT1Threads) k_reach_fast(KView k, ReachArgs a,
     if (e >= 0) {
       if (!ovf && sp > 0) {                        // one search step
         const int y = stk[--sp];
+        const int own = a.ldtab[(size_t)y * a.U + u];  // issued together with the record load
         const int4 r = a.rec[y];
-        const int ld = run_lookup(a, y, r.x, u);
+        const int ld = own >= 0 ? own : (r.x < y ? run_lookup(a, y - 1, r.x, u) : -1);
         if (ld >= 0) {
           if (nres == kT1Res) ovf = true; else res[nres++] = ld;
         } else {
