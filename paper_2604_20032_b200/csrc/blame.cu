@@ -105,12 +105,21 @@ __global__ void __launch_bounds__(512) k_bin_hist(int64_t S, const int32_t* __re
   for (int x = threadIdx.x; x < nb; x += blockDim.x) M[(size_t)blockIdx.x * nb + x] = h[x];
 }
 
-// pass 2a: bucket totals (thread per bucket, column sums over chunks)
-__global__ void k_bin_totals(int nb, int G, const int32_t* __restrict__ M, int32_t* __restrict__ tot) {
-  for (int b = blockIdx.x * blockDim.x + threadIdx.x; b < nb; b += gridDim.x * blockDim.x) {
-    int t = 0;
-    for (int c = 0; c < G; c++) t += M[(size_t)c * nb + b];
-    tot[b] = t;
+// pass 2a: CTA per bucket: exclusive scan of the bucket's chunk counts in
+// place (M[c][b] becomes the chunk's offset inside the bucket) + bucket total
+__global__ void k_bin_colscan(int nb, int G, int32_t* __restrict__ M, int32_t* __restrict__ tot) {
+  __shared__ int sw[33];
+  for (int b = blockIdx.x; b < nb; b += gridDim.x) {
+    int carry = 0;
+    for (int base = 0; base < G; base += blockDim.x) {
+      const int c = base + threadIdx.x;
+      const int v = c < G ? M[(size_t)c * nb + b] : 0;
+      int t;
+      const int ex = block_excl_scan(v, sw, &t);
+      if (c < G) M[(size_t)c * nb + b] = carry + ex;
+      carry += t;
+    }
+    if (threadIdx.x == 0) tot[b] = carry;
   }
 }
 
@@ -132,25 +141,14 @@ __global__ void k_bin_plan(int nb, int slice, const int32_t* __restrict__ bucket
   if (threadIdx.x == 0) { bucket_off[nb] = carry; slice_off[nb] = scarry; }
 }
 
-// pass 2c: per (chunk, bucket) write base = bucket_off[b] + sum of earlier chunks
-__global__ void k_bin_bases(int nb, int G, const int32_t* __restrict__ bucket_off, int32_t* __restrict__ M) {
-  for (int b = blockIdx.x * blockDim.x + threadIdx.x; b < nb; b += gridDim.x * blockDim.x) {
-    int run = bucket_off[b];
-    for (int c = 0; c < G; c++) {
-      const int v = M[(size_t)c * nb + b];
-      M[(size_t)c * nb + b] = run;
-      run += v;
-    }
-  }
-}
-
 // pass 3: scatter u16 keys ((pc mod R) * 8 + class) into bucket ranges
 __global__ void __launch_bounds__(512) k_bin_scatter(int64_t S, const int32_t* __restrict__ pc, const uint8_t* __restrict__ cat,
                                                      const uint8_t* __restrict__ lut, int N, int nb, int R,
-                                                     const int32_t* __restrict__ M, uint16_t* __restrict__ keys) {
+                                                     const int32_t* __restrict__ M, const int32_t* __restrict__ bucket_off,
+                                                     uint16_t* __restrict__ keys) {
   extern __shared__ int32_t cur[];               // nb cursors
   __shared__ uint8_t slut[256];
-  for (int x = threadIdx.x; x < nb; x += blockDim.x) cur[x] = M[(size_t)blockIdx.x * nb + x];
+  for (int x = threadIdx.x; x < nb; x += blockDim.x) cur[x] = bucket_off[x] + M[(size_t)blockIdx.x * nb + x];
   for (int x = threadIdx.x; x < 256; x += blockDim.x) slut[x] = lut[x];
   __syncthreads();
   const int64_t per = bin_chunk_per(S, gridDim.x);

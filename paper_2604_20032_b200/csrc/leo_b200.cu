@@ -25,14 +25,14 @@ enum KernelId {
   KID_REACH_SLOW, KID_LINK_COUNT, KID_LINK_FILL, KID_SEGSORT, KID_LINK_EMIT, KID_SYNC,
   KID_SYNC_SLOW, KID_KEY_HIST, KID_KEY_SCATTER, KID_SYNC_EMIT, KID_EDGE_TOTALS, KID_PRUNE,
   KID_PRUNE_SLOW, KID_COMPACT, KID_SEG_BOUNDS, KID_SYNC_HIST, KID_SYNC_FILL, KID_BLAME_COUNT,
-  KID_SELFBLAME_SLOW, KID_BLAME_FILL, KID_BLAME_TOTAL, KID_LINES, KID_SLICE, KID_REACH_WARP, KID_RUN_HEADS, KID_BIN_HIST, KID_BIN_PLAN, KID_BIN_SCATTER, KID_SYNC_PACK, KID_COUNT_
+  KID_SELFBLAME_SLOW, KID_BLAME_FILL, KID_BLAME_TOTAL, KID_LINES, KID_SLICE, KID_REACH_WARP, KID_RUN_HEADS, KID_BIN_HIST, KID_BIN_PLAN, KID_BIN_SCATTER, KID_SYNC_PACK, KID_SYNC_WARP, KID_COUNT_
 };
 const char* const kKernelNames[] = {
   "bin_samples", "bin_finalize", "unit_counts", "scan", "block_walk", "reach_fast",
   "reach_slow", "link_count", "link_fill", "segsort_unique", "link_emit", "sync_trace",
   "sync_trace_slow", "key_hist", "key_scatter", "sync_emit", "edge_totals", "prune_edges",
   "prune_slow", "compact", "seg_bounds", "sync_hist", "sync_fill", "blame_count",
-  "selfblame_slow", "blame_fill", "blame_total", "lines", "slice", "reach_warp", "run_heads", "bin_hist", "bin_plan", "bin_scatter", "sync_pack",
+  "selfblame_slow", "blame_fill", "blame_total", "lines", "slice", "reach_warp", "run_heads", "bin_hist", "bin_plan", "bin_scatter", "sync_pack", "sync_warp",
 };
 
 struct TraceScope {
@@ -151,6 +151,7 @@ void set_smem_attributes() {
   cudaFuncSetAttribute(k_reach_fast, cudaFuncAttributeMaxDynamicSharedMemorySize, kT1Threads * kT1Hash * 4);
   cudaFuncSetAttribute(k_bin_count, cudaFuncAttributeMaxDynamicSharedMemorySize, kBinRMax * 8 * 4);
   cudaFuncSetAttribute(k_block_walk, cudaFuncAttributeMaxDynamicSharedMemorySize, 96 * 1024);
+  cudaFuncSetAttribute(k_sync_wc_warp, cudaFuncAttributeMaxDynamicSharedMemorySize, 4 * kWcSmemInts * 4);
   done = true;
 }
 
@@ -189,7 +190,7 @@ int build_graph_impl(const LeoKernel* kk, const LeoCaps* caps, LeoEdges* out, Le
   int32_t *ucnt, *dcnt, *use_ptr, *def_ptr, *ev_res, *q_block, *q_unit, *q_list, *q_off, *q_len, *qres;
   int32_t *ctr, *slow_list, *slow2, *slow3, *cand_cnt, *cand_off, *uniq, *eoff, *ldtab, *scan_tmp, *gtab = nullptr;
   int4* brec;
-  int32_t *pcnt, *poff, *pcur, *puniq, *puoff, *reach_scr, *scan_tmp2, *wlist;
+  int32_t *pcnt, *poff, *pcur, *puniq, *puoff, *reach_scr, *scan_tmp2, *wlist, *wclist;
   uint64_t *cand, *skeys, *ssorted;
   uint32_t* wcword;
   uint8_t* setword;
@@ -205,7 +206,7 @@ int build_graph_impl(const LeoKernel* kk, const LeoCaps* caps, LeoEdges* out, Le
   ar.want(&scan_tmp, scan_scratch_ints(std::max<int64_t>(std::max<int64_t>(N, cap_cand), 1)) + 64);
   ar.want(&reach_scr, (int64_t)RW * 3 * (B + 1));
   ar.want(&scan_tmp2, scan_scratch_ints(std::max<int64_t>(N, 1)) + 64);
-  ar.want(&wlist, N);
+  ar.want(&wlist, N); ar.want(&wclist, cap_slow);
   ar.want(&sync_scr, (int64_t)SW * sync_slow_bytes_per_worker(B));
   const int n_ids = k.dialect == LEO_INTEL ? 32 : 8;
   ar.want(&wcword, N); ar.want(&setword, N); ar.want(&lastset, (int64_t)B * n_ids);
@@ -234,8 +235,11 @@ int build_graph_impl(const LeoKernel* kk, const LeoCaps* caps, LeoEdges* out, Le
       TRACED(KID_SYNC_PACK, k_block_setters<<<grid_for(B, T), T, 0, st>>>(k, setword, n_ids, lastset));
     TRACED(KID_SYNC_PACK, k_wait_list<<<grid_for(N, T), T, 0, st>>>(k, own, wlist, &ctr[8]));
     SyncArgs sa{caps ? caps->debug_flags : 0, skeys, cap_sync, &ctr[3], slow2, &ctr[4], cap_slow, *diags, status,
-                wcword, setword, lastset, n_ids, wlist, &ctr[8]};
+                wcword, setword, lastset, n_ids, wlist, &ctr[8], wclist, &ctr[10]};
     TRACED(KID_SYNC, k_sync<false><<<grid_for(N, 64), 64, 0, st>>>(k, sa, nullptr, 0));
+    if (k.dialect == LEO_AMD)
+      TRACED(KID_SYNC_WARP, k_sync_wc_warp<<<num_sms() * 2, 128, 4 * kWcSmemInts * 4, st>>>(
+          k, sa, wclist, &ctr[10], cap_slow, slow2, &ctr[4]));
     TRACED(KID_SYNC_SLOW, k_sync<true><<<1, SW, 0, st>>>(k, sa, sync_scr, SW));
     TRACED(KID_KEY_HIST, k_key_hist<<<grid_for(cap_sync, T), T, 0, st>>>(skeys, &ctr[3], cap_sync, pcnt));
     TRACED(KID_SCAN, scan_exclusive(pcnt, poff, nullptr, N, scan_tmp2, nullptr, st));
@@ -438,10 +442,9 @@ static int bin_impl(const LeoSamples* s, int32_t n_instr, int32_t* lat, int32_t*
     const int smem = R * 8 * 4;
     const int slice = (int)std::min<int64_t>(65536, std::max<int64_t>(4096, S / (num_sms() * 3)));
     TRACED(KID_BIN_HIST, k_bin_hist<<<G, 512, nb * 4, st>>>(S, s->pc, n_instr, nb, R, M, status));
-    TRACED(KID_BIN_PLAN, k_bin_totals<<<grid_for(nb, 128), 128, 0, st>>>(nb, G, M, btot));
+    TRACED(KID_BIN_PLAN, k_bin_colscan<<<std::min(nb, num_sms() * 4), 256, 0, st>>>(nb, G, M, btot));
     TRACED(KID_BIN_PLAN, k_bin_plan<<<1, 1024, 0, st>>>(nb, slice, btot, boff, soff));
-    TRACED(KID_BIN_PLAN, k_bin_bases<<<grid_for(nb, 128), 128, 0, st>>>(nb, G, boff, M));
-    TRACED(KID_BIN_SCATTER, k_bin_scatter<<<G, 512, nb * 4, st>>>(S, s->pc, s->cat, s->cat_to_cs, n_instr, nb, R, M, keys));
+    TRACED(KID_BIN_SCATTER, k_bin_scatter<<<G, 512, nb * 4, st>>>(S, s->pc, s->cat, s->cat_to_cs, n_instr, nb, R, M, boff, keys));
     TRACED(KID_BIN, k_bin_count<<<num_sms() * 3, 512, smem, st>>>(n_instr, nb, R, slice, boff, soff, keys, cls_cnt));
   } else if (S > 0) {
     TRACED(KID_BIN, k_bin_samples<<<grid_for(S / 4 + 1, 256, num_sms() * 8), 256, 0, st>>>(

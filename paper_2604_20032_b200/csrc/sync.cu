@@ -45,6 +45,8 @@ struct SyncArgs {
   int32_t n_ids;             // 8 (nvidia, ids 1..6) or 32 (intel)
   const int32_t* wait_list;  // compact waiting instructions
   const int32_t* wait_count;
+  int32_t* wc_list;          // waitcnt items for the warp tier
+  int32_t* wc_count;
 };
 
 __global__ void k_sync_pack(KView k, uint32_t* __restrict__ wcword, uint8_t* __restrict__ setword) {
@@ -156,8 +158,11 @@ LEO_DEV bool on_path(const Frame* fr, int top, int blk) {
 
 // Enumerate all chains of one (wait, counter).  Returns false on frame
 // overflow (re-run with a bigger frame stack) or an unpackable counter value.
+constexpr int kT1ChainSteps = 48;   // block scans before a waitcnt item moves to the warp tier
+
 LEO_DEV bool trace_waitcnt_one(const KView& k, int wait, int counter, int level, const SyncArgs& sa,
                                Frame* fr, int fcap, int& best_m) {
+  int steps = 0;
   WcState s;
   s.counter = counter; s.level = level; s.wait = wait;
   s.member_bit = counter == 0 ? kWcVm : kWcLgkm;
@@ -183,6 +188,7 @@ LEO_DEV bool trace_waitcnt_one(const KView& k, int wait, int counter, int level,
       if (!on_path(fr, top, c)) { p = c; break; }
     }
     if (p < 0) { top--; continue; }
+    if (++steps > kT1ChainSteps) return false;
     m = f.m; a = f.a; budget = f.budget;
     r = wc_scan(sa, k.blk_last[p], k.blk_first[p], budget, s, m, a);
     if (r < 0) return false;
@@ -195,6 +201,102 @@ LEO_DEV bool trace_waitcnt_one(const KView& k, int wait, int counter, int level,
     if (!any) { best_m = max(best_m, m); top--; }
   }
   return true;
+}
+
+// ---- tier W: one warp per long waitcnt item ---------------------------------
+// Chains are records in shared memory: (block, m, allowance, budget, parent).
+// A record is a chain that scanned its whole block without stopping and still
+// has unvisited predecessors; its path (the chain's visited set) is the
+// parent walk.  Each round every lane expands one record: for each
+// predecessor not on the record's path it scans that block with the record's
+// state and either ends the chain (stop / no unvisited predecessors: a
+// terminal, folded into best_m) or appends a child record.  Same chain set as
+// _scan_backward, enumerated breadth-first across lanes.
+constexpr int kWcCap = 768;
+constexpr int kWcSmemInts = 5 * kWcCap + 8;
+
+LEO_DEV bool rec_on_path(const int32_t* blk, const int32_t* par, int r, int b) {
+  for (int x = r; x >= 0; x = par[x]) if (blk[x] == b) return true;
+  return false;
+}
+
+__global__ void k_sync_wc_warp(KView k, SyncArgs a, const int32_t* __restrict__ list, const int32_t* count,
+                               int64_t list_cap, int32_t* slow_list, int32_t* slow_count) {
+  extern __shared__ int32_t smw[];
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, wpc = blockDim.x >> 5;
+  int32_t* blk = smw + (size_t)wid * kWcSmemInts;
+  int32_t* rm = blk + kWcCap;
+  int32_t* ra = rm + kWcCap;
+  int32_t* rb = ra + kWcCap;
+  int32_t* par = rb + kWcCap;
+  int32_t* c = par + kWcCap;     // 0 tail, 1 best_m, 2 ovf
+  const int n = (int)min((int64_t)*count, list_cap);
+  for (int t = blockIdx.x * wpc + wid; t < n; t += gridDim.x * wpc) {
+    const int it = list[t];
+    const int wait = it >> 6, counter = it & 63;
+    const uint32_t lv = counter == 0 ? k.sync_a[wait] : k.sync_b[wait];
+    const int level = (int)lv;
+    WcState s;
+    s.counter = counter; s.level = level; s.wait = wait;
+    s.member_bit = counter == 0 ? kWcVm : kWcLgkm;
+    s.nseen = 0;
+    const int b0 = k.block_of[wait];
+    if (lane == 0) {
+      c[0] = 0; c[1] = 0; c[2] = 0;
+      int m = 0, av = -1, budget = kSyncBudget;
+      int r = wc_scan(a, wait - 1, k.blk_first[b0], budget, s, m, av);
+      if (r < 0) c[2] = 1;
+      else if (r == 0) c[1] = m;
+      else {
+        bool any = false;
+        for (int q = k.pred_ptr[b0]; q < k.pred_ptr[b0 + 1]; q++) if (k.pred[q] != b0) any = true;
+        if (!any) c[1] = m;
+        else { blk[0] = b0; rm[0] = m; ra[0] = av; rb[0] = budget; par[0] = -1; c[0] = 1; }
+      }
+    }
+    __syncwarp();
+    int head = 0;
+    while (true) {
+      const int tail = c[0];
+      if (head >= tail || c[2]) break;
+      for (int r = head + lane; r < tail; r += 32) {
+        const int b = blk[r];
+        for (int q = k.pred_ptr[b]; q < k.pred_ptr[b + 1]; q++) {
+          const int p = k.pred[q];
+          if (rec_on_path(blk, par, r, p)) continue;
+          int m = rm[r], av = ra[r], budget = rb[r];
+          const int res = wc_scan(a, k.blk_last[p], k.blk_first[p], budget, s, m, av);
+          if (res < 0) { c[2] = 1; continue; }
+          if (res == 0) { atomicMax(&c[1], m); continue; }
+          // child chain: terminal unless it has a predecessor off its path (p included)
+          bool any = false;
+          for (int q2 = k.pred_ptr[p]; q2 < k.pred_ptr[p + 1] && !any; q2++) {
+            const int pp = k.pred[q2];
+            if (pp != p && !rec_on_path(blk, par, r, pp)) any = true;
+          }
+          if (!any) { atomicMax(&c[1], m); continue; }
+          const int slot = atomicAdd(&c[0], 1);
+          if (slot >= kWcCap) { c[2] = 1; continue; }
+          blk[slot] = p; rm[slot] = m; ra[slot] = av; rb[slot] = budget; par[slot] = r;
+        }
+      }
+      __syncwarp();
+      head = tail;
+      if (c[0] > kWcCap) c[2] = 1;
+      __syncwarp();
+    }
+    __syncwarp();
+    if (lane == 0) {
+      if (c[2]) {
+        const int s2 = atomicAdd(slow_count, 1);
+        if (s2 < a.slow_cap) slow_list[s2] = it;
+        else atomicOr(a.status, (uint32_t)LEO_ST_SCRATCH_OVERFLOW);
+      } else if (c[1] < level) {
+        diag_push(a.diags, a.status, LEO_DIAG_WAITCNT, wait, counter, level, c[1], counter);
+      }
+    }
+    __syncwarp();
+  }
 }
 
 // ---- exact (unpacked) waitcnt walker for the slow path ----------------------
@@ -427,8 +529,14 @@ __global__ void k_sync(KView k, SyncArgs a, char* scratch, int nworkers) {
                        : (!(a.dbg & LEO_DBG_SYNC_SLOW) && lv < kWcNone &&
                           trace_waitcnt_one(k, i, counter, (int)lv, a, fr, fcap, best_m));
         if (!ok) {
-          int s = atomicAdd(a.slow_count, 1);
-          if (s < a.slow_cap) a.slow_list[s] = (i << 6) | counter;
+          // fast tier: long chain trees go to the warp tier (or the exact
+          // walker for unpackable counter values / when forced); slow tier:
+          // frame overflow cannot recur there (frames = B + 2)
+          const bool to_warp = !SLOW && lv < kWcNone && !(a.dbg & LEO_DBG_SYNC_SLOW);
+          int32_t* lst = to_warp ? a.wc_list : a.slow_list;
+          int32_t* cnt = to_warp ? a.wc_count : a.slow_count;
+          int s = atomicAdd(cnt, 1);
+          if (s < a.slow_cap) lst[s] = (i << 6) | counter;
           else atomicOr(a.status, (uint32_t)LEO_ST_SCRATCH_OVERFLOW);
           continue;
         }
