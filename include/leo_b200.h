@@ -197,7 +197,9 @@ typedef struct LeoTrace {
   int32_t capacity;
   int32_t count;
   int32_t only_kernel;        /* -1: all kernels */
-  int32_t pad;
+  int32_t mode;               /* 0: stages serialised on the caller's stream (per-kernel
+                                 times not inflated by concurrent branches);
+                                 1: keep the fork/join branches (timeline) */
   void**  ev_begin;           /* [capacity] cudaEvent_t */
   void**  ev_end;             /* [capacity] cudaEvent_t */
   int32_t* kernel_id;         /* [capacity] host array */
@@ -220,8 +222,11 @@ typedef struct LeoCaps {
 /* LEO_OPT_ACCUMULATE_LINES: add into line_blame / line_stall instead of
  * zeroing them first (many kernels of one batch share one per-line vector) */
 enum { LEO_OPT_ACCUMULATE_LINES = 1 };
+/* LEO_DBG_NO_SMEM: skip the shared-memory-resident tiers (global-memory tiers only) */
 enum { LEO_DBG_REACH_T2 = 1, LEO_DBG_REACH_T3 = 2, LEO_DBG_SYNC_SLOW = 4, LEO_DBG_PRUNE_SLOW = 8,
-       LEO_DBG_SELF_SLOW = 16 };
+       LEO_DBG_SELF_SLOW = 16, LEO_DBG_NO_SMEM = 32, LEO_DBG_PHASES = 64 };
+/* LEO_DBG_PHASES: the shared-memory tiers record per-CTA clock64 phase
+ * marks, read back with leo_debug_phases (profiling aid) */
 
 /* ---- status word (device) ------------------------------------------------ */
 enum { LEO_ST_EDGE_OVERFLOW = 1, LEO_ST_PATH_OVERFLOW = 2, LEO_ST_DIAG_OVERFLOW = 4,
@@ -231,6 +236,11 @@ enum { LEO_ST_EDGE_OVERFLOW = 1, LEO_ST_PATH_OVERFLOW = 2, LEO_ST_DIAG_OVERFLOW 
 int leo_abi_version(void);
 /* name of traced kernel id (LeoTrace.kernel_id), NULL past the last id */
 const char* leo_kernel_name(int id);
+/* per-CTA phase marks of kernel slot `slot` (0 reach, 1 waitcnt, 2 prune):
+ * out[cta * 8 + phase] = clock64 delta from the CTA's start (LEO_DBG_PHASES) */
+int leo_debug_phases(int32_t slot, int64_t* out, int32_t n_ctas);
+/* per-item clock64 cycles of the shared-memory waitcnt tier (LEO_DBG_PHASES) */
+int leo_debug_items(int64_t* out, int32_t n);
 
 /* stage 0: raw (pc, category) stream -> lat[N], cls_cnt[N*8] (zeroed here). */
 int leo_bin_samples(const LeoSamples* s, int32_t n_instr, int32_t* lat, int32_t* cls_cnt,

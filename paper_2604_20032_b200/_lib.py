@@ -53,6 +53,8 @@ def lib():
                               C.POINTER(abi.LeoDiags), C.POINTER(abi.LeoBlame), P, P, P,
                               C.c_int32, P, P, P, P]
     L.leo_kernel_name.argtypes = [C.c_int]
+    L.leo_debug_phases.argtypes = [C.c_int32, P, C.c_int32]
+    L.leo_debug_phases.restype = C.c_int
     L.leo_kernel_name.restype = C.c_char_p
     L.leo_events_create.argtypes = [C.c_int32, P]
     L.leo_events_elapsed.argtypes = [C.c_int32, P, P, P]

@@ -45,7 +45,7 @@ class LeoConfig(C.Structure):
 
 class LeoTrace(C.Structure):
     _fields_ = [("capacity", C.c_int32), ("count", C.c_int32), ("only_kernel", C.c_int32),
-                ("pad", C.c_int32), ("ev_begin", P), ("ev_end", P), ("kernel_id", P)]
+                ("mode", C.c_int32), ("ev_begin", P), ("ev_end", P), ("kernel_id", P)]
 
 
 class LeoCaps(C.Structure):
@@ -56,7 +56,8 @@ class LeoCaps(C.Structure):
                 ("workspace_needed", C.POINTER(C.c_int64))]
 
 
-DBG_REACH_T2, DBG_REACH_T3, DBG_SYNC_SLOW, DBG_PRUNE_SLOW, DBG_SELF_SLOW = 1, 2, 4, 8, 16
+DBG_REACH_T2, DBG_REACH_T3, DBG_SYNC_SLOW, DBG_PRUNE_SLOW, DBG_SELF_SLOW, DBG_NO_SMEM = 1, 2, 4, 8, 16, 32
+DBG_PHASES = 64
 OPT_ACCUMULATE_LINES = 1
 
 

@@ -390,14 +390,10 @@ __global__ void k_blame(KView k, BlameArgs a) {
       if (self) {
         int sub = dominant_self(a.p, j);
         if (sub == LEO_SB_MEMORY_LATENCY && (kMemoryClasses & BIT(k.opclass[j]))) {
-          int32_t seen[kSeenCap];
-          int r = (a.dbg & LEO_DBG_SELF_SLOW) ? -1
-                  : traces_to_load(k, a.brbeg, a.brend, a.bprod, a.bmeta, j, seen, kSeenCap, nullptr, 0);
-          if (r < 0) {
-            int s = atomicAdd(a.slow_count, 1);
-            if (s < a.slow_cap) a.slow_list[s] = j;
-            else atomicOr(a.status, (uint32_t)LEO_ST_SCRATCH_OVERFLOW);
-          } else if (r) sub = LEO_SB_INDIRECT_ADDRESSING;
+          // _address_traces_to_load runs in k_selfblame_warp (warp per candidate)
+          int s = atomicAdd(a.slow_count, 1);
+          if (s < a.slow_cap) a.slow_list[s] = j;
+          else atomicOr(a.status, (uint32_t)LEO_ST_SCRATCH_OVERFLOW);
         }
         a.self_sub[j] = sub;
         a.ecount[j] = 1;
@@ -446,14 +442,85 @@ __global__ void k_blame(KView k, BlameArgs a) {
 template __global__ void k_blame<0>(KView, BlameArgs);
 template __global__ void k_blame<1>(KView, BlameArgs);
 
-__global__ void k_selfblame_slow(KView k, BlameArgs a, int32_t* scratch, int nworkers) {
-  const int ns = (int)min((int64_t)*a.slow_count, a.slow_cap);
+// _address_traces_to_load (analysis.py:390-411), warp per candidate: the BFS
+// frontier is expanded by all lanes at once (one level per round, <= 8
+// rounds), visited set = open-addressing hash in shared memory.  The answer
+// is whether some MEMORY_PRODUCER other than the stalled instruction is
+// discovered within 8 RAW hops through non-producer intermediates, which is
+// what the reference's sequential BFS returns.  Hash / frontier overflow
+// re-runs the candidate on the global-stamp worker.
+constexpr int kSBHash = 512, kSBFront = 256;
+constexpr int kSBWarpInts = kSBHash + 2 * kSBFront + 8;
+
+__global__ void k_selfblame_warp(KView k, BlameArgs a, int32_t* slow2, int32_t* slow2_count) {
+  extern __shared__ int32_t sbm[];
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, wpc = blockDim.x >> 5;
+  int32_t* hash = sbm + (size_t)wid * kSBWarpInts;
+  int32_t* fa = hash + kSBHash;
+  int32_t* fb = fa + kSBFront;
+  int32_t* c = fb + kSBFront;     // 0 ncur, 1 nnext, 2 found, 3 ovf, 4 nhash
+  const int n = (int)min((int64_t)*a.slow_count, a.slow_cap);
+  for (int t = blockIdx.x * wpc + wid; t < n; t += gridDim.x * wpc) {
+    const int j = a.slow_list[t];
+    for (int x = lane; x < kSBHash; x += 32) hash[x] = -1;
+    __syncwarp();
+    if (lane == 0) {
+      c[0] = 1; c[1] = 0; c[2] = 0; c[3] = (a.dbg & LEO_DBG_SELF_SLOW) ? 1 : 0; c[4] = 1;
+      fa[0] = j;
+      hash[(((uint32_t)j * 2654435761u) >> 23) & (kSBHash - 1)] = j;
+    }
+    __syncwarp();
+    int32_t *cur = fa, *nxt = fb;
+    for (int depth = 0; depth < 8; depth++) {
+      const int ncur = c[0];
+      if (ncur == 0 || c[2] || c[3]) break;
+      for (int x = lane; x < ncur; x += 32) {
+        const int node = cur[x];
+        for (int e = a.brbeg[node]; e < a.brend[node]; e++) {
+          if (((a.bmeta[e] >> 27) & 7) != LEO_EK_RAW) continue;
+          const int p = a.bprod[e];
+          uint32_t h = (((uint32_t)p * 2654435761u) >> 23) & (kSBHash - 1);
+          bool fresh = false;
+          for (int probe = 0; probe < kSBHash; probe++) {
+            const int32_t prev = atomicCAS(&hash[h], -1, p);
+            if (prev == -1) { fresh = true; atomicAdd(&c[4], 1); break; }
+            if (prev == p) break;
+            h = (h + 1) & (kSBHash - 1);
+          }
+          if (!fresh) continue;
+          if (kMemoryProducer & BIT(k.opclass[p])) { c[2] = 1; continue; }
+          const int pos = atomicAdd(&c[1], 1);
+          if (pos < kSBFront) nxt[pos] = p; else c[3] = 1;
+        }
+      }
+      __syncwarp();
+      if (c[4] > kSBHash / 2) c[3] = 1;
+      if (lane == 0) { c[0] = c[1]; c[1] = 0; }
+      __syncwarp();
+      int32_t* tmp = cur; cur = nxt; nxt = tmp;
+    }
+    __syncwarp();
+    if (lane == 0) {
+      if (c[2]) a.self_sub[j] = LEO_SB_INDIRECT_ADDRESSING;
+      else if (c[3]) {
+        const int s2 = atomicAdd(slow2_count, 1);
+        if (s2 < a.slow_cap) slow2[s2] = j;
+        else atomicOr(a.status, (uint32_t)LEO_ST_SCRATCH_OVERFLOW);
+      }
+    }
+    __syncwarp();
+  }
+}
+
+__global__ void k_selfblame_slow(KView k, BlameArgs a, const int32_t* list, const int32_t* count,
+                                 int32_t* scratch, int nworkers) {
+  const int ns = (int)min((int64_t)*count, a.slow_cap);
   const int w = blockIdx.x * blockDim.x + threadIdx.x;
   if (w >= nworkers) return;
   int32_t* stamp = scratch + (size_t)w * 2 * (k.N + 1);
   int32_t* seen = stamp + (k.N + 1);
   for (int t = w; t < ns; t += nworkers) {
-    int j = a.slow_list[t];
+    int j = list[t];
     int r = traces_to_load(k, a.brbeg, a.brend, a.bprod, a.bmeta, j, seen, k.N + 1, stamp, j + 1);
     if (r > 0) a.self_sub[j] = LEO_SB_INDIRECT_ADDRESSING;
   }

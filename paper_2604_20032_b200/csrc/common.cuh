@@ -97,7 +97,27 @@ struct PySum {
   }
 };
 
+// ---- profiling aid: per-CTA phase marks (LEO_DBG_PHASES) ----------------------
+__device__ long long g_phase_ts[4][1024][8];
+__device__ long long g_item_cycles[8192];      // per-item cycles of the waitcnt tier
+struct PhaseMarks {
+  int on; long long t0;
+  LEO_DEV PhaseMarks(int dbg) {
+#ifdef __CUDA_ARCH__
+    on = (dbg & LEO_DBG_PHASES) && blockIdx.x < 1024;
+    t0 = clock64();
+#endif
+  }
+  LEO_DEV void mark(int slot, int ph) const {
+#ifdef __CUDA_ARCH__
+    if (on && threadIdx.x == 0) g_phase_ts[slot][blockIdx.x][ph] = clock64() - t0;
+#endif
+  }
+};
+
 // ---- launch helpers ---------------------------------------------------------
+// dynamic shared memory a shared-memory-resident tier may request per CTA
+constexpr int kSmemResidentMax = 200 * 1024;
 inline int grid_for(int64_t n, int threads, int max_blocks = 148 * 32) {
   int64_t g = (n + threads - 1) / threads;
   if (g < 1) g = 1;

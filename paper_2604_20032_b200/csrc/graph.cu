@@ -22,6 +22,7 @@
 //   G5 segsort_unique  per consumer: reference sort order + dedup on the full key
 //   G6 k_link_emit     edges in (consumer, producer, kind, class, index, span) order
 #include "prims.cuh"
+#include "stage.cuh"
 
 namespace leo {
 
@@ -58,7 +59,9 @@ struct WalkArgs {
   int32_t* q_unit;           // [use units]
   int32_t* q_list;           // [use units]
   int32_t* q_count;          // scalar
-  int32_t* ldtab;            // [B * U] last def of unit u in block b, -1 if none
+  int32_t* ldtab;            // [U * Bp] column-major: last def of unit u in block b, -1 if none
+  int32_t* qtab;             // [U * Bp] column-major: query slot of (b, u), -1 if none
+  int32_t Bp;                // column stride (B rounded up to 4: 16-byte aligned columns)
   int32_t* gtab;             // global per-warp tables (when U too large for smem) or null
 };
 
@@ -122,11 +125,12 @@ __global__ void k_block_walk(KView k, WalkArgs a, int warps_per_cta) {
       }
       __syncwarp();
     }
-    // dense row of the block's last definitions (block_defs depgraph.py:143-149)
-    int32_t* row = a.ldtab + (size_t)b * U;
+    // the block's last definitions (block_defs depgraph.py:143-149) and its
+    // upward-exposed queries, one entry per unit column
     for (int u = lane; u < U; u += 32) {
-      int ld = last[u];
-      row[u] = ld >= first ? ld : -1;
+      const int ld = last[u], qs = qtab[u];
+      a.ldtab[(size_t)u * a.Bp + b] = ld >= first ? ld : -1;
+      a.qtab[(size_t)u * a.Bp + b] = qs >= ev_block ? qs : -1;
     }
     __syncwarp();
   }
@@ -141,7 +145,7 @@ __global__ void k_block_walk(KView k, WalkArgs a, int warps_per_cta) {
 // Block record (one 16-byte load per search step):
 //   rec[y] = {h = runhead(y), np = |preds(h)|, p0, p1}
 //   np <= 2: p0/p1 are the predecessors of h; np > 2: p0 = pred_ptr[h].
-__global__ void k_block_records(KView k, int4* __restrict__ rec) {
+__global__ void k_block_records(KView k, int4* __restrict__ rec, int32_t* __restrict__ rh) {
   for (int b = blockIdx.x * blockDim.x + threadIdx.x; b < k.B; b += gridDim.x * blockDim.x) {
     int x = b;
     while (x > 0 && k.pred_ptr[x + 1] - k.pred_ptr[x] == 1 && k.pred[k.pred_ptr[x]] == x - 1) x--;
@@ -151,14 +155,16 @@ __global__ void k_block_records(KView k, int4* __restrict__ rec) {
     if (np <= 2) { r.z = np > 0 ? k.pred[q0] : -1; r.w = np > 1 ? k.pred[q0 + 1] : -1; }
     else { r.z = q0; r.w = -1; }
     rec[b] = r;
+    rh[b] = x;
   }
 }
 
 struct ReachArgs {
   int32_t dbg;               // LEO_DBG_* routing (testing)
-  const int32_t* ldtab;      // [B * U]
+  const int32_t* ldtab;      // [U * Bp] column-major
   const int4* rec;           // [B]
   int32_t U;
+  int32_t Bp;
   const int32_t* q_block;
   const int32_t* q_unit;
   int32_t* q_off;            // [use units] result offset per query slot
@@ -175,12 +181,12 @@ struct ReachArgs {
 // Entering block y backward: the nearest definition of u in y, y-1, ...,
 // runhead(y) (loads issued four at a time), or -1.
 LEO_DEV int run_lookup(const ReachArgs& a, int y, int h, int u) {
-  const size_t U = (size_t)a.U;
+  const int32_t* col = a.ldtab + (size_t)u * a.Bp;
   for (int x = y; x >= h; x -= 4) {
-    int v0 = a.ldtab[(size_t)x * U + u];
-    int v1 = x - 1 >= h ? a.ldtab[(size_t)(x - 1) * U + u] : -1;
-    int v2 = x - 2 >= h ? a.ldtab[(size_t)(x - 2) * U + u] : -1;
-    int v3 = x - 3 >= h ? a.ldtab[(size_t)(x - 3) * U + u] : -1;
+    int v0 = col[x];
+    int v1 = x - 1 >= h ? col[x - 1] : -1;
+    int v2 = x - 2 >= h ? col[x - 2] : -1;
+    int v3 = x - 3 >= h ? col[x - 3] : -1;
     if (v0 >= 0) return v0;
     if (v1 >= 0) return v1;
     if (v2 >= 0) return v2;
@@ -259,6 +265,160 @@ LEO_DEV void reach_commit(const ReachArgs& a, int e, const int32_t* res, int nre
   a.q_len[e] = nres;
 }
 
+// Tier 0 (shared-memory resident): one CTA per register unit.  The CTA stages
+// the unit's last-def and query columns plus the block -> run-head map and the
+// predecessor CSR with TMA bulk copies, turns the last-def column into
+// near[y] = nearest def of u in [runhead(y), y] (or -(runhead + 1) when that
+// stretch of the run is transparent), and resolves every (b, u) query of the
+// unit by a thread-private DFS whose visited set is a bitmap over blocks in
+// shared memory.  Every search step is a shared-memory access.  Queries whose
+// stack or result list overflows go to tier 2.
+constexpr int kRUStack = 32, kRURes = 32;
+
+__host__ __device__ inline size_t reach_unit_smem(int B, int threads) {
+  const size_t Bp = (size_t)((B + 3) & ~3);
+  const size_t W = (size_t)((B + 31) >> 5);
+  return 16 + carve_bytes(Bp, 4) * 4                                    // rh, cell, qs, qlist
+         + carve_bytes(B + 1, 4) + carve_bytes(2 * (size_t)B + 4, 4)    // pred_ptr, pred (<= 2 per block)
+         + carve_bytes(W * threads, 4)                                  // visited bitmaps
+         + carve_bytes((size_t)kRUStack * threads, 4) + carve_bytes((size_t)kRURes * threads, 4);
+}
+
+__global__ void k_reach_unit(KView k, ReachArgs a, const int32_t* __restrict__ qtab,
+                             const int32_t* __restrict__ rh_g) {
+  extern __shared__ __align__(16) unsigned char sm_raw[];
+  __shared__ int nq, rbase;
+  __shared__ int swarp[33];
+  __shared__ long long wmax[32];
+  const int B = k.B, Bp = a.Bp, W = (B + 31) >> 5, T = blockDim.x, tid = threadIdx.x;
+  SmemCarve cv{sm_raw};
+  uint64_t* bar = cv.take<uint64_t>(2);
+  int32_t* rh = cv.take<int32_t>(Bp);
+  int32_t* cell = cv.take<int32_t>(Bp);
+  int32_t* qs = cv.take<int32_t>(Bp);
+  int32_t* ql = cv.take<int32_t>(Bp);
+  int32_t* pptr = cv.take<int32_t>(B + 1);
+  int32_t* pred = cv.take<int32_t>(2 * (size_t)B + 4);
+  uint32_t* vis = cv.take<uint32_t>((size_t)W * T);
+  int32_t* stk = cv.take<int32_t>((size_t)kRUStack * T);
+  int32_t* res = cv.take<int32_t>((size_t)kRURes * T);
+  PhaseMarks pm(a.dbg);
+  StageBar sb;
+  sb.init(bar);
+  bool first = true;
+  for (int u = blockIdx.x; u < k.U; u += gridDim.x) {
+    sb.begin();
+    if (first) {
+      const int E = k.pred_ptr[B];          // <= 2 per block ([target, fallthrough])
+      sb.copy(rh, rh_g, (size_t)B * 4);
+      sb.copy(pptr, k.pred_ptr, (size_t)(B + 1) * 4);
+      sb.copy(pred, k.pred, (size_t)E * 4);
+      first = false;
+    }
+    sb.copy(cell, a.ldtab + (size_t)u * Bp, (size_t)B * 4);
+    sb.copy(qs, qtab + (size_t)u * Bp, (size_t)B * 4);
+    if (tid == 0) nq = 0;
+    sb.commit_and_wait();
+    pm.mark(0, 1);
+    // near[y] = last def of u in [runhead(y), y]: an inclusive max-scan of
+    // key(x) = runhead(x) << 32 | (def(x) + 1).  Run heads never decrease, so
+    // the running max carries y's own run head and the latest def inside the
+    // run.  Thread-contiguous chunks, shuffle scan of chunk maxima.
+    {
+      const int per = (B + T - 1) / T, lo = tid * per, hi = min(B, lo + per);
+      long long run = -1;
+      for (int y = lo; y < hi; y++) run = max(run, ((long long)rh[y] << 32) | (long long)(cell[y] + 1));
+      long long inc = run;
+      for (int o = 1; o < 32; o <<= 1) {
+        const long long v = __shfl_up_sync(0xffffffffu, inc, o);
+        if ((tid & 31) >= o) inc = max(inc, v);
+      }
+      if ((tid & 31) == 31) wmax[tid >> 5] = inc;
+      __syncthreads();
+      long long carry = -1;
+      for (int w = 0; w < (tid >> 5); w++) carry = max(carry, wmax[w]);
+      const long long prev = __shfl_up_sync(0xffffffffu, inc, 1);
+      if ((tid & 31) > 0) carry = max(carry, prev);
+      for (int y = lo; y < hi; y++) {
+        carry = max(carry, ((long long)rh[y] << 32) | (long long)(cell[y] + 1));
+        const int d = (int)(carry & 0xffffffffLL) - 1;
+        cell[y] = ((int)(carry >> 32) == rh[y] && d >= 0) ? d : -(rh[y] + 1);
+      }
+    }
+    __syncthreads();
+    pm.mark(0, 2);
+    for (int y = tid; y < B; y += T)
+      if (qs[y] >= 0) ql[atomicAdd(&nq, 1)] = y;
+    __syncthreads();
+    pm.mark(0, 3);
+    const int n = nq;
+    // rounds of T queries; one global reservation per CTA per round
+    for (int base = 0; base < n; base += T) {
+      const int t = base + tid;
+      int e = -1, nres = 0;
+      bool ovf = false;
+      if (t < n) {
+        const int b = ql[t];
+        e = qs[b];
+        ovf = (a.dbg & (LEO_DBG_REACH_T2 | LEO_DBG_REACH_T3)) != 0;
+        int sp = 0;
+        if (!ovf) {
+          for (int w = 0; w < W; w++) vis[w * T + tid] = 0u;
+          // Entering block p backward either ends at its nearest def (a result)
+          // or crosses the transparent stretch to run head h, whose expansion is
+          // shared by every entry of the run: the bitmap marks result blocks
+          // (cell >= 0) and expanded heads (cell < 0), which are disjoint.
+          auto visit = [&](int p) {
+            const int c = cell[p];
+            const int key = c >= 0 ? p : -c - 1;
+            uint32_t* word = &vis[(key >> 5) * T + tid];
+            const uint32_t m = 1u << (key & 31);
+            if (*word & m) return;
+            *word |= m;
+            if (c >= 0) {
+              if (nres == kRURes) ovf = true;
+              else res[(nres++) * T + tid] = c;
+            } else if (sp == kRUStack) {
+              ovf = true;
+            } else {
+              stk[(sp++) * T + tid] = key;
+            }
+          };
+          for (int q = pptr[b]; q < pptr[b + 1]; q++) visit(pred[q]);
+          while (sp > 0 && !ovf) {
+            const int h = stk[(--sp) * T + tid];
+            for (int q = pptr[h]; q < pptr[h + 1]; q++) visit(pred[q]);
+          }
+        }
+        if (ovf) {                                 // tier 2 re-runs the query
+          const int s2 = atomicAdd(a.slow_count, 1);
+          if (s2 < a.slow_cap) a.slow_list[s2] = e;
+          else { a.q_off[e] = 0; a.q_len[e] = 0; atomicOr(a.status, (uint32_t)LEO_ST_SCRATCH_OVERFLOW); }
+        }
+      }
+      const int cnt = (t < n && !ovf) ? nres : 0;
+      int tot;
+      const int ex = block_excl_scan(cnt, swarp, &tot);
+      if (tid == 0) rbase = tot > 0 ? atomicAdd(a.qres_count, tot) : 0;
+      __syncthreads();
+      if (t < n && !ovf) {
+        const int off = rbase + ex;
+        if ((int64_t)off + nres > a.qres_cap) {
+          atomicOr(a.status, (uint32_t)LEO_ST_SCRATCH_OVERFLOW);
+          a.q_off[e] = 0; a.q_len[e] = 0;
+        } else {
+          for (int x = 0; x < nres; x++) a.qres[off + x] = res[x * T + tid];
+          a.q_off[e] = off;
+          a.q_len[e] = nres;
+        }
+      }
+      __syncthreads();
+    }
+    __syncthreads();
+    pm.mark(0, 4);
+  }
+}
+
 // Tier 1: lockstep per-lane state machine.  Every lane owns one query at a
 // time and advances it by one search step per loop iteration; a lane whose
 // query finished fetches the next from a shared queue (warp-aggregated
@@ -334,7 +494,7 @@ __global__ void __launch_bounds__(kT1Threads) k_reach_fast(KView k, ReachArgs a,
     if (e >= 0) {
       if (!ovf && sp > 0) {                        // one search step
         const int y = stk[--sp];
-        const int own = a.ldtab[(size_t)y * a.U + u];  // issued together with the record load
+        const int own = a.ldtab[(size_t)u * a.Bp + y];  // issued together with the record load
         const int4 r = a.rec[y];
         const int ld = own >= 0 ? own : (r.x < y ? run_lookup(a, y - 1, r.x, u) : -1);
         if (ld >= 0) {

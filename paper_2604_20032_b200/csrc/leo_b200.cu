@@ -152,6 +152,10 @@ void set_smem_attributes() {
   cudaFuncSetAttribute(k_bin_count, cudaFuncAttributeMaxDynamicSharedMemorySize, kBinRMax * 8 * 4);
   cudaFuncSetAttribute(k_block_walk, cudaFuncAttributeMaxDynamicSharedMemorySize, 96 * 1024);
   cudaFuncSetAttribute(k_sync_wc_warp, cudaFuncAttributeMaxDynamicSharedMemorySize, 4 * kWcSmemInts * 4);
+  cudaFuncSetAttribute(k_reach_unit, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemResidentMax);
+  cudaFuncSetAttribute(k_sync_wc_smem, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemResidentMax);
+  cudaFuncSetAttribute(k_prune_edges_smem<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemResidentMax);
+  cudaFuncSetAttribute(k_prune_edges_smem<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemResidentMax);
   done = true;
 }
 
@@ -190,9 +194,9 @@ int build_graph_impl(const LeoKernel* kk, const LeoCaps* caps, LeoEdges* out, Le
   int32_t *ucnt, *dcnt, *use_ptr, *def_ptr, *ev_res, *q_block, *q_unit, *q_list, *q_off, *q_len, *qres;
   int32_t *ctr, *slow_list, *slow2, *slow3, *cand_cnt, *cand_off, *uniq, *eoff, *ldtab, *scan_tmp, *gtab = nullptr;
   int4* brec;
-  int32_t *pcnt, *poff, *pcur, *puniq, *puoff, *reach_scr, *scan_tmp2, *wlist, *wclist;
+  int32_t *pcnt, *poff, *pcur, *puniq, *puoff, *reach_scr, *scan_tmp2, *wlist, *wclist, *qtab, *rhead;
   uint64_t *cand, *skeys, *ssorted;
-  uint32_t* wcword;
+  uint32_t *wcword, *bev;
   uint8_t* setword;
   int32_t* lastset;
   char* sync_scr;
@@ -200,7 +204,9 @@ int build_graph_impl(const LeoKernel* kk, const LeoCaps* caps, LeoEdges* out, Le
   ar.want(&ev_res, NU); ar.want(&q_block, NU); ar.want(&q_unit, NU); ar.want(&q_list, NU);
   ar.want(&q_off, NU); ar.want(&q_len, NU); ar.want(&qres, cap_qres); ar.want(&ctr, 16);
   ar.want(&slow_list, NU + 1024); ar.want(&slow2, cap_slow); ar.want(&slow3, NU + 1024); ar.want(&cand_cnt, N); ar.want(&cand_off, N + 1);
-  ar.want(&uniq, N); ar.want(&eoff, N + 1); ar.want(&ldtab, (int64_t)B * U); ar.want(&brec, B);
+  const int Bp = (B + 3) & ~3;   // 16-byte aligned unit columns
+  ar.want(&uniq, N); ar.want(&eoff, N + 1); ar.want(&ldtab, (int64_t)Bp * U); ar.want(&qtab, (int64_t)Bp * U);
+  ar.want(&brec, B); ar.want(&rhead, B);
   ar.want(&cand, cap_cand); ar.want(&skeys, cap_sync); ar.want(&ssorted, cap_sync);
   ar.want(&pcnt, N); ar.want(&poff, N + 1); ar.want(&pcur, N); ar.want(&puniq, N); ar.want(&puoff, N + 1);
   ar.want(&scan_tmp, scan_scratch_ints(std::max<int64_t>(std::max<int64_t>(N, cap_cand), 1)) + 64);
@@ -209,7 +215,7 @@ int build_graph_impl(const LeoKernel* kk, const LeoCaps* caps, LeoEdges* out, Le
   ar.want(&wlist, N); ar.want(&wclist, cap_slow);
   ar.want(&sync_scr, (int64_t)SW * sync_slow_bytes_per_worker(B));
   const int n_ids = k.dialect == LEO_INTEL ? 32 : 8;
-  ar.want(&wcword, N); ar.want(&setword, N); ar.want(&lastset, (int64_t)B * n_ids);
+  ar.want(&wcword, N); ar.want(&bev, B); ar.want(&setword, N); ar.want(&lastset, (int64_t)B * n_ids);
   if (!smem_tab) ar.want(&gtab, (int64_t)walk_warps * 2 * U);
   LEO_CUDA_CHECK(ar.commit());
   // counters: 0 q_count, 1 qres_count, 2 reach slow, 3 sync keys, 4 sync slow, 5 n_regular, 6 n_sync
@@ -221,7 +227,7 @@ int build_graph_impl(const LeoKernel* kk, const LeoCaps* caps, LeoEdges* out, Le
   SidePool& sp = side_pool();
   // traced runs stay on one stream so per-kernel event times are not
   // inflated by queueing behind concurrent branches
-  const bool fork = tr == nullptr;
+  const bool fork = tr == nullptr || (tr->mode & 1);
   cudaStream_t s_sync = fork ? sp.s[0] : st;
   if (fork) link_streams(st, s_sync, sp.e[0]);
   const int kind = k.dialect == LEO_AMD ? LEO_EK_MEM_WAITCNT : k.dialect == LEO_NVIDIA ? LEO_EK_MEM_BARRIER : LEO_EK_MEM_SWSB;
@@ -230,13 +236,19 @@ int build_graph_impl(const LeoKernel* kk, const LeoCaps* caps, LeoEdges* out, Le
     cudaMemsetAsync(pcnt, 0, (size_t)std::max(N, 1) * 4, st);
     cudaMemsetAsync(pcur, 0, (size_t)std::max(N, 1) * 4, st);
     cudaMemsetAsync(sync_scr, 0, (size_t)SW * sync_slow_bytes_per_worker(B), st);
-    TRACED(KID_SYNC_PACK, k_sync_pack<<<grid_for(N, T), T, 0, st>>>(k, wcword, setword));
+    cudaMemsetAsync(bev, 0, (size_t)std::max(B, 1) * 4, st);
+    TRACED(KID_SYNC_PACK, k_sync_pack<<<grid_for(N, T), T, 0, st>>>(k, wcword, setword, bev));
     if (k.dialect != LEO_AMD && B > 0)
       TRACED(KID_SYNC_PACK, k_block_setters<<<grid_for(B, T), T, 0, st>>>(k, setword, n_ids, lastset));
     TRACED(KID_SYNC_PACK, k_wait_list<<<grid_for(N, T), T, 0, st>>>(k, own, wlist, &ctr[8]));
     SyncArgs sa{caps ? caps->debug_flags : 0, skeys, cap_sync, &ctr[3], slow2, &ctr[4], cap_slow, *diags, status,
                 wcword, setword, lastset, n_ids, wlist, &ctr[8], wclist, &ctr[10]};
-    TRACED(KID_SYNC, k_sync<false><<<grid_for(N, 64), 64, 0, st>>>(k, sa, nullptr, 0));
+    const size_t wc_smem = sync_smem_bytes(N, B, 128);
+    const int dbg_flags = caps ? caps->debug_flags : 0;
+    if (k.dialect == LEO_AMD && B > 0 && wc_smem <= (size_t)kSmemResidentMax && !(dbg_flags & LEO_DBG_NO_SMEM))
+      TRACED(KID_SYNC, k_sync_wc_smem<<<SM, 128, wc_smem, st>>>(k, sa, bev));
+    else
+      TRACED(KID_SYNC, k_sync<false><<<grid_for(N, 64), 64, 0, st>>>(k, sa, nullptr, 0));
     if (k.dialect == LEO_AMD)
       TRACED(KID_SYNC_WARP, k_sync_wc_warp<<<num_sms() * 2, 128, 4 * kWcSmemInts * 4, st>>>(
           k, sa, wclist, &ctr[10], cap_slow, slow2, &ctr[4]));
@@ -251,16 +263,24 @@ int build_graph_impl(const LeoKernel* kk, const LeoCaps* caps, LeoEdges* out, Le
   TRACED(KID_SCAN, scan_exclusive(ucnt, use_ptr, nullptr, N, scan_tmp, nullptr, st));
   TRACED(KID_SCAN, scan_exclusive(dcnt, def_ptr, nullptr, N, scan_tmp, nullptr, st));
 
-  WalkArgs wa{use_ptr, def_ptr, ev_res, q_block, q_unit, q_list, &ctr[0], ldtab, gtab};
+  WalkArgs wa{use_ptr, def_ptr, ev_res, q_block, q_unit, q_list, &ctr[0], ldtab, qtab, Bp, gtab};
   size_t smem = smem_tab ? (size_t)wpc * 2 * U * 4 : 0;
   if (B > 0) TRACED(KID_BLOCK_WALK, k_block_walk<<<std::max(1, walk_ctas), wpc * 32, smem, st>>>(k, wa, wpc));
 
-  if (B > 0) TRACED(KID_RUN_HEADS, k_block_records<<<grid_for(B, T), T, 0, st>>>(k, brec));
-  ReachArgs ra{caps ? caps->debug_flags : 0, ldtab, brec, U, q_block, q_unit, q_off, q_len, qres, cap_qres, &ctr[1],
+  if (B > 0) TRACED(KID_RUN_HEADS, k_block_records<<<grid_for(B, T), T, 0, st>>>(k, brec, rhead));
+  ReachArgs ra{caps ? caps->debug_flags : 0, ldtab, brec, U, Bp, q_block, q_unit, q_off, q_len, qres, cap_qres, &ctr[1],
                slow_list, &ctr[2], NU + 1024, status};
-  // tier 1 is persistent: enough CTAs to fill the chip, queries fetched dynamically
-  TRACED(KID_REACH_FAST, k_reach_fast<<<std::max(1, std::min<int>(grid_for(NU, kT1Threads), SM * 3)), kT1Threads,
-                                        kT1Threads * kT1Hash * 4, st>>>(k, ra, q_list, &ctr[0], &ctr[9]));
+  const int dbg = caps ? caps->debug_flags : 0;
+  const int ru_threads = 128;
+  const size_t ru_smem = reach_unit_smem(B, ru_threads);
+  if (B > 0 && U > 0 && ru_smem <= (size_t)kSmemResidentMax && !(dbg & LEO_DBG_NO_SMEM)) {
+    // tier 0: the CFG and one unit's columns resident in shared memory, CTA per unit
+    TRACED(KID_REACH_FAST, k_reach_unit<<<std::min(U, SM * 8), ru_threads, ru_smem, st>>>(k, ra, qtab, rhead));
+  } else {
+    // tier 1 is persistent: enough CTAs to fill the chip, queries fetched dynamically
+    TRACED(KID_REACH_FAST, k_reach_fast<<<std::max(1, std::min<int>(grid_for(NU, kT1Threads), SM * 3)), kT1Threads,
+                                          kT1Threads * kT1Hash * 4, st>>>(k, ra, q_list, &ctr[0], &ctr[9]));
+  }
   {
     const int wpc_r = 4;
     const size_t sm_r = (size_t)wpc_r * kWarpSmemInts * 4;
@@ -310,7 +330,16 @@ int prune_impl(const LeoKernel* kk, const LeoProfile* pp, const LeoConfig* cfg, 
   cudaMemsetAsync(paths->count, 0, sizeof(int32_t), st);
   PruneArgs a{caps ? caps->debug_flags : 0, *cfg, in->prod, in->cons, in->meta, in->count, (int32_t)cap_in, keep, npaths, pfirst, dist,
               *paths, slow_list, &ctr[0], cap_slow, *diags, status};
-  TRACED(KID_PRUNE, k_prune_edges<<<grid_for(cap_in, 128, num_sms() * 16), 128, 0, st>>>(k, p, a));
+  {
+    const int dbg = caps ? caps->debug_flags : 0;
+    const size_t staged = prune_smem_bytes(k.N, k.B, 128, true), unstaged = prune_smem_bytes(k.N, k.B, 128, false);
+    if (dbg & LEO_DBG_NO_SMEM)
+      TRACED(KID_PRUNE, k_prune_edges<<<grid_for(cap_in, 128, num_sms() * 16), 128, 0, st>>>(k, p, a));
+    else if (staged <= (size_t)kSmemResidentMax)
+      TRACED(KID_PRUNE, k_prune_edges_smem<true><<<num_sms(), 128, staged, st>>>(k, p, a));
+    else
+      TRACED(KID_PRUNE, k_prune_edges_smem<false><<<num_sms() * 2, 128, unstaged, st>>>(k, p, a));
+  }
   TRACED(KID_PRUNE_SLOW, k_prune_slow<<<1, PW, 0, st>>>(k, p, a, slow_scr, PW));
   TRACED(KID_SCAN, scan_exclusive(keep, pos, in->count, cap_in, scan_tmp, nullptr, st));
   TRACED(KID_COMPACT, k_compact<<<grid_for(cap_in, 256), 256, 0, st>>>(a, pos, in->n_regular, *out, status));
@@ -381,10 +410,11 @@ int blame_impl(const LeoKernel* kk, const LeoProfile* pp, const LeoEdges* pruned
   const int BW = 64;
   Arena ar{st};
   IncomingBufs bb;
-  int32_t *ecount, *self_sub, *eoff, *slow_list, *ctr, *scan_tmp, *slow_scr;
+  int32_t *ecount, *self_sub, *eoff, *slow_list, *slow2, *ctr, *scan_tmp, *slow_scr;
   double *jtotal, *jnsum;
   want_incoming(ar, bb, N, 1);
   ar.want(&ecount, N); ar.want(&self_sub, N); ar.want(&eoff, N + 1); ar.want(&slow_list, cap_slow);
+  ar.want(&slow2, cap_slow);
   ar.want(&ctr, 4); ar.want(&scan_tmp, scan_scratch_ints(std::max(N, 1)) + 64);
   ar.want(&slow_scr, (int64_t)BW * 2 * (N + 1)); ar.want(&jtotal, N); ar.want(&jnsum, N);
   LEO_CUDA_CHECK(ar.commit());
@@ -394,7 +424,8 @@ int blame_impl(const LeoKernel* kk, const LeoProfile* pp, const LeoEdges* pruned
   BlameArgs a{caps ? caps->debug_flags : 0, own, p, pruned->prod, pruned->meta, paths->dist, inc, binc.rbeg, binc.rend, base->prod, base->meta,
               ecount, self_sub, jtotal, jnsum, eoff, *out, slow_list, &ctr[0], cap_slow, status};
   TRACED(KID_BLAME_COUNT, k_blame<0><<<grid_for(N, 128), 128, 0, st>>>(k, a));
-  TRACED(KID_SELFBLAME_SLOW, k_selfblame_slow<<<1, BW, 0, st>>>(k, a, slow_scr, BW));
+  TRACED(KID_SELFBLAME_SLOW, k_selfblame_warp<<<num_sms(), 128, 4 * kSBWarpInts * 4, st>>>(k, a, slow2, &ctr[1]));
+  TRACED(KID_SELFBLAME_SLOW, k_selfblame_slow<<<1, BW, 0, st>>>(k, a, slow2, &ctr[1], slow_scr, BW));
   TRACED(KID_SCAN, scan_exclusive(ecount, eoff, nullptr, N, scan_tmp, nullptr, st));
   TRACED(KID_BLAME_FILL, k_blame<1><<<grid_for(N, 128), 128, 0, st>>>(k, a));
   TRACED(KID_BLAME_TOTAL, k_blame_count<<<1, 1, 0, st>>>(eoff, N, *out));
@@ -478,6 +509,19 @@ int leo_events_destroy(int32_t n, void** events) {
   return 0;
 }
 
+int leo_debug_items(int64_t* out, int32_t n) {
+  if (n < 0 || n > 8192) return -1;
+  LEO_CUDA_CHECK(cudaMemcpyFromSymbol(out, g_item_cycles, (size_t)n * sizeof(long long)));
+  return 0;
+}
+
+int leo_debug_phases(int32_t slot, int64_t* out, int32_t n_ctas) {
+  if (slot < 0 || slot >= 4 || n_ctas < 0 || n_ctas > 1024) return -1;
+  LEO_CUDA_CHECK(cudaMemcpyFromSymbol(out, g_phase_ts, (size_t)n_ctas * 8 * sizeof(long long),
+                                      (size_t)slot * 1024 * 8 * sizeof(long long)));
+  return 0;
+}
+
 const char* leo_kernel_name(int id) { return (id >= 0 && id < KID_COUNT_) ? kKernelNames[id] : nullptr; }
 
 int leo_build_graph(const LeoKernel* k, const LeoCaps* caps, LeoEdges* out, LeoDiags* diags,
@@ -538,7 +582,7 @@ int leo_analyze(const LeoKernel* k, const LeoProfile* p, const LeoSamples* sampl
   SidePool& sp = side_pool();
   LeoTrace* tr = caps ? caps->trace : nullptr;
   // stage-0 binning only feeds pruning and blame: run it beside build_graph
-  const bool fork = tr == nullptr;
+  const bool fork = tr == nullptr || (tr->mode & 1);
   if (samples) {
     cudaStream_t s_bin = fork ? sp.s[1] : st;
     if (fork) link_streams(st, s_bin, sp.e[2]);

@@ -17,6 +17,7 @@
 //                   edge arena / path buffer overflowed the register budget.
 //   scan + k_compact  order-preserving compaction.
 #include "prims.cuh"
+#include "stage.cuh"
 
 namespace leo {
 
@@ -141,8 +142,12 @@ struct PruneArgs {
 
 // stage 1/2/4 predicates + stage-3 DFS for edge e.  Returns false when the
 // DFS needs the slow path.
+// `deferred` (optional): do not reserve path-pool space here; report the
+// valid-path count and leave vlen/vacc + pfirst[e] to the caller, which
+// reserves pool space for a whole CTA round with one atomic.
 LEO_DEV bool prune_one(const KView& k, const PView& p, const PruneArgs& a, int e, DfsEnt* stk, int scap,
-                       BackNode* arena, int acap, int32_t* vlen, double* vacc, int vcap) {
+                       BackNode* arena, int acap, int32_t* vlen, double* vacc, int vcap,
+                       int* deferred = nullptr) {
   const uint32_t m = a.meta[e];
   const int kind = (m >> 27) & 7;
   const int pr = a.prod[e], cn = a.cons[e];
@@ -174,7 +179,13 @@ LEO_DEV bool prune_one(const KView& k, const PView& p, const PruneArgs& a, int e
       int r = enumerate_paths(k, pr, cn, a.cfg.threshold[poc], a.cfg.max_paths, a.cfg.max_depth,
                               stk, scap, arena, acap, vlen, vacc, vcap, &nv);
       if (r == DFS_OVERFLOW) return false;
-      if (nv > 0) {
+      if (nv > 0 && deferred) {
+        *deferred = nv;
+        int64_t s = 0;
+        for (int x = 0; x < nv; x++) s += vlen[x];
+        dist = __ddiv_rn((double)s, (double)nv);
+        if (r == DFS_TRUNC) diag_push(a.diags, a.status, LEO_DIAG_PATH_CAPPED, pr, cn, 1, 0, e);
+      } else if (nv > 0) {
         int off = atomicAdd(a.paths.count, nv);
         if (off + nv > a.paths.capacity) {
           atomicOr(a.status, (uint32_t)LEO_ST_PATH_OVERFLOW);
@@ -227,6 +238,95 @@ __global__ void __launch_bounds__(128) k_prune_edges(KView k, PView p, PruneArgs
       }
     }
   }
+}
+
+// Shared-memory tier: the per-thread DFS state (stack, back-edge arena, valid
+// paths) lives in shared memory instead of local memory (which thrashes L1 at
+// ~1.5 KB per thread), and when the instruction -> block map and the block /
+// successor tables fit, every CTA stages them with TMA bulk copies so each
+// DFS pop is a shared-memory access.  Persistent CTAs, edges grid-strided.
+// Overflowing edges take the global-scratch worker (k_prune_slow).
+constexpr int kPSStack = 16, kPSArena = 16, kPSPaths = 8;
+constexpr int kPSThreadBytes = ((kPSStack * (int)sizeof(DfsEnt) + kPSArena * (int)sizeof(BackNode) +
+                                 kPSPaths * 12 + 7) & ~7) + 8;   // 8-byte pad: 2-way bank spread
+
+__host__ __device__ inline size_t prune_image_bytes(int N, int B) {
+  return carve_bytes(N, 4) + carve_bytes(B, 4) * 2 + carve_bytes(B + 1, 4) + carve_bytes(2 * (size_t)B + 4, 4);
+}
+__host__ __device__ inline size_t prune_smem_bytes(int N, int B, int threads, bool stage) {
+  return 16 + (stage ? prune_image_bytes(N, B) : 0) + (size_t)kPSThreadBytes * threads;
+}
+
+template <bool STAGE>
+__global__ void k_prune_edges_smem(KView k, PView p, PruneArgs a) {
+  extern __shared__ __align__(16) unsigned char sm_raw[];
+  SmemCarve cv{sm_raw};
+  uint64_t* bar = cv.take<uint64_t>(2);
+  PhaseMarks pm(a.dbg);
+  KView ks = k;
+  if (STAGE) {
+    const int N = k.N, B = k.B;
+    int32_t* bo = cv.take<int32_t>(N);
+    int32_t* bf = cv.take<int32_t>(B);
+    int32_t* bl = cv.take<int32_t>(B);
+    int32_t* sp = cv.take<int32_t>(B + 1);
+    int32_t* su = cv.take<int32_t>(2 * (size_t)B + 4);
+    StageBar sb;
+    sb.init(bar);
+    sb.begin();
+    sb.copy(bo, k.block_of, (size_t)N * 4);
+    sb.copy(bf, k.blk_first, (size_t)B * 4);
+    sb.copy(bl, k.blk_last, (size_t)B * 4);
+    sb.copy(sp, k.succ_ptr, (size_t)(B + 1) * 4);
+    sb.copy(su, k.succ, (size_t)min(k.succ_ptr[B], 2 * B + 4) * 4);
+    sb.commit_and_wait();
+    ks.block_of = bo; ks.blk_first = bf; ks.blk_last = bl; ks.succ_ptr = sp; ks.succ = su;
+  }
+  pm.mark(2, 1);
+  unsigned char* mine = cv.p + (size_t)threadIdx.x * kPSThreadBytes;
+  DfsEnt* stk = (DfsEnt*)mine;
+  BackNode* arena = (BackNode*)(mine + kPSStack * sizeof(DfsEnt));
+  double* vacc = (double*)(((uintptr_t)(arena + kPSArena) + 7) & ~(uintptr_t)7);
+  int32_t* vlen = (int32_t*)(vacc + kPSPaths);
+  __shared__ int swarp[33];
+  __shared__ int rbase;
+  const int n = *a.n_in;
+  const bool big_paths = a.cfg.max_paths > 64 || (a.dbg & LEO_DBG_PRUNE_SLOW);
+  // rounds of one edge per thread; valid paths reserved once per CTA round
+  for (int base = blockIdx.x * blockDim.x; base < n; base += gridDim.x * blockDim.x) {
+    const int e = base + threadIdx.x;
+    int nvd = 0;
+    if (e < n) {
+      bool ok = !big_paths && prune_one(ks, p, a, e, stk, kPSStack, arena, kPSArena, vlen, vacc, kPSPaths, &nvd);
+      if (!ok) {
+        nvd = 0;
+        int s2 = atomicAdd(a.slow_count, 1);
+        if (s2 < a.slow_cap) {
+          a.slow_list[s2] = e;
+        } else {
+          a.keep[e] = 0; a.npaths[e] = 0; a.pfirst[e] = -1; a.dist[e] = 1.0;
+          atomicOr(a.status, (uint32_t)LEO_ST_SCRATCH_OVERFLOW);
+        }
+      }
+    }
+    int tot;
+    const int ex = block_excl_scan(nvd, swarp, &tot);
+    if (threadIdx.x == 0) rbase = tot > 0 ? atomicAdd(a.paths.count, tot) : 0;
+    __syncthreads();
+    if (nvd > 0) {
+      const int off = rbase + ex;
+      if (off + nvd > a.paths.capacity) {
+        atomicOr(a.status, (uint32_t)LEO_ST_PATH_OVERFLOW);
+        a.npaths[e] = 0; a.pfirst[e] = -1;
+      } else {
+        for (int x = 0; x < nvd; x++) { a.paths.len[off + x] = vlen[x]; a.paths.accum[off + x] = vacc[x]; }
+        a.pfirst[e] = off;
+      }
+    }
+    __syncthreads();
+  }
+  __syncthreads();
+  pm.mark(2, 2);
 }
 
 __host__ __device__ inline size_t prune_slow_bytes(int max_depth, int max_paths) {

@@ -20,6 +20,7 @@
 // producer, sorted + deduplicated per producer and appended after the
 // raw/guard edges in (producer, consumer) order (_materialize_sync :485-492).
 #include "prims.cuh"
+#include "stage.cuh"
 
 namespace leo {
 
@@ -49,7 +50,8 @@ struct SyncArgs {
   int32_t* wc_count;
 };
 
-__global__ void k_sync_pack(KView k, uint32_t* __restrict__ wcword, uint8_t* __restrict__ setword) {
+__global__ void k_sync_pack(KView k, uint32_t* __restrict__ wcword, uint8_t* __restrict__ setword,
+                            uint32_t* __restrict__ bev) {
   for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < k.N; i += gridDim.x * blockDim.x) {
     const uint8_t sk = k.sync_kind[i];
     const uint32_t a = k.sync_a[i], b = k.sync_b[i];
@@ -66,6 +68,17 @@ __global__ void k_sync_pack(KView k, uint32_t* __restrict__ wcword, uint8_t* __r
         if (kLgkmcnt & BIT(k.opclass[i])) w |= kWcLgkm;
       }
       wcword[i] = w;
+      // per-block event flags: bit c = the block holds an instruction the
+      // counter-c visitor reacts to (a wait with a value for c, or a member)
+      uint32_t ev = 0;
+      if (w & kWcIsWait) {
+        if ((w & kWcBig) || (w & 0x3FF) != kWcNone) ev |= 1;
+        if ((w & kWcBig) || ((w >> 10) & 0x3FF) != kWcNone) ev |= 2;
+      } else {
+        if (w & kWcVm) ev |= 1;
+        if (w & kWcLgkm) ev |= 2;
+      }
+      if (ev) atomicOr(&bev[k.block_of[i]], ev);
     } else if (k.dialect == LEO_NVIDIA) {
       setword[i] = sk == LEO_SYNC_BARRIER ? (uint8_t)((a | (a >> 8)) & 0x7E) : 0;
     } else {
@@ -98,11 +111,37 @@ LEO_DEV void sync_emit(const SyncArgs& a, int producer, int wait) {
 
 struct Frame { int blk, q, m, a, budget; };
 
+// Chain-walk state of one (wait, counter).  Edges found are buffered (and
+// deduplicated) in `seen` and emitted in batches, one global atomic per batch
+// (the destructor flushes, so every return path emits).
+constexpr int kWcSeen = 32;
 struct WcState {
   int counter, level, wait;
   uint32_t member_bit;
-  int32_t seen[16];
-  int nseen;
+  int32_t seen[kWcSeen];
+  int nseen = 0;
+  const SyncArgs* sa = nullptr;
+  uint64_t* cbuf = nullptr;   // optional CTA buffer in shared memory (one global reservation per CTA)
+  int* ccnt = nullptr;
+  int ccap = 0;
+  LEO_DEV void flush() {
+    if (nseen == 0 || !sa) return;
+    if (cbuf) {
+      const int pos = atomicAdd(ccnt, nseen);
+      if (pos + nseen <= ccap) {
+        for (int t = 0; t < nseen; t++) cbuf[pos + t] = ((uint64_t)(uint32_t)seen[t] << 32) | (uint32_t)wait;
+        nseen = 0;
+        return;
+      }
+    }
+    const int base = atomicAdd(sa->key_count, nseen);
+    for (int t = 0; t < nseen; t++) {
+      if (base + t < sa->key_cap) sa->keys[base + t] = ((uint64_t)(uint32_t)seen[t] << 32) | (uint32_t)wait;
+      else atomicOr(sa->status, (uint32_t)LEO_ST_SCRATCH_OVERFLOW);
+    }
+    nseen = 0;
+  }
+  LEO_DEV ~WcState() { flush(); }
 };
 
 // waitcnt visitor (depgraph.py:368-384) on a packed word; returns 0 to stop,
@@ -117,12 +156,12 @@ LEO_DEV int wc_visit(uint32_t w, int x, WcState& s, int& m, int& a, const SyncAr
     }
   } else if (w & s.member_bit) {
     if (a != 0) {
-      if (m >= s.level) {   // pending[level:] -> edge (emitted once per wait when possible)
+      if (m >= s.level) {   // pending[level:] -> edge (buffered, deduplicated per batch)
         bool dup = false;
         for (int t = 0; t < s.nseen; t++) if (s.seen[t] == x) { dup = true; break; }
         if (!dup) {
-          if (s.nseen < 16) s.seen[s.nseen++] = x;
-          sync_emit(sa, x, s.wait);
+          if (s.nseen == kWcSeen) s.flush();
+          s.seen[s.nseen++] = x;
         }
       }
       m++;
@@ -161,12 +200,12 @@ LEO_DEV bool on_path(const Frame* fr, int top, int blk) {
 constexpr int kT1ChainSteps = 48;   // block scans before a waitcnt item moves to the warp tier
 
 LEO_DEV bool trace_waitcnt_one(const KView& k, int wait, int counter, int level, const SyncArgs& sa,
-                               Frame* fr, int fcap, int& best_m) {
+                               Frame* fr, int fcap, int& best_m, int max_steps = kT1ChainSteps) {
   int steps = 0;
   WcState s;
   s.counter = counter; s.level = level; s.wait = wait;
   s.member_bit = counter == 0 ? kWcVm : kWcLgkm;
-  s.nseen = 0;
+  s.nseen = 0; s.sa = &sa;
   const int b0 = k.block_of[wait];
   int m = 0, a = -1, budget = kSyncBudget;
   int r = wc_scan(sa, wait - 1, k.blk_first[b0], budget, s, m, a);
@@ -188,7 +227,7 @@ LEO_DEV bool trace_waitcnt_one(const KView& k, int wait, int counter, int level,
       if (!on_path(fr, top, c)) { p = c; break; }
     }
     if (p < 0) { top--; continue; }
-    if (++steps > kT1ChainSteps) return false;
+    if (++steps > max_steps) return false;
     m = f.m; a = f.a; budget = f.budget;
     r = wc_scan(sa, k.blk_last[p], k.blk_first[p], budget, s, m, a);
     if (r < 0) return false;
@@ -239,7 +278,7 @@ __global__ void k_sync_wc_warp(KView k, SyncArgs a, const int32_t* __restrict__ 
     WcState s;
     s.counter = counter; s.level = level; s.wait = wait;
     s.member_bit = counter == 0 ? kWcVm : kWcLgkm;
-    s.nseen = 0;
+    s.nseen = 0; s.sa = &a;
     const int b0 = k.block_of[wait];
     if (lane == 0) {
       c[0] = 0; c[1] = 0; c[2] = 0;
@@ -320,7 +359,7 @@ LEO_DEV int wc_visit_exact(const KView& k, int x, WcState& s, int& m, int& a, co
 LEO_DEV bool trace_waitcnt_exact(const KView& k, int wait, int counter, int level, const SyncArgs& sa,
                                  Frame* fr, int fcap, int& best_m) {
   WcState s;
-  s.counter = counter; s.level = level; s.wait = wait; s.nseen = 0;
+  s.counter = counter; s.level = level; s.wait = wait; s.nseen = 0; s.sa = nullptr;
   const int b0 = k.block_of[wait];
   int m = 0, a = -1, budget = kSyncBudget;
   bool stopped = false;
@@ -576,6 +615,165 @@ __global__ void k_sync(KView k, SyncArgs a, char* scratch, int nworkers) {
       }
     }
   }
+}
+
+// Block scan with the per-block event flag: a block without events for the
+// counter only spends budget (same stop rule as wc_scan: a chain stops when it
+// would visit an instruction with no budget left).
+LEO_DEV int wc_scan_blk(const SyncArgs& sa, const uint32_t* bev, int blk, int hi, int lo, int& budget,
+                        WcState& s, int& m, int& a) {
+  if (!((bev[blk] >> s.counter) & 1)) {
+    const int len = hi - lo + 1;
+    if (len <= 0) return 1;
+    if (budget >= len) { budget -= len; return 1; }
+    budget = 0;
+    return 0;
+  }
+  return wc_scan(sa, hi, lo, budget, s, m, a);
+}
+
+// trace_waitcnt_one with O(1) on-path tests: the blocks of the current chain
+// are bits of a thread-private bitmap in shared memory (column `pb`, stride
+// T words), set on push and cleared on pop.
+LEO_DEV bool trace_waitcnt_bits(const KView& k, const uint32_t* bev, uint32_t* pb, int T, int wait, int counter,
+                                int level, const SyncArgs& sa, Frame* fr, int fcap, int& best_m, int max_steps,
+                                uint64_t* cbuf, int* ccnt, int ccap) {
+  auto bit = [&](int b) -> bool { return (pb[(b >> 5) * T] >> (b & 31)) & 1u; };
+  auto setb = [&](int b) { pb[(b >> 5) * T] |= 1u << (b & 31); };
+  auto clrb = [&](int b) { pb[(b >> 5) * T] &= ~(1u << (b & 31)); };
+  int steps = 0;
+  WcState s;
+  s.counter = counter; s.level = level; s.wait = wait;
+  s.member_bit = counter == 0 ? kWcVm : kWcLgkm;
+  s.nseen = 0; s.sa = &sa; s.cbuf = cbuf; s.ccnt = ccnt; s.ccap = ccap;
+  const int b0 = k.block_of[wait];
+  int m = 0, a = -1, budget = kSyncBudget;
+  int r = wc_scan_blk(sa, bev, b0, wait - 1, k.blk_first[b0], budget, s, m, a);
+  if (r < 0) return false;
+  best_m = 0;
+  if (r == 0) { best_m = m; return true; }
+  {
+    bool any = false;
+    for (int q = k.pred_ptr[b0]; q < k.pred_ptr[b0 + 1]; q++) if (k.pred[q] != b0) any = true;
+    if (!any) { best_m = m; return true; }
+  }
+  int top = 0;
+  fr[top++] = Frame{b0, k.pred_ptr[b0], m, a, budget};
+  setb(b0);
+  auto bail = [&]() { for (int t = 0; t < top; t++) clrb(fr[t].blk); return false; };
+  while (top > 0) {
+    Frame& f = fr[top - 1];
+    int p = -1;
+    const int qe = k.pred_ptr[f.blk + 1];
+    while (f.q < qe) {
+      const int c = k.pred[f.q++];
+      if (!bit(c)) { p = c; break; }
+    }
+    if (p < 0) { clrb(f.blk); top--; continue; }
+    if (++steps > max_steps) return bail();
+    m = f.m; a = f.a; budget = f.budget;
+    r = wc_scan_blk(sa, bev, p, k.blk_last[p], k.blk_first[p], budget, s, m, a);
+    if (r < 0) return bail();
+    if (r == 0) { best_m = max(best_m, m); continue; }
+    if (top == fcap) return bail();
+    fr[top++] = Frame{p, k.pred_ptr[p], m, a, budget};
+    setb(p);
+    bool any = false;
+    for (int q = k.pred_ptr[p]; q < k.pred_ptr[p + 1] && !any; q++)
+      if (!bit(k.pred[q])) any = true;
+    if (!any) { best_m = max(best_m, m); clrb(p); top--; }
+  }
+  return true;
+}
+
+// Shared-memory-resident waitcnt tier (amd): every CTA stages the packed scan
+// words and the block table / predecessor CSR with TMA bulk copies, then runs
+// the exact chain enumeration of trace_waitcnt_one at shared-memory latency.
+// Items are spread one per warp first (item t -> warp t % nwarps, lane
+// t / nwarps), so lanes of a warp rarely serialise behind each other.  Items
+// whose chain tree outgrows the frame stack or the step bound go to the warp
+// tier (global memory); unpackable counter values to the exact walker.
+constexpr int kWcSmemSteps = 4096;
+
+constexpr int kWcCtaKeys = 1024;
+__host__ __device__ inline size_t sync_smem_bytes(int N, int B, int threads) {
+  return 16 + 8 * kWcCtaKeys + carve_bytes(N, 4) + carve_bytes(B, 4) * 3 + carve_bytes(B + 1, 4) + carve_bytes(2 * (size_t)B + 4, 4)
+         + carve_bytes((size_t)((B + 31) >> 5) * threads, 4);
+}
+
+__global__ void k_sync_wc_smem(KView k, SyncArgs a, const uint32_t* __restrict__ bev_g) {
+  extern __shared__ __align__(16) unsigned char sm_raw[];
+  const int N = k.N, B = k.B;
+  SmemCarve cv{sm_raw};
+  uint64_t* bar = cv.take<uint64_t>(2);
+  uint64_t* kbuf = cv.take<uint64_t>(kWcCtaKeys);
+  __shared__ int kcnt, kbase;
+  if (threadIdx.x == 0) kcnt = 0;
+  uint32_t* ww = cv.take<uint32_t>(N);
+  int32_t* bf = cv.take<int32_t>(B);
+  int32_t* bl = cv.take<int32_t>(B);
+  int32_t* pp = cv.take<int32_t>(B + 1);
+  int32_t* pr = cv.take<int32_t>(2 * (size_t)B + 4);
+  uint32_t* bev4 = cv.take<uint32_t>(B);
+  const int T = blockDim.x, W = (B + 31) >> 5;
+  uint32_t* pbits = cv.take<uint32_t>((size_t)W * T);
+  for (int x = threadIdx.x; x < W * T; x += T) pbits[x] = 0u;
+  PhaseMarks pm(a.dbg);
+  StageBar sb;
+  sb.init(bar);
+  sb.begin();
+  sb.copy(ww, a.wcword, (size_t)N * 4);
+  sb.copy(bf, k.blk_first, (size_t)B * 4);
+  sb.copy(bl, k.blk_last, (size_t)B * 4);
+  sb.copy(pp, k.pred_ptr, (size_t)(B + 1) * 4);
+  sb.copy(pr, k.pred, (size_t)k.pred_ptr[B] * 4);
+  sb.copy(bev4, bev_g, (size_t)B * 4);
+  sb.commit_and_wait();
+  pm.mark(1, 1);
+  const uint32_t* bev = bev4;
+  KView ks = k;
+  ks.blk_first = bf; ks.blk_last = bl; ks.pred_ptr = pp; ks.pred = pr;
+  SyncArgs as = a;
+  as.wcword = ww;
+  const int n_items = *a.wait_count;
+  const int lane = threadIdx.x & 31;
+  const int nwarps = gridDim.x * (blockDim.x >> 5);
+  const int gw = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+  Frame fr[kFrames];
+  for (int t = lane * nwarps + gw; t < n_items; t += 32 * nwarps) {
+    const int i = a.wait_list[t];
+    if (k.sync_kind[i] != LEO_SYNC_WAITCNT) continue;
+    for (int counter = 0; counter < 2; counter++) {   // vmcnt before lgkmcnt (:410-415)
+      const uint32_t lv = counter == 0 ? k.sync_a[i] : k.sync_b[i];
+      if (lv == LEO_NONE_U32) continue;
+      int best_m = 0;
+      const long long c0 = clock64();
+      const bool ok = !(a.dbg & LEO_DBG_SYNC_SLOW) && lv < kWcNone &&
+                      trace_waitcnt_bits(ks, bev, pbits + threadIdx.x, T, i, counter, (int)lv, as, fr, kFrames,
+                                         best_m, kWcSmemSteps, kbuf, &kcnt, kWcCtaKeys);
+      if ((a.dbg & LEO_DBG_PHASES) && t < 4096) g_item_cycles[t * 2 + counter] = clock64() - c0;
+      if (!ok) {
+        const bool to_warp = lv < kWcNone && !(a.dbg & LEO_DBG_SYNC_SLOW);
+        int32_t* lst = to_warp ? a.wc_list : a.slow_list;
+        int32_t* cnt = to_warp ? a.wc_count : a.slow_count;
+        const int s2 = atomicAdd(cnt, 1);
+        if (s2 < a.slow_cap) lst[s2] = (i << 6) | counter;
+        else atomicOr(a.status, (uint32_t)LEO_ST_SCRATCH_OVERFLOW);
+        continue;
+      }
+      if ((long long)best_m < (long long)lv)
+        diag_push(a.diags, a.status, LEO_DIAG_WAITCNT, i, counter, (int)lv, best_m, counter);
+    }
+  }
+  __syncthreads();
+  const int nk = min(kcnt, kWcCtaKeys);
+  if (threadIdx.x == 0) kbase = nk > 0 ? atomicAdd(a.key_count, nk) : 0;
+  __syncthreads();
+  for (int x = threadIdx.x; x < nk; x += blockDim.x) {
+    if (kbase + x < a.key_cap) a.keys[kbase + x] = kbuf[x];
+    else atomicOr(a.status, (uint32_t)LEO_ST_SCRATCH_OVERFLOW);
+  }
+  pm.mark(1, 2);
 }
 
 template __global__ void k_sync<false>(KView, SyncArgs, char*, int);

@@ -215,10 +215,13 @@ class Analyzer:
         check(rc, "leo_analyze")
 
     # -- CUDA graph ----------------------------------------------------------
-    def capture(self, dp: DeviceProfile, cfg: abi.LeoConfig, samples: DeviceSamples | None = None):
+    def capture(self, dp: DeviceProfile, cfg: abi.LeoConfig, samples: DeviceSamples | None = None,
+                trace_in_graph: bool = False):
         """Capture the whole stream-ordered pipeline (no host syncs inside) into
         one CUDA graph; `replay()` then re-runs it on the current buffers.
-        Buffers must already be sized (call run() first)."""
+        Buffers must already be sized (call run() first).  `trace_in_graph`:
+        the tracer's events become event-record nodes of the graph (a replay
+        timeline)."""
         tracer = self.tracer
         self.set_tracer(None)
         self._graph_args = (dp, cfg, samples)
@@ -229,6 +232,9 @@ class Analyzer:
             self.launch(dp, cfg, samples)
         torch.cuda.current_stream(self.device).wait_stream(side)
         torch.cuda.synchronize(self.device)
+        if trace_in_graph and tracer is not None:
+            tracer.reset()
+            self.set_tracer(tracer)
         with torch.cuda.graph(g, capture_error_mode="thread_local"):
             self.launch(dp, cfg, samples)
         torch.cuda.synchronize(self.device)
@@ -327,7 +333,7 @@ class Tracer:
     recorded by the library on the launching stream around each kernel (or
     only around `only_kernel`)."""
 
-    def __init__(self, capacity: int = 4096, only_kernel: int = -1):
+    def __init__(self, capacity: int = 4096, only_kernel: int = -1, timeline: bool = False):
         L = lib()
         self.capacity = capacity
         self.begin = (C.c_void_p * capacity)()
@@ -335,7 +341,8 @@ class Tracer:
         self.ids = (C.c_int32 * capacity)()
         check(L.leo_events_create(capacity, self.begin), "leo_events_create")
         check(L.leo_events_create(capacity, self.end), "leo_events_create")
-        self.struct = abi.LeoTrace(capacity, 0, only_kernel, 0, C.cast(self.begin, C.c_void_p),
+        self.struct = abi.LeoTrace(capacity, 0, only_kernel, 1 if timeline else 0,
+                                   C.cast(self.begin, C.c_void_p),
                                    C.cast(self.end, C.c_void_p), C.cast(self.ids, C.c_void_p))
 
     def reset(self, only_kernel: int | None = None):
@@ -350,6 +357,20 @@ class Tracer:
         ms = (C.c_float * max(n, 1))()
         check(L.leo_events_elapsed(n, self.begin, self.end, ms), "leo_events_elapsed")
         return [(L.leo_kernel_name(self.ids[i]).decode(), float(ms[i])) for i in range(n)]
+
+    def timeline(self) -> list[tuple[str, float, float]]:
+        """(kernel name, start ms, end ms) relative to the first recorded
+        launch; with timeline=True the branches keep running concurrently."""
+        L = lib()
+        n = min(self.struct.count, self.capacity)
+        if n == 0:
+            return []
+        base = (C.c_void_p * n)(*([self.begin[0]] * n))
+        t0 = (C.c_float * n)()
+        t1 = (C.c_float * n)()
+        check(L.leo_events_elapsed(n, base, self.begin, t0), "leo_events_elapsed")
+        check(L.leo_events_elapsed(n, base, self.end, t1), "leo_events_elapsed")
+        return [(L.leo_kernel_name(self.ids[i]).decode(), float(t0[i]), float(t1[i])) for i in range(n)]
 
     def summary(self) -> dict[str, float]:
         out: dict[str, float] = {}

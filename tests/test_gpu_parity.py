@@ -108,7 +108,7 @@ def test_device_full_c5_properties(cuda):
     assert deeper.sum() >= 0
 
 
-@pytest.mark.parametrize("flags", [1, 2 | 4 | 8 | 16])
+@pytest.mark.parametrize("flags", [1, 2 | 4 | 8 | 16, 32])
 @pytest.mark.parametrize("fname", ["corpus_c1.npz", "random.npz", "synth.npz"])
 def test_device_fallback_tiers_match_golden(fname, flags, golden_cases, cuda):
     """Every work item forced onto the larger tiers (warp / global-scratch
