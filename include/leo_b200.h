@@ -129,6 +129,11 @@ typedef struct LeoSamples {
   const int32_t* pc;          /* [S] instruction index */
   const uint8_t* cat;         /* [S] vendor stall category id */
   const uint8_t* cat_to_cs;   /* [256] vendor category id -> CommonStall (map_stall) */
+  /* optional host sources (pinned memory): when set, pc / cat are device
+   * buffers the library fills with an asynchronous copy on the binning branch,
+   * so the transfer of the sample stream overlaps graph construction */
+  const int32_t* pc_host;
+  const uint8_t* cat_host;
 } LeoSamples;
 
 /* ---- analysis configuration (analysis.py:115-124) ------------------------ */

@@ -32,7 +32,8 @@ class LeoProfile(C.Structure):
 
 
 class LeoSamples(C.Structure):
-    _fields_ = [("n_samples", C.c_int64), ("pc", P), ("cat", P), ("cat_to_cs", P)]
+    _fields_ = [("n_samples", C.c_int64), ("pc", P), ("cat", P), ("cat_to_cs", P),
+                ("pc_host", P), ("cat_host", P)]
 
 
 class LeoConfig(C.Structure):

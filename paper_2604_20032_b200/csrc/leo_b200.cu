@@ -454,6 +454,10 @@ static int bin_impl(const LeoSamples* s, int32_t n_instr, int32_t* lat, int32_t*
   set_smem_attributes();
   cudaMemsetAsync(cls_cnt, 0, (size_t)std::max(n_instr, 1) * 32, st);
   const int64_t S = s->n_samples;
+  if (S > 0 && s->pc_host)
+    LEO_CUDA_CHECK(cudaMemcpyAsync((void*)s->pc, s->pc_host, (size_t)S * 4, cudaMemcpyHostToDevice, st));
+  if (S > 0 && s->cat_host)
+    LEO_CUDA_CHECK(cudaMemcpyAsync((void*)s->cat, s->cat_host, (size_t)S, cudaMemcpyHostToDevice, st));
   const int R = (n_instr + kBinR - 1) / kBinR <= kBinMaxBuckets ? kBinR : kBinRMax;
   const int nb = std::max(1, (n_instr + R - 1) / R);
   const bool bucketed = nb <= kBinMaxBuckets && S > 0;

@@ -100,32 +100,51 @@ __global__ void scan_tile_apply(const int32_t* __restrict__ in, const int32_t* n
 }
 
 // one CTA scans the whole array tile by tile (small arrays: one launch)
+// Single CTA, thread-contiguous chunks: pass 1 sums each thread's chunk
+// (independent 16-byte loads), one block scan of the chunk sums, pass 2
+// writes the running prefix.  Two reads of the input (L2-resident), one
+// block-wide barrier phase instead of one per 8K-element tile.
 __global__ void __launch_bounds__(1024) scan_single_cta(const int32_t* __restrict__ in, const int32_t* n_dev,
                                                         int64_t n_cap, int32_t* __restrict__ out,
                                                         int32_t* total_out) {
   __shared__ int sw[33];
-  const int64_t n = n_dev ? (int64_t)*n_dev : n_cap;
-  int carry = 0;
-  for (int64_t base = 0; base < n; base += (int64_t)blockDim.x * kScanItems) {
-    const int64_t i0 = base + (int64_t)threadIdx.x * kScanItems;
-    int v[kScanItems];
-    int s = 0;
-#pragma unroll
-    for (int k = 0; k < kScanItems; k++) { v[k] = i0 + k < n ? in[i0 + k] : 0; s += v[k]; }
-    int tot;
-    int ex = block_excl_scan(s, sw, &tot) + carry;
-#pragma unroll
-    for (int k = 0; k < kScanItems; k++) { if (i0 + k < n) out[i0 + k] = ex; ex += v[k]; }
-    carry += tot;
+  const int n = (int)(n_dev ? (int64_t)*n_dev : n_cap);
+  const int per = ((n + blockDim.x - 1) / blockDim.x + 3) & ~3;   // multiple of 4
+  const int lo = min(n, (int)threadIdx.x * per), hi = min(n, lo + per);
+  const bool vec = ((((uintptr_t)in) & 15) == 0);
+  int s = 0;
+  if (vec) {
+    int x = lo;
+    for (; x + 4 <= hi; x += 4) {
+      const int4 v = *reinterpret_cast<const int4*>(in + x);
+      s += v.x + v.y + v.z + v.w;
+    }
+    for (; x < hi; x++) s += in[x];
+  } else {
+    for (int x = lo; x < hi; x++) s += in[x];
   }
-  if (threadIdx.x == 0) { out[n] = carry; if (total_out) *total_out = carry; }
+  int tot;
+  int run = block_excl_scan(s, sw, &tot);
+  if (vec && ((((uintptr_t)out) & 15) == 0)) {
+    int x = lo;
+    for (; x + 4 <= hi; x += 4) {
+      const int4 v = *reinterpret_cast<const int4*>(in + x);
+      int4 o;
+      o.x = run; run += v.x; o.y = run; run += v.y; o.z = run; run += v.z; o.w = run; run += v.w;
+      *reinterpret_cast<int4*>(out + x) = o;
+    }
+    for (; x < hi; x++) { const int v = in[x]; out[x] = run; run += v; }
+  } else {
+    for (int x = lo; x < hi; x++) { const int v = in[x]; out[x] = run; run += v; }
+  }
+  if (threadIdx.x == 0) { out[n] = tot; if (total_out) *total_out = tot; }
 }
 
 // exclusive scan of in[0..n) into out[0..n] (out[n] = total); n from n_dev if
 // given else n_cap.  scratch: >= tiles(n_cap) ints.  total_out optional.
 inline void scan_exclusive(const int32_t* in, int32_t* out, const int32_t* n_dev, int64_t n_cap,
                            int32_t* scratch, int32_t* total_out, cudaStream_t st) {
-  if (n_cap <= 65536) {
+  if (n_cap <= (1 << 18)) {
     scan_single_cta<<<1, 1024, 0, st>>>(in, n_dev, n_cap, out, total_out);
     return;
   }

@@ -68,11 +68,48 @@ LEO_DEV int enumerate_paths(const KView& k, int producer, int consumer, double t
   const double w0 = issue_weight(k, producer);
   if (w0 > thr) return DFS_OK;
   stk[sp++] = DfsEnt{producer, 1, -1, 0, w0};
+  const bool unit_w = k.dialect != LEO_NVIDIA;     // every issue weight is 1.0
   while (sp > 0) {
     DfsEnt e = stk[--sp];
     if (budget <= 0 || nv >= max_paths) { truncated = 1; break; }
     budget--;
     const int nb = k.block_of[e.node];
+    if (unit_w && e.node < k.blk_last[nb]) {
+      // Straight run e.node+1 .. blk_last: each step pushes its successor and
+      // the LIFO pops it right back, so the run is a sequence of consecutive
+      // pops that can be resolved in closed form.  Step i reaches node
+      // x+i with len+i, acc+i; the first of {consumer reached, acc > thr,
+      // len >= max_depth} ends the run (checked in that order), each step
+      // before it costs one pop of budget.
+      const int x = e.node, L = k.blk_last[nb];
+      const int i_end = L - x;
+      const int i_c = (consumer > x && consumer <= L) ? consumer - x : 0x7fffffff;
+      int i_thr;
+      {
+        const double f = thr - e.acc;
+        i_thr = f < 0.0 ? 1 : (f > 1e9 ? 0x3fffffff : (int)floor(f) + 1);
+        while (i_thr > 1 && __dadd_rn(e.acc, (double)(i_thr - 1)) > thr) i_thr--;
+        while (i_thr < 0x3fffffff && !(__dadd_rn(e.acc, (double)i_thr) > thr)) i_thr++;
+      }
+      const int i_dep = max(1, max_depth - e.len);
+      const int i_stop = min(i_c, min(i_thr, i_dep));
+      if (i_stop <= i_end) {
+        const int need = i_stop - 1;
+        if (budget < need) { budget = 0; truncated = 1; break; }
+        budget -= need;
+        if (i_stop == i_c) {
+          if (nv == vcap) return DFS_OVERFLOW;
+          vlen[nv] = e.len + i_c - 1; vacc[nv] = __dadd_rn(e.acc, (double)(i_c - 1)); nv++;
+          if (nv >= max_paths) truncated = 1;
+        } else if (i_stop != i_thr) {
+          truncated = 1;                              // max_depth
+        }
+        continue;
+      }
+      if (budget < i_end) { budget = 0; truncated = 1; break; }
+      budget -= i_end;
+      e.node = L; e.len += i_end; e.acc = __dadd_rn(e.acc, (double)i_end);
+    }
     int succ_n, s0 = -1, s1 = -1;
     if (e.node < k.blk_last[nb]) { succ_n = 1; s0 = e.node + 1; }
     else {

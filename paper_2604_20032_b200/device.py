@@ -90,6 +90,13 @@ class DeviceSamples:
         self.struct = abi.LeoSamples(self.n, ptr(pc), ptr(cat), ptr(lut))
         return self
 
+    def set_host_sources(self, pc_host: torch.Tensor | None, cat_host: torch.Tensor | None):
+        """Pinned host tensors the library copies into pc / cat on the binning
+        branch (overlapping the build); None: samples already on the device."""
+        self.host_src = (pc_host, cat_host)
+        self.struct.pc_host = pc_host.data_ptr() if pc_host is not None else None
+        self.struct.cat_host = cat_host.data_ptr() if cat_host is not None else None
+
 
 # counter slots in one int32 device vector
 C_BASE, C_BASE_REG, C_PR, C_PR_REG, C_PATHS, C_DIAGS, C_BLAME, C_STATUS = range(8)
