@@ -345,7 +345,7 @@ LEO_DEV int dominant_self(const PView& p, int j) {     // _dominant_class :379-3
   return kSelfByClass[dom];
 }
 
-constexpr int kSeenCap = 96;
+constexpr int kSeenCap = 24;
 
 // pass 0: decide self vs edges, entry count, cached sums; pass 1: write entries
 template <int PASS>
@@ -390,10 +390,18 @@ __global__ void k_blame(KView k, BlameArgs a) {
       if (self) {
         int sub = dominant_self(a.p, j);
         if (sub == LEO_SB_MEMORY_LATENCY && (kMemoryClasses & BIT(k.opclass[j]))) {
-          // _address_traces_to_load runs in k_selfblame_warp (warp per candidate)
-          int s = atomicAdd(a.slow_count, 1);
-          if (s < a.slow_cap) a.slow_list[s] = j;
-          else atomicOr(a.status, (uint32_t)LEO_ST_SCRATCH_OVERFLOW);
+          // _address_traces_to_load: small searches inline (<= kSeenCap nodes),
+          // larger ones in k_selfblame_warp (warp per candidate)
+          int32_t seen[kSeenCap];
+          const int r = (a.dbg & LEO_DBG_SELF_SLOW) ? -1
+                        : traces_to_load(k, a.brbeg, a.brend, a.bprod, a.bmeta, j, seen, kSeenCap, nullptr, 0);
+          if (r < 0) {
+            int s = atomicAdd(a.slow_count, 1);
+            if (s < a.slow_cap) a.slow_list[s] = j;
+            else atomicOr(a.status, (uint32_t)LEO_ST_SCRATCH_OVERFLOW);
+          } else if (r) {
+            sub = LEO_SB_INDIRECT_ADDRESSING;
+          }
         }
         a.self_sub[j] = sub;
         a.ecount[j] = 1;
@@ -472,8 +480,11 @@ __global__ void k_selfblame_warp(KView k, BlameArgs a, int32_t* slow2, int32_t* 
     __syncwarp();
     int32_t *cur = fa, *nxt = fb;
     for (int depth = 0; depth < 8; depth++) {
+      // every lane reads the loop control before any lane can modify it
       const int ncur = c[0];
-      if (ncur == 0 || c[2] || c[3]) break;
+      const bool stop = ncur == 0 || c[2] || c[3];
+      __syncwarp();
+      if (stop) break;
       for (int x = lane; x < ncur; x += 32) {
         const int node = cur[x];
         for (int e = a.brbeg[node]; e < a.brend[node]; e++) {
@@ -532,7 +543,8 @@ __global__ void k_blame_count(const int32_t* eoff, int N, LeoBlame out) { *out.c
 __global__ void k_lines(KView k, PView p, Range own, const int32_t* __restrict__ pprod, LeoBlame b,
                         const int32_t* __restrict__ line_id, double* __restrict__ line_blame,
                         double* __restrict__ line_stall) {
-  const int n = min(*b.count, b.capacity);
+  // an overflowed entry list has unwritten holes: the host re-runs bigger
+  const int n = *b.count <= b.capacity ? *b.count : 0;
   const int stride = gridDim.x * blockDim.x;
   for (int x = blockIdx.x * blockDim.x + threadIdx.x; x < n; x += stride) {
     int e = b.edge[x];

@@ -567,8 +567,11 @@ __global__ void k_reach_warp(KView k, ReachArgs a, const int32_t* __restrict__ l
     __syncwarp();
     int32_t *cur = fa, *nxt = fb;
     while (true) {
+      // every lane reads the loop control before any lane can modify it
       const int ncur = c[1];
-      if (ncur == 0 || c[3]) break;
+      const bool stop = ncur == 0 || c[3];
+      __syncwarp();
+      if (stop) break;
       for (int x = lane; x < ncur; x += 32) {
         const int y = cur[x];
         const int4 r = a.rec[y];

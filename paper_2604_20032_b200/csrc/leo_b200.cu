@@ -7,6 +7,7 @@
 #include <algorithm>
 #include <cstdio>
 #include <cstring>
+#include <cstdlib>
 
 #include "prims.cuh"
 #include "graph.cu"
@@ -25,14 +26,14 @@ enum KernelId {
   KID_REACH_SLOW, KID_LINK_COUNT, KID_LINK_FILL, KID_SEGSORT, KID_LINK_EMIT, KID_SYNC,
   KID_SYNC_SLOW, KID_KEY_HIST, KID_KEY_SCATTER, KID_SYNC_EMIT, KID_EDGE_TOTALS, KID_PRUNE,
   KID_PRUNE_SLOW, KID_COMPACT, KID_SEG_BOUNDS, KID_SYNC_HIST, KID_SYNC_FILL, KID_BLAME_COUNT,
-  KID_SELFBLAME_SLOW, KID_BLAME_FILL, KID_BLAME_TOTAL, KID_LINES, KID_SLICE, KID_REACH_WARP, KID_RUN_HEADS, KID_BIN_HIST, KID_BIN_PLAN, KID_BIN_SCATTER, KID_SYNC_PACK, KID_SYNC_WARP, KID_COUNT_
+  KID_SELFBLAME_SLOW, KID_BLAME_FILL, KID_BLAME_TOTAL, KID_LINES, KID_SLICE, KID_REACH_WARP, KID_RUN_HEADS, KID_BIN_HIST, KID_BIN_PLAN, KID_BIN_SCATTER, KID_SYNC_PACK, KID_SYNC_WARP, KID_SELFBLAME_WARP, KID_COUNT_
 };
 const char* const kKernelNames[] = {
   "bin_samples", "bin_finalize", "unit_counts", "scan", "block_walk", "reach_fast",
   "reach_slow", "link_count", "link_fill", "segsort_unique", "link_emit", "sync_trace",
   "sync_trace_slow", "key_hist", "key_scatter", "sync_emit", "edge_totals", "prune_edges",
   "prune_slow", "compact", "seg_bounds", "sync_hist", "sync_fill", "blame_count",
-  "selfblame_slow", "blame_fill", "blame_total", "lines", "slice", "reach_warp", "run_heads", "bin_hist", "bin_plan", "bin_scatter", "sync_pack", "sync_warp",
+  "selfblame_slow", "blame_fill", "blame_total", "lines", "slice", "reach_warp", "run_heads", "bin_hist", "bin_plan", "bin_scatter", "sync_pack", "sync_warp", "selfblame_warp",
 };
 
 struct TraceScope {
@@ -47,7 +48,28 @@ struct TraceScope {
   }
   ~TraceScope() { if (slot >= 0) cudaEventRecord((cudaEvent_t)t->ev_end[slot], st); }
 };
-#define TRACED(id, ...) do { TraceScope _ts(tr, id, st); __VA_ARGS__; } while (0)
+// LEO_DEBUG_SYNC=1: synchronise after every kernel and report the first
+// failing (or hanging: last printed) kernel on stderr (debugging aid)
+bool debug_sync_env() {
+  static int v = -1;
+  if (v < 0) { const char* e = getenv("LEO_DEBUG_SYNC"); v = (e && e[0] == '1') ? 1 : 0; }
+  return v == 1;
+}
+inline void debug_sync_after(int id, cudaStream_t st) {
+  if (!debug_sync_env()) return;
+  cudaError_t e = cudaStreamSynchronize(st);
+  if (e == cudaSuccess) e = cudaGetLastError();
+  if (e != cudaSuccess) fprintf(stderr, "[leo debug] kernel %d failed: %s\n", id, cudaGetErrorString(e));
+}
+#define TRACED(id, ...) do { if (debug_sync_env()) { fprintf(stderr, "[leo debug] launch %d\n", (int)(id)); fflush(stderr); } \
+  { TraceScope _ts(tr, id, st); __VA_ARGS__; } debug_sync_after(id, st); } while (0)
+
+// LEO_NO_FORK=1: run every stage on the caller's stream (debugging aid)
+bool no_fork_env() {
+  static int v = -1;
+  if (v < 0) { const char* e = getenv("LEO_NO_FORK"); v = (e && e[0] == '1') ? 1 : 0; }
+  return v == 1;
+}
 
 int g_num_sms = 0;
 int num_sms() {
@@ -227,7 +249,7 @@ int build_graph_impl(const LeoKernel* kk, const LeoCaps* caps, LeoEdges* out, Le
   SidePool& sp = side_pool();
   // traced runs stay on one stream so per-kernel event times are not
   // inflated by queueing behind concurrent branches
-  const bool fork = tr == nullptr || (tr->mode & 1);
+  const bool fork = (tr == nullptr || (tr->mode & 1)) && !no_fork_env();
   cudaStream_t s_sync = fork ? sp.s[0] : st;
   if (fork) link_streams(st, s_sync, sp.e[0]);
   const int kind = k.dialect == LEO_AMD ? LEO_EK_MEM_WAITCNT : k.dialect == LEO_NVIDIA ? LEO_EK_MEM_BARRIER : LEO_EK_MEM_SWSB;
@@ -256,7 +278,7 @@ int build_graph_impl(const LeoKernel* kk, const LeoCaps* caps, LeoEdges* out, Le
     TRACED(KID_KEY_HIST, k_key_hist<<<grid_for(cap_sync, T), T, 0, st>>>(skeys, &ctr[3], cap_sync, pcnt));
     TRACED(KID_SCAN, scan_exclusive(pcnt, poff, nullptr, N, scan_tmp2, nullptr, st));
     TRACED(KID_KEY_SCATTER, k_key_scatter<<<grid_for(cap_sync, T), T, 0, st>>>(skeys, &ctr[3], cap_sync, poff, pcur, ssorted));
-    TRACED(KID_SEGSORT, segsort_unique_u64<<<grid_for(N, 128), 128, 0, st>>>(ssorted, poff, pcnt, nullptr, N, puniq));
+    TRACED(KID_SEGSORT, segsort_unique_u64<<<grid_for(N, 128), 128, 0, st>>>(ssorted, poff, pcnt, nullptr, N, puniq, cap_sync));
     TRACED(KID_SCAN, scan_exclusive(puniq, puoff, nullptr, N, scan_tmp2, &ctr[6], st));
   }
   TRACED(KID_UNIT_COUNTS, k_unit_counts<<<grid_for(N, T), T, 0, st>>>(k, ucnt, dcnt));
@@ -293,7 +315,7 @@ int build_graph_impl(const LeoKernel* kk, const LeoCaps* caps, LeoEdges* out, Le
   TRACED(KID_LINK_COUNT, k_link<0><<<grid_for(N, T), T, 0, st>>>(k, la));
   TRACED(KID_SCAN, scan_exclusive(cand_cnt, cand_off, nullptr, N, scan_tmp, nullptr, st));
   TRACED(KID_LINK_FILL, k_link<1><<<grid_for(N, T), T, 0, st>>>(k, la));
-  TRACED(KID_SEGSORT, segsort_unique_u64<<<grid_for(N, 128), 128, 0, st>>>(cand, cand_off, cand_cnt, nullptr, N, uniq));
+  TRACED(KID_SEGSORT, segsort_unique_u64<<<grid_for(N, 128), 128, 0, st>>>(cand, cand_off, cand_cnt, nullptr, N, uniq, cap_cand));
   TRACED(KID_SCAN, scan_exclusive(uniq, eoff, nullptr, N, scan_tmp, &ctr[5], st));
   TRACED(KID_LINK_EMIT, k_link_emit<<<grid_for(N, T), T, 0, st>>>(k, cand_off, cand, uniq, eoff, *out, status));
 
@@ -333,12 +355,13 @@ int prune_impl(const LeoKernel* kk, const LeoProfile* pp, const LeoConfig* cfg, 
   {
     const int dbg = caps ? caps->debug_flags : 0;
     const size_t staged = prune_smem_bytes(k.N, k.B, 128, true), unstaged = prune_smem_bytes(k.N, k.B, 128, false);
-    if (dbg & LEO_DBG_NO_SMEM)
-      TRACED(KID_PRUNE, k_prune_edges<<<grid_for(cap_in, 128, num_sms() * 16), 128, 0, st>>>(k, p, a));
-    else if (staged <= (size_t)kSmemResidentMax)
+    // staged CFG image when it fits; otherwise the many-CTA global-memory
+    // kernel (thread per edge, no per-round CTA barriers) balances better
+    (void)unstaged;
+    if (!(dbg & LEO_DBG_NO_SMEM) && staged <= (size_t)kSmemResidentMax)
       TRACED(KID_PRUNE, k_prune_edges_smem<true><<<num_sms(), 128, staged, st>>>(k, p, a));
     else
-      TRACED(KID_PRUNE, k_prune_edges_smem<false><<<num_sms() * 2, 128, unstaged, st>>>(k, p, a));
+      TRACED(KID_PRUNE, k_prune_edges<<<grid_for(cap_in, 128, num_sms() * 16), 128, 0, st>>>(k, p, a));
   }
   TRACED(KID_PRUNE_SLOW, k_prune_slow<<<1, PW, 0, st>>>(k, p, a, slow_scr, PW));
   TRACED(KID_SCAN, scan_exclusive(keep, pos, in->count, cap_in, scan_tmp, nullptr, st));
@@ -370,7 +393,7 @@ Incoming build_incoming(IncomingBufs& b, int N, const LeoEdges* e, bool with_syn
     TRACED(KID_SYNC_HIST, k_sync_hist<<<grid_for(e->capacity, 256), 256, 0, st>>>(e->cons, e->n_regular, e->count, b.scnt));
     TRACED(KID_SCAN, scan_exclusive(b.scnt, b.soff, nullptr, N, b.tmp, nullptr, st));
     TRACED(KID_SYNC_FILL, k_sync_fill<<<grid_for(e->capacity, 256), 256, 0, st>>>(e->cons, e->n_regular, e->count, b.soff, b.scur, b.sidx));
-    TRACED(KID_SEGSORT, segsort_unique_u64<<<grid_for(N, 128), 128, 0, st>>>(b.sidx, b.soff, b.scnt, nullptr, N, b.uniq));
+    TRACED(KID_SEGSORT, segsort_unique_u64<<<grid_for(N, 128), 128, 0, st>>>(b.sidx, b.soff, b.scnt, nullptr, N, b.uniq, e->capacity));
   } else {
     cudaMemsetAsync(b.soff, 0, (size_t)(N + 1) * 4, st);
   }
@@ -424,7 +447,7 @@ int blame_impl(const LeoKernel* kk, const LeoProfile* pp, const LeoEdges* pruned
   BlameArgs a{caps ? caps->debug_flags : 0, own, p, pruned->prod, pruned->meta, paths->dist, inc, binc.rbeg, binc.rend, base->prod, base->meta,
               ecount, self_sub, jtotal, jnsum, eoff, *out, slow_list, &ctr[0], cap_slow, status};
   TRACED(KID_BLAME_COUNT, k_blame<0><<<grid_for(N, 128), 128, 0, st>>>(k, a));
-  TRACED(KID_SELFBLAME_SLOW, k_selfblame_warp<<<num_sms(), 128, 4 * kSBWarpInts * 4, st>>>(k, a, slow2, &ctr[1]));
+  TRACED(KID_SELFBLAME_WARP, k_selfblame_warp<<<num_sms(), 128, 4 * kSBWarpInts * 4, st>>>(k, a, slow2, &ctr[1]));
   TRACED(KID_SELFBLAME_SLOW, k_selfblame_slow<<<1, BW, 0, st>>>(k, a, slow2, &ctr[1], slow_scr, BW));
   TRACED(KID_SCAN, scan_exclusive(ecount, eoff, nullptr, N, scan_tmp, nullptr, st));
   TRACED(KID_BLAME_FILL, k_blame<1><<<grid_for(N, 128), 128, 0, st>>>(k, a));
@@ -586,7 +609,7 @@ int leo_analyze(const LeoKernel* k, const LeoProfile* p, const LeoSamples* sampl
   SidePool& sp = side_pool();
   LeoTrace* tr = caps ? caps->trace : nullptr;
   // stage-0 binning only feeds pruning and blame: run it beside build_graph
-  const bool fork = tr == nullptr || (tr->mode & 1);
+  const bool fork = (tr == nullptr || (tr->mode & 1)) && !no_fork_env();
   if (samples) {
     cudaStream_t s_bin = fork ? sp.s[1] : st;
     if (fork) link_streams(st, s_bin, sp.e[2]);

@@ -178,13 +178,15 @@ LEO_DEV void shell_sort_u64(uint64_t* a, int n) {
 }
 
 // Sort keys[begin[s] .. begin[s]+len[s]) ascending, drop duplicates in place,
-// write the unique count to uniq[s].
+// write the unique count to uniq[s].  Segments reaching past `cap` (the
+// producer overflowed its buffer and flagged it) are left empty.
 __global__ void segsort_unique_u64(uint64_t* __restrict__ keys, const int32_t* __restrict__ begin,
                                    const int32_t* __restrict__ len, const int32_t* nseg_dev, int nseg_cap,
-                                   int32_t* __restrict__ uniq) {
+                                   int32_t* __restrict__ uniq, int64_t cap) {
   int nseg = nseg_dev ? *nseg_dev : nseg_cap;
   for (int s = blockIdx.x * blockDim.x + threadIdx.x; s < nseg; s += gridDim.x * blockDim.x) {
     int n = len[s];
+    if ((int64_t)begin[s] + n > cap) { uniq[s] = 0; continue; }
     uint64_t* a = keys + begin[s];
     if (n <= 1) { uniq[s] = n; continue; }
     if (n <= 24) {

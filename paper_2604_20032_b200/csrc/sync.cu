@@ -296,8 +296,11 @@ __global__ void k_sync_wc_warp(KView k, SyncArgs a, const int32_t* __restrict__ 
     __syncwarp();
     int head = 0;
     while (true) {
+      // every lane reads the loop control before any lane can modify it
       const int tail = c[0];
-      if (head >= tail || c[2]) break;
+      const bool stop = head >= tail || c[2];
+      __syncwarp();
+      if (stop) break;
       for (int r = head + lane; r < tail; r += 32) {
         const int b = blk[r];
         for (int q = k.pred_ptr[b]; q < k.pred_ptr[b + 1]; q++) {

@@ -23,6 +23,7 @@ ap.add_argument("--scale", type=float, default=1.0)
 ap.add_argument("--flags", type=int, default=0)
 ap.add_argument("--timeline", action="store_true")
 ap.add_argument("--phases", action="store_true")
+ap.add_argument("--debug-guard", action="store_true")
 args = ap.parse_args()
 
 dev = torch.device("cuda:0")
@@ -96,3 +97,12 @@ if args.phases:
     order = np.argsort(-it)[:12]
     print("slowest waitcnt items (t*2+counter, cycles):", [(int(x), int(it[x])) for x in order])
     print("item cycles: sum", int(it.sum()), "count>0", int((it > 0).sum()), "p50", int(np.median(it[it > 0])))
+
+if args.debug_guard:
+    import numpy as np
+    import ctypes as C
+    from paper_2604_20032_b200._lib import lib
+    it = np.zeros(16, dtype=np.int64)
+    lib().leo_debug_items.argtypes = [C.c_void_p, C.c_int32]
+    lib().leo_debug_items(it.ctypes.data_as(C.c_void_p), 16)
+    print("guard record:", it[:8].tolist())
