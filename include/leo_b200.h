@@ -282,6 +282,34 @@ int leo_events_destroy(int32_t n, void** events);
  * into `p->lat` / `p->cls_cnt` (which must then be writable), build_graph,
  * run_pruning, slice, attribute_blame(pruned, base) and the per-line rollup,
  * all stream-ordered with no host synchronisation. */
+/* ---- report assembly on device outputs (report.py:96-199, analysis.py:499-561)
+ * single_dep_coverage before (base graph minus sync edges) and after (pruned),
+ * rank_hotspots, per-hotspot cause order and trace_chain.  Blame entries must
+ * be the ones leo_analyze / leo_blame produced (grouped by stalled instruction
+ * in increasing order).  Variable-size results use the given capacities; a
+ * hotspot with more than max_causes entries sets LEO_ST_SCRATCH_OVERFLOW and
+ * reports its true count in n_causes. */
+typedef struct LeoReport {
+  int32_t  top_n;             /* hotspots wanted (<= 4096 on the device path) */
+  int32_t  include_unsampled; /* zero-stall instructions after the sampled ones */
+  int32_t  chain_depth;       /* trace_chain max_depth (hops incl. the start) */
+  int32_t  max_causes;        /* capacity of each hotspot's cause list */
+  int32_t* coverage;          /* [4] nodes/qualified before, nodes/qualified after */
+  int32_t* n_hot;             /* [1] */
+  int32_t* hot;               /* [top_n] instruction indices, ranked */
+  int32_t* n_causes;          /* [top_n] */
+  int32_t* causes;            /* [top_n * max_causes] blame entry indices, report order */
+  int32_t* chain_len;         /* [top_n] hops incl. the start */
+  int32_t* chain_node;        /* [top_n * chain_depth] instruction of each hop */
+  int32_t* chain_entry;       /* [top_n * chain_depth] entry that reached the hop (-1: start) */
+  int32_t* chain_self;        /* [top_n] self-blame entry ending the chain, -1 none */
+} LeoReport;
+
+/* replaces report.build_report's assembly (report.py:132-199) after the
+ * analysis: all outputs stay on the device, stream-ordered. */
+int leo_report(const LeoKernel* k, const LeoProfile* p, const LeoEdges* base, const LeoEdges* pruned,
+               const LeoBlame* blame, LeoReport* out, uint32_t* status, void* stream);
+
 int leo_analyze(const LeoKernel* k, const LeoProfile* p, const LeoSamples* samples,
                 const LeoConfig* cfg, const LeoCaps* caps, LeoEdges* base, LeoEdges* pruned,
                 LeoPaths* paths, LeoDiags* diags, LeoBlame* blame, uint32_t* slice_bitmap,

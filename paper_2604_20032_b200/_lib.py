@@ -52,6 +52,9 @@ def lib():
                               C.POINTER(abi.LeoEdges), C.POINTER(abi.LeoPaths),
                               C.POINTER(abi.LeoDiags), C.POINTER(abi.LeoBlame), P, P, P,
                               C.c_int32, P, P, P, P]
+    L.leo_report.argtypes = [C.POINTER(abi.LeoKernel), C.POINTER(abi.LeoProfile),
+                             C.POINTER(abi.LeoEdges), C.POINTER(abi.LeoEdges),
+                             C.POINTER(abi.LeoBlame), C.POINTER(abi.LeoReport), P, P]
     L.leo_kernel_name.argtypes = [C.c_int]
     L.leo_debug_phases.argtypes = [C.c_int32, P, C.c_int32]
     L.leo_debug_phases.restype = C.c_int
@@ -62,7 +65,7 @@ def lib():
     for f in ("leo_events_create", "leo_events_elapsed", "leo_events_destroy"):
         getattr(L, f).restype = C.c_int
     for f in ("leo_bin_samples", "leo_build_graph", "leo_prune", "leo_slice", "leo_blame",
-              "leo_analyze"):
+              "leo_analyze", "leo_report"):
         getattr(L, f).restype = C.c_int
     _lib = L
     return L

@@ -86,6 +86,13 @@ class LeoBlame(C.Structure):
                 ("blame", P), ("factors", P), ("count", P)]
 
 
+class LeoReport(C.Structure):
+    _fields_ = [("top_n", C.c_int32), ("include_unsampled", C.c_int32), ("chain_depth", C.c_int32),
+                ("max_causes", C.c_int32), ("coverage", P), ("n_hot", P), ("hot", P),
+                ("n_causes", P), ("causes", P), ("chain_len", P), ("chain_node", P),
+                ("chain_entry", P), ("chain_self", P)]
+
+
 DIAG_UNRESOLVED, DIAG_WAITCNT, DIAG_NO_SETTER, DIAG_PATH_CAPPED = 1, 2, 3, 4
 ST_EDGE_OVERFLOW, ST_PATH_OVERFLOW, ST_DIAG_OVERFLOW = 1, 2, 4
 ST_BLAME_OVERFLOW, ST_SCRATCH_OVERFLOW, ST_BAD_INPUT = 8, 16, 32

@@ -31,7 +31,7 @@ import weakref
 import numpy as np
 import torch
 
-from . import abi, device, diagnostics, soa, types
+from . import abi, device, diagnostics, report, soa, types
 from . import enums as E
 
 _DEVICE = None
@@ -437,3 +437,38 @@ class Session:
         torch.cuda.current_stream(self.dev).synchronize()
         self.last_d2h = sum(t.numel() * t.element_size() for t in out.values()) + c.nbytes
         return {k: v.numpy() for k, v in out.items()}
+
+
+# --------------------------------------------------------------------------
+# report assembly on device outputs (report.py:128-213)
+
+def build_report_soa(ks, prof, config, meta, top_n: int = 10, include_unsampled: bool = False,
+                     chain_depth: int = 32, samples=None, dev=None, R=None):
+    """StallReport of one kernel given as SoA + ReportMeta (the analysis, the
+    coverage, the ranking, the cause order and the chains run on the device;
+    the host formats)."""
+    dev = torch.device(dev) if dev is not None else _dev()
+    dk = device.DeviceKernel(ks, dev)
+    dp = device.DeviceProfile(prof, ks.n_instr, dev)
+    ds = device.DeviceSamples(*samples, dev) if samples is not None else None
+    an = device.Analyzer(dk, dev)
+    an.run(dp, _config_of(config, ks.dialect), ds)
+    r = an.result()
+    r["lat"] = dp.lat.cpu().numpy()
+    r["cls_cnt"] = dp.cls_cnt.cpu().numpy().reshape(-1, 8)
+    rep = an.report(dp, top_n, include_unsampled, chain_depth)
+    bdiag, pdiag = _split_diags(ks, r)
+    diags = tuple(ks.prefix_diagnostics) + tuple(bdiag) + tuple(pdiag)
+    return report.assemble(ks, meta, r, rep, diags, R)
+
+
+def build_report(cfg, profile, config, top_n: int = 10, include_unsampled: bool = False,
+                 chain_depth: int = 32):
+    """report.build_report (report.py:128-213) with the analysis and the report
+    assembly on the GPU; takes and returns the reference's objects."""
+    import sys
+    attach = sys.modules[type(profile).__module__].attach      # profile.attach (profile.py)
+    attached = attach(cfg, profile)
+    ks, prof = soa.encode_attached(attached)
+    meta = report.meta_from_reference(cfg, profile, config)
+    return build_report_soa(ks, prof, config, meta, top_n, include_unsampled, chain_depth)

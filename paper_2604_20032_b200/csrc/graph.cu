@@ -284,8 +284,10 @@ __host__ __device__ inline size_t reach_unit_smem(int B, int threads) {
          + carve_bytes((size_t)kRUStack * threads, 4) + carve_bytes((size_t)kRURes * threads, 4);
 }
 
+// `parts` CTAs share one unit (each takes every parts-th query) so that
+// kernels with few register units still fill the chip.
 __global__ void k_reach_unit(KView k, ReachArgs a, const int32_t* __restrict__ qtab,
-                             const int32_t* __restrict__ rh_g) {
+                             const int32_t* __restrict__ rh_g, int parts) {
   extern __shared__ __align__(16) unsigned char sm_raw[];
   __shared__ int nq, rbase;
   __shared__ int swarp[33];
@@ -306,7 +308,8 @@ __global__ void k_reach_unit(KView k, ReachArgs a, const int32_t* __restrict__ q
   StageBar sb;
   sb.init(bar);
   bool first = true;
-  for (int u = blockIdx.x; u < k.U; u += gridDim.x) {
+  const int part = blockIdx.x % parts;
+  for (int u = blockIdx.x / parts; u < k.U; u += gridDim.x / parts) {
     sb.begin();
     if (first) {
       const int E = k.pred_ptr[B];          // <= 2 per block ([target, fallthrough])
@@ -347,13 +350,22 @@ __global__ void k_reach_unit(KView k, ReachArgs a, const int32_t* __restrict__ q
     }
     __syncthreads();
     pm.mark(0, 2);
-    for (int y = tid; y < B; y += T)
-      if (qs[y] >= 0) ql[atomicAdd(&nq, 1)] = y;
+    // ordered compaction of the unit's query blocks (every CTA sharing the
+    // unit derives the same list, then takes its share of it)
+    {
+      const int per = (B + T - 1) / T, lo = min(B, tid * per), hi = min(B, lo + per);
+      int cnt = 0;
+      for (int y = lo; y < hi; y++) cnt += qs[y] >= 0;
+      int tot;
+      int pos = block_excl_scan(cnt, swarp, &tot);
+      for (int y = lo; y < hi; y++) if (qs[y] >= 0) ql[pos++] = y;
+      if (tid == 0) nq = tot;
+    }
     __syncthreads();
     pm.mark(0, 3);
     const int n = nq;
     // rounds of T queries; one global reservation per CTA per round
-    for (int base = 0; base < n; base += T) {
+    for (int base = part * T; base < n; base += T * parts) {
       const int t = base + tid;
       int e = -1, nres = 0;
       bool ovf = false;

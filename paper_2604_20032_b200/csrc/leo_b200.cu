@@ -14,6 +14,7 @@
 #include "sync.cu"
 #include "prune.cu"
 #include "blame.cu"
+#include "report.cu"
 
 
 using namespace leo;
@@ -293,11 +294,13 @@ int build_graph_impl(const LeoKernel* kk, const LeoCaps* caps, LeoEdges* out, Le
   ReachArgs ra{caps ? caps->debug_flags : 0, ldtab, brec, U, Bp, q_block, q_unit, q_off, q_len, qres, cap_qres, &ctr[1],
                slow_list, &ctr[2], NU + 1024, status};
   const int dbg = caps ? caps->debug_flags : 0;
-  const int ru_threads = 128;
+  int ru_threads = 128;
+  while (ru_threads > 32 && reach_unit_smem(B, ru_threads) > (size_t)kSmemResidentMax) ru_threads >>= 1;
   const size_t ru_smem = reach_unit_smem(B, ru_threads);
+  const int ru_parts = std::max(1, std::min(8, (2 * SM + U - 1) / std::max(U, 1)));
   if (B > 0 && U > 0 && ru_smem <= (size_t)kSmemResidentMax && !(dbg & LEO_DBG_NO_SMEM)) {
     // tier 0: the CFG and one unit's columns resident in shared memory, CTA per unit
-    TRACED(KID_REACH_FAST, k_reach_unit<<<std::min(U, SM * 8), ru_threads, ru_smem, st>>>(k, ra, qtab, rhead));
+    TRACED(KID_REACH_FAST, k_reach_unit<<<std::min(U, SM * 8) * ru_parts, ru_threads, ru_smem, st>>>(k, ra, qtab, rhead, ru_parts));
   } else {
     // tier 1 is persistent: enough CTAs to fill the chip, queries fetched dynamically
     TRACED(KID_REACH_FAST, k_reach_fast<<<std::max(1, std::min<int>(grid_for(NU, kT1Threads), SM * 3)), kT1Threads,
@@ -596,6 +599,41 @@ int leo_blame(const LeoKernel* k, const LeoProfile* p, const LeoEdges* pruned, c
                      status, st);
   ar.release();
   return r;
+}
+
+int leo_report(const LeoKernel* k, const LeoProfile* p, const LeoEdges* base, const LeoEdges* pruned,
+               const LeoBlame* blame, LeoReport* r, uint32_t* status, void* stream) {
+  WsScope ws_scope(nullptr);
+  if (int e = check_kernel(k)) return e;
+  if (!r || r->top_n < 0 || r->top_n > 4096 || r->chain_depth < 0 || r->max_causes < 0) return -3;
+  cudaStream_t st = (cudaStream_t)stream;
+  const int N = k->n_instr;
+  Arena ar{st};
+  int32_t *mask, *cnt;
+  ar.want(&mask, N); ar.want(&cnt, N);
+  LEO_CUDA_CHECK(ar.commit());
+  cudaMemsetAsync(r->coverage, 0, 4 * sizeof(int32_t), st);
+  const int T = 256;
+  // before: base graph minus sync edges (the raw/guard prefix, report.py:135-137)
+  cudaMemsetAsync(mask, 0, (size_t)std::max(N, 1) * 4, st);
+  cudaMemsetAsync(cnt, 0, (size_t)std::max(N, 1) * 4, st);
+  k_cov_edges<<<grid_for(base->capacity, T), T, 0, st>>>(base->cons, base->meta, base->n_regular, base->capacity, mask, cnt);
+  k_cov_nodes<<<grid_for(N, T, num_sms() * 4), T, 0, st>>>(N, mask, cnt, r->coverage);
+  // after: every pruned edge
+  cudaMemsetAsync(mask, 0, (size_t)std::max(N, 1) * 4, st);
+  cudaMemsetAsync(cnt, 0, (size_t)std::max(N, 1) * 4, st);
+  k_cov_edges<<<grid_for(pruned->capacity, T), T, 0, st>>>(pruned->cons, pruned->meta, pruned->count, pruned->capacity, mask, cnt);
+  k_cov_nodes<<<grid_for(N, T, num_sms() * 4), T, 0, st>>>(N, mask, cnt, r->coverage + 2);
+  k_report_rank<<<1, 1024, 0, st>>>(N, p->lat, r->top_n, r->include_unsampled, r->hot, r->n_hot);
+  if (r->top_n > 0) {
+    ReportArgs a{r->n_hot, r->hot, blame->stalled, blame->edge, blame->blame, blame->count, blame->capacity,
+                 pruned->prod, r->max_causes, r->chain_depth, r->n_causes, r->causes, r->chain_len,
+                 r->chain_node, r->chain_entry, r->chain_self, status};
+    k_report_hot<<<r->top_n, 32, 0, st>>>(a);
+  }
+  ar.release();
+  LEO_CUDA_CHECK(cudaGetLastError());
+  return 0;
 }
 
 int leo_analyze(const LeoKernel* k, const LeoProfile* p, const LeoSamples* samples, const LeoConfig* cfg,

@@ -317,6 +317,40 @@ class Analyzer:
             status=int(np.uint32(c[C_STATUS])))
 
 
+    def report(self, dp: DeviceProfile, top_n: int = 10, include_unsampled: bool = False,
+               chain_depth: int = 32) -> dict:
+        """leo_report on the buffers of the last analysis (report assembly on
+        the device: coverage, hotspot ranking, cause order, trace_chain)."""
+        if not 0 <= top_n <= 4096:
+            raise ValueError("top_n must be in [0, 4096] on the device report path")
+        d, L = self.device, lib()
+        max_causes = 16
+        for _ in range(8):
+            i32 = lambda m: torch.zeros(max(m, 1), dtype=torch.int32, device=d)  # noqa: E731
+            cov, n_hot, hot = i32(4), i32(1), i32(top_n)
+            n_causes, causes = i32(top_n), i32(top_n * max_causes)
+            chain_len, chain_self = i32(top_n), i32(top_n)
+            chain_node, chain_entry = i32(top_n * chain_depth), i32(top_n * chain_depth)
+            status = i32(1)
+            rs = abi.LeoReport(top_n, int(include_unsampled), chain_depth, max_causes, ptr(cov),
+                               ptr(n_hot), ptr(hot), ptr(n_causes), ptr(causes), ptr(chain_len),
+                               ptr(chain_node), ptr(chain_entry), ptr(chain_self))
+            st = torch.cuda.current_stream(d)
+            check(L.leo_report(C.byref(self.dk.struct), C.byref(dp.struct), C.byref(self.s_base),
+                               C.byref(self.s_pruned), C.byref(self.s_blame), C.byref(rs),
+                               ptr(status), st.cuda_stream), "leo_report")
+            nc = n_causes.cpu().numpy()
+            if int(status.item()) == 0:
+                break
+            max_causes = int(nc.max()) + 1
+        h = lambda t: t.cpu().numpy()  # noqa: E731
+        return dict(coverage=h(cov), n_hot=int(n_hot.item()), hot=h(hot), n_causes=nc,
+                    causes=h(causes).reshape(max(top_n, 1), max_causes),
+                    chain_len=h(chain_len), chain_node=h(chain_node).reshape(max(top_n, 1), chain_depth),
+                    chain_entry=h(chain_entry).reshape(max(top_n, 1), chain_depth),
+                    chain_self=h(chain_self))
+
+
 def analyze_soa(ks, prof, cfg: abi.LeoConfig | None = None, samples=None, device="cuda",
                 debug_flags: int = 0) -> dict:
     """One-shot convenience: upload, run, download."""
