@@ -291,7 +291,15 @@ def run_ours(args, ws, rank, local):
     torch.cuda.synchronize()
     breakdown = tracer.summary()
     n_launch = sum(3 if k == "scan" else 1 for k, _ in tracer.records())
-    dominant = max(breakdown, key=breakdown.get)
+    # dominant kernel = the longest single launch among kernels with a byte
+    # model (scan / segsort are many differently-sized launches)
+    recs = tracer.records()
+    n_of = {}
+    for k, _ in recs:
+        n_of[k] = n_of.get(k, 0) + 1
+    per_launch = {k: ms for k, ms in recs
+                  if n_of[k] == 1 and roofline.kernel_bytes(k, ks, wl0, eager) is not None}
+    dominant = max(per_launch, key=per_launch.get) if per_launch else max(breakdown, key=breakdown.get)
     tracer.reset(only_kernel=device.kernel_id(dominant))
     an0.set_tracer(None)
 

@@ -62,7 +62,10 @@ def kernel_bytes(name: str, ks, wl, res) -> int | None:
         "link_fill": 4 * z["M"] + 4 * z["NU"] + 8 * z["NU"],
         "segsort_unique": 16 * z["NU"] + 4 * N,
         "lines": 16 * z["NB"] + 8 * z["L"] + 8 * N,
-        "reach_fast": 8 * z["NU"],
+        # dense last-def + query tables read once (unit columns), CFG, results
+        "reach_fast": 8 * z["B"] * int(ks.n_units) + 4 * z["B"] + 12 * z["CE"] + 12 * z["NU"],
+        # base-graph RAW incoming of the candidates + per-candidate verdicts
+        "selfblame_warp": 12 * z["E"] + 8 * N,
     }
     v = table.get(name)
     return int(v) if v is not None else None
