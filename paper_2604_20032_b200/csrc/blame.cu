@@ -284,6 +284,9 @@ LEO_DEV int traces_to_load(const KView& k, const int32_t* brbeg, const int32_t* 
   int n = 1, lo = 0, hi = 1;
   seen[0] = index;
   if (stamp) stamp[index] = stamp_val;
+  // 64-bit presence filter in a register: most discoveries are new and skip
+  // the linear scan of `seen` (local memory) entirely
+  uint64_t filt = 1ull << (((uint32_t)index * 2654435761u) >> 26);
   for (int depth = 0; depth < 8; depth++) {
     for (int a = lo; a < hi; a++) {
       const int node = seen[a];
@@ -291,12 +294,14 @@ LEO_DEV int traces_to_load(const KView& k, const int32_t* brbeg, const int32_t* 
         if (((bmeta[e] >> 27) & 7) != LEO_EK_RAW) continue;
         const int p = bprod[e];
         bool dup = false;
+        const uint64_t fb = 1ull << (((uint32_t)p * 2654435761u) >> 26);
         if (stamp) dup = stamp[p] == stamp_val;
-        else for (int x = 0; x < n; x++) if (seen[x] == p) { dup = true; break; }
+        else if (filt & fb) for (int x = 0; x < n; x++) if (seen[x] == p) { dup = true; break; }
         if (dup) continue;
         if (kMemoryProducer & BIT(k.opclass[p])) return 1;
         if (n == cap) return -1;
         seen[n++] = p;
+        filt |= fb;
         if (stamp) stamp[p] = stamp_val;
       }
     }

@@ -266,10 +266,14 @@ int build_graph_impl(const LeoKernel* kk, const LeoCaps* caps, LeoEdges* out, Le
     TRACED(KID_SYNC_PACK, k_wait_list<<<grid_for(N, T), T, 0, st>>>(k, own, wlist, &ctr[8]));
     SyncArgs sa{caps ? caps->debug_flags : 0, skeys, cap_sync, &ctr[3], slow2, &ctr[4], cap_slow, *diags, status,
                 wcword, setword, lastset, n_ids, wlist, &ctr[8], wclist, &ctr[10]};
-    const size_t wc_smem = sync_smem_bytes(N, B, 128);
+    // as many threads per CTA as the image allows: more warps hide the
+    // shared-memory latency of the event-list build and spread the items
+    int wc_threads = 512;
+    while (wc_threads > 128 && sync_smem_bytes(N, B, wc_threads) > (size_t)kSmemResidentMax) wc_threads >>= 1;
+    const size_t wc_smem = sync_smem_bytes(N, B, wc_threads);
     const int dbg_flags = caps ? caps->debug_flags : 0;
     if (k.dialect == LEO_AMD && B > 0 && wc_smem <= (size_t)kSmemResidentMax && !(dbg_flags & LEO_DBG_NO_SMEM))
-      TRACED(KID_SYNC, k_sync_wc_smem<<<SM, 128, wc_smem, st>>>(k, sa, bev));
+      TRACED(KID_SYNC, k_sync_wc_smem<<<SM, wc_threads, wc_smem, st>>>(k, sa, bev));
     else
       TRACED(KID_SYNC, k_sync<false><<<grid_for(N, 64), 64, 0, st>>>(k, sa, nullptr, 0));
     if (k.dialect == LEO_AMD)

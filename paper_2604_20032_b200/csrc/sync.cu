@@ -120,6 +120,7 @@ struct WcState {
   uint32_t member_bit;
   int32_t seen[kWcSeen];
   int nseen = 0;
+  uint64_t filt = 0;
   const SyncArgs* sa = nullptr;
   uint64_t* cbuf = nullptr;   // optional CTA buffer in shared memory (one global reservation per CTA)
   int* ccnt = nullptr;
@@ -157,11 +158,15 @@ LEO_DEV int wc_visit(uint32_t w, int x, WcState& s, int& m, int& a, const SyncAr
   } else if (w & s.member_bit) {
     if (a != 0) {
       if (m >= s.level) {   // pending[level:] -> edge (buffered, deduplicated per batch)
+        // register presence filter first: most members are new to the batch
+        const uint64_t fb = 1ull << (((uint32_t)x * 2654435761u) >> 26);
         bool dup = false;
-        for (int t = 0; t < s.nseen; t++) if (s.seen[t] == x) { dup = true; break; }
+        if (s.filt & fb)
+          for (int t = 0; t < s.nseen; t++) if (s.seen[t] == x) { dup = true; break; }
         if (!dup) {
-          if (s.nseen == kWcSeen) s.flush();
+          if (s.nseen == kWcSeen) { s.flush(); s.filt = 0; }
           s.seen[s.nseen++] = x;
+          s.filt |= fb;
         }
       }
       m++;
@@ -623,8 +628,40 @@ __global__ void k_sync(KView k, SyncArgs a, char* scratch, int nworkers) {
 // Block scan with the per-block event flag: a block without events for the
 // counter only spends budget (same stop rule as wc_scan: a chain stops when it
 // would visit an instruction with no budget left).
+// Per-block event lists (shared memory): for counter c, the instructions of
+// block b the visitor reacts to, as offsets from the block's first
+// instruction, ascending: rel[c][ptr[c][b] .. ptr[c][b+1]).
+struct EvList {
+  const int32_t* ptr[2];
+  const uint16_t* rel[2];
+  const int32_t* bf;
+  const uint32_t* ww;
+};
+
 LEO_DEV int wc_scan_blk(const SyncArgs& sa, const uint32_t* bev, int blk, int hi, int lo, int& budget,
-                        WcState& s, int& m, int& a) {
+                        WcState& s, int& m, int& a, const EvList* ev = nullptr) {
+  if (ev) {
+    // visit only the events in [lo, hi], youngest first; the instructions in
+    // between only spend budget (a chain stops before visiting an
+    // instruction with no budget left, as in wc_scan)
+    const int c = s.counter, base = ev->bf[blk], B0 = budget;
+    const int e0 = ev->ptr[c][blk];
+    for (int e = ev->ptr[c][blk + 1] - 1; e >= e0; e--) {
+      const int x = base + ev->rel[c][e];
+      if (x > hi) continue;
+      if (x < lo) break;
+      const int used = hi - x + 1;
+      if (B0 < used) { budget = 0; return 0; }
+      budget = B0 - used;
+      const int r = wc_visit(ev->ww[x], x, s, m, a, sa);
+      if (r <= 0) return r;
+    }
+    const int len = hi - lo + 1;
+    if (len <= 0) { budget = B0; return 1; }
+    if (B0 >= len) { budget = B0 - len; return 1; }
+    budget = 0;
+    return 0;
+  }
   if (!((bev[blk] >> s.counter) & 1)) {
     const int len = hi - lo + 1;
     if (len <= 0) return 1;
@@ -640,7 +677,7 @@ LEO_DEV int wc_scan_blk(const SyncArgs& sa, const uint32_t* bev, int blk, int hi
 // T words), set on push and cleared on pop.
 LEO_DEV bool trace_waitcnt_bits(const KView& k, const uint32_t* bev, uint32_t* pb, int T, int wait, int counter,
                                 int level, const SyncArgs& sa, Frame* fr, int fcap, int& best_m, int max_steps,
-                                uint64_t* cbuf, int* ccnt, int ccap) {
+                                uint64_t* cbuf, int* ccnt, int ccap, const EvList* ev) {
   auto bit = [&](int b) -> bool { return (pb[(b >> 5) * T] >> (b & 31)) & 1u; };
   auto setb = [&](int b) { pb[(b >> 5) * T] |= 1u << (b & 31); };
   auto clrb = [&](int b) { pb[(b >> 5) * T] &= ~(1u << (b & 31)); };
@@ -651,7 +688,7 @@ LEO_DEV bool trace_waitcnt_bits(const KView& k, const uint32_t* bev, uint32_t* p
   s.nseen = 0; s.sa = &sa; s.cbuf = cbuf; s.ccnt = ccnt; s.ccap = ccap;
   const int b0 = k.block_of[wait];
   int m = 0, a = -1, budget = kSyncBudget;
-  int r = wc_scan_blk(sa, bev, b0, wait - 1, k.blk_first[b0], budget, s, m, a);
+  int r = wc_scan_blk(sa, bev, b0, wait - 1, k.blk_first[b0], budget, s, m, a, ev);
   if (r < 0) return false;
   best_m = 0;
   if (r == 0) { best_m = m; return true; }
@@ -675,7 +712,7 @@ LEO_DEV bool trace_waitcnt_bits(const KView& k, const uint32_t* bev, uint32_t* p
     if (p < 0) { clrb(f.blk); top--; continue; }
     if (++steps > max_steps) return bail();
     m = f.m; a = f.a; budget = f.budget;
-    r = wc_scan_blk(sa, bev, p, k.blk_last[p], k.blk_first[p], budget, s, m, a);
+    r = wc_scan_blk(sa, bev, p, k.blk_last[p], k.blk_first[p], budget, s, m, a, ev);
     if (r < 0) return bail();
     if (r == 0) { best_m = max(best_m, m); continue; }
     if (top == fcap) return bail();
@@ -700,7 +737,7 @@ constexpr int kWcSmemSteps = 4096;
 
 constexpr int kWcCtaKeys = 1024;
 __host__ __device__ inline size_t sync_smem_bytes(int N, int B, int threads) {
-  return 16 + 8 * kWcCtaKeys + carve_bytes(N, 4) + carve_bytes(B, 4) * 3 + carve_bytes(B + 1, 4) + carve_bytes(2 * (size_t)B + 4, 4)
+  return 16 + 8 * kWcCtaKeys + 2 * carve_bytes(B + 1, 4) + 2 * carve_bytes(N, 2) + carve_bytes(N, 4) + carve_bytes(B, 4) * 3 + carve_bytes(B + 1, 4) + carve_bytes(2 * (size_t)B + 4, 4)
          + carve_bytes((size_t)((B + 31) >> 5) * threads, 4);
 }
 
@@ -720,6 +757,13 @@ __global__ void k_sync_wc_smem(KView k, SyncArgs a, const uint32_t* __restrict__
   uint32_t* bev4 = cv.take<uint32_t>(B);
   const int T = blockDim.x, W = (B + 31) >> 5;
   uint32_t* pbits = cv.take<uint32_t>((size_t)W * T);
+  int32_t* evp0 = cv.take<int32_t>(B + 1);
+  int32_t* evp1 = cv.take<int32_t>(B + 1);
+  uint16_t* evr0 = cv.take<uint16_t>(N);
+  uint16_t* evr1 = cv.take<uint16_t>(N);
+  __shared__ int swarp[33];
+  __shared__ int ev_ok;
+  if (threadIdx.x == 0) ev_ok = 1;
   for (int x = threadIdx.x; x < W * T; x += T) pbits[x] = 0u;
   PhaseMarks pm(a.dbg);
   StageBar sb;
@@ -734,6 +778,49 @@ __global__ void k_sync_wc_smem(KView k, SyncArgs a, const uint32_t* __restrict__
   sb.commit_and_wait();
   pm.mark(1, 1);
   const uint32_t* bev = bev4;
+  // per-block event lists for both counters (count, scan, fill; in smem)
+  auto evbits = [](uint32_t w) -> uint32_t {
+    if (w & kWcIsWait)
+      return (w & kWcBig) ? 3u : (((w & 0x3FF) != kWcNone) ? 1u : 0u) | ((((w >> 10) & 0x3FF) != kWcNone) ? 2u : 0u);
+    return ((w & kWcVm) ? 1u : 0u) | ((w & kWcLgkm) ? 2u : 0u);
+  };
+  {
+    // counts: block per thread round-robin (neighbouring lanes read
+    // neighbouring instructions: few bank conflicts)
+    for (int b = threadIdx.x; b < B; b += T) {
+      if (bl[b] - bf[b] >= 65535) ev_ok = 0;
+      int c0 = 0, c1 = 0;
+      for (int x = bf[b]; x <= bl[b]; x++) { const uint32_t f = evbits(ww[x]); c0 += f & 1; c1 += f >> 1; }
+      evp0[b] = c0; evp1[b] = c1;
+    }
+    __syncthreads();
+    // exclusive scan of the counts (thread-contiguous chunks)
+    const int per = (B + T - 1) / T, lo = min(B, (int)threadIdx.x * per), hi = min(B, lo + per);
+    int s0 = 0, s1 = 0;
+    for (int b = lo; b < hi; b++) { s0 += evp0[b]; s1 += evp1[b]; }
+    int t0, t1;
+    int r0 = block_excl_scan(s0, swarp, &t0);
+    int r1 = block_excl_scan(s1, swarp, &t1);
+    for (int b = lo; b < hi; b++) {
+      const int c0 = evp0[b], c1 = evp1[b];
+      evp0[b] = r0; evp1[b] = r1;
+      r0 += c0; r1 += c1;
+    }
+    if (threadIdx.x == 0) { evp0[B] = t0; evp1[B] = t1; }
+    __syncthreads();
+    for (int b = threadIdx.x; b < B; b += T) {
+      int q0 = evp0[b], q1 = evp1[b];
+      for (int x = bf[b]; x <= bl[b]; x++) {
+        const uint32_t f = evbits(ww[x]);
+        if (f & 1) evr0[q0++] = (uint16_t)(x - bf[b]);
+        if (f & 2) evr1[q1++] = (uint16_t)(x - bf[b]);
+      }
+    }
+    __syncthreads();
+  }
+  pm.mark(1, 2);
+  EvList evl{{evp0, evp1}, {evr0, evr1}, bf, ww};
+  const EvList* ev = ev_ok ? &evl : nullptr;
   KView ks = k;
   ks.blk_first = bf; ks.blk_last = bl; ks.pred_ptr = pp; ks.pred = pr;
   SyncArgs as = a;
@@ -753,7 +840,7 @@ __global__ void k_sync_wc_smem(KView k, SyncArgs a, const uint32_t* __restrict__
       const long long c0 = clock64();
       const bool ok = !(a.dbg & LEO_DBG_SYNC_SLOW) && lv < kWcNone &&
                       trace_waitcnt_bits(ks, bev, pbits + threadIdx.x, T, i, counter, (int)lv, as, fr, kFrames,
-                                         best_m, kWcSmemSteps, kbuf, &kcnt, kWcCtaKeys);
+                                         best_m, kWcSmemSteps, kbuf, &kcnt, kWcCtaKeys, ev);
       if ((a.dbg & LEO_DBG_PHASES) && t < 4096) g_item_cycles[t * 2 + counter] = clock64() - c0;
       if (!ok) {
         const bool to_warp = lv < kWcNone && !(a.dbg & LEO_DBG_SYNC_SLOW);
@@ -776,7 +863,7 @@ __global__ void k_sync_wc_smem(KView k, SyncArgs a, const uint32_t* __restrict__
     if (kbase + x < a.key_cap) a.keys[kbase + x] = kbuf[x];
     else atomicOr(a.status, (uint32_t)LEO_ST_SCRATCH_OVERFLOW);
   }
-  pm.mark(1, 2);
+  pm.mark(1, 3);
 }
 
 template __global__ void k_sync<false>(KView, SyncArgs, char*, int);
