@@ -31,6 +31,7 @@ namespace leo {
 __global__ void k_bin_samples(int64_t S, const int32_t* __restrict__ pc, const uint8_t* __restrict__ cat,
                               const uint8_t* __restrict__ lut, int N, int32_t* __restrict__ cls_cnt,
                               uint32_t* status) {
+  pdl_wait();
   __shared__ uint8_t slut[256];
   for (int x = threadIdx.x; x < 256; x += blockDim.x) slut[x] = lut[x];
   __syncthreads();
@@ -77,6 +78,7 @@ LEO_DEV int64_t bin_chunk_per(int64_t S, int G) { return (((S + G - 1) / G) + 3)
 // pass 1: chunk-local bucket histogram -> M[c * nb + b]
 __global__ void __launch_bounds__(512) k_bin_hist(int64_t S, const int32_t* __restrict__ pc, int N, int nb, int R,
                                                   int32_t* __restrict__ M, uint32_t* status) {
+  pdl_wait();
   extern __shared__ int32_t h[];                 // nb
   for (int x = threadIdx.x; x < nb; x += blockDim.x) h[x] = 0;
   __syncthreads();
@@ -108,6 +110,7 @@ __global__ void __launch_bounds__(512) k_bin_hist(int64_t S, const int32_t* __re
 // pass 2a: CTA per bucket: exclusive scan of the bucket's chunk counts in
 // place (M[c][b] becomes the chunk's offset inside the bucket) + bucket total
 __global__ void k_bin_colscan(int nb, int G, int32_t* __restrict__ M, int32_t* __restrict__ tot) {
+  pdl_wait();
   __shared__ int sw[33];
   for (int b = blockIdx.x; b < nb; b += gridDim.x) {
     int carry = 0;
@@ -126,6 +129,7 @@ __global__ void k_bin_colscan(int nb, int G, int32_t* __restrict__ M, int32_t* _
 // pass 2b (single CTA): bucket offsets + slice offsets
 __global__ void k_bin_plan(int nb, int slice, const int32_t* __restrict__ bucket_cnt, int32_t* __restrict__ bucket_off,
                            int32_t* __restrict__ slice_off) {
+  pdl_wait();
   __shared__ int sw[33];
   int carry = 0, scarry = 0;
   for (int base = 0; base < nb; base += blockDim.x) {
@@ -146,6 +150,7 @@ __global__ void __launch_bounds__(512) k_bin_scatter(int64_t S, const int32_t* _
                                                      const uint8_t* __restrict__ lut, int N, int nb, int R,
                                                      const int32_t* __restrict__ M, const int32_t* __restrict__ bucket_off,
                                                      uint16_t* __restrict__ keys) {
+  pdl_wait();
   extern __shared__ int32_t cur[];               // nb cursors
   __shared__ uint8_t slut[256];
   for (int x = threadIdx.x; x < nb; x += blockDim.x) cur[x] = bucket_off[x] + M[(size_t)blockIdx.x * nb + x];
@@ -184,6 +189,7 @@ __global__ void __launch_bounds__(512) k_bin_count(int N, int nb, int R, int sli
                                                    const int32_t* __restrict__ slice_off,
                                                    const uint16_t* __restrict__ keys,
                                                    int32_t* __restrict__ cls_cnt) {
+  pdl_wait();
   extern __shared__ int32_t cnt[];              // R * 8
   const int total_slices = slice_off[nb];
   for (int sl = blockIdx.x; sl < total_slices; sl += gridDim.x) {
@@ -222,6 +228,7 @@ __global__ void __launch_bounds__(512) k_bin_count(int N, int nb, int R, int sli
 }
 
 __global__ void k_bin_finalize(int N, const int32_t* __restrict__ cls_cnt, int32_t* __restrict__ lat) {
+  pdl_wait();
   for (int j = blockIdx.x * blockDim.x + threadIdx.x; j < N; j += gridDim.x * blockDim.x) {
     const int4* row = reinterpret_cast<const int4*>(cls_cnt + (size_t)j * 8);
     int4 a = row[0], b = row[1];
@@ -233,6 +240,7 @@ __global__ void k_bin_finalize(int N, const int32_t* __restrict__ cls_cnt, int32
 // regular (raw/guard) edges [0, n_reg) are sorted by consumer
 __global__ void k_seg_bounds(const int32_t* __restrict__ cons, const int32_t* n_reg_dev,
                              int32_t* __restrict__ rbeg, int32_t* __restrict__ rend) {
+  pdl_wait();
   const int n = *n_reg_dev;
   for (int e = blockIdx.x * blockDim.x + threadIdx.x; e < n; e += gridDim.x * blockDim.x) {
     int c = cons[e];
@@ -243,6 +251,7 @@ __global__ void k_seg_bounds(const int32_t* __restrict__ cons, const int32_t* n_
 // sync edges [n_reg, n) : histogram by consumer
 __global__ void k_sync_hist(const int32_t* __restrict__ cons, const int32_t* n_reg_dev, const int32_t* n_dev,
                             int32_t* __restrict__ cnt) {
+  pdl_wait();
   const int r = *n_reg_dev, n = *n_dev;
   for (int e = r + blockIdx.x * blockDim.x + threadIdx.x; e < n; e += gridDim.x * blockDim.x)
     atomicAdd(&cnt[cons[e]], 1);
@@ -250,6 +259,7 @@ __global__ void k_sync_hist(const int32_t* __restrict__ cons, const int32_t* n_r
 __global__ void k_sync_fill(const int32_t* __restrict__ cons, const int32_t* n_reg_dev, const int32_t* n_dev,
                             const int32_t* __restrict__ off, int32_t* __restrict__ cursor,
                             uint64_t* __restrict__ out) {
+  pdl_wait();
   const int r = *n_reg_dev, n = *n_dev;
   for (int e = r + blockIdx.x * blockDim.x + threadIdx.x; e < n; e += gridDim.x * blockDim.x) {
     int c = cons[e];
@@ -355,6 +365,7 @@ constexpr int kSeenCap = 24;
 // pass 0: decide self vs edges, entry count, cached sums; pass 1: write entries
 template <int PASS>
 __global__ void k_blame(KView k, BlameArgs a) {
+  pdl_wait();
   for (int j = blockIdx.x * blockDim.x + threadIdx.x; j < k.N; j += gridDim.x * blockDim.x) {
     const int lat = a.p.lat[j];
     const double s_j = (double)((int64_t)lat * a.p.period);
@@ -466,6 +477,7 @@ constexpr int kSBHash = 512, kSBFront = 256;
 constexpr int kSBWarpInts = kSBHash + 2 * kSBFront + 8;
 
 __global__ void k_selfblame_warp(KView k, BlameArgs a, int32_t* slow2, int32_t* slow2_count) {
+  pdl_wait();
   extern __shared__ int32_t sbm[];
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, wpc = blockDim.x >> 5;
   int32_t* hash = sbm + (size_t)wid * kSBWarpInts;
@@ -530,6 +542,7 @@ __global__ void k_selfblame_warp(KView k, BlameArgs a, int32_t* slow2, int32_t* 
 
 __global__ void k_selfblame_slow(KView k, BlameArgs a, const int32_t* list, const int32_t* count,
                                  int32_t* scratch, int nworkers) {
+  pdl_wait();
   const int ns = (int)min((int64_t)*count, a.slow_cap);
   const int w = blockIdx.x * blockDim.x + threadIdx.x;
   if (w >= nworkers) return;
@@ -542,12 +555,14 @@ __global__ void k_selfblame_slow(KView k, BlameArgs a, const int32_t* list, cons
   }
 }
 
-__global__ void k_blame_count(const int32_t* eoff, int N, LeoBlame out) { *out.count = eoff[N]; }
+__global__ void k_blame_count(const int32_t* eoff, int N, LeoBlame out) {
+  pdl_wait(); *out.count = eoff[N]; }
 
 // ---- per-source-line rollup -----------------------------------------------------
 __global__ void k_lines(KView k, PView p, Range own, const int32_t* __restrict__ pprod, LeoBlame b,
                         const int32_t* __restrict__ line_id, double* __restrict__ line_blame,
                         double* __restrict__ line_stall) {
+  pdl_wait();
   // an overflowed entry list has unwritten holes: the host re-runs bigger
   const int n = *b.count <= b.capacity ? *b.count : 0;
   const int stride = gridDim.x * blockDim.x;
@@ -575,6 +590,7 @@ struct SliceArgs {
 };
 
 __global__ void k_slice(int N, SliceArgs a) {
+  pdl_wait();
   cg::grid_group grid = cg::this_grid();
   const int tid = blockIdx.x * blockDim.x + threadIdx.x, nt = gridDim.x * blockDim.x;
   if (tid == 0) { a.counts[0] = 0; a.counts[1] = 0; }

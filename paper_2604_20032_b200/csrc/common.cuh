@@ -2,6 +2,8 @@
 #pragma once
 #include <cstdint>
 #include <cuda_runtime.h>
+#include <cstdlib>
+#include <utility>
 
 #include "../../include/leo_b200.h"
 
@@ -115,6 +117,17 @@ struct PhaseMarks {
   }
 };
 
+// ---- programmatic dependent launch ------------------------------------------
+// Every pipeline kernel is launched with programmatic stream serialization
+// (leo_launch) and starts with pdl_wait(): the kernel may be scheduled while
+// its predecessor drains, and waits here until the predecessor grid has
+// completed and its memory is visible (a no-op without the attribute).
+LEO_DEV void pdl_wait() {
+#ifdef __CUDA_ARCH__
+  asm volatile("griddepcontrol.wait;" ::: "memory");
+#endif
+}
+
 // ---- launch helpers ---------------------------------------------------------
 // dynamic shared memory a shared-memory-resident tier may request per CTA
 constexpr int kSmemResidentMax = 200 * 1024;
@@ -123,6 +136,29 @@ inline int grid_for(int64_t n, int threads, int max_blocks = 148 * 32) {
   if (g < 1) g = 1;
   if (g > max_blocks) g = max_blocks;
   return (int)g;
+}
+
+// LEO_NO_PDL=1 launches without the programmatic-serialization attribute
+inline bool pdl_enabled() {
+  static int v = -1;
+  if (v < 0) { const char* e = getenv("LEO_NO_PDL"); v = (e && e[0] == '1') ? 0 : 1; }
+  return v == 1;
+}
+
+template <typename... KArgs, typename... Args>
+inline void leo_launch(void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t st,
+                       Args&&... args) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = st;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = pdl_enabled() ? 1 : 0;
+  cudaLaunchKernelEx(&cfg, kern, std::forward<Args>(args)...);
 }
 
 #define LEO_CUDA_CHECK(x)                                      \

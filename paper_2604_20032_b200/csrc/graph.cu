@@ -27,6 +27,7 @@
 namespace leo {
 
 __global__ void k_unit_counts(KView k, int32_t* __restrict__ ucnt, int32_t* __restrict__ dcnt) {
+  pdl_wait();
   for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < k.N; i += gridDim.x * blockDim.x) {
     int u = 0, d = 0;
     for (int q = k.opnd_ptr[i]; q < k.opnd_ptr[i + 1]; q++) {
@@ -68,6 +69,7 @@ struct WalkArgs {
 // warp per block; blocks visited in increasing order per warp so that stale
 // table entries (from earlier blocks) are recognisable by index comparison.
 __global__ void k_block_walk(KView k, WalkArgs a, int warps_per_cta) {
+  pdl_wait();
   extern __shared__ int32_t smem[];
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
   const int gw = blockIdx.x * warps_per_cta + wid, nw = gridDim.x * warps_per_cta;
@@ -146,6 +148,7 @@ __global__ void k_block_walk(KView k, WalkArgs a, int warps_per_cta) {
 //   rec[y] = {h = runhead(y), np = |preds(h)|, p0, p1}
 //   np <= 2: p0/p1 are the predecessors of h; np > 2: p0 = pred_ptr[h].
 __global__ void k_block_records(KView k, int4* __restrict__ rec, int32_t* __restrict__ rh) {
+  pdl_wait();
   for (int b = blockIdx.x * blockDim.x + threadIdx.x; b < k.B; b += gridDim.x * blockDim.x) {
     int x = b;
     while (x > 0 && k.pred_ptr[x + 1] - k.pred_ptr[x] == 1 && k.pred[k.pred_ptr[x]] == x - 1) x--;
@@ -288,6 +291,7 @@ __host__ __device__ inline size_t reach_unit_smem(int B, int threads) {
 // kernels with few register units still fill the chip.
 __global__ void k_reach_unit(KView k, ReachArgs a, const int32_t* __restrict__ qtab,
                              const int32_t* __restrict__ rh_g, int parts) {
+  pdl_wait();
   extern __shared__ __align__(16) unsigned char sm_raw[];
   __shared__ int nq, rbase;
   __shared__ int swarp[33];
@@ -442,6 +446,7 @@ constexpr int kT1Hash = 128, kT1Limit = 96, kT1Stack = 96, kT1Res = 32, kT1Threa
 __global__ void __launch_bounds__(kT1Threads) k_reach_fast(KView k, ReachArgs a,
                                                            const int32_t* __restrict__ q_list,
                                                            const int32_t* q_count, int32_t* q_head) {
+  pdl_wait();
   extern __shared__ int32_t hsm[];
   const int nq = *q_count;
   const int lane = threadIdx.x & 31;
@@ -552,6 +557,7 @@ LEO_DEV bool hash_insert(int32_t* h, int key, int* count) {
 __global__ void k_reach_warp(KView k, ReachArgs a, const int32_t* __restrict__ list,
                              const int32_t* count, int64_t list_cap, int32_t* slow_list,
                              int32_t* slow_count) {
+  pdl_wait();
   extern __shared__ int32_t smem[];
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
   const int wpc = blockDim.x >> 5;
@@ -634,6 +640,7 @@ __global__ void k_reach_warp(KView k, ReachArgs a, const int32_t* __restrict__ l
 // of B entries each); stamps are query slot + 1, so no clearing between queries.
 __global__ void k_reach_slow(KView k, ReachArgs a, const int32_t* list, const int32_t* count,
                              int32_t* scratch, int nworkers) {
+  pdl_wait();
   const int ns = (int)min((int64_t)*count, a.slow_cap);
   const int w = blockIdx.x * blockDim.x + threadIdx.x;
   if (w >= nworkers) return;
@@ -673,6 +680,7 @@ LEO_DEV uint64_t link_key(int producer, int kind, uint32_t r) {
 // mode 0: count candidates + unresolved diagnostics; mode 1: write keys
 template <int MODE>
 __global__ void k_link(KView k, LinkArgs a) {
+  pdl_wait();
   for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < k.N; i += gridDim.x * blockDim.x) {
     int e = a.use_ptr[i];
     int cnt = 0;
@@ -709,6 +717,7 @@ __constant__ static const int kRankToClass[8] = {3, 2, 1, 5, 6, 4, 0, 7};
 __global__ void k_link_emit(KView k, const int32_t* __restrict__ cand_off, const uint64_t* __restrict__ cand,
                             const int32_t* __restrict__ uniq, const int32_t* __restrict__ eoff,
                             LeoEdges out, uint32_t* status) {
+  pdl_wait();
   for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < k.N; i += gridDim.x * blockDim.x) {
     int n = uniq[i], o = eoff[i];
     if (o + n > out.capacity) { if (n) atomicOr(status, (uint32_t)LEO_ST_EDGE_OVERFLOW); continue; }

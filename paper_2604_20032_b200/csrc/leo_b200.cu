@@ -260,10 +260,10 @@ int build_graph_impl(const LeoKernel* kk, const LeoCaps* caps, LeoEdges* out, Le
     cudaMemsetAsync(pcur, 0, (size_t)std::max(N, 1) * 4, st);
     cudaMemsetAsync(sync_scr, 0, (size_t)SW * sync_slow_bytes_per_worker(B), st);
     cudaMemsetAsync(bev, 0, (size_t)std::max(B, 1) * 4, st);
-    TRACED(KID_SYNC_PACK, k_sync_pack<<<grid_for(N, T), T, 0, st>>>(k, wcword, setword, bev));
+    TRACED(KID_SYNC_PACK, leo_launch(k_sync_pack, grid_for(N, T), T, 0, st, k, wcword, setword, bev));
     if (k.dialect != LEO_AMD && B > 0)
-      TRACED(KID_SYNC_PACK, k_block_setters<<<grid_for(B, T), T, 0, st>>>(k, setword, n_ids, lastset));
-    TRACED(KID_SYNC_PACK, k_wait_list<<<grid_for(N, T), T, 0, st>>>(k, own, wlist, &ctr[8]));
+      TRACED(KID_SYNC_PACK, leo_launch(k_block_setters, grid_for(B, T), T, 0, st, k, setword, n_ids, lastset));
+    TRACED(KID_SYNC_PACK, leo_launch(k_wait_list, grid_for(N, T), T, 0, st, k, own, wlist, &ctr[8]));
     SyncArgs sa{caps ? caps->debug_flags : 0, skeys, cap_sync, &ctr[3], slow2, &ctr[4], cap_slow, *diags, status,
                 wcword, setword, lastset, n_ids, wlist, &ctr[8], wclist, &ctr[10]};
     // as many threads per CTA as the image allows: more warps hide the
@@ -273,28 +273,28 @@ int build_graph_impl(const LeoKernel* kk, const LeoCaps* caps, LeoEdges* out, Le
     const size_t wc_smem = sync_smem_bytes(N, B, wc_threads);
     const int dbg_flags = caps ? caps->debug_flags : 0;
     if (k.dialect == LEO_AMD && B > 0 && wc_smem <= (size_t)kSmemResidentMax && !(dbg_flags & LEO_DBG_NO_SMEM))
-      TRACED(KID_SYNC, k_sync_wc_smem<<<SM, wc_threads, wc_smem, st>>>(k, sa, bev));
+      TRACED(KID_SYNC, leo_launch(k_sync_wc_smem, SM, wc_threads, wc_smem, st, k, sa, bev));
     else
-      TRACED(KID_SYNC, k_sync<false><<<grid_for(N, 64), 64, 0, st>>>(k, sa, nullptr, 0));
+      TRACED(KID_SYNC, leo_launch(k_sync<false>, grid_for(N, 64), 64, 0, st, k, sa, nullptr, 0));
     if (k.dialect == LEO_AMD)
-      TRACED(KID_SYNC_WARP, k_sync_wc_warp<<<num_sms() * 2, 128, 4 * kWcSmemInts * 4, st>>>(
+      TRACED(KID_SYNC_WARP, leo_launch(k_sync_wc_warp, num_sms() * 2, 128, 4 * kWcSmemInts * 4, st, 
           k, sa, wclist, &ctr[10], cap_slow, slow2, &ctr[4]));
-    TRACED(KID_SYNC_SLOW, k_sync<true><<<1, SW, 0, st>>>(k, sa, sync_scr, SW));
-    TRACED(KID_KEY_HIST, k_key_hist<<<grid_for(cap_sync, T), T, 0, st>>>(skeys, &ctr[3], cap_sync, pcnt));
+    TRACED(KID_SYNC_SLOW, leo_launch(k_sync<true>, 1, SW, 0, st, k, sa, sync_scr, SW));
+    TRACED(KID_KEY_HIST, leo_launch(k_key_hist, grid_for(cap_sync, T), T, 0, st, skeys, &ctr[3], cap_sync, pcnt));
     TRACED(KID_SCAN, scan_exclusive(pcnt, poff, nullptr, N, scan_tmp2, nullptr, st));
-    TRACED(KID_KEY_SCATTER, k_key_scatter<<<grid_for(cap_sync, T), T, 0, st>>>(skeys, &ctr[3], cap_sync, poff, pcur, ssorted));
-    TRACED(KID_SEGSORT, segsort_unique_u64<<<grid_for(N, 128), 128, 0, st>>>(ssorted, poff, pcnt, nullptr, N, puniq, cap_sync));
+    TRACED(KID_KEY_SCATTER, leo_launch(k_key_scatter, grid_for(cap_sync, T), T, 0, st, skeys, &ctr[3], cap_sync, poff, pcur, ssorted));
+    TRACED(KID_SEGSORT, leo_launch(segsort_unique_u64, grid_for(N, 128), 128, 0, st, ssorted, poff, pcnt, nullptr, N, puniq, cap_sync));
     TRACED(KID_SCAN, scan_exclusive(puniq, puoff, nullptr, N, scan_tmp2, &ctr[6], st));
   }
-  TRACED(KID_UNIT_COUNTS, k_unit_counts<<<grid_for(N, T), T, 0, st>>>(k, ucnt, dcnt));
+  TRACED(KID_UNIT_COUNTS, leo_launch(k_unit_counts, grid_for(N, T), T, 0, st, k, ucnt, dcnt));
   TRACED(KID_SCAN, scan_exclusive(ucnt, use_ptr, nullptr, N, scan_tmp, nullptr, st));
   TRACED(KID_SCAN, scan_exclusive(dcnt, def_ptr, nullptr, N, scan_tmp, nullptr, st));
 
   WalkArgs wa{use_ptr, def_ptr, ev_res, q_block, q_unit, q_list, &ctr[0], ldtab, qtab, Bp, gtab};
   size_t smem = smem_tab ? (size_t)wpc * 2 * U * 4 : 0;
-  if (B > 0) TRACED(KID_BLOCK_WALK, k_block_walk<<<std::max(1, walk_ctas), wpc * 32, smem, st>>>(k, wa, wpc));
+  if (B > 0) TRACED(KID_BLOCK_WALK, leo_launch(k_block_walk, std::max(1, walk_ctas), wpc * 32, smem, st, k, wa, wpc));
 
-  if (B > 0) TRACED(KID_RUN_HEADS, k_block_records<<<grid_for(B, T), T, 0, st>>>(k, brec, rhead));
+  if (B > 0) TRACED(KID_RUN_HEADS, leo_launch(k_block_records, grid_for(B, T), T, 0, st, k, brec, rhead));
   ReachArgs ra{caps ? caps->debug_flags : 0, ldtab, brec, U, Bp, q_block, q_unit, q_off, q_len, qres, cap_qres, &ctr[1],
                slow_list, &ctr[2], NU + 1024, status};
   const int dbg = caps ? caps->debug_flags : 0;
@@ -304,31 +304,31 @@ int build_graph_impl(const LeoKernel* kk, const LeoCaps* caps, LeoEdges* out, Le
   const int ru_parts = std::max(1, std::min(8, (2 * SM + U - 1) / std::max(U, 1)));
   if (B > 0 && U > 0 && ru_smem <= (size_t)kSmemResidentMax && !(dbg & LEO_DBG_NO_SMEM)) {
     // tier 0: the CFG and one unit's columns resident in shared memory, CTA per unit
-    TRACED(KID_REACH_FAST, k_reach_unit<<<std::min(U, SM * 8) * ru_parts, ru_threads, ru_smem, st>>>(k, ra, qtab, rhead, ru_parts));
+    TRACED(KID_REACH_FAST, leo_launch(k_reach_unit, std::min(U, SM * 8) * ru_parts, ru_threads, ru_smem, st, k, ra, qtab, rhead, ru_parts));
   } else {
     // tier 1 is persistent: enough CTAs to fill the chip, queries fetched dynamically
-    TRACED(KID_REACH_FAST, k_reach_fast<<<std::max(1, std::min<int>(grid_for(NU, kT1Threads), SM * 3)), kT1Threads,
-                                          kT1Threads * kT1Hash * 4, st>>>(k, ra, q_list, &ctr[0], &ctr[9]));
+    TRACED(KID_REACH_FAST, leo_launch(k_reach_fast, std::max(1, std::min<int>(grid_for(NU, kT1Threads), SM * 3)), kT1Threads,
+                                          kT1Threads * kT1Hash * 4, st, k, ra, q_list, &ctr[0], &ctr[9]));
   }
   {
     const int wpc_r = 4;
     const size_t sm_r = (size_t)wpc_r * kWarpSmemInts * 4;
-    TRACED(KID_REACH_WARP, k_reach_warp<<<std::max(1, std::min<int>(SM * 4, (int)((NU + 1024 + wpc_r - 1) / wpc_r))),
-                                          wpc_r * 32, sm_r, st>>>(k, ra, slow_list, &ctr[2], NU + 1024, slow3, &ctr[7]));
+    TRACED(KID_REACH_WARP, leo_launch(k_reach_warp, std::max(1, std::min<int>(SM * 4, (int)((NU + 1024 + wpc_r - 1) / wpc_r))),
+                                          wpc_r * 32, sm_r, st, k, ra, slow_list, &ctr[2], NU + 1024, slow3, &ctr[7]));
   }
-  TRACED(KID_REACH_SLOW, k_reach_slow<<<(RW + 63) / 64, 64, 0, st>>>(k, ra, slow3, &ctr[7], reach_scr, RW));
+  TRACED(KID_REACH_SLOW, leo_launch(k_reach_slow, (RW + 63) / 64, 64, 0, st, k, ra, slow3, &ctr[7], reach_scr, RW));
 
   LinkArgs la{use_ptr, ev_res, q_off, q_len, qres, cand_cnt, cand_off, cand, cap_cand, *diags, status, own};
-  TRACED(KID_LINK_COUNT, k_link<0><<<grid_for(N, T), T, 0, st>>>(k, la));
+  TRACED(KID_LINK_COUNT, leo_launch(k_link<0>, grid_for(N, T), T, 0, st, k, la));
   TRACED(KID_SCAN, scan_exclusive(cand_cnt, cand_off, nullptr, N, scan_tmp, nullptr, st));
-  TRACED(KID_LINK_FILL, k_link<1><<<grid_for(N, T), T, 0, st>>>(k, la));
-  TRACED(KID_SEGSORT, segsort_unique_u64<<<grid_for(N, 128), 128, 0, st>>>(cand, cand_off, cand_cnt, nullptr, N, uniq, cap_cand));
+  TRACED(KID_LINK_FILL, leo_launch(k_link<1>, grid_for(N, T), T, 0, st, k, la));
+  TRACED(KID_SEGSORT, leo_launch(segsort_unique_u64, grid_for(N, 128), 128, 0, st, cand, cand_off, cand_cnt, nullptr, N, uniq, cap_cand));
   TRACED(KID_SCAN, scan_exclusive(uniq, eoff, nullptr, N, scan_tmp, &ctr[5], st));
-  TRACED(KID_LINK_EMIT, k_link_emit<<<grid_for(N, T), T, 0, st>>>(k, cand_off, cand, uniq, eoff, *out, status));
+  TRACED(KID_LINK_EMIT, leo_launch(k_link_emit, grid_for(N, T), T, 0, st, k, cand_off, cand, uniq, eoff, *out, status));
 
   if (fork) link_streams(s_sync, st, sp.e[1]);   // join
-  TRACED(KID_SYNC_EMIT, k_sync_emit<<<grid_for(N, T), T, 0, st>>>(N, kind, ssorted, poff, puniq, puoff, &ctr[5], *out, status));
-  TRACED(KID_EDGE_TOTALS, k_edge_totals<<<1, 1, 0, st>>>(&ctr[5], &ctr[6], *out, status));
+  TRACED(KID_SYNC_EMIT, leo_launch(k_sync_emit, grid_for(N, T), T, 0, st, N, kind, ssorted, poff, puniq, puoff, &ctr[5], *out, status));
+  TRACED(KID_EDGE_TOTALS, leo_launch(k_edge_totals, 1, 1, 0, st, &ctr[5], &ctr[6], *out, status));
   ar.release();
   LEO_CUDA_CHECK(cudaGetLastError());
   return 0;
@@ -366,13 +366,13 @@ int prune_impl(const LeoKernel* kk, const LeoProfile* pp, const LeoConfig* cfg, 
     // kernel (thread per edge, no per-round CTA barriers) balances better
     (void)unstaged;
     if (!(dbg & LEO_DBG_NO_SMEM) && staged <= (size_t)kSmemResidentMax)
-      TRACED(KID_PRUNE, k_prune_edges_smem<true><<<num_sms(), 128, staged, st>>>(k, p, a));
+      TRACED(KID_PRUNE, leo_launch(k_prune_edges_smem<true>, num_sms(), 128, staged, st, k, p, a));
     else
-      TRACED(KID_PRUNE, k_prune_edges<<<grid_for(cap_in, 128, num_sms() * 16), 128, 0, st>>>(k, p, a));
+      TRACED(KID_PRUNE, leo_launch(k_prune_edges, grid_for(cap_in, 128, num_sms() * 16), 128, 0, st, k, p, a));
   }
-  TRACED(KID_PRUNE_SLOW, k_prune_slow<<<1, PW, 0, st>>>(k, p, a, slow_scr, PW));
+  TRACED(KID_PRUNE_SLOW, leo_launch(k_prune_slow, 1, PW, 0, st, k, p, a, slow_scr, PW));
   TRACED(KID_SCAN, scan_exclusive(keep, pos, in->count, cap_in, scan_tmp, nullptr, st));
-  TRACED(KID_COMPACT, k_compact<<<grid_for(cap_in, 256), 256, 0, st>>>(a, pos, in->n_regular, *out, status));
+  TRACED(KID_COMPACT, leo_launch(k_compact, grid_for(cap_in, 256), 256, 0, st, a, pos, in->n_regular, *out, status));
   ar.release();
   LEO_CUDA_CHECK(cudaGetLastError());
   return 0;
@@ -395,12 +395,12 @@ Incoming build_incoming(IncomingBufs& b, int N, const LeoEdges* e, bool with_syn
   cudaMemsetAsync(b.rend, 0, nb, st);
   cudaMemsetAsync(b.scnt, 0, nb, st);
   cudaMemsetAsync(b.scur, 0, nb, st);
-  TRACED(KID_SEG_BOUNDS, k_seg_bounds<<<grid_for(e->capacity, 256), 256, 0, st>>>(e->cons, e->n_regular, b.rbeg, b.rend));
+  TRACED(KID_SEG_BOUNDS, leo_launch(k_seg_bounds, grid_for(e->capacity, 256), 256, 0, st, e->cons, e->n_regular, b.rbeg, b.rend));
   if (with_sync) {
-    TRACED(KID_SYNC_HIST, k_sync_hist<<<grid_for(e->capacity, 256), 256, 0, st>>>(e->cons, e->n_regular, e->count, b.scnt));
+    TRACED(KID_SYNC_HIST, leo_launch(k_sync_hist, grid_for(e->capacity, 256), 256, 0, st, e->cons, e->n_regular, e->count, b.scnt));
     TRACED(KID_SCAN, scan_exclusive(b.scnt, b.soff, nullptr, N, b.tmp, nullptr, st));
-    TRACED(KID_SYNC_FILL, k_sync_fill<<<grid_for(e->capacity, 256), 256, 0, st>>>(e->cons, e->n_regular, e->count, b.soff, b.scur, b.sidx));
-    TRACED(KID_SEGSORT, segsort_unique_u64<<<grid_for(N, 128), 128, 0, st>>>(b.sidx, b.soff, b.scnt, nullptr, N, b.uniq, e->capacity));
+    TRACED(KID_SYNC_FILL, leo_launch(k_sync_fill, grid_for(e->capacity, 256), 256, 0, st, e->cons, e->n_regular, e->count, b.soff, b.scur, b.sidx));
+    TRACED(KID_SEGSORT, leo_launch(segsort_unique_u64, grid_for(N, 128), 128, 0, st, b.sidx, b.soff, b.scnt, nullptr, N, b.uniq, e->capacity));
   } else {
     cudaMemsetAsync(b.soff, 0, (size_t)(N + 1) * 4, st);
   }
@@ -453,18 +453,18 @@ int blame_impl(const LeoKernel* kk, const LeoProfile* pp, const LeoEdges* pruned
   Incoming binc = build_incoming(bb, N, base, false, tr, st);   // RAW edges only
   BlameArgs a{caps ? caps->debug_flags : 0, own, p, pruned->prod, pruned->meta, paths->dist, inc, binc.rbeg, binc.rend, base->prod, base->meta,
               ecount, self_sub, jtotal, jnsum, eoff, *out, slow_list, &ctr[0], cap_slow, status};
-  TRACED(KID_BLAME_COUNT, k_blame<0><<<grid_for(N, 128), 128, 0, st>>>(k, a));
-  TRACED(KID_SELFBLAME_WARP, k_selfblame_warp<<<num_sms(), 128, 4 * kSBWarpInts * 4, st>>>(k, a, slow2, &ctr[1]));
-  TRACED(KID_SELFBLAME_SLOW, k_selfblame_slow<<<1, BW, 0, st>>>(k, a, slow2, &ctr[1], slow_scr, BW));
+  TRACED(KID_BLAME_COUNT, leo_launch(k_blame<0>, grid_for(N, 128), 128, 0, st, k, a));
+  TRACED(KID_SELFBLAME_WARP, leo_launch(k_selfblame_warp, num_sms(), 128, 4 * kSBWarpInts * 4, st, k, a, slow2, &ctr[1]));
+  TRACED(KID_SELFBLAME_SLOW, leo_launch(k_selfblame_slow, 1, BW, 0, st, k, a, slow2, &ctr[1], slow_scr, BW));
   TRACED(KID_SCAN, scan_exclusive(ecount, eoff, nullptr, N, scan_tmp, nullptr, st));
-  TRACED(KID_BLAME_FILL, k_blame<1><<<grid_for(N, 128), 128, 0, st>>>(k, a));
-  TRACED(KID_BLAME_TOTAL, k_blame_count<<<1, 1, 0, st>>>(eoff, N, *out));
+  TRACED(KID_BLAME_FILL, leo_launch(k_blame<1>, grid_for(N, 128), 128, 0, st, k, a));
+  TRACED(KID_BLAME_TOTAL, leo_launch(k_blame_count, 1, 1, 0, st, eoff, N, *out));
   if (line_id && line_blame && line_stall && n_lines > 0) {
     if (!(caps && (caps->options & LEO_OPT_ACCUMULATE_LINES))) {
       cudaMemsetAsync(line_blame, 0, (size_t)n_lines * 8, st);
       cudaMemsetAsync(line_stall, 0, (size_t)n_lines * 8, st);
     }
-    TRACED(KID_LINES, k_lines<<<grid_for(std::max<int64_t>(out->capacity, N), 256), 256, 0, st>>>(k, p, own, pruned->prod, *out,
+    TRACED(KID_LINES, leo_launch(k_lines, grid_for(std::max<int64_t>(out->capacity, N), 256), 256, 0, st, k, p, own, pruned->prod, *out,
                                                                                line_id, line_blame, line_stall));
   }
   ar.release();
@@ -506,16 +506,16 @@ static int bin_impl(const LeoSamples* s, int32_t n_instr, int32_t* lat, int32_t*
   if (bucketed) {
     const int smem = R * 8 * 4;
     const int slice = (int)std::min<int64_t>(65536, std::max<int64_t>(4096, S / (num_sms() * 3)));
-    TRACED(KID_BIN_HIST, k_bin_hist<<<G, 512, nb * 4, st>>>(S, s->pc, n_instr, nb, R, M, status));
-    TRACED(KID_BIN_PLAN, k_bin_colscan<<<std::min(nb, num_sms() * 4), 256, 0, st>>>(nb, G, M, btot));
-    TRACED(KID_BIN_PLAN, k_bin_plan<<<1, 1024, 0, st>>>(nb, slice, btot, boff, soff));
-    TRACED(KID_BIN_SCATTER, k_bin_scatter<<<G, 512, nb * 4, st>>>(S, s->pc, s->cat, s->cat_to_cs, n_instr, nb, R, M, boff, keys));
-    TRACED(KID_BIN, k_bin_count<<<num_sms() * 3, 512, smem, st>>>(n_instr, nb, R, slice, boff, soff, keys, cls_cnt));
+    TRACED(KID_BIN_HIST, leo_launch(k_bin_hist, G, 512, nb * 4, st, S, s->pc, n_instr, nb, R, M, status));
+    TRACED(KID_BIN_PLAN, leo_launch(k_bin_colscan, std::min(nb, num_sms() * 4), 256, 0, st, nb, G, M, btot));
+    TRACED(KID_BIN_PLAN, leo_launch(k_bin_plan, 1, 1024, 0, st, nb, slice, btot, boff, soff));
+    TRACED(KID_BIN_SCATTER, leo_launch(k_bin_scatter, G, 512, nb * 4, st, S, s->pc, s->cat, s->cat_to_cs, n_instr, nb, R, M, boff, keys));
+    TRACED(KID_BIN, leo_launch(k_bin_count, num_sms() * 3, 512, smem, st, n_instr, nb, R, slice, boff, soff, keys, cls_cnt));
   } else if (S > 0) {
-    TRACED(KID_BIN, k_bin_samples<<<grid_for(S / 4 + 1, 256, num_sms() * 8), 256, 0, st>>>(
+    TRACED(KID_BIN, leo_launch(k_bin_samples, grid_for(S / 4 + 1, 256, num_sms() * 8), 256, 0, st, 
         S, s->pc, s->cat, s->cat_to_cs, n_instr, cls_cnt, status));
   }
-  TRACED(KID_BIN_FINALIZE, k_bin_finalize<<<grid_for(n_instr, 256), 256, 0, st>>>(n_instr, cls_cnt, lat));
+  TRACED(KID_BIN_FINALIZE, leo_launch(k_bin_finalize, grid_for(n_instr, 256), 256, 0, st, n_instr, cls_cnt, lat));
   ar.release();
   LEO_CUDA_CHECK(cudaGetLastError());
   return 0;
@@ -621,19 +621,19 @@ int leo_report(const LeoKernel* k, const LeoProfile* p, const LeoEdges* base, co
   // before: base graph minus sync edges (the raw/guard prefix, report.py:135-137)
   cudaMemsetAsync(mask, 0, (size_t)std::max(N, 1) * 4, st);
   cudaMemsetAsync(cnt, 0, (size_t)std::max(N, 1) * 4, st);
-  k_cov_edges<<<grid_for(base->capacity, T), T, 0, st>>>(base->cons, base->meta, base->n_regular, base->capacity, mask, cnt);
-  k_cov_nodes<<<grid_for(N, T, num_sms() * 4), T, 0, st>>>(N, mask, cnt, r->coverage);
+  leo_launch(k_cov_edges, grid_for(base->capacity, T), T, 0, st, base->cons, base->meta, base->n_regular, base->capacity, mask, cnt);
+  leo_launch(k_cov_nodes, grid_for(N, T, num_sms() * 4), T, 0, st, N, mask, cnt, r->coverage);
   // after: every pruned edge
   cudaMemsetAsync(mask, 0, (size_t)std::max(N, 1) * 4, st);
   cudaMemsetAsync(cnt, 0, (size_t)std::max(N, 1) * 4, st);
-  k_cov_edges<<<grid_for(pruned->capacity, T), T, 0, st>>>(pruned->cons, pruned->meta, pruned->count, pruned->capacity, mask, cnt);
-  k_cov_nodes<<<grid_for(N, T, num_sms() * 4), T, 0, st>>>(N, mask, cnt, r->coverage + 2);
-  k_report_rank<<<1, 1024, 0, st>>>(N, p->lat, r->top_n, r->include_unsampled, r->hot, r->n_hot);
+  leo_launch(k_cov_edges, grid_for(pruned->capacity, T), T, 0, st, pruned->cons, pruned->meta, pruned->count, pruned->capacity, mask, cnt);
+  leo_launch(k_cov_nodes, grid_for(N, T, num_sms() * 4), T, 0, st, N, mask, cnt, r->coverage + 2);
+  leo_launch(k_report_rank, 1, 1024, 0, st, N, p->lat, r->top_n, r->include_unsampled, r->hot, r->n_hot);
   if (r->top_n > 0) {
     ReportArgs a{r->n_hot, r->hot, blame->stalled, blame->edge, blame->blame, blame->count, blame->capacity,
                  pruned->prod, r->max_causes, r->chain_depth, r->n_causes, r->causes, r->chain_len,
                  r->chain_node, r->chain_entry, r->chain_self, status};
-    k_report_hot<<<r->top_n, 32, 0, st>>>(a);
+    leo_launch(k_report_hot, r->top_n, 32, 0, st, a);
   }
   ar.release();
   LEO_CUDA_CHECK(cudaGetLastError());

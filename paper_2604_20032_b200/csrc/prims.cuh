@@ -45,6 +45,7 @@ LEO_DEV int block_excl_scan(int v, int* smem_warp, int* total) {
 
 __global__ void scan_tile_sums(const int32_t* __restrict__ in, const int32_t* n_dev, int64_t n_cap,
                                int32_t* __restrict__ tile_sums) {
+  pdl_wait();
   __shared__ int sw[33];
   int64_t n = n_dev ? (int64_t)*n_dev : n_cap;
   int64_t base = (int64_t)blockIdx.x * kScanTile;
@@ -60,6 +61,7 @@ __global__ void scan_tile_sums(const int32_t* __restrict__ in, const int32_t* n_
 
 // single CTA: exclusive scan of the tile sums (in place); grand total -> *total_out
 __global__ void scan_tile_prefix(int32_t* tile_sums, int ntiles, int32_t* total_out) {
+  pdl_wait();
   __shared__ int sw[33];
   int carry = 0;
   for (int base = 0; base < ntiles; base += blockDim.x) {
@@ -75,6 +77,7 @@ __global__ void scan_tile_prefix(int32_t* tile_sums, int ntiles, int32_t* total_
 
 __global__ void scan_tile_apply(const int32_t* __restrict__ in, const int32_t* n_dev, int64_t n_cap,
                                 const int32_t* __restrict__ tile_sums, int32_t* __restrict__ out) {
+  pdl_wait();
   __shared__ int sw[33];
   int64_t n = n_dev ? (int64_t)*n_dev : n_cap;
   int64_t base = (int64_t)blockIdx.x * kScanTile + (int64_t)threadIdx.x * kScanItems;
@@ -107,6 +110,7 @@ __global__ void scan_tile_apply(const int32_t* __restrict__ in, const int32_t* n
 __global__ void __launch_bounds__(1024) scan_single_cta(const int32_t* __restrict__ in, const int32_t* n_dev,
                                                         int64_t n_cap, int32_t* __restrict__ out,
                                                         int32_t* total_out) {
+  pdl_wait();
   __shared__ int sw[33];
   const int n = (int)(n_dev ? (int64_t)*n_dev : n_cap);
   const int per = ((n + blockDim.x - 1) / blockDim.x + 3) & ~3;   // multiple of 4
@@ -145,14 +149,14 @@ __global__ void __launch_bounds__(1024) scan_single_cta(const int32_t* __restric
 inline void scan_exclusive(const int32_t* in, int32_t* out, const int32_t* n_dev, int64_t n_cap,
                            int32_t* scratch, int32_t* total_out, cudaStream_t st) {
   if (n_cap <= (1 << 18)) {
-    scan_single_cta<<<1, 1024, 0, st>>>(in, n_dev, n_cap, out, total_out);
+    leo_launch(scan_single_cta, 1, 1024, 0, st, in, n_dev, n_cap, out, total_out);
     return;
   }
   int64_t ntiles = (n_cap + kScanTile - 1) / kScanTile;
   if (ntiles < 1) ntiles = 1;
-  scan_tile_sums<<<(unsigned)ntiles, kScanThreads, 0, st>>>(in, n_dev, n_cap, scratch);
-  scan_tile_prefix<<<1, 1024, 0, st>>>(scratch, (int)ntiles, total_out);
-  scan_tile_apply<<<(unsigned)ntiles, kScanThreads, 0, st>>>(in, n_dev, n_cap, scratch, out);
+  leo_launch(scan_tile_sums, (unsigned)ntiles, kScanThreads, 0, st, in, n_dev, n_cap, scratch);
+  leo_launch(scan_tile_prefix, 1, 1024, 0, st, scratch, (int)ntiles, total_out);
+  leo_launch(scan_tile_apply, (unsigned)ntiles, kScanThreads, 0, st, in, n_dev, n_cap, scratch, out);
 }
 inline int64_t scan_scratch_ints(int64_t n_cap) { return (n_cap + kScanTile - 1) / kScanTile + 1; }
 
@@ -183,6 +187,7 @@ LEO_DEV void shell_sort_u64(uint64_t* a, int n) {
 __global__ void segsort_unique_u64(uint64_t* __restrict__ keys, const int32_t* __restrict__ begin,
                                    const int32_t* __restrict__ len, const int32_t* nseg_dev, int nseg_cap,
                                    int32_t* __restrict__ uniq, int64_t cap) {
+  pdl_wait();
   int nseg = nseg_dev ? *nseg_dev : nseg_cap;
   for (int s = blockIdx.x * blockDim.x + threadIdx.x; s < nseg; s += gridDim.x * blockDim.x) {
     int n = len[s];

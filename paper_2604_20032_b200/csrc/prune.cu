@@ -255,6 +255,7 @@ LEO_DEV bool prune_one(const KView& k, const PView& p, const PruneArgs& a, int e
 constexpr int kDfsStack = 20, kDfsArena = 24, kDfsPaths = 64;
 
 __global__ void __launch_bounds__(128) k_prune_edges(KView k, PView p, PruneArgs a) {
+  pdl_wait();
   const int n = *a.n_in;
   DfsEnt stk[kDfsStack];
   BackNode arena[kDfsArena];
@@ -296,6 +297,7 @@ __host__ __device__ inline size_t prune_smem_bytes(int N, int B, int threads, bo
 
 template <bool STAGE>
 __global__ void k_prune_edges_smem(KView k, PView p, PruneArgs a) {
+  pdl_wait();
   extern __shared__ __align__(16) unsigned char sm_raw[];
   SmemCarve cv{sm_raw};
   uint64_t* bar = cv.take<uint64_t>(2);
@@ -372,6 +374,7 @@ __host__ __device__ inline size_t prune_slow_bytes(int max_depth, int max_paths)
 }
 
 __global__ void k_prune_slow(KView k, PView p, PruneArgs a, char* scratch, int nworkers) {
+  pdl_wait();
   const int ns = (int)min((int64_t)*a.slow_count, a.slow_cap);
   const int w = blockIdx.x * blockDim.x + threadIdx.x;
   if (w >= nworkers) return;
@@ -390,6 +393,7 @@ __global__ void k_prune_slow(KView k, PView p, PruneArgs a, char* scratch, int n
 
 __global__ void k_compact(PruneArgs a, const int32_t* __restrict__ pos, const int32_t* n_reg_in,
                           LeoEdges out, uint32_t* status) {
+  pdl_wait();
   const int n = *a.n_in;
   for (int e = blockIdx.x * blockDim.x + threadIdx.x; e < n; e += gridDim.x * blockDim.x) {
     if (!a.keep[e]) continue;

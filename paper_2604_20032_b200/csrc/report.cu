@@ -27,6 +27,7 @@ namespace leo {
 __global__ void k_cov_edges(const int32_t* __restrict__ cons, const uint32_t* __restrict__ meta,
                             const int32_t* n_dev, int32_t cap, int32_t* __restrict__ mask,
                             int32_t* __restrict__ cnt) {
+  pdl_wait();
   const int n = min(*n_dev, cap);
   for (int e = blockIdx.x * blockDim.x + threadIdx.x; e < n; e += gridDim.x * blockDim.x) {
     const int c = cons[e];
@@ -37,6 +38,7 @@ __global__ void k_cov_edges(const int32_t* __restrict__ cons, const uint32_t* __
 
 __global__ void k_cov_nodes(int N, const int32_t* __restrict__ mask, const int32_t* __restrict__ cnt,
                             int32_t* __restrict__ out) {
+  pdl_wait();
   __shared__ int sw[33];
   int nodes = 0, qual = 0;
   for (int j = blockIdx.x * blockDim.x + threadIdx.x; j < N; j += gridDim.x * blockDim.x) {
@@ -79,6 +81,7 @@ LEO_DEV int cta_compact(int N, const int32_t* lat, Pred pred, int32_t* out, int 
 __global__ void __launch_bounds__(1024) k_report_rank(int N, const int32_t* __restrict__ lat, int top_n,
                                                       int include_unsampled, int32_t* __restrict__ hot,
                                                       int32_t* __restrict__ n_hot) {
+  pdl_wait();
   __shared__ int sw[33];
   __shared__ unsigned long long key[kRankMax];
   int32_t* sel = hot;                    // the selection is staged in the output
@@ -170,6 +173,7 @@ LEO_DEV int lower_entry(const int32_t* st, int n, int j) {
 // cause order key pieces: report.py:160-163 (self = -1 first on ties);
 // trace_chain analysis.py:520-522 (self = +inf last on ties)
 __global__ void k_report_hot(ReportArgs a) {
+  pdl_wait();
   const int h = blockIdx.x;
   if (h >= *a.n_hot || threadIdx.x != 0) return;
   const int nb = *a.b_count <= a.b_cap ? *a.b_count : 0;

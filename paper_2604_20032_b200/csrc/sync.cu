@@ -52,6 +52,7 @@ struct SyncArgs {
 
 __global__ void k_sync_pack(KView k, uint32_t* __restrict__ wcword, uint8_t* __restrict__ setword,
                             uint32_t* __restrict__ bev) {
+  pdl_wait();
   for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < k.N; i += gridDim.x * blockDim.x) {
     const uint8_t sk = k.sync_kind[i];
     const uint32_t a = k.sync_a[i], b = k.sync_b[i];
@@ -89,6 +90,7 @@ __global__ void k_sync_pack(KView k, uint32_t* __restrict__ wcword, uint8_t* __r
 
 __global__ void k_block_setters(KView k, const uint8_t* __restrict__ setword, int n_ids,
                                 int32_t* __restrict__ lastset) {
+  pdl_wait();
   for (int b = blockIdx.x * blockDim.x + threadIdx.x; b < k.B; b += gridDim.x * blockDim.x) {
     int32_t* row = lastset + (size_t)b * n_ids;
     for (int t = 0; t < n_ids; t++) row[t] = -1;
@@ -266,6 +268,7 @@ LEO_DEV bool rec_on_path(const int32_t* blk, const int32_t* par, int r, int b) {
 
 __global__ void k_sync_wc_warp(KView k, SyncArgs a, const int32_t* __restrict__ list, const int32_t* count,
                                int64_t list_cap, int32_t* slow_list, int32_t* slow_count) {
+  pdl_wait();
   extern __shared__ int32_t smw[];
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, wpc = blockDim.x >> 5;
   int32_t* blk = smw + (size_t)wid * kWcSmemInts;
@@ -513,6 +516,7 @@ __host__ __device__ inline size_t sync_slow_bytes_per_worker(int B) {
 
 // compact list of waiting instructions (so no lane idles on non-waits)
 __global__ void k_wait_list(KView k, Range own, int32_t* __restrict__ list, int32_t* count) {
+  pdl_wait();
   for (int i0 = blockIdx.x * blockDim.x; i0 < k.N; i0 += gridDim.x * blockDim.x) {
     const int i = i0 + threadIdx.x;
     bool w = false;
@@ -534,6 +538,7 @@ __global__ void k_wait_list(KView k, Range own, int32_t* __restrict__ list, int3
 // barriers 1..6, intel tokens 0..31.  Overflowing items go to the slow list.
 template <bool SLOW>
 __global__ void k_sync(KView k, SyncArgs a, char* scratch, int nworkers) {
+  pdl_wait();
   const int dialect = k.dialect;
   int n_items, stride, start;
   if (SLOW) {
@@ -742,6 +747,7 @@ __host__ __device__ inline size_t sync_smem_bytes(int N, int B, int threads) {
 }
 
 __global__ void k_sync_wc_smem(KView k, SyncArgs a, const uint32_t* __restrict__ bev_g) {
+  pdl_wait();
   extern __shared__ __align__(16) unsigned char sm_raw[];
   const int N = k.N, B = k.B;
   SmemCarve cv{sm_raw};
@@ -872,6 +878,7 @@ template __global__ void k_sync<true>(KView, SyncArgs, char*, int);
 // ---- group raw keys by producer, dedup, append after the raw/guard edges ----
 __global__ void k_key_hist(const uint64_t* __restrict__ keys, const int32_t* n_dev, int64_t cap,
                            int32_t* __restrict__ cnt) {
+  pdl_wait();
   int64_t n = min((int64_t)*n_dev, cap);
   for (int64_t x = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; x < n; x += (int64_t)gridDim.x * blockDim.x)
     atomicAdd(&cnt[(int)(keys[x] >> 32)], 1);
@@ -879,6 +886,7 @@ __global__ void k_key_hist(const uint64_t* __restrict__ keys, const int32_t* n_d
 __global__ void k_key_scatter(const uint64_t* __restrict__ keys, const int32_t* n_dev, int64_t cap,
                               const int32_t* __restrict__ off, int32_t* __restrict__ cursor,
                               uint64_t* __restrict__ out) {
+  pdl_wait();
   int64_t n = min((int64_t)*n_dev, cap);
   for (int64_t x = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; x < n; x += (int64_t)gridDim.x * blockDim.x) {
     int p = (int)(keys[x] >> 32);
@@ -889,6 +897,7 @@ __global__ void k_sync_emit(int N, int kind, const uint64_t* __restrict__ sorted
                             const int32_t* __restrict__ off, const int32_t* __restrict__ uniq,
                             const int32_t* __restrict__ uoff, const int32_t* n_regular,
                             LeoEdges out, uint32_t* status) {
+  pdl_wait();
   const int base = *n_regular;
   for (int p = blockIdx.x * blockDim.x + threadIdx.x; p < N; p += gridDim.x * blockDim.x) {
     int n = uniq[p], o = base + uoff[p];
@@ -904,6 +913,7 @@ __global__ void k_sync_emit(int N, int kind, const uint64_t* __restrict__ sorted
 // counts are clamped to the capacity so downstream kernels never read past the
 // buffers; an overflow is signalled in the status word and the host re-runs.
 __global__ void k_edge_totals(const int32_t* n_regular, const int32_t* n_sync, LeoEdges out, uint32_t* status) {
+  pdl_wait();
   int r = *n_regular, t = *n_regular + *n_sync;
   if (t > out.capacity) atomicOr(status, (uint32_t)LEO_ST_EDGE_OVERFLOW);
   *out.n_regular = min(r, out.capacity);
