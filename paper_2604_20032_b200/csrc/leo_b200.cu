@@ -286,6 +286,8 @@ int build_graph_impl(const LeoKernel* kk, const LeoCaps* caps, LeoEdges* out, Le
     TRACED(KID_SEGSORT, leo_launch(segsort_unique_u64, grid_for(N, 128), 128, 0, st, ssorted, poff, pcnt, nullptr, N, puniq, cap_sync));
     TRACED(KID_SCAN, scan_exclusive(puniq, puoff, nullptr, N, scan_tmp2, &ctr[6], st));
   }
+  // (a fused one-CTA count + scan is latency-bound on the operand loads: the
+  // grid-wide count and two single-pass scans are faster)
   TRACED(KID_UNIT_COUNTS, leo_launch(k_unit_counts, grid_for(N, T), T, 0, st, k, ucnt, dcnt));
   TRACED(KID_SCAN, scan_exclusive(ucnt, use_ptr, nullptr, N, scan_tmp, nullptr, st));
   TRACED(KID_SCAN, scan_exclusive(dcnt, def_ptr, nullptr, N, scan_tmp, nullptr, st));

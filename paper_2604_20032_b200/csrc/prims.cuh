@@ -194,6 +194,19 @@ __global__ void segsort_unique_u64(uint64_t* __restrict__ keys, const int32_t* _
     if ((int64_t)begin[s] + n > cap) { uniq[s] = 0; continue; }
     uint64_t* a = keys + begin[s];
     if (n <= 1) { uniq[s] = n; continue; }
+    if (n <= 4) {
+      // register sorting network (no local-memory array): the common case
+      uint64_t r0 = a[0], r1 = a[1], r2 = n > 2 ? a[2] : ~0ull, r3 = n > 3 ? a[3] : ~0ull;
+      auto cs = [](uint64_t& x, uint64_t& y) { const uint64_t lo = x < y ? x : y; y = x < y ? y : x; x = lo; };
+      cs(r0, r1); cs(r2, r3); cs(r0, r2); cs(r1, r3); cs(r1, r2);
+      int u = 0;
+      a[u++] = r0;
+      if (r1 != r0) a[u++] = r1;
+      if (n > 2 && r2 != r1) a[u++] = r2;
+      if (n > 3 && r3 != r2) a[u++] = r3;
+      uniq[s] = u;
+      continue;
+    }
     if (n <= 24) {
       uint64_t r[24];
       for (int i = 0; i < n; i++) r[i] = a[i];
