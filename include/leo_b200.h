@@ -244,6 +244,10 @@ const char* leo_kernel_name(int id);
 /* per-CTA phase marks of kernel slot `slot` (0 reach, 1 waitcnt, 2 prune):
  * out[cta * 8 + phase] = clock64 delta from the CTA's start (LEO_DBG_PHASES) */
 int leo_debug_phases(int32_t slot, int64_t* out, int32_t n_ctas);
+/* build_graph work counters of the last LEO_DBG_PHASES call: [0] queries,
+ * [2] reach tier-2 items, [7] tier-3 items, [3] sync keys, [4] exact-walker
+ * items, [8] waits, [10] waitcnt warp-tier items */
+int leo_debug_tiers(int32_t* out);
 /* per-item clock64 cycles of the shared-memory waitcnt tier (LEO_DBG_PHASES) */
 int leo_debug_items(int64_t* out, int32_t n);
 

@@ -102,6 +102,10 @@ struct PySum {
 // ---- profiling aid: per-CTA phase marks (LEO_DBG_PHASES) ----------------------
 __device__ long long g_phase_ts[4][1024][8];
 __device__ long long g_item_cycles[8192];      // per-item cycles of the waitcnt tier
+__device__ int g_tier_counts[16];              // build_graph counters (LEO_DBG_PHASES)
+__global__ void k_copy_counts(const int32_t* ctr, int n) {
+  for (int i = threadIdx.x; i < n && i < 16; i += blockDim.x) g_tier_counts[i] = ctr[i];
+}
 struct PhaseMarks {
   int on; long long t0;
   LEO_DEV PhaseMarks(int dbg) {

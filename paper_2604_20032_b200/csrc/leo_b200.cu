@@ -177,6 +177,7 @@ void set_smem_attributes() {
   cudaFuncSetAttribute(k_sync_wc_warp, cudaFuncAttributeMaxDynamicSharedMemorySize, 4 * kWcSmemInts * 4);
   cudaFuncSetAttribute(k_reach_unit, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemResidentMax);
   cudaFuncSetAttribute(k_sync_wc_smem, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemResidentMax);
+  cudaFuncSetAttribute(k_sync_setter_smem, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kDHBytes);
   cudaFuncSetAttribute(k_prune_edges_smem<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemResidentMax);
   cudaFuncSetAttribute(k_prune_edges_smem<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemResidentMax);
   done = true;
@@ -217,7 +218,7 @@ int build_graph_impl(const LeoKernel* kk, const LeoCaps* caps, LeoEdges* out, Le
   int32_t *ucnt, *dcnt, *use_ptr, *def_ptr, *ev_res, *q_block, *q_unit, *q_list, *q_off, *q_len, *qres;
   int32_t *ctr, *slow_list, *slow2, *slow3, *cand_cnt, *cand_off, *uniq, *eoff, *ldtab, *scan_tmp, *gtab = nullptr;
   int4* brec;
-  int32_t *pcnt, *poff, *pcur, *puniq, *puoff, *reach_scr, *scan_tmp2, *wlist, *wclist, *qtab, *rhead;
+  int32_t *pcnt, *poff, *pcur, *puniq, *puoff, *reach_scr, *scan_tmp2, *wlist, *wclist, *qtab, *rhead, *slow3s;
   uint64_t *cand, *skeys, *ssorted;
   uint32_t *wcword, *bev;
   uint8_t* setword;
@@ -235,7 +236,7 @@ int build_graph_impl(const LeoKernel* kk, const LeoCaps* caps, LeoEdges* out, Le
   ar.want(&scan_tmp, scan_scratch_ints(std::max<int64_t>(std::max<int64_t>(N, cap_cand), 1)) + 64);
   ar.want(&reach_scr, (int64_t)RW * 3 * (B + 1));
   ar.want(&scan_tmp2, scan_scratch_ints(std::max<int64_t>(N, 1)) + 64);
-  ar.want(&wlist, N); ar.want(&wclist, cap_slow);
+  ar.want(&wlist, N); ar.want(&wclist, cap_slow); ar.want(&slow3s, cap_slow);
   ar.want(&sync_scr, (int64_t)SW * sync_slow_bytes_per_worker(B));
   const int n_ids = k.dialect == LEO_INTEL ? 32 : 8;
   ar.want(&wcword, N); ar.want(&bev, B); ar.want(&setword, N); ar.want(&lastset, (int64_t)B * n_ids);
@@ -279,7 +280,16 @@ int build_graph_impl(const LeoKernel* kk, const LeoCaps* caps, LeoEdges* out, Le
     if (k.dialect == LEO_AMD)
       TRACED(KID_SYNC_WARP, leo_launch(k_sync_wc_warp, num_sms() * 2, 128, 4 * kWcSmemInts * 4, st, 
           k, sa, wclist, &ctr[10], cap_slow, slow2, &ctr[4]));
-    TRACED(KID_SYNC_SLOW, leo_launch(k_sync<true>, 1, SW, 0, st, k, sa, sync_scr, SW));
+    if (k.dialect != LEO_AMD) {
+      // setter searches: CTA per item in shared memory first; the rest (and
+      // forced-slow items) on the global-scratch workers
+      TRACED(KID_SYNC_SLOW, leo_launch(k_sync_setter_smem, SM, 32, kDHBytes, st, k, sa, slow3s, &ctr[11]));
+      SyncArgs sb = sa;
+      sb.slow_list = slow3s; sb.slow_count = &ctr[11];
+      TRACED(KID_SYNC_SLOW, leo_launch(k_sync<true>, 1, SW, 0, st, k, sb, sync_scr, SW));
+    } else {
+      TRACED(KID_SYNC_SLOW, leo_launch(k_sync<true>, 1, SW, 0, st, k, sa, sync_scr, SW));
+    }
     TRACED(KID_KEY_HIST, leo_launch(k_key_hist, grid_for(cap_sync, T), T, 0, st, skeys, &ctr[3], cap_sync, pcnt));
     TRACED(KID_SCAN, scan_exclusive(pcnt, poff, nullptr, N, scan_tmp2, nullptr, st));
     TRACED(KID_KEY_SCATTER, leo_launch(k_key_scatter, grid_for(cap_sync, T), T, 0, st, skeys, &ctr[3], cap_sync, poff, pcur, ssorted));
@@ -331,6 +341,7 @@ int build_graph_impl(const LeoKernel* kk, const LeoCaps* caps, LeoEdges* out, Le
   if (fork) link_streams(s_sync, st, sp.e[1]);   // join
   TRACED(KID_SYNC_EMIT, leo_launch(k_sync_emit, grid_for(N, T), T, 0, st, N, kind, ssorted, poff, puniq, puoff, &ctr[5], *out, status));
   TRACED(KID_EDGE_TOTALS, leo_launch(k_edge_totals, 1, 1, 0, st, &ctr[5], &ctr[6], *out, status));
+  if (caps && (caps->debug_flags & LEO_DBG_PHASES)) k_copy_counts<<<1, 32, 0, st>>>(ctr, 16);
   ar.release();
   LEO_CUDA_CHECK(cudaGetLastError());
   return 0;
@@ -542,6 +553,11 @@ int leo_events_elapsed(int32_t n, void* const* begin, void* const* end, float* m
 }
 int leo_events_destroy(int32_t n, void** events) {
   for (int i = 0; i < n; i++) cudaEventDestroy((cudaEvent_t)events[i]);
+  return 0;
+}
+
+int leo_debug_tiers(int32_t* out) {
+  LEO_CUDA_CHECK(cudaMemcpyFromSymbol(out, g_tier_counts, 16 * sizeof(int)));
   return 0;
 }
 

@@ -367,46 +367,63 @@ LEO_DEV int wc_visit_exact(const KView& k, int x, WcState& s, int& m, int& a, co
   }
   return 1;
 }
+// Exact walker (global scratch).  `onp` (optional, zeroed, one int per
+// block) marks the blocks of the current chain (O(1) on-path tests, left
+// zeroed on return); `wcword` (optional) lets packable instructions take the
+// one-load packed visitor, only big counter values reading the unpacked
+// fields.
 LEO_DEV bool trace_waitcnt_exact(const KView& k, int wait, int counter, int level, const SyncArgs& sa,
-                                 Frame* fr, int fcap, int& best_m) {
+                                 Frame* fr, int fcap, int& best_m, int32_t* onp = nullptr,
+                                 const uint32_t* wcword = nullptr) {
   WcState s;
-  s.counter = counter; s.level = level; s.wait = wait; s.nseen = 0; s.sa = nullptr;
+  s.counter = counter; s.level = level; s.wait = wait; s.nseen = 0; s.sa = &sa;
+  s.member_bit = counter == 0 ? kWcVm : kWcLgkm;
+  auto visit = [&](int x, int& m, int& a) -> int {
+    if (wcword) {
+      const uint32_t w = wcword[x];
+      if (!(w & kWcBig)) return wc_visit(w, x, s, m, a, sa);
+    }
+    return wc_visit_exact(k, x, s, m, a, sa);
+  };
+  auto onpath = [&](int top, int blk) { return onp ? onp[blk] != 0 : on_path(fr, top, blk); };
   const int b0 = k.block_of[wait];
   int m = 0, a = -1, budget = kSyncBudget;
   bool stopped = false;
   for (int x = wait - 1; x >= k.blk_first[b0]; x--) {
     if (budget == 0) { stopped = true; break; }
     budget--;
-    if (!wc_visit_exact(k, x, s, m, a, sa)) { stopped = true; break; }
+    if (!visit(x, m, a)) { stopped = true; break; }
   }
   best_m = 0;
   if (stopped) { best_m = m; return true; }
-  int top = 0;
-  fr[top++] = Frame{b0, k.pred_ptr[b0], m, a, budget};
   bool any0 = false;
   for (int q = k.pred_ptr[b0]; q < k.pred_ptr[b0 + 1]; q++) if (k.pred[q] != b0) any0 = true;
   if (!any0) { best_m = m; return true; }
+  int top = 0;
+  fr[top++] = Frame{b0, k.pred_ptr[b0], m, a, budget};
+  if (onp) onp[b0] = 1;
   while (top > 0) {
     Frame& f = fr[top - 1];
     int p = -1;
     while (f.q < k.pred_ptr[f.blk + 1]) {
       int c = k.pred[f.q++];
-      if (!on_path(fr, top, c)) { p = c; break; }
+      if (!onpath(top, c)) { p = c; break; }
     }
-    if (p < 0) { top--; continue; }
+    if (p < 0) { if (onp) onp[f.blk] = 0; top--; continue; }
     m = f.m; a = f.a; budget = f.budget; stopped = false;
     for (int x = k.blk_last[p]; x >= k.blk_first[p]; x--) {
       if (budget == 0) { stopped = true; break; }
       budget--;
-      if (!wc_visit_exact(k, x, s, m, a, sa)) { stopped = true; break; }
+      if (!visit(x, m, a)) { stopped = true; break; }
     }
     if (stopped) { best_m = max(best_m, m); continue; }
-    if (top == fcap) return false;
+    if (top == fcap) { if (onp) for (int t = 0; t < top; t++) onp[fr[t].blk] = 0; return false; }
     fr[top++] = Frame{p, k.pred_ptr[p], m, a, budget};
+    if (onp) onp[p] = 1;
     bool any = false;
     for (int q = k.pred_ptr[p]; q < k.pred_ptr[p + 1] && !any; q++)
-      if (!on_path(fr, top, k.pred[q])) any = true;
-    if (!any) { best_m = max(best_m, m); top--; }
+      if (!onpath(top, k.pred[q])) any = true;
+    if (!any) { best_m = max(best_m, m); if (onp) onp[p] = 0; top--; }
   }
   return true;
 }
@@ -507,6 +524,58 @@ LEO_DEV int setter_search(const KView& k, int wait, int id, const SyncArgs& sa, 
   return found;
 }
 
+// Dijkstra state in shared memory (one CTA per overflowed setter item): an
+// open-addressing table block -> (dist, state) and a binary heap with lazy
+// deletion.  A search never leaves the 4096-instruction budget, so it
+// settles at most 4096 blocks: 8192 table slots and a 16384-entry heap
+// always suffice (a full table / heap still reports overflow).
+constexpr int kDHSlots = 8192, kDHHeap = 16384;
+constexpr size_t kDHBytes = (size_t)kDHSlots * 9 + (size_t)kDHHeap * 8 + 64;
+
+struct DijHash {
+  int32_t* key; int32_t* dist; uint8_t* state; uint64_t* heap; int n;
+  LEO_DEV int slot(int blk) {              // existing or new slot, -1 when full
+    uint32_t h = ((uint32_t)blk * 2654435761u) >> 19;     // 13 bits
+    for (int p = 0; p < kDHSlots; p++) {
+      const int sl = (int)((h + p) & (kDHSlots - 1));
+      if (key[sl] == blk) return sl;
+      if (key[sl] == -1) { key[sl] = blk; state[sl] = 0; return sl; }
+    }
+    return -1;
+  }
+  LEO_DEV bool relax(int blk, int d) {
+    const int sl = slot(blk);
+    if (sl < 0) return false;
+    if (state[sl] == 2) return true;                       // finalised
+    if (state[sl] == 1 && dist[sl] <= d) return true;
+    state[sl] = 1; dist[sl] = d;
+    if (n == kDHHeap) return false;
+    int i = n++;
+    const uint64_t kk = ((uint64_t)(uint32_t)d << 32) | (uint32_t)blk;
+    while (i > 0) { const int pp = (i - 1) >> 1; if (heap[pp] <= kk) break; heap[i] = heap[pp]; i = pp; }
+    heap[i] = kk;
+    return true;
+  }
+  LEO_DEV bool pop(int& blk, int& d) {
+    while (n > 0) {
+      const uint64_t top = heap[0], last = heap[--n];
+      int i = 0;
+      while (true) {
+        int c = 2 * i + 1;
+        if (c >= n) break;
+        if (c + 1 < n && heap[c + 1] < heap[c]) c++;
+        if (heap[c] >= last) break;
+        heap[i] = heap[c]; i = c;
+      }
+      if (n > 0) heap[i] = last;
+      blk = (int)(uint32_t)top; d = (int)(top >> 32);
+      const int sl = slot(blk);
+      if (sl >= 0 && state[sl] == 1 && dist[sl] == d) { state[sl] = 2; return true; }
+    }
+    return false;
+  }
+};
+
 constexpr int kFrames = 24, kDij = 64;
 
 __host__ __device__ inline size_t sync_slow_bytes_per_worker(int B) {
@@ -577,7 +646,8 @@ __global__ void k_sync(KView k, SyncArgs a, char* scratch, int nworkers) {
         uint32_t lv = counter == 0 ? k.sync_a[i] : k.sync_b[i];
         if (lv == LEO_NONE_U32) continue;
         int best_m = 0;
-        bool ok = SLOW ? trace_waitcnt_exact(k, i, counter, (int)min(lv, 0x7FFFFFFFu), a, fr, fcap, best_m)
+        bool ok = SLOW ? trace_waitcnt_exact(k, i, counter, (int)min(lv, 0x7FFFFFFFu), a, fr, fcap, best_m,
+                                             stamp, a.wcword)
                        : (!(a.dbg & LEO_DBG_SYNC_SLOW) && lv < kWcNone &&
                           trace_waitcnt_one(k, i, counter, (int)lv, a, fr, fcap, best_m));
         if (!ok) {
@@ -870,6 +940,37 @@ __global__ void k_sync_wc_smem(KView k, SyncArgs a, const uint32_t* __restrict__
     else atomicOr(a.status, (uint32_t)LEO_ST_SCRATCH_OVERFLOW);
   }
   pm.mark(1, 3);
+}
+
+// Setter searches that overflowed the thread tier's 64-node Dijkstra (nvidia
+// barriers / intel SWSB tokens): one CTA per item, the search state in shared
+// memory (DijHash); items still overflowing go to the global-scratch worker.
+__global__ void k_sync_setter_smem(KView k, SyncArgs a, int32_t* slow_out, int32_t* slow_out_count) {
+  pdl_wait();
+  extern __shared__ __align__(16) unsigned char sm_raw[];
+  SmemCarve cv{sm_raw};
+  uint64_t* heap = cv.take<uint64_t>(kDHHeap);
+  int32_t* key = cv.take<int32_t>(kDHSlots);
+  int32_t* dist = cv.take<int32_t>(kDHSlots);
+  uint8_t* state = cv.take<uint8_t>(kDHSlots);
+  const int n_items = (int)min((int64_t)*a.slow_count, a.slow_cap);
+  for (int t = blockIdx.x; t < n_items; t += gridDim.x) {
+    for (int x = threadIdx.x; x < kDHSlots; x += blockDim.x) key[x] = -1;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      const int it = a.slow_list[t], i = it >> 6, id = it & 63;
+      DijHash dj{key, dist, state, heap, 0};
+      const int f = (a.dbg & LEO_DBG_SYNC_SLOW) ? -1 : setter_search(k, i, id, a, dj);
+      if (f < 0) {
+        const int s2 = atomicAdd(slow_out_count, 1);
+        if (s2 < a.slow_cap) slow_out[s2] = it;
+        else atomicOr(a.status, (uint32_t)LEO_ST_SCRATCH_OVERFLOW);
+      } else if (!f) {
+        diag_push(a.diags, a.status, LEO_DIAG_NO_SETTER, i, id, 0, 0, id);
+      }
+    }
+    __syncthreads();
+  }
 }
 
 template __global__ void k_sync<false>(KView, SyncArgs, char*, int);
