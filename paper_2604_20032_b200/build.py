@@ -53,6 +53,27 @@ def build(force: bool = False, verbose: bool = False) -> Path:
     return LIB
 
 
+FRONT = PKG / "libleo_front.so"
+FRONT_SRC = PKG / "native" / "leo_front.cpp"
+
+
+def build_front(force: bool = False) -> Path:
+    """Host-only C++ listing front-end (native/leo_front.cpp -> libleo_front.so)."""
+    hdr = PKG.parent / "include" / "leo_front.h"
+    if not force and FRONT.exists() and FRONT.stat().st_mtime >= max(FRONT_SRC.stat().st_mtime,
+                                                                     hdr.stat().st_mtime):
+        return FRONT
+    cmd = [os.environ.get("CXX", "g++"), "-O2", "-std=c++17", "-fPIC", "-shared", "-Wall",
+           "-o", str(FRONT) + ".tmp", str(FRONT_SRC)]
+    r = subprocess.run(cmd, capture_output=True, text=True)
+    if r.returncode != 0:
+        sys.stderr.write(r.stdout + r.stderr)
+        raise RuntimeError("g++ failed building libleo_front.so")
+    os.replace(str(FRONT) + ".tmp", FRONT)
+    return FRONT
+
+
 if __name__ == "__main__":
+    build_front(force="--force" in sys.argv)
     build(force="--force" in sys.argv, verbose="-v" in sys.argv)
     print(LIB)

@@ -28,6 +28,16 @@ def test_library_exports_every_declared_symbol():
     assert L.leo_abi_version() == 1
 
 
+def test_front_library_exports_every_declared_symbol():
+    from paper_2604_20032_b200 import build
+    L = C.CDLL(str(build.build_front()))
+    text = (ROOT / "include" / "leo_front.h").read_text()
+    names = sorted(set(re.findall(r"(leo_front_\w+)\s*\(", text)))
+    assert len(names) >= 8
+    for n in names:
+        assert hasattr(L, n), n
+
+
 def test_library_is_sm100a():
     import subprocess
     out = subprocess.run(["/usr/local/cuda/bin/cuobjdump", "--list-elf",
