@@ -65,3 +65,36 @@ def test_device_report_matches_reference(report_cases):
                 i = next((x for x, (p, q) in enumerate(zip(got, want)) if p != q), min(len(got), len(want)))
                 bad.append((ks.name, kind, got[max(0, i - 80):i + 40], want[max(0, i - 80):i + 40]))
     assert not bad, f"{len(bad)} report renderings differ: {bad[:5]}"
+
+
+@pytest.mark.gpu
+def test_listing_text_to_report_end_to_end(report_cases):
+    """Listing text -> native front-end -> device analysis + report assembly
+    -> rendered report, byte-identical to the reference's corpus reports
+    (profile SoA from the golden fixture: profile JSON loading stays on the
+    reference side)."""
+    torch = pytest.importorskip("torch")
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    from conftest import GOLDEN
+    from paper_2604_20032_b200 import api, front, report
+    z = np.load(GOLDEN / "front.npz")
+    fcases, tables = json.loads(str(z["cases"])), json.loads(str(z["tables"]))
+    checked = 0
+    for ks_ref, pf, cfg, exp in report_cases:
+        if not ks_ref.name.startswith("corpus_"):
+            continue
+        d = ks_ref.dialect
+        text = next(c["text"] for c in fcases if c["dialect"] == d and "ltimes_noview" in c["text"][:400])
+        ks, meta = front.parse_kernels_soa(d, text, tables[d])["ltimes_noview"]
+        rmeta = json.loads(str(exp["rmeta"][0]))
+        rm = report.meta_from_fixture(rmeta, meta["mnemonics"],
+                                      [s if s is not None else "" for s in meta["src_locs"]])
+        ks.prefix_diagnostics = ks_ref.prefix_diagnostics       # attach diagnostics (profile side)
+        rep = api.build_report_soa(ks, pf, golden_io.config_of(cfg, d), rm, top_n=rmeta["top_n"],
+                                   include_unsampled=rmeta["include_unsampled"],
+                                   chain_depth=rmeta["chain_depth"])
+        assert report.render_text(rep) == str(exp["text"][0]), ks_ref.name
+        assert report.render_structured(rep) == str(exp["json"][0]), ks_ref.name
+        checked += 1
+    assert checked == 9
