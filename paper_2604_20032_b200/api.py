@@ -376,6 +376,10 @@ class Session:
         self.h_lb = self._pinned(an.line_blame)
         self.h_ls = self._pinned(an.line_stall)
         cap = an.caps.blame
+        # blame entries: the graph copies a prefix sized from this sizing run
+        # (the count is a device value); a longer result copies its tail
+        nbl0 = int(an.counts()[device.C_BLAME])
+        self.k_pre = min(cap, int(nbl0 * 1.1) + 256)
         self.h_st = torch.empty(cap, dtype=torch.int32).pin_memory()
         self.h_ed = torch.empty(cap, dtype=torch.int32).pin_memory()
         self.h_bl = torch.empty(cap, dtype=torch.float64).pin_memory()
@@ -389,6 +393,10 @@ class Session:
             self.h_ctr.copy_(an.ctr, non_blocking=True)
             self.h_lb.copy_(an.line_blame, non_blocking=True)
             self.h_ls.copy_(an.line_stall, non_blocking=True)
+            k = self.k_pre
+            self.h_st[:k].copy_(an.bl_stalled[:k], non_blocking=True)
+            self.h_ed[:k].copy_(an.bl_edge[:k], non_blocking=True)
+            self.h_bl[:k].copy_(an.bl_blame[:k], non_blocking=True)
         torch.cuda.synchronize(self.dev)
         self.graph = g
 
@@ -406,12 +414,14 @@ class Session:
             c = self.h_ctr.numpy()
             nbl = int(c[device.C_BLAME])
             if c[device.C_STATUS] == 0 and nbl <= self.an.caps.blame:
-                an = self.an
-                self.h_st[:nbl].copy_(an.bl_stalled[:nbl], non_blocking=True)
-                self.h_ed[:nbl].copy_(an.bl_edge[:nbl], non_blocking=True)
-                self.h_bl[:nbl].copy_(an.bl_blame[:nbl], non_blocking=True)
-                torch.cuda.current_stream(self.dev).synchronize()
-                self.last_d2h = (c.nbytes + self.h_lb.numel() * 8 + self.h_ls.numel() * 8 + nbl * 16)
+                an, k = self.an, self.k_pre
+                if nbl > k:                       # tail beyond the in-graph prefix
+                    self.h_st[k:nbl].copy_(an.bl_stalled[k:nbl], non_blocking=True)
+                    self.h_ed[k:nbl].copy_(an.bl_edge[k:nbl], non_blocking=True)
+                    self.h_bl[k:nbl].copy_(an.bl_blame[k:nbl], non_blocking=True)
+                    torch.cuda.current_stream(self.dev).synchronize()
+                self.last_d2h = (c.nbytes + self.h_lb.numel() * 8 + self.h_ls.numel() * 8
+                                 + max(nbl, self.k_pre) * 16)
                 return {"e_stalled": self.h_st[:nbl].numpy().copy(), "e_edge": self.h_ed[:nbl].numpy().copy(),
                         "e_blame": self.h_bl[:nbl].numpy().copy(), "line_blame": self.h_lb.numpy().copy(),
                         "line_stall": self.h_ls.numpy().copy()}
