@@ -321,8 +321,64 @@ LEO_DEV int traces_to_load(const KView& k, const int32_t* brbeg, const int32_t* 
   return 0;
 }
 
+// ---- _address_traces_to_load for every instruction at once -------------------
+// The reference BFS (analysis.py:390-411) answers: is some MEMORY_PRODUCER q
+// other than j within 8 RAW hops of j, through intermediates that are not
+// memory producers?  That is a shortest-path question, so it is computed for
+// all nodes by 7 rounds of Jacobi relaxation over the base graph's RAW
+// incoming edges, keeping per node the two nearest producer targets with
+// distinct ids (the second one answers "nearest target != j" for a load j),
+// then one evaluation round.  Runs on a side branch beside pruning.
+constexpr uint8_t kMpInf = 99;
+struct MpLab { uint8_t* d1; int32_t* t1; uint8_t* d2; int32_t* t2; };
+
+LEO_DEV void mp_insert(int d, int t, int& D1, int& T1, int& D2, int& T2) {
+  if (t == T1) { if (d < D1) D1 = d; return; }
+  if (d < D1) { D2 = D1; T2 = T1; D1 = d; T1 = t; return; }
+  if (t == T2) { if (d < D2) D2 = d; return; }
+  if (d < D2) { D2 = d; T2 = t; }
+}
+
+__global__ void k_mp_round(KView k, const int32_t* __restrict__ rbeg, const int32_t* __restrict__ rend,
+                           const int32_t* __restrict__ bprod, const uint32_t* __restrict__ bmeta,
+                           MpLab in, MpLab out, int first) {
+  pdl_wait();
+  for (int v = blockIdx.x * blockDim.x + threadIdx.x; v < k.N; v += gridDim.x * blockDim.x) {
+    int D1 = kMpInf, T1 = -1, D2 = kMpInf, T2 = -1;
+    if (!(kMemoryProducer & BIT(k.opclass[v]))) {            // producers never relay
+      for (int e = rbeg[v]; e < rend[v]; e++) {
+        if (((bmeta[e] >> 27) & 7) != LEO_EK_RAW) continue;
+        const int p = bprod[e];
+        if (kMemoryProducer & BIT(k.opclass[p])) { mp_insert(1, p, D1, T1, D2, T2); continue; }
+        if (first) continue;
+        if (in.d1[p] < 8) mp_insert(in.d1[p] + 1, in.t1[p], D1, T1, D2, T2);
+        if (in.d2[p] < 8) mp_insert(in.d2[p] + 1, in.t2[p], D1, T1, D2, T2);
+      }
+    }
+    out.d1[v] = (uint8_t)D1; out.t1[v] = T1; out.d2[v] = (uint8_t)D2; out.t2[v] = T2;
+  }
+}
+
+__global__ void k_mp_final(KView k, const int32_t* __restrict__ rbeg, const int32_t* __restrict__ rend,
+                           const int32_t* __restrict__ bprod, const uint32_t* __restrict__ bmeta, MpLab lab,
+                           uint8_t* __restrict__ ok) {
+  pdl_wait();
+  for (int j = blockIdx.x * blockDim.x + threadIdx.x; j < k.N; j += gridDim.x * blockDim.x) {
+    bool hit = false;
+    for (int e = rbeg[j]; e < rend[j] && !hit; e++) {
+      if (((bmeta[e] >> 27) & 7) != LEO_EK_RAW) continue;
+      const int p = bprod[e];
+      if (kMemoryProducer & BIT(k.opclass[p])) { hit = p != j; continue; }
+      const int d = lab.t1[p] != j ? lab.d1[p] : lab.d2[p];   // nearest target other than j
+      hit = d + 1 <= 8;
+    }
+    ok[j] = hit ? 1 : 0;
+  }
+}
+
 struct BlameArgs {
   int32_t dbg;
+  const uint8_t* mp_ok;       // per-instruction _address_traces_to_load (null: search here)
   Range own;
   PView p;
   const int32_t* pprod;
@@ -405,7 +461,9 @@ __global__ void k_blame(KView k, BlameArgs a) {
       }
       if (self) {
         int sub = dominant_self(a.p, j);
-        if (sub == LEO_SB_MEMORY_LATENCY && (kMemoryClasses & BIT(k.opclass[j]))) {
+        if (sub == LEO_SB_MEMORY_LATENCY && (kMemoryClasses & BIT(k.opclass[j])) && a.mp_ok) {
+          if (a.mp_ok[j]) sub = LEO_SB_INDIRECT_ADDRESSING;
+        } else if (sub == LEO_SB_MEMORY_LATENCY && (kMemoryClasses & BIT(k.opclass[j]))) {
           // _address_traces_to_load: small searches inline (<= kSeenCap nodes),
           // larger ones in k_selfblame_warp (warp per candidate)
           int32_t seen[kSeenCap];

@@ -27,14 +27,14 @@ enum KernelId {
   KID_REACH_SLOW, KID_LINK_COUNT, KID_LINK_FILL, KID_SEGSORT, KID_LINK_EMIT, KID_SYNC,
   KID_SYNC_SLOW, KID_KEY_HIST, KID_KEY_SCATTER, KID_SYNC_EMIT, KID_EDGE_TOTALS, KID_PRUNE,
   KID_PRUNE_SLOW, KID_COMPACT, KID_SEG_BOUNDS, KID_SYNC_HIST, KID_SYNC_FILL, KID_BLAME_COUNT,
-  KID_SELFBLAME_SLOW, KID_BLAME_FILL, KID_BLAME_TOTAL, KID_LINES, KID_SLICE, KID_REACH_WARP, KID_RUN_HEADS, KID_BIN_HIST, KID_BIN_PLAN, KID_BIN_SCATTER, KID_SYNC_PACK, KID_SYNC_WARP, KID_SELFBLAME_WARP, KID_COUNT_
+  KID_SELFBLAME_SLOW, KID_BLAME_FILL, KID_BLAME_TOTAL, KID_LINES, KID_SLICE, KID_REACH_WARP, KID_RUN_HEADS, KID_BIN_HIST, KID_BIN_PLAN, KID_BIN_SCATTER, KID_SYNC_PACK, KID_SYNC_WARP, KID_SELFBLAME_WARP, KID_SELF_ADDR, KID_COUNT_
 };
 const char* const kKernelNames[] = {
   "bin_samples", "bin_finalize", "unit_counts", "scan", "block_walk", "reach_fast",
   "reach_slow", "link_count", "link_fill", "segsort_unique", "link_emit", "sync_trace",
   "sync_trace_slow", "key_hist", "key_scatter", "sync_emit", "edge_totals", "prune_edges",
   "prune_slow", "compact", "seg_bounds", "sync_hist", "sync_fill", "blame_count",
-  "selfblame_slow", "blame_fill", "blame_total", "lines", "slice", "reach_warp", "run_heads", "bin_hist", "bin_plan", "bin_scatter", "sync_pack", "sync_warp", "selfblame_warp",
+  "selfblame_slow", "blame_fill", "blame_total", "lines", "slice", "reach_warp", "run_heads", "bin_hist", "bin_plan", "bin_scatter", "sync_pack", "sync_warp", "selfblame_warp", "self_addr",
 };
 
 struct TraceScope {
@@ -146,7 +146,7 @@ inline int64_t pick(int64_t hint, int64_t dflt) { return hint > 0 ? hint : dflt;
 // (independent stages run as parallel branches; under stream capture they
 // become parallel branches of the CUDA graph).  Created once per host thread.
 struct SidePool {
-  cudaStream_t s[3] = {nullptr, nullptr, nullptr};
+  cudaStream_t s[4] = {nullptr, nullptr, nullptr, nullptr};
   cudaEvent_t e[8] = {};
   bool ok = false;
   void init() {
@@ -441,10 +441,38 @@ int slice_impl(const LeoKernel* kk, const LeoProfile* pp, const LeoEdges* pruned
   return 0;
 }
 
+// _address_traces_to_load for all instructions (k_mp_round x7 + k_mp_final)
+// over the base graph's RAW incoming edges; the CSR is kept for blame.
+struct AddrBufs {
+  IncomingBufs bb;
+  uint8_t *d1a, *d2a, *d1b, *d2b, *ok;
+  int32_t *t1a, *t2a, *t1b, *t2b;
+};
+void want_addr(Arena& ar, AddrBufs& b, int N) {
+  want_incoming(ar, b.bb, N, 1);
+  ar.want(&b.d1a, N); ar.want(&b.d2a, N); ar.want(&b.d1b, N); ar.want(&b.d2b, N); ar.want(&b.ok, N);
+  ar.want(&b.t1a, N); ar.want(&b.t2a, N); ar.want(&b.t1b, N); ar.want(&b.t2b, N);
+}
+Incoming addr_impl(const KView& k, const LeoEdges* base, AddrBufs& b, LeoTrace* tr, cudaStream_t st) {
+  Incoming binc = build_incoming(b.bb, k.N, base, false, tr, st);   // RAW edges only
+  MpLab A{b.d1a, b.t1a, b.d2a, b.t2a}, Bl{b.d1b, b.t1b, b.d2b, b.t2b};
+  const int g = grid_for(k.N, 256);
+  TRACED(KID_SELF_ADDR, leo_launch(k_mp_round, g, 256, 0, st, k, binc.rbeg, binc.rend, base->prod, base->meta, A, A, 1));
+  for (int r = 1; r < 7; r++) {
+    const MpLab& in = (r & 1) ? A : Bl;
+    const MpLab& out = (r & 1) ? Bl : A;
+    TRACED(KID_SELF_ADDR, leo_launch(k_mp_round, g, 256, 0, st, k, binc.rbeg, binc.rend, base->prod, base->meta, in, out, 0));
+  }
+  // round r writes Bl when r is odd, A when even: round 6 (the last) wrote A
+  TRACED(KID_SELF_ADDR, leo_launch(k_mp_final, g, 256, 0, st, k, binc.rbeg, binc.rend, base->prod, base->meta, A, b.ok));
+  return binc;
+}
+
 int blame_impl(const LeoKernel* kk, const LeoProfile* pp, const LeoEdges* pruned, const LeoPaths* paths,
                const LeoEdges* base, const Incoming& inc, const int32_t* line_id, int32_t n_lines,
                LeoBlame* out, double* line_blame, double* line_stall, const LeoCaps* caps,
-               uint32_t* status, cudaStream_t st, Range own = Range{0, 0}) {
+               uint32_t* status, cudaStream_t st, Range own = Range{0, 0},
+               const Incoming* binc_pre = nullptr, const uint8_t* mp_ok_pre = nullptr) {
   LeoTrace* tr = caps ? caps->trace : nullptr;
   KView k = make_kview(kk);
   const int N = k.N;
@@ -452,10 +480,12 @@ int blame_impl(const LeoKernel* kk, const LeoProfile* pp, const LeoEdges* pruned
   const int64_t cap_slow = pick(caps ? caps->slow_items : 0, N / 4 + 1024);
   const int BW = 64;
   Arena ar{st};
-  IncomingBufs bb;
+  AddrBufs ab;
   int32_t *ecount, *self_sub, *eoff, *slow_list, *slow2, *ctr, *scan_tmp, *slow_scr;
   double *jtotal, *jnsum;
-  want_incoming(ar, bb, N, 1);
+  const int dbg = caps ? caps->debug_flags : 0;
+  const bool own_addr = binc_pre == nullptr;
+  if (own_addr) want_addr(ar, ab, N);
   ar.want(&ecount, N); ar.want(&self_sub, N); ar.want(&eoff, N + 1); ar.want(&slow_list, cap_slow);
   ar.want(&slow2, cap_slow);
   ar.want(&ctr, 4); ar.want(&scan_tmp, scan_scratch_ints(std::max(N, 1)) + 64);
@@ -463,12 +493,18 @@ int blame_impl(const LeoKernel* kk, const LeoProfile* pp, const LeoEdges* pruned
   LEO_CUDA_CHECK(ar.commit());
   cudaMemsetAsync(ctr, 0, 16, st);
   cudaMemsetAsync(slow_scr, 0, (size_t)BW * 2 * (N + 1) * sizeof(int32_t), st);   // stamps
-  Incoming binc = build_incoming(bb, N, base, false, tr, st);   // RAW edges only
-  BlameArgs a{caps ? caps->debug_flags : 0, own, p, pruned->prod, pruned->meta, paths->dist, inc, binc.rbeg, binc.rend, base->prod, base->meta,
+  // the indirect-addressing test comes precomputed from a side branch
+  // (leo_analyze) or is computed here; LEO_DBG_SELF_SLOW keeps the per-
+  // candidate BFS tiers instead (cross-checked against the same goldens)
+  Incoming binc = own_addr ? addr_impl(k, base, ab, tr, st) : *binc_pre;
+  const uint8_t* mp_ok = (dbg & LEO_DBG_SELF_SLOW) ? nullptr : (own_addr ? ab.ok : mp_ok_pre);
+  BlameArgs a{dbg, mp_ok, own, p, pruned->prod, pruned->meta, paths->dist, inc, binc.rbeg, binc.rend, base->prod, base->meta,
               ecount, self_sub, jtotal, jnsum, eoff, *out, slow_list, &ctr[0], cap_slow, status};
   TRACED(KID_BLAME_COUNT, leo_launch(k_blame<0>, grid_for(N, 128), 128, 0, st, k, a));
-  TRACED(KID_SELFBLAME_WARP, leo_launch(k_selfblame_warp, num_sms(), 128, 4 * kSBWarpInts * 4, st, k, a, slow2, &ctr[1]));
-  TRACED(KID_SELFBLAME_SLOW, leo_launch(k_selfblame_slow, 1, BW, 0, st, k, a, slow2, &ctr[1], slow_scr, BW));
+  if (!mp_ok) {
+    TRACED(KID_SELFBLAME_WARP, leo_launch(k_selfblame_warp, num_sms(), 128, 4 * kSBWarpInts * 4, st, k, a, slow2, &ctr[1]));
+    TRACED(KID_SELFBLAME_SLOW, leo_launch(k_selfblame_slow, 1, BW, 0, st, k, a, slow2, &ctr[1], slow_scr, BW));
+  }
   TRACED(KID_SCAN, scan_exclusive(ecount, eoff, nullptr, N, scan_tmp, nullptr, st));
   TRACED(KID_BLAME_FILL, leo_launch(k_blame<1>, grid_for(N, 128), 128, 0, st, k, a));
   TRACED(KID_BLAME_TOTAL, leo_launch(k_blame_count, 1, 1, 0, st, eoff, N, *out));
@@ -679,6 +715,15 @@ int leo_analyze(const LeoKernel* k, const LeoProfile* p, const LeoSamples* sampl
   const Range own{cfg->consumer_lo, cfg->consumer_hi};
   int r = build_graph_impl(k, caps, base, diags, status, st, own);
   if (r) return r;
+  // side branch: base-graph RAW CSR + the indirect-addressing test for all
+  // instructions, overlapping pruning; joined before blame
+  Arena ar_addr{st};
+  AddrBufs ab;
+  want_addr(ar_addr, ab, k->n_instr);
+  LEO_CUDA_CHECK(ar_addr.commit());
+  cudaStream_t s_addr = fork ? sp.s[3] : st;
+  if (fork) link_streams(st, s_addr, sp.e[6]);
+  const Incoming binc = addr_impl(make_kview(k), base, ab, tr, s_addr);
   if (samples && fork) link_streams(sp.s[1], st, sp.e[3]);
   r = prune_impl(k, p, cfg, base, pruned, paths, diags, caps, status, st);
   if (r) return r;
@@ -695,9 +740,12 @@ int leo_analyze(const LeoKernel* k, const LeoProfile* p, const LeoSamples* sampl
     r = slice_impl(k, p, pruned, inc, slice_bitmap, slice_level, tr, fork ? sp.s[2] : st);
     if (r) { ar.release(); return r; }
   }
-  r = blame_impl(k, p, pruned, paths, base, inc, line_id, n_lines, blame, line_blame, line_stall, caps, status, st, own);
+  if (fork) link_streams(s_addr, st, sp.e[7]);
+  r = blame_impl(k, p, pruned, paths, base, inc, line_id, n_lines, blame, line_blame, line_stall, caps, status, st, own,
+                 &binc, ab.ok);
   if (do_slice && fork) link_streams(sp.s[2], st, sp.e[5]);
   ar.release();
+  ar_addr.release();
   return r;
 }
 
