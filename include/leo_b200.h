@@ -110,6 +110,13 @@ typedef struct LeoKernel {
   const int32_t*  succ;
   const int32_t*  pred_ptr;   /* [B+1] predecessors sorted disasm.py:596 */
   const int32_t*  pred;
+  /* optional: the kernel is a concatenation of independent kernels (a batch,
+   * no CFG edge between members); seg_block[n_segments+1] are the members'
+   * first blocks (device), max_seg_blocks the largest member.  0 / NULL: one
+   * segment.  Shared-memory tiers then stage one member at a time. */
+  int32_t n_segments;
+  int32_t max_seg_blocks;
+  const int32_t*  seg_block;
 } LeoKernel;
 
 /* ---- per-instruction profile (profile.py:114-170, 284-329) --------------- */

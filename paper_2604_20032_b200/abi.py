@@ -7,6 +7,8 @@ from __future__ import annotations
 
 import ctypes as C
 
+import numpy as np
+
 from . import enums as E
 
 P = C.c_void_p
@@ -21,6 +23,7 @@ class LeoKernel(C.Structure):
         ("sync_kind", P), ("sync_a", P), ("sync_b", P),
         ("blk_first", P), ("blk_last", P), ("succ_ptr", P), ("succ", P),
         ("pred_ptr", P), ("pred", P),
+        ("n_segments", C.c_int32), ("max_seg_blocks", C.c_int32), ("seg_block", P),
     ]
 
 
@@ -144,6 +147,11 @@ def kernel_struct(ks, ptr) -> LeoKernel:
     for name in ("opclass", "block_of", "opnd_ptr", "opnd", "sync_kind", "sync_a", "sync_b",
                  "blk_first", "blk_last", "succ_ptr", "succ", "pred_ptr", "pred"):
         setattr(k, name, ptr(name))
+    sb = getattr(ks, "seg_block", None)
+    if sb is not None and len(sb) > 2:
+        k.n_segments = len(sb) - 1
+        k.max_seg_blocks = int(np.diff(np.asarray(sb)).max())
+        k.seg_block = ptr("seg_block")
     return k
 
 

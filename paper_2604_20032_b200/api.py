@@ -339,6 +339,8 @@ class Session:
         """Put one step's inputs into pinned host buffers (outside timing)."""
         for n in self.H2D_FIELDS:
             self._h("k_" + n, getattr(ks, n))
+        if getattr(ks, "seg_block", None) is not None:
+            self._h("k_seg_block", ks.seg_block)
         self._h("line_id", ks.line_id)
         for n in ("exec_cnt", "total", "eff", "sampled"):
             self._h("p_" + n, getattr(prof_meta, n))
@@ -354,6 +356,8 @@ class Session:
     def _h2d(self):
         for n in self.H2D_FIELDS:
             self.dk.t[n].view(-1).copy_(self._host["k_" + n], non_blocking=True)
+        if "k_seg_block" in self._host:
+            self.dk.t["seg_block"].view(-1).copy_(self._host["k_seg_block"], non_blocking=True)
         self.dk.line_id.copy_(self._host["line_id"], non_blocking=True)
         for n in ("exec_cnt", "total", "eff", "sampled"):
             getattr(self.dp, n).copy_(self._host["p_" + n], non_blocking=True)

@@ -96,7 +96,7 @@ def concat(workloads) -> Batch:
         unit_base=unit_base, n_units=int(ext.sum()),
         offset=np.concatenate([k.offset for k in ks_list]),
         line_id=np.concatenate([k.line_id for k in ks_list]).astype(np.int32),
-        lines=lines)
+        lines=lines, seg_block=boff.astype(np.int32))
     ps = [w.profile for w in workloads]
     profile = ProfileSoA(
         period=period, lat=np.concatenate([p.lat for p in ps]),

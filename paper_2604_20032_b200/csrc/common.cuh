@@ -53,6 +53,7 @@ struct KView {
 };
 
 inline KView make_kview(const LeoKernel* k) {
+  // (LeoKernel.n_segments / seg_block are read by the segment-aware tiers)
   KView v;
   v.N = k->n_instr; v.B = k->n_blocks; v.U = k->n_units; v.dialect = k->dialect;
   for (int c = 0; c < 8; c++) v.unit_base[c] = k->unit_base[c];

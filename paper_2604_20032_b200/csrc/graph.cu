@@ -289,43 +289,60 @@ __host__ __device__ inline size_t reach_unit_smem(int B, int threads) {
 
 // `parts` CTAs share one unit (each takes every parts-th query) so that
 // kernels with few register units still fill the chip.
+// Segments (LeoKernel.seg_block): a concatenated batch of independent
+// kernels is staged one member kernel at a time (per_seg CTAs per segment,
+// block ids rebased to the segment); bcap = largest segment's block count.
 __global__ void k_reach_unit(KView k, ReachArgs a, const int32_t* __restrict__ qtab,
-                             const int32_t* __restrict__ rh_g, int parts) {
+                             const int32_t* __restrict__ rh_g, int parts,
+                             const int32_t* __restrict__ seg_block, int per_seg, int bcap) {
   pdl_wait();
   extern __shared__ __align__(16) unsigned char sm_raw[];
   __shared__ int nq, rbase;
   __shared__ int swarp[33];
   __shared__ long long wmax[32];
-  const int B = k.B, Bp = a.Bp, W = (B + 31) >> 5, T = blockDim.x, tid = threadIdx.x;
+  const int Bp = a.Bp, T = blockDim.x, tid = threadIdx.x;
+  const int seg = blockIdx.x / per_seg, lcta = blockIdx.x % per_seg;
+  const int sb0 = seg_block ? seg_block[seg] : 0, sb1 = seg_block ? seg_block[seg + 1] : k.B;
+  const int B = sb1 - sb0, W = (B + 31) >> 5;
+  const int Bcp = (bcap + 3) & ~3, Wc = (bcap + 31) >> 5;
+  const int P0 = k.pred_ptr[sb0], P1 = k.pred_ptr[sb1];
   SmemCarve cv{sm_raw};
   uint64_t* bar = cv.take<uint64_t>(2);
-  int32_t* rh = cv.take<int32_t>(Bp);
-  int32_t* cell = cv.take<int32_t>(Bp);
-  int32_t* qs = cv.take<int32_t>(Bp);
-  int32_t* ql = cv.take<int32_t>(Bp);
-  int32_t* pptr = cv.take<int32_t>(B + 1);
-  int32_t* pred = cv.take<int32_t>(2 * (size_t)B + 4);
-  uint32_t* vis = cv.take<uint32_t>((size_t)W * T);
+  int32_t* rh = cv.take<int32_t>(Bcp);
+  int32_t* cell = cv.take<int32_t>(Bcp);
+  int32_t* qs = cv.take<int32_t>(Bcp);
+  int32_t* ql = cv.take<int32_t>(Bcp);
+  int32_t* pptr = cv.take<int32_t>(bcap + 1);
+  int32_t* pred = cv.take<int32_t>(2 * (size_t)bcap + 4);
+  uint32_t* vis = cv.take<uint32_t>((size_t)Wc * T);
   int32_t* stk = cv.take<int32_t>((size_t)kRUStack * T);
   int32_t* res = cv.take<int32_t>((size_t)kRURes * T);
   PhaseMarks pm(a.dbg);
   StageBar sb;
   sb.init(bar);
-  bool first = true;
-  const int part = blockIdx.x % parts;
-  for (int u = blockIdx.x / parts; u < k.U; u += gridDim.x / parts) {
+  bool first = true, rebase = false;
+  const int part = lcta % parts;
+  for (int u = lcta / parts; u < k.U; u += per_seg / parts) {
     sb.begin();
     if (first) {
-      const int E = k.pred_ptr[B];          // <= 2 per block ([target, fallthrough])
-      sb.copy(rh, rh_g, (size_t)B * 4);
-      sb.copy(pptr, k.pred_ptr, (size_t)(B + 1) * 4);
-      sb.copy(pred, k.pred, (size_t)E * 4);
+      // <= 2 predecessors per block ([target, fallthrough]); none leaves the segment
+      sb.copy(rh, rh_g + sb0, (size_t)B * 4);
+      sb.copy(pptr, k.pred_ptr + sb0, (size_t)(B + 1) * 4);
+      sb.copy(pred, k.pred + P0, (size_t)(P1 - P0) * 4);
       first = false;
+      rebase = sb0 != 0;
     }
-    sb.copy(cell, a.ldtab + (size_t)u * Bp, (size_t)B * 4);
-    sb.copy(qs, qtab + (size_t)u * Bp, (size_t)B * 4);
+    sb.copy(cell, a.ldtab + (size_t)u * Bp + sb0, (size_t)B * 4);
+    sb.copy(qs, qtab + (size_t)u * Bp + sb0, (size_t)B * 4);
     if (tid == 0) nq = 0;
     sb.commit_and_wait();
+    if (rebase) {                            // segment-local block ids
+      for (int y = tid; y < B; y += T) rh[y] -= sb0;
+      for (int y = tid; y <= B; y += T) pptr[y] -= P0;
+      for (int q = tid; q < P1 - P0; q += T) pred[q] -= sb0;
+      rebase = false;
+      __syncthreads();
+    }
     pm.mark(0, 1);
     // near[y] = last def of u in [runhead(y), y]: an inclusive max-scan of
     // key(x) = runhead(x) << 32 | (def(x) + 1).  Run heads never decrease, so

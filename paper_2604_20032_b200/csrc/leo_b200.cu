@@ -310,13 +310,19 @@ int build_graph_impl(const LeoKernel* kk, const LeoCaps* caps, LeoEdges* out, Le
   ReachArgs ra{caps ? caps->debug_flags : 0, ldtab, brec, U, Bp, q_block, q_unit, q_off, q_len, qres, cap_qres, &ctr[1],
                slow_list, &ctr[2], NU + 1024, status};
   const int dbg = caps ? caps->debug_flags : 0;
+  // segments: members of a concatenated batch are staged one at a time
+  const int n_seg = (kk->n_segments > 1 && kk->seg_block) ? kk->n_segments : 1;
+  const int bcap = n_seg > 1 ? kk->max_seg_blocks : B;
   int ru_threads = 128;
-  while (ru_threads > 32 && reach_unit_smem(B, ru_threads) > (size_t)kSmemResidentMax) ru_threads >>= 1;
-  const size_t ru_smem = reach_unit_smem(B, ru_threads);
-  const int ru_parts = std::max(1, std::min(8, (2 * SM + U - 1) / std::max(U, 1)));
+  while (ru_threads > 32 && reach_unit_smem(bcap, ru_threads) > (size_t)kSmemResidentMax) ru_threads >>= 1;
+  const size_t ru_smem = reach_unit_smem(bcap, ru_threads);
+  const int ru_parts = n_seg > 1 ? 1 : std::max(1, std::min(8, (2 * SM + U - 1) / std::max(U, 1)));
+  const int per_seg = n_seg > 1 ? std::max(1, std::min(U, (4 * SM + n_seg - 1) / n_seg))
+                                : std::min(U, SM * 8) * ru_parts;
   if (B > 0 && U > 0 && ru_smem <= (size_t)kSmemResidentMax && !(dbg & LEO_DBG_NO_SMEM)) {
     // tier 0: the CFG and one unit's columns resident in shared memory, CTA per unit
-    TRACED(KID_REACH_FAST, leo_launch(k_reach_unit, std::min(U, SM * 8) * ru_parts, ru_threads, ru_smem, st, k, ra, qtab, rhead, ru_parts));
+    TRACED(KID_REACH_FAST, leo_launch(k_reach_unit, n_seg * per_seg, ru_threads, ru_smem, st, k, ra, qtab, rhead, ru_parts,
+                                                 n_seg > 1 ? kk->seg_block : nullptr, per_seg, bcap));
   } else {
     // tier 1 is persistent: enough CTAs to fill the chip, queries fetched dynamically
     TRACED(KID_REACH_FAST, leo_launch(k_reach_fast, std::max(1, std::min<int>(grid_for(NU, kT1Threads), SM * 3)), kT1Threads,

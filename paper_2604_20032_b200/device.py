@@ -45,6 +45,8 @@ class DeviceKernel:
         self.ks = ks
         self.device = torch.device(device)
         self.t = {n: to_device(getattr(ks, n), self.device) for n in K_ARRAYS}
+        if getattr(ks, "seg_block", None) is not None:
+            self.t["seg_block"] = to_device(np.asarray(ks.seg_block, dtype=np.int32), self.device)
         self.line_id = to_device(np.asarray(ks.line_id, dtype=np.int32), self.device)
         self.n_lines = int(len(ks.lines)) if ks.lines is not None else int(ks.line_id.max()) + 1
         self.struct = abi.kernel_struct(ks, lambda n: self.t[n].data_ptr())

@@ -50,6 +50,7 @@ class KernelSoA:
     line_id: np.ndarray          # i32[N]   index into `lines`
     lines: list = field(default_factory=list)       # line key strings
     prefix_diagnostics: tuple = ()                  # attach + cfg diagnostics
+    seg_block: np.ndarray | None = None             # batches: members' first blocks [S+1]
 
     @property
     def n_instr(self) -> int:
