@@ -73,6 +73,7 @@ std::vector<std::string> split_ws(const std::string& s) {   // str.split()
 }
 std::vector<std::string> splitlines(const std::string& t) {   // str.splitlines() (ASCII breaks)
   std::vector<std::string> out;
+  out.reserve(t.size() / 32 + 16);
   size_t i = 0, n = t.size();
   while (i < n) {
     size_t j = i;
@@ -541,7 +542,8 @@ std::vector<std::pair<std::string, std::vector<Instr>>> parse_listing(int d, con
       rest = rest.substr(0, bpos);
     }
     in.oc = table.classify(in.mnemonic);
-    std::vector<std::pair<Reg, bool>> regs;
+    thread_local std::vector<std::pair<Reg, bool>> regs;
+    regs.clear();
     int64_t vm = -1, lg = -1;
     {
       const std::string body = strip(rest);
@@ -602,6 +604,7 @@ std::vector<std::pair<std::string, std::vector<Instr>>> parse_listing(int d, con
         }
       }
     }
+    in.srcs.reserve(regs.size());
     if (source_only(in.oc) || regs.empty()) {
       for (auto& r : regs) in.srcs.push_back(r.first);
     } else {
@@ -649,6 +652,7 @@ bool is_cond(const Instr& i) {
 void build(Kernel& K) {
   auto& ins = K.ins;
   const int n = (int)ins.size();
+  K.opnd.reserve((size_t)n * 4);
   if (n == 0) fail("kernel " + py_repr(K.name) + " has no instructions");
   std::unordered_map<std::string, int> labels;
   for (int i = 0; i < n; i++)
