@@ -254,10 +254,17 @@ def run_ours(args, ws, rank, local):
     from paper_2604_20032_b200 import api, device, roofline
     from paper_2604_20032_b200 import dist as D
 
-    torch.cuda.set_device(local)
-    dev = torch.device("cuda", local)
+    # LEO_BENCH_SHARE_GPU=1 (testing only): every rank on cuda:0 over gloo, so
+    # the multi-rank path can be exercised on a one-GPU box
+    share = os.environ.get("LEO_BENCH_SHARE_GPU") == "1"
+    dev_index = 0 if share else local
+    torch.cuda.set_device(dev_index)
+    dev = torch.device("cuda", dev_index)
     if ws > 1:
-        dist.init_process_group("nccl", device_id=dev)
+        if share:
+            dist.init_process_group("gloo")
+        else:
+            dist.init_process_group("nccl", device_id=dev)
     plan = build_plan(args, ws, rank, dev)
     first = plan.items[0]
     an0, wl0 = first["an"], first["wl"]
