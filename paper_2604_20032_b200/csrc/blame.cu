@@ -330,7 +330,15 @@ LEO_DEV int traces_to_load(const KView& k, const int32_t* brbeg, const int32_t* 
 // distinct ids (the second one answers "nearest target != j" for a load j),
 // then one evaluation round.  Runs on a side branch beside pruning.
 constexpr uint8_t kMpInf = 99;
-struct MpLab { uint8_t* d1; int32_t* t1; uint8_t* d2; int32_t* t2; };
+// Labels pack (distance << 24 | target) in one 32-bit word per candidate
+// (target -1 -> 0xFFFFFF); a node's two candidates are one 8-byte load.
+// The RAW in-edges are first rewritten as one word per base edge (producer
+// id, flagged when it is a memory producer; -1 for other kinds), so a round
+// issues its edge loads and then its label loads independently.
+constexpr uint32_t kMpT = 0xFFFFFFu, kMpPF = 0x40000000u;
+LEO_DEV uint32_t mp_pack(int d, int t) { return ((uint32_t)d << 24) | ((uint32_t)t & kMpT); }
+LEO_DEV int mp_d(uint32_t w) { return (int)(w >> 24); }
+LEO_DEV int mp_t(uint32_t w) { const uint32_t t = w & kMpT; return t == kMpT ? -1 : (int)t; }
 
 LEO_DEV void mp_insert(int d, int t, int& D1, int& T1, int& D2, int& T2) {
   if (t == T1) { if (d < D1) D1 = d; return; }
@@ -339,38 +347,75 @@ LEO_DEV void mp_insert(int d, int t, int& D1, int& T1, int& D2, int& T2) {
   if (d < D2) { D2 = d; T2 = t; }
 }
 
-__global__ void k_mp_round(KView k, const int32_t* __restrict__ rbeg, const int32_t* __restrict__ rend,
+__global__ void k_mp_edges(KView k, const int32_t* __restrict__ n_regular, int64_t cap,
                            const int32_t* __restrict__ bprod, const uint32_t* __restrict__ bmeta,
-                           MpLab in, MpLab out, int first) {
+                           int32_t* __restrict__ ep) {
+  pdl_wait();
+  const int64_t n = min((int64_t)*n_regular, cap);
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < n; e += (int64_t)gridDim.x * blockDim.x) {
+    int w = -1;
+    if (((bmeta[e] >> 27) & 7) == LEO_EK_RAW) {
+      const int p = bprod[e];
+      w = (kMemoryProducer & BIT(k.opclass[p])) ? (int)(p | kMpPF) : p;
+    }
+    ep[e] = w;
+  }
+}
+
+constexpr int kMpUnroll = 4;
+
+__global__ void k_mp_round(KView k, const int32_t* __restrict__ rbeg, const int32_t* __restrict__ rend,
+                           const int32_t* __restrict__ ep, const uint2* __restrict__ in,
+                           uint2* __restrict__ out, int first) {
   pdl_wait();
   for (int v = blockIdx.x * blockDim.x + threadIdx.x; v < k.N; v += gridDim.x * blockDim.x) {
     int D1 = kMpInf, T1 = -1, D2 = kMpInf, T2 = -1;
     if (!(kMemoryProducer & BIT(k.opclass[v]))) {            // producers never relay
-      for (int e = rbeg[v]; e < rend[v]; e++) {
-        if (((bmeta[e] >> 27) & 7) != LEO_EK_RAW) continue;
-        const int p = bprod[e];
-        if (kMemoryProducer & BIT(k.opclass[p])) { mp_insert(1, p, D1, T1, D2, T2); continue; }
-        if (first) continue;
-        if (in.d1[p] < 8) mp_insert(in.d1[p] + 1, in.t1[p], D1, T1, D2, T2);
-        if (in.d2[p] < 8) mp_insert(in.d2[p] + 1, in.t2[p], D1, T1, D2, T2);
+      const int e1 = rend[v];
+      for (int e = rbeg[v]; e < e1; e += kMpUnroll) {
+        int q[kMpUnroll];
+        uint2 L[kMpUnroll];
+#pragma unroll
+        for (int x = 0; x < kMpUnroll; x++) q[x] = e + x < e1 ? ep[e + x] : -1;
+#pragma unroll
+        for (int x = 0; x < kMpUnroll; x++)
+          L[x] = (!first && q[x] >= 0 && !(q[x] & kMpPF)) ? in[q[x]] : make_uint2(0xFFFFFFFFu, 0xFFFFFFFFu);
+#pragma unroll
+        for (int x = 0; x < kMpUnroll; x++) {
+          if (q[x] < 0) continue;
+          if (q[x] & kMpPF) { mp_insert(1, (int)(q[x] & ~kMpPF), D1, T1, D2, T2); continue; }
+          if (first) continue;
+          if (mp_d(L[x].x) < 8) mp_insert(mp_d(L[x].x) + 1, mp_t(L[x].x), D1, T1, D2, T2);
+          if (mp_d(L[x].y) < 8) mp_insert(mp_d(L[x].y) + 1, mp_t(L[x].y), D1, T1, D2, T2);
+        }
       }
     }
-    out.d1[v] = (uint8_t)D1; out.t1[v] = T1; out.d2[v] = (uint8_t)D2; out.t2[v] = T2;
+    out[v] = make_uint2(mp_pack(D1, T1), mp_pack(D2, T2));
   }
 }
 
 __global__ void k_mp_final(KView k, const int32_t* __restrict__ rbeg, const int32_t* __restrict__ rend,
-                           const int32_t* __restrict__ bprod, const uint32_t* __restrict__ bmeta, MpLab lab,
+                           const int32_t* __restrict__ ep, const uint2* __restrict__ lab,
                            uint8_t* __restrict__ ok) {
   pdl_wait();
   for (int j = blockIdx.x * blockDim.x + threadIdx.x; j < k.N; j += gridDim.x * blockDim.x) {
     bool hit = false;
-    for (int e = rbeg[j]; e < rend[j] && !hit; e++) {
-      if (((bmeta[e] >> 27) & 7) != LEO_EK_RAW) continue;
-      const int p = bprod[e];
-      if (kMemoryProducer & BIT(k.opclass[p])) { hit = p != j; continue; }
-      const int d = lab.t1[p] != j ? lab.d1[p] : lab.d2[p];   // nearest target other than j
-      hit = d + 1 <= 8;
+    const int e1 = rend[j];
+    for (int e = rbeg[j]; e < e1 && !hit; e += kMpUnroll) {
+      int q[kMpUnroll];
+      uint2 L[kMpUnroll];
+#pragma unroll
+      for (int x = 0; x < kMpUnroll; x++) q[x] = e + x < e1 ? ep[e + x] : -1;
+#pragma unroll
+      for (int x = 0; x < kMpUnroll; x++)
+        L[x] = (q[x] >= 0 && !(q[x] & kMpPF)) ? lab[q[x]] : make_uint2(0xFFFFFFFFu, 0xFFFFFFFFu);
+#pragma unroll
+      for (int x = 0; x < kMpUnroll; x++) {
+        if (hit || q[x] < 0) continue;
+        if (q[x] & kMpPF) { hit = (int)(q[x] & ~kMpPF) != j; continue; }
+        const int d = mp_t(L[x].x) != j ? mp_d(L[x].x) : mp_d(L[x].y);   // nearest target other than j
+        hit = d + 1 <= 8;
+      }
     }
     ok[j] = hit ? 1 : 0;
   }

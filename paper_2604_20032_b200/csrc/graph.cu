@@ -26,8 +26,34 @@
 
 namespace leo {
 
-__global__ void k_unit_counts(KView k, int32_t* __restrict__ ucnt, int32_t* __restrict__ dcnt) {
+LEO_DEV int warp_incl_max(int v) {
+  const int lane = threadIdx.x & 31;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const int t = __shfl_up_sync(0xffffffffu, v, o);
+    if (lane >= o) v = max(v, t);
+  }
+  return v;
+}
+
+// Per-instruction use/def unit counts, and in the same launch the
+// fallthrough-run records of the blocks (both only read the kernel SoA).
+//
+// Fallthrough runs: runhead(b) = first block of the maximal run ending at b in
+// which every block but the first has exactly one predecessor, the previous
+// block.  A backward search entering the run at y can only leave it through
+// preds(runhead(y)), so a run is resolved with independent loads of the dense
+// last-def table instead of one search level per block.  runhead is an
+// inclusive max-scan of (b starts a run ? b : -1) over the CTA's blocks; only
+// the run entering the CTA's range from below is walked serially (one thread).
+//
+// Block record (one 16-byte load per search step):
+//   rec[y] = {h = runhead(y), np = |preds(h)|, p0, p1}
+//   np <= 2: p0/p1 are the predecessors of h; np > 2: p0 = pred_ptr[h].
+__global__ void k_unit_counts(KView k, int32_t* __restrict__ ucnt, int32_t* __restrict__ dcnt,
+                              int4* __restrict__ rec, int32_t* __restrict__ rh) {
   pdl_wait();
+  __shared__ int sw[33];
   for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < k.N; i += gridDim.x * blockDim.x) {
     int u = 0, d = 0;
     for (int q = k.opnd_ptr[i]; q < k.opnd_ptr[i + 1]; q++) {
@@ -36,6 +62,43 @@ __global__ void k_unit_counts(KView k, int32_t* __restrict__ ucnt, int32_t* __re
     }
     ucnt[i] = u;
     dcnt[i] = d;
+  }
+  if (!rec) return;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
+  for (int b0 = blockIdx.x * blockDim.x; b0 < k.B; b0 += gridDim.x * blockDim.x) {
+    const int b = b0 + threadIdx.x;
+    bool cont = false;
+    if (b < k.B && b > 0) {
+      const int q0 = k.pred_ptr[b];
+      cont = k.pred_ptr[b + 1] - q0 == 1 && k.pred[q0] == b - 1;
+    }
+    int h = warp_incl_max(cont || b >= k.B ? -1 : b);
+    if (lane == 31) sw[warp] = h;
+    __syncthreads();
+    if (warp == 0) {
+      const int w = warp_incl_max(lane < nw ? sw[lane] : -1);
+      if (lane < nw) sw[lane] = w;
+    }
+    if (threadIdx.x == 0) {
+      // head of the run entering from below b0
+      int x = b0;
+      if (cont)
+        while (x > 0 && k.pred_ptr[x + 1] - k.pred_ptr[x] == 1 && k.pred[k.pred_ptr[x]] == x - 1) x--;
+      sw[32] = x;
+    }
+    __syncthreads();
+    if (warp > 0) h = max(h, sw[warp - 1]);
+    if (h < 0) h = sw[32];
+    if (b < k.B) {
+      const int q0 = k.pred_ptr[h], np = k.pred_ptr[h + 1] - q0;
+      int4 r;
+      r.x = h; r.y = np;
+      if (np <= 2) { r.z = np > 0 ? k.pred[q0] : -1; r.w = np > 1 ? k.pred[q0 + 1] : -1; }
+      else { r.z = q0; r.w = -1; }
+      rec[b] = r;
+      rh[b] = h;
+    }
+    __syncthreads();
   }
 }
 
@@ -66,66 +129,112 @@ struct WalkArgs {
   int32_t* gtab;             // global per-warp tables (when U too large for smem) or null
 };
 
+// per-warp staging of a window of <= 32 instructions' unit events
+constexpr int kWalkUse = 384, kWalkDef = 192, kWalkLeads = 64;
+constexpr int kWalkStage = kWalkUse + kWalkDef + kWalkLeads;
+
 // warp per block; blocks visited in increasing order per warp so that stale
 // table entries (from earlier blocks) are recognisable by index comparison.
+// The block's instructions are taken 32 at a time: one lane per instruction
+// loads its event offsets and expands its operands into per-warp unit lists
+// (independent loads), then the in-order walk runs on shared memory only.
+// New query slots are buffered per warp and published with one atomic.
 __global__ void k_block_walk(KView k, WalkArgs a, int warps_per_cta) {
   pdl_wait();
   extern __shared__ int32_t smem[];
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
   const int gw = blockIdx.x * warps_per_cta + wid, nw = gridDim.x * warps_per_cta;
   const int U = k.U;
-  int32_t* last = a.gtab ? a.gtab + (size_t)gw * 2 * U : smem + (size_t)wid * 2 * U;
+  int32_t* wsm = smem + (size_t)wid * ((a.gtab ? 0 : 2 * U) + kWalkStage);
+  int32_t* last = a.gtab ? a.gtab + (size_t)gw * 2 * U : wsm;
   int32_t* qtab = last + U;
+  int32_t* evu = a.gtab ? wsm : wsm + 2 * U;
+  int32_t* evd = evu + kWalkUse;
+  int32_t* leads = evd + kWalkDef;
+  int nlead = 0;                                   // warp-uniform
+  const unsigned lt = (1u << lane) - 1;
+  auto publish = [&]() {
+    int qbase = 0;
+    if (lane == 0) qbase = atomicAdd(a.q_count, nlead);
+    qbase = __shfl_sync(0xffffffffu, qbase, 0);
+    for (int x = lane; x < nlead; x += 32) a.q_list[qbase + x] = leads[x];
+    nlead = 0;
+    __syncwarp();
+  };
   for (int u = lane; u < U; u += 32) { last[u] = -1; qtab[u] = -1; }
   __syncwarp();
   for (int b = gw; b < k.B; b += nw) {
     const int first = k.blk_first[b], lastI = k.blk_last[b];
     const int ev_block = a.use_ptr[first];
-    for (int i = first; i <= lastI; i++) {
-      const int e0 = a.use_ptr[i], e1 = a.use_ptr[i + 1];
-      for (int base = e0; base < e1; base += 32) {
-        const int e = base + lane;
-        const bool valid = e < e1;
-        int u = -1, res = 0;
-        bool fresh = false;
-        if (valid) {
-          int opos; uint32_t oref;
-          u = event_unit(k, i, e - e0, false, &opos, &oref);
-          int ld = last[u];
-          if (ld >= first) res = ld;
-          else if (qtab[u] >= ev_block) res = -(qtab[u] + 1);
-          else fresh = true;
-        }
-        // first claimant of (block, unit) creates the query: qtab[u] still
-        // holds a stale slot (< ev_block) until one lane's CAS replaces it
-        bool lead = false;
-        if (fresh) {
-          const int seen = qtab[u];
-          const int prev = atomicCAS(&qtab[u], seen, e);
-          if (prev == seen) { lead = true; res = -(e + 1); }
-          else res = -(prev + 1);          // another lane of this chunk claimed it
-        }
-        const unsigned lm = __ballot_sync(0xffffffffu, lead);
-        if (lm) {
-          int qbase = 0;
-          if (lane == 0) qbase = atomicAdd(a.q_count, __popc(lm));
-          qbase = __shfl_sync(0xffffffffu, qbase, 0);
-          if (lead) {
-            a.q_block[e] = b;
-            a.q_unit[e] = u;
-            a.q_list[qbase + __popc(lm & ((1u << lane) - 1))] = e;
-          }
-        }
-        if (valid) a.ev_res[e] = res;
-        __syncwarp();
+    for (int w0 = first; w0 <= lastI; w0 += 32) {
+      const int i = w0 + lane, nin = min(32, lastI - w0 + 1);
+      const bool in = lane < nin;
+      int u0 = 0, u1 = 0, d0 = 0, d1 = 0, q0 = 0, q1 = 0;
+      if (in) {
+        u0 = a.use_ptr[i]; u1 = a.use_ptr[i + 1];
+        d0 = a.def_ptr[i]; d1 = a.def_ptr[i + 1];
+        q0 = k.opnd_ptr[i]; q1 = k.opnd_ptr[i + 1];
       }
-      const int d0 = a.def_ptr[i], d1 = a.def_ptr[i + 1];
-      for (int d = d0 + lane; d < d1; d += 32) {
-        int opos; uint32_t oref;
-        int u = event_unit(k, i, d - d0, true, &opos, &oref);
-        last[u] = i;
+      const int ub = __shfl_sync(0xffffffffu, u0, 0), ue = __shfl_sync(0xffffffffu, u1, nin - 1);
+      const int db = __shfl_sync(0xffffffffu, d0, 0), de = __shfl_sync(0xffffffffu, d1, nin - 1);
+      const bool staged = ue - ub <= kWalkUse && de - db <= kWalkDef;
+      if (staged && in) {
+        int pu = u0 - ub, pd = d0 - db;
+        for (int q = q0; q < q1; q++) {
+          const uint32_t r = k.opnd[q];
+          const int s = op_span(r), base = unit_of(k, r);
+          if (op_role(r) == LEO_ROLE_DST) { for (int x = 0; x < s; x++) evd[pd++] = base + x; }
+          else { for (int x = 0; x < s; x++) evu[pu++] = base + x; }
+        }
       }
       __syncwarp();
+      for (int j = 0; j < nin; j++) {
+        const int ii = w0 + j;
+        const int e0 = __shfl_sync(0xffffffffu, u0, j), e1 = __shfl_sync(0xffffffffu, u1, j);
+        for (int base = e0; base < e1; base += 32) {
+          const int e = base + lane;
+          const bool valid = e < e1;
+          int u = -1, res = 0;
+          bool fresh = false;
+          if (valid) {
+            if (staged) u = evu[e - ub];
+            else { int opos; uint32_t oref; u = event_unit(k, ii, e - e0, false, &opos, &oref); }
+            const int ld = last[u];
+            if (ld >= first) res = ld;
+            else if (qtab[u] >= ev_block) res = -(qtab[u] + 1);
+            else fresh = true;
+          }
+          // first claimant of (block, unit) creates the query: qtab[u] still
+          // holds a stale slot (< ev_block) until one lane's CAS replaces it
+          bool lead = false;
+          if (fresh) {
+            const int seen = qtab[u];
+            const int prev = atomicCAS(&qtab[u], seen, e);
+            if (prev == seen) { lead = true; res = -(e + 1); }
+            else res = -(prev + 1);          // another lane of this chunk claimed it
+          }
+          const unsigned lm = __ballot_sync(0xffffffffu, lead);
+          if (lm) {
+            if (nlead + __popc(lm) > kWalkLeads) publish();
+            if (lead) {
+              leads[nlead + __popc(lm & lt)] = e;
+              a.q_block[e] = b;
+              a.q_unit[e] = u;
+            }
+            nlead += __popc(lm);
+          }
+          if (valid) a.ev_res[e] = res;
+          __syncwarp();
+        }
+        const int f0 = __shfl_sync(0xffffffffu, d0, j), f1 = __shfl_sync(0xffffffffu, d1, j);
+        for (int d = f0 + lane; d < f1; d += 32) {
+          int u;
+          if (staged) u = evd[d - db];
+          else { int opos; uint32_t oref; u = event_unit(k, ii, d - f0, true, &opos, &oref); }
+          last[u] = ii;
+        }
+        __syncwarp();
+      }
     }
     // the block's last definitions (block_defs depgraph.py:143-149) and its
     // upward-exposed queries, one entry per unit column
@@ -136,30 +245,7 @@ __global__ void k_block_walk(KView k, WalkArgs a, int warps_per_cta) {
     }
     __syncwarp();
   }
-}
-
-// Fallthrough runs: runhead(b) = first block of the maximal run ending at b in
-// which every block but the first has exactly one predecessor, the previous
-// block.  A backward search entering the run at y can only leave it through
-// preds(runhead(y)), so a run is resolved with independent loads of the dense
-// last-def table instead of one search level per block.
-//
-// Block record (one 16-byte load per search step):
-//   rec[y] = {h = runhead(y), np = |preds(h)|, p0, p1}
-//   np <= 2: p0/p1 are the predecessors of h; np > 2: p0 = pred_ptr[h].
-__global__ void k_block_records(KView k, int4* __restrict__ rec, int32_t* __restrict__ rh) {
-  pdl_wait();
-  for (int b = blockIdx.x * blockDim.x + threadIdx.x; b < k.B; b += gridDim.x * blockDim.x) {
-    int x = b;
-    while (x > 0 && k.pred_ptr[x + 1] - k.pred_ptr[x] == 1 && k.pred[k.pred_ptr[x]] == x - 1) x--;
-    const int q0 = k.pred_ptr[x], np = k.pred_ptr[x + 1] - q0;
-    int4 r;
-    r.x = x; r.y = np;
-    if (np <= 2) { r.z = np > 0 ? k.pred[q0] : -1; r.w = np > 1 ? k.pred[q0 + 1] : -1; }
-    else { r.z = q0; r.w = -1; }
-    rec[b] = r;
-    rh[b] = x;
-  }
+  if (nlead) publish();
 }
 
 struct ReachArgs {

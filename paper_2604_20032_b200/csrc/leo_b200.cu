@@ -206,9 +206,11 @@ int build_graph_impl(const LeoKernel* kk, const LeoCaps* caps, LeoEdges* out, Le
   const int SM = num_sms();
 
   // per-warp unit tables in shared memory when they fit
+  auto walk_bytes = [&](int w, bool tab) { return (size_t)w * ((tab ? 2 * (size_t)U : 0) + kWalkStage) * 4; };
   int wpc = 8;
-  while (wpc > 1 && (size_t)wpc * 2 * U * 4 > 96 * 1024) wpc >>= 1;
-  const bool smem_tab = (size_t)2 * U * 4 <= 96 * 1024;
+  while (wpc > 1 && walk_bytes(wpc, true) > 96 * 1024) wpc >>= 1;
+  const bool smem_tab = walk_bytes(wpc, true) <= 96 * 1024;
+  if (!smem_tab) wpc = 8;
   const int walk_ctas = std::min<int>((B + wpc - 1) / wpc, SM * 8);
   const int walk_warps = std::max(1, walk_ctas) * wpc;
 
@@ -298,15 +300,15 @@ int build_graph_impl(const LeoKernel* kk, const LeoCaps* caps, LeoEdges* out, Le
   }
   // (a fused one-CTA count + scan is latency-bound on the operand loads: the
   // grid-wide count and two single-pass scans are faster)
-  TRACED(KID_UNIT_COUNTS, leo_launch(k_unit_counts, grid_for(N, T), T, 0, st, k, ucnt, dcnt));
+  TRACED(KID_UNIT_COUNTS, leo_launch(k_unit_counts, std::max(grid_for(N, T), grid_for(B, T)), T, 0, st, k, ucnt, dcnt,
+                                     B > 0 ? brec : nullptr, rhead));
   TRACED(KID_SCAN, scan_exclusive(ucnt, use_ptr, nullptr, N, scan_tmp, nullptr, st));
   TRACED(KID_SCAN, scan_exclusive(dcnt, def_ptr, nullptr, N, scan_tmp, nullptr, st));
 
   WalkArgs wa{use_ptr, def_ptr, ev_res, q_block, q_unit, q_list, &ctr[0], ldtab, qtab, Bp, gtab};
-  size_t smem = smem_tab ? (size_t)wpc * 2 * U * 4 : 0;
+  const size_t smem = walk_bytes(wpc, smem_tab);
   if (B > 0) TRACED(KID_BLOCK_WALK, leo_launch(k_block_walk, std::max(1, walk_ctas), wpc * 32, smem, st, k, wa, wpc));
 
-  if (B > 0) TRACED(KID_RUN_HEADS, leo_launch(k_block_records, grid_for(B, T), T, 0, st, k, brec, rhead));
   ReachArgs ra{caps ? caps->debug_flags : 0, ldtab, brec, U, Bp, q_block, q_unit, q_off, q_len, qres, cap_qres, &ctr[1],
                slow_list, &ctr[2], NU + 1024, status};
   const int dbg = caps ? caps->debug_flags : 0;
@@ -451,26 +453,27 @@ int slice_impl(const LeoKernel* kk, const LeoProfile* pp, const LeoEdges* pruned
 // over the base graph's RAW incoming edges; the CSR is kept for blame.
 struct AddrBufs {
   IncomingBufs bb;
-  uint8_t *d1a, *d2a, *d1b, *d2b, *ok;
-  int32_t *t1a, *t2a, *t1b, *t2b;
+  uint2 *la, *lb;
+  int32_t* ep;
+  uint8_t* ok;
 };
-void want_addr(Arena& ar, AddrBufs& b, int N) {
+void want_addr(Arena& ar, AddrBufs& b, int N, int64_t edge_cap) {
   want_incoming(ar, b.bb, N, 1);
-  ar.want(&b.d1a, N); ar.want(&b.d2a, N); ar.want(&b.d1b, N); ar.want(&b.d2b, N); ar.want(&b.ok, N);
-  ar.want(&b.t1a, N); ar.want(&b.t2a, N); ar.want(&b.t1b, N); ar.want(&b.t2b, N);
+  ar.want(&b.la, N); ar.want(&b.lb, N); ar.want(&b.ok, N); ar.want(&b.ep, std::max<int64_t>(edge_cap, 1));
 }
 Incoming addr_impl(const KView& k, const LeoEdges* base, AddrBufs& b, LeoTrace* tr, cudaStream_t st) {
   Incoming binc = build_incoming(b.bb, k.N, base, false, tr, st);   // RAW edges only
-  MpLab A{b.d1a, b.t1a, b.d2a, b.t2a}, Bl{b.d1b, b.t1b, b.d2b, b.t2b};
-  const int g = grid_for(k.N, 256);
-  TRACED(KID_SELF_ADDR, leo_launch(k_mp_round, g, 256, 0, st, k, binc.rbeg, binc.rend, base->prod, base->meta, A, A, 1));
+  const int g = grid_for(k.N, 128);
+  TRACED(KID_SELF_ADDR, leo_launch(k_mp_edges, grid_for(base->capacity, 256, num_sms() * 8), 256, 0, st, k,
+                                   base->n_regular, (int64_t)base->capacity, base->prod, base->meta, b.ep));
+  TRACED(KID_SELF_ADDR, leo_launch(k_mp_round, g, 128, 0, st, k, binc.rbeg, binc.rend, b.ep, b.la, b.la, 1));
   for (int r = 1; r < 7; r++) {
-    const MpLab& in = (r & 1) ? A : Bl;
-    const MpLab& out = (r & 1) ? Bl : A;
-    TRACED(KID_SELF_ADDR, leo_launch(k_mp_round, g, 256, 0, st, k, binc.rbeg, binc.rend, base->prod, base->meta, in, out, 0));
+    const uint2* in = (r & 1) ? b.la : b.lb;
+    uint2* out = (r & 1) ? b.lb : b.la;
+    TRACED(KID_SELF_ADDR, leo_launch(k_mp_round, g, 128, 0, st, k, binc.rbeg, binc.rend, b.ep, in, out, 0));
   }
-  // round r writes Bl when r is odd, A when even: round 6 (the last) wrote A
-  TRACED(KID_SELF_ADDR, leo_launch(k_mp_final, g, 256, 0, st, k, binc.rbeg, binc.rend, base->prod, base->meta, A, b.ok));
+  // round r writes lb when r is odd, la when even: round 6 (the last) wrote la
+  TRACED(KID_SELF_ADDR, leo_launch(k_mp_final, g, 128, 0, st, k, binc.rbeg, binc.rend, b.ep, b.la, b.ok));
   return binc;
 }
 
@@ -491,7 +494,7 @@ int blame_impl(const LeoKernel* kk, const LeoProfile* pp, const LeoEdges* pruned
   double *jtotal, *jnsum;
   const int dbg = caps ? caps->debug_flags : 0;
   const bool own_addr = binc_pre == nullptr;
-  if (own_addr) want_addr(ar, ab, N);
+  if (own_addr) want_addr(ar, ab, N, base->capacity);
   ar.want(&ecount, N); ar.want(&self_sub, N); ar.want(&eoff, N + 1); ar.want(&slow_list, cap_slow);
   ar.want(&slow2, cap_slow);
   ar.want(&ctr, 4); ar.want(&scan_tmp, scan_scratch_ints(std::max(N, 1)) + 64);
@@ -721,23 +724,49 @@ int leo_analyze(const LeoKernel* k, const LeoProfile* p, const LeoSamples* sampl
   const Range own{cfg->consumer_lo, cfg->consumer_hi};
   int r = build_graph_impl(k, caps, base, diags, status, st, own);
   if (r) return r;
+  // LEO_DBG_STOP=s (profiling only): end the pipeline after stage s
+  // (1 build, 2 prune, 3 incoming CSR, 4 slice) to time prefixes in a graph
+  const char* stop_env = getenv("LEO_DBG_STOP");
+  const int stop = stop_env ? atoi(stop_env) : 0;
+  if (stop == 1 || stop == 6) {                 // 6: build + pruning, no addressing branch
+    if (samples && fork) link_streams(sp.s[1], st, sp.e[3]);
+    if (stop == 6) r = prune_impl(k, p, cfg, base, pruned, paths, diags, caps, status, st);
+    return r;
+  }
   // side branch: base-graph RAW CSR + the indirect-addressing test for all
   // instructions, overlapping pruning; joined before blame
   Arena ar_addr{st};
   AddrBufs ab;
-  want_addr(ar_addr, ab, k->n_instr);
+  want_addr(ar_addr, ab, k->n_instr, base->capacity);
   LEO_CUDA_CHECK(ar_addr.commit());
   cudaStream_t s_addr = fork ? sp.s[3] : st;
   if (fork) link_streams(st, s_addr, sp.e[6]);
   const Incoming binc = addr_impl(make_kview(k), base, ab, tr, s_addr);
+  if (stop == 5) {                              // build + the addressing branch
+    if (fork) link_streams(s_addr, st, sp.e[7]);
+    if (samples && fork) link_streams(sp.s[1], st, sp.e[3]);
+    ar_addr.release();
+    return 0;
+  }
   if (samples && fork) link_streams(sp.s[1], st, sp.e[3]);
   r = prune_impl(k, p, cfg, base, pruned, paths, diags, caps, status, st);
   if (r) return r;
+  if (stop == 2) {
+    if (fork) link_streams(s_addr, st, sp.e[7]);
+    ar_addr.release();
+    return 0;
+  }
   Arena ar{st};
   IncomingBufs ib;
   want_incoming(ar, ib, k->n_instr, pruned->capacity);
   LEO_CUDA_CHECK(ar.commit());
   Incoming inc = build_incoming(ib, k->n_instr, pruned, true, tr, st);
+  if (stop == 3) {
+    if (fork) link_streams(s_addr, st, sp.e[7]);
+    ar.release();
+    ar_addr.release();
+    return 0;
+  }
   // the slice and blame attribution both read the pruned incoming CSR: run
   // them as parallel branches
   const bool do_slice = slice_level && slice_bitmap;
@@ -747,6 +776,12 @@ int leo_analyze(const LeoKernel* k, const LeoProfile* p, const LeoSamples* sampl
     if (r) { ar.release(); return r; }
   }
   if (fork) link_streams(s_addr, st, sp.e[7]);
+  if (stop == 4) {
+    if (do_slice && fork) link_streams(sp.s[2], st, sp.e[5]);
+    ar.release();
+    ar_addr.release();
+    return 0;
+  }
   r = blame_impl(k, p, pruned, paths, base, inc, line_id, n_lines, blame, line_blame, line_stall, caps, status, st, own,
                  &binc, ab.ok);
   if (do_slice && fork) link_streams(sp.s[2], st, sp.e[5]);
