@@ -178,6 +178,7 @@ void set_smem_attributes() {
   cudaFuncSetAttribute(k_reach_unit, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemResidentMax);
   cudaFuncSetAttribute(k_sync_wc_smem, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemResidentMax);
   cudaFuncSetAttribute(k_sync_setter_smem, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kDHBytes);
+  cudaFuncSetAttribute(k_sync_setter_cta, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemResidentMax);
   cudaFuncSetAttribute(k_prune_edges_smem<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemResidentMax);
   cudaFuncSetAttribute(k_prune_edges_smem<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemResidentMax);
   done = true;
@@ -265,7 +266,7 @@ int build_graph_impl(const LeoKernel* kk, const LeoCaps* caps, LeoEdges* out, Le
     cudaMemsetAsync(bev, 0, (size_t)std::max(B, 1) * 4, st);
     TRACED(KID_SYNC_PACK, leo_launch(k_sync_pack, grid_for(N, T), T, 0, st, k, wcword, setword, bev));
     if (k.dialect != LEO_AMD && B > 0)
-      TRACED(KID_SYNC_PACK, leo_launch(k_block_setters, grid_for(B, T), T, 0, st, k, setword, n_ids, lastset));
+      TRACED(KID_SYNC_PACK, leo_launch(k_block_setters, grid_for(B, T), T, 0, st, k, setword, n_ids, lastset, bev));
     TRACED(KID_SYNC_PACK, leo_launch(k_wait_list, grid_for(N, T), T, 0, st, k, own, wlist, &ctr[8]));
     SyncArgs sa{caps ? caps->debug_flags : 0, skeys, cap_sync, &ctr[3], slow2, &ctr[4], cap_slow, *diags, status,
                 wcword, setword, lastset, n_ids, wlist, &ctr[8], wclist, &ctr[10]};
@@ -285,7 +286,11 @@ int build_graph_impl(const LeoKernel* kk, const LeoCaps* caps, LeoEdges* out, Le
     if (k.dialect != LEO_AMD) {
       // setter searches: CTA per item in shared memory first; the rest (and
       // forced-slow items) on the global-scratch workers
-      TRACED(KID_SYNC_SLOW, leo_launch(k_sync_setter_smem, SM, 32, kDHBytes, st, k, sa, slow3s, &ctr[11]));
+      const size_t cta_smem = setter_cta_smem(B);
+      if (B > 0 && cta_smem <= (size_t)kSmemResidentMax && !(dbg_flags & (LEO_DBG_NO_SMEM | LEO_DBG_SYNC_SLOW)))
+        TRACED(KID_SYNC_SLOW, leo_launch(k_sync_setter_cta, SM, kSWWarps * 32, cta_smem, st, k, sa, bev, slow3s, &ctr[11]));
+      else
+        TRACED(KID_SYNC_SLOW, leo_launch(k_sync_setter_smem, SM, 32, kDHBytes, st, k, sa, slow3s, &ctr[11]));
       SyncArgs sb = sa;
       sb.slow_list = slow3s; sb.slow_count = &ctr[11];
       TRACED(KID_SYNC_SLOW, leo_launch(k_sync<true>, 1, SW, 0, st, k, sb, sync_scr, SW));

@@ -12,6 +12,9 @@ namespace leo {
 constexpr int kScanThreads = 512;
 constexpr int kScanItems = 8;
 constexpr int kScanTile = kScanThreads * kScanItems;
+// one CTA walks arrays up to this size (its latency grows with n / 1024
+// elements per thread); larger arrays take the two-launch tiled scan
+constexpr int64_t kScanSingleMax = 1 << 14;
 
 LEO_DEV int warp_incl_scan(int v) {
   const int lane = threadIdx.x & 31;
@@ -59,27 +62,23 @@ __global__ void scan_tile_sums(const int32_t* __restrict__ in, const int32_t* n_
   if (threadIdx.x == 0) tile_sums[blockIdx.x] = total;
 }
 
-// single CTA: exclusive scan of the tile sums (in place); grand total -> *total_out
-__global__ void scan_tile_prefix(int32_t* tile_sums, int ntiles, int32_t* total_out) {
-  pdl_wait();
-  __shared__ int sw[33];
-  int carry = 0;
-  for (int base = 0; base < ntiles; base += blockDim.x) {
-    int i = base + threadIdx.x;
-    int v = i < ntiles ? tile_sums[i] : 0;
-    int tot;
-    int ex = block_excl_scan(v, sw, &tot);
-    if (i < ntiles) tile_sums[i] = ex + carry;
-    carry += tot;
-  }
-  if (threadIdx.x == 0 && total_out) *total_out = carry;
-}
-
+// tile_sums are raw per-tile sums: each CTA adds up the sums of the tiles
+// before it (a few hundred L2-resident ints) instead of a separate prefix launch
 __global__ void scan_tile_apply(const int32_t* __restrict__ in, const int32_t* n_dev, int64_t n_cap,
-                                const int32_t* __restrict__ tile_sums, int32_t* __restrict__ out) {
+                                const int32_t* __restrict__ tile_sums, int32_t* __restrict__ out,
+                                int32_t* total_out) {
   pdl_wait();
   __shared__ int sw[33];
+  __shared__ int tile_base;
   int64_t n = n_dev ? (int64_t)*n_dev : n_cap;
+  {
+    int acc = 0;
+    for (int t = threadIdx.x; t < (int)blockIdx.x; t += blockDim.x) acc += tile_sums[t];
+    int tot;
+    block_excl_scan(acc, sw, &tot);
+    if (threadIdx.x == 0) tile_base = tot;
+    __syncthreads();
+  }
   int64_t base = (int64_t)blockIdx.x * kScanTile + (int64_t)threadIdx.x * kScanItems;
   int v[kScanItems];
   int s = 0;
@@ -90,7 +89,7 @@ __global__ void scan_tile_apply(const int32_t* __restrict__ in, const int32_t* n
     s += v[k];
   }
   int total;
-  int ex = block_excl_scan(s, sw, &total) + tile_sums[blockIdx.x];
+  int ex = block_excl_scan(s, sw, &total) + tile_base;
 #pragma unroll
   for (int k = 0; k < kScanItems; k++) {
     int64_t i = base + k;
@@ -99,7 +98,10 @@ __global__ void scan_tile_apply(const int32_t* __restrict__ in, const int32_t* n
   }
   // out[n] = total (CSR end) written by the last tile owner
   const int64_t last_tile = n > 0 ? (n - 1) / kScanTile : 0;
-  if ((int64_t)blockIdx.x == last_tile && threadIdx.x == 0) out[n] = tile_sums[blockIdx.x] + total;
+  if ((int64_t)blockIdx.x == last_tile && threadIdx.x == 0) {
+    out[n] = tile_base + total;
+    if (total_out) *total_out = tile_base + total;
+  }
 }
 
 // one CTA scans the whole array tile by tile (small arrays: one launch)
@@ -148,15 +150,14 @@ __global__ void __launch_bounds__(1024) scan_single_cta(const int32_t* __restric
 // given else n_cap.  scratch: >= tiles(n_cap) ints.  total_out optional.
 inline void scan_exclusive(const int32_t* in, int32_t* out, const int32_t* n_dev, int64_t n_cap,
                            int32_t* scratch, int32_t* total_out, cudaStream_t st) {
-  if (n_cap <= (1 << 18)) {
+  if (n_cap <= kScanSingleMax) {
     leo_launch(scan_single_cta, 1, 1024, 0, st, in, n_dev, n_cap, out, total_out);
     return;
   }
   int64_t ntiles = (n_cap + kScanTile - 1) / kScanTile;
   if (ntiles < 1) ntiles = 1;
   leo_launch(scan_tile_sums, (unsigned)ntiles, kScanThreads, 0, st, in, n_dev, n_cap, scratch);
-  leo_launch(scan_tile_prefix, 1, 1024, 0, st, scratch, (int)ntiles, total_out);
-  leo_launch(scan_tile_apply, (unsigned)ntiles, kScanThreads, 0, st, in, n_dev, n_cap, scratch, out);
+  leo_launch(scan_tile_apply, (unsigned)ntiles, kScanThreads, 0, st, in, n_dev, n_cap, scratch, out, total_out);
 }
 inline int64_t scan_scratch_ints(int64_t n_cap) { return (n_cap + kScanTile - 1) / kScanTile + 1; }
 

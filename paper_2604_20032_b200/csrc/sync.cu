@@ -88,20 +88,25 @@ __global__ void k_sync_pack(KView k, uint32_t* __restrict__ wcword, uint8_t* __r
   }
 }
 
+// lastset rows, and setmask[b] = the ids some instruction of block b sets
 __global__ void k_block_setters(KView k, const uint8_t* __restrict__ setword, int n_ids,
-                                int32_t* __restrict__ lastset) {
+                                int32_t* __restrict__ lastset, uint32_t* __restrict__ setmask) {
   pdl_wait();
   for (int b = blockIdx.x * blockDim.x + threadIdx.x; b < k.B; b += gridDim.x * blockDim.x) {
     int32_t* row = lastset + (size_t)b * n_ids;
     for (int t = 0; t < n_ids; t++) row[t] = -1;
+    uint32_t m = 0;
     for (int x = k.blk_first[b]; x <= k.blk_last[b]; x++) {
       const uint8_t s = setword[x];
       if (k.dialect == LEO_NVIDIA) {
         for (int id = 1; id <= 6; id++) if ((s >> id) & 1) row[id] = x;
+        m |= s & 0x7E;
       } else if (s != 0xFF) {
         row[s] = x;
+        m |= 1u << s;
       }
     }
+    setmask[b] = m;
   }
 }
 
@@ -485,6 +490,23 @@ struct DijHeap {
   }
 };
 
+// The wait's own block: 1 = setter found (emitted), 0 = none and no budget
+// left for other blocks, -1 = the block search is needed.
+LEO_DEV int setter_in_block(const KView& k, int wait, int id, const SyncArgs& sa) {
+  const int b0 = k.block_of[wait];
+  const int first0 = k.blk_first[b0];
+  const int lo = wait - min(wait - first0, kSyncBudget);
+  for (int x = wait - 1; x >= lo; x -= 8) {
+    uint8_t w[8];
+#pragma unroll
+    for (int t = 0; t < 8; t++) w[t] = (x - t >= lo) ? sa.setword[x - t] : 0;
+#pragma unroll
+    for (int t = 0; t < 8; t++)
+      if (x - t >= lo && set_hit(k.dialect, w[t], id)) { sync_emit(sa, x - t, wait); return 1; }
+  }
+  return wait - first0 >= kSyncBudget ? 0 : -1;
+}
+
 // Setter search for one (wait, id).  Returns -1 on overflow, else found (0/1).
 template <class Dij>
 LEO_DEV int setter_search(const KView& k, int wait, int id, const SyncArgs& sa, Dij& dj) {
@@ -682,11 +704,10 @@ __global__ void k_sync(KView k, SyncArgs a, char* scratch, int nworkers) {
         if (SLOW) {
           DijHeap dj{stamp, gdist, heap, t + 1, 0, 4 * k.B + 8};
           f = setter_search(k, i, id, a, dj);
-        } else if (a.dbg & LEO_DBG_SYNC_SLOW) {
-          f = -1;
         } else {
-          DijSmall dj{lnode, ldist, ldone, kDij, 0};
-          f = setter_search(k, i, id, a, dj);
+          // nearest setter inside the wait's own block; block searches are
+          // deferred to the warp / CTA tiers
+          f = (a.dbg & LEO_DBG_SYNC_SLOW) ? -1 : setter_in_block(k, i, id, a);
         }
         if (f < 0) {
           int s = atomicAdd(a.slow_count, 1);
@@ -970,6 +991,144 @@ __global__ void k_sync_setter_smem(KView k, SyncArgs a, int32_t* slow_out, int32
       }
     }
     __syncthreads();
+  }
+}
+
+// ---- setter searches: warp per item, CFG image in shared memory -------------
+// The block search of _trace_setter (depgraph.py:431-443) reduces to shortest
+// paths: setter block p yields its last setter s iff dist(p) + (last(p) - s +
+// 1) <= budget, dist over setter-free, b0-free predecessor paths weighted by
+// block length.  Any exact shortest-path method gives the same set, so a warp
+// relaxes a frontier in parallel (label-correcting Bellman-Ford) instead of
+// one thread running Dijkstra: each round every lane expands one frontier
+// block, and a block whose distance drops joins the next frontier once.
+// Distances live in a per-warp open-addressing table in shared memory; the
+// CFG image (block bounds, setter-id masks, predecessor CSR) is staged once
+// per CTA with TMA bulk copies.  A full table or frontier sends the item on
+// to the global-scratch Dijkstra tier.
+constexpr int kSWSlots = 1024, kSWFront = 512, kSWWarps = 4;
+
+__host__ __device__ inline size_t setter_cta_smem(int B) {
+  return 16 + carve_bytes(B, 4) * 3 + carve_bytes((size_t)B + 1, 4) + carve_bytes(2 * (size_t)B + 4, 4)
+         + (size_t)kSWWarps * (carve_bytes(kSWSlots, 4) * 3 + carve_bytes(2 * kSWFront, 4) + 16);
+}
+
+__global__ void __launch_bounds__(kSWWarps * 32) k_sync_setter_cta(KView k, SyncArgs a, const uint32_t* __restrict__ setmask_g,
+                                                                 int32_t* slow_out, int32_t* slow_out_count) {
+  pdl_wait();
+  extern __shared__ __align__(16) unsigned char sm_raw[];
+  const int B = k.B, lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  SmemCarve cv{sm_raw};
+  uint64_t* bar = cv.take<uint64_t>(2);
+  int32_t* bf = cv.take<int32_t>(B);
+  int32_t* bl = cv.take<int32_t>(B);
+  uint32_t* smask = cv.take<uint32_t>(B);
+  int32_t* pptr = cv.take<int32_t>(B + 1);
+  int32_t* pred = cv.take<int32_t>(2 * (size_t)B + 4);
+  unsigned char* wbase = cv.p;
+  cv.p = wbase + (size_t)wid * (carve_bytes(kSWSlots, 4) * 3 + carve_bytes(2 * kSWFront, 4) + 16);
+  int32_t* key = cv.take<int32_t>(kSWSlots);
+  int32_t* dist = cv.take<int32_t>(kSWSlots);
+  int32_t* fst = cv.take<int32_t>(kSWSlots);
+  int32_t* front = cv.take<int32_t>(2 * kSWFront);
+  int32_t* wctl = cv.take<int32_t>(4);        // [0] next frontier size, [1] overflow
+  const int n_items = (int)min((int64_t)*a.slow_count, a.slow_cap);
+  if ((int)blockIdx.x * kSWWarps >= n_items) return;
+  StageBar sb;
+  sb.init(bar);
+  sb.begin();
+  const int P = k.pred_ptr[B];
+  sb.copy(bf, k.blk_first, (size_t)B * 4);
+  sb.copy(bl, k.blk_last, (size_t)B * 4);
+  sb.copy(smask, setmask_g, (size_t)B * 4);
+  sb.copy(pptr, k.pred_ptr, (size_t)(B + 1) * 4);
+  sb.copy(pred, k.pred, (size_t)P * 4);
+  sb.commit_and_wait();
+
+  auto find = [&](int p) -> int {
+    uint32_t h = ((uint32_t)p * 2654435761u) >> 22;             // 10 bits
+    for (int t = 0; t < kSWSlots; t++) {
+      const int sl = (int)((h + t) & (kSWSlots - 1));
+      const int kk = key[sl];
+      if (kk == p) return sl;
+      if (kk == -1) return -1;
+    }
+    return -1;
+  };
+  for (int it = blockIdx.x * kSWWarps + wid; it < n_items; it += gridDim.x * kSWWarps) {
+    const int item = a.slow_list[it], i = item >> 6, id = item & 63;
+    const int b0 = k.block_of[i];
+    const int cost0 = i - bf[b0];
+    for (int x = lane; x < kSWSlots; x += 32) { key[x] = -1; dist[x] = 0x7FFFFFFF; fst[x] = 0; }
+    if (lane == 0) { wctl[0] = 0; wctl[1] = 0; }
+    __syncwarp();
+    int round = 1;
+    int32_t* cur = front;
+    int32_t* nxt = front + kSWFront;
+    // relax pp with distance d; a drop queues pp for round `round + 1`
+    auto relax = [&](int pp, int d) {
+      uint32_t h = ((uint32_t)pp * 2654435761u) >> 22;
+      int sl = -1;
+      for (int t = 0; t < kSWSlots; t++) {
+        const int c = (int)((h + t) & (kSWSlots - 1));
+        const int prev = atomicCAS(&key[c], -1, pp);
+        if (prev == -1 || prev == pp) { sl = c; break; }
+      }
+      if (sl < 0) { wctl[1] = 1; return; }
+      if (atomicMin(&dist[sl], d) > d && atomicExch(&fst[sl], round + 1) != round + 1) {
+        const int f = atomicAdd(&wctl[0], 1);
+        if (f < kSWFront) nxt[f] = pp; else wctl[1] = 1;
+      }
+    };
+    // round 0: the wait block's predecessors (b0 itself is never re-entered)
+    for (int q = pptr[b0] + lane; q < pptr[b0 + 1]; q += 32) {
+      const int pp = pred[q];
+      if (pp != b0) relax(pp, cost0);
+    }
+    __syncwarp();
+    int nf = min(wctl[0], kSWFront);
+    bool ovf = wctl[1] != 0;
+    __syncwarp();
+    while (nf > 0 && !ovf) {
+      { int32_t* t = cur; cur = nxt; nxt = t; }
+      round++;
+      if (lane == 0) wctl[0] = 0;
+      __syncwarp();
+      for (int x = lane; x < nf; x += 32) {
+        const int p = cur[x];
+        if ((smask[p] >> id) & 1) continue;                   // setter blocks end the path
+        const int sl = find(p);
+        const int nd = dist[sl] + (bl[p] - bf[p] + 1);
+        if (nd >= kSyncBudget) continue;
+        for (int q = pptr[p]; q < pptr[p + 1]; q++) {
+          const int pp = pred[q];
+          if (pp != b0) relax(pp, nd);
+        }
+      }
+      __syncwarp();
+      nf = min(wctl[0], kSWFront);
+      ovf = wctl[1] != 0;
+      __syncwarp();
+    }
+    if (ovf) {
+      if (lane == 0) {
+        const int s2 = atomicAdd(slow_out_count, 1);
+        if (s2 < a.slow_cap) slow_out[s2] = item;
+        else atomicOr(a.status, (uint32_t)LEO_ST_SCRATCH_OVERFLOW);
+      }
+      __syncwarp();
+      continue;
+    }
+    // settled: every reached setter block within the budget yields its last setter
+    bool found = false;
+    for (int x = lane; x < kSWSlots; x += 32) {
+      const int p = key[x];
+      if (p < 0 || !((smask[p] >> id) & 1)) continue;
+      const int s = a.lastset[(size_t)p * a.n_ids + id];
+      if (dist[x] + (bl[p] - s + 1) <= kSyncBudget) { sync_emit(a, s, i); found = true; }
+    }
+    if (!__any_sync(0xffffffffu, found) && lane == 0) diag_push(a.diags, a.status, LEO_DIAG_NO_SETTER, i, id, 0, 0, id);
+    __syncwarp();
   }
 }
 
