@@ -102,7 +102,8 @@ struct PySum {
 
 // ---- profiling aid: per-CTA phase marks (LEO_DBG_PHASES) ----------------------
 __device__ long long g_phase_ts[4][1024][8];
-__device__ long long g_item_cycles[8192];      // per-item cycles of the waitcnt tier
+__device__ long long g_item_cycles[16384];     // per-item cycles: waitcnt tier [0, 8192), reach tier 0 [8192, 16384)
+__device__ int g_reach_item_ctr;
 __device__ int g_tier_counts[16];              // build_graph counters (LEO_DBG_PHASES)
 __global__ void k_copy_counts(const int32_t* ctr, int n) {
   for (int i = threadIdx.x; i < n && i < 16; i += blockDim.x) g_tier_counts[i] = ctr[i];

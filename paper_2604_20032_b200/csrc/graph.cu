@@ -480,7 +480,8 @@ __global__ void k_reach_unit(KView k, ReachArgs a, const int32_t* __restrict__ q
         const int b = ql[t];
         e = qs[b];
         ovf = (a.dbg & (LEO_DBG_REACH_T2 | LEO_DBG_REACH_T3)) != 0;
-        int sp = 0;
+        int sp = 0, nvis = 0;
+        const long long qc0 = clock64();
         if (!ovf) {
           for (int w = 0; w < W; w++) vis[w * T + tid] = 0u;
           // Entering block p backward either ends at its nearest def (a result)
@@ -494,6 +495,7 @@ __global__ void k_reach_unit(KView k, ReachArgs a, const int32_t* __restrict__ q
             const uint32_t m = 1u << (key & 31);
             if (*word & m) return;
             *word |= m;
+            nvis++;
             if (c >= 0) {
               if (nres == kRURes) ovf = true;
               else res[(nres++) * T + tid] = c;
@@ -508,6 +510,10 @@ __global__ void k_reach_unit(KView k, ReachArgs a, const int32_t* __restrict__ q
             const int h = stk[(--sp) * T + tid];
             for (int q = pptr[h]; q < pptr[h + 1]; q++) visit(pred[q]);
           }
+        }
+        if ((a.dbg & LEO_DBG_PHASES) && clock64() - qc0 > 14000) {   // per-query tail record (profiling)
+          const int slot = atomicAdd(&g_reach_item_ctr, 1);
+          if (slot < 8192) g_item_cycles[8192 + slot] = ((clock64() - qc0) << 24) | min(nvis, 0xFFFFFF);
         }
         if (ovf) {                                 // tier 2 re-runs the query
           const int s2 = atomicAdd(a.slow_count, 1);

@@ -45,9 +45,17 @@ struct TraceScope {
     if (x >= t->capacity) return;
     slot = x;
     t->kernel_id[x] = id;
-    cudaEventRecord((cudaEvent_t)t->ev_begin[x], st);
+    record((cudaEvent_t)t->ev_begin[x]);
   }
-  ~TraceScope() { if (slot >= 0) cudaEventRecord((cudaEvent_t)t->ev_end[slot], st); }
+  // inside a stream capture the record becomes an event-record node (a
+  // timeline of graph replays)
+  void record(cudaEvent_t ev) {
+    cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
+    cudaStreamIsCapturing(st, &cs);
+    if (cs == cudaStreamCaptureStatusActive) cudaEventRecordWithFlags(ev, st, cudaEventRecordExternal);
+    else cudaEventRecord(ev, st);
+  }
+  ~TraceScope() { if (slot >= 0) record((cudaEvent_t)t->ev_end[slot]); }
 };
 // LEO_DEBUG_SYNC=1: synchronise after every kernel and report the first
 // failing (or hanging: last printed) kernel on stderr (debugging aid)
@@ -269,7 +277,11 @@ int build_graph_impl(const LeoKernel* kk, const LeoCaps* caps, LeoEdges* out, Le
       TRACED(KID_SYNC_PACK, leo_launch(k_block_setters, grid_for(B, T), T, 0, st, k, setword, n_ids, lastset, bev));
     TRACED(KID_SYNC_PACK, leo_launch(k_wait_list, grid_for(N, T), T, 0, st, k, own, wlist, &ctr[8]));
     SyncArgs sa{caps ? caps->debug_flags : 0, skeys, cap_sync, &ctr[3], slow2, &ctr[4], cap_slow, *diags, status,
-                wcword, setword, lastset, n_ids, wlist, &ctr[8], wclist, &ctr[10]};
+                wcword, setword, lastset, n_ids, wlist, &ctr[8], wclist, &ctr[10], 0};
+    const int sdbg = caps ? caps->debug_flags : 0;
+    const bool setter_cta = k.dialect != LEO_AMD && B > 0 && setter_cta_smem(B) <= (size_t)kSmemResidentMax &&
+                            !(sdbg & (LEO_DBG_NO_SMEM | LEO_DBG_SYNC_SLOW));
+    sa.defer_search = setter_cta ? 1 : 0;
     // as many threads per CTA as the image allows: more warps hide the
     // shared-memory latency of the event-list build and spread the items
     int wc_threads = 512;
@@ -277,7 +289,11 @@ int build_graph_impl(const LeoKernel* kk, const LeoCaps* caps, LeoEdges* out, Le
     const size_t wc_smem = sync_smem_bytes(N, B, wc_threads);
     const int dbg_flags = caps ? caps->debug_flags : 0;
     if (k.dialect == LEO_AMD && B > 0 && wc_smem <= (size_t)kSmemResidentMax && !(dbg_flags & LEO_DBG_NO_SMEM))
-      TRACED(KID_SYNC, leo_launch(k_sync_wc_smem, SM, wc_threads, wc_smem, st, k, sa, bev));
+      {
+      const char* ws = getenv("LEO_WC_STEPS");
+      const int wc_steps = ws ? atoi(ws) : kWcSmemSteps;
+      TRACED(KID_SYNC, leo_launch(k_sync_wc_smem, SM, wc_threads, wc_smem, st, k, sa, bev, wc_steps));
+    }
     else
       TRACED(KID_SYNC, leo_launch(k_sync<false>, grid_for(N, 64), 64, 0, st, k, sa, nullptr, 0));
     if (k.dialect == LEO_AMD)
@@ -286,9 +302,9 @@ int build_graph_impl(const LeoKernel* kk, const LeoCaps* caps, LeoEdges* out, Le
     if (k.dialect != LEO_AMD) {
       // setter searches: CTA per item in shared memory first; the rest (and
       // forced-slow items) on the global-scratch workers
-      const size_t cta_smem = setter_cta_smem(B);
-      if (B > 0 && cta_smem <= (size_t)kSmemResidentMax && !(dbg_flags & (LEO_DBG_NO_SMEM | LEO_DBG_SYNC_SLOW)))
-        TRACED(KID_SYNC_SLOW, leo_launch(k_sync_setter_cta, SM, kSWWarps * 32, cta_smem, st, k, sa, bev, slow3s, &ctr[11]));
+      if (setter_cta)
+        TRACED(KID_SYNC_SLOW, leo_launch(k_sync_setter_cta, SM, kSWWarps * 32, setter_cta_smem(B), st, k, sa, bev, slow3s,
+                                         &ctr[11]));
       else
         TRACED(KID_SYNC_SLOW, leo_launch(k_sync_setter_smem, SM, 32, kDHBytes, st, k, sa, slow3s, &ctr[11]));
       SyncArgs sb = sa;
@@ -317,6 +333,10 @@ int build_graph_impl(const LeoKernel* kk, const LeoCaps* caps, LeoEdges* out, Le
   ReachArgs ra{caps ? caps->debug_flags : 0, ldtab, brec, U, Bp, q_block, q_unit, q_off, q_len, qres, cap_qres, &ctr[1],
                slow_list, &ctr[2], NU + 1024, status};
   const int dbg = caps ? caps->debug_flags : 0;
+  if (dbg & LEO_DBG_PHASES) {
+    static const int zero = 0;
+    cudaMemcpyToSymbolAsync(g_reach_item_ctr, &zero, sizeof(int), 0, cudaMemcpyHostToDevice, st);
+  }
   // segments: members of a concatenated batch are staged one at a time
   const int n_seg = (kk->n_segments > 1 && kk->seg_block) ? kk->n_segments : 1;
   const int bcap = n_seg > 1 ? kk->max_seg_blocks : B;
@@ -612,7 +632,7 @@ int leo_debug_tiers(int32_t* out) {
 }
 
 int leo_debug_items(int64_t* out, int32_t n) {
-  if (n < 0 || n > 8192) return -1;
+  if (n < 0 || n > 16384) return -1;
   LEO_CUDA_CHECK(cudaMemcpyFromSymbol(out, g_item_cycles, (size_t)n * sizeof(long long)));
   return 0;
 }

@@ -48,6 +48,7 @@ struct SyncArgs {
   const int32_t* wait_count;
   int32_t* wc_list;          // waitcnt items for the warp tier
   int32_t* wc_count;
+  int32_t defer_search;      // nvidia/intel: block searches all go to k_sync_setter_cta
 };
 
 __global__ void k_sync_pack(KView k, uint32_t* __restrict__ wcword, uint8_t* __restrict__ setword,
@@ -704,10 +705,15 @@ __global__ void k_sync(KView k, SyncArgs a, char* scratch, int nworkers) {
         if (SLOW) {
           DijHeap dj{stamp, gdist, heap, t + 1, 0, 4 * k.B + 8};
           f = setter_search(k, i, id, a, dj);
+        } else if (a.dbg & LEO_DBG_SYNC_SLOW) {
+          f = -1;
+        } else if (a.defer_search) {
+          // nearest setter inside the wait's own block; block searches go to
+          // the warp-per-item tier (CFG image in shared memory)
+          f = setter_in_block(k, i, id, a);
         } else {
-          // nearest setter inside the wait's own block; block searches are
-          // deferred to the warp / CTA tiers
-          f = (a.dbg & LEO_DBG_SYNC_SLOW) ? -1 : setter_in_block(k, i, id, a);
+          DijSmall dj{lnode, ldist, ldone, kDij, 0};
+          f = setter_search(k, i, id, a, dj);
         }
         if (f < 0) {
           int s = atomicAdd(a.slow_count, 1);
@@ -837,7 +843,7 @@ __host__ __device__ inline size_t sync_smem_bytes(int N, int B, int threads) {
          + carve_bytes((size_t)((B + 31) >> 5) * threads, 4);
 }
 
-__global__ void k_sync_wc_smem(KView k, SyncArgs a, const uint32_t* __restrict__ bev_g) {
+__global__ void k_sync_wc_smem(KView k, SyncArgs a, const uint32_t* __restrict__ bev_g, int max_steps) {
   pdl_wait();
   extern __shared__ __align__(16) unsigned char sm_raw[];
   const int N = k.N, B = k.B;
@@ -937,7 +943,7 @@ __global__ void k_sync_wc_smem(KView k, SyncArgs a, const uint32_t* __restrict__
       const long long c0 = clock64();
       const bool ok = !(a.dbg & LEO_DBG_SYNC_SLOW) && lv < kWcNone &&
                       trace_waitcnt_bits(ks, bev, pbits + threadIdx.x, T, i, counter, (int)lv, as, fr, kFrames,
-                                         best_m, kWcSmemSteps, kbuf, &kcnt, kWcCtaKeys, ev);
+                                         best_m, max_steps, kbuf, &kcnt, kWcCtaKeys, ev);
       if ((a.dbg & LEO_DBG_PHASES) && t < 4096) g_item_cycles[t * 2 + counter] = clock64() - c0;
       if (!ok) {
         const bool to_warp = lv < kWcNone && !(a.dbg & LEO_DBG_SYNC_SLOW);

@@ -22,6 +22,7 @@ ap.add_argument("--warmup", type=int, default=1)
 ap.add_argument("--scale", type=float, default=1.0)
 ap.add_argument("--flags", type=int, default=0)
 ap.add_argument("--timeline", action="store_true")
+ap.add_argument("--graph-timeline", action="store_true")
 ap.add_argument("--phases", action="store_true")
 ap.add_argument("--debug-guard", action="store_true")
 args = ap.parse_args()
@@ -66,6 +67,24 @@ if args.timeline:
     for name, t0, t1 in sorted(tl, key=lambda x: x[1]):
         print(f"  {t0 * 1e3:8.1f} {t1 * 1e3:8.1f} {1e3 * (t1 - t0):7.1f}  {name}")
 
+if args.graph_timeline:
+    # the same, inside a CUDA graph replay (event-record nodes around kernels)
+    tr = device.Tracer(capacity=4096, timeline=True)
+    an.set_tracer(tr)
+    an.capture(dp, cfg, ds, trace_in_graph=True)
+    for _ in range(3):
+        flush.zero_()
+        torch.cuda.synchronize()
+        torch.cuda._sleep(20_000_000)
+        an.replay()
+        torch.cuda.synchronize()
+    tl = tr.timeline()
+    an.set_tracer(None)
+    end = max(t1 for _, _, t1 in tl)
+    print(f"graph timeline: {end * 1e3:.1f} us")
+    for name, t0, t1 in sorted(tl, key=lambda x: x[1]):
+        print(f"  {t0 * 1e3:8.1f} {t1 * 1e3:8.1f} {1e3 * (t1 - t0):7.1f}  {name}")
+
 if args.phases:
     # per-CTA clock64 phase marks of the shared-memory tiers (LEO_DBG_PHASES)
     import numpy as np
@@ -90,13 +109,26 @@ if args.phases:
         print(f"{nm}: {len(rows)} CTAs, cumulative clock64 at phase ends (median / max):")
         for i, p in enumerate(ph):
             print(f"   {p:10s} {int(np.median(rows[:, i])):9d} {int(rows[:, i].max()):9d}")
-    it = np.zeros(8192, dtype=np.int64)
+    it2 = np.zeros(16384, dtype=np.int64)
     lib().leo_debug_items.argtypes = [C.c_void_p, C.c_int32]
-    lib().leo_debug_items(it.ctypes.data_as(C.c_void_p), 8192)
+    lib().leo_debug_items(it2.ctypes.data_as(C.c_void_p), 16384)
+    it = it2[:8192]
+    rq = it2[8192:]
+    rq = rq[rq > 0]
+    if len(rq):
+        cyc, nv = rq >> 24, rq & 0xFFFFFF
+        o = np.argsort(-cyc)
+        print(f"reach tier-0 queries: {len(rq)} (first 8192); cycles p50 {int(np.median(cyc))} p99 "
+              f"{int(np.percentile(cyc, 99))} max {int(cyc.max())}; visits p50 {int(np.median(nv))} "
+              f"p99 {int(np.percentile(nv, 99))} max {int(nv.max())}")
+        print("  slowest (cycles, visits):", [(int(cyc[x]), int(nv[x])) for x in o[:12]])
+        print("  cycles per visit (queries > 20 visits): p50",
+              int(np.median(cyc[nv > 20] / nv[nv > 20])) if (nv > 20).any() else 0)
     wl_list = None
     order = np.argsort(-it)[:12]
     print("slowest waitcnt items (t*2+counter, cycles):", [(int(x), int(it[x])) for x in order])
-    print("item cycles: sum", int(it.sum()), "count>0", int((it > 0).sum()), "p50", int(np.median(it[it > 0])))
+    if (it > 0).any():
+        print("item cycles: sum", int(it.sum()), "count>0", int((it > 0).sum()), "p50", int(np.median(it[it > 0])))
 
 if args.debug_guard:
     import numpy as np
