@@ -8,11 +8,15 @@ import fails loudly (build it with `python -m paper_2604_20032_b200.build` or
 from __future__ import annotations
 
 import ctypes as C
+import os
 from pathlib import Path
 
 from . import abi
 
 LIB_PATH = Path(__file__).resolve().parent / "libleo_b200.so"
+# A/B timing of library variants (profiling only): LEO_LIB_VARIANT=<path>
+if os.environ.get("LEO_LIB_VARIANT"):
+    LIB_PATH = Path(os.environ["LEO_LIB_VARIANT"]).resolve()
 ABI_VERSION = 1
 
 _lib = None

@@ -463,6 +463,50 @@ LEO_DEV int dominant_self(const PView& p, int j) {     // _dominant_class :379-3
 
 constexpr int kSeenCap = 24;
 
+// issue_count with its loads issued together (no dependent branch on exec_cnt)
+LEO_DEV double issue_count_ld(const PView& p, int i) {
+  const int64_t ec = p.exec_cnt[i];
+  const uint8_t sm = p.sampled[i];
+  const int32_t tt = p.total[i], lt = p.lat[i];
+  if (ec >= 0) return (double)ec;
+  if (sm) return (double)(tt >= 0 ? tt : lt);
+  return 1.0;
+}
+
+// The per-edge operands of one stalled instruction, loaded kBU edges at a
+// time (independent loads), consumed in edge order so every floating-point
+// sum keeps the reference's order.
+constexpr int kBU = 4;
+struct EdgeBatch {
+  int e[kBU], pr[kBU], cls[kBU];
+  double d[kBU], ef[kBU], ic[kBU];
+  LEO_DEV void load(const BlameArgs& a, int j, int r0, int nr, int s0, int deg, int x0, bool with_cls) {
+#pragma unroll
+    for (int u = 0; u < kBU; u++) {
+      const int x = x0 + u;
+      e[u] = x < deg ? (x < nr ? r0 + x : (int)a.inc.sidx[s0 + (x - nr)]) : -1;
+    }
+#pragma unroll
+    for (int u = 0; u < kBU; u++) {
+      pr[u] = 0; d[u] = 1.0; cls[u] = 0;
+      if (e[u] >= 0) {
+        pr[u] = a.pprod[e[u]];
+        d[u] = a.pdist[e[u]];
+        if (with_cls) cls[u] = kMatchClass[(a.pmeta[e[u]] >> 30) & 3];
+      }
+    }
+#pragma unroll
+    for (int u = 0; u < kBU; u++) {
+      ef[u] = 1.0; ic[u] = 0.0;
+      if (e[u] >= 0) {
+        ef[u] = a.p.eff[pr[u]];
+        ic[u] = issue_count_ld(a.p, pr[u]);
+        if (with_cls) cls[u] = a.p.cls_cnt[(size_t)j * 8 + cls[u]];
+      }
+    }
+  }
+};
+
 // pass 0: decide self vs edges, entry count, cached sums; pass 1: write entries
 template <int PASS>
 __global__ void k_blame(KView k, BlameArgs a) {
@@ -472,97 +516,95 @@ __global__ void k_blame(KView k, BlameArgs a) {
     const double s_j = (double)((int64_t)lat * a.p.period);
     if (PASS == 0) { a.ecount[j] = 0; a.self_sub[j] = -1; }
     if (s_j == 0 || !a.own.has(j)) continue;
-    const int deg = a.inc.deg(j);
-    if (PASS == 0) {
-      bool self = deg == 0;
-      double total = 0.0, n_sum = 0.0;
-      if (!self) {
-        double d_min = 0, e_min = 0;
-        PySum ns;
-        for (int x = 0; x < deg; x++) {
-          int e = a.inc.edge(j, x);
-          int pr = a.pprod[e];
-          double d = a.pdist[e], ef = a.p.eff[pr];
-          if (x == 0 || d < d_min) d_min = d;
-          if (x == 0 || ef < e_min) e_min = ef;
-          ns.add(issue_count(a.p, pr));
+    const int r0 = a.inc.rbeg[j], nr = a.inc.rend[j] - r0, s0 = a.inc.soff[j];
+    const int deg = nr + (a.inc.soff[j + 1] - s0);
+    if (PASS == 1 && a.self_sub[j] >= 0) {
+      const int o = a.eoff[j];
+      if (o + 1 > a.out.capacity) { atomicOr(a.status, (uint32_t)LEO_ST_BLAME_OVERFLOW); continue; }
+      a.out.stalled[o] = j;
+      a.out.edge[o] = -1;
+      a.out.sub[o] = (uint8_t)a.self_sub[j];
+      a.out.blame[o] = s_j;
+      for (int c = 0; c < 4; c++) a.out.factors[(size_t)o * 4 + c] = 0.0;
+      continue;
+    }
+    bool self = deg == 0;
+    double total = 0.0, n_sum = 0.0, d_min = 0, e_min = 0;
+    if (!self) {
+      PySum ns;
+      for (int x0 = 0; x0 < deg; x0 += kBU) {
+        EdgeBatch eb;
+        eb.load(a, j, r0, nr, s0, deg, x0, false);
+#pragma unroll
+        for (int u = 0; u < kBU; u++) {
+          if (eb.e[u] < 0) continue;
+          if (x0 + u == 0 || eb.d[u] < d_min) d_min = eb.d[u];
+          if (x0 + u == 0 || eb.ef[u] < e_min) e_min = eb.ef[u];
+          if (PASS == 0) ns.add(eb.ic[u]);
         }
-        n_sum = ns.value();
-        if (n_sum == 0) self = true;
-        else {
-          PySum ts;
-          for (int x = 0; x < deg; x++) {
-            int e = a.inc.edge(j, x);
-            int pr = a.pprod[e];
-            double f0 = __ddiv_rn(d_min, a.pdist[e]);
-            double f1 = __ddiv_rn(e_min, a.p.eff[pr]);
-            double f2 = __ddiv_rn(issue_count(a.p, pr), n_sum);
-            double f3 = __ddiv_rn((double)a.p.cls_cnt[(size_t)j * 8 + kMatchClass[(a.pmeta[e] >> 30) & 3]], (double)lat);
-            ts.add(__dmul_rn(__dmul_rn(__dmul_rn(f0, f1), f2), f3));
+      }
+      if (PASS == 0) n_sum = ns.value();
+      else { total = a.jtotal[j]; n_sum = a.jnsum[j]; }
+      if (PASS == 0 && n_sum == 0) self = true;
+      else {
+        const int o = PASS == 1 ? a.eoff[j] : 0;
+        if (PASS == 1 && o + a.ecount[j] > a.out.capacity) { atomicOr(a.status, (uint32_t)LEO_ST_BLAME_OVERFLOW); continue; }
+        PySum ts;
+        for (int x0 = 0; x0 < deg; x0 += kBU) {
+          EdgeBatch eb;
+          eb.load(a, j, r0, nr, s0, deg, x0, true);
+#pragma unroll
+          for (int u = 0; u < kBU; u++) {
+            if (eb.e[u] < 0) continue;
+            const double f0 = __ddiv_rn(d_min, eb.d[u]);
+            const double f1 = __ddiv_rn(e_min, eb.ef[u]);
+            const double f2 = __ddiv_rn(eb.ic[u], n_sum);
+            const double f3 = __ddiv_rn((double)eb.cls[u], (double)lat);
+            const double prod = __dmul_rn(__dmul_rn(__dmul_rn(f0, f1), f2), f3);
+            if (PASS == 0) {
+              ts.add(prod);
+            } else {
+              const int x = o + x0 + u;
+              a.out.stalled[x] = j;
+              a.out.edge[x] = eb.e[u];
+              a.out.sub[x] = 255;
+              a.out.blame[x] = __ddiv_rn(__dmul_rn(s_j, prod), total);
+              double* f = a.out.factors + (size_t)x * 4;
+              f[0] = f0; f[1] = f1; f[2] = f2; f[3] = f3;
+            }
           }
+        }
+        if (PASS == 0) {
           total = ts.value();
           if (total == 0.0) self = true;
         }
       }
-      if (self) {
-        int sub = dominant_self(a.p, j);
-        if (sub == LEO_SB_MEMORY_LATENCY && (kMemoryClasses & BIT(k.opclass[j])) && a.mp_ok) {
-          if (a.mp_ok[j]) sub = LEO_SB_INDIRECT_ADDRESSING;
-        } else if (sub == LEO_SB_MEMORY_LATENCY && (kMemoryClasses & BIT(k.opclass[j]))) {
-          // _address_traces_to_load: small searches inline (<= kSeenCap nodes),
-          // larger ones in k_selfblame_warp (warp per candidate)
-          int32_t seen[kSeenCap];
-          const int r = (a.dbg & LEO_DBG_SELF_SLOW) ? -1
-                        : traces_to_load(k, a.brbeg, a.brend, a.bprod, a.bmeta, j, seen, kSeenCap, nullptr, 0);
-          if (r < 0) {
-            int s = atomicAdd(a.slow_count, 1);
-            if (s < a.slow_cap) a.slow_list[s] = j;
-            else atomicOr(a.status, (uint32_t)LEO_ST_SCRATCH_OVERFLOW);
-          } else if (r) {
-            sub = LEO_SB_INDIRECT_ADDRESSING;
-          }
+    }
+    if (PASS == 1) continue;
+    if (self) {
+      int sub = dominant_self(a.p, j);
+      if (sub == LEO_SB_MEMORY_LATENCY && (kMemoryClasses & BIT(k.opclass[j])) && a.mp_ok) {
+        if (a.mp_ok[j]) sub = LEO_SB_INDIRECT_ADDRESSING;
+      } else if (sub == LEO_SB_MEMORY_LATENCY && (kMemoryClasses & BIT(k.opclass[j]))) {
+        // _address_traces_to_load: small searches inline (<= kSeenCap nodes),
+        // larger ones in k_selfblame_warp (warp per candidate)
+        int32_t seen[kSeenCap];
+        const int r = (a.dbg & LEO_DBG_SELF_SLOW) ? -1
+                      : traces_to_load(k, a.brbeg, a.brend, a.bprod, a.bmeta, j, seen, kSeenCap, nullptr, 0);
+        if (r < 0) {
+          int s2 = atomicAdd(a.slow_count, 1);
+          if (s2 < a.slow_cap) a.slow_list[s2] = j;
+          else atomicOr(a.status, (uint32_t)LEO_ST_SCRATCH_OVERFLOW);
+        } else if (r) {
+          sub = LEO_SB_INDIRECT_ADDRESSING;
         }
-        a.self_sub[j] = sub;
-        a.ecount[j] = 1;
-      } else {
-        a.ecount[j] = deg;
-        a.jtotal[j] = total;
-        a.jnsum[j] = n_sum;
       }
+      a.self_sub[j] = sub;
+      a.ecount[j] = 1;
     } else {
-      const int o = a.eoff[j];
-      if (o + a.ecount[j] > a.out.capacity) { atomicOr(a.status, (uint32_t)LEO_ST_BLAME_OVERFLOW); continue; }
-      if (a.self_sub[j] >= 0) {
-        a.out.stalled[o] = j;
-        a.out.edge[o] = -1;
-        a.out.sub[o] = (uint8_t)a.self_sub[j];
-        a.out.blame[o] = s_j;
-        for (int c = 0; c < 4; c++) a.out.factors[(size_t)o * 4 + c] = 0.0;
-        continue;
-      }
-      double d_min = 0, e_min = 0;
-      for (int x = 0; x < deg; x++) {
-        int e = a.inc.edge(j, x);
-        double d = a.pdist[e], ef = a.p.eff[a.pprod[e]];
-        if (x == 0 || d < d_min) d_min = d;
-        if (x == 0 || ef < e_min) e_min = ef;
-      }
-      const double total = a.jtotal[j], n_sum = a.jnsum[j];
-      for (int x = 0; x < deg; x++) {
-        int e = a.inc.edge(j, x);
-        int pr = a.pprod[e];
-        double f0 = __ddiv_rn(d_min, a.pdist[e]);
-        double f1 = __ddiv_rn(e_min, a.p.eff[pr]);
-        double f2 = __ddiv_rn(issue_count(a.p, pr), n_sum);
-        double f3 = __ddiv_rn((double)a.p.cls_cnt[(size_t)j * 8 + kMatchClass[(a.pmeta[e] >> 30) & 3]], (double)lat);
-        double prod = __dmul_rn(__dmul_rn(__dmul_rn(f0, f1), f2), f3);
-        a.out.stalled[o + x] = j;
-        a.out.edge[o + x] = e;
-        a.out.sub[o + x] = 255;
-        a.out.blame[o + x] = __ddiv_rn(__dmul_rn(s_j, prod), total);
-        double* f = a.out.factors + (size_t)(o + x) * 4;
-        f[0] = f0; f[1] = f1; f[2] = f2; f[3] = f3;
-      }
+      a.ecount[j] = deg;
+      a.jtotal[j] = total;
+      a.jnsum[j] = n_sum;
     }
   }
 }

@@ -185,17 +185,35 @@ LEO_DEV void shell_sort_u64(uint64_t* a, int n) {
 // Sort keys[begin[s] .. begin[s]+len[s]) ascending, drop duplicates in place,
 // write the unique count to uniq[s].  Segments reaching past `cap` (the
 // producer overflowed its buffer and flagged it) are left empty.
-__global__ void segsort_unique_u64(uint64_t* __restrict__ keys, const int32_t* __restrict__ begin,
-                                   const int32_t* __restrict__ len, const int32_t* nseg_dev, int nseg_cap,
-                                   int32_t* __restrict__ uniq, int64_t cap) {
+// Lane per segment for short segments (register network / insertion sort);
+// segments of 25..kSegWarpMax keys are sorted by the whole warp (bitonic sort
+// in shared memory, ballot compaction), longer ones fall back to a shell sort.
+constexpr int kSegWarpMax = 256, kSegThreads = 128;
+
+__global__ void __launch_bounds__(kSegThreads) segsort_unique_u64(uint64_t* __restrict__ keys,
+                                                                  const int32_t* __restrict__ begin,
+                                                                  const int32_t* __restrict__ len,
+                                                                  const int32_t* nseg_dev, int nseg_cap,
+                                                                  int32_t* __restrict__ uniq, int64_t cap) {
   pdl_wait();
-  int nseg = nseg_dev ? *nseg_dev : nseg_cap;
-  for (int s = blockIdx.x * blockDim.x + threadIdx.x; s < nseg; s += gridDim.x * blockDim.x) {
-    int n = len[s];
-    if ((int64_t)begin[s] + n > cap) { uniq[s] = 0; continue; }
-    uint64_t* a = keys + begin[s];
-    if (n <= 1) { uniq[s] = n; continue; }
-    if (n <= 4) {
+  __shared__ uint64_t wbuf[kSegThreads / 32][kSegWarpMax];
+  uint64_t* buf = wbuf[threadIdx.x >> 5];
+  const int lane = threadIdx.x & 31;
+  const int nseg = nseg_dev ? *nseg_dev : nseg_cap;
+  // whole warps iterate together (the cooperative path needs every lane)
+  for (int s0 = blockIdx.x * blockDim.x + (threadIdx.x & ~31); s0 < nseg; s0 += gridDim.x * blockDim.x) {
+    const int s = s0 + lane;
+    int n = 0, b = 0;
+    bool mine = false;
+    if (s < nseg) {
+      n = len[s];
+      b = begin[s];
+      if ((int64_t)b + n > cap) { uniq[s] = 0; n = 0; }
+      else mine = true;
+    }
+    uint64_t* a = keys + b;
+    if (mine && n <= 1) { uniq[s] = n; mine = false; }
+    if (mine && n <= 4) {
       // register sorting network (no local-memory array): the common case
       uint64_t r0 = a[0], r1 = a[1], r2 = n > 2 ? a[2] : ~0ull, r3 = n > 3 ? a[3] : ~0ull;
       auto cs = [](uint64_t& x, uint64_t& y) { const uint64_t lo = x < y ? x : y; y = x < y ? y : x; x = lo; };
@@ -206,9 +224,8 @@ __global__ void segsort_unique_u64(uint64_t* __restrict__ keys, const int32_t* _
       if (n > 2 && r2 != r1) a[u++] = r2;
       if (n > 3 && r3 != r2) a[u++] = r3;
       uniq[s] = u;
-      continue;
-    }
-    if (n <= 24) {
+      mine = false;
+    } else if (mine && n <= 24) {
       uint64_t r[24];
       for (int i = 0; i < n; i++) r[i] = a[i];
       sort_small_u64(r, n);
@@ -216,14 +233,50 @@ __global__ void segsort_unique_u64(uint64_t* __restrict__ keys, const int32_t* _
       for (int i = 0; i < n; i++)
         if (i == 0 || r[i] != r[i - 1]) a[u++] = r[i];
       uniq[s] = u;
-    } else {
+      mine = false;
+    } else if (mine && n > kSegWarpMax) {
       shell_sort_u64(a, n);
       int u = 0;
       for (int i = 0; i < n; i++) {
-        uint64_t x = a[i];
+        const uint64_t x = a[i];
         if (i == 0 || x != a[u - 1]) a[u++] = x;
       }
       uniq[s] = u;
+      mine = false;
+    }
+    unsigned big = __ballot_sync(0xffffffffu, mine);
+    while (big) {
+      const int src = __ffs(big) - 1;
+      big &= big - 1;
+      const int sn = __shfl_sync(0xffffffffu, n, src), sb = __shfl_sync(0xffffffffu, b, src);
+      uint64_t* sa = keys + sb;
+      int P = 32;
+      while (P < sn) P <<= 1;
+      for (int i = lane; i < P; i += 32) buf[i] = i < sn ? sa[i] : ~0ull;
+      __syncwarp();
+      for (int k2 = 2; k2 <= P; k2 <<= 1)
+        for (int jj = k2 >> 1; jj > 0; jj >>= 1) {
+          for (int i = lane; i < P; i += 32) {
+            const int ixj = i ^ jj;
+            if (ixj > i) {
+              const uint64_t x = buf[i], y = buf[ixj];
+              if ((x > y) == ((i & k2) == 0)) { buf[i] = y; buf[ixj] = x; }
+            }
+          }
+          __syncwarp();
+        }
+      int base = 0;
+      for (int i0 = 0; i0 < sn; i0 += 32) {
+        const int i = i0 + lane;
+        const bool keep = i < sn && (i == 0 || buf[i] != buf[i - 1]);
+        const unsigned m = __ballot_sync(0xffffffffu, keep);
+        const uint64_t v = i < sn ? buf[i] : 0;
+        __syncwarp();
+        if (keep) sa[base + __popc(m & ((1u << lane) - 1))] = v;
+        base += __popc(m);
+      }
+      if (lane == src) uniq[s] = base;
+      __syncwarp();
     }
   }
 }
