@@ -507,26 +507,56 @@ struct EdgeBatch {
   }
 };
 
-// pass 0: decide self vs edges, entry count, cached sums; pass 1: write entries
+// self verdict of stalled instruction j (dominant class, indirect addressing)
+LEO_DEV void blame_self(const KView& k, const BlameArgs& a, int j) {
+  int sub = dominant_self(a.p, j);
+  if (sub == LEO_SB_MEMORY_LATENCY && (kMemoryClasses & BIT(k.opclass[j])) && a.mp_ok) {
+    if (a.mp_ok[j]) sub = LEO_SB_INDIRECT_ADDRESSING;
+  } else if (sub == LEO_SB_MEMORY_LATENCY && (kMemoryClasses & BIT(k.opclass[j]))) {
+    // _address_traces_to_load: small searches inline (<= kSeenCap nodes),
+    // larger ones in k_selfblame_warp (warp per candidate)
+    int32_t seen[kSeenCap];
+    const int r = (a.dbg & LEO_DBG_SELF_SLOW) ? -1
+                  : traces_to_load(k, a.brbeg, a.brend, a.bprod, a.bmeta, j, seen, kSeenCap, nullptr, 0);
+    if (r < 0) {
+      int s2 = atomicAdd(a.slow_count, 1);
+      if (s2 < a.slow_cap) a.slow_list[s2] = j;
+      else atomicOr(a.status, (uint32_t)LEO_ST_SCRATCH_OVERFLOW);
+    } else if (r) {
+      sub = LEO_SB_INDIRECT_ADDRESSING;
+    }
+  }
+  a.self_sub[j] = sub;
+  a.ecount[j] = 1;
+}
+
+// Stalled instructions with more than kBlameWarpDeg incoming edges (a
+// waitcnt consumer can have hundreds of sync producers) are done by the whole
+// warp: lanes load and evaluate edges in parallel, and every lane replays the
+// ordered sums / first-minimum scans through shuffles, so the floating-point
+// order is the reference's.
+constexpr int kBlameWarpDeg = 12;
+
+// one instruction, thread path; returns true when the warp path must take it
 template <int PASS>
-__global__ void k_blame(KView k, BlameArgs a) {
-  pdl_wait();
-  for (int j = blockIdx.x * blockDim.x + threadIdx.x; j < k.N; j += gridDim.x * blockDim.x) {
+LEO_DEV bool blame_one(const KView& k, const BlameArgs& a, int j) {
+  {
     const int lat = a.p.lat[j];
     const double s_j = (double)((int64_t)lat * a.p.period);
     if (PASS == 0) { a.ecount[j] = 0; a.self_sub[j] = -1; }
-    if (s_j == 0 || !a.own.has(j)) continue;
+    if (s_j == 0 || !a.own.has(j)) return false;
     const int r0 = a.inc.rbeg[j], nr = a.inc.rend[j] - r0, s0 = a.inc.soff[j];
     const int deg = nr + (a.inc.soff[j + 1] - s0);
+    if (deg > kBlameWarpDeg && (PASS == 0 || a.self_sub[j] < 0)) return true;
     if (PASS == 1 && a.self_sub[j] >= 0) {
       const int o = a.eoff[j];
-      if (o + 1 > a.out.capacity) { atomicOr(a.status, (uint32_t)LEO_ST_BLAME_OVERFLOW); continue; }
+      if (o + 1 > a.out.capacity) { atomicOr(a.status, (uint32_t)LEO_ST_BLAME_OVERFLOW); return false; }
       a.out.stalled[o] = j;
       a.out.edge[o] = -1;
       a.out.sub[o] = (uint8_t)a.self_sub[j];
       a.out.blame[o] = s_j;
       for (int c = 0; c < 4; c++) a.out.factors[(size_t)o * 4 + c] = 0.0;
-      continue;
+      return false;
     }
     bool self = deg == 0;
     double total = 0.0, n_sum = 0.0, d_min = 0, e_min = 0;
@@ -548,7 +578,7 @@ __global__ void k_blame(KView k, BlameArgs a) {
       if (PASS == 0 && n_sum == 0) self = true;
       else {
         const int o = PASS == 1 ? a.eoff[j] : 0;
-        if (PASS == 1 && o + a.ecount[j] > a.out.capacity) { atomicOr(a.status, (uint32_t)LEO_ST_BLAME_OVERFLOW); continue; }
+        if (PASS == 1 && o + a.ecount[j] > a.out.capacity) { atomicOr(a.status, (uint32_t)LEO_ST_BLAME_OVERFLOW); return false; }
         PySum ts;
         for (int x0 = 0; x0 < deg; x0 += kBU) {
           EdgeBatch eb;
@@ -580,31 +610,114 @@ __global__ void k_blame(KView k, BlameArgs a) {
         }
       }
     }
-    if (PASS == 1) continue;
+    if (PASS == 1) return false;
     if (self) {
-      int sub = dominant_self(a.p, j);
-      if (sub == LEO_SB_MEMORY_LATENCY && (kMemoryClasses & BIT(k.opclass[j])) && a.mp_ok) {
-        if (a.mp_ok[j]) sub = LEO_SB_INDIRECT_ADDRESSING;
-      } else if (sub == LEO_SB_MEMORY_LATENCY && (kMemoryClasses & BIT(k.opclass[j]))) {
-        // _address_traces_to_load: small searches inline (<= kSeenCap nodes),
-        // larger ones in k_selfblame_warp (warp per candidate)
-        int32_t seen[kSeenCap];
-        const int r = (a.dbg & LEO_DBG_SELF_SLOW) ? -1
-                      : traces_to_load(k, a.brbeg, a.brend, a.bprod, a.bmeta, j, seen, kSeenCap, nullptr, 0);
-        if (r < 0) {
-          int s2 = atomicAdd(a.slow_count, 1);
-          if (s2 < a.slow_cap) a.slow_list[s2] = j;
-          else atomicOr(a.status, (uint32_t)LEO_ST_SCRATCH_OVERFLOW);
-        } else if (r) {
-          sub = LEO_SB_INDIRECT_ADDRESSING;
-        }
-      }
-      a.self_sub[j] = sub;
-      a.ecount[j] = 1;
+      blame_self(k, a, j);
     } else {
       a.ecount[j] = deg;
       a.jtotal[j] = total;
       a.jnsum[j] = n_sum;
+    }
+  }
+  return false;
+}
+
+template <int PASS>
+LEO_DEV void blame_warp(const KView& k, const BlameArgs& a, int j, int lane) {
+  const int lat = a.p.lat[j];
+  const double s_j = (double)((int64_t)lat * a.p.period);
+  const int r0 = a.inc.rbeg[j], nr = a.inc.rend[j] - r0, s0 = a.inc.soff[j];
+  const int deg = nr + (a.inc.soff[j + 1] - s0);
+  const int o = PASS == 1 ? a.eoff[j] : 0;
+  if (PASS == 1 && o + a.ecount[j] > a.out.capacity) {
+    if (lane == 0) atomicOr(a.status, (uint32_t)LEO_ST_BLAME_OVERFLOW);
+    return;
+  }
+  // first minima (x == 0 || v < min) and the issue-count sum, in edge order
+  double d_min = 0, e_min = 0;
+  PySum ns;
+  for (int x0 = 0; x0 < deg; x0 += 32) {
+    const int x = x0 + lane;
+    double d = 0, ef = 0, ic = 0;
+    if (x < deg) {
+      const int e = x < nr ? r0 + x : (int)a.inc.sidx[s0 + (x - nr)];
+      const int pr = a.pprod[e];
+      d = a.pdist[e];
+      ef = a.p.eff[pr];
+      if (PASS == 0) ic = issue_count_ld(a.p, pr);
+    }
+    const int m = min(32, deg - x0);
+    for (int t = 0; t < m; t++) {
+      const double dv = __shfl_sync(0xffffffffu, d, t), ev = __shfl_sync(0xffffffffu, ef, t);
+      if (x0 + t == 0 || dv < d_min) d_min = dv;
+      if (x0 + t == 0 || ev < e_min) e_min = ev;
+      if (PASS == 0) ns.add(__shfl_sync(0xffffffffu, ic, t));
+    }
+  }
+  double n_sum, total = 0.0;
+  if (PASS == 0) {
+    n_sum = ns.value();
+    if (n_sum == 0) {
+      if (lane == 0) blame_self(k, a, j);
+      return;
+    }
+  } else {
+    n_sum = a.jnsum[j];
+    total = a.jtotal[j];
+  }
+  PySum ts;
+  for (int x0 = 0; x0 < deg; x0 += 32) {
+    const int x = x0 + lane;
+    double prod = 0;
+    if (x < deg) {
+      const int e = x < nr ? r0 + x : (int)a.inc.sidx[s0 + (x - nr)];
+      const int pr = a.pprod[e];
+      const double f0 = __ddiv_rn(d_min, a.pdist[e]);
+      const double f1 = __ddiv_rn(e_min, a.p.eff[pr]);
+      const double f2 = __ddiv_rn(issue_count_ld(a.p, pr), n_sum);
+      const double f3 = __ddiv_rn((double)a.p.cls_cnt[(size_t)j * 8 + kMatchClass[(a.pmeta[e] >> 30) & 3]], (double)lat);
+      prod = __dmul_rn(__dmul_rn(__dmul_rn(f0, f1), f2), f3);
+      if (PASS == 1) {
+        const int w = o + x;
+        a.out.stalled[w] = j;
+        a.out.edge[w] = e;
+        a.out.sub[w] = 255;
+        a.out.blame[w] = __ddiv_rn(__dmul_rn(s_j, prod), total);
+        double* f = a.out.factors + (size_t)w * 4;
+        f[0] = f0; f[1] = f1; f[2] = f2; f[3] = f3;
+      }
+    }
+    if (PASS == 0) {
+      const int m = min(32, deg - x0);
+      for (int t = 0; t < m; t++) ts.add(__shfl_sync(0xffffffffu, prod, t));
+    }
+  }
+  if (PASS == 0 && lane == 0) {
+    total = ts.value();
+    if (total == 0.0) blame_self(k, a, j);
+    else {
+      a.ecount[j] = deg;
+      a.jtotal[j] = total;
+      a.jnsum[j] = n_sum;
+    }
+  }
+}
+
+// pass 0: decide self vs edges, entry count, cached sums; pass 1: write entries
+template <int PASS>
+__global__ void k_blame(KView k, BlameArgs a) {
+  pdl_wait();
+  const int lane = threadIdx.x & 31;
+  // whole warps iterate together (the warp path needs every lane)
+  for (int j0 = blockIdx.x * blockDim.x + (threadIdx.x & ~31); j0 < k.N; j0 += gridDim.x * blockDim.x) {
+    const int j = j0 + lane;
+    const bool heavy = j < k.N && blame_one<PASS>(k, a, j);
+    unsigned hv = __ballot_sync(0xffffffffu, heavy);
+    while (hv) {
+      const int src = __ffs(hv) - 1;
+      hv &= hv - 1;
+      blame_warp<PASS>(k, a, j0 + src, lane);
+      __syncwarp();
     }
   }
 }
