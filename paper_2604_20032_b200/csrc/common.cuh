@@ -151,6 +151,32 @@ inline bool pdl_enabled() {
   return v == 1;
 }
 
+// Scheduling priority of the launches issued by this host thread: the
+// register-dataflow chain (the step's critical path) runs at the device's
+// greatest priority, the side branches that only need to finish before their
+// join (vendor sync tracing, binning, the addressing test) at the least, so
+// their CTAs fill the SMs the critical chain leaves free instead of
+// displacing it.  LEO_NO_PRIO=1 launches everything at the default priority.
+struct LaunchPrio {
+  static int& current() { static thread_local int p = 1; return p; }   // 1 = high, 0 = low
+};
+struct LowPriority {
+  int saved;
+  explicit LowPriority(bool on = true) : saved(LaunchPrio::current()) { if (on) LaunchPrio::current() = 0; }
+  ~LowPriority() { LaunchPrio::current() = saved; }
+};
+inline int prio_value(bool high) {
+  static int least = 0, greatest = 0, init = 0, off = 0;
+  if (!init) {
+    cudaDeviceGetStreamPriorityRange(&least, &greatest);
+    const char* e = getenv("LEO_NO_PRIO");
+    off = (e && e[0] == '1') ? 1 : 0;
+    init = 1;
+  }
+  if (off) return least;
+  return high ? greatest : least;
+}
+
 template <typename... KArgs, typename... Args>
 inline void leo_launch(void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t st,
                        Args&&... args) {
@@ -159,11 +185,18 @@ inline void leo_launch(void (*kern)(KArgs...), dim3 grid, dim3 block, size_t sme
   cfg.blockDim = block;
   cfg.dynamicSmemBytes = smem;
   cfg.stream = st;
-  cudaLaunchAttribute attr[1];
-  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
-  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cudaLaunchAttribute attr[2];
+  int na = 0;
+  if (pdl_enabled()) {
+    attr[na].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[na].val.programmaticStreamSerializationAllowed = 1;
+    na++;
+  }
+  attr[na].id = cudaLaunchAttributePriority;
+  attr[na].val.priority = prio_value(LaunchPrio::current() != 0);
+  na++;
   cfg.attrs = attr;
-  cfg.numAttrs = pdl_enabled() ? 1 : 0;
+  cfg.numAttrs = na;
   cudaLaunchKernelEx(&cfg, kern, std::forward<Args>(args)...);
 }
 

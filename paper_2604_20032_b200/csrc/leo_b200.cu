@@ -74,6 +74,19 @@ inline void debug_sync_after(int id, cudaStream_t st) {
   { TraceScope _ts(tr, id, st); __VA_ARGS__; } debug_sync_after(id, st); } while (0)
 
 // LEO_NO_FORK=1: run every stage on the caller's stream (debugging aid)
+// critical-path probe (profiling only): LEO_DBG_DELAY_<BRANCH>=<us> puts a
+// spin of that length at the head of the branch; if the step grows by the
+// same amount, the branch has no slack
+__global__ void k_spin(long long cycles) {
+  const long long t0 = clock64();
+  while (clock64() - t0 < cycles) {}
+}
+void dbg_delay(const char* env, cudaStream_t st) {
+  const char* v = getenv(env);
+  if (!v) return;
+  const double us = atof(v);
+  if (us > 0) k_spin<<<1, 1, 0, st>>>((long long)(us * 1965.0));
+}
 bool no_fork_env() {
   static int v = -1;
   if (v < 0) { const char* e = getenv("LEO_NO_FORK"); v = (e && e[0] == '1') ? 1 : 0; }
@@ -265,8 +278,18 @@ int build_graph_impl(const LeoKernel* kk, const LeoCaps* caps, LeoEdges* out, Le
   const bool fork = (tr == nullptr || (tr->mode & 1)) && !no_fork_env();
   cudaStream_t s_sync = fork ? sp.s[0] : st;
   if (fork) link_streams(st, s_sync, sp.e[0]);
+  dbg_delay("LEO_DBG_DELAY_SYNC", s_sync);
+  dbg_delay("LEO_DBG_DELAY_REACH", st);
   const int kind = k.dialect == LEO_AMD ? LEO_EK_MEM_WAITCNT : k.dialect == LEO_NVIDIA ? LEO_EK_MEM_BARRIER : LEO_EK_MEM_SWSB;
+  // the sync branch yields the SMs to the dataflow chain only when it runs a
+  // shared-memory tier (then it is the shorter branch; the thread-private
+  // Dijkstra path of big NVIDIA / Intel kernels is the long one)
+  const int sdbg0 = caps ? caps->debug_flags : 0;
+  const bool sync_smem_tier = !(sdbg0 & LEO_DBG_NO_SMEM) && B > 0 &&
+      (k.dialect == LEO_AMD ? sync_smem_bytes(N, B, 128) <= (size_t)kSmemResidentMax
+                            : setter_cta_smem(B) <= (size_t)kSmemResidentMax);
   {
+    LowPriority low_prio(sync_smem_tier);
     cudaStream_t st = s_sync;   // shadows the caller's stream for the TRACED scopes
     cudaMemsetAsync(pcnt, 0, (size_t)std::max(N, 1) * 4, st);
     cudaMemsetAsync(pcur, 0, (size_t)std::max(N, 1) * 4, st);
@@ -292,7 +315,11 @@ int build_graph_impl(const LeoKernel* kk, const LeoCaps* caps, LeoEdges* out, Le
       {
       const char* ws = getenv("LEO_WC_STEPS");
       const int wc_steps = ws ? atoi(ws) : kWcSmemSteps;
-      TRACED(KID_SYNC, leo_launch(k_sync_wc_smem, SM, wc_threads, wc_smem, st, k, sa, bev, wc_steps));
+      // half the SMs: the run time is the longest item's, and the other half
+      // stays free for the reach tier running beside it
+      const char* wcc = getenv("LEO_WC_CTAS");
+      const int wc_ctas = wcc ? atoi(wcc) : std::max(1, SM / 2);
+      TRACED(KID_SYNC, leo_launch(k_sync_wc_smem, wc_ctas, wc_threads, wc_smem, st, k, sa, bev, wc_steps));
     }
     else
       TRACED(KID_SYNC, leo_launch(k_sync<false>, grid_for(N, 64), 64, 0, st, k, sa, nullptr, 0));
@@ -743,6 +770,8 @@ int leo_analyze(const LeoKernel* k, const LeoProfile* p, const LeoSamples* sampl
   if (samples) {
     cudaStream_t s_bin = fork ? sp.s[1] : st;
     if (fork) link_streams(st, s_bin, sp.e[2]);
+    dbg_delay("LEO_DBG_DELAY_BIN", s_bin);
+    LowPriority low_prio;
     int r = bin_impl(samples, k->n_instr, (int32_t*)p->lat, (int32_t*)p->cls_cnt, tr, s_bin);
     if (r) return r;
   }
@@ -766,7 +795,11 @@ int leo_analyze(const LeoKernel* k, const LeoProfile* p, const LeoSamples* sampl
   LEO_CUDA_CHECK(ar_addr.commit());
   cudaStream_t s_addr = fork ? sp.s[3] : st;
   if (fork) link_streams(st, s_addr, sp.e[6]);
-  const Incoming binc = addr_impl(make_kview(k), base, ab, tr, s_addr);
+  Incoming binc;
+  {
+    LowPriority low_prio;
+    binc = addr_impl(make_kview(k), base, ab, tr, s_addr);
+  }
   if (stop == 5) {                              // build + the addressing branch
     if (fork) link_streams(s_addr, st, sp.e[7]);
     if (samples && fork) link_streams(sp.s[1], st, sp.e[3]);
