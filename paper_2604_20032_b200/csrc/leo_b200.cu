@@ -277,8 +277,6 @@ int build_graph_impl(const LeoKernel* kk, const LeoCaps* caps, LeoEdges* out, Le
   // inflated by queueing behind concurrent branches
   const bool fork = (tr == nullptr || (tr->mode & 1)) && !no_fork_env();
   cudaStream_t s_sync = fork ? sp.s[0] : st;
-  if (fork) link_streams(st, s_sync, sp.e[0]);
-  dbg_delay("LEO_DBG_DELAY_SYNC", s_sync);
   dbg_delay("LEO_DBG_DELAY_REACH", st);
   const int kind = k.dialect == LEO_AMD ? LEO_EK_MEM_WAITCNT : k.dialect == LEO_NVIDIA ? LEO_EK_MEM_BARRIER : LEO_EK_MEM_SWSB;
   // the sync branch yields the SMs to the dataflow chain only when it runs a
@@ -288,7 +286,16 @@ int build_graph_impl(const LeoKernel* kk, const LeoCaps* caps, LeoEdges* out, Le
   const bool sync_smem_tier = !(sdbg0 & LEO_DBG_NO_SMEM) && B > 0 &&
       (k.dialect == LEO_AMD ? sync_smem_bytes(N, B, 128) <= (size_t)kSmemResidentMax
                             : setter_cta_smem(B) <= (size_t)kSmemResidentMax);
-  {
+  // The sync branch forks off the dataflow chain.  With a shared-memory sync
+  // tier (the shorter branch) it forks only once the chain's first kernels
+  // are queued (after the unit-count scans), so its CTAs do not take the SMs the
+  // chain's head needs; LEO_SYNC_FORK_AT=0/1/2 (start / after the unit
+  // scans / after the block walk) overrides.
+  const char* fa_env = getenv("LEO_SYNC_FORK_AT");
+  const int fork_at = fa_env ? atoi(fa_env) : (sync_smem_tier ? 1 : 0);
+  auto enqueue_sync = [&]() {
+    if (fork) link_streams(st, s_sync, sp.e[0]);
+    dbg_delay("LEO_DBG_DELAY_SYNC", s_sync);
     LowPriority low_prio(sync_smem_tier);
     cudaStream_t st = s_sync;   // shadows the caller's stream for the TRACED scopes
     cudaMemsetAsync(pcnt, 0, (size_t)std::max(N, 1) * 4, st);
@@ -345,17 +352,20 @@ int build_graph_impl(const LeoKernel* kk, const LeoCaps* caps, LeoEdges* out, Le
     TRACED(KID_KEY_SCATTER, leo_launch(k_key_scatter, grid_for(cap_sync, T), T, 0, st, skeys, &ctr[3], cap_sync, poff, pcur, ssorted));
     TRACED(KID_SEGSORT, leo_launch(segsort_unique_u64, grid_for(N, 128), 128, 0, st, ssorted, poff, pcnt, nullptr, N, puniq, cap_sync));
     TRACED(KID_SCAN, scan_exclusive(puniq, puoff, nullptr, N, scan_tmp2, &ctr[6], st));
-  }
+  };
+  if (fork_at <= 0) enqueue_sync();
   // (a fused one-CTA count + scan is latency-bound on the operand loads: the
   // grid-wide count and two single-pass scans are faster)
   TRACED(KID_UNIT_COUNTS, leo_launch(k_unit_counts, std::max(grid_for(N, T), grid_for(B, T)), T, 0, st, k, ucnt, dcnt,
                                      B > 0 ? brec : nullptr, rhead));
   TRACED(KID_SCAN, scan_exclusive(ucnt, use_ptr, nullptr, N, scan_tmp, nullptr, st));
   TRACED(KID_SCAN, scan_exclusive(dcnt, def_ptr, nullptr, N, scan_tmp, nullptr, st));
+  if (fork_at == 1) enqueue_sync();
 
   WalkArgs wa{use_ptr, def_ptr, ev_res, q_block, q_unit, q_list, &ctr[0], ldtab, qtab, Bp, gtab};
   const size_t smem = walk_bytes(wpc, smem_tab);
   if (B > 0) TRACED(KID_BLOCK_WALK, leo_launch(k_block_walk, std::max(1, walk_ctas), wpc * 32, smem, st, k, wa, wpc));
+  if (fork_at >= 2) enqueue_sync();
 
   ReachArgs ra{caps ? caps->debug_flags : 0, ldtab, brec, U, Bp, q_block, q_unit, q_off, q_len, qres, cap_qres, &ctr[1],
                slow_list, &ctr[2], NU + 1024, status};
