@@ -313,12 +313,51 @@ class Session:
         self.pc = torch.empty(max(n_samples, 1), dtype=torch.int32, device=self.dev)
         self.cat = torch.empty(max(n_samples, 1), dtype=torch.uint8, device=self.dev)
         self.lut = torch.empty(256, dtype=torch.uint8, device=self.dev)
+        self.pin = pin
+        self._host = {}
+        self.h_pack = None
+        if pin:
+            self._pack_inputs()
         self.ds = device.DeviceSamples.from_tensors(self.pc[:n_samples], self.cat[:n_samples], self.lut)
         self.an = device.Analyzer(self.dk, self.dev)
-        self.pin = pin
         self.use_graph = True
         self.graph = None
-        self._host = {}
+
+    def _pack_inputs(self):
+        """Re-home every per-call input (kernel SoA, line ids, profile
+        metadata, category table) into one device buffer mirrored by one
+        pinned host buffer, so a call's H2D is a single copy instead of one
+        per array.  Raw samples stay separate (the library pulls them on the
+        binning branch)."""
+        dk, dp = self.dk, self.dp
+        specs = [("k_" + n, dk.t[n]) for n in self.H2D_FIELDS]
+        if "seg_block" in dk.t:
+            specs.append(("k_seg_block", dk.t["seg_block"]))
+        specs.append(("line_id", dk.line_id))
+        specs += [("p_" + n, getattr(dp, n)) for n in ("exec_cnt", "total", "eff", "sampled")]
+        specs.append(("lut", self.lut))
+        layout, off = [], 0
+        for name, t in specs:
+            nb = t.numel() * t.element_size()
+            layout.append((name, off, nb, t))
+            off = (off + nb + 15) & ~15
+        self.d_pack = torch.empty(max(off, 16), dtype=torch.uint8, device=self.dev)
+        self.h_pack = torch.empty(max(off, 16), dtype=torch.uint8).pin_memory()
+        for name, o, nb, t in layout:
+            dv = self.d_pack[o:o + nb].view(t.dtype).view(t.shape)
+            dv.copy_(t)
+            self._host[name] = self.h_pack[o:o + nb].view(t.dtype).view(t.shape)
+            if name.startswith("k_"):
+                dk.t[name[2:]] = dv
+            elif name == "line_id":
+                dk.line_id = dv
+            elif name.startswith("p_"):
+                setattr(dp, name[2:], dv)
+            else:
+                self.lut = dv
+        dk.struct = abi.kernel_struct(dk.ks, lambda n: dk.t[n].data_ptr())
+        dp.struct = abi.LeoProfile(dp.period, device.ptr(dp.lat), device.ptr(dp.cls_cnt), device.ptr(dp.exec_cnt),
+                                   device.ptr(dp.total), device.ptr(dp.eff), device.ptr(dp.sampled))
 
     def _h(self, name, arr):
         """pinned host staging copy of a numpy input"""
@@ -351,9 +390,14 @@ class Session:
         self.ds.set_host_sources(self._host["pc"], self._host["cat"].view(torch.uint8))
 
     def h2d_bytes(self) -> int:
+        if self.h_pack is not None:
+            return self.h_pack.numel() + sum(self._host[n].numel() * self._host[n].element_size() for n in ("pc", "cat"))
         return sum(t.numel() * t.element_size() for t in self._host.values())
 
     def _h2d(self):
+        if self.h_pack is not None:
+            self.d_pack.copy_(self.h_pack, non_blocking=True)
+            return
         for n in self.H2D_FIELDS:
             self.dk.t[n].view(-1).copy_(self._host["k_" + n], non_blocking=True)
         if "k_seg_block" in self._host:
