@@ -380,7 +380,13 @@ int build_graph_impl(const LeoKernel* kk, const LeoCaps* caps, LeoEdges* out, Le
   int ru_threads = 128;
   while (ru_threads > 32 && reach_unit_smem(bcap, ru_threads) > (size_t)kSmemResidentMax) ru_threads >>= 1;
   const size_t ru_smem = reach_unit_smem(bcap, ru_threads);
-  const int ru_parts = n_seg > 1 ? 1 : std::max(1, std::min(8, (2 * SM + U - 1) / std::max(U, 1)));
+  // CTAs per unit: one when the units alone cover the SMs (every extra CTA
+  // re-stages the CFG and takes shared memory the sync branch also wants),
+  // else enough to reach ~1.5 CTAs per SM (measured: C2 1 part 283 us vs 2
+  // parts 289 us; C3 5 parts 381 us vs 7 parts 387 us).  LEO_RU_PARTS overrides.
+  const char* rp_env = getenv("LEO_RU_PARTS");
+  const int ru_parts = n_seg > 1 ? 1 : rp_env ? std::max(1, atoi(rp_env))
+                       : U >= SM ? 1 : std::max(1, std::min(8, (3 * SM + 2 * U - 1) / (2 * std::max(U, 1))));
   const int per_seg = n_seg > 1 ? std::max(1, std::min(U, (4 * SM + n_seg - 1) / n_seg))
                                 : std::min(U, SM * 8) * ru_parts;
   if (B > 0 && U > 0 && ru_smem <= (size_t)kSmemResidentMax && !(dbg & LEO_DBG_NO_SMEM)) {
