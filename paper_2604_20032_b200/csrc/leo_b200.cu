@@ -5,6 +5,7 @@
 // same stream.  No host synchronisation happens inside the pipeline: every
 // data-dependent size lives in device memory and the kernels read it there.
 #include <algorithm>
+#include <functional>
 #include <cstdio>
 #include <cstring>
 #include <cstdlib>
@@ -216,7 +217,8 @@ int check_kernel(const LeoKernel* k) {
 // ---------------------------------------------------------------------------
 // build_graph
 int build_graph_impl(const LeoKernel* kk, const LeoCaps* caps, LeoEdges* out, LeoDiags* diags,
-                     uint32_t* status, cudaStream_t st, Range own = Range{0, 0}) {
+                     uint32_t* status, cudaStream_t st, Range own = Range{0, 0},
+                     const std::function<int()>& after_walk = {}) {
   LeoTrace* tr = caps ? caps->trace : nullptr;
   KView k = make_kview(kk);
   const int N = k.N, B = k.B, U = k.U;
@@ -365,6 +367,11 @@ int build_graph_impl(const LeoKernel* kk, const LeoCaps* caps, LeoEdges* out, Le
   WalkArgs wa{use_ptr, def_ptr, ev_res, q_block, q_unit, q_list, &ctr[0], ldtab, qtab, Bp, gtab};
   const size_t smem = walk_bytes(wpc, smem_tab);
   if (B > 0) TRACED(KID_BLOCK_WALK, leo_launch(k_block_walk, std::max(1, walk_ctas), wpc * 32, smem, st, k, wa, wpc));
+  // a caller's side branch (leo_analyze: stage-0 binning) forks here, after
+  // the dataflow chain's head has been queued
+  if (after_walk) {
+    if (int e = after_walk()) return e;
+  }
   if (fork_at >= 2) enqueue_sync();
 
   ReachArgs ra{caps ? caps->debug_flags : 0, ldtab, brec, U, Bp, q_block, q_unit, q_off, q_len, qres, cap_qres, &ctr[1],
@@ -783,16 +790,25 @@ int leo_analyze(const LeoKernel* k, const LeoProfile* p, const LeoSamples* sampl
   LeoTrace* tr = caps ? caps->trace : nullptr;
   // stage-0 binning only feeds pruning and blame: run it beside build_graph
   const bool fork = (tr == nullptr || (tr->mode & 1)) && !no_fork_env();
-  if (samples) {
+  auto enqueue_bin = [&]() -> int {
+    if (!samples) return 0;
     cudaStream_t s_bin = fork ? sp.s[1] : st;
     if (fork) link_streams(st, s_bin, sp.e[2]);
     dbg_delay("LEO_DBG_DELAY_BIN", s_bin);
     LowPriority low_prio;
-    int r = bin_impl(samples, k->n_instr, (int32_t*)p->lat, (int32_t*)p->cls_cnt, tr, s_bin);
-    if (r) return r;
+    return bin_impl(samples, k->n_instr, (int32_t*)p->lat, (int32_t*)p->cls_cnt, tr, s_bin);
+  };
+  // Up to 16 M samples the binning branch forks after the block walk: it has
+  // the whole build as slack, and started with the build it takes SMs from
+  // the dataflow chain's head.  Bigger streams (C5: 100 M, ~1 ms of binning)
+  // need the whole build to hide in.
+  const bool late_bin = samples && samples->n_samples <= (16ll << 20);
+  if (!late_bin) {
+    if (int e = enqueue_bin()) return e;
   }
   const Range own{cfg->consumer_lo, cfg->consumer_hi};
-  int r = build_graph_impl(k, caps, base, diags, status, st, own);
+  int r = build_graph_impl(k, caps, base, diags, status, st, own,
+                           late_bin ? std::function<int()>(enqueue_bin) : std::function<int()>());
   if (r) return r;
   // LEO_DBG_STOP=s (profiling only): end the pipeline after stage s
   // (1 build, 2 prune, 3 incoming CSR, 4 slice) to time prefixes in a graph
