@@ -457,12 +457,18 @@ int prune_impl(const LeoKernel* kk, const LeoProfile* pp, const LeoConfig* cfg, 
               *paths, slow_list, &ctr[0], cap_slow, *diags, status};
   {
     const int dbg = caps ? caps->debug_flags : 0;
-    const size_t staged = prune_smem_bytes(k.N, k.B, 128, true), unstaged = prune_smem_bytes(k.N, k.B, 128, false);
+    const char* pt_env = getenv("LEO_PRUNE_THREADS");
+    const char* pc_env = getenv("LEO_PRUNE_CTAS");
+    // 256 threads per CTA when the image and the per-thread DFS state fit
+    // (one edge per thread per round at C2 size: prune 45 -> 37 us)
+    const int pthreads = pt_env ? atoi(pt_env)
+                         : prune_smem_bytes(k.N, k.B, 256, true) <= (size_t)kSmemResidentMax ? 256 : 128;
+    const size_t staged = prune_smem_bytes(k.N, k.B, pthreads, true), unstaged = prune_smem_bytes(k.N, k.B, 128, false);
     // staged CFG image when it fits; otherwise the many-CTA global-memory
     // kernel (thread per edge, no per-round CTA barriers) balances better
     (void)unstaged;
     if (!(dbg & LEO_DBG_NO_SMEM) && staged <= (size_t)kSmemResidentMax)
-      TRACED(KID_PRUNE, leo_launch(k_prune_edges_smem<true>, num_sms(), 128, staged, st, k, p, a));
+      TRACED(KID_PRUNE, leo_launch(k_prune_edges_smem<true>, pc_env ? atoi(pc_env) : num_sms(), pthreads, staged, st, k, p, a));
     else
       TRACED(KID_PRUNE, leo_launch(k_prune_edges, grid_for(cap_in, 128, num_sms() * 16), 128, 0, st, k, p, a));
   }
