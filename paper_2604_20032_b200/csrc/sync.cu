@@ -897,6 +897,7 @@ __global__ void k_sync_wc_smem(KView k, SyncArgs a, const uint32_t* __restrict__
       evp0[b] = c0; evp1[b] = c1;
     }
     __syncthreads();
+    pm.mark(1, 4);
     // exclusive scan of the counts (thread-contiguous chunks)
     const int per = (B + T - 1) / T, lo = min(B, (int)threadIdx.x * per), hi = min(B, lo + per);
     int s0 = 0, s1 = 0;
@@ -911,6 +912,7 @@ __global__ void k_sync_wc_smem(KView k, SyncArgs a, const uint32_t* __restrict__
     }
     if (threadIdx.x == 0) { evp0[B] = t0; evp1[B] = t1; }
     __syncthreads();
+    pm.mark(1, 5);
     for (int b = threadIdx.x; b < B; b += T) {
       int q0 = evp0[b], q1 = evp1[b];
       for (int x = bf[b]; x <= bl[b]; x++) {

@@ -97,7 +97,7 @@ if args.phases:
     an2.launch(dp, cfg, ds)
     torch.cuda.synchronize()
     names = {0: ("reach_unit", ["staged", "near", "qlist", "queries"]),
-             1: ("sync_wc_smem", ["staged", "events", "items"]),
+             1: ("sync_wc_smem", ["staged", "events", "items", "ev_count", "ev_scan"]),
              2: ("prune_edges_smem", ["staged", "edges"])}
     for slot, (nm, ph) in names.items():
         buf = np.zeros((1024, 8), dtype=np.int64)
