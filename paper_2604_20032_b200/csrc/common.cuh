@@ -158,11 +158,19 @@ inline bool pdl_enabled() {
 // their CTAs fill the SMs the critical chain leaves free instead of
 // displacing it.  LEO_NO_PRIO=1 launches everything at the default priority.
 struct LaunchPrio {
-  static int& current() { static thread_local int p = 1; return p; }   // 1 = high, 0 = low
+  // 1 = greatest, 0 = least, -1 = no priority attribute (the default)
+  static int& current() { static thread_local int p = -1; return p; }
+};
+struct HighPriority {
+  int saved;
+  explicit HighPriority(bool on) : saved(LaunchPrio::current()) { if (on) LaunchPrio::current() = 1; }
+  ~HighPriority() { LaunchPrio::current() = saved; }
 };
 struct LowPriority {
   int saved;
-  explicit LowPriority(bool on = true) : saved(LaunchPrio::current()) { if (on) LaunchPrio::current() = 0; }
+  explicit LowPriority(bool on = true) : saved(LaunchPrio::current()) {
+    if (on && saved >= 0) LaunchPrio::current() = 0;   // only inside a prioritised call
+  }
   ~LowPriority() { LaunchPrio::current() = saved; }
 };
 inline int prio_value(bool high) {
@@ -192,9 +200,11 @@ inline void leo_launch(void (*kern)(KArgs...), dim3 grid, dim3 block, size_t sme
     attr[na].val.programmaticStreamSerializationAllowed = 1;
     na++;
   }
-  attr[na].id = cudaLaunchAttributePriority;
-  attr[na].val.priority = prio_value(LaunchPrio::current() != 0);
-  na++;
+  if (LaunchPrio::current() >= 0) {
+    attr[na].id = cudaLaunchAttributePriority;
+    attr[na].val.priority = prio_value(LaunchPrio::current() != 0);
+    na++;
+  }
   cfg.attrs = attr;
   cfg.numAttrs = na;
   cudaLaunchKernelEx(&cfg, kern, std::forward<Args>(args)...);

@@ -793,6 +793,14 @@ int leo_analyze(const LeoKernel* k, const LeoProfile* p, const LeoSamples* sampl
   if (!cfg) return -3;
   cudaStream_t st = (cudaStream_t)stream;
   SidePool& sp = side_pool();
+  // Launch priorities only where measured to help: kernels whose vendor sync
+  // tracing runs a shared-memory tier (the dataflow chain is then the critical
+  // branch).  Big NVIDIA / Intel kernels run everything at the default.
+  const int adbg = caps ? caps->debug_flags : 0;
+  const bool prio = !(adbg & LEO_DBG_NO_SMEM) && k->n_blocks > 0 &&
+      (k->dialect == LEO_AMD ? sync_smem_bytes(k->n_instr, k->n_blocks, 128) <= (size_t)kSmemResidentMax
+                             : setter_cta_smem(k->n_blocks) <= (size_t)kSmemResidentMax);
+  HighPriority high_prio(prio);
   LeoTrace* tr = caps ? caps->trace : nullptr;
   // stage-0 binning only feeds pruning and blame: run it beside build_graph
   const bool fork = (tr == nullptr || (tr->mode & 1)) && !no_fork_env();
@@ -801,7 +809,9 @@ int leo_analyze(const LeoKernel* k, const LeoProfile* p, const LeoSamples* sampl
     cudaStream_t s_bin = fork ? sp.s[1] : st;
     if (fork) link_streams(st, s_bin, sp.e[2]);
     dbg_delay("LEO_DBG_DELAY_BIN", s_bin);
-    LowPriority low_prio;
+    // small streams bin at the least priority; a big stream (C5) is itself a
+    // long branch and keeps the default
+    LowPriority low_prio(samples->n_samples <= (16ll << 20));
     return bin_impl(samples, k->n_instr, (int32_t*)p->lat, (int32_t*)p->cls_cnt, tr, s_bin);
   };
   // Up to 16 M samples the binning branch forks after the block walk: it has
