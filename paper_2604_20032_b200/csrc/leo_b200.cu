@@ -818,7 +818,9 @@ int leo_analyze(const LeoKernel* k, const LeoProfile* p, const LeoSamples* sampl
   // the whole build as slack, and started with the build it takes SMs from
   // the dataflow chain's head.  Bigger streams (C5: 100 M, ~1 ms of binning)
   // need the whole build to hide in.
-  const bool late_bin = samples && samples->n_samples <= (16ll << 20);
+  // (a stream still in host memory forks at once: its transfer needs the
+  // whole build to hide in)
+  const bool late_bin = samples && samples->n_samples <= (16ll << 20) && !samples->pc_host;
   if (!late_bin) {
     if (int e = enqueue_bin()) return e;
   }
