@@ -79,6 +79,30 @@ def test_device_matches_oracle_synthetic(tag, scale, cuda):
     assert np.isclose(r["line_stall"].sum(), total, rtol=1e-9)
 
 
+@pytest.mark.parametrize("tag,knobs", [
+    ("c2", {"LEO_SYNC_FORK_AT": "0", "LEO_RU_PARTS": "3", "LEO_WC_CTAS": "148", "LEO_PRUNE_THREADS": "128"}),
+    ("c2", {"LEO_WC_STEPS": "32", "LEO_NO_PRIO": "1"}),
+    ("c3", {"LEO_SYNC_FORK_AT": "2", "LEO_RU_PARTS": "1", "LEO_PRUNE_THREADS": "128"}),
+])
+def test_device_schedule_knobs_exact(tag, knobs, cuda, monkeypatch):
+    """The scheduling knobs (fork points, CTAs per unit, waitcnt tier size
+    and step limit, prune CTA size) move work between tiers and branches; the
+    results must not move.  Half-size C2 / C3 against the oracle."""
+    from oracle import oracle
+    from paper_2604_20032_b200 import abi, device, synth
+    for k, v in knobs.items():
+        monkeypatch.setenv(k, v)
+    wl = synth.config_workload(tag, scale=0.5)
+    ks = wl.kernel
+    r = device.analyze_soa(ks, wl.profile, abi.make_config(dialect=ks.dialect),
+                           samples=(wl.pc, wl.cat, wl.lut), device=cuda)
+    assert r["status"] == 0
+    pf = synth.bin_host(wl)
+    o = oracle.run(ks, pf)
+    errs = parity.compare(parity.oracle_outputs(ks, o), device_outputs(ks, r), rel=0.0, line_rel=1e-9)
+    assert not errs, errs
+
+
 def test_device_full_c5_properties(cuda):
     """C5 at full size (1M instructions, 100M samples): size-independent
     properties — binning conserves S, blame conserves stall cycles per line
