@@ -213,15 +213,17 @@ __global__ void k_block_walk(KView k, WalkArgs a, int warps_per_cta) {
             if (prev == seen) { lead = true; res = -(e + 1); }
             else res = -(prev + 1);          // another lane of this chunk claimed it
           }
-          const unsigned lm = __ballot_sync(0xffffffffu, lead);
-          if (lm) {
-            if (nlead + __popc(lm) > kWalkLeads) publish();
-            if (lead) {
-              leads[nlead + __popc(lm & lt)] = e;
-              a.q_block[e] = b;
-              a.q_unit[e] = u;
+          if (a.q_list) {                  // the query list feeds tier 1 only
+            const unsigned lm = __ballot_sync(0xffffffffu, lead);
+            if (lm) {
+              if (nlead + __popc(lm) > kWalkLeads) publish();
+              if (lead) leads[nlead + __popc(lm & lt)] = e;
+              nlead += __popc(lm);
             }
-            nlead += __popc(lm);
+          }
+          if (lead) {
+            a.q_block[e] = b;
+            a.q_unit[e] = u;
           }
           if (valid) a.ev_res[e] = res;
           __syncwarp();
@@ -245,7 +247,7 @@ __global__ void k_block_walk(KView k, WalkArgs a, int warps_per_cta) {
     }
     __syncwarp();
   }
-  if (nlead) publish();
+  if (a.q_list && nlead) publish();
 }
 
 struct ReachArgs {

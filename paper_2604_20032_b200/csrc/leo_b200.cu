@@ -364,7 +364,15 @@ int build_graph_impl(const LeoKernel* kk, const LeoCaps* caps, LeoEdges* out, Le
   TRACED(KID_SCAN, scan_exclusive(dcnt, def_ptr, nullptr, N, scan_tmp, nullptr, st));
   if (fork_at == 1) enqueue_sync();
 
-  WalkArgs wa{use_ptr, def_ptr, ev_res, q_block, q_unit, q_list, &ctr[0], ldtab, qtab, Bp, gtab};
+  // tier 0 (shared-memory reach) reads the query columns, not the list
+  const int n_seg0 = (kk->n_segments > 1 && kk->seg_block) ? kk->n_segments : 1;
+  const int bcap0 = n_seg0 > 1 ? kk->max_seg_blocks : B;
+  int ru_threads0 = 128;
+  while (ru_threads0 > 32 && reach_unit_smem(bcap0, ru_threads0) > (size_t)kSmemResidentMax) ru_threads0 >>= 1;
+  const int wdbg = caps ? caps->debug_flags : 0;
+  const bool tier0 = B > 0 && U > 0 && reach_unit_smem(bcap0, ru_threads0) <= (size_t)kSmemResidentMax &&
+                     !(wdbg & LEO_DBG_NO_SMEM);
+  WalkArgs wa{use_ptr, def_ptr, ev_res, q_block, q_unit, tier0 ? nullptr : q_list, &ctr[0], ldtab, qtab, Bp, gtab};
   const size_t smem = walk_bytes(wpc, smem_tab);
   if (B > 0) TRACED(KID_BLOCK_WALK, leo_launch(k_block_walk, std::max(1, walk_ctas), wpc * 32, smem, st, k, wa, wpc));
   // a caller's side branch (leo_analyze: stage-0 binning) forks here, after
@@ -396,7 +404,7 @@ int build_graph_impl(const LeoKernel* kk, const LeoCaps* caps, LeoEdges* out, Le
                        : U >= SM ? 1 : std::max(1, std::min(8, (3 * SM + 2 * U - 1) / (2 * std::max(U, 1))));
   const int per_seg = n_seg > 1 ? std::max(1, std::min(U, (4 * SM + n_seg - 1) / n_seg))
                                 : std::min(U, SM * 8) * ru_parts;
-  if (B > 0 && U > 0 && ru_smem <= (size_t)kSmemResidentMax && !(dbg & LEO_DBG_NO_SMEM)) {
+  if (tier0) {
     // tier 0: the CFG and one unit's columns resident in shared memory, CTA per unit
     TRACED(KID_REACH_FAST, leo_launch(k_reach_unit, n_seg * per_seg, ru_threads, ru_smem, st, k, ra, qtab, rhead, ru_parts,
                                                  n_seg > 1 ? kk->seg_block : nullptr, per_seg, bcap));
