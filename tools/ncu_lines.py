@@ -34,10 +34,17 @@ for r in rows:
     except ValueError:
         continue
     key = (cur_file, int(r[0]), r[1].strip()[:70])
-    a = agg.setdefault(key, [0, 0])
+    a = agg.setdefault(key, [0, 0, {}])
     a[0] += v
     a[1] += ex
+    for i, name in enumerate(h):
+        if name.startswith("stall_") and "(Not" not in name:
+            try:
+                a[2][name[6:]] = a[2].get(name[6:], 0) + int(float(r[i] or 0))
+            except ValueError:
+                pass
 tot = sum(v[0] for v in agg.values())
 print(f"{tot} stall samples")
-for (f, ln, src), (v, ex) in sorted(agg.items(), key=lambda x: -x[1][0])[:top]:
-    print(f"{100 * v / max(tot, 1):5.1f}% {v:6d} {ex:8d}  {f}:{ln}  {src}")
+for (f, ln, src), (v, ex, rs) in sorted(agg.items(), key=lambda x: -x[1][0])[:top]:
+    why = " ".join(f"{k}={n}" for k, n in sorted(rs.items(), key=lambda x: -x[1])[:3] if n)
+    print(f"{100 * v / max(tot, 1):5.1f}% {v:6d} {ex:8d}  {f}:{ln}  {src}  [{why}]")
