@@ -439,6 +439,7 @@ __global__ void k_reach_unit(KView k, ReachArgs a, const int32_t* __restrict__ q
     {
       const int per = (B + T - 1) / T, lo = tid * per, hi = min(B, lo + per);
       long long run = -1;
+#pragma unroll 8
       for (int y = lo; y < hi; y++) run = max(run, ((long long)rh[y] << 32) | (long long)(cell[y] + 1));
       long long inc = run;
       for (int o = 1; o < 32; o <<= 1) {
@@ -451,6 +452,7 @@ __global__ void k_reach_unit(KView k, ReachArgs a, const int32_t* __restrict__ q
       for (int w = 0; w < (tid >> 5); w++) carry = max(carry, wmax[w]);
       const long long prev = __shfl_up_sync(0xffffffffu, inc, 1);
       if ((tid & 31) > 0) carry = max(carry, prev);
+#pragma unroll 8
       for (int y = lo; y < hi; y++) {
         carry = max(carry, ((long long)rh[y] << 32) | (long long)(cell[y] + 1));
         const int d = (int)(carry & 0xffffffffLL) - 1;
@@ -464,6 +466,7 @@ __global__ void k_reach_unit(KView k, ReachArgs a, const int32_t* __restrict__ q
     {
       const int per = (B + T - 1) / T, lo = min(B, tid * per), hi = min(B, lo + per);
       int cnt = 0;
+#pragma unroll 8
       for (int y = lo; y < hi; y++) cnt += qs[y] >= 0;
       int tot;
       int pos = block_excl_scan(cnt, swarp, &tot);
