@@ -145,42 +145,94 @@ __global__ void k_bin_plan(int nb, int slice, const int32_t* __restrict__ bucket
   if (threadIdx.x == 0) { bucket_off[nb] = carry; slice_off[nb] = scarry; }
 }
 
-// pass 3: scatter u16 keys ((pc mod R) * 8 + class) into bucket ranges
+// pass 3: scatter u16 keys ((pc mod R) * 8 + class) into bucket ranges.
+// A sample-by-sample scatter writes one 2-byte key per 32-byte sector (16x
+// write amplification at 100 M samples).  Instead each CTA sorts sub-chunks
+// of kBinSub samples by bucket in shared memory (histogram, scan, local
+// scatter) and copies every bucket's run out contiguously, so consecutive
+// threads write consecutive keys.
+constexpr int kBinSub = 8192;
+
 __global__ void __launch_bounds__(512) k_bin_scatter(int64_t S, const int32_t* __restrict__ pc, const uint8_t* __restrict__ cat,
                                                      const uint8_t* __restrict__ lut, int N, int nb, int R,
                                                      const int32_t* __restrict__ M, const int32_t* __restrict__ bucket_off,
                                                      uint16_t* __restrict__ keys) {
   pdl_wait();
-  extern __shared__ int32_t cur[];               // nb cursors
+  extern __shared__ int32_t dyn[];
+  int32_t* cur = dyn;                            // nb: global cursor per bucket (this chunk)
+  int32_t* lcnt = dyn + nb;                      // nb: sub-chunk histogram, then local offsets
+  int32_t* lpos = lcnt + nb;                     // nb: local fill cursors
+  uint16_t* lkey = reinterpret_cast<uint16_t*>(lpos + nb);      // kBinSub keys
+  uint16_t* lbkt = lkey + kBinSub;                              // kBinSub buckets
   __shared__ uint8_t slut[256];
+  __shared__ int sw[33];
   for (int x = threadIdx.x; x < nb; x += blockDim.x) cur[x] = bucket_off[x] + M[(size_t)blockIdx.x * nb + x];
   for (int x = threadIdx.x; x < 256; x += blockDim.x) slut[x] = lut[x];
-  __syncthreads();
   const int64_t per = bin_chunk_per(S, gridDim.x);
   const int64_t s0 = (int64_t)blockIdx.x * per, s1 = min(S, s0 + per);
-  if (s0 >= s1) return;
-  const int64_t v0 = s0 / 4, v1 = s1 / 4;
-  const int4* pc4 = reinterpret_cast<const int4*>(pc);
-  const uint32_t* cat4 = reinterpret_cast<const uint32_t*>(cat);
-  for (int64_t v = v0 + threadIdx.x; v < v1; v += blockDim.x) {
-    const int4 p = pc4[v];
-    const uint32_t c = cat4[v];
-    const int ps[4] = {p.x, p.y, p.z, p.w};
+  for (int64_t c0 = s0; c0 < s1; c0 += kBinSub) {
+    const int n = (int)min((int64_t)kBinSub, s1 - c0);
+    for (int x = threadIdx.x; x < nb; x += blockDim.x) lcnt[x] = 0;
+    __syncthreads();
+    // histogram of the sub-chunk (c0 is a multiple of 4: int4 loads)
+    const int nv = n / 4;
+    const int4* pc4 = reinterpret_cast<const int4*>(pc + c0);
+    const uint32_t* cat4 = reinterpret_cast<const uint32_t*>(cat + c0);
+    for (int v = threadIdx.x; v < nv; v += blockDim.x) {
+      const int4 p = pc4[v];
+      const int ps[4] = {p.x, p.y, p.z, p.w};
 #pragma unroll
-    for (int t = 0; t < 4; t++) {
-      const int j = ps[t];
+      for (int t = 0; t < 4; t++)
+        if (ps[t] >= 0 && ps[t] < N) atomicAdd(&lcnt[ps[t] / R], 1);
+    }
+    for (int x = nv * 4 + threadIdx.x; x < n; x += blockDim.x) {
+      const int j = pc[c0 + x];
+      if (j >= 0 && j < N) atomicAdd(&lcnt[j / R], 1);
+    }
+    __syncthreads();
+    // local offsets (exclusive scan over buckets, thread-contiguous chunks)
+    {
+      const int pb = (nb + blockDim.x - 1) / blockDim.x, lo = min(nb, (int)threadIdx.x * pb), hi = min(nb, lo + pb);
+      int sum = 0;
+      for (int x = lo; x < hi; x++) sum += lcnt[x];
+      int tot;
+      int run = block_excl_scan(sum, sw, &tot);
+      for (int x = lo; x < hi; x++) { const int v = lcnt[x]; lcnt[x] = run; lpos[x] = run; run += v; }
+    }
+    __syncthreads();
+    // local scatter into shared memory
+    for (int v = threadIdx.x; v < nv; v += blockDim.x) {
+      const int4 p = pc4[v];
+      const uint32_t c = cat4[v];
+      const int ps[4] = {p.x, p.y, p.z, p.w};
+#pragma unroll
+      for (int t = 0; t < 4; t++) {
+        const int j = ps[t];
+        if (j < 0 || j >= N) continue;
+        const int b = j / R;
+        const int q = atomicAdd(&lpos[b], 1);
+        lkey[q] = (uint16_t)(((j - b * R) << 3) | slut[(c >> (8 * t)) & 0xFF]);
+        lbkt[q] = (uint16_t)b;
+      }
+    }
+    for (int x = nv * 4 + threadIdx.x; x < n; x += blockDim.x) {
+      const int j = pc[c0 + x];
       if (j < 0 || j >= N) continue;
       const int b = j / R;
-      const int pos = atomicAdd(&cur[b], 1);
-      keys[pos] = (uint16_t)(((j - b * R) << 3) | slut[(c >> (8 * t)) & 0xFF]);
+      const int q = atomicAdd(&lpos[b], 1);
+      lkey[q] = (uint16_t)(((j - b * R) << 3) | slut[cat[c0 + x]]);
+      lbkt[q] = (uint16_t)b;
     }
-  }
-  for (int64_t x = v1 * 4 + threadIdx.x; x < s1; x += blockDim.x) {
-    const int j = pc[x];
-    if (j < 0 || j >= N) continue;
-    const int b = j / R;
-    const int pos = atomicAdd(&cur[b], 1);
-    keys[pos] = (uint16_t)(((j - b * R) << 3) | slut[cat[x]]);
+    __syncthreads();
+    // runs out: element q of bucket b lands at cur[b] + (q - lcnt[b])
+    const int nk = lpos[nb - 1] > 0 ? lpos[nb - 1] : 0;   // valid keys = end of the last bucket
+    for (int q = threadIdx.x; q < nk; q += blockDim.x) {
+      const int b = lbkt[q];
+      keys[cur[b] + (q - lcnt[b])] = lkey[q];
+    }
+    __syncthreads();
+    for (int x = threadIdx.x; x < nb; x += blockDim.x) cur[x] += lpos[x] - lcnt[x];
+    __syncthreads();
   }
 }
 

@@ -195,12 +195,14 @@ void set_smem_attributes() {
   if (done) return;
   cudaFuncSetAttribute(k_reach_fast, cudaFuncAttributeMaxDynamicSharedMemorySize, kT1Threads * kT1Hash * 4);
   cudaFuncSetAttribute(k_bin_count, cudaFuncAttributeMaxDynamicSharedMemorySize, kBinRMax * 8 * 4);
+  cudaFuncSetAttribute(k_bin_scatter, cudaFuncAttributeMaxDynamicSharedMemorySize, kBinMaxBuckets * 12 + kBinSub * 4);
   cudaFuncSetAttribute(k_block_walk, cudaFuncAttributeMaxDynamicSharedMemorySize, 96 * 1024);
   cudaFuncSetAttribute(k_sync_wc_warp, cudaFuncAttributeMaxDynamicSharedMemorySize, 4 * kWcSmemInts * 4);
   cudaFuncSetAttribute(k_reach_unit, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemResidentMax);
   cudaFuncSetAttribute(k_sync_wc_smem, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemResidentMax);
   cudaFuncSetAttribute(k_sync_setter_smem, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kDHBytes);
-  cudaFuncSetAttribute(k_sync_setter_cta, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemResidentMax);
+  cudaFuncSetAttribute(k_sync_setter_cta<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemResidentMax);
+  cudaFuncSetAttribute(k_sync_setter_cta<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)(16 + setter_warp_tables_smem()));
   cudaFuncSetAttribute(k_prune_edges_smem<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemResidentMax);
   cudaFuncSetAttribute(k_prune_edges_smem<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemResidentMax);
   done = true;
@@ -311,9 +313,11 @@ int build_graph_impl(const LeoKernel* kk, const LeoCaps* caps, LeoEdges* out, Le
     SyncArgs sa{caps ? caps->debug_flags : 0, skeys, cap_sync, &ctr[3], slow2, &ctr[4], cap_slow, *diags, status,
                 wcword, setword, lastset, n_ids, wlist, &ctr[8], wclist, &ctr[10], 0};
     const int sdbg = caps ? caps->debug_flags : 0;
-    const bool setter_cta = k.dialect != LEO_AMD && B > 0 && setter_cta_smem(B) <= (size_t)kSmemResidentMax &&
-                            !(sdbg & (LEO_DBG_NO_SMEM | LEO_DBG_SYNC_SLOW));
-    sa.defer_search = setter_cta ? 1 : 0;
+    const bool setter_staged = setter_cta_smem(B) <= (size_t)kSmemResidentMax && !getenv("LEO_SETTER_GLOBAL");
+    const bool setter_cta = k.dialect != LEO_AMD && B > 0 && !(sdbg & (LEO_DBG_NO_SMEM | LEO_DBG_SYNC_SLOW));
+    // staged: every block search goes to the warp tier; from L2 the warp tier
+    // only takes what overflows the thread-private Dijkstra (measured on C5)
+    sa.defer_search = setter_cta && setter_staged ? 1 : 0;
     // as many threads per CTA as the image allows: more warps hide the
     // shared-memory latency of the event-list build and spread the items
     int wc_threads = 512;
@@ -338,9 +342,14 @@ int build_graph_impl(const LeoKernel* kk, const LeoCaps* caps, LeoEdges* out, Le
     if (k.dialect != LEO_AMD) {
       // setter searches: CTA per item in shared memory first; the rest (and
       // forced-slow items) on the global-scratch workers
-      if (setter_cta)
-        TRACED(KID_SYNC_SLOW, leo_launch(k_sync_setter_cta, SM, kSWWarps * 32, setter_cta_smem(B), st, k, sa, bev, slow3s,
-                                         &ctr[11]));
+      // warp per item; the CFG image staged in shared memory when it fits,
+      // else read from L2 (big NVIDIA / Intel kernels)
+      if (setter_cta && setter_staged)
+        TRACED(KID_SYNC_SLOW, leo_launch(k_sync_setter_cta<true>, SM, kSWWarps * 32, setter_cta_smem(B), st, k, sa, bev,
+                                         slow3s, &ctr[11]));
+      else if (setter_cta)
+        TRACED(KID_SYNC_SLOW, leo_launch(k_sync_setter_cta<false>, SM * 4, kSWWarps * 32, 16 + setter_warp_tables_smem(), st,
+                                         k, sa, bev, slow3s, &ctr[11]));
       else
         TRACED(KID_SYNC_SLOW, leo_launch(k_sync_setter_smem, SM, 32, kDHBytes, st, k, sa, slow3s, &ctr[11]));
       SyncArgs sb = sa;
@@ -656,7 +665,8 @@ static int bin_impl(const LeoSamples* s, int32_t n_instr, int32_t* lat, int32_t*
     TRACED(KID_BIN_HIST, leo_launch(k_bin_hist, G, 512, nb * 4, st, S, s->pc, n_instr, nb, R, M, status));
     TRACED(KID_BIN_PLAN, leo_launch(k_bin_colscan, std::min(nb, num_sms() * 4), 256, 0, st, nb, G, M, btot));
     TRACED(KID_BIN_PLAN, leo_launch(k_bin_plan, 1, 1024, 0, st, nb, slice, btot, boff, soff));
-    TRACED(KID_BIN_SCATTER, leo_launch(k_bin_scatter, G, 512, nb * 4, st, S, s->pc, s->cat, s->cat_to_cs, n_instr, nb, R, M, boff, keys));
+    TRACED(KID_BIN_SCATTER, leo_launch(k_bin_scatter, G, 512, (size_t)nb * 12 + (size_t)kBinSub * 4, st, S, s->pc, s->cat,
+                                       s->cat_to_cs, n_instr, nb, R, M, boff, keys));
     TRACED(KID_BIN, leo_launch(k_bin_count, num_sms() * 3, 512, smem, st, n_instr, nb, R, slice, boff, soff, keys, cls_cnt));
   } else if (S > 0) {
     TRACED(KID_BIN, leo_launch(k_bin_samples, grid_for(S / 4 + 1, 256, num_sms() * 8), 256, 0, st, 

@@ -1016,11 +1016,18 @@ __global__ void k_sync_setter_smem(KView k, SyncArgs a, int32_t* slow_out, int32
 // to the global-scratch Dijkstra tier.
 constexpr int kSWSlots = 1024, kSWFront = 512, kSWWarps = 4;
 
+__host__ __device__ inline size_t setter_warp_tables_smem() {
+  return (size_t)kSWWarps * (carve_bytes(kSWSlots, 4) * 3 + carve_bytes(2 * kSWFront, 4) + 16);
+}
 __host__ __device__ inline size_t setter_cta_smem(int B) {
   return 16 + carve_bytes(B, 4) * 3 + carve_bytes((size_t)B + 1, 4) + carve_bytes(2 * (size_t)B + 4, 4)
-         + (size_t)kSWWarps * (carve_bytes(kSWSlots, 4) * 3 + carve_bytes(2 * kSWFront, 4) + 16);
+         + setter_warp_tables_smem();
 }
 
+// STAGE = false (the CFG image does not fit): the same searches read the
+// block tables from global memory (L2-resident), only the per-warp tables
+// live in shared memory.
+template <bool STAGE>
 __global__ void __launch_bounds__(kSWWarps * 32) k_sync_setter_cta(KView k, SyncArgs a, const uint32_t* __restrict__ setmask_g,
                                                                  int32_t* slow_out, int32_t* slow_out_count) {
   pdl_wait();
@@ -1028,11 +1035,18 @@ __global__ void __launch_bounds__(kSWWarps * 32) k_sync_setter_cta(KView k, Sync
   const int B = k.B, lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
   SmemCarve cv{sm_raw};
   uint64_t* bar = cv.take<uint64_t>(2);
-  int32_t* bf = cv.take<int32_t>(B);
-  int32_t* bl = cv.take<int32_t>(B);
-  uint32_t* smask = cv.take<uint32_t>(B);
-  int32_t* pptr = cv.take<int32_t>(B + 1);
-  int32_t* pred = cv.take<int32_t>(2 * (size_t)B + 4);
+  const int32_t* bf = k.blk_first;
+  const int32_t* bl = k.blk_last;
+  const uint32_t* smask = setmask_g;
+  const int32_t* pptr = k.pred_ptr;
+  const int32_t* pred = k.pred;
+  int32_t *sbf = nullptr, *sbl = nullptr, *spptr = nullptr, *spred = nullptr;
+  uint32_t* ssmask = nullptr;
+  if (STAGE) {
+    sbf = cv.take<int32_t>(B); sbl = cv.take<int32_t>(B); ssmask = cv.take<uint32_t>(B);
+    spptr = cv.take<int32_t>(B + 1); spred = cv.take<int32_t>(2 * (size_t)B + 4);
+    bf = sbf; bl = sbl; smask = ssmask; pptr = spptr; pred = spred;
+  }
   unsigned char* wbase = cv.p;
   cv.p = wbase + (size_t)wid * (carve_bytes(kSWSlots, 4) * 3 + carve_bytes(2 * kSWFront, 4) + 16);
   int32_t* key = cv.take<int32_t>(kSWSlots);
@@ -1042,16 +1056,18 @@ __global__ void __launch_bounds__(kSWWarps * 32) k_sync_setter_cta(KView k, Sync
   int32_t* wctl = cv.take<int32_t>(4);        // [0] next frontier size, [1] overflow
   const int n_items = (int)min((int64_t)*a.slow_count, a.slow_cap);
   if ((int)blockIdx.x * kSWWarps >= n_items) return;
-  StageBar sb;
-  sb.init(bar);
-  sb.begin();
-  const int P = k.pred_ptr[B];
-  sb.copy(bf, k.blk_first, (size_t)B * 4);
-  sb.copy(bl, k.blk_last, (size_t)B * 4);
-  sb.copy(smask, setmask_g, (size_t)B * 4);
-  sb.copy(pptr, k.pred_ptr, (size_t)(B + 1) * 4);
-  sb.copy(pred, k.pred, (size_t)P * 4);
-  sb.commit_and_wait();
+  if (STAGE) {
+    StageBar sb;
+    sb.init(bar);
+    sb.begin();
+    const int P = k.pred_ptr[B];
+    sb.copy(sbf, k.blk_first, (size_t)B * 4);
+    sb.copy(sbl, k.blk_last, (size_t)B * 4);
+    sb.copy(ssmask, setmask_g, (size_t)B * 4);
+    sb.copy(spptr, k.pred_ptr, (size_t)(B + 1) * 4);
+    sb.copy(spred, k.pred, (size_t)P * 4);
+    sb.commit_and_wait();
+  }
 
   auto find = [&](int p) -> int {
     uint32_t h = ((uint32_t)p * 2654435761u) >> 22;             // 10 bits
@@ -1140,6 +1156,8 @@ __global__ void __launch_bounds__(kSWWarps * 32) k_sync_setter_cta(KView k, Sync
   }
 }
 
+template __global__ void k_sync_setter_cta<true>(KView, SyncArgs, const uint32_t*, int32_t*, int32_t*);
+template __global__ void k_sync_setter_cta<false>(KView, SyncArgs, const uint32_t*, int32_t*, int32_t*);
 template __global__ void k_sync<false>(KView, SyncArgs, char*, int);
 template __global__ void k_sync<true>(KView, SyncArgs, char*, int);
 

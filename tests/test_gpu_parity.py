@@ -83,6 +83,8 @@ def test_device_matches_oracle_synthetic(tag, scale, cuda):
     ("c2", {"LEO_SYNC_FORK_AT": "0", "LEO_RU_PARTS": "3", "LEO_WC_CTAS": "148", "LEO_PRUNE_THREADS": "128"}),
     ("c2", {"LEO_WC_STEPS": "32", "LEO_NO_PRIO": "1"}),
     ("c3", {"LEO_SYNC_FORK_AT": "2", "LEO_RU_PARTS": "1", "LEO_PRUNE_THREADS": "128"}),
+    ("c3", {"LEO_SETTER_GLOBAL": "1"}),
+    ("c5", {"LEO_SETTER_GLOBAL": "1"}),
 ])
 def test_device_schedule_knobs_exact(tag, knobs, cuda, monkeypatch):
     """The scheduling knobs (fork points, CTAs per unit, waitcnt tier size
@@ -92,7 +94,7 @@ def test_device_schedule_knobs_exact(tag, knobs, cuda, monkeypatch):
     from paper_2604_20032_b200 import abi, device, synth
     for k, v in knobs.items():
         monkeypatch.setenv(k, v)
-    wl = synth.config_workload(tag, scale=0.5)
+    wl = synth.config_workload(tag, scale=0.05 if tag == "c5" else 0.5)
     ks = wl.kernel
     r = device.analyze_soa(ks, wl.profile, abi.make_config(dialect=ks.dialect),
                            samples=(wl.pc, wl.cat, wl.lut), device=cuda)
