@@ -87,7 +87,25 @@ __global__ void __launch_bounds__(512) k_bin_hist(int64_t S, const int32_t* __re
   if (s0 < s1) {
     const int64_t v0 = s0 / 4, v1 = s1 / 4;     // s0 is a multiple of 4
     const int4* pc4 = reinterpret_cast<const int4*>(pc);
-    for (int64_t v = v0 + threadIdx.x; v < v1; v += blockDim.x) {
+    // four 16-byte loads in flight per thread
+    const int64_t step = (int64_t)blockDim.x;
+    int64_t v = v0 + threadIdx.x;
+    for (; v + 3 * step < v1; v += 4 * step) {
+      int4 q[4];
+#pragma unroll
+      for (int u = 0; u < 4; u++) q[u] = pc4[v + u * step];
+#pragma unroll
+      for (int u = 0; u < 4; u++) {
+        const int ps[4] = {q[u].x, q[u].y, q[u].z, q[u].w};
+#pragma unroll
+        for (int t = 0; t < 4; t++) {
+          const int j = ps[t];
+          if (j < 0 || j >= N) { atomicOr(status, (uint32_t)LEO_ST_BAD_INPUT); continue; }
+          atomicAdd(&h[j / R], 1);
+        }
+      }
+    }
+    for (; v < v1; v += step) {
       const int4 p = pc4[v];
       const int ps[4] = {p.x, p.y, p.z, p.w};
 #pragma unroll
