@@ -369,8 +369,12 @@ int build_graph_impl(const LeoKernel* kk, const LeoCaps* caps, LeoEdges* out, Le
   // grid-wide count and two single-pass scans are faster)
   TRACED(KID_UNIT_COUNTS, leo_launch(k_unit_counts, std::max(grid_for(N, T), grid_for(B, T)), T, 0, st, k, ucnt, dcnt,
                                      B > 0 ? brec : nullptr, rhead));
-  TRACED(KID_SCAN, scan_exclusive(ucnt, use_ptr, nullptr, N, scan_tmp, nullptr, st));
-  TRACED(KID_SCAN, scan_exclusive(dcnt, def_ptr, nullptr, N, scan_tmp, nullptr, st));
+  if (N <= kScanSingleMax) {        // both unit prefix sums in one launch (one CTA each)
+    TRACED(KID_SCAN, leo_launch(scan_single_cta_pair, 2, 1024, 0, st, ucnt, use_ptr, dcnt, def_ptr, N));
+  } else {
+    TRACED(KID_SCAN, scan_exclusive(ucnt, use_ptr, nullptr, N, scan_tmp, nullptr, st));
+    TRACED(KID_SCAN, scan_exclusive(dcnt, def_ptr, nullptr, N, scan_tmp, nullptr, st));
+  }
   if (fork_at == 1) enqueue_sync();
 
   // tier 0 (shared-memory reach) reads the query columns, not the list

@@ -109,12 +109,8 @@ __global__ void scan_tile_apply(const int32_t* __restrict__ in, const int32_t* n
 // (independent 16-byte loads), one block scan of the chunk sums, pass 2
 // writes the running prefix.  Two reads of the input (L2-resident), one
 // block-wide barrier phase instead of one per 8K-element tile.
-__global__ void __launch_bounds__(1024) scan_single_cta(const int32_t* __restrict__ in, const int32_t* n_dev,
-                                                        int64_t n_cap, int32_t* __restrict__ out,
-                                                        int32_t* total_out) {
-  pdl_wait();
+LEO_DEV void scan_one_cta(const int32_t* __restrict__ in, int n, int32_t* __restrict__ out, int32_t* total_out) {
   __shared__ int sw[33];
-  const int n = (int)(n_dev ? (int64_t)*n_dev : n_cap);
   const int per = ((n + blockDim.x - 1) / blockDim.x + 3) & ~3;   // multiple of 4
   const int lo = min(n, (int)threadIdx.x * per), hi = min(n, lo + per);
   const bool vec = ((((uintptr_t)in) & 15) == 0);
@@ -144,6 +140,22 @@ __global__ void __launch_bounds__(1024) scan_single_cta(const int32_t* __restric
     for (int x = lo; x < hi; x++) { const int v = in[x]; out[x] = run; run += v; }
   }
   if (threadIdx.x == 0) { out[n] = tot; if (total_out) *total_out = tot; }
+}
+
+__global__ void __launch_bounds__(1024) scan_single_cta(const int32_t* __restrict__ in, const int32_t* n_dev,
+                                                        int64_t n_cap, int32_t* __restrict__ out,
+                                                        int32_t* total_out) {
+  pdl_wait();
+  scan_one_cta(in, (int)(n_dev ? (int64_t)*n_dev : n_cap), out, total_out);
+}
+
+// two independent scans of n elements in one launch (CTA 0: a, CTA 1: b)
+__global__ void __launch_bounds__(1024) scan_single_cta_pair(const int32_t* __restrict__ a_in, int32_t* __restrict__ a_out,
+                                                             const int32_t* __restrict__ b_in, int32_t* __restrict__ b_out,
+                                                             int n) {
+  pdl_wait();
+  if (blockIdx.x == 0) scan_one_cta(a_in, n, a_out, nullptr);
+  else scan_one_cta(b_in, n, b_out, nullptr);
 }
 
 // exclusive scan of in[0..n) into out[0..n] (out[n] = total); n from n_dev if
