@@ -443,8 +443,9 @@ int build_graph_impl(const LeoKernel* kk, const LeoCaps* caps, LeoEdges* out, Le
   TRACED(KID_LINK_EMIT, leo_launch(k_link_emit, grid_for(N, T), T, 0, st, k, cand_off, cand, uniq, eoff, *out, status));
 
   if (fork) link_streams(s_sync, st, sp.e[1]);   // join
-  TRACED(KID_SYNC_EMIT, leo_launch(k_sync_emit, grid_for(N, T), T, 0, st, N, kind, ssorted, poff, puniq, puoff, &ctr[5], *out, status));
-  TRACED(KID_EDGE_TOTALS, leo_launch(k_edge_totals, 1, 1, 0, st, &ctr[5], &ctr[6], *out, status));
+  // (also writes the edge totals)
+  TRACED(KID_SYNC_EMIT, leo_launch(k_sync_emit, grid_for(N, T), T, 0, st, N, kind, ssorted, poff, puniq, puoff, &ctr[5],
+                                   &ctr[6], *out, status));
   if (caps && (caps->debug_flags & LEO_DBG_PHASES)) k_copy_counts<<<1, 32, 0, st>>>(ctr, 16);
   ar.release();
   LEO_CUDA_CHECK(cudaGetLastError());

@@ -1182,9 +1182,15 @@ __global__ void k_key_scatter(const uint64_t* __restrict__ keys, const int32_t* 
 __global__ void k_sync_emit(int N, int kind, const uint64_t* __restrict__ sorted,
                             const int32_t* __restrict__ off, const int32_t* __restrict__ uniq,
                             const int32_t* __restrict__ uoff, const int32_t* n_regular,
-                            LeoEdges out, uint32_t* status) {
+                            const int32_t* n_sync, LeoEdges out, uint32_t* status) {
   pdl_wait();
   const int base = *n_regular;
+  if (blockIdx.x == 0 && threadIdx.x == 0) {     // edge totals (was k_edge_totals)
+    const int t = base + *n_sync;
+    if (t > out.capacity) atomicOr(status, (uint32_t)LEO_ST_EDGE_OVERFLOW);
+    *out.n_regular = min(base, out.capacity);
+    *out.count = min(t, out.capacity);
+  }
   for (int p = blockIdx.x * blockDim.x + threadIdx.x; p < N; p += gridDim.x * blockDim.x) {
     int n = uniq[p], o = base + uoff[p];
     if (o + n > out.capacity) { if (n) atomicOr(status, (uint32_t)LEO_ST_EDGE_OVERFLOW); continue; }
@@ -1196,14 +1202,8 @@ __global__ void k_sync_emit(int N, int kind, const uint64_t* __restrict__ sorted
     }
   }
 }
-// counts are clamped to the capacity so downstream kernels never read past the
-// buffers; an overflow is signalled in the status word and the host re-runs.
-__global__ void k_edge_totals(const int32_t* n_regular, const int32_t* n_sync, LeoEdges out, uint32_t* status) {
-  pdl_wait();
-  int r = *n_regular, t = *n_regular + *n_sync;
-  if (t > out.capacity) atomicOr(status, (uint32_t)LEO_ST_EDGE_OVERFLOW);
-  *out.n_regular = min(r, out.capacity);
-  *out.count = min(t, out.capacity);
-}
+// (edge totals are clamped to the capacity so downstream kernels never read
+// past the buffers; an overflow is signalled in the status word and the host
+// re-runs)
 
 }  // namespace leo
