@@ -514,6 +514,9 @@ struct BlameArgs {
   int32_t* slow_count;
   int64_t slow_cap;
   uint32_t* status;
+  double* zero_lb;          // pass 1 also zeroes the line vectors (null: accumulate / no lines)
+  double* zero_ls;
+  int32_t n_lines;
 };
 
 LEO_DEV double issue_count(const PView& p, int i) {   // profile.py:321-329
@@ -778,6 +781,15 @@ template <int PASS>
 __global__ void k_blame(KView k, BlameArgs a) {
   pdl_wait();
   const int lane = threadIdx.x & 31;
+  if (PASS == 1) {
+    // the entry count (was k_blame_count) and the line vectors k_lines adds into
+    if (blockIdx.x == 0 && threadIdx.x == 0) *a.out.count = a.eoff[k.N];
+    if (a.zero_lb)
+      for (int x = blockIdx.x * blockDim.x + threadIdx.x; x < a.n_lines; x += gridDim.x * blockDim.x) {
+        a.zero_lb[x] = 0.0;
+        a.zero_ls[x] = 0.0;
+      }
+  }
   // whole warps iterate together (the warp path needs every lane)
   for (int j0 = blockIdx.x * blockDim.x + (threadIdx.x & ~31); j0 < k.N; j0 += gridDim.x * blockDim.x) {
     const int j = j0 + lane;
@@ -883,8 +895,6 @@ __global__ void k_selfblame_slow(KView k, BlameArgs a, const int32_t* list, cons
   }
 }
 
-__global__ void k_blame_count(const int32_t* eoff, int N, LeoBlame out) {
-  pdl_wait(); *out.count = eoff[N]; }
 
 // ---- per-source-line rollup -----------------------------------------------------
 __global__ void k_lines(KView k, PView p, Range own, const int32_t* __restrict__ pprod, LeoBlame b,

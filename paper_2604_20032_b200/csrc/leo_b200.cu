@@ -611,7 +611,11 @@ int blame_impl(const LeoKernel* kk, const LeoProfile* pp, const LeoEdges* pruned
   Incoming binc = own_addr ? addr_impl(k, base, ab, tr, st) : *binc_pre;
   const uint8_t* mp_ok = (dbg & LEO_DBG_SELF_SLOW) ? nullptr : (own_addr ? ab.ok : mp_ok_pre);
   BlameArgs a{dbg, mp_ok, own, p, pruned->prod, pruned->meta, paths->dist, inc, binc.rbeg, binc.rend, base->prod, base->meta,
-              ecount, self_sub, jtotal, jnsum, eoff, *out, slow_list, &ctr[0], cap_slow, status};
+              ecount, self_sub, jtotal, jnsum, eoff, *out, slow_list, &ctr[0], cap_slow, status, nullptr, nullptr, 0};
+  const bool lines_on = line_id && line_blame && line_stall && n_lines > 0;
+  if (lines_on && !(caps && (caps->options & LEO_OPT_ACCUMULATE_LINES))) {
+    a.zero_lb = line_blame; a.zero_ls = line_stall; a.n_lines = n_lines;
+  }
   TRACED(KID_BLAME_COUNT, leo_launch(k_blame<0>, grid_for(N, 128), 128, 0, st, k, a));
   if (!mp_ok) {
     TRACED(KID_SELFBLAME_WARP, leo_launch(k_selfblame_warp, num_sms(), 128, 4 * kSBWarpInts * 4, st, k, a, slow2, &ctr[1]));
@@ -619,12 +623,8 @@ int blame_impl(const LeoKernel* kk, const LeoProfile* pp, const LeoEdges* pruned
   }
   TRACED(KID_SCAN, scan_exclusive(ecount, eoff, nullptr, N, scan_tmp, nullptr, st));
   TRACED(KID_BLAME_FILL, leo_launch(k_blame<1>, grid_for(N, 128), 128, 0, st, k, a));
-  TRACED(KID_BLAME_TOTAL, leo_launch(k_blame_count, 1, 1, 0, st, eoff, N, *out));
-  if (line_id && line_blame && line_stall && n_lines > 0) {
-    if (!(caps && (caps->options & LEO_OPT_ACCUMULATE_LINES))) {
-      cudaMemsetAsync(line_blame, 0, (size_t)n_lines * 8, st);
-      cudaMemsetAsync(line_stall, 0, (size_t)n_lines * 8, st);
-    }
+  // (k_blame<1> also wrote the entry count and zeroed the line vectors)
+  if (lines_on) {
     TRACED(KID_LINES, leo_launch(k_lines, grid_for(std::max<int64_t>(out->capacity, N), 256), 256, 0, st, k, p, own, pruned->prod, *out,
                                                                                line_id, line_blame, line_stall));
   }
