@@ -456,7 +456,7 @@ int build_graph_impl(const LeoKernel* kk, const LeoCaps* caps, LeoEdges* out, Le
 // run_pruning
 int prune_impl(const LeoKernel* kk, const LeoProfile* pp, const LeoConfig* cfg, const LeoEdges* in,
                LeoEdges* out, LeoPaths* paths, LeoDiags* diags, const LeoCaps* caps, uint32_t* status,
-               cudaStream_t st) {
+               cudaStream_t st, ZeroSet zero = ZeroSet{{nullptr, nullptr, nullptr, nullptr}, 0}) {
   LeoTrace* tr = caps ? caps->trace : nullptr;
   KView k = make_kview(kk);
   PView p = make_pview(pp);
@@ -496,7 +496,8 @@ int prune_impl(const LeoKernel* kk, const LeoProfile* pp, const LeoConfig* cfg, 
   }
   TRACED(KID_PRUNE_SLOW, leo_launch(k_prune_slow, 1, PW, 0, st, k, p, a, slow_scr, PW));
   TRACED(KID_SCAN, scan_exclusive(keep, pos, in->count, cap_in, scan_tmp, nullptr, st));
-  TRACED(KID_COMPACT, leo_launch(k_compact, grid_for(cap_in, 256), 256, 0, st, a, pos, in->n_regular, *out, status));
+  TRACED(KID_COMPACT, leo_launch(k_compact, grid_for(std::max<int64_t>(cap_in, zero.n), 256), 256, 0, st, a, pos,
+                                 in->n_regular, *out, status, zero));
   ar.release();
   LEO_CUDA_CHECK(cudaGetLastError());
   return 0;
@@ -513,12 +514,15 @@ void want_incoming(Arena& ar, IncomingBufs& b, int N, int64_t cap) {
   ar.want(&b.scur, N); ar.want(&b.sidx, cap); ar.want(&b.tmp, scan_scratch_ints(std::max(N, 1)) + 64);
   ar.want(&b.uniq, N);
 }
-Incoming build_incoming(IncomingBufs& b, int N, const LeoEdges* e, bool with_sync, LeoTrace* tr, cudaStream_t st) {
-  const size_t nb = (size_t)std::max(N, 1) * 4;
-  cudaMemsetAsync(b.rbeg, 0, nb, st);
-  cudaMemsetAsync(b.rend, 0, nb, st);
-  cudaMemsetAsync(b.scnt, 0, nb, st);
-  cudaMemsetAsync(b.scur, 0, nb, st);
+Incoming build_incoming(IncomingBufs& b, int N, const LeoEdges* e, bool with_sync, LeoTrace* tr, cudaStream_t st,
+                        bool prezeroed = false) {
+  if (!prezeroed) {                // (else the producing kernel cleared rbeg / rend / scnt / scur)
+    const size_t nb = (size_t)std::max(N, 1) * 4;
+    cudaMemsetAsync(b.rbeg, 0, nb, st);
+    cudaMemsetAsync(b.rend, 0, nb, st);
+    cudaMemsetAsync(b.scnt, 0, nb, st);
+    cudaMemsetAsync(b.scur, 0, nb, st);
+  }
   TRACED(KID_SEG_BOUNDS, leo_launch(k_seg_bounds, grid_for(e->capacity, 256), 256, 0, st, e->cons, e->n_regular, b.rbeg, b.rend));
   if (with_sync) {
     TRACED(KID_SYNC_HIST, leo_launch(k_sync_hist, grid_for(e->capacity, 256), 256, 0, st, e->cons, e->n_regular, e->count, b.scnt));
@@ -880,18 +884,22 @@ int leo_analyze(const LeoKernel* k, const LeoProfile* p, const LeoSamples* sampl
     return 0;
   }
   if (samples && fork) link_streams(sp.s[1], st, sp.e[3]);
-  r = prune_impl(k, p, cfg, base, pruned, paths, diags, caps, status, st);
-  if (r) return r;
-  if (stop == 2) {
-    if (fork) link_streams(s_addr, st, sp.e[7]);
-    ar_addr.release();
-    return 0;
-  }
+  // the pruned graph's incoming-CSR buffers exist before pruning so its
+  // compaction kernel can clear them
   Arena ar{st};
   IncomingBufs ib;
   want_incoming(ar, ib, k->n_instr, pruned->capacity);
   LEO_CUDA_CHECK(ar.commit());
-  Incoming inc = build_incoming(ib, k->n_instr, pruned, true, tr, st);
+  r = prune_impl(k, p, cfg, base, pruned, paths, diags, caps, status, st,
+                 ZeroSet{{ib.rbeg, ib.rend, ib.scnt, ib.scur}, k->n_instr});
+  if (r) { ar.release(); return r; }
+  if (stop == 2) {
+    if (fork) link_streams(s_addr, st, sp.e[7]);
+    ar.release();
+    ar_addr.release();
+    return 0;
+  }
+  Incoming inc = build_incoming(ib, k->n_instr, pruned, true, tr, st, true);
   if (stop == 3) {
     if (fork) link_streams(s_addr, st, sp.e[7]);
     ar.release();

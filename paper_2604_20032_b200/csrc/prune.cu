@@ -391,9 +391,17 @@ __global__ void k_prune_slow(KView k, PView p, PruneArgs a, char* scratch, int n
   }
 }
 
+// `zero` (optional): four int arrays of zn elements the next stage expects
+// zeroed (the pruned graph's incoming-CSR bounds and counters), cleared here
+// instead of by four memset nodes
+struct ZeroSet { int32_t* p[4]; int n; };
+
 __global__ void k_compact(PruneArgs a, const int32_t* __restrict__ pos, const int32_t* n_reg_in,
-                          LeoEdges out, uint32_t* status) {
+                          LeoEdges out, uint32_t* status, ZeroSet zero) {
   pdl_wait();
+  for (int x = blockIdx.x * blockDim.x + threadIdx.x; x < zero.n; x += gridDim.x * blockDim.x) {
+    zero.p[0][x] = 0; zero.p[1][x] = 0; zero.p[2][x] = 0; zero.p[3][x] = 0;
+  }
   const int n = *a.n_in;
   for (int e = blockIdx.x * blockDim.x + threadIdx.x; e < n; e += gridDim.x * blockDim.x) {
     if (!a.keep[e]) continue;
