@@ -608,7 +608,9 @@ int blame_impl(const LeoKernel* kk, const LeoProfile* pp, const LeoEdges* pruned
   ar.want(&slow_scr, (int64_t)BW * 2 * (N + 1)); ar.want(&jtotal, N); ar.want(&jnsum, N);
   LEO_CUDA_CHECK(ar.commit());
   cudaMemsetAsync(ctr, 0, 16, st);
-  cudaMemsetAsync(slow_scr, 0, (size_t)BW * 2 * (N + 1) * sizeof(int32_t), st);   // stamps
+  // the slow self-blame worker's stamps matter only when it runs (no
+  // precomputed addressing verdict: LEO_DBG_SELF_SLOW)
+  if (dbg & LEO_DBG_SELF_SLOW) cudaMemsetAsync(slow_scr, 0, (size_t)BW * 2 * (N + 1) * sizeof(int32_t), st);
   // the indirect-addressing test comes precomputed from a side branch
   // (leo_analyze) or is computed here; LEO_DBG_SELF_SLOW keeps the per-
   // candidate BFS tiers instead (cross-checked against the same goldens)
