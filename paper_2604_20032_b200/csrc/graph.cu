@@ -762,6 +762,10 @@ __global__ void k_reach_slow(KView k, ReachArgs a, const int32_t* list, const in
   int32_t* stamp = scratch + (size_t)w * 3 * (B + 1);
   int32_t* stk = stamp + (B + 1);
   int32_t* res = stk + (B + 1);
+  // a worker with items clears its own stamps (no memset node ahead of the
+  // build for a tier that usually has nothing to do)
+  if (w < ns)
+    for (int x = 0; x <= B; x++) stamp[x] = 0;
   for (int t = w; t < ns; t += nworkers) {
     int e = list[t];
     int nres = 0;

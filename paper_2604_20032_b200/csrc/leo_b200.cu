@@ -272,7 +272,6 @@ int build_graph_impl(const LeoKernel* kk, const LeoCaps* caps, LeoEdges* out, Le
   LEO_CUDA_CHECK(ar.commit());
   // counters: 0 q_count, 1 qres_count, 2 reach slow, 3 sync keys, 4 sync slow, 5 n_regular, 6 n_sync
   cudaMemsetAsync(ctr, 0, 16 * sizeof(int32_t), st);
-  cudaMemsetAsync(reach_scr, 0, (size_t)RW * 3 * (B + 1) * sizeof(int32_t), st);
   const int T = 256;
   // fork: vendor sync tracing runs on a side stream, concurrently with the
   // register dataflow chain below
