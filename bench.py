@@ -14,11 +14,15 @@ all ranks (each rank analyses its own kernel of the configured shape:
 weak scaling by kernel).  Device time from CUDA events; L2 is
 flushed (256 MiB write) between timed steps; max over ranks.
 
-The default workload is BASELINE.json configs[1] (C2): a synthetic AMD GCN
-kernel, 10,000 instructions with s_waitcnt vmcnt/lgkmcnt edges, 1,000,000 PC
-samples.  `--impl reference` times the CPU restatement (oracle/, the port of
-the reference's Python path; the reference itself is pure Python and does not
-travel to the GPU box) on the host cores on the same workload.
+The default workload is BASELINE.json configs[4] (C5), the largest
+configuration that fits one GPU: one synthetic NVIDIA kernel of 1,000,000
+instructions (branchy CFG, barrier masks, stall cycles) and 100,000,000 raw PC
+samples.  C2 / C3 / C4 are selectable with --config.  `--impl reference`
+times the CPU restatement (oracle/, the port of the reference's Python path;
+the reference itself is pure Python and does not travel to the GPU box) on the
+host cores on the same workload: one kernel per step on one core (the
+reference is single-threaded per kernel), C4 kernels spread over
+every host core.
 """
 
 from __future__ import annotations
@@ -52,7 +56,7 @@ def parse():
     ap.add_argument("--steps", type=int, default=50)
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--config", default="c2", choices=["c2", "c3", "c4", "c5"])
+    ap.add_argument("--config", default="c5", choices=["c2", "c3", "c4", "c5"])
     ap.add_argument("--c4-kernels", type=int, default=2000)
     ap.add_argument("--scale", type=float, default=1.0)
     ap.add_argument("--trace", action="store_true", help="print per-kernel device time")
@@ -164,26 +168,81 @@ def cpu_port_time(wl, seconds: float, min_iters: int = 1):
     return times, stages
 
 
+def host_cpu() -> str:
+    """Host CPU model and logical core count (cpu_baseline.host)."""
+    model = "unknown"
+    try:
+        for ln in open("/proc/cpuinfo"):
+            if ln.startswith("model name"):
+                model = ln.split(":", 1)[1].strip()
+                break
+    except OSError:
+        pass
+    return f"{model} x{os.cpu_count()} logical cores"
+
+
+def workload_config(args) -> dict:
+    """The `config` object both arms print (identical keys and values)."""
+    from paper_2604_20032_b200 import synth
+    if args.config == "c4":
+        n_instr, n_samples = synth.C4_INSTR, synth.C4_SAMPLES
+        extra = {"kernels": args.c4_kernels}
+    else:
+        c = synth.CONFIGS[args.config]
+        n_instr, n_samples = c["n_instr"], c["n_samples"]
+        extra = {"kernels": 1}
+    sc = args.scale
+    return {"workload": WORKLOADS[args.config], "tag": args.config, "scale": sc,
+            "n_instr_per_kernel": max(64, int(n_instr * sc)),
+            "n_samples_per_kernel": max(1, int(n_samples * sc)), **extra}
+
+
+def pool_time(wls, cores: int):
+    """Oracle port over a list of kernels on `cores` host threads (ctypes
+    releases the GIL inside the C oracle): wall seconds."""
+    from concurrent.futures import ThreadPoolExecutor
+    t0 = time.perf_counter()
+    with ThreadPoolExecutor(cores) as ex:
+        list(ex.map(lambda w: cpu_port_time(w, 0.0), wls))
+    return time.perf_counter() - t0
+
+
 def run_reference(args, ws, rank):
+    """The reference's CPU path (oracle port) on the host cores, rank 0 only."""
     if rank != 0:
         return 0
     from paper_2604_20032_b200 import synth
-    wl = synth.config_workload(args.config, scale=args.scale)
+    cores = os.cpu_count() or 1
+    if args.config == "c4":
+        # each step: a bounded sample of the 2,000-kernel batch, kernels spread
+        # over every host core (the reference's permitted per-kernel concurrency)
+        lines = synth.LineTable(4096, seed=999)
+        n = min(args.c4_kernels, 2 * cores)
+        wls = [synth.c4_kernel(k, lines, scale=args.scale) for k in range(n)]
+        run = lambda: pool_time(wls, cores)  # noqa: E731
+        S = sum(w.n_samples for w in wls)
+        used = cores
+        sample = (f"C4 kernels 0..{n - 1} of {args.c4_kernels} per step on {cores} threads "
+                  f"(oracle/leo_oracle.c per kernel: binning + build + prune + slice + blame + lines)")
+    else:
+        wl = synth.config_workload(args.config, scale=args.scale)
+        run = lambda: float(np.sum(cpu_port_time(wl, 0.0)[0]))  # noqa: E731
+        S = wl.n_samples
+        used = 1
+        sample = (f"full {args.config} workload per step on one core (oracle/leo_oracle.c: "
+                  f"binning + build + prune + slice + blame + lines; the reference analyses one "
+                  f"kernel single-threaded, SPEC.md:351)")
     for _ in range(max(args.warmup, 0)):
-        cpu_port_time(wl, 0.0)
-    times = []
-    for _ in range(args.steps):
-        t, _ = cpu_port_time(wl, 0.0)
-        times.extend(t)
+        run()
+    times = [run() for _ in range(args.steps)]
     T = float(np.sum(times))
-    value = wl.n_samples * len(times) / T
+    value = S * len(times) / T
     line = {"impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": ws,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * T / len(times),
             "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "int32/f64",
-            "data": "synthetic", "config": {"workload": WORKLOADS[args.config], "scale": args.scale},
-            "cpu_baseline": {"value": value, "unit": UNIT, "cores": 1, "kind": "port",
-                             "sample": f"full {args.config} workload per step (oracle/leo_oracle.c, "
-                                       f"binning + build + prune + slice + blame + lines)"},
+            "data": "synthetic", "config": workload_config(args),
+            "cpu_baseline": {"value": value, "unit": UNIT, "cores": used, "kind": "port",
+                             "sample": sample, "host": host_cpu()},
             "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
     return 0
@@ -447,14 +506,14 @@ def run_ours(args, ws, rank, local):
             "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": ws, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": T_max / args.steps, "higher_is_better": True,
             "scaling": "weak", "vs_baseline": None, "dtype": "int32/f64", "data": "synthetic",
-            "config": {"workload": WORKLOADS[args.config], "scale": args.scale,
-                       "per_rank": plan.mode, "kernels_per_rank": len(plan.items),
-                       "n_instr": ks.n_instr, "n_samples_per_step_all_ranks": S_total,
-                       "edges": int(c0[device.C_BASE]), "pruned_edges": int(c0[device.C_PR]),
-                       "blame_entries": int(c0[device.C_BLAME]),
-                       "l2": "flushed between timed steps (256 MiB write)",
-                       "launch": "CUDA graph replay of the whole pipeline" if use_graph else "eager",
-                       "parallelism": f"x{ws}" + (" + NCCL all-reduce of f64 line vectors" if ws > 1 else "")},
+            "config": workload_config(args),
+            "run": {"per_rank": plan.mode, "kernels_per_rank": len(plan.items),
+                    "n_instr": ks.n_instr, "n_samples_per_step_all_ranks": S_total,
+                    "edges": int(c0[device.C_BASE]), "pruned_edges": int(c0[device.C_PR]),
+                    "blame_entries": int(c0[device.C_BLAME]),
+                    "l2": "flushed between timed steps (256 MiB write)",
+                    "launch": "CUDA graph replay of the whole pipeline" if use_graph else "eager",
+                    "parallelism": f"x{ws}" + (" + NCCL all-reduce of f64 line vectors" if ws > 1 else "")},
             "roofline": {"bound": "hbm", "kernel": dominant, "achieved": achieved, "peak": peak,
                          "unit": "GB/s", "frac": (achieved / peak) if achieved else None,
                          "traffic": traffic, "alg_bytes_per_launch": alg,
@@ -490,6 +549,7 @@ def cpu_baseline(args, plan):
         times, _ = cpu_port_time(items[0], args.cpu_seconds)
         S = items[0].n_samples
         return {"value": S / float(np.mean(times)), "unit": UNIT, "cores": 1, "kind": "port",
+                "host": host_cpu(),
                 "sample": f"full {args.config} workload x{len(times)} (oracle/leo_oracle.c: binning "
                           f"+ build + prune + slice + blame + lines; {np.mean(times) * 1e3:.1f} ms each)"}
     cores = os.cpu_count() or 1
@@ -502,7 +562,7 @@ def cpu_baseline(args, plan):
             done += len(batch)
             S += sum(w.n_samples for w in batch)
     dt = time.perf_counter() - t0
-    return {"value": S / dt, "unit": UNIT, "cores": cores, "kind": "port",
+    return {"value": S / dt, "unit": UNIT, "cores": cores, "kind": "port", "host": host_cpu(),
             "sample": f"{done} of the rank's {len(items)} C4 kernels on {cores} threads "
                       f"(oracle/leo_oracle.c per kernel)"}
 
