@@ -42,8 +42,13 @@ class LineTable:
     def __len__(self):
         return self.n
 
+    def __iter__(self):
+        return (self[i] for i in range(self.n))
+
     def __getitem__(self, lid: int) -> str:
         lid = int(lid)
+        if lid < 0 or lid >= self.n:
+            raise IndexError(lid)
         if lid == self.n - 1:
             return "<unknown>"
         f = int(np.searchsorted(self.base, lid, side="right") - 1)
@@ -214,19 +219,24 @@ def make_kernel(dialect: str, n_instr: int, seed: int, name: str | None = None,
         sync_kind[sends] = E.SYNC_SWSB
         sync_a[sends] = (np.arange(sends.shape[0]) % 32).astype(np.uint32)
         sync_b[sends] = 0
-        # ~20 % of ALU ops wait.dst on a token set within the last 16 instructions
+        # ~20 % of ALU ops wait sbid.wait.dst, 5 % sbid.wait.src,
+        # on a token set within the last 16 instructions in layout order -- in
+        # the waiter's block or in an earlier one (cross-block setter searches
+        # over the nested loops).  The SoA keeps dst | src as one mask
+        # (depgraph.py:466-482 waits on their union).
         alu = np.isin(opclass, [OC["fp_arith"], OC["int_arith"], OC["conversion"]])
-        cand = np.flatnonzero(alu & (rng.random(n) < .25))
-        pos = np.searchsorted(sends, cand) - 1
-        ok = pos >= 0
-        cand, pos = cand[ok], pos[ok]
-        # (mostly) in the setter's own block: the nearest setter then wins alone
-        near = ((cand - sends[pos]) <= 16) & ((block_of[cand] == block_of[sends[pos]])
-                                              | (rng.random(cand.shape[0]) < 0.05))
-        cand, pos = cand[near], pos[near]
-        sync_kind[cand] = E.SYNC_SWSB
-        sync_a[cand] = E.NONE_U32
-        sync_b[cand] = (np.uint32(1) << sync_a[sends[pos]]).astype(np.uint32)
+        u = rng.random(n)
+        for lo, hi in ((0.0, 0.20), (0.20, 0.25)):          # dst, then src waits
+            cand = np.flatnonzero(alu & (u >= lo) & (u < hi))
+            back = rng.integers(1, 17, size=cand.shape[0])   # setter 1..16 instructions back
+            pos = np.searchsorted(sends, cand - back, side="right") - 1
+            ok = (pos >= 0)
+            cand, pos = cand[ok], pos[ok]
+            ok = (cand - sends[pos]) <= 16
+            cand, pos = cand[ok], pos[ok]
+            sync_kind[cand] = E.SYNC_SWSB                    # (sync_a stays None: no set)
+            sync_b[cand] = np.where(sync_b[cand] == E.NONE_U32, 0, sync_b[cand]) | \
+                (np.uint32(1) << sync_a[sends[pos]]).astype(np.uint32)
 
     # operand CSR: srcs, guard, dests
     cnt = n_src + (guard >= 0) + has_dest

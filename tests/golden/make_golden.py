@@ -47,12 +47,14 @@ from paper_2604_20032_b200 import soa, synth  # noqa: E402
 OUT = REPO / "tests" / "golden"
 
 
-def expected_for(att, cfg):
-    """Reference outputs for one attached kernel, as arrays."""
+def expected_for(att, cfg, ks=None, pf=None):
+    """Reference outputs for one attached kernel, as arrays (`ks` / `pf`: the
+    SoA the kernel was decoded from, when the caller has it)."""
     g = depgraph.build_graph(att)
     pr = analysis.run_pruning(g, cfg)
     bl = analysis.attribute_blame(pr, base_graph=g)
-    ks, pf = soa.encode_attached(att)
+    if ks is None:
+        ks, pf = soa.encode_attached(att)
     x = {}
 
     def edge_arrays(edges, prefix):
