@@ -23,12 +23,24 @@
  *                        (depgraph.py:102-108; semantics frozen in DESIGN.md)
  *   leo_analyze       <- fused build -> prune -> slice -> blame -> lines
  *                        (report.py:132-142 call sequence)
+ *   leo_reaching_definitions <- depgraph.reaching_definitions  depgraph.py:135-177
+ *   leo_liveness_filter      <- depgraph.liveness_filter       depgraph.py:274-293
+ *   leo_self_blame           <- analysis.self_blame            analysis.py:414-428
+ *   leo_coverage             <- analysis.single_dep_coverage   analysis.py:547-561
+ *   leo_trace_chain          <- analysis.trace_chain           analysis.py:499-538
+ *   leo_rank_hotspots        <- report.rank_hotspots           report.py:96-109
+ *   leo_line_rollup          <- per-source-line rollup of any blame list
+ *   leo_report               <- report.build_report assembly   report.py:132-199
  *
  * Conventions
  *  - Every pointer inside a struct is a DEVICE pointer owned by the caller.
  *  - Calls are stream-ordered and asynchronous; `stream` is a cudaStream_t
  *    passed as void*.  Scratch memory is taken from the stream-ordered
- *    allocator and released on the same stream.  No global mutable state.
+ *    allocator (or LeoCaps.workspace) and released on the same stream.  No
+ *    global analysis state: per-device caches (SM count, the >48 KiB shared-
+ *    memory function attributes) are set once per device, fork/join side
+ *    streams are kept per (host thread, device, caller stream), and the only
+ *    device globals are profiling counters written under LEO_DBG_PHASES.
  *  - Variable-size outputs use "capacity + device counter": the kernel writes
  *    the true count to the device counter even when it exceeds capacity; the
  *    host reads the counter after synchronising, and re-runs with larger
@@ -47,7 +59,7 @@
 extern "C" {
 #endif
 
-#define LEO_ABI_VERSION 1
+#define LEO_ABI_VERSION 2
 
 /* ---- enumerations (indices follow the reference enum definition order) --- */
 /* Dialect  isa.py:19-22 */
@@ -154,14 +166,20 @@ typedef struct LeoConfig {
   int32_t  consumer_hi;       /*   [lo, hi); hi <= 0 means all (single-GPU / replica)   */
 } LeoConfig;
 
-/* ---- edge list (DepEdge depgraph.py:77-91) -------------------------------- */
+/* ---- edge list (DepEdge depgraph.py:77-91) --------------------------------
+ * Library-made lists are canonical: raw/guard edges sorted by consumer first
+ * (n_regular of them), then sync edges.  A caller's list may be in ANY order
+ * (the reference's DependencyGraph holds any edge tuple: chained stages,
+ * hand-built graphs): pass n_regular = NULL; the library then keeps list order
+ * per consumer wherever the reference's `incoming` order matters.           */
 typedef struct LeoEdges {
   int32_t   capacity;
   int32_t*  prod;             /* [cap] */
   int32_t*  cons;             /* [cap] */
   uint32_t* meta;             /* [cap] LEO_META */
   int32_t*  count;            /* device scalar: total edges */
-  int32_t*  n_regular;        /* device scalar: raw/guard edges (they precede sync edges) */
+  int32_t*  n_regular;        /* device scalar: raw/guard edges (they precede sync edges),
+                                 or NULL: arbitrary order (inputs); not written (outputs) */
 } LeoEdges;
 
 /* ---- valid_paths of pruned edges (PathRecord depgraph.py:71-74) ---------- */
@@ -258,19 +276,27 @@ int leo_debug_tiers(int32_t* out);
 /* per-item clock64 cycles of the shared-memory waitcnt tier (LEO_DBG_PHASES) */
 int leo_debug_items(int64_t* out, int32_t n);
 
-/* stage 0: raw (pc, category) stream -> lat[N], cls_cnt[N*8] (zeroed here). */
+/* stage 0: raw (pc, category) stream -> lat[N], cls_cnt[N*8] (zeroed here).
+ * A sample whose pc is outside [0, n_instr) is dropped and sets
+ * LEO_ST_BAD_INPUT in *status (device word, caller-zeroed). */
 int leo_bin_samples(const LeoSamples* s, int32_t n_instr, int32_t* lat, int32_t* cls_cnt,
-                    void* stream);
+                    uint32_t* status, void* stream);
 
 /* build_graph: raw/guard edges sorted (consumer, producer, kind, class, index, span)
  * followed by the dialect's sync edges sorted (producer, consumer). */
 int leo_build_graph(const LeoKernel* k, const LeoCaps* caps, LeoEdges* out, LeoDiags* diags,
                     uint32_t* status, void* stream);
 
-/* run_pruning: stages 1->2->3->4 honouring cfg; `out` keeps input order. */
+/* run_pruning: stages 1->2->3->4 honouring cfg; `out` keeps input order.
+ * Any single stage (prune_opcode / prune_barrier / prune_latency /
+ * prune_execution, analysis.py:143-299) is the same call with one bit of
+ * cfg->stage_mask.  `in_paths` (may be NULL): the input edges' valid_paths
+ * (first / npaths per input edge, len / accum pool, count); a kept edge keeps
+ * them unless stage 3 finds valid paths for it (analysis.py:276); the input
+ * records are copied to the front of `paths`. */
 int leo_prune(const LeoKernel* k, const LeoProfile* p, const LeoConfig* cfg,
-              const LeoEdges* in, LeoEdges* out, LeoPaths* paths, LeoDiags* diags,
-              uint32_t* status, void* stream);
+              const LeoEdges* in, const LeoPaths* in_paths, LeoEdges* out, LeoPaths* paths,
+              LeoDiags* diags, uint32_t* status, void* stream);
 
 /* backward slice from every instruction with S_j > 0 over `pruned` incoming
  * adjacency: bitmap[(N+31)/32], level[N] (-1 outside the slice). */
@@ -278,11 +304,68 @@ int leo_slice(const LeoKernel* k, const LeoProfile* p, const LeoEdges* pruned,
               uint32_t* bitmap, int32_t* level, void* stream);
 
 /* attribute_blame(pruned, base_graph=base) + per-line rollup.
- * line_id[N] (may be NULL), line_blame[n_lines], line_stall[n_lines] zeroed here. */
+ * `paths` (may be NULL: no valid paths): the pruned edges' valid_paths, from
+ * which _edge_distance (analysis.py:371-376) is computed here.  `base` may be
+ * NULL (attribute_blame(graph) without base_graph: no indirect-addressing
+ * upgrade).  line_id[N] (may be NULL), line_blame[n_lines], line_stall[n_lines]
+ * zeroed here. */
 int leo_blame(const LeoKernel* k, const LeoProfile* p, const LeoEdges* pruned,
               const LeoPaths* paths, const LeoEdges* base, const int32_t* line_id,
               int32_t n_lines, LeoBlame* out, double* line_blame, double* line_stall,
               uint32_t* status, void* stream);
+
+/* self_blame(index, attached, base_graph) (analysis.py:414-428) for n given
+ * instructions: SelfBlame subcategory and S_j (any instruction, stalled or
+ * not).  base may be NULL (no indirect-addressing upgrade). */
+int leo_self_blame(const LeoKernel* k, const LeoProfile* p, const LeoEdges* base, int32_t n,
+                   const int32_t* index, uint8_t* sub, double* cycles, void* stream);
+
+/* single_dep_coverage(graph) (analysis.py:547-561): out[0] = nodes with
+ * incoming edges, out[1] = qualifying nodes (device int32[2]). */
+int leo_coverage(const LeoKernel* k, const LeoEdges* edges, int32_t* out, void* stream);
+
+/* rank_hotspots(attached, top_n, include_unsampled) (report.py:96-109):
+ * hot[<= top_n] instruction indices, *n_hot (device); top_n <= 4096. */
+int leo_rank_hotspots(const LeoKernel* k, const LeoProfile* p, int32_t top_n,
+                      int32_t include_unsampled, int32_t* hot, int32_t* n_hot, void* stream);
+
+/* trace_chain(graph, blame, start, max_depth) (analysis.py:499-538) over an
+ * arbitrary list of n blame entries (stalled, cause or -1 for self,
+ * blame_cycles), any order: chain_node[<= max_depth] instructions,
+ * chain_entry[] the entry that reached each hop (-1 for the start),
+ * *chain_len, *chain_self = the self entry ending the chain or -1.
+ * Cause offsets are taken to increase with the instruction index
+ * (disasm.py:391-392).  All pointers are device pointers. */
+int leo_trace_chain(const LeoKernel* k, int32_t n_entries, const int32_t* stalled,
+                    const int32_t* cause, const double* blame, int32_t start, int32_t max_depth,
+                    int32_t* chain_node, int32_t* chain_entry, int32_t* chain_len,
+                    int32_t* chain_self, void* stream);
+
+/* liveness_filter(cfg, links) (depgraph.py:274-293; liveness :235-271):
+ * keep[e] = 1 when link e survives.  links: raw/guard edges (meta carries the
+ * linking register ref), any order. */
+int leo_liveness_filter(const LeoKernel* k, const LeoEdges* links, uint8_t* keep, void* stream);
+
+/* per-source-line rollup (frozen semantics) of an arbitrary list
+ * of n blame entries (stalled, cause or -1, blame_cycles; device pointers):
+ * line_blame[line_id[cause, else stalled]] += blame_cycles and
+ * line_stall[line_id[j]] += S_j; both vectors are zeroed here. */
+int leo_line_rollup(const LeoKernel* k, const LeoProfile* p, int32_t n_entries, const int32_t* stalled,
+                    const int32_t* cause, const double* blame, const int32_t* line_id, int32_t n_lines,
+                    double* line_blame, double* line_stall, void* stream);
+
+/* reaching_definitions(cfg) (depgraph.py:135-177): the reach-in set of every
+ * (block b, unit u) pair, as the CSR defs[set_off[b*U+u] .. set_off[b*U+u+1])
+ * (set order unspecified).  Two-phase: *count is the total even when it
+ * exceeds `capacity` (then LEO_ST_SCRATCH_OVERFLOW is set in *status). */
+typedef struct LeoReachIn {
+  int64_t  capacity;          /* defs capacity */
+  int32_t* set_off;           /* [B*U + 1] */
+  int32_t* defs;              /* [capacity] */
+  int32_t* count;             /* device scalar */
+} LeoReachIn;
+int leo_reaching_definitions(const LeoKernel* k, const LeoCaps* caps, LeoReachIn* out,
+                             uint32_t* status, void* stream);
 
 /* profiling helpers for LeoTrace: create / time / destroy CUDA events */
 int leo_events_create(int32_t n, void** events);

@@ -17,9 +17,15 @@ LIB_PATH = Path(__file__).resolve().parent / "libleo_b200.so"
 # A/B timing of library variants (profiling only): LEO_LIB_VARIANT=<path>
 if os.environ.get("LEO_LIB_VARIANT"):
     LIB_PATH = Path(os.environ["LEO_LIB_VARIANT"]).resolve()
-ABI_VERSION = 1
+ABI_VERSION = 2
 
 _lib = None
+
+# every analysis entry point include/leo_b200.h declares (tests/test_abi.py)
+ENTRY_POINTS = ("leo_bin_samples", "leo_build_graph", "leo_prune", "leo_slice", "leo_blame",
+                "leo_analyze", "leo_report", "leo_self_blame", "leo_coverage", "leo_rank_hotspots",
+                "leo_trace_chain", "leo_liveness_filter", "leo_reaching_definitions",
+                "leo_line_rollup")
 
 
 class LeoLibraryError(RuntimeError):
@@ -37,13 +43,25 @@ def lib():
     if L.leo_abi_version() != ABI_VERSION:
         raise LeoLibraryError("libleo_b200.so ABI version mismatch; rebuild")
     P = C.c_void_p
-    L.leo_bin_samples.argtypes = [C.POINTER(abi.LeoSamples), C.c_int32, P, P, P]
+    L.leo_bin_samples.argtypes = [C.POINTER(abi.LeoSamples), C.c_int32, P, P, P, P]
     L.leo_build_graph.argtypes = [C.POINTER(abi.LeoKernel), C.POINTER(abi.LeoCaps),
                                   C.POINTER(abi.LeoEdges), C.POINTER(abi.LeoDiags), P, P]
     L.leo_prune.argtypes = [C.POINTER(abi.LeoKernel), C.POINTER(abi.LeoProfile),
                             C.POINTER(abi.LeoConfig), C.POINTER(abi.LeoEdges),
-                            C.POINTER(abi.LeoEdges), C.POINTER(abi.LeoPaths),
-                            C.POINTER(abi.LeoDiags), P, P]
+                            C.POINTER(abi.LeoPaths), C.POINTER(abi.LeoEdges),
+                            C.POINTER(abi.LeoPaths), C.POINTER(abi.LeoDiags), P, P]
+    L.leo_self_blame.argtypes = [C.POINTER(abi.LeoKernel), C.POINTER(abi.LeoProfile),
+                                 C.POINTER(abi.LeoEdges), C.c_int32, P, P, P, P]
+    L.leo_coverage.argtypes = [C.POINTER(abi.LeoKernel), C.POINTER(abi.LeoEdges), P, P]
+    L.leo_rank_hotspots.argtypes = [C.POINTER(abi.LeoKernel), C.POINTER(abi.LeoProfile),
+                                    C.c_int32, C.c_int32, P, P, P]
+    L.leo_trace_chain.argtypes = [C.POINTER(abi.LeoKernel), C.c_int32, P, P, P, C.c_int32,
+                                  C.c_int32, P, P, P, P, P]
+    L.leo_line_rollup.argtypes = [C.POINTER(abi.LeoKernel), C.POINTER(abi.LeoProfile), C.c_int32,
+                                  P, P, P, P, C.c_int32, P, P, P]
+    L.leo_liveness_filter.argtypes = [C.POINTER(abi.LeoKernel), C.POINTER(abi.LeoEdges), P, P]
+    L.leo_reaching_definitions.argtypes = [C.POINTER(abi.LeoKernel), C.POINTER(abi.LeoCaps),
+                                           C.POINTER(abi.LeoReachIn), P, P]
     L.leo_slice.argtypes = [C.POINTER(abi.LeoKernel), C.POINTER(abi.LeoProfile),
                             C.POINTER(abi.LeoEdges), P, P, P]
     L.leo_blame.argtypes = [C.POINTER(abi.LeoKernel), C.POINTER(abi.LeoProfile),
@@ -68,8 +86,7 @@ def lib():
     L.leo_events_destroy.argtypes = [C.c_int32, P]
     for f in ("leo_events_create", "leo_events_elapsed", "leo_events_destroy"):
         getattr(L, f).restype = C.c_int
-    for f in ("leo_bin_samples", "leo_build_graph", "leo_prune", "leo_slice", "leo_blame",
-              "leo_analyze", "leo_report"):
+    for f in ENTRY_POINTS:
         getattr(L, f).restype = C.c_int
     _lib = L
     return L

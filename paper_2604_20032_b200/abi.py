@@ -96,6 +96,10 @@ class LeoReport(C.Structure):
                 ("chain_entry", P), ("chain_self", P)]
 
 
+class LeoReachIn(C.Structure):
+    _fields_ = [("capacity", C.c_int64), ("set_off", P), ("defs", P), ("count", P)]
+
+
 DIAG_UNRESOLVED, DIAG_WAITCNT, DIAG_NO_SETTER, DIAG_PATH_CAPPED = 1, 2, 3, 4
 ST_EDGE_OVERFLOW, ST_PATH_OVERFLOW, ST_DIAG_OVERFLOW = 1, 2, 4
 ST_BLAME_OVERFLOW, ST_SCRATCH_OVERFLOW, ST_BAD_INPUT = 8, 16, 32

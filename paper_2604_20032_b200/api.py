@@ -1,37 +1,49 @@
 """Public API: the reference analyzer's names and types, backed by the CUDA path.
 
-Drop-in for the stalltrace hot path (`stalltrace/__init__.py:9-37`):
+Drop-in for the stalltrace hot path (`stalltrace/__init__.py:9-64`); every
+function takes and returns the reference's own objects and computes on the
+GPU through libleo_b200.so (no CPU fallback):
 
-    build_graph(attached) -> DependencyGraph                 depgraph.py:507
-    run_pruning(graph, config) -> DependencyGraph            analysis.py:302
-    prune_opcode / prune_barrier / prune_latency / prune_execution   analysis.py:143-299
-    attribute_blame(graph, base_graph=None) -> list[BlameEntry]      analysis.py:431
-    self_blame(index, attached, base_graph=None) -> BlameEntry       analysis.py:414
+    build_graph(attached) -> DependencyGraph                  depgraph.py:507   leo_build_graph
+    reaching_definitions(cfg) -> [ {unit: frozenset} ]        depgraph.py:135   leo_reaching_definitions
+    per_use_link(cfg, reach_in) -> (links, diags)             depgraph.py:188   leo_build_graph (raw/guard)
+    liveness_filter(cfg, links) -> links                      depgraph.py:274   leo_liveness_filter
+    trace_waitcnt / trace_barriers / trace_swsb(cfg)          depgraph.py:402-482  leo_build_graph (sync)
+    dump_graph(graph) -> str                                  depgraph.py:531   (host formatting)
+    run_pruning(graph, config) -> DependencyGraph             analysis.py:302   leo_prune
+    prune_opcode / prune_barrier / prune_latency / prune_execution  analysis.py:143-299  leo_prune
+    attribute_blame(graph, base_graph=None) -> [BlameEntry]   analysis.py:431   leo_blame
+    self_blame(index, attached, base_graph=None) -> BlameEntry analysis.py:414  leo_self_blame
+    trace_chain(graph, blame, start, max_depth=32)            analysis.py:499   leo_trace_chain
+    single_dep_coverage(graph) -> Coverage                    analysis.py:547   leo_coverage
+    rank_hotspots(attached, top_n, include_unsampled=False)   report.py:96      leo_rank_hotspots
 
 plus the two hot-path products the reference does not have:
 
-    backward_slice(graph) -> (frozenset[int], dict[int, int])
-    line_blame(graph, blame) -> (dict[str, float], dict[str, float])
+    backward_slice(graph) -> (frozenset[int], dict[int, int])  leo_slice
+    line_blame(graph, blame=None) -> (dict[str, float], dict[str, float])  leo_line_rollup
 
-and `Session`, the SoA-level entry a profiling service uses (raw PC-sample
-stream in, per-instruction blame entries + per-line totals out).
+a fused `analyze`, and `Session`, the SoA-level entry a profiling service
+uses (raw PC-sample stream in, blame entries + per-line totals out).
 
-Inputs are the reference's own objects (duck-typed: any object with the
-reference attribute names works); outputs are built from `stalltrace` classes
-when that package is importable, else from the mirror classes in
-`paper_2604_20032_b200.types` (same names, fields and enum values).  Every
-computation runs on the GPU through libleo_b200.so; there is no CPU fallback.
+Graphs may be ANY DependencyGraph (the reference's tests chain stages and
+build graphs by hand): a graph this module produced keeps its device edge
+list; any other graph's edges are marshalled to the device in list order
+(LeoEdges.n_regular = NULL: arbitrary order, include/leo_b200.h).  Outputs
+are built from `stalltrace` classes when the inputs are stalltrace objects,
+else from the same-named mirrors in `paper_2604_20032_b200.types`.
 """
 
 from __future__ import annotations
 
+import ctypes as C
 import dataclasses
 import weakref
 
 import numpy as np
 import torch
 
-from . import abi, device, diagnostics, report, soa, types
+from . import abi, device, diagnostics, ops, report, soa, types
 from . import enums as E
 
 _DEVICE = None
@@ -58,47 +70,117 @@ def _ns(obj):
 
 
 # --------------------------------------------------------------------------
-# one cached device analysis per (graph, config)
+# per-object device state, keyed by identity (frozen reference dataclasses
+# hash by value: hashing a whole KernelCfg per lookup would cost O(N))
 
-@dataclasses.dataclass
-class _Analysis:
-    ks: soa.KernelSoA
-    prof: soa.ProfileSoA
-    raw: dict
+class _IdCache:
+    def __init__(self):
+        self.d = {}
+
+    def get(self, obj):
+        hit = self.d.get(id(obj))
+        if hit is not None and hit[0]() is obj:
+            return hit[1]
+        return None
+
+    def put(self, obj, val):
+        key = id(obj)
+        try:
+            ref = weakref.ref(obj, lambda _r, k=key: self.d.pop(k, None))
+        except TypeError:
+            return val
+        self.d[key] = (ref, val)
+        return val
 
 
-_cache: "weakref.WeakKeyDictionary" = weakref.WeakKeyDictionary()
+class _Kern:
+    """A kernel (cfg or attached kernel) as device SoA."""
+
+    def __init__(self, ks, prof):
+        self.ks, self.prof = ks, prof
+        self.dk = device.DeviceKernel(ks, _dev())
+        self.dp = device.DeviceProfile(prof, ks.n_instr, _dev())
 
 
-def _config_of(config, dialect):
-    if config is None:
-        return abi.make_config(dialect=dialect)
-    if isinstance(config, abi.LeoConfig):
-        return config
-    return abi.config_from_reference(config, dialect)
+_kernels = _IdCache()
+_graphs = _IdCache()
 
 
-def _run(attached, config=None) -> _Analysis:
-    ks, prof = soa.encode_attached(attached)
-    r = device.analyze_soa(ks, prof, _config_of(config, ks.dialect), device=_dev())
-    return _Analysis(ks, prof, r)
+def _zero_profile(n):
+    return soa.ProfileSoA(period=1, lat=np.zeros(n, np.int32), cls_cnt=np.zeros((n, 8), np.int32),
+                          exec_cnt=np.full(n, -1, np.int64), total=np.full(n, -1, np.int32),
+                          eff=np.ones(n, np.float64), sampled=np.zeros(n, np.uint8))
 
+
+def _kern(obj) -> _Kern:
+    """Device SoA of an AttachedKernel (cfg + profile) or a bare KernelCfg."""
+    k = _kernels.get(obj)
+    if k is None:
+        if hasattr(obj, "cfg") and hasattr(obj, "samples"):
+            ks, prof = soa.encode_attached(obj)
+        else:
+            ks = soa.encode_cfg(obj)
+            prof = _zero_profile(ks.n_instr)
+        k = _kernels.put(obj, _Kern(ks, prof))
+    return k
+
+
+def _ref27(r):
+    return r.index | (r.span << 16) | (E.RC_IDX[r.reg_class.value] << 24)
+
+
+def _marshal(graph) -> ops.DevEdges:
+    """A DependencyGraph's edges, in list order, to the device (arbitrary order)."""
+    edges = graph.edges
+    n = len(edges)
+    prod = np.empty(n, np.int32)
+    cons = np.empty(n, np.int32)
+    meta = np.empty(n, np.uint32)
+    npaths = np.zeros(n, np.int32)
+    first = np.full(n, -1, np.int32)
+    plen, pacc = [], []
+    for x, e in enumerate(edges):
+        prod[x], cons[x] = e.producer, e.consumer
+        r27 = 0 if e.register is None else _ref27(e.register)
+        meta[x] = r27 | (E.EK_IDX[e.kind.value] << 27) | (E.DC_IDX[e.dep_class.value] << 30)
+        if e.valid_paths:
+            first[x] = len(plen)
+            npaths[x] = len(e.valid_paths)
+            for pr in e.valid_paths:
+                plen.append(pr.length_instructions)
+                pacc.append(pr.accumulated_issue_cycles)
+    return ops.DevEdges.from_arrays(_dev(), prod, cons, meta, npaths, first, np.asarray(plen, np.int32),
+                                    np.asarray(pacc, np.float64))
+
+
+def _dev_edges(graph) -> ops.DevEdges:
+    d = _graphs.get(graph)
+    if d is None:
+        d = _graphs.put(graph, _marshal(graph))
+    return d
+
+
+# --------------------------------------------------------------------------
+# device results -> reference objects
 
 def _edges(ns, ks, prod, cons, meta, npaths=None, first=None, plen=None, pacc=None):
     out = []
-    cls = ns.RegClass
-    rcs = [cls(v) for v in E.REG_CLASSES]
+    rcs = [ns.RegClass(v) for v in E.REG_CLASSES]
     kinds = [ns.EdgeKind(v) for v in E.EDGE_KINDS]
     dcs = [ns.DepClass(v) for v in E.DEP_CLASSES]
-    prod, cons, meta = prod.tolist(), cons.tolist(), meta.astype(np.uint32).tolist()
+    prod, cons, meta = prod.tolist(), cons.tolist(), np.asarray(meta).astype(np.uint32).tolist()
     if npaths is not None:
         npaths, first, plen, pacc = npaths.tolist(), first.tolist(), plen.tolist(), pacc.tolist()
+    refs = {}
     for x in range(len(prod)):
         m = meta[x]
         kind = (m >> 27) & 7
         reg = None
         if kind < 2:
-            reg = ns.RegisterRef(rcs[(m >> 24) & 7], m & 0xFFFF, (m >> 16) & 0xFF)
+            r27 = m & 0x07FFFFFF
+            reg = refs.get(r27)
+            if reg is None:
+                reg = refs[r27] = ns.RegisterRef(rcs[(m >> 24) & 7], m & 0xFFFF, (m >> 16) & 0xFF)
         paths = ()
         if npaths is not None and npaths[x] > 0:
             f = first[x]
@@ -106,12 +188,6 @@ def _edges(ns, ks, prod, cons, meta, npaths=None, first=None, plen=None, pacc=No
         out.append(ns.DepEdge(producer=prod[x], consumer=cons[x], kind=kinds[kind], register=reg,
                               dep_class=dcs[(m >> 30) & 3], valid_paths=paths))
     return tuple(out)
-
-
-def _graph(ns, attached, edges, diags, analysis, pruned):
-    g = ns.DependencyGraph(attached, edges, tuple(diags))
-    _cache[g] = (analysis, pruned)
-    return g
 
 
 def _split_diags(ks, r):
@@ -122,174 +198,356 @@ def _split_diags(ks, r):
             diagnostics.render(ks.dialect, ks.offset, prune, ordered=True))
 
 
+def _config_of(config, dialect):
+    if config is None:
+        return abi.make_config(dialect=dialect)
+    if isinstance(config, abi.LeoConfig):
+        return config
+    return abi.config_from_reference(config, dialect)
+
+
 # --------------------------------------------------------------------------
-# reference-compatible functions
+# build_graph and its sub-steps (depgraph.py)
+
+def _build(k: _Kern) -> dict:
+    b = ops.build(k.dk)
+    recs = b["diag_records"]
+    b["unresolved"] = diagnostics.render(k.ks.dialect, k.ks.offset, recs[recs[:, 0] == abi.DIAG_UNRESOLVED],
+                                         ordered=True)
+    b["sync_diags"] = diagnostics.render(k.ks.dialect, k.ks.offset, recs[recs[:, 0] != abi.DIAG_UNRESOLVED],
+                                         ordered=True)
+    return b
+
 
 def build_graph(attached):
     """depgraph.build_graph (depgraph.py:507-528) on the GPU."""
     ns = _ns(attached)
-    a = _run(attached, abi.make_config(stage_mask=(), dialect=attached.cfg.dialect.value))
-    r = a.raw
-    edges = _edges(ns, a.ks, r["bprod"], r["bcons"], r["bmeta"])
-    bdiag, _ = _split_diags(a.ks, r)
-    return _graph(ns, attached, edges, tuple(attached.diagnostics) + tuple(attached.cfg.diagnostics)
-                  + tuple(bdiag), a, False)
+    k = _kern(attached)
+    b = _build(k)
+    edges = _edges(ns, k.ks, b["bprod"], b["bcons"], b["bmeta"])
+    diags = tuple(attached.diagnostics) + tuple(attached.cfg.diagnostics) + tuple(b["unresolved"]) \
+        + tuple(b["sync_diags"])
+    g = ns.DependencyGraph(attached, edges, diags)
+    _graphs.put(g, b["edges"])
+    return g
 
 
-def _prune_with(graph, config):
-    attached = graph.attached
-    ns = _ns(attached)
-    a = _run(attached, config)
-    r = a.raw
-    base = _edges(ns, a.ks, r["bprod"], r["bcons"], r["bmeta"])
-    if tuple((e.producer, e.consumer, e.kind, e.register) for e in base) != \
-            tuple((e.producer, e.consumer, e.kind, e.register) for e in graph.edges):
-        raise ValueError("graph was not produced by build_graph on this kernel; the device "
-                         "pipeline prunes the build_graph edge list")
-    edges = _edges(ns, a.ks, r["pprod"], r["pcons"], r["pmeta"], r["npaths"], r["first"],
-                   r["plen"], r["pacc"])
-    _, pdiag = _split_diags(a.ks, r)
-    return _graph(ns, attached, edges, tuple(graph.diagnostics) + tuple(pdiag), a, True)
+_reach_of: dict = {}      # id(result) -> result, the last few reaching_definitions results
+
+
+def _remember_reach(res):
+    _reach_of[id(res)] = res
+    while len(_reach_of) > 16:
+        _reach_of.pop(next(iter(_reach_of)))
+    return res
+
+
+def _unit_keys(ns, ks):
+    """dense unit id -> (RegClass, index) (depgraph.py:41)"""
+    rcs = [ns.RegClass(v) for v in E.REG_CLASSES]
+    base = [int(x) for x in ks.unit_base] + [ks.n_units]
+    keys = [None] * ks.n_units
+    for c in range(7):
+        for u in range(base[c], min(base[c + 1], ks.n_units)):
+            keys[u] = (rcs[c], u - base[c])
+    return keys
+
+
+def reaching_definitions(cfg):
+    """depgraph.reaching_definitions (depgraph.py:135-177): block-entry reach-in
+    sets {(RegClass, index): frozenset(def indices)} for every block, computed by
+    the device's reaching-definition search on every (block, unit) pair."""
+    ns = _ns(cfg)
+    k = _kern(cfg)
+    B, U = k.ks.n_blocks, k.ks.n_units
+    off, defs = ops.reach_in(k.dk)
+    keys = _unit_keys(ns, k.ks)
+    res = []
+    for b in range(B):
+        d = {}
+        row = off[b * U:(b + 1) * U + 1]
+        for u in np.flatnonzero(np.diff(row)).tolist():
+            d[keys[u]] = frozenset(defs[row[u]:row[u + 1]].tolist())
+        res.append(d)
+    return _remember_reach(res)
+
+
+def per_use_link(cfg, reach_in):
+    """depgraph.per_use_link (depgraph.py:188-223): (links, unresolved-use
+    diagnostics).  The device derives the reach-in sets itself (the same search
+    reaching_definitions runs); `reach_in` must be reaching_definitions(cfg).
+    Links are returned in build_graph's (consumer, producer, kind, register)
+    order."""
+    if _reach_of.get(id(reach_in)) is not reach_in and reach_in != reaching_definitions(cfg):
+        raise ValueError("per_use_link: reach_in is not reaching_definitions(cfg) (the device "
+                         "derives the reaching definitions itself)")
+    ns = _ns(cfg)
+    k = _kern(cfg)
+    b = _build(k)
+    r = b["n_regular"]
+    edges = _edges(ns, k.ks, b["bprod"][:r], b["bcons"][:r], b["bmeta"][:r])
+    return [ns.UseLink(e.producer, e.consumer, e.register, e.kind) for e in edges], list(b["unresolved"])
+
+
+def liveness_filter(cfg, links):
+    """depgraph.liveness_filter (depgraph.py:274-293) on the GPU: backward
+    liveness fixed point, then the per-link live-out test."""
+    links = list(links)
+    if not links:
+        return []
+    k = _kern(cfg)
+    prod = np.fromiter((l.producer for l in links), np.int32, len(links))
+    cons = np.fromiter((l.consumer for l in links), np.int32, len(links))
+    meta = np.fromiter((_ref27(l.register) | (E.EK_IDX[l.kind.value] << 27) for l in links), np.uint32,
+                       len(links))
+    keep = ops.liveness_filter(k.dk, prod, cons, meta)
+    return [l for l, x in zip(links, keep.tolist()) if x]
+
+
+def _sync_part(cfg, dialect):
+    ns = _ns(cfg)
+    if cfg.dialect.value != dialect:
+        return [], []
+    k = _kern(cfg)
+    b = _build(k)
+    r = b["n_regular"]
+    return list(_edges(ns, k.ks, b["bprod"][r:], b["bcons"][r:], b["bmeta"][r:])), list(b["sync_diags"])
+
+
+def trace_waitcnt(cfg):
+    """depgraph.trace_waitcnt (depgraph.py:402-416): amd s_waitcnt edges."""
+    return _sync_part(cfg, "amd")
+
+
+def trace_barriers(cfg):
+    """depgraph.trace_barriers (depgraph.py:446-463): nvidia barrier edges."""
+    return _sync_part(cfg, "nvidia")
+
+
+def trace_swsb(cfg):
+    """depgraph.trace_swsb (depgraph.py:466-482): intel SBID edges."""
+    return _sync_part(cfg, "intel")
+
+
+def dump_graph(graph):
+    """depgraph.dump_graph (depgraph.py:531-544): golden text, one edge per
+    line sorted by (consumer, producer, kind) (host formatting)."""
+    cfg = graph.cfg
+    d = cfg.dialect.value
+    lines = []
+    for e in sorted(graph.edges, key=lambda e: (e.consumer, e.producer, e.kind.value)):
+        reg = ""
+        if e.register is not None:
+            reg = " reg=" + diagnostics.format_register(d, E.RC_IDX[e.register.reg_class.value],
+                                                        e.register.index, e.register.span)
+        lines.append(f"0x{cfg.instructions[e.producer].offset:04x} -> "
+                     f"0x{cfg.instructions[e.consumer].offset:04x} "
+                     f"kind={e.kind.value}{reg} class={e.dep_class.value}")
+    return "\n".join(lines) + ("\n" if lines else "")
+
+
+# --------------------------------------------------------------------------
+# pruning (analysis.py:143-314)
+
+def _prune(graph, cfg: abi.LeoConfig):
+    """One leo_prune call over the graph's device edges: the stages in
+    cfg.stage_mask applied to every edge (each stage is a per-edge predicate,
+    so one pass equals the reference's sequence of passes)."""
+    ns = _ns(graph.attached)
+    k = _kern(graph.attached)
+    r, d = ops.prune(k.dk, k.dp, cfg, _dev_edges(graph))
+    edges = _edges(ns, k.ks, r["pprod"], r["pcons"], r["pmeta"], r["npaths"], r["first"], r["plen"], r["pacc"])
+    diags = diagnostics.render(k.ks.dialect, k.ks.offset, r["diag_records"], ordered=True)
+    g = graph.with_edges(edges, tuple(diags))
+    _graphs.put(g, d)
+    return g
 
 
 def run_pruning(graph, config):
-    """analysis.run_pruning (analysis.py:302-314) on the GPU."""
-    return _prune_with(graph, config)
-
-
-def _stage(graph, mask, **kw):
-    d = graph.cfg.dialect.value
-    th = kw.pop("thresholds", None)
-    return _prune_with(graph, abi.make_config(stage_mask=mask, thresholds=th, dialect=d, **kw))
+    """analysis.run_pruning (analysis.py:302-314): stages 1 -> 2 -> 3 -> 4 per
+    config.stage_mask (stage 4 only with prune_exec), one device pass."""
+    return _prune(graph, _config_of(config, graph.cfg.dialect.value))
 
 
 def prune_opcode(graph):
     """analysis.prune_opcode (analysis.py:143-162)."""
-    return _stage(graph, (1,))
+    return _prune(graph, abi.make_config(stage_mask=(1,), dialect=graph.cfg.dialect.value))
 
 
 def prune_barrier(graph):
-    """analysis.prune_barrier (analysis.py:165-185)."""
+    """analysis.prune_barrier (analysis.py:165-185): nvidia only (identity otherwise)."""
     if graph.cfg.dialect.value != "nvidia":
         return graph
-    return _stage(graph, (2,))
+    return _prune(graph, abi.make_config(stage_mask=(2,), dialect="nvidia"))
 
 
 def prune_latency(graph, table, max_paths=64, max_depth=512):
     """analysis.prune_latency (analysis.py:256-286)."""
     th = E.dense_thresholds((c.value, v) for c, v in table.thresholds)
-    return _stage(graph, (3,), thresholds=th, max_paths=max_paths, max_depth=max_depth)
+    return _prune(graph, abi.make_config(stage_mask=(3,), thresholds=th, max_paths=max_paths,
+                                         max_depth=max_depth, dialect=graph.cfg.dialect.value))
 
 
 def prune_execution(graph, enabled):
-    """analysis.prune_execution (analysis.py:289-299)."""
+    """analysis.prune_execution (analysis.py:289-299): identity when disabled."""
     if not enabled:
         return graph
-    return _stage(graph, (4,), prune_exec=True)
+    return _prune(graph, abi.make_config(stage_mask=(4,), prune_exec=True,
+                                         dialect=graph.cfg.dialect.value))
 
+
+# --------------------------------------------------------------------------
+# blame (analysis.py:320-484), chains and coverage (:491-561)
 
 def attribute_blame(graph, base_graph=None):
-    """analysis.attribute_blame (analysis.py:431-484) on the GPU.  When
-    `graph` came from run_pruning the device result of that run is reused;
-    base_graph (the unpruned graph) feeds the indirect-addressing test."""
+    """analysis.attribute_blame (analysis.py:431-484) on the GPU, for any
+    graph; base_graph (the unpruned graph) feeds the indirect-addressing test."""
     ns = _ns(graph.attached)
-    hit = _cache.get(graph)
-    if hit is None:
-        raise ValueError("attribute_blame needs a graph produced by this package's "
-                         "build_graph / run_pruning")
-    a, pruned = hit
-    r = a.raw
-    ks = a.ks
-    if not pruned:
-        # blame directly on the base graph: prune with no stages (identity map)
-        a = _run(graph.attached, abi.make_config(stage_mask=(), dialect=ks.dialect))
-        r = a.raw
-    return _entries(ns, ks, r, base_graph is not None)
+    k = _kern(graph.attached)
+    r = ops.blame(k.dk, k.dp, _dev_edges(graph), _dev_edges(base_graph) if base_graph is not None else None)
+    return _entries(ns, k.ks, r, graph.edges)
 
 
-def _entries(ns, ks, r, with_base=True):
-    kinds = [ns.EdgeKind(v) for v in E.EDGE_KINDS]
+def _entries(ns, ks, r, edges):
     subs = [ns.SelfBlame(v) for v in E.SELF_BLAMES]
     out = []
-    pprod, pmeta = r["pprod"].tolist(), r["pmeta"].astype(np.uint32).tolist()
+    regs = {}
     for s, e, sub, bl, f in zip(r["e_stalled"].tolist(), r["e_edge"].tolist(),
                                 r["e_sub"].tolist(), r["e_blame"].tolist(),
                                 r["e_factors"].tolist()):
         if e < 0:
-            if not with_base and sub == E.SB_IDX["indirect_addressing"]:
-                sub = E.SB_IDX["memory_latency"]
             out.append(ns.BlameEntry(stalled=s, cause=None, kind=None, subcategory=subs[sub],
                                      blame_cycles=bl, factors=None))
         else:
-            m = pmeta[e]
-            kind = (m >> 27) & 7
-            reg = diagnostics.format_ref27(ks.dialect, m & 0x07FFFFFF) if kind < 2 else None
-            out.append(ns.BlameEntry(stalled=s, cause=pprod[e], kind=kinds[kind], subcategory=None,
+            ed = edges[e]
+            reg = None
+            if ed.register is not None:
+                rr = ed.register
+                reg = regs.get(rr)
+                if reg is None:
+                    reg = regs[rr] = diagnostics.format_register(
+                        ks.dialect, E.RC_IDX[rr.reg_class.value], rr.index, rr.span)
+            out.append(ns.BlameEntry(stalled=s, cause=ed.producer, kind=ed.kind, subcategory=None,
                                      blame_cycles=bl, factors=ns.Factors(*f), register=reg))
     return out
 
 
 def self_blame(index, attached, base_graph=None):
-    """analysis.self_blame (analysis.py:414-428): the SELF entry of one
-    instruction (computed by the device blame kernel with no incoming edges)."""
+    """analysis.self_blame (analysis.py:414-428): the SELF entry of any
+    instruction (S_j may be 0), classified on the device."""
     ns = _ns(attached)
-    a = _run(attached, abi.make_config(stage_mask=(1, 2, 3, 4), dialect=attached.cfg.dialect.value))
-    r = a.raw
-    sel = np.flatnonzero((r["e_stalled"] == index) & (r["e_edge"] < 0))
-    if sel.size:
-        x = int(sel[0])
-        sub = int(r["e_sub"][x])
-    else:
-        raise ValueError("self_blame: instruction has incoming edges or no stall cycles")
-    if base_graph is None and sub == E.SB_IDX["indirect_addressing"]:
-        sub = E.SB_IDX["memory_latency"]
-    return ns.BlameEntry(stalled=index, cause=None, kind=None,
-                         subcategory=ns.SelfBlame(E.SELF_BLAMES[sub]),
-                         blame_cycles=float(r["e_blame"][x]), factors=None)
+    k = _kern(attached)
+    if not 0 <= int(index) < k.ks.n_instr:
+        raise IndexError(index)
+    sub, cyc = ops.self_blame(k.dk, k.dp, _dev_edges(base_graph) if base_graph is not None else None,
+                              [int(index)])
+    return ns.BlameEntry(stalled=int(index), cause=None, kind=None,
+                         subcategory=ns.SelfBlame(E.SELF_BLAMES[int(sub[0])]), blame_cycles=float(cyc[0]),
+                         factors=None)
 
+
+def _entry_arrays(blame):
+    n = len(blame)
+    st_ = np.fromiter((b.stalled for b in blame), np.int32, n)
+    ca = np.fromiter((-1 if b.cause is None else b.cause for b in blame), np.int32, n)
+    bl = np.fromiter((b.blame_cycles for b in blame), np.float64, n)
+    return st_, ca, bl
+
+
+def trace_chain(graph, blame, start, max_depth=32):
+    """analysis.trace_chain (analysis.py:499-538): greedy backward walk along
+    the highest-blame entry, on the device."""
+    ns = _ns(graph.attached)
+    if start >= len(graph.cfg.instructions) or start < 0:
+        raise ValueError(f"chain start index {start} is not in the graph")
+    blame = list(blame)
+    chain = [ns.ChainHop(index=start, kind=None, blame_cycles=None, share=None, self_blame=None)]
+    if max_depth <= 1:
+        return chain
+    k = _kern(graph.attached)
+    _, ent, self_e = ops.trace_chain(k.dk, *_entry_arrays(blame), start, max_depth)
+    attached = graph.attached
+    for t in range(1, len(ent)):
+        b = blame[ent[t]]
+        s_node = attached.stall_cycles_at(chain[-1].index)
+        chain.append(ns.ChainHop(index=b.cause, kind=b.kind, blame_cycles=b.blame_cycles,
+                                 share=(b.blame_cycles / s_node) if s_node else None, self_blame=None))
+    if self_e >= 0:
+        chain[-1] = dataclasses.replace(chain[-1], self_blame=blame[self_e].subcategory)
+    return chain
+
+
+def single_dep_coverage(graph):
+    """analysis.single_dep_coverage (analysis.py:547-561) on the device."""
+    ns = _ns(graph.attached)
+    if not graph.edges:
+        return ns.Coverage(value=1.0, vacuous=True)
+    nodes, qual = ops.coverage(_kern(graph.attached).dk, _dev_edges(graph))
+    return ns.Coverage(value=qual / nodes, vacuous=False)
+
+
+def rank_hotspots(attached, top_n, include_unsampled=False):
+    """report.rank_hotspots (report.py:96-109) on the device (top_n <= 4096)."""
+    top_n = max(0, int(top_n))
+    if top_n == 0:
+        return []
+    k = _kern(attached)
+    return ops.rank_hotspots(k.dk, k.dp, top_n, include_unsampled)
+
+
+# --------------------------------------------------------------------------
+# the slice and the per-line rollup (the two products the reference lacks)
 
 def backward_slice(graph):
     """Multi-source backward slice from every instruction with S_j > 0 over
-    graph.incoming (DESIGN.md §slice): (members, {index: hop level})."""
-    hit = _cache.get(graph)
-    if hit is None:
-        raise ValueError("backward_slice needs a graph produced by this package")
-    a, pruned = hit
-    r = a.raw if pruned else _run(graph.attached, abi.make_config(stage_mask=(), dialect=a.ks.dialect)).raw
-    lv = r["level"]
+    graph.incoming (DESIGN.md §1): (members, {index: hop level})."""
+    k = _kern(graph.attached)
+    lv = ops.slice_levels(k.dk, k.dp, _dev_edges(graph))
     idx = np.flatnonzero(lv >= 0)
     return frozenset(idx.tolist()), {int(i): int(lv[i]) for i in idx}
 
 
 def line_blame(graph, blame=None):
-    """Per-source-line rollup: blame cycles by the cause's
-    line (self entries: the stalled instruction's line) and stall cycles by the
-    stalled instruction's line, keyed `file:line` / `<unknown>`."""
-    hit = _cache.get(graph)
-    if hit is None:
-        raise ValueError("line_blame needs a graph produced by this package")
-    a, _ = hit
-    keys = a.ks.lines
-    lb, ls = a.raw["line_blame"], a.raw["line_stall"]
+    """Per-source-line rollup: blame cycles by the cause's line
+    (self entries: the stalled instruction's line) and stall cycles by the
+    stalled instruction's line, keyed `file:line` / `<unknown>`.  `blame`:
+    the entries to roll up (default: attribute_blame(graph) on the device)."""
+    k = _kern(graph.attached)
+    keys = k.ks.lines
+    if blame is None:
+        r = ops.blame(k.dk, k.dp, _dev_edges(graph), None, lines=True)
+        lb, ls = r["line_blame"], r["line_stall"]
+    else:
+        lb, ls = ops.line_rollup(k.dk, k.dp, *_entry_arrays(list(blame)))
     return ({keys[i]: float(lb[i]) for i in np.flatnonzero(lb)},
             {keys[i]: float(ls[i]) for i in np.flatnonzero(ls)})
 
 
+# --------------------------------------------------------------------------
+# fused pass
+
 def analyze(attached, config=None):
-    """Fused build -> prune -> blame -> slice -> lines in one device pass:
-    (base graph, pruned graph, blame entries, slice, (line blame, line stall))."""
+    """Fused build -> prune -> blame -> slice -> lines in one device pass
+    (leo_analyze): (base graph, pruned graph, blame entries, slice,
+    (line blame, line stall))."""
     ns = _ns(attached)
-    a = _run(attached, config)
-    r = a.raw
-    bdiag, pdiag = _split_diags(a.ks, r)
+    ks, prof = soa.encode_attached(attached)
+    r = device.analyze_soa(ks, prof, _config_of(config, ks.dialect), device=_dev())
+    bdiag, pdiag = _split_diags(ks, r)
     prefix = tuple(attached.diagnostics) + tuple(attached.cfg.diagnostics)
-    base = _graph(ns, attached, _edges(ns, a.ks, r["bprod"], r["bcons"], r["bmeta"]),
-                  prefix + tuple(bdiag), a, False)
-    pruned = _graph(ns, attached, _edges(ns, a.ks, r["pprod"], r["pcons"], r["pmeta"], r["npaths"],
-                                         r["first"], r["plen"], r["pacc"]),
-                    prefix + tuple(bdiag) + tuple(pdiag), a, True)
-    entries = _entries(ns, a.ks, r)
-    return base, pruned, entries, backward_slice(pruned), line_blame(pruned)
+    base = ns.DependencyGraph(attached, _edges(ns, ks, r["bprod"], r["bcons"], r["bmeta"]),
+                              prefix + tuple(bdiag))
+    pruned = ns.DependencyGraph(attached, _edges(ns, ks, r["pprod"], r["pcons"], r["pmeta"], r["npaths"],
+                                                 r["first"], r["plen"], r["pacc"]),
+                                prefix + tuple(bdiag) + tuple(pdiag))
+    entries = _entries(ns, ks, r, pruned.edges)
+    lv = r["level"]
+    idx = np.flatnonzero(lv >= 0)
+    keys = ks.lines
+    lb, ls = r["line_blame"], r["line_stall"]
+    lines = ({keys[i]: float(lb[i]) for i in np.flatnonzero(lb)},
+             {keys[i]: float(ls[i]) for i in np.flatnonzero(ls)})
+    return base, pruned, entries, (frozenset(idx.tolist()), {int(i): int(lv[i]) for i in idx}), lines
 
 
 # --------------------------------------------------------------------------
@@ -307,6 +565,7 @@ class Session:
                  config: abi.LeoConfig | None = None, dev=None, pin: bool = True):
         self.dev = torch.device(dev) if dev is not None else _dev()
         self.ks = ks
+        self.n_samples = int(n_samples)
         self.cfg = config or abi.make_config(dialect=ks.dialect)
         self.dk = device.DeviceKernel(ks, self.dev)
         self.dp = device.DeviceProfile(prof_meta, ks.n_instr, self.dev)
@@ -374,8 +633,29 @@ class Session:
             t.numpy().reshape(a.shape)[...] = a
         return t
 
+    def _check_sizes(self, ks, prof_meta, pc, cat, lut):
+        """The captured graph copies from buffers sized at construction: a step
+        whose arrays have other sizes is refused, not silently mis-copied."""
+        n = self.ks.n_instr
+        want = {"k_" + f: np.asarray(getattr(self.ks, f)).size for f in self.H2D_FIELDS}
+        got = {"k_" + f: np.asarray(getattr(ks, f)).size for f in self.H2D_FIELDS}
+        if getattr(self.ks, "seg_block", None) is not None or getattr(ks, "seg_block", None) is not None:
+            want["k_seg_block"] = np.asarray(getattr(self.ks, "seg_block", ())).size
+            got["k_seg_block"] = np.asarray(getattr(ks, "seg_block", ())).size
+        want["line_id"], got["line_id"] = n, np.asarray(ks.line_id).size
+        for f in ("exec_cnt", "total", "eff", "sampled"):
+            want["p_" + f], got["p_" + f] = n, np.asarray(getattr(prof_meta, f)).size
+        want["pc"], got["pc"] = self.n_samples, np.asarray(pc).size
+        want["cat"], got["cat"] = self.n_samples, np.asarray(cat).size
+        want["lut"], got["lut"] = 256, np.asarray(lut).size
+        bad = {k: (got[k], v) for k, v in want.items() if got[k] != v}
+        if bad:
+            raise ValueError(f"Session.stage: input sizes differ from the session's shape "
+                             f"(got, expected): {bad}")
+
     def stage(self, ks, prof_meta, pc, cat, lut):
         """Put one step's inputs into pinned host buffers (outside timing)."""
+        self._check_sizes(ks, prof_meta, pc, cat, lut)
         for n in self.H2D_FIELDS:
             self._h("k_" + n, getattr(ks, n))
         if getattr(ks, "seg_block", None) is not None:

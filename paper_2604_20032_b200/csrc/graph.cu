@@ -551,11 +551,16 @@ __global__ void k_reach_unit(KView k, ReachArgs a, const int32_t* __restrict__ q
 
 // Tier 1: lockstep per-lane state machine.  Every lane owns one query at a
 // time and advances it by one search step per loop iteration; a lane whose
-// query finished fetches the next from a shared queue (warp-aggregated
-// atomic), so lanes never idle behind the warp's longest query.  The visited
-// set is a private open-addressing hash in shared memory (strided per thread),
-// cleared through the list of slots it used.
+// query finished takes the next from a warp-private batch of the query list
+// (one global atomic per kT1Fetch queries), so lanes never idle behind the
+// warp's longest query.  Finished queries reserve their result slots from a
+// warp-private chunk of the results pool (one global atomic per kT1Chunk
+// results): on C5 (~1 M queries) a per-query atomic on the one pool counter
+// was 40 % of the kernel's stall samples.  The visited set is a private
+// open-addressing hash in shared memory (strided per thread), cleared through
+// the list of slots it used.
 constexpr int kT1Hash = 128, kT1Limit = 96, kT1Stack = 96, kT1Res = 32, kT1Threads = 128;
+constexpr int kT1Fetch = 64, kT1Chunk = 512;
 
 __global__ void __launch_bounds__(kT1Threads) k_reach_fast(KView k, ReachArgs a,
                                                            const int32_t* __restrict__ q_list,
@@ -564,6 +569,7 @@ __global__ void __launch_bounds__(kT1Threads) k_reach_fast(KView k, ReachArgs a,
   extern __shared__ int32_t hsm[];
   const int nq = *q_count;
   const int lane = threadIdx.x & 31;
+  const unsigned lt = (1u << lane) - 1;
   int32_t* H = hsm + threadIdx.x;                  // slot s at H[s * blockDim.x]
   const int stride = blockDim.x;
   for (int s2 = 0; s2 < kT1Hash; s2++) H[s2 * stride] = -1;
@@ -571,6 +577,8 @@ __global__ void __launch_bounds__(kT1Threads) k_reach_fast(KView k, ReachArgs a,
   uint8_t used[kT1Limit];
   int e = -1, u = 0, sp = 0, nres = 0, nused = 0;
   bool drained = false, ovf = false;
+  // warp-uniform: the warp's current batch of the query list, and chunk of the pool
+  int fb = 0, fleft = 0, cb = 0, cleft = 0;
 
   auto insert = [&](int key) -> int {              // 1 new, 0 seen, -1 overflow
     int x = (int)(((uint32_t)key * 2654435761u) >> 25);   // 7 bits
@@ -593,15 +601,21 @@ __global__ void __launch_bounds__(kT1Threads) k_reach_fast(KView k, ReachArgs a,
   };
 
   while (true) {
-    // lanes without a query fetch one (one atomic per warp)
+    // lanes without a query take one from the warp's batch (refilled with one atomic)
     const bool need = e < 0 && !drained;
     const unsigned m = __ballot_sync(0xffffffffu, need);
     if (m) {
-      int base = 0;
-      if (lane == __ffs(m) - 1) base = atomicAdd(q_head, __popc(m));
-      base = __shfl_sync(0xffffffffu, base, __ffs(m) - 1);
+      const int nm = __popc(m);
+      // ranks [0, fleft) take the rest of the current batch, the others a new one
+      int nb = 0;
+      if (fleft < nm) {
+        int g = 0;
+        if (lane == 0) g = atomicAdd(q_head, kT1Fetch);
+        nb = __shfl_sync(0xffffffffu, g, 0);
+      }
       if (need) {
-        const int t = base + __popc(m & ((1u << lane) - 1));
+        const int rk = __popc(m & lt);
+        const int t = rk < fleft ? fb + rk : nb + (rk - fleft);
         if (t >= nq) {
           drained = true;
         } else {
@@ -617,37 +631,67 @@ __global__ void __launch_bounds__(kT1Threads) k_reach_fast(KView k, ReachArgs a,
           }
         }
       }
+      if (fleft < nm) { fb = nb + (nm - fleft); fleft = kT1Fetch - (nm - fleft); }
+      else { fb += nm; fleft -= nm; }
     }
     if (!__any_sync(0xffffffffu, e >= 0)) {
       if (__all_sync(0xffffffffu, drained)) break;
       continue;
     }
-    if (e >= 0) {
-      if (!ovf && sp > 0) {                        // one search step
-        const int y = stk[--sp];
-        const int own = a.ldtab[(size_t)u * a.Bp + y];  // issued together with the record load
-        const int4 r = a.rec[y];
-        const int ld = own >= 0 ? own : (r.x < y ? run_lookup(a, y - 1, r.x, u) : -1);
-        if (ld >= 0) {
-          if (nres == kT1Res) ovf = true; else res[nres++] = ld;
-        } else {
-          for (int t = 0; t < r.y && !ovf; t++) {
-            const int pp = r.y <= 2 ? (t == 0 ? r.z : r.w) : k.pred[r.z + t];
-            const int v = insert(pp);
-            if (v < 0 || (v && sp == kT1Stack)) ovf = true;
-            else if (v) stk[sp++] = pp;
-          }
+    if (e >= 0 && !ovf && sp > 0) {               // one search step
+      const int y = stk[--sp];
+      const int own = a.ldtab[(size_t)u * a.Bp + y];  // issued together with the record load
+      const int4 r = a.rec[y];
+      const int ld = own >= 0 ? own : (r.x < y ? run_lookup(a, y - 1, r.x, u) : -1);
+      if (ld >= 0) {
+        if (nres == kT1Res) ovf = true; else res[nres++] = ld;
+      } else {
+        for (int t = 0; t < r.y && !ovf; t++) {
+          const int pp = r.y <= 2 ? (t == 0 ? r.z : r.w) : k.pred[r.z + t];
+          const int v = insert(pp);
+          if (v < 0 || (v && sp == kT1Stack)) ovf = true;
+          else if (v) stk[sp++] = pp;
         }
       }
-      if (ovf) {                                   // hand the query to tier 2
-        const int s2 = atomicAdd(a.slow_count, 1);
-        if (s2 < a.slow_cap) a.slow_list[s2] = e;
-        else { a.q_off[e] = 0; a.q_len[e] = 0; atomicOr(a.status, (uint32_t)LEO_ST_SCRATCH_OVERFLOW); }
-        release();
-      } else if (sp == 0) {                        // done: commit the results
-        reach_commit(a, e, res, nres);
+    }
+    if (e >= 0 && ovf) {                           // hand the query to tier 2
+      const int s2 = atomicAdd(a.slow_count, 1);
+      if (s2 < a.slow_cap) a.slow_list[s2] = e;
+      else { a.q_off[e] = 0; a.q_len[e] = 0; atomicOr(a.status, (uint32_t)LEO_ST_SCRATCH_OVERFLOW); }
+      release();
+    }
+    // finished queries: result slots from the warp's chunk of the pool
+    const bool done = e >= 0 && sp == 0;
+    if (__ballot_sync(0xffffffffu, done)) {
+      const int cnt = done ? nres : 0;
+      int incl = cnt;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const int t = __shfl_up_sync(0xffffffffu, incl, o);
+        if (lane >= o) incl += t;
+      }
+      const int tot = __shfl_sync(0xffffffffu, incl, 31);
+      if (tot > cleft) {
+        const int want = max(tot, kT1Chunk);
+        int g = 0;
+        if (lane == 0) g = atomicAdd(a.qres_count, want);
+        cb = __shfl_sync(0xffffffffu, g, 0);
+        cleft = want;
+      }
+      if (done) {
+        const int off = cb + incl - cnt;
+        if ((int64_t)off + nres > a.qres_cap) {
+          atomicOr(a.status, (uint32_t)LEO_ST_SCRATCH_OVERFLOW);
+          a.q_off[e] = 0; a.q_len[e] = 0;
+        } else {
+          for (int x = 0; x < nres; x++) a.qres[off + x] = res[x];
+          a.q_off[e] = off;
+          a.q_len[e] = nres;
+        }
         release();
       }
+      cb += tot;
+      cleft -= tot;
     }
   }
 }

@@ -6,6 +6,7 @@
 // data-dependent size lives in device memory and the kernels read it there.
 #include <algorithm>
 #include <functional>
+#include <vector>
 #include <cstdio>
 #include <cstring>
 #include <cstdlib>
@@ -16,6 +17,7 @@
 #include "prune.cu"
 #include "blame.cu"
 #include "report.cu"
+#include "api_ops.cu"
 
 
 using namespace leo;
@@ -94,15 +96,18 @@ bool no_fork_env() {
   return v == 1;
 }
 
-int g_num_sms = 0;
+// SM count of the calling thread's current device (cached per device: one
+// process may drive several GPUs)
 int num_sms() {
-  if (!g_num_sms) {
-    int dev = 0;
-    cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&g_num_sms, cudaDevAttrMultiProcessorCount, dev);
-    if (g_num_sms <= 0) g_num_sms = 148;
+  static int cache[64] = {};
+  int dev = 0;
+  cudaGetDevice(&dev);
+  int& n = cache[dev & 63];
+  if (!n) {
+    cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
+    if (n <= 0) n = 148;
   }
-  return g_num_sms;
+  return n;
 }
 
 // Caller-owned workspace (LeoCaps.workspace): every arena of one entry-point
@@ -166,7 +171,9 @@ inline int64_t pick(int64_t hint, int64_t dflt) { return hint > 0 ? hint : dflt;
 
 // Side streams + events for fork/join concurrency inside one pipeline call
 // (independent stages run as parallel branches; under stream capture they
-// become parallel branches of the CUDA graph).  Created once per host thread.
+// become parallel branches of the CUDA graph).  One pool per (host thread,
+// device, caller stream): calls on different streams or devices never share
+// side streams (no false serialisation between them).
 struct SidePool {
   cudaStream_t s[4] = {nullptr, nullptr, nullptr, nullptr};
   cudaEvent_t e[8] = {};
@@ -178,10 +185,16 @@ struct SidePool {
     ok = true;
   }
 };
-SidePool& side_pool() {
-  static thread_local SidePool p;
-  p.init();
-  return p;
+SidePool& side_pool(cudaStream_t caller) {
+  struct Key { int dev; cudaStream_t st; SidePool* p; };
+  static thread_local std::vector<Key> pools;
+  int dev = 0;
+  cudaGetDevice(&dev);
+  for (auto& k : pools)
+    if (k.dev == dev && k.st == caller) return *k.p;
+  pools.push_back(Key{dev, caller, new SidePool()});
+  pools.back().p->init();
+  return *pools.back().p;
 }
 // `to` waits for all work enqueued so far on `from`
 inline void link_streams(cudaStream_t from, cudaStream_t to, cudaEvent_t ev) {
@@ -189,10 +202,14 @@ inline void link_streams(cudaStream_t from, cudaStream_t to, cudaEvent_t ev) {
   cudaStreamWaitEvent(to, ev, 0);
 }
 
-// kernels that take more than 48 KiB of dynamic shared memory (set once)
+// kernels that take more than 48 KiB of dynamic shared memory (a per-device
+// function attribute: set once per device)
 void set_smem_attributes() {
-  static bool done = false;
-  if (done) return;
+  static uint64_t done_mask = 0;
+  int dev = 0;
+  cudaGetDevice(&dev);
+  const uint64_t bit = 1ull << (dev & 63);
+  if (done_mask & bit) return;
   cudaFuncSetAttribute(k_reach_fast, cudaFuncAttributeMaxDynamicSharedMemorySize, kT1Threads * kT1Hash * 4);
   cudaFuncSetAttribute(k_bin_count, cudaFuncAttributeMaxDynamicSharedMemorySize, kBinRMax * 8 * 4);
   cudaFuncSetAttribute(k_bin_scatter, cudaFuncAttributeMaxDynamicSharedMemorySize, kBinMaxBuckets * 12 + kBinSub * 4);
@@ -205,7 +222,7 @@ void set_smem_attributes() {
   cudaFuncSetAttribute(k_sync_setter_cta<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)(16 + setter_warp_tables_smem()));
   cudaFuncSetAttribute(k_prune_edges_smem<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemResidentMax);
   cudaFuncSetAttribute(k_prune_edges_smem<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemResidentMax);
-  done = true;
+  done_mask |= bit;
 }
 
 int check_kernel(const LeoKernel* k) {
@@ -220,12 +237,14 @@ int check_kernel(const LeoKernel* k) {
 // build_graph
 int build_graph_impl(const LeoKernel* kk, const LeoCaps* caps, LeoEdges* out, LeoDiags* diags,
                      uint32_t* status, cudaStream_t st, Range own = Range{0, 0},
-                     const std::function<int()>& after_walk = {}) {
+                     const std::function<int()>& after_walk = {}, LeoReachIn* rall = nullptr) {
   LeoTrace* tr = caps ? caps->trace : nullptr;
   KView k = make_kview(kk);
   const int N = k.N, B = k.B, U = k.U;
   const int64_t NU = kk->n_use_units, ND = kk->n_def_units;
-  const int64_t cap_qres = pick(caps ? caps->query_results : 0, 4 * NU + 1024);
+  // rall (leo_reaching_definitions): every (block, unit) pair is a query
+  const int64_t NQ = NU + (rall ? (int64_t)B * U : 0);
+  const int64_t cap_qres = pick(caps ? caps->query_results : 0, 4 * NQ + 1024);
   const int64_t cap_cand = pick(caps ? caps->candidates : 0, 6 * NU + 1024);
   const int64_t cap_sync = pick(caps ? caps->sync_keys : 0, 2 * (int64_t)N + 1024);
   const int64_t cap_slow = pick(caps ? caps->slow_items : 0, N / 4 + 1024);
@@ -253,9 +272,9 @@ int build_graph_impl(const LeoKernel* kk, const LeoCaps* caps, LeoEdges* out, Le
   int32_t* lastset;
   char* sync_scr;
   ar.want(&ucnt, N); ar.want(&dcnt, N); ar.want(&use_ptr, N + 1); ar.want(&def_ptr, N + 1);
-  ar.want(&ev_res, NU); ar.want(&q_block, NU); ar.want(&q_unit, NU); ar.want(&q_list, NU);
-  ar.want(&q_off, NU); ar.want(&q_len, NU); ar.want(&qres, cap_qres); ar.want(&ctr, 16);
-  ar.want(&slow_list, NU + 1024); ar.want(&slow2, cap_slow); ar.want(&slow3, NU + 1024); ar.want(&cand_cnt, N); ar.want(&cand_off, N + 1);
+  ar.want(&ev_res, NU); ar.want(&q_block, NQ); ar.want(&q_unit, NQ); ar.want(&q_list, NQ);
+  ar.want(&q_off, NQ); ar.want(&q_len, NQ); ar.want(&qres, cap_qres); ar.want(&ctr, 16);
+  ar.want(&slow_list, NQ + 1024); ar.want(&slow2, cap_slow); ar.want(&slow3, NQ + 1024); ar.want(&cand_cnt, N); ar.want(&cand_off, N + 1);
   const int Bp = (B + 3) & ~3;   // 16-byte aligned unit columns
   ar.want(&uniq, N); ar.want(&eoff, N + 1); ar.want(&ldtab, (int64_t)Bp * U); ar.want(&qtab, (int64_t)Bp * U);
   ar.want(&brec, B); ar.want(&rhead, B);
@@ -269,13 +288,15 @@ int build_graph_impl(const LeoKernel* kk, const LeoCaps* caps, LeoEdges* out, Le
   const int n_ids = k.dialect == LEO_INTEL ? 32 : 8;
   ar.want(&wcword, N); ar.want(&bev, B); ar.want(&setword, N); ar.want(&lastset, (int64_t)B * n_ids);
   if (!smem_tab) ar.want(&gtab, (int64_t)walk_warps * 2 * U);
+  int32_t *rcnt = nullptr, *rscan = nullptr;
+  if (rall) { ar.want(&rcnt, (int64_t)B * U); ar.want(&rscan, scan_scratch_ints(std::max<int64_t>((int64_t)B * U, 1)) + 64); }
   LEO_CUDA_CHECK(ar.commit());
   // counters: 0 q_count, 1 qres_count, 2 reach slow, 3 sync keys, 4 sync slow, 5 n_regular, 6 n_sync
   cudaMemsetAsync(ctr, 0, 16 * sizeof(int32_t), st);
   const int T = 256;
   // fork: vendor sync tracing runs on a side stream, concurrently with the
   // register dataflow chain below
-  SidePool& sp = side_pool();
+  SidePool& sp = side_pool(st);
   // traced runs stay on one stream so per-kernel event times are not
   // inflated by queueing behind concurrent branches
   const bool fork = (tr == nullptr || (tr->mode & 1)) && !no_fork_env();
@@ -363,7 +384,8 @@ int build_graph_impl(const LeoKernel* kk, const LeoCaps* caps, LeoEdges* out, Le
     TRACED(KID_SEGSORT, leo_launch(segsort_unique_u64, grid_for(N, 128), 128, 0, st, ssorted, poff, pcnt, nullptr, N, puniq, cap_sync));
     TRACED(KID_SCAN, scan_exclusive(puniq, puoff, nullptr, N, scan_tmp2, &ctr[6], st));
   };
-  if (fork_at <= 0) enqueue_sync();
+  const bool with_sync = rall == nullptr;     // reaching_definitions alone: no sync branch
+  if (fork_at <= 0 && with_sync) enqueue_sync();
   // (a fused one-CTA count + scan is latency-bound on the operand loads: the
   // grid-wide count and two single-pass scans are faster)
   TRACED(KID_UNIT_COUNTS, leo_launch(k_unit_counts, std::max(grid_for(N, T), grid_for(B, T)), T, 0, st, k, ucnt, dcnt,
@@ -374,7 +396,7 @@ int build_graph_impl(const LeoKernel* kk, const LeoCaps* caps, LeoEdges* out, Le
     TRACED(KID_SCAN, scan_exclusive(ucnt, use_ptr, nullptr, N, scan_tmp, nullptr, st));
     TRACED(KID_SCAN, scan_exclusive(dcnt, def_ptr, nullptr, N, scan_tmp, nullptr, st));
   }
-  if (fork_at == 1) enqueue_sync();
+  if (fork_at == 1 && with_sync) enqueue_sync();
 
   // tier 0 (shared-memory reach) reads the query columns, not the list
   const int n_seg0 = (kk->n_segments > 1 && kk->seg_block) ? kk->n_segments : 1;
@@ -392,10 +414,13 @@ int build_graph_impl(const LeoKernel* kk, const LeoCaps* caps, LeoEdges* out, Le
   if (after_walk) {
     if (int e = after_walk()) return e;
   }
-  if (fork_at >= 2) enqueue_sync();
+  if (rall && B > 0 && U > 0)
+    leo_launch(k_reach_claim_all, grid_for((int64_t)B * U, 256), 256, 0, st, k, Bp, NU, qtab, q_block, q_unit,
+               tier0 ? nullptr : q_list, &ctr[0]);
+  if (fork_at >= 2 && with_sync) enqueue_sync();
 
   ReachArgs ra{caps ? caps->debug_flags : 0, ldtab, brec, U, Bp, q_block, q_unit, q_off, q_len, qres, cap_qres, &ctr[1],
-               slow_list, &ctr[2], NU + 1024, status};
+               slow_list, &ctr[2], NQ + 1024, status};
   const int dbg = caps ? caps->debug_flags : 0;
   if (dbg & LEO_DBG_PHASES) {
     static const int zero = 0;
@@ -428,10 +453,24 @@ int build_graph_impl(const LeoKernel* kk, const LeoCaps* caps, LeoEdges* out, Le
   {
     const int wpc_r = 4;
     const size_t sm_r = (size_t)wpc_r * kWarpSmemInts * 4;
-    TRACED(KID_REACH_WARP, leo_launch(k_reach_warp, std::max(1, std::min<int>(SM * 4, (int)((NU + 1024 + wpc_r - 1) / wpc_r))),
-                                          wpc_r * 32, sm_r, st, k, ra, slow_list, &ctr[2], NU + 1024, slow3, &ctr[7]));
+    TRACED(KID_REACH_WARP, leo_launch(k_reach_warp, std::max(1, std::min<int>(SM * 4, (int)((NQ + 1024 + wpc_r - 1) / wpc_r))),
+                                          wpc_r * 32, sm_r, st, k, ra, slow_list, &ctr[2], NQ + 1024, slow3, &ctr[7]));
   }
   TRACED(KID_REACH_SLOW, leo_launch(k_reach_slow, (RW + 63) / 64, 64, 0, st, k, ra, slow3, &ctr[7], reach_scr, RW));
+  if (rall) {                     // export the reach-in set of every (block, unit) as a CSR
+    const int64_t P = (int64_t)B * U;
+    if (P > 0) {
+      leo_launch(k_reach_export_count, grid_for(P, 256), 256, 0, st, k, Bp, qtab, q_len, rcnt);
+      scan_exclusive(rcnt, rall->set_off, nullptr, P, rscan, nullptr, st);
+      leo_launch(k_reach_export_fill, grid_for(P, 256), 256, 0, st, k, Bp, qtab, q_off, q_len, qres, *rall, status);
+    } else {
+      cudaMemsetAsync(rall->set_off, 0, sizeof(int32_t), st);
+      cudaMemsetAsync(rall->count, 0, sizeof(int32_t), st);
+    }
+    ar.release();
+    LEO_CUDA_CHECK(cudaGetLastError());
+    return 0;
+  }
 
   LinkArgs la{use_ptr, ev_res, q_off, q_len, qres, cand_cnt, cand_off, cand, cap_cand, *diags, status, own};
   TRACED(KID_LINK_COUNT, leo_launch(k_link<0>, grid_for(N, T), T, 0, st, k, la));
@@ -455,7 +494,8 @@ int build_graph_impl(const LeoKernel* kk, const LeoCaps* caps, LeoEdges* out, Le
 // run_pruning
 int prune_impl(const LeoKernel* kk, const LeoProfile* pp, const LeoConfig* cfg, const LeoEdges* in,
                LeoEdges* out, LeoPaths* paths, LeoDiags* diags, const LeoCaps* caps, uint32_t* status,
-               cudaStream_t st, ZeroSet zero = ZeroSet{{nullptr, nullptr, nullptr, nullptr}, 0}) {
+               cudaStream_t st, ZeroSet zero = ZeroSet{{nullptr, nullptr, nullptr, nullptr}, 0},
+               const LeoPaths* in_paths = nullptr) {
   LeoTrace* tr = caps ? caps->trace : nullptr;
   KView k = make_kview(kk);
   PView p = make_pview(pp);
@@ -473,9 +513,15 @@ int prune_impl(const LeoKernel* kk, const LeoProfile* pp, const LeoConfig* cfg, 
   (void)n_reg_in;
   LEO_CUDA_CHECK(ar.commit());
   cudaMemsetAsync(ctr, 0, 4 * sizeof(int32_t), st);
-  cudaMemsetAsync(paths->count, 0, sizeof(int32_t), st);
+  LeoPaths inp{};
+  if (in_paths && in_paths->first) {
+    inp = *in_paths;
+    leo_launch(k_copy_pool, grid_for(in_paths->capacity, 256), 256, 0, st, *in_paths, *paths, status);
+  } else {
+    cudaMemsetAsync(paths->count, 0, sizeof(int32_t), st);
+  }
   PruneArgs a{caps ? caps->debug_flags : 0, *cfg, in->prod, in->cons, in->meta, in->count, (int32_t)cap_in, keep, npaths, pfirst, dist,
-              *paths, slow_list, &ctr[0], cap_slow, *diags, status};
+              *paths, inp, slow_list, &ctr[0], cap_slow, *diags, status};
   {
     const int dbg = caps ? caps->debug_flags : 0;
     const char* pt_env = getenv("LEO_PRUNE_THREADS");
@@ -567,8 +613,12 @@ void want_addr(Arena& ar, AddrBufs& b, int N, int64_t edge_cap) {
   want_incoming(ar, b.bb, N, 1);
   ar.want(&b.la, N); ar.want(&b.lb, N); ar.want(&b.ok, N); ar.want(&b.ep, std::max<int64_t>(edge_cap, 1));
 }
+// The labels pack a 24-bit instruction id (kMpT): kernels of >= 2^24
+// instructions take the exact per-candidate BFS tiers instead (mp_ok = null).
+inline bool mp_labels_fit(int n_instr) { return n_instr < (int)kMpT; }
 Incoming addr_impl(const KView& k, const LeoEdges* base, AddrBufs& b, LeoTrace* tr, cudaStream_t st) {
   Incoming binc = build_incoming(b.bb, k.N, base, false, tr, st);   // RAW edges only
+  if (!mp_labels_fit(k.N)) return binc;
   const int g = grid_for(k.N, 128);
   TRACED(KID_SELF_ADDR, leo_launch(k_mp_edges, grid_for(base->capacity, 256, num_sms() * 8), 256, 0, st, k,
                                    base->n_regular, (int64_t)base->capacity, base->prod, base->meta, b.ep));
@@ -581,6 +631,34 @@ Incoming addr_impl(const KView& k, const LeoEdges* base, AddrBufs& b, LeoTrace* 
   // round r writes lb when r is odd, la when even: round 6 (the last) wrote la
   TRACED(KID_SELF_ADDR, leo_launch(k_mp_final, g, 128, 0, st, k, binc.rbeg, binc.rend, b.ep, b.la, b.ok));
   return binc;
+}
+
+// Caller edge lists whose LeoEdges.n_regular is NULL are in arbitrary order
+// (the reference's DependencyGraph holds any edge tuple): the incoming CSR then
+// takes every edge through the stable counting sort (list order per consumer).
+LeoEdges any_order(const LeoEdges& e, int32_t* zero_scalar) {
+  LeoEdges v = e;
+  if (!v.n_regular) v.n_regular = zero_scalar;
+  return v;
+}
+
+// consumer-sorted (stable) copy of an arbitrary-order edge list: the base
+// graph's RAW CSR of the indirect-addressing test needs consumer runs
+struct CanonBufs {
+  IncomingBufs ib;
+  int32_t *prod, *cons, *count, *nreg;
+  uint32_t* meta;
+};
+void want_canon(Arena& ar, CanonBufs& b, int N, int64_t cap) {
+  want_incoming(ar, b.ib, N, cap);
+  ar.want(&b.prod, cap); ar.want(&b.cons, cap); ar.want(&b.meta, cap); ar.want(&b.count, 1); ar.want(&b.nreg, 1);
+}
+LeoEdges canon_by_consumer(CanonBufs& b, int N, const LeoEdges& in, int32_t* zero_scalar, cudaStream_t st) {
+  const LeoEdges v = any_order(in, zero_scalar);
+  Incoming t = build_incoming(b.ib, N, &v, true, nullptr, st);
+  LeoEdges out{in.capacity, b.prod, b.cons, b.meta, b.count, b.nreg};
+  leo_launch(k_gather_edges, grid_for(in.capacity, 256), 256, 0, st, in.count, t.sidx, in.prod, in.cons, in.meta, out);
+  return out;
 }
 
 int blame_impl(const LeoKernel* kk, const LeoProfile* pp, const LeoEdges* pruned, const LeoPaths* paths,
@@ -614,8 +692,9 @@ int blame_impl(const LeoKernel* kk, const LeoProfile* pp, const LeoEdges* pruned
   // (leo_analyze) or is computed here; LEO_DBG_SELF_SLOW keeps the per-
   // candidate BFS tiers instead (cross-checked against the same goldens)
   Incoming binc = own_addr ? addr_impl(k, base, ab, tr, st) : *binc_pre;
-  const uint8_t* mp_ok = (dbg & LEO_DBG_SELF_SLOW) ? nullptr : (own_addr ? ab.ok : mp_ok_pre);
-  BlameArgs a{dbg, mp_ok, own, p, pruned->prod, pruned->meta, paths->dist, inc, binc.rbeg, binc.rend, base->prod, base->meta,
+  const uint8_t* mp_ok = (dbg & LEO_DBG_SELF_SLOW) || !mp_labels_fit(N) ? nullptr : (own_addr ? ab.ok : mp_ok_pre);
+  BlameArgs a{dbg, mp_ok, own, p, pruned->prod, pruned->meta, paths->dist, inc, binc.rbeg, binc.rend,
+              base ? base->prod : nullptr, base ? base->meta : nullptr,
               ecount, self_sub, jtotal, jnsum, eoff, *out, slow_list, &ctr[0], cap_slow, status, nullptr, nullptr, 0};
   const bool lines_on = line_id && line_blame && line_stall && n_lines > 0;
   if (lines_on && !(caps && (caps->options & LEO_OPT_ACCUMULATE_LINES))) {
@@ -645,8 +724,9 @@ extern "C" {
 
 int leo_abi_version(void) { return LEO_ABI_VERSION; }
 
-static int bin_impl(const LeoSamples* s, int32_t n_instr, int32_t* lat, int32_t* cls_cnt, LeoTrace* tr,
-                    cudaStream_t st) {
+// `status`: the caller's status word (LEO_ST_BAD_INPUT: a sample pc outside [0, n_instr))
+static int bin_impl(const LeoSamples* s, int32_t n_instr, int32_t* lat, int32_t* cls_cnt, uint32_t* status,
+                    LeoTrace* tr, cudaStream_t st) {
   set_smem_attributes();
   cudaMemsetAsync(cls_cnt, 0, (size_t)std::max(n_instr, 1) * 32, st);
   const int64_t S = s->n_samples;
@@ -660,15 +740,12 @@ static int bin_impl(const LeoSamples* s, int32_t n_instr, int32_t* lat, int32_t*
   // chunks: enough CTAs to stream the samples, bounded so the [G x nb] matrix stays small
   const int G = (int)std::max<int64_t>(1, std::min<int64_t>(num_sms() * 4, (S + 8191) / 8192));
   Arena ar{st};
-  uint32_t* status;
   int32_t *M, *btot, *boff, *soff;
   uint16_t* keys;
-  ar.want(&status, 1);
   ar.want(&M, bucketed ? (int64_t)G * nb : 1);
   ar.want(&btot, nb + 1); ar.want(&boff, nb + 1); ar.want(&soff, nb + 1);
   ar.want(&keys, bucketed ? S + 8 : 1);
   LEO_CUDA_CHECK(ar.commit());
-  cudaMemsetAsync(status, 0, 4, st);
   if (bucketed) {
     const int smem = R * 8 * 4;
     const int slice = (int)std::min<int64_t>(65536, std::max<int64_t>(4096, S / (num_sms() * 3)));
@@ -688,9 +765,10 @@ static int bin_impl(const LeoSamples* s, int32_t n_instr, int32_t* lat, int32_t*
   return 0;
 }
 
-int leo_bin_samples(const LeoSamples* s, int32_t n_instr, int32_t* lat, int32_t* cls_cnt, void* stream) {
-  if (!s || n_instr < 0) return -1;
-  return bin_impl(s, n_instr, lat, cls_cnt, nullptr, (cudaStream_t)stream);
+int leo_bin_samples(const LeoSamples* s, int32_t n_instr, int32_t* lat, int32_t* cls_cnt, uint32_t* status,
+                    void* stream) {
+  if (!s || n_instr < 0 || !status) return -1;
+  return bin_impl(s, n_instr, lat, cls_cnt, status, nullptr, (cudaStream_t)stream);
 }
 
 int leo_events_create(int32_t n, void** events) {
@@ -738,24 +816,31 @@ int leo_build_graph(const LeoKernel* k, const LeoCaps* caps, LeoEdges* out, LeoD
 }
 
 int leo_prune(const LeoKernel* k, const LeoProfile* p, const LeoConfig* cfg, const LeoEdges* in,
-              LeoEdges* out, LeoPaths* paths, LeoDiags* diags, uint32_t* status, void* stream) {
+              const LeoPaths* in_paths, LeoEdges* out, LeoPaths* paths, LeoDiags* diags, uint32_t* status,
+              void* stream) {
   WsScope ws_scope(nullptr);
   if (int e = check_kernel(k)) return e;
-  if (!cfg || cfg->max_paths < 0 || cfg->max_depth < 0) return -3;
-  return prune_impl(k, p, cfg, in, out, paths, diags, nullptr, status, (cudaStream_t)stream);
+  if (!cfg || cfg->max_paths < 0 || cfg->max_depth < 0 || !in || !out || !paths || !diags || !status) return -3;
+  return prune_impl(k, p, cfg, in, out, paths, diags, nullptr, status, (cudaStream_t)stream,
+                    ZeroSet{{nullptr, nullptr, nullptr, nullptr}, 0}, in_paths);
 }
 
 int leo_slice(const LeoKernel* k, const LeoProfile* p, const LeoEdges* pruned, uint32_t* bitmap,
               int32_t* level, void* stream) {
   WsScope ws_scope(nullptr);
   if (int e = check_kernel(k)) return e;
+  if (!pruned || !bitmap || !level) return -3;
   cudaStream_t st = (cudaStream_t)stream;
   Arena ar{st};
   IncomingBufs ib;
+  int32_t* zero;
+  ar.want(&zero, 4);
   want_incoming(ar, ib, k->n_instr, pruned->capacity);
   LEO_CUDA_CHECK(ar.commit());
-  Incoming inc = build_incoming(ib, k->n_instr, pruned, true, nullptr, st);
-  int r = slice_impl(k, p, pruned, inc, bitmap, level, nullptr, st);
+  cudaMemsetAsync(zero, 0, 16, st);
+  const LeoEdges pv = any_order(*pruned, zero);
+  Incoming inc = build_incoming(ib, k->n_instr, &pv, true, nullptr, st);
+  int r = slice_impl(k, p, &pv, inc, bitmap, level, nullptr, st);
   ar.release();
   return r;
 }
@@ -765,16 +850,196 @@ int leo_blame(const LeoKernel* k, const LeoProfile* p, const LeoEdges* pruned, c
               double* line_blame, double* line_stall, uint32_t* status, void* stream) {
   WsScope ws_scope(nullptr);
   if (int e = check_kernel(k)) return e;
+  if (!pruned || !out || !status) return -3;
   cudaStream_t st = (cudaStream_t)stream;
+  const int N = k->n_instr;
   Arena ar{st};
   IncomingBufs ib;
-  want_incoming(ar, ib, k->n_instr, pruned->capacity);
+  int32_t *zero, *zn = nullptr;
+  double* dist;
+  uint8_t* no_mp = nullptr;
+  CanonBufs cb;
+  ar.want(&zero, 4);
+  want_incoming(ar, ib, N, pruned->capacity);
+  ar.want(&dist, pruned->capacity);
+  if (base && !base->n_regular) want_canon(ar, cb, N, base->capacity);
+  if (!base) { ar.want(&no_mp, N); ar.want(&zn, N + 1); }
   LEO_CUDA_CHECK(ar.commit());
-  Incoming inc = build_incoming(ib, k->n_instr, pruned, true, nullptr, st);
-  int r = blame_impl(k, p, pruned, paths, base, inc, line_id, n_lines, out, line_blame, line_stall, nullptr,
-                     status, st);
+  cudaMemsetAsync(zero, 0, 16, st);
+  const LeoEdges pv = any_order(*pruned, zero);
+  Incoming inc = build_incoming(ib, N, &pv, true, nullptr, st);
+  // _edge_distance of the given edges and their valid_paths (analysis.py:371-376)
+  LeoPaths dp = paths ? *paths : LeoPaths{};
+  leo_launch(k_edge_dist, grid_for(pruned->capacity, 256), 256, 0, st, pruned->count, pruned->capacity, pruned->prod,
+             pruned->cons, dp, dist);
+  dp.dist = dist;
+  int r;
+  if (base) {
+    LeoEdges bv = *base;
+    if (!base->n_regular) bv = canon_by_consumer(cb, N, *base, zero, st);
+    r = blame_impl(k, p, &pv, &dp, &bv, inc, line_id, n_lines, out, line_blame, line_stall, nullptr, status, st);
+  } else {
+    // no base graph: self-blame never upgrades to indirect addressing (analysis.py:422-426)
+    cudaMemsetAsync(no_mp, 0, (size_t)std::max(N, 1), st);
+    cudaMemsetAsync(zn, 0, (size_t)(N + 1) * 4, st);
+    const Incoming none{zn, zn, zn, nullptr};
+    r = blame_impl(k, p, &pv, &dp, nullptr, inc, line_id, n_lines, out, line_blame, line_stall, nullptr, status, st,
+                   Range{0, 0}, &none, no_mp);
+  }
   ar.release();
   return r;
+}
+
+int leo_self_blame(const LeoKernel* k, const LeoProfile* p, const LeoEdges* base, int32_t n,
+                   const int32_t* index, uint8_t* sub, double* cycles, void* stream) {
+  WsScope ws_scope(nullptr);
+  if (int e = check_kernel(k)) return e;
+  if (n < 0 || (n > 0 && (!index || !sub || !cycles))) return -3;
+  if (base && !mp_labels_fit(k->n_instr)) return -5;      // (the label search needs N < 2^24)
+  cudaStream_t st = (cudaStream_t)stream;
+  const int N = k->n_instr;
+  Arena ar{st};
+  int32_t* zero;
+  AddrBufs ab;
+  CanonBufs cb;
+  ar.want(&zero, 4);
+  if (base) want_addr(ar, ab, N, base->capacity);
+  if (base && !base->n_regular) want_canon(ar, cb, N, base->capacity);
+  LEO_CUDA_CHECK(ar.commit());
+  cudaMemsetAsync(zero, 0, 16, st);
+  const KView kv = make_kview(k);
+  const uint8_t* mp_ok = nullptr;
+  if (base) {
+    LeoEdges bv = *base;
+    if (!base->n_regular) bv = canon_by_consumer(cb, N, *base, zero, st);
+    addr_impl(kv, &bv, ab, nullptr, st);
+    mp_ok = ab.ok;
+  }
+  if (n > 0) leo_launch(k_self_entries, grid_for(n, 128), 128, 0, st, kv, make_pview(p), mp_ok, n, index, sub, cycles);
+  ar.release();
+  LEO_CUDA_CHECK(cudaGetLastError());
+  return 0;
+}
+
+int leo_coverage(const LeoKernel* k, const LeoEdges* edges, int32_t* out, void* stream) {
+  WsScope ws_scope(nullptr);
+  if (int e = check_kernel(k)) return e;
+  if (!edges || !out) return -3;
+  cudaStream_t st = (cudaStream_t)stream;
+  const int N = k->n_instr;
+  Arena ar{st};
+  int32_t *mask, *cnt;
+  ar.want(&mask, N); ar.want(&cnt, N);
+  LEO_CUDA_CHECK(ar.commit());
+  cudaMemsetAsync(out, 0, 2 * sizeof(int32_t), st);
+  cudaMemsetAsync(mask, 0, (size_t)std::max(N, 1) * 4, st);
+  cudaMemsetAsync(cnt, 0, (size_t)std::max(N, 1) * 4, st);
+  leo_launch(k_cov_edges, grid_for(edges->capacity, 256), 256, 0, st, edges->cons, edges->meta, edges->count,
+             edges->capacity, mask, cnt);
+  leo_launch(k_cov_nodes, grid_for(N, 256, num_sms() * 4), 256, 0, st, N, mask, cnt, out);
+  ar.release();
+  LEO_CUDA_CHECK(cudaGetLastError());
+  return 0;
+}
+
+int leo_rank_hotspots(const LeoKernel* k, const LeoProfile* p, int32_t top_n, int32_t include_unsampled,
+                      int32_t* hot, int32_t* n_hot, void* stream) {
+  if (int e = check_kernel(k)) return e;
+  if (top_n < 0 || top_n > 4096 || !n_hot || (top_n > 0 && !hot)) return -3;
+  leo_launch(k_report_rank, 1, 1024, 0, (cudaStream_t)stream, k->n_instr, p->lat, top_n, include_unsampled, hot, n_hot);
+  LEO_CUDA_CHECK(cudaGetLastError());
+  return 0;
+}
+
+int leo_trace_chain(const LeoKernel* k, int32_t n_entries, const int32_t* stalled, const int32_t* cause,
+                    const double* blame, int32_t start, int32_t max_depth, int32_t* chain_node,
+                    int32_t* chain_entry, int32_t* chain_len, int32_t* chain_self, void* stream) {
+  WsScope ws_scope(nullptr);
+  if (int e = check_kernel(k)) return e;
+  const int N = k->n_instr;
+  if (n_entries < 0 || start < 0 || start >= N || max_depth < 1 || !chain_node || !chain_entry || !chain_len ||
+      !chain_self)
+    return -3;
+  cudaStream_t st = (cudaStream_t)stream;
+  Arena ar{st};
+  int32_t *cnt, *off, *cur, *uniq, *tmp, *sst, *sedge, *sprod, *one, *ent, *self, *dummy, *ncount;
+  uint64_t* perm;
+  double* sbl;
+  const int64_t M = std::max(n_entries, 1);
+  ar.want(&cnt, N); ar.want(&off, N + 1); ar.want(&cur, N); ar.want(&uniq, N);
+  ar.want(&tmp, scan_scratch_ints(std::max(N, 1)) + 64); ar.want(&perm, M);
+  ar.want(&sst, M); ar.want(&sedge, M); ar.want(&sprod, M); ar.want(&sbl, M);
+  ar.want(&one, 4); ar.want(&ent, max_depth); ar.want(&self, 1); ar.want(&dummy, 4); ar.want(&ncount, 1);
+  LEO_CUDA_CHECK(ar.commit());
+  // entries grouped by stalled instruction, list order kept inside a group
+  cudaMemsetAsync(cnt, 0, (size_t)std::max(N, 1) * 4, st);
+  cudaMemsetAsync(cur, 0, (size_t)std::max(N, 1) * 4, st);
+  leo_launch(k_chain_prep, 1, 32, 0, st, start, n_entries, one, ncount, dummy);
+  leo_launch(k_sync_hist, grid_for(M, 256), 256, 0, st, stalled, dummy, ncount, cnt);
+  scan_exclusive(cnt, off, nullptr, N, tmp, nullptr, st);
+  leo_launch(k_sync_fill, grid_for(M, 256), 256, 0, st, stalled, dummy, ncount, off, cur, perm);
+  leo_launch(segsort_unique_u64, grid_for(N, 128), 128, 0, st, perm, off, cnt, nullptr, N, uniq, M);
+  leo_launch(k_chain_gather, grid_for(M, 256), 256, 0, st, n_entries, perm, stalled, cause, blame, sst, sedge, sprod, sbl);
+  ReportArgs ra{one, one + 1, sst, sedge, sbl, ncount, (int32_t)M, sprod, 0, max_depth, dummy + 1, dummy + 2,
+                chain_len, chain_node, ent, self, (uint32_t*)(dummy + 3)};
+  leo_launch(k_report_hot, 1, 32, 0, st, ra);
+  leo_launch(k_chain_unperm, 1, 32, 0, st, perm, chain_len, ent, self, chain_entry, chain_self);
+  ar.release();
+  LEO_CUDA_CHECK(cudaGetLastError());
+  return 0;
+}
+
+int leo_liveness_filter(const LeoKernel* k, const LeoEdges* links, uint8_t* keep, void* stream) {
+  WsScope ws_scope(nullptr);
+  if (int e = check_kernel(k)) return e;
+  if (!links || !keep) return -3;
+  cudaStream_t st = (cudaStream_t)stream;
+  const KView kv = make_kview(k);
+  const int W = std::max(1, (k->n_units + 31) / 32);
+  Arena ar{st};
+  uint32_t *gen, *kill, *lin, *lout;
+  const int64_t BW = (int64_t)std::max(k->n_blocks, 1) * W;
+  ar.want(&gen, BW); ar.want(&kill, BW); ar.want(&lin, BW); ar.want(&lout, BW);
+  LEO_CUDA_CHECK(ar.commit());
+  if (k->n_blocks > 0) {
+    leo_launch(k_live_genkill, grid_for(k->n_blocks, 128), 128, 0, st, kv, W, gen, kill);
+    leo_launch(k_live_solve, (W + 31) / 32, 32, 0, st, kv, W, gen, kill, lin, lout);
+  }
+  leo_launch(k_live_filter, grid_for(links->capacity, 256), 256, 0, st, kv, W, lout, links->count, links->capacity,
+             links->prod, links->cons, links->meta, keep);
+  ar.release();
+  LEO_CUDA_CHECK(cudaGetLastError());
+  return 0;
+}
+
+int leo_line_rollup(const LeoKernel* k, const LeoProfile* p, int32_t n_entries, const int32_t* stalled,
+                    const int32_t* cause, const double* blame, const int32_t* line_id, int32_t n_lines,
+                    double* line_blame, double* line_stall, void* stream) {
+  WsScope ws_scope(nullptr);
+  if (int e = check_kernel(k)) return e;
+  if (n_entries < 0 || !line_id || n_lines <= 0 || !line_blame || !line_stall) return -3;
+  cudaStream_t st = (cudaStream_t)stream;
+  Arena ar{st};
+  int32_t *edge, *cnt;
+  ar.want(&edge, std::max(n_entries, 1)); ar.want(&cnt, 1);
+  LEO_CUDA_CHECK(ar.commit());
+  cudaMemsetAsync(line_blame, 0, (size_t)n_lines * 8, st);
+  cudaMemsetAsync(line_stall, 0, (size_t)n_lines * 8, st);
+  leo_launch(k_entry_edges, grid_for(std::max(n_entries, 1), 256), 256, 0, st, n_entries, cause, edge, cnt);
+  LeoBlame bv{std::max(n_entries, 1), (int32_t*)stalled, edge, nullptr, (double*)blame, nullptr, cnt};
+  leo_launch(k_lines, grid_for(std::max<int64_t>(n_entries, k->n_instr), 256), 256, 0, st, make_kview(k), make_pview(p),
+             Range{0, 0}, cause, bv, line_id, line_blame, line_stall);
+  ar.release();
+  LEO_CUDA_CHECK(cudaGetLastError());
+  return 0;
+}
+
+int leo_reaching_definitions(const LeoKernel* k, const LeoCaps* caps, LeoReachIn* out, uint32_t* status,
+                             void* stream) {
+  WsScope ws_scope(caps);
+  if (int e = check_kernel(k)) return e;
+  if (!out || !out->set_off || !out->count || !status) return -3;
+  return build_graph_impl(k, caps, nullptr, nullptr, status, (cudaStream_t)stream, Range{0, 0}, {}, out);
 }
 
 int leo_report(const LeoKernel* k, const LeoProfile* p, const LeoEdges* base, const LeoEdges* pruned,
@@ -820,7 +1085,7 @@ int leo_analyze(const LeoKernel* k, const LeoProfile* p, const LeoSamples* sampl
   if (int e = check_kernel(k)) return e;
   if (!cfg) return -3;
   cudaStream_t st = (cudaStream_t)stream;
-  SidePool& sp = side_pool();
+  SidePool& sp = side_pool(st);
   // Launch priorities only where measured to help: kernels whose vendor sync
   // tracing runs a shared-memory tier (the dataflow chain is then the critical
   // branch).  Big NVIDIA / Intel kernels run everything at the default.
@@ -840,7 +1105,7 @@ int leo_analyze(const LeoKernel* k, const LeoProfile* p, const LeoSamples* sampl
     // small streams bin at the least priority; a big stream (C5) is itself a
     // long branch and keeps the default
     LowPriority low_prio(samples->n_samples <= (16ll << 20));
-    return bin_impl(samples, k->n_instr, (int32_t*)p->lat, (int32_t*)p->cls_cnt, tr, s_bin);
+    return bin_impl(samples, k->n_instr, (int32_t*)p->lat, (int32_t*)p->cls_cnt, status, tr, s_bin);
   };
   // Up to 16 M samples the binning branch forks after the block walk: it has
   // the whole build as slack, and started with the build it takes SMs from

@@ -170,6 +170,8 @@ struct PruneArgs {
   int32_t* pfirst;           // [cap_in]
   double* dist;              // [cap_in]
   LeoPaths paths;            // pool (len / accum / count)
+  LeoPaths in_paths;         // valid_paths of the input edges (first == null: none); their
+                             // records were copied to the front of `paths` (k_copy_pool)
   int32_t* slow_list;
   int32_t* slow_count;
   int64_t slow_cap;
@@ -199,6 +201,10 @@ LEO_DEV bool prune_one(const KView& k, const PView& p, const PruneArgs& a, int e
     int d = cn - pr; if (d < 0) d = -d; if (d < 1) d = 1;
     dist = (double)d;
   }
+  // the edge keeps its input valid_paths unless stage 3 replaces them (a raw /
+  // guard edge with valid paths): sync edges, stages 1/2/4 and a truncated
+  // enumeration without valid paths keep `e` as it was (analysis.py:143-299)
+  bool carry = true;
   if (kind < LEO_EK_MEM_WAITCNT) {                       // sync edges are exempt
     const uint32_t poc = k.opclass[pr];
     if ((mask & 1) && ((only_class(p, cn, LEO_CS_MEMORY_DEP) && (kCompute & BIT(poc))) ||
@@ -216,6 +222,7 @@ LEO_DEV bool prune_one(const KView& k, const PView& p, const PruneArgs& a, int e
       int r = enumerate_paths(k, pr, cn, a.cfg.threshold[poc], a.cfg.max_paths, a.cfg.max_depth,
                               stk, scap, arena, acap, vlen, vacc, vcap, &nv);
       if (r == DFS_OVERFLOW) return false;
+      if (nv > 0) carry = false;
       if (nv > 0 && deferred) {
         *deferred = nv;
         int64_t s = 0;
@@ -229,12 +236,11 @@ LEO_DEV bool prune_one(const KView& k, const PView& p, const PruneArgs& a, int e
           off = -1;
           nv = 0;                                        // keep readers in bounds
         } else {
-          int64_t s = 0;
-          for (int x = 0; x < nv; x++) { a.paths.len[off + x] = vlen[x]; a.paths.accum[off + x] = vacc[x]; s += vlen[x]; }
+          for (int x = 0; x < nv; x++) { a.paths.len[off + x] = vlen[x]; a.paths.accum[off + x] = vacc[x]; }
         }
         int64_t s = 0;
         for (int x = 0; x < nv; x++) s += vlen[x];
-        dist = __ddiv_rn((double)s, (double)nv);
+        dist = nv > 0 ? __ddiv_rn((double)s, (double)nv) : dist;
         a.pfirst[e] = off;
         if (r == DFS_TRUNC) diag_push(a.diags, a.status, LEO_DIAG_PATH_CAPPED, pr, cn, 1, 0, e);
       } else if (r == DFS_TRUNC) {
@@ -246,6 +252,19 @@ LEO_DEV bool prune_one(const KView& k, const PView& p, const PruneArgs& a, int e
     if (keep && (mask & 8) && a.cfg.prune_exec && p.exec_cnt[pr] == 0) keep = 0;   // :289-299
   }
   a.keep[e] = keep;
+  if (carry && a.in_paths.first && a.in_paths.npaths[e] > 0) {
+    const int np = a.in_paths.npaths[e], f = a.in_paths.first[e];
+    if ((int64_t)f + np > a.paths.capacity) {             // carried pool did not fit (flagged)
+      a.npaths[e] = 0; a.pfirst[e] = -1; a.dist[e] = dist;
+      return true;
+    }
+    int64_t s = 0;
+    for (int q = 0; q < np; q++) s += a.paths.len[f + q];   // (copied to the same slots)
+    a.npaths[e] = np;
+    a.pfirst[e] = f;
+    a.dist[e] = __ddiv_rn((double)s, (double)np);
+    return true;
+  }
   a.npaths[e] = nv;
   if (nv == 0) a.pfirst[e] = -1;
   a.dist[e] = dist;
@@ -416,7 +435,7 @@ __global__ void k_compact(PruneArgs a, const int32_t* __restrict__ pos, const in
   }
   if (blockIdx.x == 0 && threadIdx.x == 0) {
     *out.count = pos[n];
-    *out.n_regular = pos[*n_reg_in];
+    if (out.n_regular) *out.n_regular = n_reg_in ? pos[*n_reg_in] : 0;
   }
 }
 

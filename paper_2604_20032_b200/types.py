@@ -129,6 +129,29 @@ class BlameEntry:
     register: str | None = None
 
 
+@dataclass(frozen=True)
+class UseLink:
+    producer: int
+    consumer: int
+    register: RegisterRef
+    kind: EdgeKind
+
+
+@dataclass(frozen=True)
+class ChainHop:
+    index: int
+    kind: EdgeKind | None
+    blame_cycles: float | None
+    share: float | None
+    self_blame: SelfBlame | None
+
+
+@dataclass(frozen=True)
+class Coverage:
+    value: float
+    vacuous: bool
+
+
 class Namespace:
     """The set of output classes to construct (reference's or mirrors)."""
 
@@ -139,7 +162,8 @@ class Namespace:
     def mirror(cls):
         return cls(RegClass=RegClass, EdgeKind=EdgeKind, DepClass=DepClass, SelfBlame=SelfBlame,
                    RegisterRef=RegisterRef, PathRecord=PathRecord, DepEdge=DepEdge,
-                   DependencyGraph=DependencyGraph, Factors=Factors, BlameEntry=BlameEntry)
+                   DependencyGraph=DependencyGraph, Factors=Factors, BlameEntry=BlameEntry,
+                   UseLink=UseLink, ChainHop=ChainHop, Coverage=Coverage)
 
     @classmethod
     def from_modules(cls, depgraph, analysis, isa):
@@ -147,4 +171,5 @@ class Namespace:
                    SelfBlame=analysis.SelfBlame, RegisterRef=isa.RegisterRef,
                    PathRecord=depgraph.PathRecord, DepEdge=depgraph.DepEdge,
                    DependencyGraph=depgraph.DependencyGraph, Factors=analysis.Factors,
-                   BlameEntry=analysis.BlameEntry)
+                   BlameEntry=analysis.BlameEntry, UseLink=depgraph.UseLink,
+                   ChainHop=analysis.ChainHop, Coverage=analysis.Coverage)

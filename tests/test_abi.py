@@ -25,7 +25,7 @@ def test_library_exports_every_declared_symbol():
             "leo_analyze", "leo_abi_version"} <= set(names)
     for n in names:
         assert hasattr(L, n), n
-    assert L.leo_abi_version() == 1
+    assert L.leo_abi_version() == 2
 
 
 def test_front_library_exports_every_declared_symbol():
@@ -62,13 +62,46 @@ def test_product_has_no_oracle_dependency():
         assert not pat.search(f.read_text()), f"product file {f} references the oracle"
 
 
-def test_soa_decode_encode_roundtrip():
-    """synthetic SoA -> reference-typed objects (mirror) -> SoA is the identity"""
+def _stalltrace():
+    import importlib
+    import sys
+    for p in (ROOT / "baseline" / "_ref", Path("/root/reference/pkg/src")):
+        if (p / "stalltrace").exists():
+            if str(p) not in sys.path:
+                sys.path.append(str(p))
+            return importlib.import_module("stalltrace")
     import pytest
-    st = pytest.importorskip("stalltrace") if False else None  # noqa: F841
-    from paper_2604_20032_b200 import synth
-    wl = synth.config_workload("c2", scale=0.02)
-    ks = wl.kernel
-    assert ks.opnd_ptr[-1] == ks.opnd.shape[0]
-    assert np.all(np.diff(ks.blk_first) > 0)
-    assert np.all(ks.block_of[ks.blk_first] == np.arange(ks.n_blocks))
+    pytest.skip("stalltrace not available")
+
+
+def test_soa_decode_encode_roundtrip():
+    """synthetic SoA -> the reference's own objects -> SoA is the identity
+    (kernel arrays, CFG, sync words, line keys, profile fields)."""
+    st = _stalltrace()
+    from paper_2604_20032_b200 import soa, synth
+    for tag in ("c2", "c3", "c5"):
+        wl = synth.config_workload(tag, scale=0.002 if tag == "c5" else 0.05)
+        ks, pf = wl.kernel, synth.bin_host(wl)
+        att = soa.decode_to_reference(ks, pf, st)
+        ks2, pf2 = soa.encode_attached(att)
+        for f in ("opclass", "block_of", "opnd_ptr", "sync_kind", "sync_a", "sync_b", "blk_first",
+                  "blk_last", "succ_ptr", "succ", "pred_ptr", "pred", "offset"):
+            assert np.array_equal(np.asarray(getattr(ks, f)), np.asarray(getattr(ks2, f))), (tag, f)
+        # operands: same records per instruction (the unit numbering may compact)
+        assert np.array_equal(ks.opnd & 0x1FFFFFFF, ks2.opnd & 0x1FFFFFFF) or \
+            np.array_equal(np.asarray(ks.opnd), np.asarray(ks2.opnd)), tag
+        keys = [ks.lines[i] for i in ks.line_id]
+        keys2 = [ks2.lines[i] for i in ks2.line_id]
+        assert keys == keys2, tag
+        for f in ("lat", "cls_cnt", "exec_cnt", "total", "eff", "sampled"):
+            assert np.array_equal(np.asarray(getattr(pf, f)), np.asarray(getattr(pf2, f))), (tag, f)
+        assert pf.period == pf2.period
+
+
+def test_entry_point_table_matches_header():
+    """the loader binds exactly the analysis entry points the header declares"""
+    from paper_2604_20032_b200 import _lib
+    names = set(declared_entry_points())
+    aux = {"leo_abi_version", "leo_debug_phases", "leo_debug_tiers", "leo_debug_items",
+           "leo_events_create", "leo_events_elapsed", "leo_events_destroy"}
+    assert set(_lib.ENTRY_POINTS) == names - aux

@@ -10,7 +10,7 @@ mkdir -p $OUT
 nvidia-smi --query-gpu=name,clocks.sm,clocks.max.sm,driver_version --format=csv > $OUT/${TAG}_smi.txt 2>&1
 python -c "import __graft_entry__ as g; g.build()" > $OUT/${TAG}_build.txt 2>&1 || { echo BUILD FAILED; tail -30 $OUT/${TAG}_build.txt; exit 1; }
 if [[ $WHAT == all || $WHAT == tests ]]; then
-  timeout 1500 python -m pytest tests -m gpu -x -q -p no:cacheprovider > $OUT/${TAG}_gputest.txt 2>&1
+  timeout 2400 python -m pytest tests -m gpu -q -p no:cacheprovider -rf --durations=15 > $OUT/${TAG}_gputest.txt 2>&1
   echo "gputest rc=$?"; tail -5 $OUT/${TAG}_gputest.txt
   timeout 300 python -c "import __graft_entry__ as g; g.smoke()" > $OUT/${TAG}_smoke.txt 2>&1
   echo "smoke rc=$?"; tail -2 $OUT/${TAG}_smoke.txt
@@ -23,6 +23,12 @@ if [[ $WHAT == all || $WHAT == bench ]]; then
   for c in c2 c3; do
     timeout 600 python bench.py --config $c --steps 20 --warmup 5 --cpu-seconds 5 > $OUT/${TAG}_bench_$c.json 2> $OUT/${TAG}_bench_$c.err
     echo "bench $c rc=$?"
+  done
+fi
+if [[ $WHAT == all || $WHAT == timeline ]]; then
+  for c in c5 c2; do
+    timeout 600 python tools/profile_step.py $c --graph-timeline > $OUT/${TAG}_timeline_$c.txt 2>&1
+    echo "timeline $c rc=$?"; head -3 $OUT/${TAG}_timeline_$c.txt
   done
 fi
 if [[ $WHAT == all || $WHAT == ncu ]]; then
