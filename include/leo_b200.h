@@ -216,6 +216,11 @@ typedef struct LeoBlame {
   double*  blame;             /* [cap] blame_cycles */
   double*  factors;           /* [cap*4] dist, eff, isu, match */
   int32_t* count;             /* device scalar */
+  /* optional (NULL: not written): the entry's cause instruction (-1 for
+   * self) and its edge's meta word (kind, dep class, register ref), so a
+   * service reads back self-contained entries without the pruned graph */
+  int32_t*  cause;            /* [cap] */
+  uint32_t* meta;             /* [cap] */
 } LeoBlame;
 
 /* ---- optional device-time trace ------------------------------------------
@@ -356,7 +361,7 @@ int leo_line_rollup(const LeoKernel* k, const LeoProfile* p, int32_t n_entries, 
 
 /* reaching_definitions(cfg) (depgraph.py:135-177): the reach-in set of every
  * (block b, unit u) pair, as the CSR defs[set_off[b*U+u] .. set_off[b*U+u+1])
- * (set order unspecified).  Two-phase: *count is the total even when it
+ * (set order unspecified; a def may be listed more than once).  Two-phase: *count is the total even when it
  * exceeds `capacity` (then LEO_ST_SCRATCH_OVERFLOW is set in *status). */
 typedef struct LeoReachIn {
   int64_t  capacity;          /* defs capacity */

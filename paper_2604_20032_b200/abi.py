@@ -86,7 +86,7 @@ class LeoDiags(C.Structure):
 
 class LeoBlame(C.Structure):
     _fields_ = [("capacity", C.c_int32), ("stalled", P), ("edge", P), ("sub", P),
-                ("blame", P), ("factors", P), ("count", P)]
+                ("blame", P), ("factors", P), ("count", P), ("cause", P), ("meta", P)]
 
 
 class LeoReport(C.Structure):

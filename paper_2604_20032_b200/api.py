@@ -708,12 +708,11 @@ class Session:
         # (the count is a device value); a longer result copies its tail
         nbl0 = int(an.counts()[device.C_BLAME])
         self.k_pre = min(cap, int(nbl0 * 1.1) + 256)
-        self.h_st = torch.empty(cap, dtype=torch.int32).pin_memory()
-        self.h_ed = torch.empty(cap, dtype=torch.int32).pin_memory()
-        self.h_bl = torch.empty(cap, dtype=torch.float64).pin_memory()
+        self.h_ent = {name: torch.empty(cap * w, dtype=getattr(an, src).dtype).pin_memory()
+                      for name, src, w in self.ENTRY_FIELDS}
         # numpy views of the pinned read-back buffers (no per-call tensor ops)
         self.n_ctr, self.n_lb, self.n_ls = self.h_ctr.numpy(), self.h_lb.numpy(), self.h_ls.numpy()
-        self.n_st, self.n_ed, self.n_bl = self.h_st.numpy(), self.h_ed.numpy(), self.h_bl.numpy()
+        self.n_ent = {name: t.numpy() for name, t in self.h_ent.items()}
         g = torch.cuda.CUDAGraph()
         side = torch.cuda.Stream(self.dev)
         side.wait_stream(torch.cuda.current_stream(self.dev))
@@ -724,19 +723,38 @@ class Session:
             self.h_ctr.copy_(an.ctr, non_blocking=True)
             self.h_lb.copy_(an.line_blame, non_blocking=True)
             self.h_ls.copy_(an.line_stall, non_blocking=True)
-            k = self.k_pre
-            self.h_st[:k].copy_(an.bl_stalled[:k], non_blocking=True)
-            self.h_ed[:k].copy_(an.bl_edge[:k], non_blocking=True)
-            self.h_bl[:k].copy_(an.bl_blame[:k], non_blocking=True)
+            self._copy_entries(0, self.k_pre)
         torch.cuda.synchronize(self.dev)
         self.graph = g
 
+    # self-contained blame entries read back per call: stalled, cause (-1 =
+    # self), the cause edge's meta word (kind, dep class, register), SelfBlame
+    # subcategory, blame cycles and the four Eq. 1 factors (53 bytes each)
+    ENTRY_FIELDS = (("e_stalled", "bl_stalled", 1), ("e_cause", "bl_cause", 1), ("e_meta", "bl_meta", 1),
+                    ("e_sub", "bl_sub", 1), ("e_blame", "bl_blame", 1), ("e_factors", "bl_factors", 4))
+
+    def _copy_entries(self, lo, hi):
+        for name, src, w in self.ENTRY_FIELDS:
+            self.h_ent[name][lo * w:hi * w].copy_(getattr(self.an, src)[lo * w:hi * w], non_blocking=True)
+
+    def _entry_bytes(self, n):
+        return sum(n * w * self.h_ent[name].element_size() for name, _, w in self.ENTRY_FIELDS)
+
+    def _result(self, ent, nbl, lb, ls):
+        out = {name: ent[name][:nbl * w].copy() for name, _, w in self.ENTRY_FIELDS}
+        out["e_meta"] = out["e_meta"].view(np.uint32)
+        out["e_factors"] = out["e_factors"].reshape(-1, 4)
+        out["line_blame"], out["line_stall"] = lb, ls
+        return out
+
     def analyze(self, allreduce=None):
-        """Copy staged inputs in, run, copy results out.  Returns host dict.
-        `allreduce(line_blame, line_stall)` (multi-GPU) runs on the device line
-        vectors before they are read back.  Single-GPU calls replay one CUDA
-        graph (H2D + pipeline + D2H of counters and line vectors); the blame
-        entries are then read back at their device-reported count."""
+        """Copy staged inputs in, run, copy results out.  Returns a host dict
+        of self-contained blame entries (e_stalled, e_cause, e_meta, e_sub,
+        e_blame, e_factors) and the per-line vectors.  `allreduce(line_blame,
+        line_stall)` (multi-GPU) runs on the device line vectors before they
+        are read back.  Single-GPU calls replay one CUDA graph (H2D + pipeline
+        + D2H of counters, line vectors and the entries' expected prefix); the
+        rest of the entries is read back at the device-reported count."""
         if allreduce is None and self.use_graph:
             if getattr(self, "graph", None) is None:
                 self._capture()
@@ -745,39 +763,32 @@ class Session:
             c = self.n_ctr
             nbl = int(c[device.C_BLAME])
             if c[device.C_STATUS] == 0 and nbl <= self.an.caps.blame:
-                an, k = self.an, self.k_pre
-                if nbl > k:                       # tail beyond the in-graph prefix
-                    self.h_st[k:nbl].copy_(an.bl_stalled[k:nbl], non_blocking=True)
-                    self.h_ed[k:nbl].copy_(an.bl_edge[k:nbl], non_blocking=True)
-                    self.h_bl[k:nbl].copy_(an.bl_blame[k:nbl], non_blocking=True)
+                if nbl > self.k_pre:              # tail beyond the in-graph prefix
+                    self._copy_entries(self.k_pre, nbl)
                     torch.cuda.current_stream(self.dev).synchronize()
                 self.last_d2h = (c.nbytes + self.h_lb.numel() * 8 + self.h_ls.numel() * 8
-                                 + max(nbl, self.k_pre) * 16)
-                return {"e_stalled": self.n_st[:nbl].copy(), "e_edge": self.n_ed[:nbl].copy(),
-                        "e_blame": self.n_bl[:nbl].copy(), "line_blame": self.n_lb.copy(),
-                        "line_stall": self.n_ls.copy()}
+                                 + self._entry_bytes(max(nbl, self.k_pre)))
+                return self._result(self.n_ent, nbl, self.n_lb.copy(), self.n_ls.copy())
             self.graph = None                  # overflow: grow eagerly, recapture next call
         self._h2d()
         self.an.launch(self.dp, self.cfg, self.ds)
         c = self.an.ctr.cpu().numpy()          # sync: how much to read back
         self.an.ensure_workspace()             # persistent scratch for the next call
         nbl = min(int(c[device.C_BLAME]), self.an.caps.blame)
-        if nbl > self.an.caps.blame or c[device.C_STATUS] != 0:
+        if int(c[device.C_BLAME]) > self.an.caps.blame or c[device.C_STATUS] != 0:
             self.an.run(self.dp, self.cfg, self.ds)
             c = self.an.ctr.cpu().numpy()
             nbl = int(c[device.C_BLAME])
         if allreduce is not None:
             allreduce(self.an.line_blame, self.an.line_stall)
-        out = {
-            "e_stalled": self.an.bl_stalled[:nbl].to("cpu", non_blocking=True),
-            "e_edge": self.an.bl_edge[:nbl].to("cpu", non_blocking=True),
-            "e_blame": self.an.bl_blame[:nbl].to("cpu", non_blocking=True),
-            "line_blame": self.an.line_blame.to("cpu", non_blocking=True),
-            "line_stall": self.an.line_stall.to("cpu", non_blocking=True),
-        }
+        ent = {name: getattr(self.an, src)[:nbl * w].to("cpu", non_blocking=True)
+               for name, src, w in self.ENTRY_FIELDS}
+        lb = self.an.line_blame.to("cpu", non_blocking=True)
+        ls = self.an.line_stall.to("cpu", non_blocking=True)
         torch.cuda.current_stream(self.dev).synchronize()
-        self.last_d2h = sum(t.numel() * t.element_size() for t in out.values()) + c.nbytes
-        return {k: v.numpy() for k, v in out.items()}
+        self.last_d2h = (sum(t.numel() * t.element_size() for t in ent.values()) + c.nbytes
+                         + lb.numel() * 8 + ls.numel() * 8)
+        return self._result({k: v.numpy() for k, v in ent.items()}, nbl, lb.numpy(), ls.numpy())
 
 
 # --------------------------------------------------------------------------

@@ -62,6 +62,73 @@ __global__ void k_bin_samples(int64_t S, const int32_t* __restrict__ pc, const u
   }
 }
 
+// ---- stage 0, one pass: every CTA streams a contiguous chunk of the samples
+// (16-byte pc / 4-byte category loads) and counts (pc * 8 + class) keys in a
+// private open-addressing hash in shared memory.  Zipf-hot keys occupy the table early and are counted
+// on chip; a key that finds no slot within kBinProbe probes (the cold tail) is
+// added to cls_cnt in L2 directly.  The table is flushed with one global atomic
+// per occupied slot.  One read of the 5 bytes per sample (vs the bucketed
+// passes' hist + scatter + count: ~3 reads and a key write).
+constexpr int kBinHashSlots = 8192, kBinProbe = 8;
+constexpr uint32_t kBinEmpty = 0xFFFFFFFFu;
+
+__global__ void __launch_bounds__(512) k_bin_hash(int64_t S, const int32_t* __restrict__ pc,
+                                                  const uint8_t* __restrict__ cat,
+                                                  const uint8_t* __restrict__ lut, int N,
+                                                  int32_t* __restrict__ cls_cnt, uint32_t* status) {
+  pdl_wait();
+  extern __shared__ uint32_t hsh[];
+  uint32_t* keys = hsh;
+  uint32_t* cnts = hsh + kBinHashSlots;
+  __shared__ uint8_t slut[256];
+  for (int x = threadIdx.x; x < 256; x += blockDim.x) slut[x] = lut[x];
+  for (int x = threadIdx.x; x < kBinHashSlots; x += blockDim.x) { keys[x] = kBinEmpty; cnts[x] = 0u; }
+  __syncthreads();
+  // this CTA's chunk, in whole 4-sample vectors
+  const int64_t nvec = S / 4;
+  const int64_t per = (nvec + gridDim.x - 1) / gridDim.x;
+  const int64_t v0 = blockIdx.x * per, v1 = min(nvec, v0 + per);
+  const int4* pc4 = reinterpret_cast<const int4*>(pc);
+  const uint32_t* cat4 = reinterpret_cast<const uint32_t*>(cat);
+  // (no warp aggregation: __match_any_sync cost more than the shared-memory
+  // atomics it saves; a hot key's lanes serialise only on their shared counter)
+  auto count = [&](uint32_t key, bool ok) {
+    if (!ok) return;
+    uint32_t h = (key * 2654435761u) >> 19;              // 13 bits
+    for (int probe = 0; probe < kBinProbe; probe++, h = (h + 1) & (kBinHashSlots - 1)) {
+      uint32_t k0 = keys[h];
+      if (k0 == kBinEmpty) k0 = atomicCAS(&keys[h], kBinEmpty, key);
+      if (k0 == kBinEmpty || k0 == key) { atomicAdd(&cnts[h], 1u); return; }
+    }
+    atomicAdd(&cls_cnt[key], 1);                         // cold key: straight to L2
+  };
+  for (int64_t v = v0 + threadIdx.x; v - threadIdx.x < v1; v += blockDim.x) {
+    const bool valid = v < v1;
+    const int4 p = valid ? pc4[v] : make_int4(0, 0, 0, 0);
+    const uint32_t c = valid ? cat4[v] : 0u;
+    const int pcs[4] = {p.x, p.y, p.z, p.w};
+#pragma unroll
+    for (int t = 0; t < 4; t++) {
+      const int j = pcs[t];
+      const bool ok = valid && j >= 0 && j < N;
+      if (valid && !ok) atomicOr(status, (uint32_t)LEO_ST_BAD_INPUT);
+      count(ok ? (uint32_t)j * 8u + slut[(c >> (8 * t)) & 0xFF] : 0u, ok);
+    }
+  }
+  // tail samples (S mod 4): the last CTA
+  if (blockIdx.x == gridDim.x - 1) {
+    const int64_t s = nvec * 4 + threadIdx.x;
+    const bool in = s < S;
+    const int j = in ? pc[s] : 0;
+    const bool ok = in && j >= 0 && j < N;
+    if (in && !ok) atomicOr(status, (uint32_t)LEO_ST_BAD_INPUT);
+    count(ok ? (uint32_t)j * 8u + slut[cat[s]] : 0u, ok);
+  }
+  __syncthreads();
+  for (int x = threadIdx.x; x < kBinHashSlots; x += blockDim.x)
+    if (keys[x] != kBinEmpty) atomicAdd(&cls_cnt[keys[x]], (int)cnts[x]);
+}
+
 // ---- stage 0, bucketed: samples are partitioned by pc / R into NB buckets
 // (R instructions x 8 classes of u32 counters fit in shared memory), packed to
 // u16 keys ((pc mod R) * 8 + class), then each (bucket, slice) is counted in
@@ -626,6 +693,7 @@ LEO_DEV bool blame_one(const KView& k, const BlameArgs& a, int j) {
       if (o + 1 > a.out.capacity) { atomicOr(a.status, (uint32_t)LEO_ST_BLAME_OVERFLOW); return false; }
       a.out.stalled[o] = j;
       a.out.edge[o] = -1;
+      if (a.out.cause) { a.out.cause[o] = -1; a.out.meta[o] = 0u; }
       a.out.sub[o] = (uint8_t)a.self_sub[j];
       a.out.blame[o] = s_j;
       for (int c = 0; c < 4; c++) a.out.factors[(size_t)o * 4 + c] = 0.0;
@@ -670,6 +738,7 @@ LEO_DEV bool blame_one(const KView& k, const BlameArgs& a, int j) {
               const int x = o + x0 + u;
               a.out.stalled[x] = j;
               a.out.edge[x] = eb.e[u];
+              if (a.out.cause) { a.out.cause[x] = eb.pr[u]; a.out.meta[x] = a.pmeta[eb.e[u]]; }
               a.out.sub[x] = 255;
               a.out.blame[x] = __ddiv_rn(__dmul_rn(s_j, prod), total);
               double* f = a.out.factors + (size_t)x * 4;
@@ -754,6 +823,7 @@ LEO_DEV void blame_warp(const KView& k, const BlameArgs& a, int j, int lane) {
         const int w = o + x;
         a.out.stalled[w] = j;
         a.out.edge[w] = e;
+        if (a.out.cause) { a.out.cause[w] = pr; a.out.meta[w] = a.pmeta[e]; }
         a.out.sub[w] = 255;
         a.out.blame[w] = __ddiv_rn(__dmul_rn(s_j, prod), total);
         double* f = a.out.factors + (size_t)w * 4;
@@ -927,34 +997,48 @@ struct SliceArgs {
   uint32_t* bitmap;
 };
 
+// Appends of newly levelled nodes to the next frontier: one atomic per
+// coalesced group of lanes (a per-node atomic on the one frontier counter
+// serialised ~1 M sources at C5).
+LEO_DEV void slice_push(int32_t* nxt, int32_t* count, int p) {
+  cg::coalesced_group g = cg::coalesced_threads();
+  int base = 0;
+  if (g.thread_rank() == 0) base = atomicAdd(count, (int)g.size());
+  base = g.shfl(base, 0);
+  nxt[base + g.thread_rank()] = p;
+}
+
+// level lv for every unlevelled producer of node v's incoming (pruned) edges
+LEO_DEV void slice_expand(const SliceArgs& a, int v, int lv, int32_t* nxt, int32_t* count) {
+  const int r0 = a.inc.rbeg[v], nr = a.inc.rend[v] - r0, s0 = a.inc.soff[v];
+  const int deg = nr + (a.inc.soff[v + 1] - s0);
+  for (int x = 0; x < deg; x++) {
+    const int e = x < nr ? r0 + x : (int)a.inc.sidx[s0 + (x - nr)];
+    const int p = a.pprod[e];
+    if (a.level[p] < 0 && atomicCAS(&a.level[p], -1, lv) == -1) slice_push(nxt, count, p);
+  }
+}
+
+// Level-synchronous BFS in one cooperative kernel, thread per frontier node
+// (pruned in-degrees are small: 0.19 per instruction at C5).  Level 0 is every
+// instruction with S_j > 0; level 1 expands them straight from lat[] (no
+// level-0 frontier list: at C5 that is ~1 M nodes).
 __global__ void k_slice(int N, SliceArgs a) {
   pdl_wait();
   cg::grid_group grid = cg::this_grid();
   const int tid = blockIdx.x * blockDim.x + threadIdx.x, nt = gridDim.x * blockDim.x;
   if (tid == 0) { a.counts[0] = 0; a.counts[1] = 0; }
+  for (int j = tid; j < N; j += nt) a.level[j] = a.lat[j] != 0 ? 0 : -1;
   grid.sync();
-  for (int j = tid; j < N; j += nt) {
-    bool src = a.lat[j] != 0;
-    a.level[j] = src ? 0 : -1;
-    if (src) a.fa[atomicAdd(&a.counts[0], 1)] = j;
-  }
+  for (int j = tid; j < N; j += nt)
+    if (a.lat[j] != 0) slice_expand(a, j, 1, a.fa, &a.counts[0]);
   grid.sync();
   int32_t *cur = a.fa, *nxt = a.fb;
   int ci = 0;
-  for (int lv = 1;; lv++) {
+  for (int lv = 2;; lv++) {
     const int n = a.counts[ci];
     if (n == 0) break;
-    // warp-cooperative expansion: one warp per frontier node
-    const int lane = threadIdx.x & 31, gw = tid >> 5, nw = nt >> 5;
-    for (int f = gw; f < n; f += nw) {
-      const int v = cur[f];
-      const int deg = a.inc.deg(v);
-      for (int x = lane; x < deg; x += 32) {
-        const int p = a.pprod[a.inc.edge(v, x)];
-        if (a.level[p] < 0 && atomicCAS(&a.level[p], -1, lv) == -1)
-          nxt[atomicAdd(&a.counts[ci ^ 1], 1)] = p;
-      }
-    }
+    for (int f = tid; f < n; f += nt) slice_expand(a, cur[f], lv, nxt, &a.counts[ci ^ 1]);
     grid.sync();
     if (tid == 0) a.counts[ci] = 0;
     int32_t* t = cur; cur = nxt; nxt = t;

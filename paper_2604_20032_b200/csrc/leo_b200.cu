@@ -212,6 +212,7 @@ void set_smem_attributes() {
   if (done_mask & bit) return;
   cudaFuncSetAttribute(k_reach_fast, cudaFuncAttributeMaxDynamicSharedMemorySize, kT1Threads * kT1Hash * 4);
   cudaFuncSetAttribute(k_bin_count, cudaFuncAttributeMaxDynamicSharedMemorySize, kBinRMax * 8 * 4);
+  cudaFuncSetAttribute(k_bin_hash, cudaFuncAttributeMaxDynamicSharedMemorySize, kBinHashSlots * 8);
   cudaFuncSetAttribute(k_bin_scatter, cudaFuncAttributeMaxDynamicSharedMemorySize, kBinMaxBuckets * 12 + kBinSub * 4);
   cudaFuncSetAttribute(k_block_walk, cudaFuncAttributeMaxDynamicSharedMemorySize, 96 * 1024);
   cudaFuncSetAttribute(k_sync_wc_warp, cudaFuncAttributeMaxDynamicSharedMemorySize, 4 * kWcSmemInts * 4);
@@ -511,7 +512,13 @@ int prune_impl(const LeoKernel* kk, const LeoProfile* pp, const LeoConfig* cfg, 
   ar.want(&pos, cap_in + 1); ar.want(&slow_list, cap_slow); ar.want(&ctr, 4);
   ar.want(&scan_tmp, scan_scratch_ints(cap_in) + 64); ar.want(&slow_scr, (int64_t)PW * pslow);
   (void)n_reg_in;
+  // nvidia issue weights vary: straight runs are resolved through per-block prefix sums
+  const bool weighted = kk->dialect == LEO_NVIDIA && (cfg->stage_mask & 4) && !getenv("LEO_PRUNE_NO_WPRE");
+  double* wpre = nullptr;
+  if (weighted) ar.want(&wpre, std::max(kk->n_instr, 1));
   LEO_CUDA_CHECK(ar.commit());
+  if (weighted && kk->n_blocks > 0)
+    leo_launch(k_weight_prefix, grid_for(kk->n_blocks, 128), 128, 0, st, k, wpre);
   cudaMemsetAsync(ctr, 0, 4 * sizeof(int32_t), st);
   LeoPaths inp{};
   if (in_paths && in_paths->first) {
@@ -521,7 +528,7 @@ int prune_impl(const LeoKernel* kk, const LeoProfile* pp, const LeoConfig* cfg, 
     cudaMemsetAsync(paths->count, 0, sizeof(int32_t), st);
   }
   PruneArgs a{caps ? caps->debug_flags : 0, *cfg, in->prod, in->cons, in->meta, in->count, (int32_t)cap_in, keep, npaths, pfirst, dist,
-              *paths, inp, slow_list, &ctr[0], cap_slow, *diags, status};
+              *paths, wpre, inp, slow_list, &ctr[0], cap_slow, *diags, status};
   {
     const int dbg = caps ? caps->debug_flags : 0;
     const char* pt_env = getenv("LEO_PRUNE_THREADS");
@@ -734,6 +741,15 @@ static int bin_impl(const LeoSamples* s, int32_t n_instr, int32_t* lat, int32_t*
     LEO_CUDA_CHECK(cudaMemcpyAsync((void*)s->pc, s->pc_host, (size_t)S * 4, cudaMemcpyHostToDevice, st));
   if (S > 0 && s->cat_host)
     LEO_CUDA_CHECK(cudaMemcpyAsync((void*)s->cat, s->cat_host, (size_t)S, cudaMemcpyHostToDevice, st));
+  // big streams: one pass, per-CTA shared-memory hash (LEO_BIN_BUCKETED=1: the bucketed passes)
+  if (S >= (4ll << 20) && (int64_t)n_instr * 8 < 0xFFFFFFFFll && !getenv("LEO_BIN_BUCKETED")) {
+    const int G = num_sms() * 3;
+    TRACED(KID_BIN, leo_launch(k_bin_hash, G, 512, (size_t)kBinHashSlots * 8, st, S, s->pc, s->cat, s->cat_to_cs,
+                               n_instr, cls_cnt, status));
+    TRACED(KID_BIN_FINALIZE, leo_launch(k_bin_finalize, grid_for(n_instr, 256), 256, 0, st, n_instr, cls_cnt, lat));
+    LEO_CUDA_CHECK(cudaGetLastError());
+    return 0;
+  }
   const int R = (n_instr + kBinR - 1) / kBinR <= kBinMaxBuckets ? kBinR : kBinRMax;
   const int nb = std::max(1, (n_instr + R - 1) / R);
   const bool bucketed = nb <= kBinMaxBuckets && S > 0;
@@ -1113,7 +1129,10 @@ int leo_analyze(const LeoKernel* k, const LeoProfile* p, const LeoSamples* sampl
   // need the whole build to hide in.
   // (a stream still in host memory forks at once: its transfer needs the
   // whole build to hide in)
-  const bool late_bin = samples && samples->n_samples <= (16ll << 20) && !samples->pc_host;
+  // (the one-pass hashed binning of big streams is short enough to fork late too;
+  // LEO_BIN_EARLY=1 forks it at the start)
+  const bool late_bin = samples && !samples->pc_host && !getenv("LEO_BIN_EARLY") &&
+                        (samples->n_samples <= (16ll << 20) || !getenv("LEO_BIN_BUCKETED"));
   if (!late_bin) {
     if (int e = enqueue_bin()) return e;
   }

@@ -60,9 +60,14 @@ enum { DFS_OK = 0, DFS_TRUNC = 1, DFS_OVERFLOW = 2 };
 
 // Exact emulation of _enumerate_paths.  Returns DFS_OK / DFS_TRUNC, or
 // DFS_OVERFLOW when a caller buffer was too small (caller re-runs elsewhere).
+// `wpre` (nvidia, may be null): per-instruction prefix sums of the issue
+// weights within each block (wpre[i] = w[first(b)] + ... + w[i]), so straight
+// runs resolve in closed form with weights too (integer-valued doubles: the
+// differences are exact, as the step-by-step sums are).
 LEO_DEV int enumerate_paths(const KView& k, int producer, int consumer, double thr, int max_paths,
                             int max_depth, DfsEnt* stk, int scap, BackNode* arena, int acap,
-                            int32_t* vlen, double* vacc, int vcap, int* nvalid_out) {
+                            int32_t* vlen, double* vacc, int vcap, int* nvalid_out,
+                            const double* __restrict__ wpre = nullptr) {
   int budget = 65536, truncated = 0, sp = 0, na = 0, nv = 0;
   *nvalid_out = 0;
   const double w0 = issue_weight(k, producer);
@@ -74,7 +79,7 @@ LEO_DEV int enumerate_paths(const KView& k, int producer, int consumer, double t
     if (budget <= 0 || nv >= max_paths) { truncated = 1; break; }
     budget--;
     const int nb = k.block_of[e.node];
-    if (unit_w && e.node < k.blk_last[nb]) {
+    if ((unit_w || wpre) && e.node < k.blk_last[nb]) {
       // Straight run e.node+1 .. blk_last: each step pushes its successor and
       // the LIFO pops it right back, so the run is a sequence of consecutive
       // pops that can be resolved in closed form.  Step i reaches node
@@ -85,12 +90,23 @@ LEO_DEV int enumerate_paths(const KView& k, int producer, int consumer, double t
       const int i_end = L - x;
       const int i_c = (consumer > x && consumer <= L) ? consumer - x : 0x7fffffff;
       int i_thr;
-      {
+      if (unit_w) {
         const double f = thr - e.acc;
         i_thr = f < 0.0 ? 1 : (f > 1e9 ? 0x3fffffff : (int)floor(f) + 1);
         while (i_thr > 1 && __dadd_rn(e.acc, (double)(i_thr - 1)) > thr) i_thr--;
         while (i_thr < 0x3fffffff && !(__dadd_rn(e.acc, (double)i_thr) > thr)) i_thr++;
+      } else {
+        // first step i in [1, i_end] whose accumulation exceeds thr (weights
+        // are >= 0: monotone), else past the run
+        const double w0 = wpre[x];
+        int lo = 1, hi = i_end + 1;
+        while (lo < hi) {
+          const int mid = (lo + hi) >> 1;
+          if (__dadd_rn(e.acc, __dsub_rn(wpre[x + mid], w0)) > thr) hi = mid; else lo = mid + 1;
+        }
+        i_thr = lo <= i_end ? lo : 0x3fffffff;
       }
+      const double wrun = unit_w ? 0.0 : wpre[x];
       const int i_dep = max(1, max_depth - e.len);
       const int i_stop = min(i_c, min(i_thr, i_dep));
       if (i_stop <= i_end) {
@@ -99,7 +115,9 @@ LEO_DEV int enumerate_paths(const KView& k, int producer, int consumer, double t
         budget -= need;
         if (i_stop == i_c) {
           if (nv == vcap) return DFS_OVERFLOW;
-          vlen[nv] = e.len + i_c - 1; vacc[nv] = __dadd_rn(e.acc, (double)(i_c - 1)); nv++;
+          vlen[nv] = e.len + i_c - 1;
+          vacc[nv] = __dadd_rn(e.acc, unit_w ? (double)(i_c - 1) : __dsub_rn(wpre[x + i_c - 1], wrun));
+          nv++;
           if (nv >= max_paths) truncated = 1;
         } else if (i_stop != i_thr) {
           truncated = 1;                              // max_depth
@@ -108,7 +126,8 @@ LEO_DEV int enumerate_paths(const KView& k, int producer, int consumer, double t
       }
       if (budget < i_end) { budget = 0; truncated = 1; break; }
       budget -= i_end;
-      e.node = L; e.len += i_end; e.acc = __dadd_rn(e.acc, (double)i_end);
+      e.node = L; e.len += i_end;
+      e.acc = __dadd_rn(e.acc, unit_w ? (double)i_end : __dsub_rn(wpre[L], wrun));
     }
     int succ_n, s0 = -1, s1 = -1;
     if (e.node < k.blk_last[nb]) { succ_n = 1; s0 = e.node + 1; }
@@ -157,6 +176,15 @@ LEO_DEV int enumerate_paths(const KView& k, int producer, int consumer, double t
   return truncated ? DFS_TRUNC : DFS_OK;
 }
 
+// wpre[i] = issue weights of first(block_of(i)) .. i (thread per block)
+__global__ void k_weight_prefix(KView k, double* __restrict__ wpre) {
+  pdl_wait();
+  for (int b = blockIdx.x * blockDim.x + threadIdx.x; b < k.B; b += gridDim.x * blockDim.x) {
+    double s = 0.0;
+    for (int i = k.blk_first[b]; i <= k.blk_last[b]; i++) { s = __dadd_rn(s, issue_weight(k, i)); wpre[i] = s; }
+  }
+}
+
 struct PruneArgs {
   int32_t dbg;
   LeoConfig cfg;
@@ -170,6 +198,7 @@ struct PruneArgs {
   int32_t* pfirst;           // [cap_in]
   double* dist;              // [cap_in]
   LeoPaths paths;            // pool (len / accum / count)
+  const double* wpre;        // nvidia: per-block prefix sums of the issue weights (null: unit weights)
   LeoPaths in_paths;         // valid_paths of the input edges (first == null: none); their
                              // records were copied to the front of `paths` (k_copy_pool)
   int32_t* slow_list;
@@ -220,7 +249,7 @@ LEO_DEV bool prune_one(const KView& k, const PView& p, const PruneArgs& a, int e
     }
     if (keep && (mask & 4)) {                            // prune_latency :256-286
       int r = enumerate_paths(k, pr, cn, a.cfg.threshold[poc], a.cfg.max_paths, a.cfg.max_depth,
-                              stk, scap, arena, acap, vlen, vacc, vcap, &nv);
+                              stk, scap, arena, acap, vlen, vacc, vcap, &nv, a.wpre);
       if (r == DFS_OVERFLOW) return false;
       if (nv > 0) carry = false;
       if (nv > 0 && deferred) {

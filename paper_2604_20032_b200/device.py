@@ -152,6 +152,7 @@ class Analyzer:
         self.pa_acc = torch.empty(max(c.paths, 1), dtype=torch.float64, device=d)
         self.diag = i32(6 * c.diags)
         self.bl_stalled, self.bl_edge = i32(c.blame), i32(c.blame)
+        self.bl_cause, self.bl_meta = i32(c.blame), i32(c.blame)
         self.bl_sub = torch.empty(max(c.blame, 1), dtype=torch.uint8, device=d)
         self.bl_blame = torch.empty(max(c.blame, 1), dtype=torch.float64, device=d)
         self.bl_factors = torch.empty(max(4 * c.blame, 1), dtype=torch.float64, device=d)
@@ -172,7 +173,8 @@ class Analyzer:
                                     ptr(self.pa_len), ptr(self.pa_acc), at(C_PATHS))
         self.s_diags = abi.LeoDiags(c.diags, ptr(self.diag), at(C_DIAGS))
         self.s_blame = abi.LeoBlame(c.blame, ptr(self.bl_stalled), ptr(self.bl_edge), ptr(self.bl_sub),
-                                    ptr(self.bl_blame), ptr(self.bl_factors), at(C_BLAME))
+                                    ptr(self.bl_blame), ptr(self.bl_factors), at(C_BLAME),
+                                    ptr(self.bl_cause), ptr(self.bl_meta))
         s = self.caps.scratch_scale
         nu, n = self.n_use_units, self.dk.n_instr
         self.s_caps = abi.LeoCaps((4 * nu + 1024) * s, (6 * nu + 1024) * s, (2 * n + 1024) * s,
@@ -310,6 +312,7 @@ class Analyzer:
             plen=h(self.pa_len, npa), pacc=h(self.pa_acc, npa),
             diag_records=h(self.diag, 6 * nd).reshape(-1, 6),
             e_stalled=h(self.bl_stalled, nbl), e_edge=h(self.bl_edge, nbl),
+            e_cause=h(self.bl_cause, nbl), e_meta=h(self.bl_meta, nbl).view(np.uint32),
             e_sub=h(self.bl_sub, nbl), e_blame=h(self.bl_blame, nbl),
             e_factors=h(self.bl_factors, 4 * nbl).reshape(-1, 4),
             level=h(self.level, self.dk.n_instr),

@@ -109,7 +109,9 @@ def build(dk: device.DeviceKernel) -> dict:
 
 
 def reach_in(dk: device.DeviceKernel):
-    """leo_reaching_definitions: (set_off[B*U+1], defs) over (block, unit) pairs."""
+    """leo_reaching_definitions: (set_off[B*U+1], defs) over (block, unit) pairs
+    (set semantics: a def may be listed twice in a set, when the search reached
+    two blocks of one fallthrough run that share their nearest definition)."""
     dev, ks = dk.device, dk.ks
     B, U = ks.n_blocks, ks.n_units
     cap = 4 * B * U + 1024
