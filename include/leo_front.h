@@ -45,6 +45,35 @@ const char* leo_front_string(void* h, int32_t k, int32_t which, int32_t i);
 int64_t leo_front_strings(void* h, int32_t k, int32_t which, char* buf, int64_t cap);
 void leo_front_free(void* h);
 
+/* ---- profile documents (native/leo_profile.cpp) ----------------------------
+ * Replaces profile.load_profiles (profile.py:244-263, _load_one :186-241, the
+ * InstructionSamples / KernelProfile invariants :124-165) and profile.attach
+ * (:332-366) + soa.encode_profile.  The JSON document is decoded with CPython
+ * json.JSONDecoder.raw_decode semantics; the first error is reported with the
+ * reference's exact message text. */
+void* leo_profile_parse(const char* text, int64_t len);
+/* 0 ok, 1 ProfileError, 2 InputError (unknown vendor), 3 value outside the
+ * SoA's integer range; message copied into buf (NUL-terminated), its length
+ * in *len */
+int32_t leo_profile_error(void* h, char* buf, int32_t cap, int32_t* len);
+int32_t leo_profile_n_kernels(void* h);
+const char* leo_profile_kernel_name(void* h, int32_t k);
+/* info[0..2] = dialect, sampling period (cycles), record count */
+int32_t leo_profile_info(void* h, int32_t k, int64_t* info);
+/* records in document order; total / exec -1 = absent; cls [n, 8] counts per
+ * CommonStall (profile.py:29-43 order) */
+int32_t leo_profile_records(void* h, int32_t k, int64_t* offset, int64_t* lat, int64_t* total,
+                            int64_t* exec, double* eff, int64_t* cls);
+/* attach kernel k to a CFG (name, dialect, n instruction offsets): fills the
+ * LeoProfile columns lat i32[n], cls_cnt i32[n*8], exec i64[n], total i32[n],
+ * eff f64[n], sampled u8[n]; 0 or the error kind (leo_profile_error) */
+int32_t leo_profile_attach(void* h, int32_t k, const char* cfg_name, int32_t cfg_dialect, int32_t n,
+                           const int64_t* instr_offset, int32_t* lat, int32_t* cls, int64_t* exec,
+                           int32_t* total, double* eff, uint8_t* sampled);
+/* the skid diagnostic of the last attach ("" when every offset matched) */
+const char* leo_profile_diagnostic(void* h);
+void leo_profile_free(void* h);
+
 #ifdef __cplusplus
 }
 #endif

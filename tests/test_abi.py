@@ -32,8 +32,8 @@ def test_front_library_exports_every_declared_symbol():
     from paper_2604_20032_b200 import build
     L = C.CDLL(str(build.build_front()))
     text = (ROOT / "include" / "leo_front.h").read_text()
-    names = sorted(set(re.findall(r"(leo_front_\w+)\s*\(", text)))
-    assert len(names) >= 8
+    names = sorted(set(re.findall(r"(leo_(?:front|profile)_\w+)\s*\(", text)))
+    assert len(names) >= 17
     for n in names:
         assert hasattr(L, n), n
 
