@@ -69,20 +69,20 @@ __global__ void k_bin_samples(int64_t S, const int32_t* __restrict__ pc, const u
 // added to cls_cnt in L2 directly.  The table is flushed with one global atomic
 // per occupied slot.  One read of the 5 bytes per sample (vs the bucketed
 // passes' hist + scatter + count: ~3 reads and a key write).
-constexpr int kBinHashSlots = 8192, kBinProbe = 8;
 constexpr uint32_t kBinEmpty = 0xFFFFFFFFu;
 
-__global__ void __launch_bounds__(512) k_bin_hash(int64_t S, const int32_t* __restrict__ pc,
-                                                  const uint8_t* __restrict__ cat,
-                                                  const uint8_t* __restrict__ lut, int N,
-                                                  int32_t* __restrict__ cls_cnt, uint32_t* status) {
+template <int SLOTS, int PROBE>
+__global__ void __launch_bounds__(1024) k_bin_hash(int64_t S, const int32_t* __restrict__ pc,
+                                                   const uint8_t* __restrict__ cat,
+                                                   const uint8_t* __restrict__ lut, int N,
+                                                   int32_t* __restrict__ cls_cnt, uint32_t* status) {
   pdl_wait();
   extern __shared__ uint32_t hsh[];
   uint32_t* keys = hsh;
-  uint32_t* cnts = hsh + kBinHashSlots;
+  uint32_t* cnts = hsh + SLOTS;
   __shared__ uint8_t slut[256];
   for (int x = threadIdx.x; x < 256; x += blockDim.x) slut[x] = lut[x];
-  for (int x = threadIdx.x; x < kBinHashSlots; x += blockDim.x) { keys[x] = kBinEmpty; cnts[x] = 0u; }
+  for (int x = threadIdx.x; x < SLOTS; x += blockDim.x) { keys[x] = kBinEmpty; cnts[x] = 0u; }
   __syncthreads();
   // this CTA's chunk, in whole 4-sample vectors
   const int64_t nvec = S / 4;
@@ -90,42 +90,68 @@ __global__ void __launch_bounds__(512) k_bin_hash(int64_t S, const int32_t* __re
   const int64_t v0 = blockIdx.x * per, v1 = min(nvec, v0 + per);
   const int4* pc4 = reinterpret_cast<const int4*>(pc);
   const uint32_t* cat4 = reinterpret_cast<const uint32_t*>(cat);
+  bool bad = false;
   // (no warp aggregation: __match_any_sync cost more than the shared-memory
   // atomics it saves; a hot key's lanes serialise only on their shared counter)
-  auto count = [&](uint32_t key, bool ok) {
-    if (!ok) return;
-    uint32_t h = (key * 2654435761u) >> 19;              // 13 bits
-    for (int probe = 0; probe < kBinProbe; probe++, h = (h + 1) & (kBinHashSlots - 1)) {
+  // Slow path: probe past the home slot, claim an empty slot, or count a cold
+  // key in L2.  Fully unrolled, and every vector of four samples ends with a
+  // __syncwarp(): a warp left diverged by the probe loop otherwise issues the
+  // next vector's loads once per lane group (measured 8x the load requests).
+  auto slow = [&](uint32_t key, uint32_t h) {
+#pragma unroll
+    for (int probe = 0; probe < PROBE; probe++) {
       uint32_t k0 = keys[h];
       if (k0 == kBinEmpty) k0 = atomicCAS(&keys[h], kBinEmpty, key);
       if (k0 == kBinEmpty || k0 == key) { atomicAdd(&cnts[h], 1u); return; }
+      h = h + 1 == (uint32_t)SLOTS ? 0u : h + 1;
     }
     atomicAdd(&cls_cnt[key], 1);                         // cold key: straight to L2
   };
-  for (int64_t v = v0 + threadIdx.x; v - threadIdx.x < v1; v += blockDim.x) {
-    const bool valid = v < v1;
-    const int4 p = valid ? pc4[v] : make_int4(0, 0, 0, 0);
-    const uint32_t c = valid ? cat4[v] : 0u;
-    const int pcs[4] = {p.x, p.y, p.z, p.w};
+  auto vec = [&](const int4 p, const uint32_t c, const bool valid) {
+    const int js[4] = {p.x, p.y, p.z, p.w};
+    uint32_t key[4], h[4];
+    bool hit[4];
+#pragma unroll
+    for (int t = 0; t < 4; t++) {                        // home slot: the hot-key hit
+      const bool ok = valid && (uint32_t)js[t] < (uint32_t)N;
+      bad |= valid && !ok;
+      key[t] = ok ? (uint32_t)js[t] * 8u + slut[(c >> (8 * t)) & 0xFF] : kBinEmpty;
+      h[t] = __umulhi(key[t] * 2654435761u, (uint32_t)SLOTS);
+      hit[t] = ok && keys[h[t]] == key[t];
+    }
 #pragma unroll
     for (int t = 0; t < 4; t++) {
-      const int j = pcs[t];
-      const bool ok = valid && j >= 0 && j < N;
-      if (valid && !ok) atomicOr(status, (uint32_t)LEO_ST_BAD_INPUT);
-      count(ok ? (uint32_t)j * 8u + slut[(c >> (8 * t)) & 0xFF] : 0u, ok);
+      if (hit[t]) atomicAdd(&cnts[h[t]], 1u);
+      else if (key[t] != kBinEmpty) slow(key[t], h[t]);
     }
+    __syncwarp();
+  };
+  // two 16-byte pc loads (and their category words) in flight per thread; the
+  // loop is warp-uniform (lanes past the chunk end run as no-ops) so that the
+  // __syncwarp() in vec() always sees the full warp
+  const int64_t bd = blockDim.x;
+  const int lane = threadIdx.x & 31;
+  for (int64_t v = v0 + threadIdx.x; v - lane < v1; v += 2 * bd) {
+    const bool in0 = v < v1, in1 = v + bd < v1;
+    const int4 p0 = in0 ? pc4[v] : make_int4(0, 0, 0, 0);
+    const int4 p1 = in1 ? pc4[v + bd] : make_int4(0, 0, 0, 0);
+    const uint32_t c0 = in0 ? cat4[v] : 0u, c1 = in1 ? cat4[v + bd] : 0u;
+    vec(p0, c0, in0);
+    vec(p1, c1, in1);
   }
   // tail samples (S mod 4): the last CTA
   if (blockIdx.x == gridDim.x - 1) {
     const int64_t s = nvec * 4 + threadIdx.x;
-    const bool in = s < S;
-    const int j = in ? pc[s] : 0;
-    const bool ok = in && j >= 0 && j < N;
-    if (in && !ok) atomicOr(status, (uint32_t)LEO_ST_BAD_INPUT);
-    count(ok ? (uint32_t)j * 8u + slut[cat[s]] : 0u, ok);
+    if (s < S) {
+      const int j = pc[s];
+      const bool ok = (uint32_t)j < (uint32_t)N;
+      bad |= !ok;
+      if (ok) atomicAdd(&cls_cnt[(uint32_t)j * 8u + slut[cat[s]]], 1);
+    }
   }
+  if (bad) atomicOr(status, (uint32_t)LEO_ST_BAD_INPUT);
   __syncthreads();
-  for (int x = threadIdx.x; x < kBinHashSlots; x += blockDim.x)
+  for (int x = threadIdx.x; x < SLOTS; x += blockDim.x)
     if (keys[x] != kBinEmpty) atomicAdd(&cls_cnt[keys[x]], (int)cnts[x]);
 }
 

@@ -562,41 +562,45 @@ __global__ void k_reach_unit(KView k, ReachArgs a, const int32_t* __restrict__ q
 constexpr int kT1Hash = 128, kT1Limit = 96, kT1Stack = 96, kT1Res = 32, kT1Threads = 128;
 constexpr int kT1Fetch = 64, kT1Chunk = 512;
 
+// KT: hash key type (uint16_t when every block id < 0xFFFF: half the shared
+// memory per thread, twice the resident warps); HASH slots, LIMIT visits.
+template <typename KT, int HASH, int LIMIT>
 __global__ void __launch_bounds__(kT1Threads) k_reach_fast(KView k, ReachArgs a,
                                                            const int32_t* __restrict__ q_list,
                                                            const int32_t* q_count, int32_t* q_head) {
   pdl_wait();
-  extern __shared__ int32_t hsm[];
+  extern __shared__ __align__(16) unsigned char hsm_raw[];
+  constexpr KT kEmpty = (KT)~(KT)0;
   const int nq = *q_count;
   const int lane = threadIdx.x & 31;
   const unsigned lt = (1u << lane) - 1;
-  int32_t* H = hsm + threadIdx.x;                  // slot s at H[s * blockDim.x]
+  KT* H = reinterpret_cast<KT*>(hsm_raw) + threadIdx.x;   // slot s at H[s * blockDim.x]
   const int stride = blockDim.x;
-  for (int s2 = 0; s2 < kT1Hash; s2++) H[s2 * stride] = -1;
+  for (int s2 = 0; s2 < HASH; s2++) H[s2 * stride] = kEmpty;
   int32_t stk[kT1Stack], res[kT1Res];
-  uint8_t used[kT1Limit];
+  uint8_t used[LIMIT];
   int e = -1, u = 0, sp = 0, nres = 0, nused = 0;
   bool drained = false, ovf = false;
   // warp-uniform: the warp's current batch of the query list, and chunk of the pool
   int fb = 0, fleft = 0, cb = 0, cleft = 0;
 
   auto insert = [&](int key) -> int {              // 1 new, 0 seen, -1 overflow
-    int x = (int)(((uint32_t)key * 2654435761u) >> 25);   // 7 bits
-    for (int probe = 0; probe < kT1Hash; probe++) {
-      const int v = H[x * stride];
-      if (v == key) return 0;
-      if (v == -1) {
-        if (nused == kT1Limit) return -1;
-        H[x * stride] = key;
+    int x = (int)(((uint32_t)key * 2654435761u) >> (32 - __popc(HASH - 1)));
+    for (int probe = 0; probe < HASH; probe++) {
+      const KT v = H[x * stride];
+      if (v == (KT)key) return 0;
+      if (v == kEmpty) {
+        if (nused == LIMIT) return -1;
+        H[x * stride] = (KT)key;
         used[nused++] = (uint8_t)x;
         return 1;
       }
-      x = (x + 1) & (kT1Hash - 1);
+      x = (x + 1) & (HASH - 1);
     }
     return -1;
   };
   auto release = [&]() {
-    for (int t = 0; t < nused; t++) H[used[t] * stride] = -1;
+    for (int t = 0; t < nused; t++) H[used[t] * stride] = kEmpty;
     nused = 0; sp = 0; nres = 0; ovf = false; e = -1;
   };
 

@@ -210,9 +210,14 @@ void set_smem_attributes() {
   cudaGetDevice(&dev);
   const uint64_t bit = 1ull << (dev & 63);
   if (done_mask & bit) return;
-  cudaFuncSetAttribute(k_reach_fast, cudaFuncAttributeMaxDynamicSharedMemorySize, kT1Threads * kT1Hash * 4);
+  cudaFuncSetAttribute(k_reach_fast<int32_t, 128, 96>, cudaFuncAttributeMaxDynamicSharedMemorySize, kT1Threads * 128 * 4);
+  cudaFuncSetAttribute(k_reach_fast<uint16_t, 128, 96>, cudaFuncAttributeMaxDynamicSharedMemorySize, kT1Threads * 128 * 2);
+  cudaFuncSetAttribute(k_reach_fast<uint16_t, 64, 48>, cudaFuncAttributeMaxDynamicSharedMemorySize, kT1Threads * 64 * 2);
+  cudaFuncSetAttribute(k_reach_fast<int32_t, 64, 48>, cudaFuncAttributeMaxDynamicSharedMemorySize, kT1Threads * 64 * 4);
   cudaFuncSetAttribute(k_bin_count, cudaFuncAttributeMaxDynamicSharedMemorySize, kBinRMax * 8 * 4);
-  cudaFuncSetAttribute(k_bin_hash, cudaFuncAttributeMaxDynamicSharedMemorySize, kBinHashSlots * 8);
+  for (auto f : {k_bin_hash<8192, 8>, k_bin_hash<8192, 4>, k_bin_hash<16384, 4>, k_bin_hash<16384, 2>,
+                 k_bin_hash<26624, 4>, k_bin_hash<26624, 2>, k_bin_hash<26624, 8>})
+    cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, 26624 * 8);
   cudaFuncSetAttribute(k_bin_scatter, cudaFuncAttributeMaxDynamicSharedMemorySize, kBinMaxBuckets * 12 + kBinSub * 4);
   cudaFuncSetAttribute(k_block_walk, cudaFuncAttributeMaxDynamicSharedMemorySize, 96 * 1024);
   cudaFuncSetAttribute(k_sync_wc_warp, cudaFuncAttributeMaxDynamicSharedMemorySize, 4 * kWcSmemInts * 4);
@@ -448,8 +453,18 @@ int build_graph_impl(const LeoKernel* kk, const LeoCaps* caps, LeoEdges* out, Le
                                                  n_seg > 1 ? kk->seg_block : nullptr, per_seg, bcap));
   } else {
     // tier 1 is persistent: enough CTAs to fill the chip, queries fetched dynamically
-    TRACED(KID_REACH_FAST, leo_launch(k_reach_fast, std::max(1, std::min<int>(grid_for(NU, kT1Threads), SM * 3)), kT1Threads,
-                                          kT1Threads * kT1Hash * 4, st, k, ra, q_list, &ctr[0], &ctr[9]));
+    // geometry A/B knob LEO_T1 (profiling only): 0 i32/128, 1 u16/128, 2 u16/64, 3 i32/64
+    static const int t1 = getenv("LEO_T1") ? atoi(getenv("LEO_T1")) : 2;
+    const bool narrow = B < 0xFFFF && t1 != 0 && t1 != 3;
+    auto f = k_reach_fast<int32_t, 128, 96>;
+    int slots = 128, kb = 4;
+    if (narrow && t1 == 2) { f = k_reach_fast<uint16_t, 64, 48>; slots = 64; kb = 2; }
+    else if (narrow) { f = k_reach_fast<uint16_t, 128, 96>; kb = 2; }
+    else if (t1 == 3) { f = k_reach_fast<int32_t, 64, 48>; slots = 64; }
+    const size_t t1_smem = (size_t)kT1Threads * slots * kb;
+    const int per_sm = std::max(1, std::min(16, (int)((220 * 1024) / (t1_smem + 1024))));
+    TRACED(KID_REACH_FAST, leo_launch(f, std::max(1, std::min<int>(grid_for(NU, kT1Threads), SM * per_sm)), kT1Threads,
+                                          t1_smem, st, k, ra, q_list, &ctr[0], &ctr[9]));
   }
   {
     const int wpc_r = 4;
@@ -743,8 +758,16 @@ static int bin_impl(const LeoSamples* s, int32_t n_instr, int32_t* lat, int32_t*
     LEO_CUDA_CHECK(cudaMemcpyAsync((void*)s->cat, s->cat_host, (size_t)S, cudaMemcpyHostToDevice, st));
   // big streams: one pass, per-CTA shared-memory hash (LEO_BIN_BUCKETED=1: the bucketed passes)
   if (S >= (4ll << 20) && (int64_t)n_instr * 8 < 0xFFFFFFFFll && !getenv("LEO_BIN_BUCKETED")) {
-    const int G = num_sms() * 3;
-    TRACED(KID_BIN, leo_launch(k_bin_hash, G, 512, (size_t)kBinHashSlots * 8, st, S, s->pc, s->cat, s->cat_to_cs,
+    // table geometry (A/B knobs LEO_BIN_SLOTS / LEO_BIN_PROBE; profiling only)
+    static const int slots = getenv("LEO_BIN_SLOTS") ? atoi(getenv("LEO_BIN_SLOTS")) : 16384;
+    static const int probe = getenv("LEO_BIN_PROBE") ? atoi(getenv("LEO_BIN_PROBE")) : 2;
+    auto f = k_bin_hash<26624, 4>;
+    int threads = 1024, per_sm = 1;
+    if (slots == 8192) { f = probe == 8 ? k_bin_hash<8192, 8> : k_bin_hash<8192, 4>; threads = 512; per_sm = 3; }
+    else if (slots == 16384) f = probe == 2 ? k_bin_hash<16384, 2> : k_bin_hash<16384, 4>;
+    else f = probe == 2 ? k_bin_hash<26624, 2> : probe == 8 ? k_bin_hash<26624, 8> : k_bin_hash<26624, 4>;
+    const int G = num_sms() * per_sm;
+    TRACED(KID_BIN, leo_launch(f, G, threads, (size_t)slots * 8, st, S, s->pc, s->cat, s->cat_to_cs,
                                n_instr, cls_cnt, status));
     TRACED(KID_BIN_FINALIZE, leo_launch(k_bin_finalize, grid_for(n_instr, 256), 256, 0, st, n_instr, cls_cnt, lat));
     LEO_CUDA_CHECK(cudaGetLastError());
