@@ -6,12 +6,15 @@
 //
 // Device algorithm
 //   G0 k_unit_counts   thread/instr: use-unit and def-unit counts -> scans
-//   G1 k_block_walk    warp/basic block, per-warp unit table in shared memory:
-//                      every use-unit event resolves to its in-block reaching
-//                      def, or to an upward-exposed (block, unit) query (one
-//                      per distinct unit per block, deduplicated with
-//                      __match_any_sync); emits each block's (unit, last def)
-//                      summary sorted by unit.
+//   G1 k_block_walk    warp/basic block: every use-unit event resolves to its
+//                      in-block reaching def, or to the upward-exposed (block,
+//                      unit) query led by the block's first use of the unit.
+//                      Blocks of <= 32 instructions are staged and resolved in
+//                      parallel (one lane per use event against the staged def
+//                      list); longer blocks walk in order over a per-warp unit
+//                      table.  Writes the block's last defs and led queries
+//                      into the -1-initialised [U][B] unit columns (sparse:
+//                      one write per last def / query, not per unit).
 //   G2 k_reach         thread/query: backward search over predecessor blocks
 //                      through blocks transparent to the unit; the union of the
 //                      last defs of the defining blocks reached is exactly the
@@ -131,7 +134,7 @@ struct WalkArgs {
 
 // per-warp staging of a window of <= 32 instructions' unit events
 constexpr int kWalkUse = 384, kWalkDef = 192, kWalkLeads = 64;
-constexpr int kWalkStage = kWalkUse + kWalkDef + kWalkLeads;
+constexpr int kWalkStage = 2 * kWalkUse + 2 * kWalkDef + kWalkLeads;   // units + their instructions
 
 // warp per block; blocks visited in increasing order per warp so that stale
 // table entries (from earlier blocks) are recognisable by index comparison.
@@ -145,12 +148,18 @@ __global__ void k_block_walk(KView k, WalkArgs a, int warps_per_cta) {
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
   const int gw = blockIdx.x * warps_per_cta + wid, nw = gridDim.x * warps_per_cta;
   const int U = k.U;
-  int32_t* wsm = smem + (size_t)wid * ((a.gtab ? 0 : 2 * U) + kWalkStage);
+  int32_t* wsm = smem + (size_t)wid * ((a.gtab ? 0 : 4 * U) + kWalkStage);
   int32_t* last = a.gtab ? a.gtab + (size_t)gw * 2 * U : wsm;
   int32_t* qtab = last + U;
-  int32_t* evu = a.gtab ? wsm : wsm + 2 * U;
+  // parallel path (shared-memory tables only): per unit, the mask of the
+  // block's instructions defining it and its first use event in the block
+  uint32_t* dmask = a.gtab ? nullptr : reinterpret_cast<uint32_t*>(wsm + 2 * U);
+  int32_t* fuse = a.gtab ? nullptr : wsm + 3 * U;
+  int32_t* evu = a.gtab ? wsm : wsm + 4 * U;
   int32_t* evd = evu + kWalkUse;
-  int32_t* leads = evd + kWalkDef;
+  int32_t* evui = evd + kWalkDef;                  // instruction of each staged use / def unit
+  int32_t* evdi = evui + kWalkUse;
+  int32_t* leads = evdi + kWalkDef;
   int nlead = 0;                                   // warp-uniform
   const unsigned lt = (1u << lane) - 1;
   auto publish = [&]() {
@@ -162,10 +171,13 @@ __global__ void k_block_walk(KView k, WalkArgs a, int warps_per_cta) {
     __syncwarp();
   };
   for (int u = lane; u < U; u += 32) { last[u] = -1; qtab[u] = -1; }
+  if (dmask)
+    for (int u = lane; u < U; u += 32) { dmask[u] = 0u; fuse[u] = INT_MAX; }
   __syncwarp();
   for (int b = gw; b < k.B; b += nw) {
     const int first = k.blk_first[b], lastI = k.blk_last[b];
     const int ev_block = a.use_ptr[first];
+    bool par = false;                              // block resolved by the parallel path
     for (int w0 = first; w0 <= lastI; w0 += 32) {
       const int i = w0 + lane, nin = min(32, lastI - w0 + 1);
       const bool in = lane < nin;
@@ -183,11 +195,63 @@ __global__ void k_block_walk(KView k, WalkArgs a, int warps_per_cta) {
         for (int q = q0; q < q1; q++) {
           const uint32_t r = k.opnd[q];
           const int s = op_span(r), base = unit_of(k, r);
-          if (op_role(r) == LEO_ROLE_DST) { for (int x = 0; x < s; x++) evd[pd++] = base + x; }
-          else { for (int x = 0; x < s; x++) evu[pu++] = base + x; }
+          if (op_role(r) == LEO_ROLE_DST) { for (int x = 0; x < s; x++) { evdi[pd] = i; evd[pd++] = base + x; } }
+          else { for (int x = 0; x < s; x++) { evui[pu] = i; evu[pu++] = base + x; } }
         }
       }
       __syncwarp();
+      if (dmask && staged && w0 == first && lastI - first < 32) {
+        // The whole block is staged: every use event is resolved in parallel.
+        // dmask[u] = the block's instructions defining u (bit i - first);
+        // fuse[u] = u's first use event.  A use at i reads the highest def bit
+        // below i (uses read before the same instruction's defs); with none it
+        // joins the (block, unit) query led by u's first use, which is then
+        // upward-exposed too.  Last defs and led queries are written sparsely.
+        par = true;
+        const int nu = ue - ub, nd = de - db;
+        for (int y = lane; y < nd; y += 32) atomicOr(&dmask[evd[y]], 1u << (evdi[y] - first));
+        for (int x = lane; x < nu; x += 32) atomicMin(&fuse[evu[x]], x);
+        __syncwarp();
+        for (int x0 = 0; x0 < nu; x0 += 32) {
+          const int x = x0 + lane;
+          bool lead = false;
+          if (x < nu) {
+            const int u = evu[x], i = evui[x];
+            const uint32_t m = dmask[u] & ((1u << (i - first)) - 1u);
+            int res;
+            if (m) {
+              res = first + 31 - __clz(m);
+            } else {
+              const int l = fuse[u];
+              lead = l == x;
+              res = -(ub + l + 1);
+              if (lead) {
+                a.q_block[ub + x] = b;
+                a.q_unit[ub + x] = u;
+                a.qtab[(size_t)u * a.Bp + b] = ub + x;
+              }
+            }
+            a.ev_res[ub + x] = res;
+          }
+          if (a.q_list) {
+            const unsigned lm = __ballot_sync(0xffffffffu, lead);
+            if (lm) {
+              if (nlead + __popc(lm) > kWalkLeads) publish();
+              if (lead) leads[nlead + __popc(lm & lt)] = ub + x;
+              nlead += __popc(lm);
+            }
+          }
+        }
+        for (int y = lane; y < nd; y += 32) {
+          const int u = evd[y], i = evdi[y];
+          if (first + 31 - __clz(dmask[u]) == i) a.ldtab[(size_t)u * a.Bp + b] = i;
+        }
+        __syncwarp();
+        for (int y = lane; y < nd; y += 32) dmask[evd[y]] = 0u;
+        for (int x = lane; x < nu; x += 32) fuse[evu[x]] = INT_MAX;
+        __syncwarp();
+        continue;
+      }
       for (int j = 0; j < nin; j++) {
         const int ii = w0 + j;
         const int e0 = __shfl_sync(0xffffffffu, u0, j), e1 = __shfl_sync(0xffffffffu, u1, j);
@@ -239,11 +303,13 @@ __global__ void k_block_walk(KView k, WalkArgs a, int warps_per_cta) {
       }
     }
     // the block's last definitions (block_defs depgraph.py:143-149) and its
-    // upward-exposed queries, one entry per unit column
-    for (int u = lane; u < U; u += 32) {
-      const int ld = last[u], qs = qtab[u];
-      a.ldtab[(size_t)u * a.Bp + b] = ld >= first ? ld : -1;
-      a.qtab[(size_t)u * a.Bp + b] = qs >= ev_block ? qs : -1;
+    // upward-exposed queries into the (-1 initialised) unit columns
+    if (!par) {
+      for (int u = lane; u < U; u += 32) {
+        const int ld = last[u], qs = qtab[u];
+        if (ld >= first) a.ldtab[(size_t)u * a.Bp + b] = ld;
+        if (qs >= ev_block) a.qtab[(size_t)u * a.Bp + b] = qs;
+      }
     }
     __syncwarp();
   }
@@ -578,7 +644,6 @@ __global__ void __launch_bounds__(kT1Threads) k_reach_fast(KView k, ReachArgs a,
   const int stride = blockDim.x;
   for (int s2 = 0; s2 < HASH; s2++) H[s2 * stride] = kEmpty;
   int32_t stk[kT1Stack], res[kT1Res];
-  uint8_t used[LIMIT];
   int e = -1, u = 0, sp = 0, nres = 0, nused = 0;
   bool drained = false, ovf = false;
   // warp-uniform: the warp's current batch of the query list, and chunk of the pool
@@ -592,7 +657,7 @@ __global__ void __launch_bounds__(kT1Threads) k_reach_fast(KView k, ReachArgs a,
       if (v == kEmpty) {
         if (nused == LIMIT) return -1;
         H[x * stride] = (KT)key;
-        used[nused++] = (uint8_t)x;
+        nused++;
         return 1;
       }
       x = (x + 1) & (HASH - 1);
@@ -600,7 +665,11 @@ __global__ void __launch_bounds__(kT1Threads) k_reach_fast(KView k, ReachArgs a,
     return -1;
   };
   auto release = [&]() {
-    for (int t = 0; t < nused; t++) H[used[t] * stride] = kEmpty;
+    // clear the whole table: HASH shared stores beat replaying a list of used
+    // slots kept in local memory (its loads were 15 % of the stall samples)
+    if (nused)
+#pragma unroll 8
+      for (int t = 0; t < HASH; t++) H[t * stride] = kEmpty;
     nused = 0; sp = 0; nres = 0; ovf = false; e = -1;
   };
 

@@ -257,7 +257,7 @@ int build_graph_impl(const LeoKernel* kk, const LeoCaps* caps, LeoEdges* out, Le
   const int SM = num_sms();
 
   // per-warp unit tables in shared memory when they fit
-  auto walk_bytes = [&](int w, bool tab) { return (size_t)w * ((tab ? 2 * (size_t)U : 0) + kWalkStage) * 4; };
+  auto walk_bytes = [&](int w, bool tab) { return (size_t)w * ((tab ? 4 * (size_t)U : 0) + kWalkStage) * 4; };
   int wpc = 8;
   while (wpc > 1 && walk_bytes(wpc, true) > 96 * 1024) wpc >>= 1;
   const bool smem_tab = walk_bytes(wpc, true) <= 96 * 1024;
@@ -414,6 +414,10 @@ int build_graph_impl(const LeoKernel* kk, const LeoCaps* caps, LeoEdges* out, Le
                      !(wdbg & LEO_DBG_NO_SMEM);
   WalkArgs wa{use_ptr, def_ptr, ev_res, q_block, q_unit, tier0 ? nullptr : q_list, &ctr[0], ldtab, qtab, Bp, gtab};
   const size_t smem = walk_bytes(wpc, smem_tab);
+  if (B > 0 && U > 0) {     // the walk writes the unit columns sparsely
+    cudaMemsetAsync(ldtab, 0xFF, (size_t)Bp * U * 4, st);
+    cudaMemsetAsync(qtab, 0xFF, (size_t)Bp * U * 4, st);
+  }
   if (B > 0) TRACED(KID_BLOCK_WALK, leo_launch(k_block_walk, std::max(1, walk_ctas), wpc * 32, smem, st, k, wa, wpc));
   // a caller's side branch (leo_analyze: stage-0 binning) forks here, after
   // the dataflow chain's head has been queued
