@@ -22,6 +22,22 @@
 
 using namespace leo;
 
+namespace leo {
+int scan_coop_grid() {
+  static int cache[64] = {};
+  int dev = 0;
+  cudaGetDevice(&dev);
+  int& g = cache[dev & 63];
+  if (!g) {
+    int per = 0, sms = 0;
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, scan_coop, kCsThreads, 0);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    g = std::max(1, per) * std::max(1, sms);
+  }
+  return g;
+}
+}  // namespace leo
+
 namespace {
 
 // ---- optional device-time trace (LeoTrace) ---------------------------------
@@ -1147,7 +1163,8 @@ int leo_analyze(const LeoKernel* k, const LeoProfile* p, const LeoSamples* sampl
     dbg_delay("LEO_DBG_DELAY_BIN", s_bin);
     // small streams bin at the least priority; a big stream (C5) is itself a
     // long branch and keeps the default
-    LowPriority low_prio(samples->n_samples <= (16ll << 20));
+    static const int bin_lo = getenv("LEO_BIN_LOWPRIO") ? atoi(getenv("LEO_BIN_LOWPRIO")) : -1;
+    LowPriority low_prio(bin_lo >= 0 ? bin_lo == 1 : samples->n_samples <= (16ll << 20));
     return bin_impl(samples, k->n_instr, (int32_t*)p->lat, (int32_t*)p->cls_cnt, status, tr, s_bin);
   };
   // Up to 16 M samples the binning branch forks after the block walk: it has

@@ -5,6 +5,8 @@
 // upper bound (`cap`) for launch sizing, so the whole pipeline runs without a
 // host round trip (and can be captured in a CUDA graph).
 #pragma once
+#include <cooperative_groups.h>
+
 #include "common.cuh"
 
 namespace leo {
@@ -158,12 +160,128 @@ __global__ void __launch_bounds__(1024) scan_single_cta_pair(const int32_t* __re
   else scan_one_cta(b_in, n, b_out, nullptr);
 }
 
+// ---- one-launch scan: co-resident CTAs (cooperative launch), tile sums, one
+// grid barrier, then each tile adds the sums before it and writes its prefix.
+// A CTA that owns one tile keeps it in registers across the barrier (one read
+// of the input).  Replaces the tile-sum + apply launch pair (two launches and a
+// dependent drain on the critical chain per scan).
+constexpr int kCsThreads = 512, kCsItems = 16, kCsTile = kCsThreads * kCsItems;
+
+LEO_DEV int block_reduce_sum(int v, int* sw) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  if (lane == 0) sw[warp] = v;
+  __syncthreads();
+  if (warp == 0) {
+    int w = lane < nw ? sw[lane] : 0;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) w += __shfl_xor_sync(0xffffffffu, w, o);
+    if (lane == 0) sw[32] = w;
+  }
+  __syncthreads();
+  const int r = sw[32];
+  __syncthreads();
+  return r;
+}
+
+__global__ void __launch_bounds__(kCsThreads) scan_coop(const int32_t* __restrict__ in, const int32_t* n_dev,
+                                                        int64_t n_cap, int32_t* __restrict__ tsum,
+                                                        int32_t* __restrict__ out, int32_t* total_out) {
+  __shared__ int sw[33];
+  const int64_t n = n_dev ? (int64_t)*n_dev : n_cap;
+  const int64_t ntiles = n > 0 ? (n + kCsTile - 1) / kCsTile : 1;
+  const bool one = ntiles <= (int64_t)gridDim.x;
+  const int tid = threadIdx.x;
+  int v[kCsItems];
+  auto load = [&](int64_t t) {
+    const int64_t base = t * kCsTile + (int64_t)tid * kCsItems;
+    if (base + kCsItems <= n) {
+      const int4* p = reinterpret_cast<const int4*>(in + base);
+#pragma unroll
+      for (int q = 0; q < kCsItems / 4; q++) {
+        const int4 x = p[q];
+        v[4 * q] = x.x; v[4 * q + 1] = x.y; v[4 * q + 2] = x.z; v[4 * q + 3] = x.w;
+      }
+    } else {
+#pragma unroll
+      for (int k = 0; k < kCsItems; k++) v[k] = base + k < n ? in[base + k] : 0;
+    }
+  };
+  for (int64_t t = blockIdx.x; t < ntiles; t += gridDim.x) {
+    load(t);
+    int s = 0;
+#pragma unroll
+    for (int k = 0; k < kCsItems; k++) s += v[k];
+    const int tot = block_reduce_sum(s, sw);
+    if (tid == 0) tsum[t] = tot;
+  }
+  cooperative_groups::this_grid().sync();
+  for (int64_t t = blockIdx.x; t < ntiles; t += gridDim.x) {
+    if (!one) load(t);
+    int acc = 0;
+    for (int64_t x = tid; x < t; x += kCsThreads) acc += tsum[x];
+    const int prefix = block_reduce_sum(acc, sw);
+    int s = 0;
+#pragma unroll
+    for (int k = 0; k < kCsItems; k++) s += v[k];
+    int tile_total;
+    int ex = block_excl_scan(s, sw, &tile_total) + prefix;
+    const int64_t base = t * kCsTile + (int64_t)tid * kCsItems;
+    if (base + kCsItems <= n) {
+      int4* p = reinterpret_cast<int4*>(out + base);
+#pragma unroll
+      for (int q = 0; q < kCsItems / 4; q++) {
+        int4 o;
+        o.x = ex; ex += v[4 * q]; o.y = ex; ex += v[4 * q + 1];
+        o.z = ex; ex += v[4 * q + 2]; o.w = ex; ex += v[4 * q + 3];
+        p[q] = o;
+      }
+    } else {
+#pragma unroll
+      for (int k = 0; k < kCsItems; k++) {
+        if (base + k < n) out[base + k] = ex;
+        ex += v[k];
+      }
+    }
+    if (t == ntiles - 1 && tid == 0) {
+      out[n] = prefix + tile_total;
+      if (total_out) *total_out = prefix + tile_total;
+    }
+  }
+}
+
+int scan_coop_grid();   // co-resident CTAs of scan_coop on the current device (leo_b200.cu)
+
 // exclusive scan of in[0..n) into out[0..n] (out[n] = total); n from n_dev if
 // given else n_cap.  scratch: >= tiles(n_cap) ints.  total_out optional.
+// in / out must be 16-byte aligned (arena allocations are 256-byte aligned).
 inline void scan_exclusive(const int32_t* in, int32_t* out, const int32_t* n_dev, int64_t n_cap,
                            int32_t* scratch, int32_t* total_out, cudaStream_t st) {
   if (n_cap <= kScanSingleMax) {
     leo_launch(scan_single_cta, 1, 1024, 0, st, in, n_dev, n_cap, out, total_out);
+    return;
+  }
+  if (!getenv("LEO_SCAN_TILED")) {     // one launch: -2..-15 us per step on C2/C3/C5 (measured A/B)
+    const int64_t ntiles = (n_cap + kCsTile - 1) / kCsTile;
+    const int grid = (int)std::max<int64_t>(1, std::min<int64_t>(ntiles, scan_coop_grid()));
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(grid);
+    cfg.blockDim = dim3(kCsThreads);
+    cfg.stream = st;
+    cudaLaunchAttribute attr[2];
+    int na = 0;
+    attr[na].id = cudaLaunchAttributeCooperative;
+    attr[na].val.cooperative = 1;
+    na++;
+    if (LaunchPrio::current() >= 0) {
+      attr[na].id = cudaLaunchAttributePriority;
+      attr[na].val.priority = prio_value(LaunchPrio::current() != 0);
+      na++;
+    }
+    cfg.attrs = attr;
+    cfg.numAttrs = na;
+    cudaLaunchKernelEx(&cfg, scan_coop, in, n_dev, n_cap, scratch, out, total_out);
     return;
   }
   int64_t ntiles = (n_cap + kScanTile - 1) / kScanTile;

@@ -38,6 +38,17 @@ def test_front_library_exports_every_declared_symbol():
         assert hasattr(L, n), n
 
 
+def test_library_has_no_undefined_internal_symbols():
+    """dlopen on a GPU box binds eagerly; an internal symbol left undefined
+    (declared in a header, defined in another namespace) fails there only."""
+    import subprocess
+    out = subprocess.run(["nm", "-D", "--undefined-only",
+                          str(ROOT / "paper_2604_20032_b200" / "libleo_b200.so")],
+                         capture_output=True, text=True).stdout
+    bad = [ln for ln in out.splitlines() if "_ZN3leo" in ln]
+    assert not bad, bad
+
+
 def test_library_is_sm100a():
     import subprocess
     out = subprocess.run(["/usr/local/cuda/bin/cuobjdump", "--list-elf",
