@@ -24,6 +24,8 @@ if [[ $WHAT == all || $WHAT == bench ]]; then
     timeout 600 python bench.py --config $c --steps 20 --warmup 5 --cpu-seconds 5 > $OUT/${TAG}_bench_$c.json 2> $OUT/${TAG}_bench_$c.err
     echo "bench $c rc=$?"
   done
+  timeout 1800 python bench.py --config c4 --steps 5 --warmup 3 --cpu-seconds 5 > $OUT/${TAG}_bench_c4.json 2> $OUT/${TAG}_bench_c4.err
+  echo "bench c4 rc=$?"; tail -c 300 $OUT/${TAG}_bench_c4.json
 fi
 if [[ $WHAT == all || $WHAT == timeline ]]; then
   for c in c5 c2; do
@@ -39,4 +41,13 @@ if [[ $WHAT == all || $WHAT == ncu ]]; then
      -k 'regex:k_(bin_|reach_|block_walk|prune_edges|slice|mp_round|link|sync|blame|lines|compact)' -s 0 -c 40 \
      -o $OUT/${TAG}_c5_full -f python tools/profile_step.py c5 --steps 1 --warmup 0 > $OUT/${TAG}_ncu_full.txt 2>&1
   echo "ncu full rc=$?"; tail -3 $OUT/${TAG}_ncu_full.txt
+fi
+if [[ $WHAT == all || $WHAT == ncu4 ]]; then
+  timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none --csv \
+     --log-file $OUT/${TAG}_c4_launches.csv python tools/profile_step.py c4 --steps 1 --warmup 1 > $OUT/${TAG}_ncu4_list.txt 2>&1
+  echo "ncu c4 list rc=$?"
+  timeout 1500 ncu --set full --clock-control none --import-source on \
+     -k 'regex:k_(bin_|reach_|block_walk|prune_edges|slice|mp_round|link|sync|blame|lines|compact)' -s 0 -c 40 \
+     -o $OUT/${TAG}_c4_full -f python tools/profile_step.py c4 --steps 1 --warmup 0 > $OUT/${TAG}_ncu4_full.txt 2>&1
+  echo "ncu c4 full rc=$?"; tail -3 $OUT/${TAG}_ncu4_full.txt
 fi

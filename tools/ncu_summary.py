@@ -27,7 +27,7 @@ TRACE_TO_KERNEL = {
     "prune_edges": ("k_prune_edges_smem", "k_prune_edges"),
     "blame_count": ("k_blame<0>",),
     "blame_fill": ("k_blame<1>",),
-    "bin_samples": ("k_bin_count", "k_bin_samples"),
+    "bin_samples": ("k_bin_hash", "k_bin_count", "k_bin_samples"),
     "block_walk": ("k_block_walk",),
     "slice": ("k_slice",),
     "segsort_unique": ("segsort_unique_u64",),

@@ -20,6 +20,7 @@ ap.add_argument("config", nargs="?", default="c2")
 ap.add_argument("--steps", type=int, default=2)
 ap.add_argument("--warmup", type=int, default=1)
 ap.add_argument("--scale", type=float, default=1.0)
+ap.add_argument("--c4-kernels", type=int, default=300)
 ap.add_argument("--flags", type=int, default=0)
 ap.add_argument("--timeline", action="store_true")
 ap.add_argument("--graph-timeline", action="store_true")
@@ -28,25 +29,44 @@ ap.add_argument("--debug-guard", action="store_true")
 args = ap.parse_args()
 
 dev = torch.device("cuda:0")
-wl = synth.config_workload(args.config, scale=args.scale)
-dk = device.DeviceKernel(wl.kernel, dev)
-dp = device.DeviceProfile(wl.profile, wl.kernel.n_instr, dev)
-ds = device.DeviceSamples(wl.pc, wl.cat, wl.lut, dev)
-an = device.Analyzer(dk, dev, debug_flags=args.flags)
-cfg = abi.make_config(dialect=wl.kernel.dialect)
-an.run(dp, cfg, ds)                      # sizes buffers (grow + re-run on overflow)
+if args.config == "c4":
+    # the bench's C4 batch pipelines (one concatenated batch per dialect) over
+    # the first --c4-kernels kernels of the 2,000
+    from paper_2604_20032_b200 import batch as BT
+    lines = synth.LineTable(4096, seed=999)
+    groups = {}
+    for kk in range(args.c4_kernels):
+        w = synth.c4_kernel(kk, lines)
+        groups.setdefault(BT.group_key(w), []).append(w)
+    wls = [BT.concat(groups[key]) for key in sorted(groups)]
+else:
+    wls = [synth.config_workload(args.config, scale=args.scale)]
+items = []
+for wl in wls:
+    dk = device.DeviceKernel(wl.kernel, dev)
+    dp = device.DeviceProfile(wl.profile, wl.kernel.n_instr, dev)
+    ds = device.DeviceSamples(wl.pc, wl.cat, wl.lut, dev)
+    an = device.Analyzer(dk, dev, debug_flags=args.flags)
+    cfg = abi.make_config(dialect=wl.kernel.dialect)
+    an.run(dp, cfg, ds)                      # sizes buffers (grow + re-run on overflow)
+    items.append((an, dp, cfg, ds))
+wl = wls[0]
+an, dp, cfg, ds = items[0]
 flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)
 for _ in range(args.warmup):
     flush.zero_()
-    an.launch(dp, cfg, ds)
+    for it in items:
+        it[0].launch(*it[1:])
 torch.cuda.synchronize()
 for _ in range(args.steps):
     flush.zero_()
-    an.launch(dp, cfg, ds)
+    for it in items:
+        it[0].launch(*it[1:])
 torch.cuda.synchronize()
-r = an.result()
-print(f"{args.config}: status={r['status']} edges={len(r['bprod'])} pruned={len(r['pprod'])} "
-      f"blame={len(r['e_blame'])}")
+for it in items:
+    r = it[0].result()
+    print(f"{args.config}: status={r['status']} edges={len(r['bprod'])} pruned={len(r['pprod'])} "
+          f"blame={len(r['e_blame'])}")
 
 if args.timeline:
     # eager step queued behind a GPU spin (so host launch overhead is hidden
