@@ -19,6 +19,7 @@
 //                     every S_j > 0, level-synchronous in one
 //                     cooperative kernel.
 #include <cooperative_groups.h>
+#include <cooperative_groups/scan.h>
 
 #include "prims.cuh"
 
@@ -584,6 +585,70 @@ __global__ void k_mp_final(KView k, const int32_t* __restrict__ rbeg, const int3
   }
 }
 
+// All rounds in one cooperative kernel, relaxing IN PLACE (Gauss-Seidel):
+// a label is always the top-2 of real paths of <= 8 hops, so it only
+// decreases and its fixpoint is the Jacobi result; rounds stop at the first
+// one that changes nothing (<= 7 relaxations, the Jacobi bound), then the
+// evaluation round.  flags[3]: "changed" per round, reset two rounds ahead.
+LEO_DEV uint2 mp_relax(const KView& k, const int32_t* __restrict__ rbeg, const int32_t* __restrict__ rend,
+                       const int32_t* __restrict__ ep, const uint2* lab, int v, bool first) {
+  int D1 = kMpInf, T1 = -1, D2 = kMpInf, T2 = -1;
+  if (!(kMemoryProducer & BIT(k.opclass[v]))) {
+    const int e1 = rend[v];
+    for (int e = rbeg[v]; e < e1; e += kMpUnroll) {
+      int q[kMpUnroll];
+      uint2 L[kMpUnroll];
+#pragma unroll
+      for (int x = 0; x < kMpUnroll; x++) q[x] = e + x < e1 ? ep[e + x] : -1;
+#pragma unroll
+      for (int x = 0; x < kMpUnroll; x++)
+        L[x] = (!first && q[x] >= 0 && !(q[x] & kMpPF)) ? __ldcg(&lab[q[x]])   // L2: other SMs' writes
+                                                         : make_uint2(0xFFFFFFFFu, 0xFFFFFFFFu);
+#pragma unroll
+      for (int x = 0; x < kMpUnroll; x++) {
+        if (q[x] < 0) continue;
+        if (q[x] & kMpPF) { mp_insert(1, (int)(q[x] & ~kMpPF), D1, T1, D2, T2); continue; }
+        if (first) continue;
+        if (mp_d(L[x].x) < 8) mp_insert(mp_d(L[x].x) + 1, mp_t(L[x].x), D1, T1, D2, T2);
+        if (mp_d(L[x].y) < 8) mp_insert(mp_d(L[x].y) + 1, mp_t(L[x].y), D1, T1, D2, T2);
+      }
+    }
+  }
+  return make_uint2(mp_pack(D1, T1), mp_pack(D2, T2));
+}
+
+__global__ void k_mp_coop(KView k, const int32_t* __restrict__ rbeg, const int32_t* __restrict__ rend,
+                          const int32_t* __restrict__ ep, uint2* lab, int32_t* flags, uint8_t* __restrict__ ok) {
+  cg::grid_group grid = cg::this_grid();
+  const int stride = gridDim.x * blockDim.x, t0 = blockIdx.x * blockDim.x + threadIdx.x;
+  for (int r = 0; r < 7; r++) {
+    if (t0 == 0) flags[(r + 1) % 3] = 0;
+    bool changed = false;
+    for (int v = t0; v < k.N; v += stride) {
+      const uint2 nl = mp_relax(k, rbeg, rend, ep, lab, v, r == 0);
+      if (r == 0) { __stcg(&lab[v], nl); continue; }
+      const uint2 ol = __ldcg(&lab[v]);
+      if (nl.x != ol.x || nl.y != ol.y) { __stcg(&lab[v], nl); changed = true; }
+    }
+    if (changed) flags[r % 3] = 1;
+    grid.sync();
+    if (r > 0 && *(volatile int32_t*)&flags[r % 3] == 0) break;
+  }
+  for (int j = t0; j < k.N; j += stride) {
+    bool hit = false;
+    const int e1 = rend[j];
+    for (int e = rbeg[j]; e < e1 && !hit; e++) {
+      const int q = ep[e];
+      if (q < 0) continue;
+      if (q & kMpPF) { hit = (int)(q & ~kMpPF) != j; continue; }
+      const uint2 L = __ldcg(&lab[q]);
+      const int d = mp_t(L.x) != j ? mp_d(L.x) : mp_d(L.y);   // nearest target other than j
+      hit = d + 1 <= 8;
+    }
+    ok[j] = hit ? 1 : 0;
+  }
+}
+
 struct BlameArgs {
   int32_t dbg;
   const uint8_t* mp_ok;       // per-instruction _address_traces_to_load (null: search here)
@@ -607,10 +672,31 @@ struct BlameArgs {
   int32_t* slow_count;
   int64_t slow_cap;
   uint32_t* status;
-  double* zero_lb;          // pass 1 also zeroes the line vectors (null: accumulate / no lines)
+  double* zero_lb;          // pass 0 also zeroes the line vectors (null: accumulate / no lines)
   double* zero_ls;
   int32_t n_lines;
+  // edge entries staged by pass 0 (any order; k_blame_compact moves them into
+  // stalled-instruction order): j's entries at stg_off[j] .. + ecount[j]
+  int32_t* stg_off;         // [N]
+  int32_t* stg_count;       // reservation counter
+  int64_t stg_cap;
+  int32_t* stg_edge;
+  int32_t* stg_cause;
+  double* stg_blame;        // product until the normaliser is known, then blame_cycles
+  double* stg_fac;          // [4 x]
 };
+
+// warp-aggregated reservation of n staging slots (divergent callers)
+LEO_DEV int stage_reserve(const BlameArgs& a, int n) {
+  cg::coalesced_group g = cg::coalesced_threads();
+  const int incl = cg::inclusive_scan(g, n);
+  int base = 0;
+  if (g.thread_rank() == g.size() - 1) base = atomicAdd(a.stg_count, incl);
+  base = g.shfl(base, g.size() - 1);
+  const int o = base + incl - n;
+  if ((int64_t)o + n > a.stg_cap) { atomicOr(a.status, (uint32_t)LEO_ST_BLAME_OVERFLOW); return -1; }
+  return o;
+}
 
 LEO_DEV double issue_count(const PView& p, int i) {   // profile.py:321-329
   if (p.exec_cnt[i] >= 0) return (double)p.exec_cnt[i];
@@ -744,7 +830,9 @@ LEO_DEV bool blame_one(const KView& k, const BlameArgs& a, int j) {
       else { total = a.jtotal[j]; n_sum = a.jnsum[j]; }
       if (PASS == 0 && n_sum == 0) self = true;
       else {
-        const int o = PASS == 1 ? a.eoff[j] : 0;
+        const bool stg = PASS == 0 && a.stg_cap > 0;
+        const int o = PASS == 1 ? a.eoff[j] : stg ? stage_reserve(a, deg) : 0;
+        if (PASS == 0 && o < 0) return false;
         if (PASS == 1 && o + a.ecount[j] > a.out.capacity) { atomicOr(a.status, (uint32_t)LEO_ST_BLAME_OVERFLOW); return false; }
         PySum ts;
         for (int x0 = 0; x0 < deg; x0 += kBU) {
@@ -760,6 +848,14 @@ LEO_DEV bool blame_one(const KView& k, const BlameArgs& a, int j) {
             const double prod = __dmul_rn(__dmul_rn(__dmul_rn(f0, f1), f2), f3);
             if (PASS == 0) {
               ts.add(prod);
+              const int x = o + x0 + u;
+              if (stg) {
+              a.stg_edge[x] = eb.e[u];
+              a.stg_cause[x] = eb.pr[u];
+              a.stg_blame[x] = prod;
+              double* f = a.stg_fac + (size_t)x * 4;
+              f[0] = f0; f[1] = f1; f[2] = f2; f[3] = f3;
+              }
             } else {
               const int x = o + x0 + u;
               a.out.stalled[x] = j;
@@ -775,6 +871,10 @@ LEO_DEV bool blame_one(const KView& k, const BlameArgs& a, int j) {
         if (PASS == 0) {
           total = ts.value();
           if (total == 0.0) self = true;
+          else if (stg) {
+            a.stg_off[j] = o;
+            for (int x = o; x < o + deg; x++) a.stg_blame[x] = __ddiv_rn(__dmul_rn(s_j, a.stg_blame[x]), total);
+          }
         }
       }
     }
@@ -834,6 +934,13 @@ LEO_DEV void blame_warp(const KView& k, const BlameArgs& a, int j, int lane) {
     total = a.jtotal[j];
   }
   PySum ts;
+  int so = 0;                                  // pass 0: staging slots of j's entries
+  const bool stg = PASS == 0 && a.stg_cap > 0;
+  if (stg) {
+    if (lane == 0) so = stage_reserve(a, deg);
+    so = __shfl_sync(0xffffffffu, so, 0);
+    if (so < 0) return;
+  }
   for (int x0 = 0; x0 < deg; x0 += 32) {
     const int x = x0 + lane;
     double prod = 0;
@@ -845,6 +952,14 @@ LEO_DEV void blame_warp(const KView& k, const BlameArgs& a, int j, int lane) {
       const double f2 = __ddiv_rn(issue_count_ld(a.p, pr), n_sum);
       const double f3 = __ddiv_rn((double)a.p.cls_cnt[(size_t)j * 8 + kMatchClass[(a.pmeta[e] >> 30) & 3]], (double)lat);
       prod = __dmul_rn(__dmul_rn(__dmul_rn(f0, f1), f2), f3);
+      if (stg) {
+        const int w = so + x;
+        a.stg_edge[w] = e;
+        a.stg_cause[w] = pr;
+        a.stg_blame[w] = prod;
+        double* f = a.stg_fac + (size_t)w * 4;
+        f[0] = f0; f[1] = f1; f[2] = f2; f[3] = f3;
+      }
       if (PASS == 1) {
         const int w = o + x;
         a.out.stalled[w] = j;
@@ -861,13 +976,20 @@ LEO_DEV void blame_warp(const KView& k, const BlameArgs& a, int j, int lane) {
       for (int t = 0; t < m; t++) ts.add(__shfl_sync(0xffffffffu, prod, t));
     }
   }
-  if (PASS == 0 && lane == 0) {
-    total = ts.value();
-    if (total == 0.0) blame_self(k, a, j);
-    else {
-      a.ecount[j] = deg;
-      a.jtotal[j] = total;
-      a.jnsum[j] = n_sum;
+  if (PASS == 0) {
+    total = ts.value();                        // every lane holds the same ordered sum
+    if (total == 0.0) {
+      if (lane == 0) blame_self(k, a, j);
+    } else {
+      __syncwarp();
+      if (stg)
+        for (int x = so + lane; x < so + deg; x += 32) a.stg_blame[x] = __ddiv_rn(__dmul_rn(s_j, a.stg_blame[x]), total);
+      if (lane == 0) {
+        if (stg) a.stg_off[j] = so;
+        a.ecount[j] = deg;
+        a.jtotal[j] = total;
+        a.jnsum[j] = n_sum;
+      }
     }
   }
 }
@@ -877,9 +999,9 @@ template <int PASS>
 __global__ void k_blame(KView k, BlameArgs a) {
   pdl_wait();
   const int lane = threadIdx.x & 31;
-  if (PASS == 1) {
-    // the entry count (was k_blame_count) and the line vectors k_lines adds into
-    if (blockIdx.x == 0 && threadIdx.x == 0) *a.out.count = a.eoff[k.N];
+  if (PASS == 1 && blockIdx.x == 0 && threadIdx.x == 0) *a.out.count = a.eoff[k.N];
+  if (PASS == 0) {
+    // the line vectors k_blame_compact / k_lines add into
     if (a.zero_lb)
       for (int x = blockIdx.x * blockDim.x + threadIdx.x; x < a.n_lines; x += gridDim.x * blockDim.x) {
         a.zero_lb[x] = 0.0;
@@ -901,6 +1023,79 @@ __global__ void k_blame(KView k, BlameArgs a) {
 }
 template __global__ void k_blame<0>(KView, BlameArgs);
 template __global__ void k_blame<1>(KView, BlameArgs);
+
+// Pass 1 without recomputation: every stalled instruction's entries move from
+// the staging area (pass 0, reservation order) to eoff[j] (stalled order), and
+// the per-line rollup (k_lines) is done on the way: line_blame[line(cause)] +=
+// blame_cycles, line_stall[line(j)] += S_j.  Instructions with many entries
+// are copied by the whole warp.
+LEO_DEV void compact_one(const KView& k, const BlameArgs& a, int j, int c, int lane, int step,
+                         const int32_t* __restrict__ line_id, double* line_blame) {
+  const int o = a.eoff[j], so = a.stg_off[j];
+  for (int x = lane; x < c; x += step) {
+    const int w = o + x, r = so + x;
+    const int e = a.stg_edge[r], pr = a.stg_cause[r];
+    const double bl = a.stg_blame[r];
+    a.out.stalled[w] = j;
+    a.out.edge[w] = e;
+    if (a.out.cause) { a.out.cause[w] = pr; a.out.meta[w] = a.pmeta[e]; }
+    a.out.sub[w] = 255;
+    a.out.blame[w] = bl;
+    const double2* f = reinterpret_cast<const double2*>(a.stg_fac + (size_t)r * 4);
+    double2* g = reinterpret_cast<double2*>(a.out.factors + (size_t)w * 4);
+    g[0] = f[0];
+    g[1] = f[1];
+    if (line_blame) atomicAdd(&line_blame[line_id[pr]], bl);
+  }
+}
+
+__global__ void k_blame_compact(KView k, BlameArgs a, const int32_t* __restrict__ line_id,
+                                double* line_blame, double* line_stall) {
+  pdl_wait();
+  const int lane = threadIdx.x & 31;
+  const int total = a.eoff[k.N];
+  if (blockIdx.x == 0 && threadIdx.x == 0) *a.out.count = total;
+  if (total > a.out.capacity) {                 // the host re-runs with a bigger list
+    if (blockIdx.x == 0 && threadIdx.x == 0) atomicOr(a.status, (uint32_t)LEO_ST_BLAME_OVERFLOW);
+    return;
+  }
+  for (int j0 = blockIdx.x * blockDim.x + (threadIdx.x & ~31); j0 < k.N; j0 += gridDim.x * blockDim.x) {
+    const int j = j0 + lane;
+    int c = 0;
+    bool heavy = false;
+    if (j < k.N) {
+      c = a.ecount[j];
+      if (c > 0) {
+        const double s_j = (double)((int64_t)a.p.lat[j] * a.p.period);
+        if (a.self_sub[j] >= 0) {
+          const int o = a.eoff[j];
+          a.out.stalled[o] = j;
+          a.out.edge[o] = -1;
+          if (a.out.cause) { a.out.cause[o] = -1; a.out.meta[o] = 0u; }
+          a.out.sub[o] = (uint8_t)a.self_sub[j];
+          a.out.blame[o] = s_j;
+          double2* g = reinterpret_cast<double2*>(a.out.factors + (size_t)o * 4);
+          g[0] = make_double2(0.0, 0.0);
+          g[1] = make_double2(0.0, 0.0);
+          if (line_blame) atomicAdd(&line_blame[line_id[j]], s_j);
+        } else if (c > kBlameWarpDeg) {
+          heavy = true;
+        } else {
+          compact_one(k, a, j, c, 0, 1, line_id, line_blame);
+        }
+      }
+      if (line_stall && a.p.lat[j] && a.own.has(j))
+        atomicAdd(&line_stall[line_id[j]], (double)((int64_t)a.p.lat[j] * a.p.period));
+    }
+    unsigned hv = __ballot_sync(0xffffffffu, heavy);
+    while (hv) {
+      const int src = __ffs(hv) - 1;
+      hv &= hv - 1;
+      compact_one(k, a, j0 + src, __shfl_sync(0xffffffffu, c, src), lane, 32, line_id, line_blame);
+      __syncwarp();
+    }
+  }
+}
 
 // _address_traces_to_load (analysis.py:390-411), warp per candidate: the BFS
 // frontier is expanded by all lanes at once (one level per round, <= 8

@@ -210,6 +210,37 @@ inline void leo_launch(void (*kern)(KArgs...), dim3 grid, dim3 block, size_t sme
   cudaLaunchKernelEx(&cfg, kern, std::forward<Args>(args)...);
 }
 
+// leo_launch with a thread-block cluster of `csize` CTAs along x (grid % csize == 0)
+template <typename... KArgs, typename... Args>
+inline void leo_launch_cluster(void (*kern)(KArgs...), int grid, int csize, dim3 block, size_t smem,
+                               cudaStream_t st, Args&&... args) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(grid);
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = st;
+  cudaLaunchAttribute attr[3];
+  int na = 0;
+  attr[na].id = cudaLaunchAttributeClusterDimension;
+  attr[na].val.clusterDim.x = csize;
+  attr[na].val.clusterDim.y = 1;
+  attr[na].val.clusterDim.z = 1;
+  na++;
+  if (pdl_enabled()) {
+    attr[na].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[na].val.programmaticStreamSerializationAllowed = 1;
+    na++;
+  }
+  if (LaunchPrio::current() >= 0) {
+    attr[na].id = cudaLaunchAttributePriority;
+    attr[na].val.priority = prio_value(LaunchPrio::current() != 0);
+    na++;
+  }
+  cfg.attrs = attr;
+  cfg.numAttrs = na;
+  cudaLaunchKernelEx(&cfg, kern, std::forward<Args>(args)...);
+}
+
 #define LEO_CUDA_CHECK(x)                                      \
   do {                                                         \
     cudaError_t _e = (x);                                      \

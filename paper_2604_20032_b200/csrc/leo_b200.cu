@@ -373,8 +373,12 @@ int build_graph_impl(const LeoKernel* kk, const LeoCaps* caps, LeoEdges* out, Le
       // half the SMs: the run time is the longest item's, and the other half
       // stays free for the reach tier running beside it
       const char* wcc = getenv("LEO_WC_CTAS");
-      const int wc_ctas = wcc ? atoi(wcc) : std::max(1, SM / 2);
-      TRACED(KID_SYNC, leo_launch(k_sync_wc_smem, wc_ctas, wc_threads, wc_smem, st, k, sa, bev, wc_steps));
+      // CTAs in clusters of LEO_WC_CLUSTER (default 2): the image is staged once
+      // per cluster by TMA multicast
+      const char* wcl = getenv("LEO_WC_CLUSTER");
+      const int csz = std::max(1, std::min(8, wcl ? atoi(wcl) : 2));
+      const int wc_ctas = std::max(csz, ((wcc ? atoi(wcc) : std::max(1, SM / 2)) / csz) * csz);
+      TRACED(KID_SYNC, leo_launch_cluster(k_sync_wc_smem, wc_ctas, csz, wc_threads, wc_smem, st, k, sa, bev, wc_steps));
     }
     else
       TRACED(KID_SYNC, leo_launch(k_sync<false>, grid_for(N, 64), 64, 0, st, k, sa, nullptr, 0));
@@ -474,7 +478,7 @@ int build_graph_impl(const LeoKernel* kk, const LeoCaps* caps, LeoEdges* out, Le
   } else {
     // tier 1 is persistent: enough CTAs to fill the chip, queries fetched dynamically
     // geometry A/B knob LEO_T1 (profiling only): 0 i32/128, 1 u16/128, 2 u16/64, 3 i32/64
-    static const int t1 = getenv("LEO_T1") ? atoi(getenv("LEO_T1")) : 2;
+    const int t1 = getenv("LEO_T1") ? atoi(getenv("LEO_T1")) : 2;
     const bool narrow = B < 0xFFFF && t1 != 0 && t1 != 3;
     auto f = k_reach_fast<int32_t, 128, 96>;
     int slots = 128, kb = 4;
@@ -650,10 +654,12 @@ struct AddrBufs {
   uint2 *la, *lb;
   int32_t* ep;
   uint8_t* ok;
+  int32_t* flags;       // [3] k_mp_coop round flags
 };
 void want_addr(Arena& ar, AddrBufs& b, int N, int64_t edge_cap) {
   want_incoming(ar, b.bb, N, 1);
   ar.want(&b.la, N); ar.want(&b.lb, N); ar.want(&b.ok, N); ar.want(&b.ep, std::max<int64_t>(edge_cap, 1));
+  ar.want(&b.flags, 4);
 }
 // The labels pack a 24-bit instruction id (kMpT): kernels of >= 2^24
 // instructions take the exact per-candidate BFS tiers instead (mp_ok = null).
@@ -664,6 +670,25 @@ Incoming addr_impl(const KView& k, const LeoEdges* base, AddrBufs& b, LeoTrace* 
   const int g = grid_for(k.N, 128);
   TRACED(KID_SELF_ADDR, leo_launch(k_mp_edges, grid_for(base->capacity, 256, num_sms() * 8), 256, 0, st, k,
                                    base->n_regular, (int64_t)base->capacity, base->prod, base->meta, b.ep));
+  if (getenv("LEO_MP_COOP")) {
+    // one cooperative kernel, in-place rounds until nothing changes.  Opt-in:
+    // its grid holds every SM for the whole search and starves the pruning
+    // branch it runs beside (C5 +245 us, measured A/B)
+    static int coop_grid[64] = {};
+    int dev = 0;
+    cudaGetDevice(&dev);
+    if (!coop_grid[dev & 63]) {
+      int per = 0;
+      cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, k_mp_coop, 256, 0);
+      coop_grid[dev & 63] = std::max(1, per) * num_sms();
+    }
+    const int grid = std::max(1, std::min(coop_grid[dev & 63], grid_for(k.N, 256, 1 << 30)));
+    KView kv = k;
+    int32_t* flags = b.flags;
+    void* args[] = {&kv, (void*)&binc.rbeg, (void*)&binc.rend, &b.ep, &b.la, &flags, &b.ok};
+    TRACED(KID_SELF_ADDR, cudaLaunchCooperativeKernel((void*)k_mp_coop, grid, 256, args, 0, st));
+    return binc;
+  }
   TRACED(KID_SELF_ADDR, leo_launch(k_mp_round, g, 128, 0, st, k, binc.rbeg, binc.rend, b.ep, b.la, b.la, 1));
   for (int r = 1; r < 7; r++) {
     const uint2* in = (r & 1) ? b.la : b.lb;
@@ -725,6 +750,13 @@ int blame_impl(const LeoKernel* kk, const LeoProfile* pp, const LeoEdges* pruned
   ar.want(&slow2, cap_slow);
   ar.want(&ctr, 4); ar.want(&scan_tmp, scan_scratch_ints(std::max(N, 1)) + 64);
   ar.want(&slow_scr, (int64_t)BW * 2 * (N + 1)); ar.want(&jtotal, N); ar.want(&jnsum, N);
+  // staged edge entries (pass 0): at most one per pruned edge
+  const bool two_pass = getenv("LEO_BLAME_2PASS") != nullptr;   // A/B: recompute in pass 1
+  const int64_t stg_cap = two_pass ? 1 : std::max<int64_t>(pruned->capacity, 1);
+  int32_t *stg_off, *stg_edge, *stg_cause;
+  double *stg_blame, *stg_fac;
+  ar.want(&stg_off, N); ar.want(&stg_edge, stg_cap); ar.want(&stg_cause, stg_cap);
+  ar.want(&stg_blame, stg_cap); ar.want(&stg_fac, 4 * stg_cap);
   LEO_CUDA_CHECK(ar.commit());
   cudaMemsetAsync(ctr, 0, 16, st);
   // the slow self-blame worker's stamps matter only when it runs (no
@@ -737,7 +769,8 @@ int blame_impl(const LeoKernel* kk, const LeoProfile* pp, const LeoEdges* pruned
   const uint8_t* mp_ok = (dbg & LEO_DBG_SELF_SLOW) || !mp_labels_fit(N) ? nullptr : (own_addr ? ab.ok : mp_ok_pre);
   BlameArgs a{dbg, mp_ok, own, p, pruned->prod, pruned->meta, paths->dist, inc, binc.rbeg, binc.rend,
               base ? base->prod : nullptr, base ? base->meta : nullptr,
-              ecount, self_sub, jtotal, jnsum, eoff, *out, slow_list, &ctr[0], cap_slow, status, nullptr, nullptr, 0};
+              ecount, self_sub, jtotal, jnsum, eoff, *out, slow_list, &ctr[0], cap_slow, status, nullptr, nullptr, 0,
+              stg_off, &ctr[2], two_pass ? 0 : stg_cap, stg_edge, stg_cause, stg_blame, stg_fac};
   const bool lines_on = line_id && line_blame && line_stall && n_lines > 0;
   if (lines_on && !(caps && (caps->options & LEO_OPT_ACCUMULATE_LINES))) {
     a.zero_lb = line_blame; a.zero_ls = line_stall; a.n_lines = n_lines;
@@ -748,11 +781,18 @@ int blame_impl(const LeoKernel* kk, const LeoProfile* pp, const LeoEdges* pruned
     TRACED(KID_SELFBLAME_SLOW, leo_launch(k_selfblame_slow, 1, BW, 0, st, k, a, slow2, &ctr[1], slow_scr, BW));
   }
   TRACED(KID_SCAN, scan_exclusive(ecount, eoff, nullptr, N, scan_tmp, nullptr, st));
-  TRACED(KID_BLAME_FILL, leo_launch(k_blame<1>, grid_for(N, 128), 128, 0, st, k, a));
-  // (k_blame<1> also wrote the entry count and zeroed the line vectors)
-  if (lines_on) {
-    TRACED(KID_LINES, leo_launch(k_lines, grid_for(std::max<int64_t>(out->capacity, N), 256), 256, 0, st, k, p, own, pruned->prod, *out,
-                                                                               line_id, line_blame, line_stall));
+  if (two_pass) {
+    TRACED(KID_BLAME_FILL, leo_launch(k_blame<1>, grid_for(N, 128), 128, 0, st, k, a));
+    // (k_blame<1> also wrote the entry count)
+    if (lines_on) {
+      TRACED(KID_LINES, leo_launch(k_lines, grid_for(std::max<int64_t>(out->capacity, N), 256), 256, 0, st, k, p, own, pruned->prod, *out,
+                                                                                 line_id, line_blame, line_stall));
+    }
+  } else {
+    // staged entries into stalled order + the line rollup, one pass
+    TRACED(KID_BLAME_FILL, leo_launch(k_blame_compact, grid_for(N, 256), 256, 0, st, k, a,
+                                      lines_on ? line_id : nullptr, lines_on ? line_blame : nullptr,
+                                      lines_on ? line_stall : nullptr));
   }
   ar.release();
   LEO_CUDA_CHECK(cudaGetLastError());
@@ -779,8 +819,8 @@ static int bin_impl(const LeoSamples* s, int32_t n_instr, int32_t* lat, int32_t*
   // big streams: one pass, per-CTA shared-memory hash (LEO_BIN_BUCKETED=1: the bucketed passes)
   if (S >= (4ll << 20) && (int64_t)n_instr * 8 < 0xFFFFFFFFll && !getenv("LEO_BIN_BUCKETED")) {
     // table geometry (A/B knobs LEO_BIN_SLOTS / LEO_BIN_PROBE; profiling only)
-    static const int slots = getenv("LEO_BIN_SLOTS") ? atoi(getenv("LEO_BIN_SLOTS")) : 16384;
-    static const int probe = getenv("LEO_BIN_PROBE") ? atoi(getenv("LEO_BIN_PROBE")) : 2;
+    const int slots = getenv("LEO_BIN_SLOTS") ? atoi(getenv("LEO_BIN_SLOTS")) : 16384;
+    const int probe = getenv("LEO_BIN_PROBE") ? atoi(getenv("LEO_BIN_PROBE")) : 2;
     auto f = k_bin_hash<26624, 4>;
     int threads = 1024, per_sm = 1;
     if (slots == 8192) { f = probe == 8 ? k_bin_hash<8192, 8> : k_bin_hash<8192, 4>; threads = 512; per_sm = 3; }
@@ -1163,7 +1203,7 @@ int leo_analyze(const LeoKernel* k, const LeoProfile* p, const LeoSamples* sampl
     dbg_delay("LEO_DBG_DELAY_BIN", s_bin);
     // small streams bin at the least priority; a big stream (C5) is itself a
     // long branch and keeps the default
-    static const int bin_lo = getenv("LEO_BIN_LOWPRIO") ? atoi(getenv("LEO_BIN_LOWPRIO")) : -1;
+    const int bin_lo = getenv("LEO_BIN_LOWPRIO") ? atoi(getenv("LEO_BIN_LOWPRIO")) : -1;
     LowPriority low_prio(bin_lo >= 0 ? bin_lo == 1 : samples->n_samples <= (16ll << 20));
     return bin_impl(samples, k->n_instr, (int32_t*)p->lat, (int32_t*)p->cls_cnt, status, tr, s_bin);
   };

@@ -20,8 +20,25 @@ namespace leo {
 
 LEO_DEV uint32_t smem_addr(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
 
+LEO_DEV uint32_t cluster_ctarank() {
+  uint32_t r;
+  asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
+  return r;
+}
+LEO_DEV uint32_t cluster_nctarank() {
+  uint32_t r;
+  asm volatile("mov.u32 %0, %%cluster_nctarank;" : "=r"(r));
+  return r;
+}
+// every thread of every CTA of the cluster
+LEO_DEV void cluster_sync_all() {
+  asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
+}
+
 struct StageBar {
   uint64_t* bar;
+  uint16_t mc_mask;            // != 0: cluster multicast (rank 0 issues, every CTA receives)
+  uint32_t mc_rank;
   uint32_t phase;
   uint32_t tx;                 // bytes in flight this phase (thread 0's view)
   // bulk copies queued by thread 0 (issued after expect_tx)
@@ -30,13 +47,23 @@ struct StageBar {
   uint32_t len[8];
   int n;
 
-  LEO_DEV void init(uint64_t* b) {
-    bar = b; phase = 0; tx = 0; n = 0;
+  // multicast: the CTAs of a thread-block cluster stage the same image; CTA
+  // rank 0 issues each bulk copy once with .multicast::cluster and it lands at
+  // the same offset in every CTA's shared memory, completing on every CTA's
+  // own mbarrier (one L2 / HBM fetch per cluster instead of one per CTA).
+  LEO_DEV void init(uint64_t* b, bool multicast = false) {
+    bar = b; phase = 0; tx = 0; n = 0; mc_mask = 0; mc_rank = 0;
+    if (multicast) {
+      const uint32_t nc = cluster_nctarank();
+      if (nc > 1) { mc_mask = (uint16_t)((1u << nc) - 1u); mc_rank = cluster_ctarank(); }
+    }
     if (threadIdx.x == 0) {
       asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" :: "r"(smem_addr(bar)) : "memory");
       asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
     __syncthreads();
+    // every CTA's barrier exists before the leader's copies can signal it
+    if (mc_mask) cluster_sync_all();
   }
   // Generic-proxy writes to the destination (previous round) must be ordered
   // before the async-proxy (TMA) writes of the next round.
@@ -76,9 +103,17 @@ struct StageBar {
     if (threadIdx.x == 0) {
       asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;"
                    :: "r"(smem_addr(bar)), "r"(tx) : "memory");
-      for (int i = 0; i < n; i++)
-        asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];"
-                     :: "r"(smem_addr(dst[i])), "l"(src[i]), "r"(len[i]), "r"(smem_addr(bar)) : "memory");
+      if (!mc_mask) {
+        for (int i = 0; i < n; i++)
+          asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];"
+                       :: "r"(smem_addr(dst[i])), "l"(src[i]), "r"(len[i]), "r"(smem_addr(bar)) : "memory");
+      } else if (mc_rank == 0) {
+        for (int i = 0; i < n; i++)
+          asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.multicast::cluster"
+                       " [%0], [%1], %2, [%3], %4;"
+                       :: "r"(smem_addr(dst[i])), "l"(src[i]), "r"(len[i]), "r"(smem_addr(bar)), "h"(mc_mask)
+                       : "memory");
+      }
     }
     uint32_t done = 0;
     while (!done) {

@@ -870,7 +870,7 @@ __global__ void k_sync_wc_smem(KView k, SyncArgs a, const uint32_t* __restrict__
   for (int x = threadIdx.x; x < W * T; x += T) pbits[x] = 0u;
   PhaseMarks pm(a.dbg);
   StageBar sb;
-  sb.init(bar);
+  sb.init(bar, true);                          // one fetch per cluster (launched with a cluster dim)
   sb.begin();
   sb.copy(ww, a.wcword, (size_t)N * 4);
   sb.copy(bf, k.blk_first, (size_t)B * 4);

@@ -85,11 +85,18 @@ def test_device_matches_oracle_synthetic(tag, scale, cuda):
     ("c3", {"LEO_SYNC_FORK_AT": "2", "LEO_RU_PARTS": "1", "LEO_PRUNE_THREADS": "128"}),
     ("c3", {"LEO_SETTER_GLOBAL": "1"}),
     ("c5", {"LEO_SETTER_GLOBAL": "1"}),
+    ("c5", {"LEO_T1": "0", "LEO_BIN_SLOTS": "8192", "LEO_BIN_PROBE": "8"}),
+    ("c5", {"LEO_T1": "1", "LEO_BIN_SLOTS": "26624", "LEO_BIN_PROBE": "4", "LEO_SCAN_TILED": "1"}),
+    ("c5", {"LEO_T1": "3", "LEO_BLAME_2PASS": "1", "LEO_BIN_LOWPRIO": "1", "LEO_MP_COOP": "1"}),
+    ("c2", {"LEO_BLAME_2PASS": "1", "LEO_SCAN_TILED": "1", "LEO_WC_CLUSTER": "1", "LEO_MP_COOP": "1"}),
+    ("c2", {"LEO_WC_CLUSTER": "8", "LEO_WC_CTAS": "64"}),
 ])
 def test_device_schedule_knobs_exact(tag, knobs, cuda, monkeypatch):
     """The scheduling knobs (fork points, CTAs per unit, waitcnt tier size
-    and step limit, prune CTA size) move work between tiers and branches; the
-    results must not move.  Half-size C2 / C3 against the oracle."""
+    and step limit, prune CTA size, tier-1 reach table geometry, binning
+    table geometry, one- vs two-pass blame, one-launch vs tiled scans) move
+    work between tiers and branches; the results must not move.  Half-size
+    C2 / C3 and 5 % C5 against the oracle."""
     from oracle import oracle
     from paper_2604_20032_b200 import abi, device, synth
     for k, v in knobs.items():

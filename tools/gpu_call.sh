@@ -41,6 +41,11 @@ if [[ $WHAT == all || $WHAT == ncu ]]; then
      -k 'regex:k_(bin_|reach_|block_walk|prune_edges|slice|mp_round|link|sync|blame|lines|compact)' -s 0 -c 40 \
      -o $OUT/${TAG}_c5_full -f python tools/profile_step.py c5 --steps 1 --warmup 0 > $OUT/${TAG}_ncu_full.txt 2>&1
   echo "ncu full rc=$?"; tail -3 $OUT/${TAG}_ncu_full.txt
+  # gpurun merges <= 64 MiB back: keep the raw metrics page and hot lines, drop the report
+  ncu -i $OUT/${TAG}_c5_full.ncu-rep --page raw --csv > $OUT/${TAG}_c5_full_raw.csv 2>/dev/null
+  python tools/ncu_lines.py $OUT/${TAG}_c5_full.ncu-rep 'k_(bin_hash|reach_fast|prune_edges|sync|block_walk|blame|mp_)' 25 \
+     > $OUT/${TAG}_c5_hotlines.txt 2>&1
+  rm -f $OUT/${TAG}_c5_full.ncu-rep
 fi
 if [[ $WHAT == all || $WHAT == ncu4 ]]; then
   timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none --csv \
@@ -50,4 +55,6 @@ if [[ $WHAT == all || $WHAT == ncu4 ]]; then
      -k 'regex:k_(bin_|reach_|block_walk|prune_edges|slice|mp_round|link|sync|blame|lines|compact)' -s 0 -c 40 \
      -o $OUT/${TAG}_c4_full -f python tools/profile_step.py c4 --steps 1 --warmup 0 > $OUT/${TAG}_ncu4_full.txt 2>&1
   echo "ncu c4 full rc=$?"; tail -3 $OUT/${TAG}_ncu4_full.txt
+  ncu -i $OUT/${TAG}_c4_full.ncu-rep --page raw --csv > $OUT/${TAG}_c4_full_raw.csv 2>/dev/null
+  rm -f $OUT/${TAG}_c4_full.ncu-rep
 fi

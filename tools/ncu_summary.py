@@ -53,8 +53,12 @@ def launches(path: Path):
 
 
 def full_metrics(rep: Path):
-    out = subprocess.run(["ncu", "-i", str(rep), "--page", "raw", "--csv"], capture_output=True,
-                         text=True).stdout
+    """--set full metrics from an .ncu-rep or its exported raw page (.csv)."""
+    if str(rep).endswith(".csv"):
+        out = Path(rep).read_text()
+    else:
+        out = subprocess.run(["ncu", "-i", str(rep), "--page", "raw", "--csv"], capture_output=True,
+                             text=True).stdout
     rows = list(csv.reader(io.StringIO(out)))
     h = rows[0]
     want = ["Kernel Name", "gpu__time_duration.sum", "dram__bytes_read.sum", "dram__bytes_write.sum",
@@ -62,7 +66,9 @@ def full_metrics(rep: Path):
             "smsp__thread_inst_executed_per_inst_executed.ratio", "launch__grid_size",
             "launch__block_size", "launch__shared_mem_per_block_dynamic", "launch__registers_per_thread",
             "l1tex__t_sectors_pipe_lsu_mem_global_op_ld.sum", "l1tex__t_requests_pipe_lsu_mem_global_op_ld.sum",
-            "smsp__inst_executed.sum", "sm__cycles_active.avg", "smsp__cycles_active.max"]
+            "smsp__inst_executed.sum", "sm__cycles_active.avg", "smsp__cycles_active.max",
+            "smsp__issue_active.avg.pct_of_peak_sustained_active",
+            "l1tex__data_bank_conflicts_pipe_lsu_mem_shared.sum"]
     units = rows[1]
     idx = [h.index(w) for w in want if w in h]
     recs = []
