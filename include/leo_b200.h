@@ -30,6 +30,7 @@
  *   leo_trace_chain          <- analysis.trace_chain           analysis.py:499-538
  *   leo_rank_hotspots        <- report.rank_hotspots           report.py:96-109
  *   leo_line_rollup          <- per-source-line rollup of any blame list
+ *   leo_line_compact         <- the touched lines of a rollup as a sparse list (read-back)
  *   leo_report               <- report.build_report assembly   report.py:132-199
  *
  * Conventions
@@ -358,6 +359,14 @@ int leo_liveness_filter(const LeoKernel* k, const LeoEdges* links, uint8_t* keep
 int leo_line_rollup(const LeoKernel* k, const LeoProfile* p, int32_t n_entries, const int32_t* stalled,
                     const int32_t* cause, const double* blame, const int32_t* line_id, int32_t n_lines,
                     double* line_blame, double* line_stall, void* stream);
+
+/* The lines a result touches, as a sparse list for read-back: every line x
+ * with line_blame[x] != 0 or line_stall[x] != 0, ascending, into line_ids /
+ * blame_out / stall_out (capacity entries; *count = the number of such lines,
+ * which may exceed capacity: re-run bigger).  A service reads back these
+ * instead of the dense per-line vectors (4.3 M lines at C5's line table). */
+int leo_line_compact(const double* line_blame, const double* line_stall, int32_t n_lines, int32_t capacity,
+                     int32_t* line_ids, double* blame_out, double* stall_out, int32_t* count, void* stream);
 
 /* reaching_definitions(cfg) (depgraph.py:135-177): the reach-in set of every
  * (block b, unit u) pair, as the CSR defs[set_off[b*U+u] .. set_off[b*U+u+1])

@@ -25,7 +25,7 @@ _lib = None
 ENTRY_POINTS = ("leo_bin_samples", "leo_build_graph", "leo_prune", "leo_slice", "leo_blame",
                 "leo_analyze", "leo_report", "leo_self_blame", "leo_coverage", "leo_rank_hotspots",
                 "leo_trace_chain", "leo_liveness_filter", "leo_reaching_definitions",
-                "leo_line_rollup")
+                "leo_line_rollup", "leo_line_compact")
 
 
 class LeoLibraryError(RuntimeError):
@@ -59,6 +59,7 @@ def lib():
                                   C.c_int32, P, P, P, P, P]
     L.leo_line_rollup.argtypes = [C.POINTER(abi.LeoKernel), C.POINTER(abi.LeoProfile), C.c_int32,
                                   P, P, P, P, C.c_int32, P, P, P]
+    L.leo_line_compact.argtypes = [P, P, C.c_int32, C.c_int32, P, P, P, P, P]
     L.leo_liveness_filter.argtypes = [C.POINTER(abi.LeoKernel), C.POINTER(abi.LeoEdges), P, P]
     L.leo_reaching_definitions.argtypes = [C.POINTER(abi.LeoKernel), C.POINTER(abi.LeoCaps),
                                            C.POINTER(abi.LeoReachIn), P, P]

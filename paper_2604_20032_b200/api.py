@@ -43,7 +43,7 @@ import weakref
 import numpy as np
 import torch
 
-from . import abi, device, diagnostics, ops, report, soa, types
+from . import _lib, abi, device, diagnostics, ops, report, soa, types
 from . import enums as E
 
 _DEVICE = None
@@ -694,24 +694,39 @@ class Session:
         """Size the buffers with an eager run, then capture one CUDA graph:
         H2D of the kernel SoA and profile metadata, the fused pipeline (whose
         binning branch pulls the pinned sample stream while the graph is being
-        built), and D2H of the counters and per-line vectors."""
+        built), the sparse per-line list (leo_line_compact), and D2H of the
+        counters, the touched lines and the blame entries."""
         self._h2d()
         self.an.run(self.dp, self.cfg, self.ds)
         self.an.ensure_workspace()
         self.an.run(self.dp, self.cfg, self.ds)
         an = self.an
+        L = int(an.line_blame.numel())
+        self.n_lines = L
+        self.d_lid = torch.empty(max(L, 1), dtype=torch.int32, device=self.dev)
+        self.d_lb = torch.empty(max(L, 1), dtype=torch.float64, device=self.dev)
+        self.d_ls = torch.empty(max(L, 1), dtype=torch.float64, device=self.dev)
+        self.d_lcnt = torch.zeros(1, dtype=torch.int32, device=self.dev)
+        self._compact_lines()
+        torch.cuda.synchronize(self.dev)
         self.h_ctr = self._pinned(an.ctr)
-        self.h_lb = self._pinned(an.line_blame)
-        self.h_ls = self._pinned(an.line_stall)
+        self.h_lcnt = self._pinned(self.d_lcnt)
+        self.h_lid = self._pinned(self.d_lid)
+        self.h_lb = self._pinned(self.d_lb)
+        self.h_ls = self._pinned(self.d_ls)
         cap = an.caps.blame
-        # blame entries: the graph copies a prefix sized from this sizing run
-        # (the count is a device value); a longer result copies its tail
+        # blame entries and touched lines: the graph copies prefixes sized from
+        # this sizing run (the counts are device values); a longer result
+        # copies its tail after the replay
         nbl0 = int(an.counts()[device.C_BLAME])
         self.k_pre = min(cap, int(nbl0 * 1.1) + 256)
+        nl0 = int(self.d_lcnt.item())
+        self.l_pre = min(max(L, 1), int(nl0 * 1.1) + 256)
         self.h_ent = {name: torch.empty(cap * w, dtype=getattr(an, src).dtype).pin_memory()
                       for name, src, w in self.ENTRY_FIELDS}
         # numpy views of the pinned read-back buffers (no per-call tensor ops)
-        self.n_ctr, self.n_lb, self.n_ls = self.h_ctr.numpy(), self.h_lb.numpy(), self.h_ls.numpy()
+        self.n_ctr, self.n_lcnt = self.h_ctr.numpy(), self.h_lcnt.numpy()
+        self.n_lid, self.n_lb, self.n_ls = self.h_lid.numpy(), self.h_lb.numpy(), self.h_ls.numpy()
         self.n_ent = {name: t.numpy() for name, t in self.h_ent.items()}
         g = torch.cuda.CUDAGraph()
         side = torch.cuda.Stream(self.dev)
@@ -720,12 +735,25 @@ class Session:
         with torch.cuda.graph(g, stream=side, capture_error_mode="thread_local"):
             self._h2d()
             an.launch(self.dp, self.cfg, self.ds)
+            self._compact_lines()
             self.h_ctr.copy_(an.ctr, non_blocking=True)
-            self.h_lb.copy_(an.line_blame, non_blocking=True)
-            self.h_ls.copy_(an.line_stall, non_blocking=True)
+            self.h_lcnt.copy_(self.d_lcnt, non_blocking=True)
+            self._copy_lines(0, self.l_pre)
             self._copy_entries(0, self.k_pre)
         torch.cuda.synchronize(self.dev)
         self.graph = g
+
+    def _compact_lines(self):
+        L = self.n_lines
+        rc = _lib.lib().leo_line_compact(device.ptr(self.an.line_blame), device.ptr(self.an.line_stall), L, L,
+                                         device.ptr(self.d_lid), device.ptr(self.d_lb), device.ptr(self.d_ls),
+                                         device.ptr(self.d_lcnt),
+                                         torch.cuda.current_stream(self.dev).cuda_stream)
+        _lib.check(rc, "leo_line_compact")
+
+    def _copy_lines(self, lo, hi):
+        for h, d in ((self.h_lid, self.d_lid), (self.h_lb, self.d_lb), (self.h_ls, self.d_ls)):
+            h[lo:hi].copy_(d[lo:hi], non_blocking=True)
 
     # self-contained blame entries read back per call: stalled, cause (-1 =
     # self), the cause edge's meta word (kind, dep class, register), SelfBlame
@@ -740,21 +768,34 @@ class Session:
     def _entry_bytes(self, n):
         return sum(n * w * self.h_ent[name].element_size() for name, _, w in self.ENTRY_FIELDS)
 
-    def _result(self, ent, nbl, lb, ls):
-        out = {name: ent[name][:nbl * w].copy() for name, _, w in self.ENTRY_FIELDS}
+    @staticmethod
+    def dense_lines(r: dict, n_lines: int):
+        """(line_blame, line_stall) as dense f64[n_lines] vectors from a result."""
+        lb = np.zeros(n_lines)
+        ls = np.zeros(n_lines)
+        lb[r["line_ids"]] = r["line_blame"]
+        ls[r["line_ids"]] = r["line_stall"]
+        return lb, ls
+
+    def _result(self, ent, nbl, lid, lb, ls, copy):
+        cp = (lambda a: a.copy()) if copy else (lambda a: a)
+        out = {name: cp(ent[name][:nbl * w]) for name, _, w in self.ENTRY_FIELDS}
         out["e_meta"] = out["e_meta"].view(np.uint32)
         out["e_factors"] = out["e_factors"].reshape(-1, 4)
-        out["line_blame"], out["line_stall"] = lb, ls
+        out["line_ids"], out["line_blame"], out["line_stall"] = cp(lid), cp(lb), cp(ls)
         return out
 
-    def analyze(self, allreduce=None):
+    def analyze(self, allreduce=None, copy: bool = False):
         """Copy staged inputs in, run, copy results out.  Returns a host dict
         of self-contained blame entries (e_stalled, e_cause, e_meta, e_sub,
-        e_blame, e_factors) and the per-line vectors.  `allreduce(line_blame,
-        line_stall)` (multi-GPU) runs on the device line vectors before they
-        are read back.  Single-GPU calls replay one CUDA graph (H2D + pipeline
-        + D2H of counters, line vectors and the entries' expected prefix); the
-        rest of the entries is read back at the device-reported count."""
+        e_blame, e_factors) and the touched source lines (line_ids ascending,
+        with their line_blame / line_stall totals; `dense_lines` expands them).
+        The arrays are views of the session's pinned read-back buffers, valid
+        until the next call (`copy=True` returns owned copies).
+        `allreduce(line_blame, line_stall)` (multi-GPU) runs on the device
+        line vectors before they are read back.  Single-GPU calls replay one
+        CUDA graph (H2D + pipeline + D2H of counters, touched lines and the
+        entries' expected prefix); longer results read back their tail."""
         if allreduce is None and self.use_graph:
             if getattr(self, "graph", None) is None:
                 self._capture()
@@ -762,13 +803,17 @@ class Session:
             torch.cuda.current_stream(self.dev).synchronize()
             c = self.n_ctr
             nbl = int(c[device.C_BLAME])
-            if c[device.C_STATUS] == 0 and nbl <= self.an.caps.blame:
-                if nbl > self.k_pre:              # tail beyond the in-graph prefix
-                    self._copy_entries(self.k_pre, nbl)
+            nl = int(self.n_lcnt[0])
+            if c[device.C_STATUS] == 0 and nbl <= self.an.caps.blame and nl <= self.n_lines:
+                if nbl > self.k_pre or nl > self.l_pre:   # tails beyond the in-graph prefixes
+                    if nbl > self.k_pre:
+                        self._copy_entries(self.k_pre, nbl)
+                    if nl > self.l_pre:
+                        self._copy_lines(self.l_pre, nl)
                     torch.cuda.current_stream(self.dev).synchronize()
-                self.last_d2h = (c.nbytes + self.h_lb.numel() * 8 + self.h_ls.numel() * 8
+                self.last_d2h = (c.nbytes + 4 + 20 * max(nl, self.l_pre)
                                  + self._entry_bytes(max(nbl, self.k_pre)))
-                return self._result(self.n_ent, nbl, self.n_lb.copy(), self.n_ls.copy())
+                return self._result(self.n_ent, nbl, self.n_lid[:nl], self.n_lb[:nl], self.n_ls[:nl], copy)
             self.graph = None                  # overflow: grow eagerly, recapture next call
         self._h2d()
         self.an.launch(self.dp, self.cfg, self.ds)
@@ -788,7 +833,9 @@ class Session:
         torch.cuda.current_stream(self.dev).synchronize()
         self.last_d2h = (sum(t.numel() * t.element_size() for t in ent.values()) + c.nbytes
                          + lb.numel() * 8 + ls.numel() * 8)
-        return self._result({k: v.numpy() for k, v in ent.items()}, nbl, lb.numpy(), ls.numpy())
+        lbn, lsn = lb.numpy(), ls.numpy()
+        lid = np.flatnonzero((lbn != 0) | (lsn != 0)).astype(np.int32)
+        return self._result({k: v.numpy() for k, v in ent.items()}, nbl, lid, lbn[lid], lsn[lid], True)
 
 
 # --------------------------------------------------------------------------

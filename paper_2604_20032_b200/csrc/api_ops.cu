@@ -17,9 +17,29 @@
 //   k_reach_claim_all reaching_definitions (:135-177) for every (block, unit):
 //                     the production query search run on all pairs, exported
 //                     as a CSR of reach-in sets
+//   k_line_flag / k_line_scatter  the per-line totals as a sparse list (the
+//                     lines a kernel touches), stable order, for read-back
 #include "prims.cuh"
 
 namespace leo {
+
+__global__ void k_line_flag(int n, const double* __restrict__ lb, const double* __restrict__ ls,
+                            int32_t* __restrict__ flag) {
+  pdl_wait();
+  for (int x = blockIdx.x * blockDim.x + threadIdx.x; x < n; x += gridDim.x * blockDim.x)
+    flag[x] = (lb[x] != 0.0 || ls[x] != 0.0) ? 1 : 0;
+}
+
+__global__ void k_line_scatter(int n, const double* __restrict__ lb, const double* __restrict__ ls,
+                               const int32_t* __restrict__ off, int32_t cap, int32_t* __restrict__ ids,
+                               double* __restrict__ lb_out, double* __restrict__ ls_out, int32_t* count) {
+  pdl_wait();
+  for (int x = blockIdx.x * blockDim.x + threadIdx.x; x < n; x += gridDim.x * blockDim.x) {
+    const int o = off[x];
+    if (off[x + 1] != o && o < cap) { ids[o] = x; lb_out[o] = lb[x]; ls_out[o] = ls[x]; }
+  }
+  if (blockIdx.x == 0 && threadIdx.x == 0) *count = off[n];
+}
 
 __global__ void k_gather_edges(const int32_t* __restrict__ n_dev, const uint64_t* __restrict__ idx,
                                const int32_t* __restrict__ prod, const int32_t* __restrict__ cons,

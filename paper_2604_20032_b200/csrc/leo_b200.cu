@@ -1133,6 +1133,25 @@ int leo_line_rollup(const LeoKernel* k, const LeoProfile* p, int32_t n_entries, 
   return 0;
 }
 
+int leo_line_compact(const double* line_blame, const double* line_stall, int32_t n_lines, int32_t capacity,
+                     int32_t* line_ids, double* blame_out, double* stall_out, int32_t* count, void* stream) {
+  if (n_lines < 0 || capacity < 0 || !line_blame || !line_stall || !line_ids || !blame_out || !stall_out || !count)
+    return -3;
+  cudaStream_t st = (cudaStream_t)stream;
+  Arena ar{st};
+  int32_t *flag, *off, *scr;
+  ar.want(&flag, std::max(n_lines, 1)); ar.want(&off, (int64_t)n_lines + 1);
+  ar.want(&scr, scan_scratch_ints(std::max(n_lines, 1)) + 64);
+  LEO_CUDA_CHECK(ar.commit());
+  leo_launch(k_line_flag, grid_for(std::max(n_lines, 1), 256), 256, 0, st, n_lines, line_blame, line_stall, flag);
+  scan_exclusive(flag, off, nullptr, n_lines, scr, nullptr, st);
+  leo_launch(k_line_scatter, grid_for(std::max(n_lines, 1), 256), 256, 0, st, n_lines, line_blame, line_stall,
+             off, capacity, line_ids, blame_out, stall_out, count);
+  ar.release();
+  LEO_CUDA_CHECK(cudaGetLastError());
+  return 0;
+}
+
 int leo_reaching_definitions(const LeoKernel* k, const LeoCaps* caps, LeoReachIn* out, uint32_t* status,
                              void* stream) {
   WsScope ws_scope(caps);

@@ -39,12 +39,19 @@ def test_session_graph_matches_oracle(tag, scale, cuda):
     sess = api.Session(ks, wl.profile, wl.n_samples, abi.make_config(dialect=ks.dialect), cuda)
     sess.stage(ks, wl.profile, wl.pc, wl.cat, wl.lut)
     o = oracle.run(ks, synth.bin_host(wl), abi.make_config(dialect=ks.dialect))
+    L = len(o.line_blame)
     for call in range(3):                      # capture, then replays
         r = sess.analyze()
         assert sess.graph is not None
         assert full_entries_match(r, o), call
-        np.testing.assert_allclose(r["line_blame"], o.line_blame, rtol=1e-9)
-        np.testing.assert_allclose(r["line_stall"], o.line_stall, rtol=1e-9)
+        assert np.all(np.diff(r["line_ids"]) > 0)          # touched lines, ascending
+        lb, ls = api.Session.dense_lines(r, L)
+        np.testing.assert_allclose(lb, o.line_blame, rtol=1e-9)
+        np.testing.assert_allclose(ls, o.line_stall, rtol=1e-9)
+        nz = np.flatnonzero((o.line_blame != 0) | (o.line_stall != 0))
+        assert np.array_equal(r["line_ids"], nz)
+    owned = sess.analyze(copy=True)            # owned copies survive the next call
+    assert full_entries_match(owned, o)
     # new samples staged into the same pinned buffers: the replay sees them
     rng = np.random.default_rng(5)
     pc2 = rng.permutation(wl.pc)
@@ -54,7 +61,8 @@ def test_session_graph_matches_oracle(tag, scale, cuda):
     o2 = oracle.run(ks, synth.bin_host(wl), abi.make_config(dialect=ks.dialect))
     r = sess.analyze()
     assert full_entries_match(r, o2)
-    np.testing.assert_allclose(r["line_blame"], o2.line_blame, rtol=1e-9)
+    np.testing.assert_allclose(api.Session.dense_lines(r, L)[0], o2.line_blame, rtol=1e-9)
+    assert full_entries_match(owned, o)       # the earlier owned result is untouched
     # the eager path (the multi-GPU call shape, a line all-reduce hook) reads back the same
     r = sess.analyze(allreduce=lambda lb, ls: None)
     assert full_entries_match(r, o2)
