@@ -282,7 +282,11 @@ int build_graph_impl(const LeoKernel* kk, const LeoCaps* caps, LeoEdges* out, Le
   const int walk_warps = std::max(1, walk_ctas) * wpc;
 
   const int RW = 128;        // slow reach workers
-  const int SW = 16;         // slow sync workers
+  // slow sync workers: block-indexed scratch spans the largest batch member;
+  // as many workers as ~192 MB of scratch allows (16..2048)
+  const int sync_bcap = (kk->n_segments > 1 && kk->seg_block) ? std::max(1, (int)kk->max_seg_blocks) : B;
+  const int SW = (int)std::max<int64_t>(16, std::min<int64_t>(2048, ((int64_t)192 << 20) /
+                                        (int64_t)sync_slow_bytes_per_worker(sync_bcap)) & ~(int64_t)15);
   Arena ar{st};
   int32_t *ucnt, *dcnt, *use_ptr, *def_ptr, *ev_res, *q_block, *q_unit, *q_list, *q_off, *q_len, *qres;
   int32_t *ctr, *slow_list, *slow2, *slow3, *cand_cnt, *cand_off, *uniq, *eoff, *ldtab, *scan_tmp, *gtab = nullptr;
@@ -306,7 +310,7 @@ int build_graph_impl(const LeoKernel* kk, const LeoCaps* caps, LeoEdges* out, Le
   ar.want(&reach_scr, (int64_t)RW * 3 * (B + 1));
   ar.want(&scan_tmp2, scan_scratch_ints(std::max<int64_t>(N, 1)) + 64);
   ar.want(&wlist, N); ar.want(&wclist, cap_slow); ar.want(&slow3s, cap_slow);
-  ar.want(&sync_scr, (int64_t)SW * sync_slow_bytes_per_worker(B));
+  ar.want(&sync_scr, (int64_t)SW * sync_slow_bytes_per_worker(sync_bcap));
   const int n_ids = k.dialect == LEO_INTEL ? 32 : 8;
   ar.want(&wcword, N); ar.want(&bev, B); ar.want(&setword, N); ar.want(&lastset, (int64_t)B * n_ids);
   if (!smem_tab) ar.want(&gtab, (int64_t)walk_warps * 2 * U);
@@ -346,14 +350,14 @@ int build_graph_impl(const LeoKernel* kk, const LeoCaps* caps, LeoEdges* out, Le
     cudaStream_t st = s_sync;   // shadows the caller's stream for the TRACED scopes
     cudaMemsetAsync(pcnt, 0, (size_t)std::max(N, 1) * 4, st);
     cudaMemsetAsync(pcur, 0, (size_t)std::max(N, 1) * 4, st);
-    cudaMemsetAsync(sync_scr, 0, (size_t)SW * sync_slow_bytes_per_worker(B), st);
     cudaMemsetAsync(bev, 0, (size_t)std::max(B, 1) * 4, st);
     TRACED(KID_SYNC_PACK, leo_launch(k_sync_pack, grid_for(N, T), T, 0, st, k, wcword, setword, bev));
     if (k.dialect != LEO_AMD && B > 0)
       TRACED(KID_SYNC_PACK, leo_launch(k_block_setters, grid_for(B, T), T, 0, st, k, setword, n_ids, lastset, bev));
     TRACED(KID_SYNC_PACK, leo_launch(k_wait_list, grid_for(N, T), T, 0, st, k, own, wlist, &ctr[8]));
     SyncArgs sa{caps ? caps->debug_flags : 0, skeys, cap_sync, &ctr[3], slow2, &ctr[4], cap_slow, *diags, status,
-                wcword, setword, lastset, n_ids, wlist, &ctr[8], wclist, &ctr[10], 0};
+                wcword, setword, lastset, n_ids, wlist, &ctr[8], wclist, &ctr[10], 0,
+                kk->n_segments > 1 ? kk->seg_block : nullptr, kk->n_segments, sync_bcap};
     const int sdbg = caps ? caps->debug_flags : 0;
     const bool setter_staged = setter_cta_smem(B) <= (size_t)kSmemResidentMax && !getenv("LEO_SETTER_GLOBAL");
     const bool setter_cta = k.dialect != LEO_AMD && B > 0 && !(sdbg & (LEO_DBG_NO_SMEM | LEO_DBG_SYNC_SLOW));
@@ -400,9 +404,9 @@ int build_graph_impl(const LeoKernel* kk, const LeoCaps* caps, LeoEdges* out, Le
         TRACED(KID_SYNC_SLOW, leo_launch(k_sync_setter_smem, SM, 32, kDHBytes, st, k, sa, slow3s, &ctr[11]));
       SyncArgs sb = sa;
       sb.slow_list = slow3s; sb.slow_count = &ctr[11];
-      TRACED(KID_SYNC_SLOW, leo_launch(k_sync<true>, 1, SW, 0, st, k, sb, sync_scr, SW));
+      TRACED(KID_SYNC_SLOW, leo_launch(k_sync<true>, (SW + 63) / 64, 64, 0, st, k, sb, sync_scr, SW));
     } else {
-      TRACED(KID_SYNC_SLOW, leo_launch(k_sync<true>, 1, SW, 0, st, k, sa, sync_scr, SW));
+      TRACED(KID_SYNC_SLOW, leo_launch(k_sync<true>, (SW + 63) / 64, 64, 0, st, k, sa, sync_scr, SW));
     }
     TRACED(KID_KEY_HIST, leo_launch(k_key_hist, grid_for(cap_sync, T), T, 0, st, skeys, &ctr[3], cap_sync, pcnt));
     TRACED(KID_SCAN, scan_exclusive(pcnt, poff, nullptr, N, scan_tmp2, nullptr, st));
@@ -431,7 +435,7 @@ int build_graph_impl(const LeoKernel* kk, const LeoCaps* caps, LeoEdges* out, Le
   while (ru_threads0 > 32 && reach_unit_smem(bcap0, ru_threads0) > (size_t)kSmemResidentMax) ru_threads0 >>= 1;
   const int wdbg = caps ? caps->debug_flags : 0;
   const bool tier0 = B > 0 && U > 0 && reach_unit_smem(bcap0, ru_threads0) <= (size_t)kSmemResidentMax &&
-                     !(wdbg & LEO_DBG_NO_SMEM);
+                     !(wdbg & LEO_DBG_NO_SMEM) && !getenv("LEO_REACH_NO_T0");
   WalkArgs wa{use_ptr, def_ptr, ev_res, q_block, q_unit, tier0 ? nullptr : q_list, &ctr[0], ldtab, qtab, Bp, gtab};
   const size_t smem = walk_bytes(wpc, smem_tab);
   if (B > 0 && U > 0) {     // the walk writes the unit columns sparsely
@@ -469,7 +473,9 @@ int build_graph_impl(const LeoKernel* kk, const LeoCaps* caps, LeoEdges* out, Le
   const char* rp_env = getenv("LEO_RU_PARTS");
   const int ru_parts = n_seg > 1 ? 1 : rp_env ? std::max(1, atoi(rp_env))
                        : U >= SM ? 1 : std::max(1, std::min(8, (3 * SM + 2 * U - 1) / (2 * std::max(U, 1))));
-  const int per_seg = n_seg > 1 ? std::max(1, std::min(U, (4 * SM + n_seg - 1) / n_seg))
+  const char* ps_env = getenv("LEO_RU_PERSEG");
+  const int per_seg = n_seg > 1 ? (ps_env ? std::max(1, std::min(U, atoi(ps_env)))
+                                          : std::max(1, std::min(U, (4 * SM + n_seg - 1) / n_seg)))
                                 : std::min(U, SM * 8) * ru_parts;
   if (tier0) {
     // tier 0: the CFG and one unit's columns resident in shared memory, CTA per unit

@@ -49,7 +49,24 @@ struct SyncArgs {
   int32_t* wc_list;          // waitcnt items for the warp tier
   int32_t* wc_count;
   int32_t defer_search;      // nvidia/intel: block searches all go to k_sync_setter_cta
+  // slow tier scratch geometry: a concatenated batch (LeoKernel.seg_block) is
+  // searched member by member, so a worker's block-indexed scratch spans the
+  // largest member (bcap blocks), addressed relative to the item's member
+  const int32_t* seg_block;  // [n_seg + 1] or null
+  int32_t n_seg;
+  int32_t bcap;
 };
+
+// first block of the batch member holding block b (0 without segments)
+LEO_DEV int seg_base_of(const SyncArgs& a, int b) {
+  if (!a.seg_block || a.n_seg <= 1) return 0;
+  int lo = 0, hi = a.n_seg - 1;                 // largest s with seg_block[s] <= b
+  while (lo < hi) {
+    const int mid = (lo + hi + 1) >> 1;
+    if (a.seg_block[mid] <= b) lo = mid; else hi = mid - 1;
+  }
+  return a.seg_block[lo];
+}
 
 __global__ void k_sync_pack(KView k, uint32_t* __restrict__ wcword, uint8_t* __restrict__ setword,
                             uint32_t* __restrict__ bev) {
@@ -650,18 +667,28 @@ __global__ void k_sync(KView k, SyncArgs a, char* scratch, int nworkers) {
   int fcap = kFrames;
   int32_t *stamp = nullptr, *gdist = nullptr;
   uint64_t* heap = nullptr;
+  const int bcap = SLOW ? a.bcap : k.B;
   if (SLOW) {
-    char* base = scratch + (size_t)start * sync_slow_bytes_per_worker(k.B);
+    char* base = scratch + (size_t)start * sync_slow_bytes_per_worker(bcap);
     fr = (Frame*)base;
-    stamp = (int32_t*)(base + (size_t)(k.B + 2) * sizeof(Frame));
-    gdist = stamp + (k.B + 2);
-    heap = (uint64_t*)(((uintptr_t)(gdist + (k.B + 2)) + 7) & ~(uintptr_t)7);
-    fcap = k.B + 2;
+    stamp = (int32_t*)(base + (size_t)(bcap + 2) * sizeof(Frame));
+    gdist = stamp + (bcap + 2);
+    heap = (uint64_t*)(((uintptr_t)(gdist + (bcap + 2)) + 7) & ~(uintptr_t)7);
+    fcap = bcap + 2;
+    // a worker with items clears its own stamps (no memset of every worker's
+    // scratch ahead of a tier that usually has little to do); the walkers
+    // leave the on-path flags cleared after each item
+    if (start < n_items)
+      for (int x = 0; x < bcap + 2; x++) stamp[x] = 0;
   }
   for (int t = start; t < n_items; t += stride) {
     int i, only = -1;
     if (SLOW) { int it = a.slow_list[t]; i = it >> 6; only = it & 63; }
     else i = a.wait_list[t];
+    // block-indexed scratch relative to the item's batch member
+    const int sbase = SLOW ? seg_base_of(a, k.block_of[i]) : 0;
+    int32_t* stamp_m = SLOW ? stamp - sbase : nullptr;
+    int32_t* gdist_m = SLOW ? gdist - sbase : nullptr;
     if (dialect == LEO_AMD) {
       if (k.sync_kind[i] != LEO_SYNC_WAITCNT) continue;
       for (int counter = 0; counter < 2; counter++) {   // vmcnt before lgkmcnt (:410-415)
@@ -670,7 +697,7 @@ __global__ void k_sync(KView k, SyncArgs a, char* scratch, int nworkers) {
         if (lv == LEO_NONE_U32) continue;
         int best_m = 0;
         bool ok = SLOW ? trace_waitcnt_exact(k, i, counter, (int)min(lv, 0x7FFFFFFFu), a, fr, fcap, best_m,
-                                             stamp, a.wcword)
+                                             stamp_m, a.wcword)
                        : (!(a.dbg & LEO_DBG_SYNC_SLOW) && lv < kWcNone &&
                           trace_waitcnt_one(k, i, counter, (int)lv, a, fr, fcap, best_m));
         if (!ok) {
@@ -703,7 +730,7 @@ __global__ void k_sync(KView k, SyncArgs a, char* scratch, int nworkers) {
         if (only >= 0 && only != id) continue;
         int f;
         if (SLOW) {
-          DijHeap dj{stamp, gdist, heap, t + 1, 0, 4 * k.B + 8};
+          DijHeap dj{stamp_m, gdist_m, heap, t + 1, 0, 4 * bcap + 8};
           f = setter_search(k, i, id, a, dj);
         } else if (a.dbg & LEO_DBG_SYNC_SLOW) {
           f = -1;

@@ -18,21 +18,35 @@ if len(sys.argv) > 1 and sys.argv[1] == "--child":
     from paper_2604_20032_b200 import abi, device, synth
     cfgname, steps = sys.argv[2], int(sys.argv[3])
     dev = torch.device("cuda:0")
-    wl = synth.config_workload(cfgname)
-    dk = device.DeviceKernel(wl.kernel, dev)
-    dp = device.DeviceProfile(wl.profile, wl.kernel.n_instr, dev)
-    ds = device.DeviceSamples(wl.pc, wl.cat, wl.lut, dev)
-    an = device.Analyzer(dk, dev)
-    cfg = abi.make_config(dialect=wl.kernel.dialect)
-    an.run(dp, cfg, ds)
-    an.capture(dp, cfg, ds)
+    if cfgname.startswith("c4"):           # c4:K = the bench's batch pipelines over K kernels
+        from paper_2604_20032_b200 import batch as BT
+        K = int(cfgname.split(":")[1]) if ":" in cfgname else 300
+        lines = synth.LineTable(4096, seed=999)
+        groups = {}
+        for kk in range(K):
+            w = synth.c4_kernel(kk, lines)
+            groups.setdefault(BT.group_key(w), []).append(w)
+        wls = [BT.concat(groups[key]) for key in sorted(groups)]
+    else:
+        wls = [synth.config_workload(cfgname)]
+    ans = []
+    for wl in wls:
+        dk = device.DeviceKernel(wl.kernel, dev)
+        dp = device.DeviceProfile(wl.profile, wl.kernel.n_instr, dev)
+        ds = device.DeviceSamples(wl.pc, wl.cat, wl.lut, dev)
+        an = device.Analyzer(dk, dev)
+        cfg = abi.make_config(dialect=wl.kernel.dialect)
+        an.run(dp, cfg, ds)
+        an.capture(dp, cfg, ds)
+        ans.append((an, dk, dp, ds))
     flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)
     ts = []
     for s in range(steps + 3):
         flush.zero_()
         a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         a.record()
-        an.replay()
+        for x in ans:
+            x[0].replay()
         b.record()
         torch.cuda.synchronize()
         if s >= 3:
