@@ -1024,6 +1024,56 @@ __global__ void k_blame(KView k, BlameArgs a) {
 template __global__ void k_blame<0>(KView, BlameArgs);
 template __global__ void k_blame<1>(KView, BlameArgs);
 
+// Pass 0 split by work: most stalled instructions have no pruned in-edge (C5:
+// 90 %) and take the self verdict, a few loads; the rest are listed for
+// k_blame_edges.  Keeps the light majority out of the register-heavy,
+// divergent Eq. 1 code (k_blame<0>: 94 registers, 6.8 threads / instruction).
+__global__ void k_blame_light(KView k, BlameArgs a, int32_t* __restrict__ list, int32_t* list_count) {
+  pdl_wait();
+  if (a.zero_lb)
+    for (int x = blockIdx.x * blockDim.x + threadIdx.x; x < a.n_lines; x += gridDim.x * blockDim.x) {
+      a.zero_lb[x] = 0.0;
+      a.zero_ls[x] = 0.0;
+    }
+  const int lane = threadIdx.x & 31;
+  for (int j0 = blockIdx.x * blockDim.x + (threadIdx.x & ~31); j0 < k.N; j0 += gridDim.x * blockDim.x) {
+    const int j = j0 + lane;
+    bool edges = false;
+    if (j < k.N) {
+      a.ecount[j] = 0;
+      a.self_sub[j] = -1;
+      if (a.p.lat[j] != 0 && a.own.has(j)) {
+        if (a.inc.deg(j) == 0) blame_self(k, a, j);
+        else edges = true;
+      }
+    }
+    const unsigned m = __ballot_sync(0xffffffffu, edges);
+    if (m) {
+      int base = 0;
+      if (lane == 0) base = atomicAdd(list_count, __popc(m));
+      base = __shfl_sync(0xffffffffu, base, 0);
+      if (edges) list[base + __popc(m & ((1u << lane) - 1))] = j;
+    }
+  }
+}
+
+__global__ void k_blame_edges(KView k, BlameArgs a, const int32_t* __restrict__ list, const int32_t* list_count) {
+  pdl_wait();
+  const int lane = threadIdx.x & 31, n = *list_count;
+  for (int t0 = blockIdx.x * blockDim.x + (threadIdx.x & ~31); t0 < n; t0 += gridDim.x * blockDim.x) {
+    const int t = t0 + lane;
+    const int j = t < n ? list[t] : -1;
+    const bool heavy = j >= 0 && blame_one<0>(k, a, j);
+    unsigned hv = __ballot_sync(0xffffffffu, heavy);
+    while (hv) {
+      const int src = __ffs(hv) - 1;
+      hv &= hv - 1;
+      blame_warp<0>(k, a, __shfl_sync(0xffffffffu, j, src), lane);
+      __syncwarp();
+    }
+  }
+}
+
 // Pass 1 without recomputation: every stalled instruction's entries move from
 // the staging area (pass 0, reservation order) to eoff[j] (stalled order), and
 // the per-line rollup (k_lines) is done on the way: line_blame[line(cause)] +=

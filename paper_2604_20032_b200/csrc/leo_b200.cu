@@ -759,8 +759,9 @@ int blame_impl(const LeoKernel* kk, const LeoProfile* pp, const LeoEdges* pruned
   // staged edge entries (pass 0): at most one per pruned edge
   const bool two_pass = getenv("LEO_BLAME_2PASS") != nullptr;   // A/B: recompute in pass 1
   const int64_t stg_cap = two_pass ? 1 : std::max<int64_t>(pruned->capacity, 1);
-  int32_t *stg_off, *stg_edge, *stg_cause;
+  int32_t *stg_off, *stg_edge, *stg_cause, *elist;
   double *stg_blame, *stg_fac;
+  ar.want(&elist, N);
   ar.want(&stg_off, N); ar.want(&stg_edge, stg_cap); ar.want(&stg_cause, stg_cap);
   ar.want(&stg_blame, stg_cap); ar.want(&stg_fac, 4 * stg_cap);
   LEO_CUDA_CHECK(ar.commit());
@@ -781,7 +782,14 @@ int blame_impl(const LeoKernel* kk, const LeoProfile* pp, const LeoEdges* pruned
   if (lines_on && !(caps && (caps->options & LEO_OPT_ACCUMULATE_LINES))) {
     a.zero_lb = line_blame; a.zero_ls = line_stall; a.n_lines = n_lines;
   }
-  TRACED(KID_BLAME_COUNT, leo_launch(k_blame<0>, grid_for(N, 128), 128, 0, st, k, a));
+  if (two_pass || getenv("LEO_BLAME_UNSPLIT")) {
+    TRACED(KID_BLAME_COUNT, leo_launch(k_blame<0>, grid_for(N, 128), 128, 0, st, k, a));
+  } else {
+    // light pass (self verdicts, list the instructions with edges), then Eq. 1 on the list
+    TRACED(KID_BLAME_COUNT, leo_launch(k_blame_light, grid_for(N, 256), 256, 0, st, k, a, elist, &ctr[3]));
+    TRACED(KID_BLAME_COUNT, leo_launch(k_blame_edges, grid_for(std::max<int64_t>(pruned->capacity, 1), 128), 128, 0, st,
+                                       k, a, elist, &ctr[3]));
+  }
   if (!mp_ok) {
     TRACED(KID_SELFBLAME_WARP, leo_launch(k_selfblame_warp, num_sms(), 128, 4 * kSBWarpInts * 4, st, k, a, slow2, &ctr[1]));
     TRACED(KID_SELFBLAME_SLOW, leo_launch(k_selfblame_slow, 1, BW, 0, st, k, a, slow2, &ctr[1], slow_scr, BW));
