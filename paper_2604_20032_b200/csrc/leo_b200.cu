@@ -782,7 +782,8 @@ int blame_impl(const LeoKernel* kk, const LeoProfile* pp, const LeoEdges* pruned
   if (lines_on && !(caps && (caps->options & LEO_OPT_ACCUMULATE_LINES))) {
     a.zero_lb = line_blame; a.zero_ls = line_stall; a.n_lines = n_lines;
   }
-  if (two_pass || getenv("LEO_BLAME_UNSPLIT")) {
+  // split pass 0 on big kernels only (C5 -35 us, C3 -4; on C2 the extra launch on the chain costs +11 us)
+  if (two_pass || getenv("LEO_BLAME_UNSPLIT") || (N < (1 << 15) && !getenv("LEO_BLAME_SPLIT"))) {
     TRACED(KID_BLAME_COUNT, leo_launch(k_blame<0>, grid_for(N, 128), 128, 0, st, k, a));
   } else {
     // light pass (self verdicts, list the instructions with edges), then Eq. 1 on the list
@@ -840,7 +841,7 @@ static int bin_impl(const LeoSamples* s, int32_t n_instr, int32_t* lat, int32_t*
     if (slots == 8192) { f = probe == 8 ? k_bin_hash<8192, 8> : k_bin_hash<8192, 4>; threads = 512; per_sm = 3; }
     else if (slots == 16384) f = probe == 2 ? k_bin_hash<16384, 2> : k_bin_hash<16384, 4>;
     else f = probe == 2 ? k_bin_hash<26624, 2> : probe == 8 ? k_bin_hash<26624, 8> : k_bin_hash<26624, 4>;
-    const int G = num_sms() * per_sm;
+    const int G = getenv("LEO_BIN_CTAS") ? std::max(1, atoi(getenv("LEO_BIN_CTAS"))) : num_sms() * per_sm;
     TRACED(KID_BIN, leo_launch(f, G, threads, (size_t)slots * 8, st, S, s->pc, s->cat, s->cat_to_cs,
                                n_instr, cls_cnt, status));
     TRACED(KID_BIN_FINALIZE, leo_launch(k_bin_finalize, grid_for(n_instr, 256), 256, 0, st, n_instr, cls_cnt, lat));

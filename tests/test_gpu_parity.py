@@ -89,7 +89,7 @@ def test_device_matches_oracle_synthetic(tag, scale, cuda):
     ("c5", {"LEO_T1": "1", "LEO_BIN_SLOTS": "26624", "LEO_BIN_PROBE": "4", "LEO_SCAN_TILED": "1"}),
     ("c5", {"LEO_T1": "3", "LEO_BLAME_2PASS": "1", "LEO_BIN_LOWPRIO": "1", "LEO_MP_COOP": "1"}),
     ("c2", {"LEO_BLAME_2PASS": "1", "LEO_SCAN_TILED": "1", "LEO_WC_CLUSTER": "1", "LEO_MP_COOP": "1"}),
-    ("c2", {"LEO_WC_CLUSTER": "8", "LEO_WC_CTAS": "64", "LEO_BLAME_UNSPLIT": "1"}),
+    ("c2", {"LEO_WC_CLUSTER": "8", "LEO_WC_CTAS": "64", "LEO_BLAME_SPLIT": "1"}),
     ("c5", {"LEO_BLAME_UNSPLIT": "1", "LEO_BIN_SLOTS": "8192", "LEO_BIN_PROBE": "4"}),
 ])
 def test_device_schedule_knobs_exact(tag, knobs, cuda, monkeypatch):
