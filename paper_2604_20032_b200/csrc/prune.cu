@@ -97,9 +97,20 @@ LEO_DEV int enumerate_paths(const KView& k, int producer, int consumer, double t
         while (i_thr < 0x3fffffff && !(__dadd_rn(e.acc, (double)i_thr) > thr)) i_thr++;
       } else {
         // first step i in [1, i_end] whose accumulation exceeds thr (weights
-        // are >= 0: monotone), else past the run
+        // are >= 0: monotone), else past the run.  One load decides the common
+        // cases: the run's end (or the step before the consumer) within thr
+        // means no step up to there exceeds it; only otherwise binary search.
         const double w0 = wpre[x];
+        const int probe = i_c <= i_end ? i_c - 1 : i_end;
         int lo = 1, hi = i_end + 1;
+        if (probe >= 1 && !(__dadd_rn(e.acc, __dsub_rn(wpre[x + probe], w0)) > thr)) {
+          // consumer in the run and reached within thr: i_thr >= i_c, and any
+          // such value stops the run at the same step (i_stop = min(i_c, i_dep))
+          lo = i_c <= i_end ? i_c : probe + 1;
+          if (i_c <= i_end) hi = lo;
+        } else if (probe >= 1) {
+          hi = probe;
+        }
         while (lo < hi) {
           const int mid = (lo + hi) >> 1;
           if (__dadd_rn(e.acc, __dsub_rn(wpre[x + mid], w0)) > thr) hi = mid; else lo = mid + 1;
