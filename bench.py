@@ -239,7 +239,8 @@ def run_reference(args, ws, rank):
     value = S * len(times) / T
     line = {"impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": ws,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * T / len(times),
-            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "int32/f64",
+            "higher_is_better": True, "scaling": "strong" if args.config in ("c4", "c5") else "weak",
+            "vs_baseline": None, "dtype": "int32/f64",
             "data": "synthetic", "config": workload_config(args),
             "cpu_baseline": {"value": value, "unit": UNIT, "cores": used, "kind": "port",
                              "sample": sample, "host": host_cpu()},
@@ -505,7 +506,10 @@ def run_ours(args, ws, rank, local):
         line = {
             "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": ws, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": T_max / args.steps, "higher_is_better": True,
-            "scaling": "weak", "vs_baseline": None, "dtype": "int32/f64", "data": "synthetic",
+            # C4 shards a fixed batch of 2,000 kernels, C5 a fixed 100 M-sample
+            # kernel by stalled-PC range: strong; C2 / C3 replicas: weak
+            "scaling": "strong" if args.config in ("c4", "c5") else "weak",
+            "vs_baseline": None, "dtype": "int32/f64", "data": "synthetic",
             "config": workload_config(args),
             "run": {"per_rank": plan.mode, "kernels_per_rank": len(plan.items),
                     "n_instr": ks.n_instr, "n_samples_per_step_all_ranks": S_total,

@@ -436,7 +436,8 @@ int build_graph_impl(const LeoKernel* kk, const LeoCaps* caps, LeoEdges* out, Le
   const int wdbg = caps ? caps->debug_flags : 0;
   const bool tier0 = B > 0 && U > 0 && reach_unit_smem(bcap0, ru_threads0) <= (size_t)kSmemResidentMax &&
                      !(wdbg & LEO_DBG_NO_SMEM) && !getenv("LEO_REACH_NO_T0");
-  WalkArgs wa{use_ptr, def_ptr, ev_res, q_block, q_unit, tier0 ? nullptr : q_list, &ctr[0], ldtab, qtab, Bp, gtab};
+  WalkArgs wa{use_ptr, def_ptr, ev_res, q_block, q_unit, tier0 ? nullptr : q_list, &ctr[0], ldtab, qtab, Bp, gtab,
+              rall ? Range{0, 0} : own};
   const size_t smem = walk_bytes(wpc, smem_tab);
   if (B > 0 && U > 0) {     // the walk writes the unit columns sparsely
     cudaMemsetAsync(ldtab, 0xFF, (size_t)Bp * U * 4, st);

@@ -1,6 +1,4 @@
 set -u
 mkdir -p gpurun_out
-python -c "import __graft_entry__ as g; g.build()" > gpurun_out/ab16_build.txt 2>&1 || { tail -20 gpurun_out/ab16_build.txt; exit 1; }
-timeout 1200 python -m pytest tests/test_gpu_parity.py tests/test_gpu_api.py -m gpu -q -x -p no:cacheprovider > gpurun_out/ab16_tests.txt 2>&1; echo "tests rc=$?"; tail -2 gpurun_out/ab16_tests.txt
-timeout 1500 python tools/step_ab.py c5 "X=0" "LEO_T1=1" --reps 3
-timeout 600 python tools/step_ab.py c3 "X=0" --reps 2
+python -c "import __graft_entry__ as g; g.build()" > gpurun_out/ab18_build.txt 2>&1 || { tail -20 gpurun_out/ab18_build.txt; exit 1; }
+timeout 600 python tools/shard_time.py 0 8 --timeline > gpurun_out/ab18_shard_tl.txt 2>&1; echo rc=$?
