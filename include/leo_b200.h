@@ -60,7 +60,7 @@
 extern "C" {
 #endif
 
-#define LEO_ABI_VERSION 2
+#define LEO_ABI_VERSION 3
 
 /* ---- enumerations (indices follow the reference enum definition order) --- */
 /* Dialect  isa.py:19-22 */
@@ -154,6 +154,12 @@ typedef struct LeoSamples {
    * so the transfer of the sample stream overlaps graph construction */
   const int32_t* pc_host;
   const uint8_t* cat_host;
+  /* ABI v3, optional packed stream (kernels below 2^24 instructions): one u32
+   * word per sample, pc << 8 | category (4 bytes instead of 5).  When set,
+   * pc / cat are ignored; packed_host (pinned) is copied into packed on the
+   * binning branch as pc_host / cat_host are. */
+  const uint32_t* packed;
+  const uint32_t* packed_host;
 } LeoSamples;
 
 /* ---- analysis configuration (analysis.py:115-124) ------------------------ */

@@ -569,15 +569,24 @@ class Session:
         self.cfg = config or abi.make_config(dialect=ks.dialect)
         self.dk = device.DeviceKernel(ks, self.dev)
         self.dp = device.DeviceProfile(prof_meta, ks.n_instr, self.dev)
-        self.pc = torch.empty(max(n_samples, 1), dtype=torch.int32, device=self.dev)
-        self.cat = torch.empty(max(n_samples, 1), dtype=torch.uint8, device=self.dev)
+        # raw samples travel packed (one u32 word per sample, pc << 8 | category:
+        # 4 bytes instead of 5) when every pc fits 24 bits
+        self.packed = ks.n_instr < (1 << 24)
+        if self.packed:
+            self.words = torch.empty(max(n_samples, 1), dtype=torch.int32, device=self.dev)
+        else:
+            self.pc = torch.empty(max(n_samples, 1), dtype=torch.int32, device=self.dev)
+            self.cat = torch.empty(max(n_samples, 1), dtype=torch.uint8, device=self.dev)
         self.lut = torch.empty(256, dtype=torch.uint8, device=self.dev)
         self.pin = pin
         self._host = {}
         self.h_pack = None
         if pin:
             self._pack_inputs()
-        self.ds = device.DeviceSamples.from_tensors(self.pc[:n_samples], self.cat[:n_samples], self.lut)
+        if self.packed:
+            self.ds = device.DeviceSamples.from_packed(self.words[:n_samples], self.lut)
+        else:
+            self.ds = device.DeviceSamples.from_tensors(self.pc[:n_samples], self.cat[:n_samples], self.lut)
         self.an = device.Analyzer(self.dk, self.dev)
         self.use_graph = True
         self.graph = None
@@ -663,15 +672,22 @@ class Session:
         self._h("line_id", ks.line_id)
         for n in ("exec_cnt", "total", "eff", "sampled"):
             self._h("p_" + n, getattr(prof_meta, n))
-        self._h("pc", pc)
-        self._h("cat", cat)
         self._h("lut", lut)
         # the library copies the sample stream itself, on the binning branch
-        self.ds.set_host_sources(self._host["pc"], self._host["cat"].view(torch.uint8))
+        if self.packed:
+            if not device.packable(pc):
+                raise ValueError("Session.stage: sample pc out of range (negative or >= 2^24)")
+            self._h("words", device.pack_samples(pc, cat).view(np.int32))
+            self.ds.set_host_packed(self._host["words"])
+        else:
+            self._h("pc", pc)
+            self._h("cat", cat)
+            self.ds.set_host_sources(self._host["pc"], self._host["cat"].view(torch.uint8))
 
     def h2d_bytes(self) -> int:
         if self.h_pack is not None:
-            return self.h_pack.numel() + sum(self._host[n].numel() * self._host[n].element_size() for n in ("pc", "cat"))
+            names = ("words",) if self.packed else ("pc", "cat")
+            return self.h_pack.numel() + sum(self._host[n].numel() * self._host[n].element_size() for n in names)
         return sum(t.numel() * t.element_size() for t in self._host.values())
 
     def _h2d(self):

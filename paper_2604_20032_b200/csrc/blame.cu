@@ -29,9 +29,17 @@ namespace leo {
 
 
 // ---- stage 0 ---------------------------------------------------------------
+// PACKED: the stream is one u32 word per sample, pc << 8 | category (4 B per
+// sample instead of 5; kernels below 2^24 instructions)
+LEO_DEV void unpack4(const uint4 w, int4& p, uint32_t& c) {
+  p = make_int4((int)(w.x >> 8), (int)(w.y >> 8), (int)(w.z >> 8), (int)(w.w >> 8));
+  c = (w.x & 0xFFu) | ((w.y & 0xFFu) << 8) | ((w.z & 0xFFu) << 16) | ((w.w & 0xFFu) << 24);
+}
+
+template <bool PACKED>
 __global__ void k_bin_samples(int64_t S, const int32_t* __restrict__ pc, const uint8_t* __restrict__ cat,
                               const uint8_t* __restrict__ lut, int N, int32_t* __restrict__ cls_cnt,
-                              uint32_t* status) {
+                              uint32_t* status, const uint32_t* __restrict__ packed) {
   pdl_wait();
   __shared__ uint8_t slut[256];
   for (int x = threadIdx.x; x < 256; x += blockDim.x) slut[x] = lut[x];
@@ -42,8 +50,10 @@ __global__ void k_bin_samples(int64_t S, const int32_t* __restrict__ pc, const u
   const int64_t stride = (int64_t)gridDim.x * blockDim.x;
   for (int64_t v = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; v - threadIdx.x < nvec; v += stride) {
     const bool valid = v < nvec;
-    int4 p = valid ? pc4[v] : make_int4(0, 0, 0, 0);
-    uint32_t c = valid ? cat4[v] : 0u;
+    int4 p;
+    uint32_t c;
+    if (PACKED) unpack4(valid ? reinterpret_cast<const uint4*>(packed)[v] : make_uint4(0, 0, 0, 0), p, c);
+    else { p = valid ? pc4[v] : make_int4(0, 0, 0, 0); c = valid ? cat4[v] : 0u; }
     int pcs[4] = {p.x, p.y, p.z, p.w};
 #pragma unroll
     for (int t = 0; t < 4; t++) {
@@ -57,9 +67,9 @@ __global__ void k_bin_samples(int64_t S, const int32_t* __restrict__ pc, const u
   }
   // tail
   for (int64_t s = nvec * 4 + blockIdx.x * (int64_t)blockDim.x + threadIdx.x; s < S; s += stride) {
-    int j = pc[s];
+    int j = PACKED ? (int)(packed[s] >> 8) : pc[s];
     if (j < 0 || j >= N) { atomicOr(status, (uint32_t)LEO_ST_BAD_INPUT); continue; }
-    atomicAdd(&cls_cnt[j * 8 + slut[cat[s]]], 1);
+    atomicAdd(&cls_cnt[j * 8 + slut[PACKED ? (packed[s] & 0xFFu) : cat[s]]], 1);
   }
 }
 
@@ -72,11 +82,12 @@ __global__ void k_bin_samples(int64_t S, const int32_t* __restrict__ pc, const u
 // passes' hist + scatter + count: ~3 reads and a key write).
 constexpr uint32_t kBinEmpty = 0xFFFFFFFFu;
 
-template <int SLOTS, int PROBE>
+template <int SLOTS, int PROBE, bool PACKED = false>
 __global__ void __launch_bounds__(1024) k_bin_hash(int64_t S, const int32_t* __restrict__ pc,
                                                    const uint8_t* __restrict__ cat,
                                                    const uint8_t* __restrict__ lut, int N,
-                                                   int32_t* __restrict__ cls_cnt, uint32_t* status) {
+                                                   int32_t* __restrict__ cls_cnt, uint32_t* status,
+                                                   const uint32_t* __restrict__ packed = nullptr) {
   pdl_wait();
   extern __shared__ uint32_t hsh[];
   uint32_t* keys = hsh;
@@ -132,11 +143,21 @@ __global__ void __launch_bounds__(1024) k_bin_hash(int64_t S, const int32_t* __r
   // __syncwarp() in vec() always sees the full warp
   const int64_t bd = blockDim.x;
   const int lane = threadIdx.x & 31;
+  const uint4* w4 = reinterpret_cast<const uint4*>(packed);
   for (int64_t v = v0 + threadIdx.x; v - lane < v1; v += 2 * bd) {
     const bool in0 = v < v1, in1 = v + bd < v1;
-    const int4 p0 = in0 ? pc4[v] : make_int4(0, 0, 0, 0);
-    const int4 p1 = in1 ? pc4[v + bd] : make_int4(0, 0, 0, 0);
-    const uint32_t c0 = in0 ? cat4[v] : 0u, c1 = in1 ? cat4[v + bd] : 0u;
+    int4 p0, p1;
+    uint32_t c0, c1;
+    if (PACKED) {
+      const uint4 a0 = in0 ? w4[v] : make_uint4(0, 0, 0, 0), a1 = in1 ? w4[v + bd] : make_uint4(0, 0, 0, 0);
+      unpack4(a0, p0, c0);
+      unpack4(a1, p1, c1);
+    } else {
+      p0 = in0 ? pc4[v] : make_int4(0, 0, 0, 0);
+      p1 = in1 ? pc4[v + bd] : make_int4(0, 0, 0, 0);
+      c0 = in0 ? cat4[v] : 0u;
+      c1 = in1 ? cat4[v + bd] : 0u;
+    }
     vec(p0, c0, in0);
     vec(p1, c1, in1);
   }
@@ -144,10 +165,11 @@ __global__ void __launch_bounds__(1024) k_bin_hash(int64_t S, const int32_t* __r
   if (blockIdx.x == gridDim.x - 1) {
     const int64_t s = nvec * 4 + threadIdx.x;
     if (s < S) {
-      const int j = pc[s];
+      const int j = PACKED ? (int)(packed[s] >> 8) : pc[s];
+      const uint32_t cb = PACKED ? (packed[s] & 0xFFu) : cat[s];
       const bool ok = (uint32_t)j < (uint32_t)N;
       bad |= !ok;
-      if (ok) atomicAdd(&cls_cnt[(uint32_t)j * 8u + slut[cat[s]]], 1);
+      if (ok) atomicAdd(&cls_cnt[(uint32_t)j * 8u + slut[cb]], 1);
     }
   }
   if (bad) atomicOr(status, (uint32_t)LEO_ST_BAD_INPUT);

@@ -231,8 +231,9 @@ void set_smem_attributes() {
   cudaFuncSetAttribute(k_reach_fast<uint16_t, 64, 48>, cudaFuncAttributeMaxDynamicSharedMemorySize, kT1Threads * 64 * 2);
   cudaFuncSetAttribute(k_reach_fast<int32_t, 64, 48>, cudaFuncAttributeMaxDynamicSharedMemorySize, kT1Threads * 64 * 4);
   cudaFuncSetAttribute(k_bin_count, cudaFuncAttributeMaxDynamicSharedMemorySize, kBinRMax * 8 * 4);
-  for (auto f : {k_bin_hash<8192, 8>, k_bin_hash<8192, 4>, k_bin_hash<16384, 4>, k_bin_hash<16384, 2>,
-                 k_bin_hash<26624, 4>, k_bin_hash<26624, 2>, k_bin_hash<26624, 8>})
+  for (auto f : {k_bin_hash<8192, 8, false>, k_bin_hash<8192, 4, false>, k_bin_hash<16384, 4, false>,
+                 k_bin_hash<16384, 2, false>, k_bin_hash<26624, 4, false>, k_bin_hash<26624, 2, false>,
+                 k_bin_hash<26624, 8, false>, k_bin_hash<16384, 2, true>})
     cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, 26624 * 8);
   cudaFuncSetAttribute(k_bin_scatter, cudaFuncAttributeMaxDynamicSharedMemorySize, kBinMaxBuckets * 12 + kBinSub * 4);
   cudaFuncSetAttribute(k_block_walk, cudaFuncAttributeMaxDynamicSharedMemorySize, 96 * 1024);
@@ -828,30 +829,35 @@ static int bin_impl(const LeoSamples* s, int32_t n_instr, int32_t* lat, int32_t*
   set_smem_attributes();
   cudaMemsetAsync(cls_cnt, 0, (size_t)std::max(n_instr, 1) * 32, st);
   const int64_t S = s->n_samples;
-  if (S > 0 && s->pc_host)
+  const bool packed = s->packed != nullptr;
+  if (packed && (int64_t)n_instr > (1 << 24)) return -3;     // pc must fit 24 bits
+  if (S > 0 && packed && s->packed_host)
+    LEO_CUDA_CHECK(cudaMemcpyAsync((void*)s->packed, s->packed_host, (size_t)S * 4, cudaMemcpyHostToDevice, st));
+  if (S > 0 && !packed && s->pc_host)
     LEO_CUDA_CHECK(cudaMemcpyAsync((void*)s->pc, s->pc_host, (size_t)S * 4, cudaMemcpyHostToDevice, st));
-  if (S > 0 && s->cat_host)
+  if (S > 0 && !packed && s->cat_host)
     LEO_CUDA_CHECK(cudaMemcpyAsync((void*)s->cat, s->cat_host, (size_t)S, cudaMemcpyHostToDevice, st));
   // big streams: one pass, per-CTA shared-memory hash (LEO_BIN_BUCKETED=1: the bucketed passes)
   if (S >= (4ll << 20) && (int64_t)n_instr * 8 < 0xFFFFFFFFll && !getenv("LEO_BIN_BUCKETED")) {
     // table geometry (A/B knobs LEO_BIN_SLOTS / LEO_BIN_PROBE; profiling only)
     const int slots = getenv("LEO_BIN_SLOTS") ? atoi(getenv("LEO_BIN_SLOTS")) : 16384;
     const int probe = getenv("LEO_BIN_PROBE") ? atoi(getenv("LEO_BIN_PROBE")) : 2;
-    auto f = k_bin_hash<26624, 4>;
+    auto f = k_bin_hash<26624, 4, false>;
     int threads = 1024, per_sm = 1;
     if (slots == 8192) { f = probe == 8 ? k_bin_hash<8192, 8> : k_bin_hash<8192, 4>; threads = 512; per_sm = 3; }
     else if (slots == 16384) f = probe == 2 ? k_bin_hash<16384, 2> : k_bin_hash<16384, 4>;
     else f = probe == 2 ? k_bin_hash<26624, 2> : probe == 8 ? k_bin_hash<26624, 8> : k_bin_hash<26624, 4>;
+    if (packed) { f = k_bin_hash<16384, 2, true>; threads = 1024; per_sm = 1; }   // default geometry
     const int G = getenv("LEO_BIN_CTAS") ? std::max(1, atoi(getenv("LEO_BIN_CTAS"))) : num_sms() * per_sm;
-    TRACED(KID_BIN, leo_launch(f, G, threads, (size_t)slots * 8, st, S, s->pc, s->cat, s->cat_to_cs,
-                               n_instr, cls_cnt, status));
+    TRACED(KID_BIN, leo_launch(f, G, threads, (size_t)(packed ? 16384 : slots) * 8, st, S, s->pc, s->cat,
+                               s->cat_to_cs, n_instr, cls_cnt, status, s->packed));
     TRACED(KID_BIN_FINALIZE, leo_launch(k_bin_finalize, grid_for(n_instr, 256), 256, 0, st, n_instr, cls_cnt, lat));
     LEO_CUDA_CHECK(cudaGetLastError());
     return 0;
   }
   const int R = (n_instr + kBinR - 1) / kBinR <= kBinMaxBuckets ? kBinR : kBinRMax;
   const int nb = std::max(1, (n_instr + R - 1) / R);
-  const bool bucketed = nb <= kBinMaxBuckets && S > 0;
+  const bool bucketed = nb <= kBinMaxBuckets && S > 0 && !packed;
   // chunks: enough CTAs to stream the samples, bounded so the [G x nb] matrix stays small
   const int G = (int)std::max<int64_t>(1, std::min<int64_t>(num_sms() * 4, (S + 8191) / 8192));
   Arena ar{st};
@@ -871,8 +877,8 @@ static int bin_impl(const LeoSamples* s, int32_t n_instr, int32_t* lat, int32_t*
                                        s->cat_to_cs, n_instr, nb, R, M, boff, keys));
     TRACED(KID_BIN, leo_launch(k_bin_count, num_sms() * 3, 512, smem, st, n_instr, nb, R, slice, boff, soff, keys, cls_cnt));
   } else if (S > 0) {
-    TRACED(KID_BIN, leo_launch(k_bin_samples, grid_for(S / 4 + 1, 256, num_sms() * 8), 256, 0, st, 
-        S, s->pc, s->cat, s->cat_to_cs, n_instr, cls_cnt, status));
+    TRACED(KID_BIN, leo_launch(packed ? k_bin_samples<true> : k_bin_samples<false>, grid_for(S / 4 + 1, 256, num_sms() * 8),
+                               256, 0, st, S, s->pc, s->cat, s->cat_to_cs, n_instr, cls_cnt, status, s->packed));
   }
   TRACED(KID_BIN_FINALIZE, leo_launch(k_bin_finalize, grid_for(n_instr, 256), 256, 0, st, n_instr, cls_cnt, lat));
   ar.release();
@@ -1250,7 +1256,7 @@ int leo_analyze(const LeoKernel* k, const LeoProfile* p, const LeoSamples* sampl
   // whole build to hide in)
   // (the one-pass hashed binning of big streams is short enough to fork late too;
   // LEO_BIN_EARLY=1 forks it at the start)
-  const bool late_bin = samples && !samples->pc_host && !getenv("LEO_BIN_EARLY") &&
+  const bool late_bin = samples && !samples->pc_host && !samples->packed_host && !getenv("LEO_BIN_EARLY") &&
                         (samples->n_samples <= (16ll << 20) || !getenv("LEO_BIN_BUCKETED"));
   if (!late_bin) {
     if (int e = enqueue_bin()) return e;

@@ -75,22 +75,60 @@ class DeviceProfile:
                                      ptr(self.total), ptr(self.eff), ptr(self.sampled))
 
 
+def pack_samples(pc, cat) -> np.ndarray:
+    """The packed raw-sample stream (LeoSamples.packed, ABI v3): one u32 word
+    per sample, pc << 8 | category."""
+    return (np.asarray(pc).astype(np.uint32) << np.uint32(8)) | np.asarray(cat, dtype=np.uint8).astype(np.uint32)
+
+
+def packable(pc) -> bool:
+    pc = np.asarray(pc)
+    return pc.size == 0 or (int(pc.min()) >= 0 and int(pc.max()) < (1 << 24))
+
+
 class DeviceSamples:
-    def __init__(self, pc, cat, lut, device="cuda"):
+    """A raw (pc, category) stream on the device.  `packed` (default: when
+    every pc fits 24 bits) stores it as one u32 word per sample (4 bytes
+    instead of 5, read once by the binning); False keeps pc / cat arrays."""
+
+    def __init__(self, pc, cat, lut, device="cuda", packed: bool | None = None):
         dev = torch.device(device)
         self.n = int(pc.shape[0])
-        self.pc = to_device(np.asarray(pc, dtype=np.int32), dev)
-        self.cat = to_device(np.asarray(cat, dtype=np.uint8), dev)
         self.lut = to_device(np.asarray(lut, dtype=np.uint8), dev)
-        self.struct = abi.LeoSamples(self.n, ptr(self.pc), ptr(self.cat), ptr(self.lut))
+        self.packed = packable(pc) if packed is None else packed
+        if self.packed:
+            self.words = to_device(pack_samples(pc, cat).view(np.int32), dev)
+            self.pc = self.cat = None
+            self.struct = abi.LeoSamples(self.n, None, None, ptr(self.lut))
+            self.struct.packed = ptr(self.words)
+        else:
+            self.pc = to_device(np.asarray(pc, dtype=np.int32), dev)
+            self.cat = to_device(np.asarray(cat, dtype=np.uint8), dev)
+            self.struct = abi.LeoSamples(self.n, ptr(self.pc), ptr(self.cat), ptr(self.lut))
 
     @classmethod
     def from_tensors(cls, pc: torch.Tensor, cat: torch.Tensor, lut: torch.Tensor):
         self = cls.__new__(cls)
         self.n = int(pc.numel())
-        self.pc, self.cat, self.lut = pc, cat, lut
+        self.pc, self.cat, self.lut, self.packed = pc, cat, lut, False
         self.struct = abi.LeoSamples(self.n, ptr(pc), ptr(cat), ptr(lut))
         return self
+
+    @classmethod
+    def from_packed(cls, words: torch.Tensor, lut: torch.Tensor):
+        """Device u32 (int32-typed) words pc << 8 | category."""
+        self = cls.__new__(cls)
+        self.n = int(words.numel())
+        self.words, self.lut, self.packed = words, lut, True
+        self.pc = self.cat = None
+        self.struct = abi.LeoSamples(self.n, None, None, ptr(lut))
+        self.struct.packed = ptr(words)
+        return self
+
+    def set_host_packed(self, words_host: torch.Tensor | None):
+        """Pinned host words the library copies into `words` on the binning branch."""
+        self.host_src = (words_host,)
+        self.struct.packed_host = words_host.data_ptr() if words_host is not None else None
 
     def set_host_sources(self, pc_host: torch.Tensor | None, cat_host: torch.Tensor | None):
         """Pinned host tensors the library copies into pc / cat on the binning
@@ -357,14 +395,14 @@ class Analyzer:
 
 
 def analyze_soa(ks, prof, cfg: abi.LeoConfig | None = None, samples=None, device="cuda",
-                debug_flags: int = 0) -> dict:
+                debug_flags: int = 0, packed: bool | None = None) -> dict:
     """One-shot convenience: upload, run, download."""
     dk = DeviceKernel(ks, device)
     dp = DeviceProfile(prof, ks.n_instr, device)
     ds = None
     if samples is not None:
         pc, cat, lut = samples
-        ds = DeviceSamples(pc, cat, lut, device)
+        ds = DeviceSamples(pc, cat, lut, device, packed=packed)
     an = Analyzer(dk, device, debug_flags=debug_flags)
     an.run(dp, cfg or abi.make_config(dialect=ks.dialect), ds)
     r = an.result()

@@ -216,3 +216,17 @@ def test_device_batch_matches_per_kernel_oracle(cuda):
                          ("pmeta", o.p_meta), ("e_stalled", o.e_stalled), ("e_blame", o.e_blame),
                          ("level", o.level)):
                 assert np.array_equal(got[f], e), (dialect, wl.kernel.name, f)
+
+@pytest.mark.parametrize("tag,scale", [("c2", 0.2), ("c5", 0.05)])
+def test_packed_and_split_sample_streams_agree(tag, scale, cuda):
+    """The packed stream (one u32 word per sample, LeoSamples.packed) bins to
+    the same counts and the same analysis as the pc / cat arrays, on the
+    small-stream kernel (C2 scale) and the one-pass hash (5 M samples)."""
+    from paper_2604_20032_b200 import abi, device, synth
+    wl = synth.config_workload(tag, scale=scale)
+    cfg = abi.make_config(dialect=wl.kernel.dialect)
+    a = device.analyze_soa(wl.kernel, wl.profile, cfg, samples=(wl.pc, wl.cat, wl.lut), device=cuda, packed=True)
+    b = device.analyze_soa(wl.kernel, wl.profile, cfg, samples=(wl.pc, wl.cat, wl.lut), device=cuda, packed=False)
+    assert a["status"] == 0 and b["status"] == 0
+    for key in ("lat", "cls_cnt", "bprod", "bmeta", "pprod", "e_stalled", "e_blame", "level"):
+        assert np.array_equal(a[key], b[key]), key
