@@ -714,21 +714,33 @@ __global__ void __launch_bounds__(kT1Threads) k_reach_fast(KView k, ReachArgs a,
       if (__all_sync(0xffffffffu, drained)) break;
       continue;
     }
-    if (e >= 0 && !ovf && sp > 0) {               // one search step
-      const int y = stk[--sp];
-      const int own = a.ldtab[(size_t)u * a.Bp + y];  // issued together with the record load
-      const int4 r = a.rec[y];
-      const int ld = own >= 0 ? own : (r.x < y ? run_lookup(a, y - 1, r.x, u) : -1);
-      if (ld >= 0) {
-        if (nres == kT1Res) ovf = true; else res[nres++] = ld;
-      } else {
-        for (int t = 0; t < r.y && !ovf; t++) {
-          const int pp = r.y <= 2 ? (t == 0 ? r.z : r.w) : k.pred[r.z + t];
-          const int v = insert(pp);
-          if (v < 0 || (v && sp == kT1Stack)) ovf = true;
-          else if (v) stk[sp++] = pp;
+    if (e >= 0 && !ovf && sp > 0) {
+      // up to two search steps per round: both blocks' last-def and record
+      // loads are issued before either is used (twice the loads in flight per
+      // lane, half the round overhead per visit; the visited set makes the
+      // result set independent of the order)
+      auto step = [&](int y, int own, int4 r) {
+        const int ld = own >= 0 ? own : (r.x < y ? run_lookup(a, y - 1, r.x, u) : -1);
+        if (ld >= 0) {
+          if (nres == kT1Res) ovf = true; else res[nres++] = ld;
+        } else {
+          for (int t = 0; t < r.y && !ovf; t++) {
+            const int pp = r.y <= 2 ? (t == 0 ? r.z : r.w) : k.pred[r.z + t];
+            const int v = insert(pp);
+            if (v < 0 || (v && sp == kT1Stack)) ovf = true;
+            else if (v) stk[sp++] = pp;
+          }
         }
-      }
+      };
+      const int y1 = stk[--sp];
+      const bool two = sp > 0;
+      const int y2 = two ? stk[--sp] : y1;
+      const int own1 = a.ldtab[(size_t)u * a.Bp + y1];
+      const int4 r1 = a.rec[y1];
+      const int own2 = two ? a.ldtab[(size_t)u * a.Bp + y2] : -1;
+      const int4 r2 = two ? a.rec[y2] : r1;
+      step(y1, own1, r1);
+      if (two && !ovf) step(y2, own2, r2);
     }
     if (e >= 0 && ovf) {                           // hand the query to tier 2
       const int s2 = atomicAdd(a.slow_count, 1);

@@ -91,6 +91,7 @@ def test_device_matches_oracle_synthetic(tag, scale, cuda):
     ("c2", {"LEO_BLAME_2PASS": "1", "LEO_SCAN_TILED": "1", "LEO_WC_CLUSTER": "1", "LEO_MP_COOP": "1"}),
     ("c2", {"LEO_WC_CLUSTER": "8", "LEO_WC_CTAS": "64", "LEO_BLAME_SPLIT": "1"}),
     ("c5", {"LEO_BLAME_UNSPLIT": "1", "LEO_BIN_SLOTS": "8192", "LEO_BIN_PROBE": "4"}),
+    ("c3", {"LEO_BLAME_SPLIT": "1"}),
 ])
 def test_device_schedule_knobs_exact(tag, knobs, cuda, monkeypatch):
     """The scheduling knobs (fork points, CTAs per unit, waitcnt tier size
