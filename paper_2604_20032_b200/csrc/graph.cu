@@ -629,6 +629,9 @@ __global__ void k_reach_unit(KView k, ReachArgs a, const int32_t* __restrict__ q
 // open-addressing hash in shared memory (strided per thread), cleared through
 // the list of slots it used.
 constexpr int kT1Hash = 128, kT1Limit = 96, kT1Stack = 96, kT1Res = 32, kT1Threads = 128;
+#ifndef LEO_T1_STEPS
+#define LEO_T1_STEPS 2          // search steps (blocks' loads in flight) per lane per round
+#endif
 constexpr int kT1Fetch = 64, kT1Chunk = 512;
 
 // KT: hash key type (uint16_t when every block id < 0xFFFF: half the shared
@@ -732,15 +735,20 @@ __global__ void __launch_bounds__(kT1Threads) k_reach_fast(KView k, ReachArgs a,
           }
         }
       };
-      const int y1 = stk[--sp];
-      const bool two = sp > 0;
-      const int y2 = two ? stk[--sp] : y1;
-      const int own1 = a.ldtab[(size_t)u * a.Bp + y1];
-      const int4 r1 = a.rec[y1];
-      const int own2 = two ? a.ldtab[(size_t)u * a.Bp + y2] : -1;
-      const int4 r2 = two ? a.rec[y2] : r1;
-      step(y1, own1, r1);
-      if (two && !ovf) step(y2, own2, r2);
+      int ys[LEO_T1_STEPS], owns[LEO_T1_STEPS];
+      int4 rs[LEO_T1_STEPS];
+      int ns = 0;
+#pragma unroll
+      for (int x = 0; x < LEO_T1_STEPS; x++)
+        if (sp > 0) { ys[x] = stk[--sp]; ns = x + 1; } else ys[x] = -1;
+#pragma unroll
+      for (int x = 0; x < LEO_T1_STEPS; x++) {
+        owns[x] = ys[x] >= 0 ? a.ldtab[(size_t)u * a.Bp + ys[x]] : -1;
+        rs[x] = ys[x] >= 0 ? a.rec[ys[x]] : make_int4(0, 0, 0, 0);
+      }
+#pragma unroll
+      for (int x = 0; x < LEO_T1_STEPS; x++)
+        if (x < ns && !ovf) step(ys[x], owns[x], rs[x]);
     }
     if (e >= 0 && ovf) {                           // hand the query to tier 2
       const int s2 = atomicAdd(a.slow_count, 1);

@@ -1,7 +1,5 @@
 set -u
 mkdir -p gpurun_out
-python -c "import __graft_entry__ as g; g.build()" > gpurun_out/ab20_build.txt 2>&1 || { tail -20 gpurun_out/ab20_build.txt; exit 1; }
-timeout 1500 python -m pytest tests/test_gpu_parity.py tests/test_gpu_api.py tests/test_session.py -m gpu -q -x -p no:cacheprovider > gpurun_out/ab20_tests.txt 2>&1; echo "tests rc=$?"; tail -2 gpurun_out/ab20_tests.txt
-timeout 1500 python tools/step_ab.py c5 "X=0" "LEO_MP_JACOBI=1" --reps 3
-timeout 600 python tools/step_ab.py c3 "X=0" "LEO_MP_JACOBI=1" --reps 2
-timeout 600 python tools/step_ab.py c2 "X=0" "LEO_MP_JACOBI=1" --reps 2
+python -c "import __graft_entry__ as g; g.build()" > gpurun_out/ab21_build.txt 2>&1 || { tail -20 gpurun_out/ab21_build.txt; exit 1; }
+timeout 1500 python tools/step_ab.py c5 "X=0" "LEO_LIB_VARIANT=/root/repo/abtest/libleo_t1s3.so" "LEO_LIB_VARIANT=/root/repo/abtest/libleo_t1s4.so" --reps 3
+timeout 600 python tools/step_ab.py c3 "X=0" "LEO_LIB_VARIANT=/root/repo/abtest/libleo_t1s3.so" --reps 2
