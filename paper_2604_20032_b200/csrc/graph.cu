@@ -130,7 +130,6 @@ struct WalkArgs {
   int32_t* qtab;             // [U * Bp] column-major: query slot of (b, u), -1 if none
   int32_t Bp;                // column stride (B rounded up to 4: 16-byte aligned columns)
   int32_t* gtab;             // global per-warp tables (when U too large for smem) or null
-  Range own;                 // consumer range (stalled-PC sharding): only owned uses make queries
 };
 
 // per-warp staging of a window of <= 32 instructions' unit events
@@ -211,13 +210,12 @@ __global__ void k_block_walk(KView k, WalkArgs a, int warps_per_cta) {
         par = true;
         const int nu = ue - ub, nd = de - db;
         for (int y = lane; y < nd; y += 32) atomicOr(&dmask[evd[y]], 1u << (evdi[y] - first));
-        for (int x = lane; x < nu; x += 32)
-          if (a.own.has(evui[x])) atomicMin(&fuse[evu[x]], x);
+        for (int x = lane; x < nu; x += 32) atomicMin(&fuse[evu[x]], x);
         __syncwarp();
         for (int x0 = 0; x0 < nu; x0 += 32) {
           const int x = x0 + lane;
           bool lead = false;
-          if (x < nu && a.own.has(evui[x])) {
+          if (x < nu) {
             const int u = evu[x], i = evui[x];
             const uint32_t m = dmask[u] & ((1u << (i - first)) - 1u);
             int res;
@@ -257,10 +255,9 @@ __global__ void k_block_walk(KView k, WalkArgs a, int warps_per_cta) {
       for (int j = 0; j < nin; j++) {
         const int ii = w0 + j;
         const int e0 = __shfl_sync(0xffffffffu, u0, j), e1 = __shfl_sync(0xffffffffu, u1, j);
-        const bool owned = a.own.has(ii);
         for (int base = e0; base < e1; base += 32) {
           const int e = base + lane;
-          const bool valid = e < e1 && owned;
+          const bool valid = e < e1;
           int u = -1, res = 0;
           bool fresh = false;
           if (valid) {

@@ -364,7 +364,7 @@ int build_graph_impl(const LeoKernel* kk, const LeoCaps* caps, LeoEdges* out, Le
     const bool setter_cta = k.dialect != LEO_AMD && B > 0 && !(sdbg & (LEO_DBG_NO_SMEM | LEO_DBG_SYNC_SLOW));
     // staged: every block search goes to the warp tier; from L2 the warp tier
     // only takes what overflows the thread-private Dijkstra (measured on C5)
-    sa.defer_search = setter_cta && setter_staged ? 1 : 0;
+    sa.defer_search = setter_cta && (setter_staged || getenv("LEO_SETTER_DEFER")) ? 1 : 0;
     // as many threads per CTA as the image allows: more warps hide the
     // shared-memory latency of the event-list build and spread the items
     int wc_threads = 512;
@@ -437,8 +437,9 @@ int build_graph_impl(const LeoKernel* kk, const LeoCaps* caps, LeoEdges* out, Le
   const int wdbg = caps ? caps->debug_flags : 0;
   const bool tier0 = B > 0 && U > 0 && reach_unit_smem(bcap0, ru_threads0) <= (size_t)kSmemResidentMax &&
                      !(wdbg & LEO_DBG_NO_SMEM) && !getenv("LEO_REACH_NO_T0");
-  WalkArgs wa{use_ptr, def_ptr, ev_res, q_block, q_unit, tier0 ? nullptr : q_list, &ctr[0], ldtab, qtab, Bp, gtab,
-              rall ? Range{0, 0} : own};
+  // (every use resolves, also under stalled-PC sharding: the indirect-
+  // addressing test walks the base graph's RAW edges of non-owned consumers)
+  WalkArgs wa{use_ptr, def_ptr, ev_res, q_block, q_unit, tier0 ? nullptr : q_list, &ctr[0], ldtab, qtab, Bp, gtab};
   const size_t smem = walk_bytes(wpc, smem_tab);
   if (B > 0 && U > 0) {     // the walk writes the unit columns sparsely
     cudaMemsetAsync(ldtab, 0xFF, (size_t)Bp * U * 4, st);

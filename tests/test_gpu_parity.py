@@ -175,7 +175,7 @@ def test_device_consumer_shards_recombine(tag, scale, world, cuda):
                               samples=(wl.pc, wl.cat, wl.lut), device=cuda)
     ranges = D.consumer_ranges(ks, world)
     parts = D.partition_samples(wl.pc, ranges)
-    st, bl, lb, ls = [], [], 0.0, 0.0
+    st, bl, sub, cause, lb, ls = [], [], [], [], 0.0, 0.0
     for (lo, hi), idx in zip(ranges, parts):
         r = device.analyze_soa(ks, wl.profile,
                                abi.make_config(dialect=ks.dialect, consumer_range=(lo, hi)),
@@ -183,6 +183,8 @@ def test_device_consumer_shards_recombine(tag, scale, world, cuda):
         assert r["status"] == 0
         st.append(r["e_stalled"])
         bl.append(r["e_blame"])
+        sub.append(r["e_sub"])
+        cause.append(r["e_cause"])
         lb = lb + r["line_blame"]
         ls = ls + r["line_stall"]
         own = (full["pcons"] >= lo) & (full["pcons"] < hi)
@@ -192,6 +194,10 @@ def test_device_consumer_shards_recombine(tag, scale, world, cuda):
         assert got == exp
     assert np.array_equal(np.concatenate(st), full["e_stalled"])
     assert np.array_equal(np.concatenate(bl), full["e_blame"])
+    # self-blame subcategories too: the indirect-addressing test of an owned
+    # instruction walks RAW edges of instructions other ranks own
+    assert np.array_equal(np.concatenate(sub), full["e_sub"])
+    assert np.array_equal(np.concatenate(cause), full["e_cause"])
     assert np.allclose(lb, full["line_blame"], rtol=1e-9, atol=1e-6)
     assert np.allclose(ls, full["line_stall"], rtol=1e-9, atol=1e-6)
 
