@@ -355,6 +355,24 @@ __global__ void __launch_bounds__(kSegThreads) segsort_unique_u64(uint64_t* __re
       if (n > 3 && r3 != r2) a[u++] = r3;
       uniq[s] = u;
       mine = false;
+    } else if (mine && n <= 8) {
+      // 8-key register network (Batcher odd-even merge sort, 19 exchanges)
+      uint64_t r[8];
+#pragma unroll
+      for (int i = 0; i < 8; i++) r[i] = i < n ? a[i] : ~0ull;
+      auto cs = [&](int x, int y) { const uint64_t lo = r[x] < r[y] ? r[x] : r[y]; r[y] = r[x] < r[y] ? r[y] : r[x]; r[x] = lo; };
+      cs(0, 1); cs(2, 3); cs(4, 5); cs(6, 7);
+      cs(0, 2); cs(1, 3); cs(4, 6); cs(5, 7);
+      cs(1, 2); cs(5, 6);
+      cs(0, 4); cs(1, 5); cs(2, 6); cs(3, 7);
+      cs(2, 4); cs(3, 5);
+      cs(1, 2); cs(3, 4); cs(5, 6);
+      int u = 0;
+#pragma unroll
+      for (int i = 0; i < 8; i++)
+        if (i < n && (i == 0 || r[i] != r[i - 1])) a[u++] = r[i];
+      uniq[s] = u;
+      mine = false;
     } else if (mine && n <= 24) {
       uint64_t r[24];
       for (int i = 0; i < n; i++) r[i] = a[i];
