@@ -521,6 +521,8 @@ def run_ours(args, ws, rank, local):
             "roofline": {"bound": "hbm", "kernel": dominant, "achieved": achieved, "peak": peak,
                          "unit": "GB/s", "frac": (achieved / peak) if achieved else None,
                          "traffic": traffic, "alg_bytes_per_launch": alg,
+                         "sectors_per_request": roofline.ncu_sectors_per_request(ROOT / "profiles", args.config,
+                                                                                  dominant),
                          "avg_launch_ms": avg_s * 1e3 if avg_s else None, "peak_source": peak_src},
             "pipeline_roofline": {"alg_bytes_per_step": pipe_bytes,
                                   "achieved_gbs": pipe_bytes / (T_max / args.steps / 1e3) / 1e9,

@@ -62,13 +62,25 @@ def kernel_bytes(name: str, ks, wl, res) -> int | None:
         "link_fill": 4 * z["M"] + 4 * z["NU"] + 8 * z["NU"],
         "segsort_unique": 16 * z["NU"] + 4 * N,
         "lines": 16 * z["NB"] + 8 * z["L"] + 8 * N,
-        # dense last-def + query tables read once (unit columns), CFG, results
-        "reach_fast": 8 * z["B"] * int(ks.n_units) + 4 * z["B"] + 12 * z["CE"] + 12 * z["NU"],
+        # SURVEY §8(d) terms only (the unit columns are this design's own
+        # derived tables, not algorithmic bytes): def / use units, the block
+        # records and CFG, one query + result per use unit
+        "reach_fast": 4 * (z["ND"] + z["NU"]) + 16 * z["B"] + 8 * z["CE"] + 12 * z["NU"],
         # base-graph RAW incoming of the candidates + per-candidate verdicts
         "selfblame_warp": 12 * z["E"] + 8 * N,
     }
     v = table.get(name)
     return int(v) if v is not None else None
+
+
+def ncu_sectors_per_request(profiles: Path, config: str, kernel: str):
+    """l1tex global-load sectors per request of `kernel` from the committed
+    ncu --set full summary (profiles/ncu_kernel_stats.json)."""
+    p = Path(profiles) / "ncu_kernel_stats.json"
+    try:
+        return json.loads(p.read_text()).get(config, {}).get(kernel, {}).get("sectors_per_request")
+    except Exception:
+        return None
 
 
 def ncu_traffic(profiles: Path, config: str, kernel: str):

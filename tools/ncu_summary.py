@@ -128,6 +128,25 @@ def main():
                 tc[trace] = int(rd + wr)
                 break
     traffic_path.write_text(json.dumps(traffic, indent=1, sort_keys=True) + "\n")
+    # per traced kernel: DRAM bytes, global-load sectors per request, warps active
+    stats_path = PROF / "ncu_kernel_stats.json"
+    stats = json.loads(stats_path.read_text()) if stats_path.exists() else {}
+    sc = stats.setdefault(config, {})
+    for trace, syms in TRACE_TO_KERNEL.items():
+        for d in recs:
+            name = short(d["Kernel Name"])
+            if any(name.startswith(sy) for sy in syms):
+                u = d["_units"]
+                sec = float(d.get("l1tex__t_sectors_pipe_lsu_mem_global_op_ld.sum", "0").replace(",", "") or 0)
+                req = float(d.get("l1tex__t_requests_pipe_lsu_mem_global_op_ld.sum", "0").replace(",", "") or 0)
+                sc[trace] = {"kernel": name, "dram_bytes": tc.get(trace),
+                             "sectors_per_request": round(sec / req, 2) if req else None,
+                             "warps_active_pct": float(d.get("sm__warps_active.avg.pct_of_peak_sustained_active", "0") or 0),
+                             "us": float(d.get("gpu__time_duration.sum", "0").replace(",", "") or 0)
+                             * {"msecond": 1e3, "usecond": 1.0, "nsecond": 1e-3}.get(
+                                 u.get("gpu__time_duration.sum", "usecond"), 1.0)}
+                break
+    stats_path.write_text(json.dumps(stats, indent=1, sort_keys=True) + "\n")
     print(f"wrote {tag}: {len(L)} launches, {len(recs)} full captures; traffic {tc}")
 
 
