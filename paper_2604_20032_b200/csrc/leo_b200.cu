@@ -466,7 +466,7 @@ int build_graph_impl(const LeoKernel* kk, const LeoCaps* caps, LeoEdges* out, Le
   // segments: members of a concatenated batch are staged one at a time
   const int n_seg = (kk->n_segments > 1 && kk->seg_block) ? kk->n_segments : 1;
   const int bcap = n_seg > 1 ? kk->max_seg_blocks : B;
-  int ru_threads = 128;
+  int ru_threads = getenv("LEO_RU_THREADS") ? std::max(32, atoi(getenv("LEO_RU_THREADS"))) : 128;
   while (ru_threads > 32 && reach_unit_smem(bcap, ru_threads) > (size_t)kSmemResidentMax) ru_threads >>= 1;
   const size_t ru_smem = reach_unit_smem(bcap, ru_threads);
   // CTAs per unit: one when the units alone cover the SMs (every extra CTA

@@ -47,6 +47,17 @@ if [[ $WHAT == all || $WHAT == ncu ]]; then
      > $OUT/${TAG}_c5_hotlines.txt 2>&1
   rm -f $OUT/${TAG}_c5_full.ncu-rep
 fi
+if [[ $WHAT == all || $WHAT == ncu23 ]]; then
+  for c in c2 c3; do
+    timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none --csv \
+       --log-file $OUT/${TAG}_${c}_launches.csv python tools/profile_step.py $c --steps 2 --warmup 1 > $OUT/${TAG}_ncu_${c}_list.txt 2>&1
+    timeout 900 ncu --set full --clock-control none -k 'regex:k_(bin_|reach_|block_walk|prune_edges|slice|sync|blame|lines|compact)' -s 0 -c 30 \
+       -o $OUT/${TAG}_${c}_full -f python tools/profile_step.py $c --steps 1 --warmup 0 > $OUT/${TAG}_ncu_${c}_full.txt 2>&1
+    echo "ncu $c rc=$?"
+    ncu -i $OUT/${TAG}_${c}_full.ncu-rep --page raw --csv > $OUT/${TAG}_${c}_full_raw.csv 2>/dev/null
+    rm -f $OUT/${TAG}_${c}_full.ncu-rep
+  done
+fi
 if [[ $WHAT == all || $WHAT == ncu4 ]]; then
   timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none --csv \
      --log-file $OUT/${TAG}_c4_launches.csv python tools/profile_step.py c4 --steps 1 --warmup 1 > $OUT/${TAG}_ncu4_list.txt 2>&1
