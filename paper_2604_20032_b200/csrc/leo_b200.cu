@@ -544,7 +544,7 @@ int build_graph_impl(const LeoKernel* kk, const LeoCaps* caps, LeoEdges* out, Le
 int prune_impl(const LeoKernel* kk, const LeoProfile* pp, const LeoConfig* cfg, const LeoEdges* in,
                LeoEdges* out, LeoPaths* paths, LeoDiags* diags, const LeoCaps* caps, uint32_t* status,
                cudaStream_t st, ZeroSet zero = ZeroSet{{nullptr, nullptr, nullptr, nullptr}, 0},
-               const LeoPaths* in_paths = nullptr) {
+               const LeoPaths* in_paths = nullptr, const double* wpre_pre = nullptr) {
   LeoTrace* tr = caps ? caps->trace : nullptr;
   KView k = make_kview(kk);
   PView p = make_pview(pp);
@@ -563,9 +563,10 @@ int prune_impl(const LeoKernel* kk, const LeoProfile* pp, const LeoConfig* cfg, 
   // nvidia issue weights vary: straight runs are resolved through per-block prefix sums
   const bool weighted = kk->dialect == LEO_NVIDIA && (cfg->stage_mask & 4) && !getenv("LEO_PRUNE_NO_WPRE");
   double* wpre = nullptr;
-  if (weighted) ar.want(&wpre, std::max(kk->n_instr, 1));
+  if (weighted && !wpre_pre) ar.want(&wpre, std::max(kk->n_instr, 1));
   LEO_CUDA_CHECK(ar.commit());
-  if (weighted && kk->n_blocks > 0)
+  if (weighted && wpre_pre) wpre = (double*)wpre_pre;      // computed on a side branch (leo_analyze)
+  else if (weighted && kk->n_blocks > 0)
     leo_launch(k_weight_prefix, grid_for(kk->n_blocks, 128), 128, 0, st, k, wpre);
   cudaMemsetAsync(ctr, 0, 4 * sizeof(int32_t), st);
   LeoPaths inp{};
@@ -1238,6 +1239,15 @@ int leo_analyze(const LeoKernel* k, const LeoProfile* p, const LeoSamples* sampl
   LeoTrace* tr = caps ? caps->trace : nullptr;
   // stage-0 binning only feeds pruning and blame: run it beside build_graph
   const bool fork = (tr == nullptr || (tr->mode & 1)) && !no_fork_env();
+  // nvidia pruning's per-block issue-weight prefix (kernel data only): built
+  // on the binning branch when there is one
+  double* wpre_pre = nullptr;
+  Arena ar_w{st};
+  struct Release { Arena& a; ~Release() { a.release(); } } release_w{ar_w};   // after the last use is queued
+  if (samples && k->dialect == LEO_NVIDIA && (cfg->stage_mask & 4) && !getenv("LEO_PRUNE_NO_WPRE")) {
+    ar_w.want(&wpre_pre, std::max(k->n_instr, 1));
+    LEO_CUDA_CHECK(ar_w.commit());
+  }
   auto enqueue_bin = [&]() -> int {
     if (!samples) return 0;
     cudaStream_t s_bin = fork ? sp.s[1] : st;
@@ -1247,7 +1257,11 @@ int leo_analyze(const LeoKernel* k, const LeoProfile* p, const LeoSamples* sampl
     // long branch and keeps the default
     const int bin_lo = getenv("LEO_BIN_LOWPRIO") ? atoi(getenv("LEO_BIN_LOWPRIO")) : -1;
     LowPriority low_prio(bin_lo >= 0 ? bin_lo == 1 : samples->n_samples <= (16ll << 20));
-    return bin_impl(samples, k->n_instr, (int32_t*)p->lat, (int32_t*)p->cls_cnt, status, tr, s_bin);
+    const int rb = bin_impl(samples, k->n_instr, (int32_t*)p->lat, (int32_t*)p->cls_cnt, status, tr, s_bin);
+    // the nvidia issue-weight prefix pruning needs, off the dataflow chain
+    if (!rb && wpre_pre && k->n_blocks > 0)
+      leo_launch(k_weight_prefix, grid_for(k->n_blocks, 128), 128, 0, s_bin, make_kview(k), wpre_pre);
+    return rb;
   };
   // Up to 16 M samples the binning branch forks after the block walk: it has
   // the whole build as slack, and started with the build it takes SMs from
@@ -1302,7 +1316,7 @@ int leo_analyze(const LeoKernel* k, const LeoProfile* p, const LeoSamples* sampl
   want_incoming(ar, ib, k->n_instr, pruned->capacity);
   LEO_CUDA_CHECK(ar.commit());
   r = prune_impl(k, p, cfg, base, pruned, paths, diags, caps, status, st,
-                 ZeroSet{{ib.rbeg, ib.rend, ib.scnt, ib.scur}, k->n_instr});
+                 ZeroSet{{ib.rbeg, ib.rend, ib.scnt, ib.scur}, k->n_instr}, nullptr, wpre_pre);
   if (r) { ar.release(); return r; }
   if (stop == 2) {
     if (fork) link_streams(s_addr, st, sp.e[7]);
