@@ -311,7 +311,10 @@ LEO_DEV bool prune_one(const KView& k, const PView& p, const PruneArgs& a, int e
   return true;
 }
 
-constexpr int kDfsStack = 20, kDfsArena = 24, kDfsPaths = 64;
+#ifndef LEO_DFS_PATHS
+#define LEO_DFS_PATHS 64
+#endif
+constexpr int kDfsStack = 20, kDfsArena = 24, kDfsPaths = LEO_DFS_PATHS;
 
 __global__ void __launch_bounds__(128) k_prune_edges(KView k, PView p, PruneArgs a) {
   pdl_wait();

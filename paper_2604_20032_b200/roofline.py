@@ -27,14 +27,17 @@ def _sizes(ks, wl, res):
     nb = int(res["e_blame"].shape[0])
     L = int(res["line_blame"].shape[0])
     cfg_edges = int(ks.succ.shape[0])
-    return dict(N=N, B=B, M=M, NU=nu, ND=nd, S=S, E=E, Ep=Ep, P=P, NB=nb, L=L, CE=cfg_edges,
+    # bytes per raw sample as the device reads them: the packed u32 stream
+    # (kernels below 2^24 instructions, device.DeviceSamples default) or i32 pc + u8 cat
+    SB = 4 if N < (1 << 24) else 5
+    return dict(N=N, B=B, M=M, NU=nu, ND=nd, S=S, SB=SB, E=E, Ep=Ep, P=P, NB=nb, L=L, CE=cfg_edges,
                 NREG=int(res.get("n_regular", E)))
 
 
 def pipeline_bytes(ks, wl, res) -> int:
     """B_alg of one step."""
     z = _sizes(ks, wl, res)
-    return int(5 * z["S"] + 32 * z["N"] + 4 * (z["ND"] + z["NU"]) + 16 * z["B"] + 8 * z["CE"]
+    return int(z["SB"] * z["S"] + 32 * z["N"] + 4 * (z["ND"] + z["NU"]) + 16 * z["B"] + 8 * z["CE"]
                + 24 * z["N"] + 32 * z["N"] + 16 * z["E"] + 16 * z["Ep"] + 16 * z["P"]
                + z["N"] / 8 + 4 * z["N"] + 56 * z["NB"] + 8 * z["L"])
 
@@ -45,7 +48,7 @@ def kernel_bytes(name: str, ks, wl, res) -> int | None:
     N, E, Ep = z["N"], z["E"], z["Ep"]
     table = {
         # raw samples (i32 pc + u8 category) read once, class counts written once
-        "bin_samples": 5 * z["S"] + 32 * N,
+        "bin_samples": z["SB"] * z["S"] + 32 * N,
         "bin_finalize": 32 * N + 4 * N,
         # operand CSR + offsets + block table in; per-use-event results + block summaries out
         "block_walk": 4 * z["M"] + 4 * N + 8 * N + 8 * z["B"] + 4 * z["NU"] + 8 * z["ND"],
