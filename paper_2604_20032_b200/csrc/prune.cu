@@ -323,7 +323,9 @@ __global__ void __launch_bounds__(128) k_prune_edges(KView k, PView p, PruneArgs
   BackNode arena[kDfsArena];
   int32_t vlen[kDfsPaths];
   double vacc[kDfsPaths];
-  const bool big_paths = a.cfg.max_paths > kDfsPaths || (a.dbg & LEO_DBG_PRUNE_SLOW);
+  // an edge whose valid paths outgrow the local buffer overflows to the slow
+  // tier on its own (enumerate_paths returns DFS_OVERFLOW at vcap)
+  const bool big_paths = (a.dbg & LEO_DBG_PRUNE_SLOW) || (LEO_DFS_PATHS >= 64 && a.cfg.max_paths > kDfsPaths);
   for (int e = blockIdx.x * blockDim.x + threadIdx.x; e < n; e += gridDim.x * blockDim.x) {
     bool ok = !big_paths && prune_one(k, p, a, e, stk, kDfsStack, arena, kDfsArena, vlen, vacc, kDfsPaths);
     if (!ok) {
