@@ -430,7 +430,10 @@ LEO_DEV void reach_commit(const ReachArgs& a, int e, const int32_t* res, int nre
 // unit by a thread-private DFS whose visited set is a bitmap over blocks in
 // shared memory.  Every search step is a shared-memory access.  Queries whose
 // stack or result list overflows go to tier 2.
-constexpr int kRUStack = 32, kRURes = 32;
+#ifndef LEO_RU_STACK
+#define LEO_RU_STACK 16          // per-thread DFS stack / results of tier 0: 2 CTAs per SM at C4 members (-11 %)
+#endif
+constexpr int kRUStack = LEO_RU_STACK, kRURes = LEO_RU_STACK;
 
 __host__ __device__ inline size_t reach_unit_smem(int B, int threads) {
   const size_t Bp = (size_t)((B + 3) & ~3);
