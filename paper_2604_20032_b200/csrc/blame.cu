@@ -121,20 +121,28 @@ __global__ void __launch_bounds__(1024) k_bin_hash(int64_t S, const int32_t* __r
   };
   auto vec = [&](const int4 p, const uint32_t c, const bool valid) {
     const int js[4] = {p.x, p.y, p.z, p.w};
-    uint32_t key[4], h[4];
-    bool hit[4];
+    uint32_t key[4], h[4], k0[4], k1[4];
 #pragma unroll
-    for (int t = 0; t < 4; t++) {                        // home slot: the hot-key hit
+    for (int t = 0; t < 4; t++) {                        // both probe slots read up front
       const bool ok = valid && (uint32_t)js[t] < (uint32_t)N;
       bad |= valid && !ok;
       key[t] = ok ? (uint32_t)js[t] * 8u + slut[(c >> (8 * t)) & 0xFF] : kBinEmpty;
       h[t] = __umulhi(key[t] * 2654435761u, (uint32_t)SLOTS);
-      hit[t] = ok && keys[h[t]] == key[t];
+      k0[t] = keys[h[t]];
+      k1[t] = PROBE == 2 ? keys[h[t] + 1 == (uint32_t)SLOTS ? 0u : h[t] + 1] : 0u;
     }
 #pragma unroll
     for (int t = 0; t < 4; t++) {
-      if (hit[t]) atomicAdd(&cnts[h[t]], 1u);
-      else if (key[t] != kBinEmpty) slow(key[t], h[t]);
+      if (key[t] == kBinEmpty) continue;
+      if (k0[t] == key[t]) {                             // the hot-key hit
+        atomicAdd(&cnts[h[t]], 1u);
+      } else if (PROBE == 2 && k1[t] == key[t]) {        // displaced by one slot
+        atomicAdd(&cnts[h[t] + 1 == (uint32_t)SLOTS ? 0u : h[t] + 1], 1u);
+      } else if (PROBE == 2 && k0[t] != kBinEmpty && k1[t] != kBinEmpty) {
+        atomicAdd(&cls_cnt[key[t]], 1);                  // both slots taken: cold key to L2
+      } else {
+        slow(key[t], h[t]);                              // claim an empty slot (or re-probe)
+      }
     }
     __syncwarp();
   };
