@@ -347,7 +347,7 @@ int build_graph_impl(const LeoKernel* kk, const LeoCaps* caps, LeoEdges* out, Le
   auto enqueue_sync = [&]() {
     if (fork) link_streams(st, s_sync, sp.e[0]);
     dbg_delay("LEO_DBG_DELAY_SYNC", s_sync);
-    LowPriority low_prio(sync_smem_tier);
+    LowPriority low_prio(sync_smem_tier || getenv("LEO_FORCE_PRIO"));
     cudaStream_t st = s_sync;   // shadows the caller's stream for the TRACED scopes
     cudaMemsetAsync(pcnt, 0, (size_t)std::max(N, 1) * 4, st);
     cudaMemsetAsync(pcur, 0, (size_t)std::max(N, 1) * 4, st);
@@ -1232,7 +1232,7 @@ int leo_analyze(const LeoKernel* k, const LeoProfile* p, const LeoSamples* sampl
   // tracing runs a shared-memory tier (the dataflow chain is then the critical
   // branch).  Big NVIDIA / Intel kernels run everything at the default.
   const int adbg = caps ? caps->debug_flags : 0;
-  const bool prio = !(adbg & LEO_DBG_NO_SMEM) && k->n_blocks > 0 &&
+  const bool prio = getenv("LEO_FORCE_PRIO") ? true : !(adbg & LEO_DBG_NO_SMEM) && k->n_blocks > 0 &&
       (k->dialect == LEO_AMD ? sync_smem_bytes(k->n_instr, k->n_blocks, 128) <= (size_t)kSmemResidentMax
                              : setter_cta_smem(k->n_blocks) <= (size_t)kSmemResidentMax);
   HighPriority high_prio(prio);
