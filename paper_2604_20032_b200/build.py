@@ -99,7 +99,7 @@ def build_front(force: bool = False) -> Path:
     srcs = (FRONT_SRC, PROFILE_SRC, hdr)
     if not force and FRONT.exists() and FRONT.stat().st_mtime >= max(x.stat().st_mtime for x in srcs):
         return FRONT
-    cmd = [os.environ.get("CXX", "g++"), "-O2", "-std=c++17", "-fPIC", "-shared", "-Wall",
+    cmd = [os.environ.get("CXX", "g++"), "-O2", "-std=c++17", "-fPIC", "-shared", "-Wall", "-pthread",
            "-o", str(FRONT) + ".tmp", str(FRONT_SRC), str(PROFILE_SRC)]
     r = subprocess.run(cmd, capture_output=True, text=True)
     if r.returncode != 0:

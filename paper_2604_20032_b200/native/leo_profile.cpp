@@ -27,6 +27,7 @@
 #include <cstdlib>
 #include <cstring>
 #include <string>
+#include <thread>
 #include <unordered_map>
 #include <vector>
 
@@ -108,6 +109,7 @@ struct JVal {
   std::string s;              // STR (UTF-8) or the big integer's digits
   std::vector<JVal> arr;
   std::vector<std::pair<std::string, JVal>> obj;   // first-insertion order, last value wins
+  std::vector<int64_t> starts;  // lazy ARR: byte offset of every element (recorded while validating)
 
   bool is_int() const { return t == INT || t == BOOL; }      // isinstance(x, int)
   int64_t ival() const { return t == BOOL ? (int64_t)b : i; }
@@ -217,9 +219,14 @@ struct Scanner {
         case '"': return scanstring(idx + 1, nullptr);
         case '{': return parse_object(idx + 1, nullptr, 0);
         case '[': return parse_array(idx + 1, nullptr, 0);
+        case 'n': if (idx + 3 < n && lit(idx, "null")) return idx + 4; break;
+        case 't': if (idx + 3 < n && lit(idx, "true")) return idx + 4; break;
+        case 'f': if (idx + 4 < n && lit(idx, "false")) return idx + 5; break;
+        case 'N': if (idx + 2 < n && lit(idx, "NaN")) return idx + 3; break;
+        case 'I': if (idx + 7 < n && lit(idx, "Infinity")) return idx + 8; break;
+        case '-': if (idx + 8 < n && lit(idx, "-Infinity")) return idx + 9; break;
       }
-      thread_local JVal scratch;
-      return scan_once(idx, &scratch, 0);
+      return match_number(idx, nullptr);        // grammar only, no conversion
     }
     switch (c) {
       case '"': v->t = JVal::STR; return scanstring(idx + 1, &v->s);
@@ -227,7 +234,8 @@ struct Scanner {
       case '[': {
         v->t = c == '{' ? JVal::OBJ : JVal::ARR;
         if (depth <= 0) {
-          const int64_t e = c == '{' ? parse_object(idx + 1, nullptr, 0) : parse_array(idx + 1, nullptr, 0);
+          const int64_t e = c == '{' ? parse_object(idx + 1, nullptr, 0)
+                                     : parse_array(idx + 1, nullptr, 0, &v->starts);
           v->lazy = true; v->a = idx; v->z = e;
           return e;
         }
@@ -252,12 +260,12 @@ struct Scanner {
         if (idx + 8 < n && lit(idx, "-Infinity")) { v->t = JVal::FLOAT; v->f = -INFINITY; return idx + 9; }
         break;
     }
-    return match_number(idx, *v);
+    return match_number(idx, v);
   }
 
   static bool dig(unsigned char c) { return c >= '0' && c <= '9'; }
 
-  int64_t match_number(int64_t start, JVal& v) {
+  int64_t match_number(int64_t start, JVal* vp) {
     const int64_t end_idx = n - 1;
     int64_t idx = start;
     bool is_float = false;
@@ -286,6 +294,8 @@ struct Scanner {
       if (dig(s[idx - 1])) is_float = true;
       else idx = e_start;
     }
+    if (!vp) return idx;
+    JVal& v = *vp;
     char buf[64];
     const int64_t len = idx - start;
     std::string big;
@@ -357,11 +367,12 @@ struct Scanner {
     return idx + 1;
   }
 
-  int64_t parse_array(int64_t idx, JVal* v, int depth) {
+  int64_t parse_array(int64_t idx, JVal* v, int depth, std::vector<int64_t>* starts = nullptr) {
     const int64_t end_idx = n - 1;
     while (idx <= end_idx && json_ws(s[idx])) idx++;
     if (idx > end_idx || s[idx] != ']') {
       for (;;) {
+        if (starts) starts->push_back(idx);
         if (v) {
           v->arr.emplace_back();
           idx = scan_once(idx, &v->arr.back(), depth);
@@ -669,6 +680,52 @@ std::string sorted_join(std::vector<std::string> keys) {
   return o;
 }
 
+// The records of a samples array, in document order.  A big lazy array is
+// split at element boundaries over host threads; each record is checked in
+// full by one thread, and the error reported is the first record's in
+// document order (what the sequential loop would raise).
+template <class F>
+void load_records(const JVal& samples, F&& one, std::vector<Rec>& out) {
+  Scanner* sc = g_scan;
+  const std::vector<int64_t>& starts = samples.starts;   // element offsets, recorded by the validation
+  const int64_t n = samples.lazy ? (int64_t)starts.size() : (int64_t)samples.arr.size();
+  unsigned nt = std::thread::hardware_concurrency();
+  nt = n < 16384 ? 1u : std::max(1u, std::min(nt, 32u));
+  out.resize((size_t)n);
+  std::vector<int64_t> err_at(nt, -1);
+  std::vector<ProfErr> errs(nt);
+  auto work = [&](unsigned w) {
+    g_scan = sc;
+    const int64_t lo = n * w / nt, hi = n * (w + 1) / nt;
+    JVal e;
+    for (int64_t t = lo; t < hi; t++) {
+      try {
+        if (samples.lazy) {
+          e = JVal();
+          sc->scan_once(starts[(size_t)t], &e, 1 << 20);
+          out[(size_t)t] = one(e);
+        } else {
+          const JVal& x = samples.arr[(size_t)t];
+          out[(size_t)t] = one(x.lazy ? sc->materialize(x) : x);
+        }
+      } catch (const ProfErr& pe) {
+        err_at[w] = t;
+        errs[w] = pe;
+        return;
+      }
+    }
+  };
+  if (nt == 1) {
+    work(0);
+  } else {
+    std::vector<std::thread> th;
+    for (unsigned w = 0; w < nt; w++) th.emplace_back(work, w);
+    for (auto& t : th) t.join();
+  }
+  for (unsigned w = 0; w < nt; w++)      // chunks are in order: the first failing chunk holds the first error
+    if (err_at[w] >= 0) throw errs[w];
+}
+
 // profile._load_one (profile.py:186-241) with the __post_init__ checks of
 // InstructionSamples (:124-144) and KernelProfile (:154-161) in order
 KProf load_one(const JVal& obj) {
@@ -715,7 +772,7 @@ KProf load_one(const JVal& obj) {
   if (samples.t != JVal::ARR) throw ProfErr{1, "samples must be an array"};
   static const char* rfields[] = {"offset", "counts", "latency_samples", "total_samples",
                                   "exec_count", "efficiency"};
-  g_scan->for_each(samples, 1 << 20, [&](const JVal& rec) {
+  auto one = [&](const JVal& rec) -> Rec {
     if (rec.t != JVal::OBJ) throw ProfErr{1, "sample record must be a JSON object"};
     {
       std::vector<std::string> extra;
@@ -787,8 +844,9 @@ KProf load_one(const JVal& obj) {
     if (ef) r.eff = ef->t == JVal::FLOAT ? ef->f : ef->big ? strtod(ef->s.c_str(), nullptr) : (double)ef->i;
     if (!(0.0 < r.eff && r.eff <= 1.0))
       throw ProfErr{1, "efficiency must be in (0,1], got " + float_repr(r.eff)};
-    kp.recs.push_back(r);
-  });
+    return r;
+  };
+  load_records(samples, one, kp.recs);
   kp.name = py_str(*obj.get("kernel"));
   {   // KernelProfile.__post_init__: duplicate offsets, smallest reported
     std::vector<int64_t> offs;

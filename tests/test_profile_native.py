@@ -88,3 +88,35 @@ def test_attach_mismatch_and_skid():
     ks.name, ks.dialect = "k", "nvidia"
     with pytest.raises(front.ProfileError, match="profile vendor amd does not match disassembly dialect nvidia"):
         doc.attach(ks, 0)
+
+
+def test_big_document_parallel_records_and_first_error():
+    """> 16 K records take the multi-threaded record pass: records stay in
+    document order, and with several bad records the error raised is the
+    first one in document order (what the reference's sequential loop
+    raises; message formats as pinned by the golden documents)."""
+    import json as _json
+    n = 40000
+    cats = ["ALU dependency", "waiting for memory", "barrier wait"]
+    recs = [{"offset": f"0x{4 * i:x}", "counts": {cats[i % 3]: i % 7, "other": 1},
+             "latency_samples": i % 7 + 1, "exec_count": i} for i in range(n)]
+    doc = {"kernel": "big", "vendor": "amd", "period_cycles": 64, "samples": recs}
+    d = front.load_profiles(_json.dumps(doc))
+    r = d.records(0)
+    assert r["offset"].tolist() == [4 * i for i in range(n)]
+    assert r["lat"].tolist() == [i % 7 + 1 for i in range(n)]
+    assert r["exec_cnt"].tolist() == list(range(n))
+    cls = r["cls_cnt"]
+    # ALU dependency -> execution_dep (1), waiting for memory -> memory_dep (0),
+    # barrier wait -> synchronization (2), other -> other (7)
+    idx = {0: 1, 1: 0, 2: 2}
+    for i in (0, 1, 2, 12345, n - 1):
+        assert cls[i, idx[i % 3]] == i % 7 and cls[i, 7] == 1
+    bad = _json.loads(_json.dumps(doc))
+    bad["samples"][31000]["bogus"] = 1                     # later chunk
+    bad["samples"][17003]["counts"]["other"] = -1          # earlier chunk: reported
+    with pytest.raises(front.ProfileError, match=r"^negative stall count at offset 0x109ac$"):
+        front.load_profiles(_json.dumps(bad))
+    bad["samples"][5]["latency_samples"] = "x"             # earliest
+    with pytest.raises(front.ProfileError, match=r"^latency_samples must be an integer at offset 0x14$"):
+        front.load_profiles(_json.dumps(bad))
