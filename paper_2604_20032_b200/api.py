@@ -570,8 +570,9 @@ class Session:
         self.dk = device.DeviceKernel(ks, self.dev)
         self.dp = device.DeviceProfile(prof_meta, ks.n_instr, self.dev)
         # raw samples travel packed (one u32 word per sample, pc << 8 | category:
-        # 4 bytes instead of 5) when every pc fits 24 bits
-        self.packed = ks.n_instr < (1 << 24)
+        # 4 bytes instead of 5) when every pc fits 24 bits and the stream is
+        # long enough for the one-pass hashed binning
+        self.packed = ks.n_instr < (1 << 24) and n_samples >= device.PACK_MIN_SAMPLES
         if self.packed:
             self.words = torch.empty(max(n_samples, 1), dtype=torch.int32, device=self.dev)
         else:

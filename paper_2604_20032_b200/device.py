@@ -8,6 +8,7 @@ grown on overflow) so repeated runs reuse memory, as a serving process would.
 from __future__ import annotations
 
 import ctypes as C
+import os
 from dataclasses import dataclass
 
 import numpy as np
@@ -86,16 +87,26 @@ def packable(pc) -> bool:
     return pc.size == 0 or (int(pc.min()) >= 0 and int(pc.max()) < (1 << 24))
 
 
+# streams this long bin in the one-pass hash, which reads the packed words as
+# cheaply as pc / cat; shorter ones take the bucketed passes, which read pc /
+# cat arrays (packing a C2-size stream cost 22 us per step, measured)
+PACK_MIN_SAMPLES = 4 << 20
+
+
 class DeviceSamples:
-    """A raw (pc, category) stream on the device.  `packed` (default: when
-    every pc fits 24 bits) stores it as one u32 word per sample (4 bytes
-    instead of 5, read once by the binning); False keeps pc / cat arrays."""
+    """A raw (pc, category) stream on the device.  `packed` (default: streams
+    of >= PACK_MIN_SAMPLES whose pcs fit 24 bits) stores it as one u32 word
+    per sample (4 bytes instead of 5, read once by the binning); False keeps
+    pc / cat arrays."""
 
     def __init__(self, pc, cat, lut, device="cuda", packed: bool | None = None):
         dev = torch.device(device)
         self.n = int(pc.shape[0])
         self.lut = to_device(np.asarray(lut, dtype=np.uint8), dev)
-        self.packed = packable(pc) if packed is None else packed
+        if packed is None:
+            packed = (int(np.asarray(pc).shape[0]) >= PACK_MIN_SAMPLES and packable(pc)
+                      and not os.environ.get("LEO_NO_PACK"))
+        self.packed = packed
         if self.packed:
             self.words = to_device(pack_samples(pc, cat).view(np.int32), dev)
             self.pc = self.cat = None

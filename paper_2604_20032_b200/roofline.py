@@ -29,7 +29,7 @@ def _sizes(ks, wl, res):
     cfg_edges = int(ks.succ.shape[0])
     # bytes per raw sample as the device reads them: the packed u32 stream
     # (kernels below 2^24 instructions, device.DeviceSamples default) or i32 pc + u8 cat
-    SB = 4 if N < (1 << 24) else 5
+    SB = 4 if (N < (1 << 24) and S >= (4 << 20)) else 5
     return dict(N=N, B=B, M=M, NU=nu, ND=nd, S=S, SB=SB, E=E, Ep=Ep, P=P, NB=nb, L=L, CE=cfg_edges,
                 NREG=int(res.get("n_regular", E)))
 
