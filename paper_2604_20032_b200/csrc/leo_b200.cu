@@ -272,6 +272,7 @@ int build_graph_impl(const LeoKernel* kk, const LeoCaps* caps, LeoEdges* out, Le
   const int64_t cap_sync = pick(caps ? caps->sync_keys : 0, 2 * (int64_t)N + 1024);
   const int64_t cap_slow = pick(caps ? caps->slow_items : 0, N / 4 + 1024);
   const int SM = num_sms();
+  constexpr int kWcCtaGrid = 8;   // CTAs of the CTA waitcnt tier (items that outgrow the warp tier are few)
 
   // per-warp unit tables in shared memory when they fit
   auto walk_bytes = [&](int w, bool tab) { return (size_t)w * ((tab ? 4 * (size_t)U : 0) + kWalkStage) * 4; };
@@ -311,6 +312,11 @@ int build_graph_impl(const LeoKernel* kk, const LeoCaps* caps, LeoEdges* out, Le
   ar.want(&reach_scr, (int64_t)RW * 3 * (B + 1));
   ar.want(&scan_tmp2, scan_scratch_ints(std::max<int64_t>(N, 1)) + 64);
   ar.want(&wlist, N); ar.want(&wclist, cap_slow); ar.want(&slow3s, cap_slow);
+  // the CTA waitcnt tier's record arenas (amd): kWcCtaGrid x 5 x kWcCtaCap ints
+  int32_t* wc_arena = nullptr;
+  const bool use_wc_cta = k.dialect == LEO_AMD && !getenv("LEO_WC_NO_CTA") &&
+                          (getenv("LEO_WC_CTA") || N >= (1 << 17) || kk->n_segments > 1);
+  if (use_wc_cta) ar.want(&wc_arena, (int64_t)kWcCtaGrid * 5 * wc_cta_cap(B));
   ar.want(&sync_scr, (int64_t)SW * sync_slow_bytes_per_worker(sync_bcap));
   const int n_ids = k.dialect == LEO_INTEL ? 32 : 8;
   ar.want(&wcword, N); ar.want(&bev, B); ar.want(&setword, N); ar.want(&lastset, (int64_t)B * n_ids);
@@ -407,7 +413,15 @@ int build_graph_impl(const LeoKernel* kk, const LeoCaps* caps, LeoEdges* out, Le
       sb.slow_list = slow3s; sb.slow_count = &ctr[11];
       TRACED(KID_SYNC_SLOW, leo_launch(k_sync<true>, (SW + 63) / 64, 64, 0, st, k, sb, sync_scr, SW));
     } else {
-      TRACED(KID_SYNC_SLOW, leo_launch(k_sync<true>, (SW + 63) / 64, 64, 0, st, k, sa, sync_scr, SW));
+      // items that outgrew the warp tier: CTA per item over a global record arena first
+      SyncArgs sb = sa;
+      // on big kernels / batches only: on C2 the extra launch on the (near-critical) sync branch cost 8 us
+      if (use_wc_cta) {
+        TRACED(KID_SYNC_SLOW, leo_launch(k_sync_wc_cta, kWcCtaGrid, 1024, 0, st, k, sa, slow2, &ctr[4], cap_slow,
+                                         wc_arena, slow3s, &ctr[11]));
+        sb.slow_list = slow3s; sb.slow_count = &ctr[11];
+      }
+      TRACED(KID_SYNC_SLOW, leo_launch(k_sync<true>, (SW + 63) / 64, 64, 0, st, k, sb, sync_scr, SW));
     }
     TRACED(KID_KEY_HIST, leo_launch(k_key_hist, grid_for(cap_sync, T), T, 0, st, skeys, &ctr[3], cap_sync, pcnt));
     TRACED(KID_SCAN, scan_exclusive(pcnt, poff, nullptr, N, scan_tmp2, nullptr, st));

@@ -372,6 +372,97 @@ __global__ void k_sync_wc_warp(KView k, SyncArgs a, const int32_t* __restrict__ 
   }
 }
 
+// ---- waitcnt items that outgrow the warp tier: CTA per item ------------------
+// The same exact chain-tree enumeration as k_sync_wc_warp (one record per
+// chain: block, state m / a / budget, parent), but breadth-first over the
+// whole CTA with the record arena in global memory (kWcCtaCap records per
+// CTA), so a tree of 10^5 chains runs level by level on 1024 threads instead
+// of depth-first on one (C4's AMD members: a single such item was ~5 ms on the
+// exact walker).  A full arena still ends in the exact walker.
+__host__ __device__ inline int wc_cta_cap(int B) {      // records per CTA arena
+  return (int)min((int64_t)1 << 20, max((int64_t)1 << 16, (int64_t)64 * B));
+}
+
+__global__ void __launch_bounds__(1024) k_sync_wc_cta(KView k, SyncArgs a, const int32_t* __restrict__ list,
+                                                      const int32_t* count, int64_t list_cap, int32_t* arena,
+                                                      int32_t* slow_list, int32_t* slow_count) {
+  pdl_wait();
+  __shared__ int c[4];   // 0 tail, 1 best_m, 2 ovf
+  const int kWcCtaCap = wc_cta_cap(k.B);
+  int32_t* blk = arena + (size_t)blockIdx.x * 5 * kWcCtaCap;
+  int32_t* rm = blk + kWcCtaCap;
+  int32_t* ra = rm + kWcCtaCap;
+  int32_t* rb = ra + kWcCtaCap;
+  int32_t* par = rb + kWcCtaCap;
+  const int n = (int)min((int64_t)*count, list_cap);
+  for (int t = blockIdx.x; t < n; t += gridDim.x) {
+    const int it = list[t];
+    const int wait = it >> 6, counter = it & 63;
+    const uint32_t lv = counter == 0 ? k.sync_a[wait] : k.sync_b[wait];
+    const int level = (int)lv;
+    WcState s;
+    s.counter = counter; s.level = level; s.wait = wait;
+    s.member_bit = counter == 0 ? kWcVm : kWcLgkm;
+    s.nseen = 0; s.sa = &a;
+    const int b0 = k.block_of[wait];
+    if (threadIdx.x == 0) {
+      c[0] = 0; c[1] = 0; c[2] = 0;
+      int m = 0, av = -1, budget = kSyncBudget;
+      const int r = wc_scan(a, wait - 1, k.blk_first[b0], budget, s, m, av);
+      if (r < 0) c[2] = 1;
+      else if (r == 0) c[1] = m;
+      else {
+        bool any = false;
+        for (int q = k.pred_ptr[b0]; q < k.pred_ptr[b0 + 1]; q++) if (k.pred[q] != b0) any = true;
+        if (!any) c[1] = m;
+        else { blk[0] = b0; rm[0] = m; ra[0] = av; rb[0] = budget; par[0] = -1; c[0] = 1; }
+      }
+    }
+    __syncthreads();
+    int head = 0;
+    while (true) {
+      const int tail = c[0];
+      const bool stop = head >= tail || c[2];
+      __syncthreads();                 // every thread read the loop control
+      if (stop) break;
+      for (int r = head + (int)threadIdx.x; r < tail; r += blockDim.x) {
+        const int b = blk[r];
+        for (int q = k.pred_ptr[b]; q < k.pred_ptr[b + 1]; q++) {
+          const int p = k.pred[q];
+          if (rec_on_path(blk, par, r, p)) continue;
+          int m = rm[r], av = ra[r], budget = rb[r];
+          const int res = wc_scan(a, k.blk_last[p], k.blk_first[p], budget, s, m, av);
+          if (res < 0) { c[2] = 1; continue; }
+          if (res == 0) { atomicMax(&c[1], m); continue; }
+          bool any = false;
+          for (int q2 = k.pred_ptr[p]; q2 < k.pred_ptr[p + 1] && !any; q2++) {
+            const int pp = k.pred[q2];
+            if (pp != p && !rec_on_path(blk, par, r, pp)) any = true;
+          }
+          if (!any) { atomicMax(&c[1], m); continue; }
+          const int slot = atomicAdd(&c[0], 1);
+          if (slot >= kWcCtaCap) { c[2] = 1; continue; }
+          blk[slot] = p; rm[slot] = m; ra[slot] = av; rb[slot] = budget; par[slot] = r;
+        }
+      }
+      __syncthreads();
+      head = tail;
+      if (threadIdx.x == 0 && c[0] > kWcCtaCap) c[2] = 1;
+      __syncthreads();
+    }
+    if (threadIdx.x == 0) {
+      if (c[2]) {
+        const int s2 = atomicAdd(slow_count, 1);
+        if (s2 < a.slow_cap) slow_list[s2] = it;
+        else atomicOr(a.status, (uint32_t)LEO_ST_SCRATCH_OVERFLOW);
+      } else if (c[1] < level) {
+        diag_push(a.diags, a.status, LEO_DIAG_WAITCNT, wait, counter, level, c[1], counter);
+      }
+    }
+    __syncthreads();
+  }
+}
+
 // ---- exact (unpacked) waitcnt walker for the slow path ----------------------
 LEO_DEV int wc_visit_exact(const KView& k, int x, WcState& s, int& m, int& a, const SyncArgs& sa) {
   if (k.sync_kind[x] == LEO_SYNC_WAITCNT) {

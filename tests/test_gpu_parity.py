@@ -82,6 +82,7 @@ def test_device_matches_oracle_synthetic(tag, scale, cuda):
 @pytest.mark.parametrize("tag,knobs", [
     ("c2", {"LEO_SYNC_FORK_AT": "0", "LEO_RU_PARTS": "3", "LEO_WC_CTAS": "148", "LEO_PRUNE_THREADS": "128"}),
     ("c2", {"LEO_WC_STEPS": "32", "LEO_NO_PRIO": "1"}),
+    ("c2", {"LEO_WC_STEPS": "16", "LEO_WC_CTA": "1"}),
     ("c3", {"LEO_SYNC_FORK_AT": "2", "LEO_RU_PARTS": "1", "LEO_PRUNE_THREADS": "128"}),
     ("c3", {"LEO_SETTER_GLOBAL": "1"}),
     ("c5", {"LEO_SETTER_GLOBAL": "1"}),
