@@ -1,21 +1,27 @@
 // blame.cu — stage-0 binning, backward slice, blame attribution, line rollup.
 //
-//   k_bin_samples     raw (pc, category) stream -> cls_cnt[N, 8] with warp-
-//                     aggregated atomics (__match_any_sync on pc*8+class, so a
-//                     Zipf-hot PC costs one atomic per warp); k_bin_finalize
-//                     sums lat[N]  (map_stall profile.py:106-111,
-//                     breakdown_at :307-313).
+//   k_bin_hash        big raw (pc, category) streams (>= 4 M samples, packed
+//                     u32 words or pc / cat arrays) -> cls_cnt[N, 8] in one
+//                     pass: a per-CTA open-addressing hash of (pc*8 + class)
+//                     keys in shared memory (two probe slots read up front;
+//                     cold keys straight to L2); k_bin_samples (small streams,
+//                     warp-aggregated atomics) and the bucketed passes
+//                     k_bin_hist/plan/scatter/count; k_bin_finalize sums lat[N]
+//                     (map_stall profile.py:106-111, breakdown_at :307-313).
 //   incoming CSR      DependencyGraph.incoming (depgraph.py:102-108): raw/guard
 //                     edges are consumer-sorted (segment bounds by adjacent-
 //                     difference), sync edges producer-sorted (stable counting
 //                     sort by consumer); incoming(j) = regular(j) ++ sync(j).
-//   k_blame<0/1>      thread per stalled instruction: Eq. 1 (attribute_blame
-//                     analysis.py:431-484) in the reference's exact floating-
-//                     point order (no FMA contraction, CPython 3.12 sum()),
-//                     self-blame (:414-428) with the depth-8 indirect-addressing
-//                     BFS on the unpruned RAW graph (:390-411).
-//   k_lines           per-source-line FP64 scatter-add.
-//   k_slice_*         multi-source backward BFS over pruned incoming edges from
+//   k_mp_*            _address_traces_to_load (analysis.py:390-411) for every
+//                     instruction: Jacobi rounds over the base RAW graph.
+//   k_blame_light /   pass 0 of attribute_blame (analysis.py:431-484): self
+//   k_blame_edges /   verdicts (self_blame :414-428) for instructions without
+//   k_blame<0>        pruned in-edges, Eq. 1 for the rest in the reference's
+//                     exact floating-point order (no FMA contraction, CPython
+//                     3.12 sum()); entries staged once.
+//   k_blame_compact   entries into stalled order + the per-line FP64 rollup
+//                     (k_blame<1> + k_lines in the two-pass A/B mode).
+//   k_slice           multi-source backward BFS over pruned incoming edges from
 //                     every S_j > 0, level-synchronous in one
 //                     cooperative kernel.
 #include <cooperative_groups.h>
