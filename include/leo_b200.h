@@ -60,7 +60,7 @@
 extern "C" {
 #endif
 
-#define LEO_ABI_VERSION 3
+#define LEO_ABI_VERSION 4
 
 /* ---- enumerations (indices follow the reference enum definition order) --- */
 /* Dialect  isa.py:19-22 */
@@ -160,6 +160,12 @@ typedef struct LeoSamples {
    * binning branch as pc_host / cat_host are. */
   const uint32_t* packed;
   const uint32_t* packed_host;
+  /* ABI v4: bytes per packed word.  0 or 4: the u32 words above.  3: one
+   * little-endian 24-bit word per sample, pc << 4 | category (kernels of at
+   * most 2^20 instructions, category ids below 16; 3 bytes per sample over
+   * PCIe instead of 4); packed / packed_host then hold 3 * n_samples bytes,
+   * `packed` 4-byte aligned. */
+  int32_t packed_bytes;
 } LeoSamples;
 
 /* ---- analysis configuration (analysis.py:115-124) ------------------------ */

@@ -17,7 +17,7 @@ LIB_PATH = Path(__file__).resolve().parent / "libleo_b200.so"
 # A/B timing of library variants (profiling only): LEO_LIB_VARIANT=<path>
 if os.environ.get("LEO_LIB_VARIANT"):
     LIB_PATH = Path(os.environ["LEO_LIB_VARIANT"]).resolve()
-ABI_VERSION = 3
+ABI_VERSION = 4
 
 _lib = None
 

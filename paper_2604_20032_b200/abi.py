@@ -36,7 +36,8 @@ class LeoProfile(C.Structure):
 
 class LeoSamples(C.Structure):
     _fields_ = [("n_samples", C.c_int64), ("pc", P), ("cat", P), ("cat_to_cs", P),
-                ("pc_host", P), ("cat_host", P), ("packed", P), ("packed_host", P)]
+                ("pc_host", P), ("cat_host", P), ("packed", P), ("packed_host", P),
+                ("packed_bytes", C.c_int32)]
 
 
 class LeoConfig(C.Structure):

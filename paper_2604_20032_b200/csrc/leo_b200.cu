@@ -231,9 +231,9 @@ void set_smem_attributes() {
   cudaFuncSetAttribute(k_reach_fast<uint16_t, 64, 48>, cudaFuncAttributeMaxDynamicSharedMemorySize, kT1Threads * 64 * 2);
   cudaFuncSetAttribute(k_reach_fast<int32_t, 64, 48>, cudaFuncAttributeMaxDynamicSharedMemorySize, kT1Threads * 64 * 4);
   cudaFuncSetAttribute(k_bin_count, cudaFuncAttributeMaxDynamicSharedMemorySize, kBinRMax * 8 * 4);
-  for (auto f : {k_bin_hash<8192, 8, false>, k_bin_hash<8192, 4, false>, k_bin_hash<16384, 4, false>,
-                 k_bin_hash<16384, 2, false>, k_bin_hash<26624, 4, false>, k_bin_hash<26624, 2, false>,
-                 k_bin_hash<26624, 8, false>, k_bin_hash<16384, 2, true>})
+  for (auto f : {k_bin_hash<8192, 8>, k_bin_hash<8192, 4>, k_bin_hash<16384, 4>,
+                 k_bin_hash<16384, 2>, k_bin_hash<26624, 4>, k_bin_hash<26624, 2>,
+                 k_bin_hash<26624, 8>, k_bin_hash<16384, 2, 4>, k_bin_hash<16384, 2, 3>})
     cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, 26624 * 8);
   cudaFuncSetAttribute(k_bin_scatter, cudaFuncAttributeMaxDynamicSharedMemorySize, kBinMaxBuckets * 12 + kBinSub * 4);
   cudaFuncSetAttribute(k_block_walk, cudaFuncAttributeMaxDynamicSharedMemorySize, 96 * 1024);
@@ -846,9 +846,13 @@ static int bin_impl(const LeoSamples* s, int32_t n_instr, int32_t* lat, int32_t*
   cudaMemsetAsync(cls_cnt, 0, (size_t)std::max(n_instr, 1) * 32, st);
   const int64_t S = s->n_samples;
   const bool packed = s->packed != nullptr;
-  if (packed && (int64_t)n_instr > (1 << 24)) return -3;     // pc must fit 24 bits
+  // bytes per packed word: 4 (pc << 8 | category) or 3 (pc << 4 | category)
+  const int pw = s->packed_bytes == 3 ? 3 : 4;
+  if (packed && s->packed_bytes != 0 && s->packed_bytes != 3 && s->packed_bytes != 4) return -3;
+  if (packed && (int64_t)n_instr > (pw == 3 ? (1 << 20) : (1 << 24))) return -3;   // pc must fit the word
+  if (packed && pw == 3 && ((uintptr_t)s->packed & 3)) return -3;                  // read as u32 triples
   if (S > 0 && packed && s->packed_host)
-    LEO_CUDA_CHECK(cudaMemcpyAsync((void*)s->packed, s->packed_host, (size_t)S * 4, cudaMemcpyHostToDevice, st));
+    LEO_CUDA_CHECK(cudaMemcpyAsync((void*)s->packed, s->packed_host, (size_t)S * pw, cudaMemcpyHostToDevice, st));
   if (S > 0 && !packed && s->pc_host)
     LEO_CUDA_CHECK(cudaMemcpyAsync((void*)s->pc, s->pc_host, (size_t)S * 4, cudaMemcpyHostToDevice, st));
   if (S > 0 && !packed && s->cat_host)
@@ -858,12 +862,15 @@ static int bin_impl(const LeoSamples* s, int32_t n_instr, int32_t* lat, int32_t*
     // table geometry (A/B knobs LEO_BIN_SLOTS / LEO_BIN_PROBE; profiling only)
     const int slots = getenv("LEO_BIN_SLOTS") ? atoi(getenv("LEO_BIN_SLOTS")) : 16384;
     const int probe = getenv("LEO_BIN_PROBE") ? atoi(getenv("LEO_BIN_PROBE")) : 2;
-    auto f = k_bin_hash<26624, 4, false>;
+    auto f = k_bin_hash<26624, 4>;
     int threads = 1024, per_sm = 1;
     if (slots == 8192) { f = probe == 8 ? k_bin_hash<8192, 8> : k_bin_hash<8192, 4>; threads = 512; per_sm = 3; }
     else if (slots == 16384) f = probe == 2 ? k_bin_hash<16384, 2> : k_bin_hash<16384, 4>;
     else f = probe == 2 ? k_bin_hash<26624, 2> : probe == 8 ? k_bin_hash<26624, 8> : k_bin_hash<26624, 4>;
-    if (packed) { f = k_bin_hash<16384, 2, true>; threads = 1024; per_sm = 1; }   // default geometry
+    if (packed) {                                        // default geometry
+      f = pw == 3 ? k_bin_hash<16384, 2, 3> : k_bin_hash<16384, 2, 4>;
+      threads = 1024; per_sm = 1;
+    }
     const int G = getenv("LEO_BIN_CTAS") ? std::max(1, atoi(getenv("LEO_BIN_CTAS"))) : num_sms() * per_sm;
     TRACED(KID_BIN, leo_launch(f, G, threads, (size_t)(packed ? 16384 : slots) * 8, st, S, s->pc, s->cat,
                                s->cat_to_cs, n_instr, cls_cnt, status, s->packed));
@@ -893,7 +900,7 @@ static int bin_impl(const LeoSamples* s, int32_t n_instr, int32_t* lat, int32_t*
                                        s->cat_to_cs, n_instr, nb, R, M, boff, keys));
     TRACED(KID_BIN, leo_launch(k_bin_count, num_sms() * 3, 512, smem, st, n_instr, nb, R, slice, boff, soff, keys, cls_cnt));
   } else if (S > 0) {
-    TRACED(KID_BIN, leo_launch(packed ? k_bin_samples<true> : k_bin_samples<false>, grid_for(S / 4 + 1, 256, num_sms() * 8),
+    TRACED(KID_BIN, leo_launch(!packed ? k_bin_samples<0> : pw == 3 ? k_bin_samples<3> : k_bin_samples<4>, grid_for(S / 4 + 1, 256, num_sms() * 8),
                                256, 0, st, S, s->pc, s->cat, s->cat_to_cs, n_instr, cls_cnt, status, s->packed));
   }
   TRACED(KID_BIN_FINALIZE, leo_launch(k_bin_finalize, grid_for(n_instr, 256), 256, 0, st, n_instr, cls_cnt, lat));

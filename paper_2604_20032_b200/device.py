@@ -87,6 +87,24 @@ def packable(pc) -> bool:
     return pc.size == 0 or (int(pc.min()) >= 0 and int(pc.max()) < (1 << 24))
 
 
+def pack_samples24(pc, cat) -> np.ndarray:
+    """The 3-byte packed stream (LeoSamples.packed_bytes = 3, ABI v4): one
+    little-endian 24-bit word per sample, pc << 4 | category, as 3 * S bytes
+    (padded with zeros to a multiple of 4)."""
+    w = (np.asarray(pc).astype(np.uint32) << np.uint32(4)) | np.asarray(cat, dtype=np.uint8).astype(np.uint32)
+    n = w.shape[0]
+    out = np.zeros((3 * n + 3) & ~3, dtype=np.uint8)
+    out[:3 * n] = w.view(np.uint8).reshape(n, 4)[:, :3].reshape(-1)
+    return out
+
+
+def packable24(pc, cat, n_instr: int) -> bool:
+    """pc < n_instr <= 2^20 and categories below 16 (the 24-bit word)."""
+    pc, cat = np.asarray(pc), np.asarray(cat)
+    return (n_instr <= (1 << 20) and (pc.size == 0 or (int(pc.min()) >= 0 and int(pc.max()) < n_instr
+                                                      and int(cat.max()) < 16)))
+
+
 # streams this long bin in the one-pass hash, which reads the packed words as
 # cheaply as pc / cat; shorter ones take the bucketed passes, which read pc /
 # cat arrays (packing a C2-size stream cost 22 us per step, measured)
@@ -97,9 +115,10 @@ class DeviceSamples:
     """A raw (pc, category) stream on the device.  `packed` (default: streams
     of >= PACK_MIN_SAMPLES whose pcs fit 24 bits) stores it as one u32 word
     per sample (4 bytes instead of 5, read once by the binning); False keeps
-    pc / cat arrays."""
+    pc / cat arrays.  `width` 3 (packed only): the 3-byte stream of
+    pack_samples24."""
 
-    def __init__(self, pc, cat, lut, device="cuda", packed: bool | None = None):
+    def __init__(self, pc, cat, lut, device="cuda", packed: bool | None = None, width: int | None = None):
         dev = torch.device(device)
         self.n = int(pc.shape[0])
         self.lut = to_device(np.asarray(lut, dtype=np.uint8), dev)
@@ -107,7 +126,17 @@ class DeviceSamples:
             packed = (int(np.asarray(pc).shape[0]) >= PACK_MIN_SAMPLES and packable(pc)
                       and not os.environ.get("LEO_NO_PACK"))
         self.packed = packed
-        if self.packed:
+        if width is None and packed and os.environ.get("LEO_PACK3"):
+            width = 3 if packable24(pc, cat, 1 << 20) else 4
+        self.width = 4
+        if self.packed and width == 3:
+            self.width = 3
+            self.words = to_device(pack_samples24(pc, cat), dev)
+            self.pc = self.cat = None
+            self.struct = abi.LeoSamples(self.n, None, None, ptr(self.lut))
+            self.struct.packed = ptr(self.words)
+            self.struct.packed_bytes = 3
+        elif self.packed:
             self.words = to_device(pack_samples(pc, cat).view(np.int32), dev)
             self.pc = self.cat = None
             self.struct = abi.LeoSamples(self.n, None, None, ptr(self.lut))
@@ -121,19 +150,21 @@ class DeviceSamples:
     def from_tensors(cls, pc: torch.Tensor, cat: torch.Tensor, lut: torch.Tensor):
         self = cls.__new__(cls)
         self.n = int(pc.numel())
-        self.pc, self.cat, self.lut, self.packed = pc, cat, lut, False
+        self.pc, self.cat, self.lut, self.packed, self.width = pc, cat, lut, False, 4
         self.struct = abi.LeoSamples(self.n, ptr(pc), ptr(cat), ptr(lut))
         return self
 
     @classmethod
-    def from_packed(cls, words: torch.Tensor, lut: torch.Tensor):
-        """Device u32 (int32-typed) words pc << 8 | category."""
+    def from_packed(cls, words: torch.Tensor, lut: torch.Tensor, n: int | None = None, width: int = 4):
+        """Device u32 (int32-typed) words pc << 8 | category (width 4), or the
+        3-byte stream of pack_samples24 (width 3, uint8 tensor, `n` samples)."""
         self = cls.__new__(cls)
-        self.n = int(words.numel())
-        self.words, self.lut, self.packed = words, lut, True
+        self.n = int(words.numel()) if n is None else int(n)
+        self.words, self.lut, self.packed, self.width = words, lut, True, width
         self.pc = self.cat = None
         self.struct = abi.LeoSamples(self.n, None, None, ptr(lut))
         self.struct.packed = ptr(words)
+        self.struct.packed_bytes = width
         return self
 
     def set_host_packed(self, words_host: torch.Tensor | None):
@@ -406,14 +437,14 @@ class Analyzer:
 
 
 def analyze_soa(ks, prof, cfg: abi.LeoConfig | None = None, samples=None, device="cuda",
-                debug_flags: int = 0, packed: bool | None = None) -> dict:
+                debug_flags: int = 0, packed: bool | None = None, width: int | None = None) -> dict:
     """One-shot convenience: upload, run, download."""
     dk = DeviceKernel(ks, device)
     dp = DeviceProfile(prof, ks.n_instr, device)
     ds = None
     if samples is not None:
         pc, cat, lut = samples
-        ds = DeviceSamples(pc, cat, lut, device, packed=packed)
+        ds = DeviceSamples(pc, cat, lut, device, packed=packed, width=width)
     an = Analyzer(dk, device, debug_flags=debug_flags)
     an.run(dp, cfg or abi.make_config(dialect=ks.dialect), ds)
     r = an.result()

@@ -25,7 +25,7 @@ def test_library_exports_every_declared_symbol():
             "leo_analyze", "leo_abi_version"} <= set(names)
     for n in names:
         assert hasattr(L, n), n
-    assert L.leo_abi_version() == 3
+    assert L.leo_abi_version() == 4
 
 
 def test_front_library_exports_every_declared_symbol():
@@ -63,7 +63,7 @@ def test_ctypes_struct_sizes_match_header():
     assert C.sizeof(abi.LeoDiag) == 24
     assert C.sizeof(abi.LeoConfig) == 16 + 16 * 8 + 8
     assert C.sizeof(abi.LeoCaps) == 72
-    assert C.sizeof(abi.LeoSamples) == 8 + 7 * 8          # ABI v3: + packed, packed_host
+    assert C.sizeof(abi.LeoSamples) == 8 + 7 * 8 + 8      # v3: + packed, packed_host; v4: + packed_bytes
     assert abi.LeoKernel.opclass.offset == 4 * 15 + 4  # 15 int32 + padding to 8
 
 

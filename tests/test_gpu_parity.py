@@ -225,16 +225,21 @@ def test_device_batch_matches_per_kernel_oracle(cuda):
                          ("level", o.level)):
                 assert np.array_equal(got[f], e), (dialect, wl.kernel.name, f)
 
+@pytest.mark.parametrize("width", [4, 3])
 @pytest.mark.parametrize("tag,scale", [("c2", 0.2), ("c5", 0.05)])
-def test_packed_and_split_sample_streams_agree(tag, scale, cuda):
-    """The packed stream (one u32 word per sample, LeoSamples.packed) bins to
-    the same counts and the same analysis as the pc / cat arrays, on the
-    small-stream kernel (C2 scale) and the one-pass hash (5 M samples)."""
+def test_packed_and_split_sample_streams_agree(tag, scale, width, cuda):
+    """The packed stream (one u32 word per sample, or the 3-byte words of
+    packed_bytes = 3) bins to the same counts and the same analysis as the
+    pc / cat arrays, on the small-stream kernel (C2 scale) and the one-pass
+    hash (5 M samples); the stream is cut to a length that is not a multiple
+    of 4 so the tail path runs too."""
     from paper_2604_20032_b200 import abi, device, synth
     wl = synth.config_workload(tag, scale=scale)
     cfg = abi.make_config(dialect=wl.kernel.dialect)
-    a = device.analyze_soa(wl.kernel, wl.profile, cfg, samples=(wl.pc, wl.cat, wl.lut), device=cuda, packed=True)
-    b = device.analyze_soa(wl.kernel, wl.profile, cfg, samples=(wl.pc, wl.cat, wl.lut), device=cuda, packed=False)
+    n = len(wl.pc) - 3
+    smp = (wl.pc[:n], wl.cat[:n], wl.lut)
+    a = device.analyze_soa(wl.kernel, wl.profile, cfg, samples=smp, device=cuda, packed=True, width=width)
+    b = device.analyze_soa(wl.kernel, wl.profile, cfg, samples=smp, device=cuda, packed=False)
     assert a["status"] == 0 and b["status"] == 0
     for key in ("lat", "cls_cnt", "bprod", "bmeta", "pprod", "e_stalled", "e_blame", "level"):
         assert np.array_equal(a[key], b[key]), key

@@ -67,3 +67,27 @@ def test_session_graph_matches_oracle(tag, scale, cuda):
     r = sess.analyze(allreduce=lambda lb, ls: None)
     assert full_entries_match(r, o2)
     assert sess.last_d2h >= 53 * len(o2.e_stalled)
+
+
+@pytest.mark.parametrize("tag,scale,width", [("c5", 0.05, 3), ("c3", 1.0, 4)])
+def test_session_packed_streams_match_oracle(tag, scale, width, cuda):
+    """Streams of >= 4 M samples travel packed: 3 bytes per sample for NVIDIA /
+    AMD kernels of at most 2^20 instructions, the u32 words otherwise (Intel's
+    17 category ids need 5 bits)."""
+    from oracle import oracle
+    from paper_2604_20032_b200 import abi, api, synth
+    wl = synth.config_workload(tag, scale=scale)
+    ks = wl.kernel
+    sess = api.Session(ks, wl.profile, wl.n_samples, abi.make_config(dialect=ks.dialect), cuda)
+    assert sess.packed and sess.pack_width == width
+    sess.stage(ks, wl.profile, wl.pc, wl.cat, wl.lut)
+    assert sess.h2d_bytes() >= width * wl.n_samples
+    o = oracle.run(ks, synth.bin_host(wl), abi.make_config(dialect=ks.dialect))
+    for call in range(2):
+        r = sess.analyze()
+        assert full_entries_match(r, o), call
+    if width == 3:
+        bad = wl.cat.copy()
+        bad[7] = 16
+        with pytest.raises(ValueError, match="category id >= 16"):
+            sess.stage(ks, wl.profile, wl.pc, bad, wl.lut)
