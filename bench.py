@@ -473,8 +473,23 @@ def run_ours(args, ws, rank, local):
     def e2e_allreduce(lb, ls):
         D.allreduce_lines(lb, ls)
 
-    for sess in sessions:
-        sess.analyze(allreduce=e2e_allreduce if ws > 1 else None)
+    # several sessions (a C4 batch pipeline per dialect) on one GPU: submit
+    # every call on its own stream, then collect, so one call's read-back
+    # overlaps the next one's upload and compute (PCIe is full duplex)
+    overlap = ws == 1 and len(sessions) > 1 and not os.environ.get("LEO_E2E_SERIAL")
+    streams = [torch.cuda.Stream(dev) for _ in sessions] if overlap else None
+
+    def e2e_call():
+        if overlap:
+            for sess, st in zip(sessions, streams):
+                sess.submit(st)
+            for sess in sessions:
+                sess.collect()
+        else:
+            for sess in sessions:
+                sess.analyze(allreduce=e2e_allreduce if ws > 1 else None)
+
+    e2e_call()
     e2e_t = []
     n_e2e = max(5, min(args.steps * 5, 50))
     for s in range(n_e2e):
@@ -482,8 +497,7 @@ def run_ours(args, ws, rank, local):
             dist.barrier()
         torch.cuda.synchronize()
         t0 = time.perf_counter()
-        for sess in sessions:
-            sess.analyze(allreduce=e2e_allreduce if ws > 1 else None)
+        e2e_call()
         e2e_t.append(time.perf_counter() - t0)
     # host-timed calls jitter with the box's CPU scheduling: the median call
     # time (max over ranks) is the reported figure, the mean rides along
@@ -531,7 +545,8 @@ def run_ours(args, ws, rank, local):
             "e2e": {"value": e2e_value, "unit": UNIT,
                     "h2d_bytes_per_step": int(sum(s.h2d_bytes() for s in sessions)),
                     "d2h_bytes_per_step": int(sum(s.last_d2h for s in sessions)),
-                    "sample": f"{len(sessions)} kernel(s) per rank through api.Session",
+                    "sample": f"{len(sessions)} kernel(s) per rank through api.Session"
+                              + (" (submit / collect on one stream each)" if overlap else ""),
                     "stat": f"median of {len(e2e_t)} calls (max over ranks)", "mean_value": e2e_mean_value},
             "gpu_launches": n_launch * len(plan.items) * args.steps,
             "clocks": clocks.summary(),

@@ -831,24 +831,50 @@ class Session:
         CUDA graph (H2D + pipeline + D2H of counters, touched lines and the
         entries' expected prefix); longer results read back their tail."""
         if allreduce is None and self.use_graph:
-            if getattr(self, "graph", None) is None:
-                self._capture()
+            self.submit()
+            r = self._collect_graph(copy)
+            if r is not None:
+                return r
+        return self._analyze_eager(allreduce, copy)
+
+    def submit(self, stream: torch.cuda.Stream | None = None):
+        """Start one call without waiting for it: replay the session's CUDA
+        graph (H2D, pipeline, D2H prefixes) on `stream` (default: the current
+        stream).  `collect()` waits and returns the result.  Sessions submitted
+        on different streams overlap each other's transfers and compute (a
+        batch of kernels: one call's read-back beside the next one's upload)."""
+        if getattr(self, "graph", None) is None:
+            self._capture()
+        self._stream = stream if stream is not None else torch.cuda.current_stream(self.dev)
+        with torch.cuda.stream(self._stream):
             self.graph.replay()
-            torch.cuda.current_stream(self.dev).synchronize()
-            c = self.n_ctr
-            nbl = int(c[device.C_BLAME])
-            nl = int(self.n_lcnt[0])
-            if c[device.C_STATUS] == 0 and nbl <= self.an.caps.blame and nl <= self.n_lines:
-                if nbl > self.k_pre or nl > self.l_pre:   # tails beyond the in-graph prefixes
+
+    def collect(self, copy: bool = False):
+        """The result of the last `submit()` (as `analyze()` returns it)."""
+        r = self._collect_graph(copy)
+        return r if r is not None else self._analyze_eager(None, copy)
+
+    def _collect_graph(self, copy):
+        st = self._stream
+        st.synchronize()
+        c = self.n_ctr
+        nbl = int(c[device.C_BLAME])
+        nl = int(self.n_lcnt[0])
+        if c[device.C_STATUS] == 0 and nbl <= self.an.caps.blame and nl <= self.n_lines:
+            if nbl > self.k_pre or nl > self.l_pre:   # tails beyond the in-graph prefixes
+                with torch.cuda.stream(st):
                     if nbl > self.k_pre:
                         self._copy_entries(self.k_pre, nbl)
                     if nl > self.l_pre:
                         self._copy_lines(self.l_pre, nl)
-                    torch.cuda.current_stream(self.dev).synchronize()
-                self.last_d2h = (c.nbytes + 4 + 20 * max(nl, self.l_pre)
-                                 + self._entry_bytes(max(nbl, self.k_pre)))
-                return self._result(self.n_ent, nbl, self.n_lid[:nl], self.n_lb[:nl], self.n_ls[:nl], copy)
-            self.graph = None                  # overflow: grow eagerly, recapture next call
+                st.synchronize()
+            self.last_d2h = (c.nbytes + 4 + 20 * max(nl, self.l_pre)
+                             + self._entry_bytes(max(nbl, self.k_pre)))
+            return self._result(self.n_ent, nbl, self.n_lid[:nl], self.n_lb[:nl], self.n_ls[:nl], copy)
+        self.graph = None                  # overflow: grow eagerly, recapture next call
+        return None
+
+    def _analyze_eager(self, allreduce, copy):
         self._h2d()
         self.an.launch(self.dp, self.cfg, self.ds)
         c = self.an.ctr.cpu().numpy()          # sync: how much to read back

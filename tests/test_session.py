@@ -91,3 +91,27 @@ def test_session_packed_streams_match_oracle(tag, scale, width, cuda):
         bad[7] = 16
         with pytest.raises(ValueError, match="category id >= 16"):
             sess.stage(ks, wl.profile, wl.pc, bad, wl.lut)
+
+
+def test_sessions_submitted_on_streams_match_serial_calls(cuda):
+    """Session.submit / collect on separate streams (calls overlapping) give
+    the same results as serial analyze() calls."""
+    from paper_2604_20032_b200 import abi, api, synth
+    sessions, refs = [], []
+    for tag, scale in (("c2", 0.2), ("c3", 0.02), ("c5", 0.004)):
+        wl = synth.config_workload(tag, scale=scale)
+        ks = wl.kernel
+        sess = api.Session(ks, wl.profile, wl.n_samples, abi.make_config(dialect=ks.dialect), cuda)
+        sess.stage(ks, wl.profile, wl.pc, wl.cat, wl.lut)
+        refs.append(sess.analyze(copy=True))
+        sessions.append(sess)
+    streams = [torch.cuda.Stream(cuda) for _ in sessions]
+    for _ in range(3):
+        for sess, st in zip(sessions, streams):
+            sess.submit(st)
+        for sess, ref in zip(sessions, refs):
+            r = sess.collect()
+            for k in ("e_stalled", "e_cause", "e_meta", "e_sub", "e_blame", "e_factors", "line_ids"):
+                assert np.array_equal(r[k], ref[k]), k
+            for k in ("line_blame", "line_stall"):         # f64 atomics: order-dependent rounding
+                np.testing.assert_allclose(r[k], ref[k], rtol=1e-9)
