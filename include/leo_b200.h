@@ -166,6 +166,10 @@ typedef struct LeoSamples {
    * PCIe instead of 4); packed / packed_host then hold 3 * n_samples bytes,
    * `packed` 4-byte aligned. */
   int32_t packed_bytes;
+  /* ABI v4, 3-byte words only: category bits, 0 / 4 (pc << 4 | category) or 5
+   * (pc << 5 | category: up to 32 category ids, Intel's 17; kernels of at
+   * most 2^19 instructions) */
+  int32_t packed_cat_bits;
 } LeoSamples;
 
 /* ---- analysis configuration (analysis.py:115-124) ------------------------ */

@@ -37,7 +37,7 @@ class LeoProfile(C.Structure):
 class LeoSamples(C.Structure):
     _fields_ = [("n_samples", C.c_int64), ("pc", P), ("cat", P), ("cat_to_cs", P),
                 ("pc_host", P), ("cat_host", P), ("packed", P), ("packed_host", P),
-                ("packed_bytes", C.c_int32)]
+                ("packed_bytes", C.c_int32), ("packed_cat_bits", C.c_int32)]
 
 
 class LeoConfig(C.Structure):

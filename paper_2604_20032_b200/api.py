@@ -574,10 +574,12 @@ class Session:
         # 4 bytes instead of 5) when every pc fits 24 bits and the stream is
         # long enough for the one-pass hashed binning
         self.packed = ks.n_instr < (1 << 24) and n_samples >= device.PACK_MIN_SAMPLES
-        # 3 bytes per sample (pc << 4 | category) when pcs fit 20 bits and the
-        # dialect's category ids 4 (NVIDIA, AMD): a quarter less over PCIe
+        # 3 bytes per sample (pc << cat_bits | category) when the pcs and the
+        # dialect's category ids fit 24 bits together (4 category bits for
+        # NVIDIA / AMD, 5 for Intel): a quarter less over PCIe
         self.pack_width = 4
-        if (self.packed and ks.n_instr <= (1 << 20) and len(E.vendor_categories(ks.dialect)) <= 16
+        self.cat_bits = device.cat_bits_for(len(E.vendor_categories(ks.dialect)))
+        if (self.packed and self.cat_bits and ks.n_instr <= (1 << (24 - self.cat_bits))
                 and not os.environ.get("LEO_PACK4")):
             self.pack_width = 3
         if self.packed and self.pack_width == 3:
@@ -594,7 +596,8 @@ class Session:
         if pin:
             self._pack_inputs()
         if self.packed and self.pack_width == 3:
-            self.ds = device.DeviceSamples.from_packed(self.words, self.lut, n=n_samples, width=3)
+            self.ds = device.DeviceSamples.from_packed(self.words, self.lut, n=n_samples, width=3,
+                                                       cat_bits=self.cat_bits)
         elif self.packed:
             self.ds = device.DeviceSamples.from_packed(self.words[:n_samples], self.lut)
         else:
@@ -687,10 +690,10 @@ class Session:
         self._h("lut", lut)
         # the library copies the sample stream itself, on the binning branch
         if self.packed and self.pack_width == 3:
-            if not device.packable24(pc, cat, self.ks.n_instr):
+            if not device.packable24(pc, cat, self.ks.n_instr, self.cat_bits):
                 raise ValueError("Session.stage: sample pc out of range (negative or >= n_instr) "
-                                 "or category id >= 16")
-            self._h("words", device.pack_samples24(pc, cat))
+                                 f"or category id >= {1 << self.cat_bits}")
+            self._h("words", device.pack_samples24(pc, cat, self.cat_bits))
             self.ds.set_host_packed(self._host["words"])
         elif self.packed:
             if not device.packable(pc):

@@ -37,37 +37,40 @@ namespace leo {
 // ---- stage 0 ---------------------------------------------------------------
 // PACK: 0 = pc / category arrays; 4 = one u32 word per sample, pc << 8 |
 // category (4 B per sample instead of 5; kernels below 2^24 instructions);
-// 3 = one little-endian 24-bit word per sample, pc << 4 | category (3 B per
-// sample; kernels of at most 2^20 instructions, categories below 16)
+// 3 = one little-endian 24-bit word per sample, pc << CB | category (3 B per
+// sample; kernels of at most 2^(24 - CB) instructions, categories below 2^CB)
 LEO_DEV void unpack4(const uint4 w, int4& p, uint32_t& c) {
   p = make_int4((int)(w.x >> 8), (int)(w.y >> 8), (int)(w.z >> 8), (int)(w.w >> 8));
   c = (w.x & 0xFFu) | ((w.y & 0xFFu) << 8) | ((w.z & 0xFFu) << 16) | ((w.w & 0xFFu) << 24);
 }
-// four 24-bit words from their 12 bytes (three u32 little-endian)
+// four 24-bit words from their 12 bytes (three u32 little-endian); CB
+// category bits (4, or 5 for Intel's 17 category ids)
+template <int CB>
 LEO_DEV void unpack4_24(const uint32_t x, const uint32_t y, const uint32_t z, int4& p, uint32_t& c) {
+  constexpr uint32_t m = (1u << CB) - 1u;
   const uint32_t w0 = x & 0xFFFFFFu, w1 = (x >> 24) | ((y & 0xFFFFu) << 8);
   const uint32_t w2 = (y >> 16) | ((z & 0xFFu) << 16), w3 = z >> 8;
-  p = make_int4((int)(w0 >> 4), (int)(w1 >> 4), (int)(w2 >> 4), (int)(w3 >> 4));
-  c = (w0 & 15u) | ((w1 & 15u) << 8) | ((w2 & 15u) << 16) | ((w3 & 15u) << 24);
+  p = make_int4((int)(w0 >> CB), (int)(w1 >> CB), (int)(w2 >> CB), (int)(w3 >> CB));
+  c = (w0 & m) | ((w1 & m) << 8) | ((w2 & m) << 16) | ((w3 & m) << 24);
 }
 // one sample of a packed stream (tails)
-template <int PACK>
+template <int PACK, int CB>
 LEO_DEV void unpack1(const uint32_t* packed, int64_t s, int& j, uint32_t& c) {
   if (PACK == 4) { const uint32_t w = packed[s]; j = (int)(w >> 8); c = w & 0xFFu; return; }
   const uint8_t* b = reinterpret_cast<const uint8_t*>(packed) + 3 * s;
   const uint32_t w = (uint32_t)b[0] | ((uint32_t)b[1] << 8) | ((uint32_t)b[2] << 16);
-  j = (int)(w >> 4); c = w & 15u;
+  j = (int)(w >> CB); c = w & ((1u << CB) - 1u);
 }
 // the v-th vector of four samples
-template <int PACK>
+template <int PACK, int CB>
 LEO_DEV void load4(const uint32_t* packed, int64_t v, bool valid, int4& p, uint32_t& c) {
   if (!valid) { p = make_int4(0, 0, 0, 0); c = 0u; return; }
   if (PACK == 4) { unpack4(reinterpret_cast<const uint4*>(packed)[v], p, c); return; }
   const uint32_t* w = packed + 3 * v;
-  unpack4_24(w[0], w[1], w[2], p, c);
+  unpack4_24<CB>(w[0], w[1], w[2], p, c);
 }
 
-template <int PACK>
+template <int PACK, int CB = 4>
 __global__ void k_bin_samples(int64_t S, const int32_t* __restrict__ pc, const uint8_t* __restrict__ cat,
                               const uint8_t* __restrict__ lut, int N, int32_t* __restrict__ cls_cnt,
                               uint32_t* status, const uint32_t* __restrict__ packed) {
@@ -83,7 +86,7 @@ __global__ void k_bin_samples(int64_t S, const int32_t* __restrict__ pc, const u
     const bool valid = v < nvec;
     int4 p;
     uint32_t c;
-    if (PACK) load4<PACK>(packed, v, valid, p, c);
+    if (PACK) load4<PACK, CB>(packed, v, valid, p, c);
     else { p = valid ? pc4[v] : make_int4(0, 0, 0, 0); c = valid ? cat4[v] : 0u; }
     int pcs[4] = {p.x, p.y, p.z, p.w};
 #pragma unroll
@@ -100,7 +103,7 @@ __global__ void k_bin_samples(int64_t S, const int32_t* __restrict__ pc, const u
   for (int64_t s = nvec * 4 + blockIdx.x * (int64_t)blockDim.x + threadIdx.x; s < S; s += stride) {
     int j;
     uint32_t cb;
-    if (PACK) unpack1<PACK>(packed, s, j, cb);
+    if (PACK) unpack1<PACK, CB>(packed, s, j, cb);
     else { j = pc[s]; cb = cat[s]; }
     if (j < 0 || j >= N) { atomicOr(status, (uint32_t)LEO_ST_BAD_INPUT); continue; }
     atomicAdd(&cls_cnt[j * 8 + slut[cb]], 1);
@@ -116,7 +119,7 @@ __global__ void k_bin_samples(int64_t S, const int32_t* __restrict__ pc, const u
 // passes' hist + scatter + count: ~3 reads and a key write).
 constexpr uint32_t kBinEmpty = 0xFFFFFFFFu;
 
-template <int SLOTS, int PROBE, int PACK = 0>
+template <int SLOTS, int PROBE, int PACK = 0, int CB = 4>
 __global__ void __launch_bounds__(1024) k_bin_hash(int64_t S, const int32_t* __restrict__ pc,
                                                    const uint8_t* __restrict__ cat,
                                                    const uint8_t* __restrict__ lut, int N,
@@ -190,8 +193,8 @@ __global__ void __launch_bounds__(1024) k_bin_hash(int64_t S, const int32_t* __r
     int4 p0, p1;
     uint32_t c0, c1;
     if (PACK) {
-      load4<PACK>(packed, v, in0, p0, c0);
-      load4<PACK>(packed, v + bd, in1, p1, c1);
+      load4<PACK, CB>(packed, v, in0, p0, c0);
+      load4<PACK, CB>(packed, v + bd, in1, p1, c1);
     } else {
       p0 = in0 ? pc4[v] : make_int4(0, 0, 0, 0);
       p1 = in1 ? pc4[v + bd] : make_int4(0, 0, 0, 0);
@@ -207,7 +210,7 @@ __global__ void __launch_bounds__(1024) k_bin_hash(int64_t S, const int32_t* __r
     if (s < S) {
       int j;
       uint32_t cb;
-      if (PACK) unpack1<PACK>(packed, s, j, cb);
+      if (PACK) unpack1<PACK, CB>(packed, s, j, cb);
       else { j = pc[s]; cb = cat[s]; }
       const bool ok = (uint32_t)j < (uint32_t)N;
       bad |= !ok;

@@ -233,7 +233,8 @@ void set_smem_attributes() {
   cudaFuncSetAttribute(k_bin_count, cudaFuncAttributeMaxDynamicSharedMemorySize, kBinRMax * 8 * 4);
   for (auto f : {k_bin_hash<8192, 8>, k_bin_hash<8192, 4>, k_bin_hash<16384, 4>,
                  k_bin_hash<16384, 2>, k_bin_hash<26624, 4>, k_bin_hash<26624, 2>,
-                 k_bin_hash<26624, 8>, k_bin_hash<16384, 2, 4>, k_bin_hash<16384, 2, 3>})
+                 k_bin_hash<26624, 8>, k_bin_hash<16384, 2, 4>, k_bin_hash<16384, 2, 3>,
+                 k_bin_hash<16384, 2, 3, 5>})
     cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, 26624 * 8);
   cudaFuncSetAttribute(k_bin_scatter, cudaFuncAttributeMaxDynamicSharedMemorySize, kBinMaxBuckets * 12 + kBinSub * 4);
   cudaFuncSetAttribute(k_block_walk, cudaFuncAttributeMaxDynamicSharedMemorySize, 96 * 1024);
@@ -848,8 +849,11 @@ static int bin_impl(const LeoSamples* s, int32_t n_instr, int32_t* lat, int32_t*
   const bool packed = s->packed != nullptr;
   // bytes per packed word: 4 (pc << 8 | category) or 3 (pc << 4 | category)
   const int pw = s->packed_bytes == 3 ? 3 : 4;
+  // 3-byte words: category bits (4 default, 5 for up to 32 category ids)
+  const int cb = s->packed_cat_bits == 0 ? 4 : s->packed_cat_bits;
   if (packed && s->packed_bytes != 0 && s->packed_bytes != 3 && s->packed_bytes != 4) return -3;
-  if (packed && (int64_t)n_instr > (pw == 3 ? (1 << 20) : (1 << 24))) return -3;   // pc must fit the word
+  if (packed && pw == 3 && cb != 4 && cb != 5) return -3;
+  if (packed && (int64_t)n_instr > (pw == 3 ? (1 << (24 - cb)) : (1 << 24))) return -3;   // pc must fit the word
   if (packed && pw == 3 && ((uintptr_t)s->packed & 3)) return -3;                  // read as u32 triples
   if (S > 0 && packed && s->packed_host)
     LEO_CUDA_CHECK(cudaMemcpyAsync((void*)s->packed, s->packed_host, (size_t)S * pw, cudaMemcpyHostToDevice, st));
@@ -868,7 +872,7 @@ static int bin_impl(const LeoSamples* s, int32_t n_instr, int32_t* lat, int32_t*
     else if (slots == 16384) f = probe == 2 ? k_bin_hash<16384, 2> : k_bin_hash<16384, 4>;
     else f = probe == 2 ? k_bin_hash<26624, 2> : probe == 8 ? k_bin_hash<26624, 8> : k_bin_hash<26624, 4>;
     if (packed) {                                        // default geometry
-      f = pw == 3 ? k_bin_hash<16384, 2, 3> : k_bin_hash<16384, 2, 4>;
+      f = pw == 4 ? k_bin_hash<16384, 2, 4> : cb == 5 ? k_bin_hash<16384, 2, 3, 5> : k_bin_hash<16384, 2, 3>;
       threads = 1024; per_sm = 1;
     }
     const int G = getenv("LEO_BIN_CTAS") ? std::max(1, atoi(getenv("LEO_BIN_CTAS"))) : num_sms() * per_sm;
@@ -900,7 +904,7 @@ static int bin_impl(const LeoSamples* s, int32_t n_instr, int32_t* lat, int32_t*
                                        s->cat_to_cs, n_instr, nb, R, M, boff, keys));
     TRACED(KID_BIN, leo_launch(k_bin_count, num_sms() * 3, 512, smem, st, n_instr, nb, R, slice, boff, soff, keys, cls_cnt));
   } else if (S > 0) {
-    TRACED(KID_BIN, leo_launch(!packed ? k_bin_samples<0> : pw == 3 ? k_bin_samples<3> : k_bin_samples<4>, grid_for(S / 4 + 1, 256, num_sms() * 8),
+    TRACED(KID_BIN, leo_launch(!packed ? k_bin_samples<0> : pw == 4 ? k_bin_samples<4> : cb == 5 ? k_bin_samples<3, 5> : k_bin_samples<3>, grid_for(S / 4 + 1, 256, num_sms() * 8),
                                256, 0, st, S, s->pc, s->cat, s->cat_to_cs, n_instr, cls_cnt, status, s->packed));
   }
   TRACED(KID_BIN_FINALIZE, leo_launch(k_bin_finalize, grid_for(n_instr, 256), 256, 0, st, n_instr, cls_cnt, lat));

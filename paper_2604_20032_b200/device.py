@@ -87,22 +87,29 @@ def packable(pc) -> bool:
     return pc.size == 0 or (int(pc.min()) >= 0 and int(pc.max()) < (1 << 24))
 
 
-def pack_samples24(pc, cat) -> np.ndarray:
+def pack_samples24(pc, cat, cat_bits: int = 4) -> np.ndarray:
     """The 3-byte packed stream (LeoSamples.packed_bytes = 3, ABI v4): one
-    little-endian 24-bit word per sample, pc << 4 | category, as 3 * S bytes
-    (padded with zeros to a multiple of 4)."""
-    w = (np.asarray(pc).astype(np.uint32) << np.uint32(4)) | np.asarray(cat, dtype=np.uint8).astype(np.uint32)
+    little-endian 24-bit word per sample, pc << cat_bits | category, as 3 * S
+    bytes (padded with zeros to a multiple of 4)."""
+    w = ((np.asarray(pc).astype(np.uint32) << np.uint32(cat_bits))
+         | np.asarray(cat, dtype=np.uint8).astype(np.uint32))
     n = w.shape[0]
     out = np.zeros((3 * n + 3) & ~3, dtype=np.uint8)
     out[:3 * n] = w.view(np.uint8).reshape(n, 4)[:, :3].reshape(-1)
     return out
 
 
-def packable24(pc, cat, n_instr: int) -> bool:
-    """pc < n_instr <= 2^20 and categories below 16 (the 24-bit word)."""
+def cat_bits_for(n_categories: int) -> int:
+    """Category bits of the 3-byte word for a dialect's category count (0: none fits)."""
+    return 4 if n_categories <= 16 else 5 if n_categories <= 32 else 0
+
+
+def packable24(pc, cat, n_instr: int, cat_bits: int = 4) -> bool:
+    """pc < n_instr <= 2^(24 - cat_bits) and categories below 2^cat_bits."""
     pc, cat = np.asarray(pc), np.asarray(cat)
-    return (n_instr <= (1 << 20) and (pc.size == 0 or (int(pc.min()) >= 0 and int(pc.max()) < n_instr
-                                                      and int(cat.max()) < 16)))
+    return (cat_bits in (4, 5) and n_instr <= (1 << (24 - cat_bits))
+            and (pc.size == 0 or (int(pc.min()) >= 0 and int(pc.max()) < n_instr
+                                  and int(cat.max()) < (1 << cat_bits))))
 
 
 # streams this long bin in the one-pass hash, which reads the packed words as
@@ -127,15 +134,19 @@ class DeviceSamples:
                       and not os.environ.get("LEO_NO_PACK"))
         self.packed = packed
         if width is None and packed and os.environ.get("LEO_PACK3"):
-            width = 3 if packable24(pc, cat, 1 << 20) else 4
+            width = 3
         self.width = 4
+        cb = 4 if self.n == 0 or int(np.asarray(cat).max()) < 16 else 5
+        if self.packed and width == 3 and not packable24(pc, cat, 1 << (24 - cb), cb):
+            raise ValueError("DeviceSamples: the stream does not fit 3-byte words")
         if self.packed and width == 3:
             self.width = 3
-            self.words = to_device(pack_samples24(pc, cat), dev)
+            self.words = to_device(pack_samples24(pc, cat, cb), dev)
             self.pc = self.cat = None
             self.struct = abi.LeoSamples(self.n, None, None, ptr(self.lut))
             self.struct.packed = ptr(self.words)
             self.struct.packed_bytes = 3
+            self.struct.packed_cat_bits = cb
         elif self.packed:
             self.words = to_device(pack_samples(pc, cat).view(np.int32), dev)
             self.pc = self.cat = None
@@ -155,7 +166,8 @@ class DeviceSamples:
         return self
 
     @classmethod
-    def from_packed(cls, words: torch.Tensor, lut: torch.Tensor, n: int | None = None, width: int = 4):
+    def from_packed(cls, words: torch.Tensor, lut: torch.Tensor, n: int | None = None, width: int = 4,
+                    cat_bits: int = 4):
         """Device u32 (int32-typed) words pc << 8 | category (width 4), or the
         3-byte stream of pack_samples24 (width 3, uint8 tensor, `n` samples)."""
         self = cls.__new__(cls)
@@ -165,6 +177,7 @@ class DeviceSamples:
         self.struct = abi.LeoSamples(self.n, None, None, ptr(lut))
         self.struct.packed = ptr(words)
         self.struct.packed_bytes = width
+        self.struct.packed_cat_bits = cat_bits if width == 3 else 0
         return self
 
     def set_host_packed(self, words_host: torch.Tensor | None):

@@ -226,7 +226,7 @@ def test_device_batch_matches_per_kernel_oracle(cuda):
                 assert np.array_equal(got[f], e), (dialect, wl.kernel.name, f)
 
 @pytest.mark.parametrize("width", [4, 3])
-@pytest.mark.parametrize("tag,scale", [("c2", 0.2), ("c5", 0.05)])
+@pytest.mark.parametrize("tag,scale", [("c2", 0.2), ("c5", 0.05), ("c3", 1.0)])
 def test_packed_and_split_sample_streams_agree(tag, scale, width, cuda):
     """The packed stream (one u32 word per sample, or the 3-byte words of
     packed_bytes = 3) bins to the same counts and the same analysis as the

@@ -69,11 +69,11 @@ def test_session_graph_matches_oracle(tag, scale, cuda):
     assert sess.last_d2h >= 53 * len(o2.e_stalled)
 
 
-@pytest.mark.parametrize("tag,scale,width", [("c5", 0.05, 3), ("c3", 1.0, 4)])
+@pytest.mark.parametrize("tag,scale,width", [("c5", 0.05, 3), ("c3", 1.0, 3)])
 def test_session_packed_streams_match_oracle(tag, scale, width, cuda):
-    """Streams of >= 4 M samples travel packed: 3 bytes per sample for NVIDIA /
-    AMD kernels of at most 2^20 instructions, the u32 words otherwise (Intel's
-    17 category ids need 5 bits)."""
+    """Streams of >= 4 M samples travel packed: 3 bytes per sample (4 category
+    bits for NVIDIA / AMD kernels of at most 2^20 instructions, 5 for Intel's
+    17 category ids and at most 2^19 instructions), else the u32 words."""
     from oracle import oracle
     from paper_2604_20032_b200 import abi, api, synth
     wl = synth.config_workload(tag, scale=scale)
@@ -88,8 +88,8 @@ def test_session_packed_streams_match_oracle(tag, scale, width, cuda):
         assert full_entries_match(r, o), call
     if width == 3:
         bad = wl.cat.copy()
-        bad[7] = 16
-        with pytest.raises(ValueError, match="category id >= 16"):
+        bad[7] = 1 << sess.cat_bits
+        with pytest.raises(ValueError, match=f"category id >= {1 << sess.cat_bits}"):
             sess.stage(ks, wl.profile, wl.pc, bad, wl.lut)
 
 
