@@ -64,3 +64,26 @@ def test_file_to_device_session(tmp_path):
     o = oracle.run(wl.kernel, synth.bin_host(wl), abi.make_config(dialect="amd"))
     assert np.array_equal(r["e_stalled"], o.e_stalled)
     assert np.array_equal(r["e_blame"], o.e_blame)
+
+
+def test_three_byte_stream_round_trip():
+    """device.pack_samples24: little-endian 24-bit words pc << cb | category
+    (ABI v4 packed_bytes = 3), 4 category bits (NVIDIA / AMD) or 5 (Intel)."""
+    from paper_2604_20032_b200 import device
+    from paper_2604_20032_b200 import enums as E
+    rng = np.random.default_rng(3)
+    for cb, n_instr in ((4, 1 << 20), (5, 1 << 19)):
+        n = 1001                                   # not a multiple of 4
+        pc = rng.integers(0, n_instr, n).astype(np.int32)
+        cat = rng.integers(0, 1 << cb, n).astype(np.uint8)
+        b = device.pack_samples24(pc, cat, cb)
+        assert b.size % 4 == 0 and b.size >= 3 * n
+        w = b[:3 * n].reshape(n, 3).astype(np.uint32)
+        w = w[:, 0] | (w[:, 1] << 8) | (w[:, 2] << 16)
+        assert np.array_equal(w >> cb, pc) and np.array_equal(w & ((1 << cb) - 1), cat)
+        assert device.packable24(pc, cat, n_instr, cb)
+        assert not device.packable24(pc, cat, 2 * n_instr, cb)          # pcs would not fit
+        bad = cat.copy()
+        bad[0] = 1 << cb
+        assert not device.packable24(pc, bad, n_instr, cb)
+    assert [device.cat_bits_for(len(E.vendor_categories(d))) for d in E.DIALECTS] == [4, 4, 5]
