@@ -118,6 +118,9 @@ __global__ void k_bin_samples(int64_t S, const int32_t* __restrict__ pc, const u
 // per occupied slot.  One read of the 5 bytes per sample (vs the bucketed
 // passes' hist + scatter + count: ~3 reads and a key write).
 constexpr uint32_t kBinEmpty = 0xFFFFFFFFu;
+// A/B knob (LEO_BIN_NOGROUP=1, set by the host): the per-vector 3-byte loads
+__device__ int g_bin_nogroup;
+LEO_DEV bool getenv_bin_nogroup() { return g_bin_nogroup != 0; }
 
 template <int SLOTS, int PROBE, int PACK = 0, int CB = 4>
 __global__ void __launch_bounds__(1024) k_bin_hash(int64_t S, const int32_t* __restrict__ pc,
@@ -188,7 +191,35 @@ __global__ void __launch_bounds__(1024) k_bin_hash(int64_t S, const int32_t* __r
   // __syncwarp() in vec() always sees the full warp
   const int64_t bd = blockDim.x;
   const int lane = threadIdx.x & 31;
-  for (int64_t v = v0 + threadIdx.x; v - lane < v1; v += 2 * bd) {
+  // 3-byte words from a 16-byte-aligned stream: a thread takes 16 samples
+  // (48 bytes) as three 16-byte loads instead of twelve 4-byte ones; the
+  // chunk's < 4 head and tail vectors outside whole groups go to warp 0
+  const bool groups = PACK == 3 && !(reinterpret_cast<uintptr_t>(packed) & 15) && !getenv_bin_nogroup();
+  if (PACK == 3 && groups) {
+    const int64_t g0 = (v0 + 3) / 4, g1 = v1 / 4;
+    const uint4* q = reinterpret_cast<const uint4*>(packed);
+    for (int64_t g = g0 + threadIdx.x; g - lane < g1; g += bd) {
+      const bool in = g < g1;
+      const uint4 zero = make_uint4(0, 0, 0, 0);
+      const uint4 a = in ? q[3 * g] : zero, b = in ? q[3 * g + 1] : zero, c = in ? q[3 * g + 2] : zero;
+      int4 p;
+      uint32_t cc;
+      unpack4_24<CB>(a.x, a.y, a.z, p, cc); vec(p, cc, in);
+      unpack4_24<CB>(a.w, b.x, b.y, p, cc); vec(p, cc, in);
+      unpack4_24<CB>(b.z, b.w, c.x, p, cc); vec(p, cc, in);
+      unpack4_24<CB>(c.y, c.z, c.w, p, cc); vec(p, cc, in);
+    }
+    if (threadIdx.x < 32) {
+      const int64_t hmax = min(v1, 4 * g0), tmin = max(hmax, 4 * g1);
+      const int64_t v = lane < 4 ? v0 + lane : tmin + (lane - 4);
+      const bool in = lane < 4 ? v < hmax : (lane < 8 && v < v1);
+      int4 p;
+      uint32_t cc;
+      load4<PACK, CB>(packed, v, in, p, cc);
+      vec(p, cc, in);
+    }
+  }
+  for (int64_t v = v0 + threadIdx.x; !groups && v - lane < v1; v += 2 * bd) {
     const bool in0 = v < v1, in1 = v + bd < v1;
     int4 p0, p1;
     uint32_t c0, c1;

@@ -871,6 +871,13 @@ static int bin_impl(const LeoSamples* s, int32_t n_instr, int32_t* lat, int32_t*
     if (slots == 8192) { f = probe == 8 ? k_bin_hash<8192, 8> : k_bin_hash<8192, 4>; threads = 512; per_sm = 3; }
     else if (slots == 16384) f = probe == 2 ? k_bin_hash<16384, 2> : k_bin_hash<16384, 4>;
     else f = probe == 2 ? k_bin_hash<26624, 2> : probe == 8 ? k_bin_hash<26624, 8> : k_bin_hash<26624, 4>;
+    if (packed && pw == 3) {
+      static int ng = -1;
+      if (ng < 0) {                                      // profiling knob: set once, before any capture
+        ng = getenv("LEO_BIN_NOGROUP") ? 1 : 0;
+        if (ng) cudaMemcpyToSymbol(g_bin_nogroup, &ng, sizeof(int));
+      }
+    }
     if (packed) {                                        // default geometry
       f = pw == 4 ? k_bin_hash<16384, 2, 4> : cb == 5 ? k_bin_hash<16384, 2, 3, 5> : k_bin_hash<16384, 2, 3>;
       threads = 1024; per_sm = 1;
