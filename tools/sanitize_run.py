@@ -3,7 +3,7 @@ synccheck / initcheck): the three corpus kernels from the golden vectors and
 synthetic C2 / C3 / C5 kernels at reduced scale with raw samples, eager
 launches through the C ABI, each checked against the oracle.
 
-    compute-sanitizer --tool racecheck python tools/sanitize_run.py [--quick]
+    compute-sanitizer --tool racecheck python tools/sanitize_run.py [--quick] [--big] [--packed3]
 """
 import sys
 from pathlib import Path
@@ -44,4 +44,18 @@ for tag, scale in runs:
                  ("level", "level")):
         assert np.array_equal(r[a], getattr(o, b)), (tag, a)
     print(tag, scale, wl.kernel.n_instr, "instrs ok", flush=True)
+# --packed3: the 3-byte sample stream (4 and 5 category bits) through the
+# one-pass binning, cut to lengths that leave partial 16-sample groups
+if "--packed3" in sys.argv:
+    for tag, scale in (("c5", 0.05), ("c3", 1.0)):
+        wl = synth.config_workload(tag, scale=scale)
+        cfg = abi.make_config(dialect=wl.kernel.dialect)
+        for cut in (0, 5, 27):
+            n = len(wl.pc) - cut
+            smp = (wl.pc[:n], wl.cat[:n], wl.lut)
+            a = device.analyze_soa(wl.kernel, wl.profile, cfg, samples=smp, device=dev, packed=True, width=3)
+            b = device.analyze_soa(wl.kernel, wl.profile, cfg, samples=smp, device=dev, packed=False)
+            for key in ("lat", "cls_cnt", "e_blame"):
+                assert np.array_equal(a[key], b[key]), (tag, cut, key)
+        print(tag, "3-byte stream ok", flush=True)
 print("sanitize_run ok")
